@@ -1,0 +1,285 @@
+/*
+ * tg_capi.h — the C-ABI drop-in boundary of the B200 tiergraph hot path.
+ *
+ * Plain pointers and sizes only (no torch, no STL). Every entry point names the
+ * reference interface it replaces (reference = arXiv 2111.05894 `tiergraph`,
+ * files under proj/include/tiergraph and proj/src). The C++ drop-in headers in
+ * include/tiergraph/*.hpp are implemented on top of these calls, and the
+ * Python host mirror (paper_2111_05894_b200/tiergraph.py) binds them with
+ * ctypes; INTEGRATION.md shows the bindings.
+ *
+ * Pointer arguments marked "host|device" may be either: the library inspects
+ * them (cudaPointerGetAttributes) and stages host memory through the context's
+ * stream. All calls are stream-ordered on the context's stream; calls that
+ * return results in host memory synchronise that stream before returning.
+ * Calls with an `_async` suffix never synchronise and take device pointers.
+ *
+ * Errors: every int-returning call returns TG_OK or one of the codes below,
+ * which mirror the reference CLI's exit codes for its exception classes
+ * (tools/tiergraph_cli.cpp:589-601; types.hpp:13-29). The thread-local
+ * message of the last failure is available from tg_last_error().
+ */
+#ifndef TG_CAPI_H_
+#define TG_CAPI_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define TG_OK 0
+#define TG_ERR_DOMAIN 2   /* reference DomainError (types.hpp:26-29) */
+#define TG_ERR_FORMAT 3   /* reference FormatError (types.hpp:20-23) */
+#define TG_ERR_IO 4       /* reference IoError     (types.hpp:13-16) */
+#define TG_ERR_INTERNAL 5 /* CUDA / allocation failures (CLI exit 5)  */
+
+#define TG_MAX_DEVICES 16
+
+/* Message of the last failing call on this thread. */
+const char* tg_last_error(void);
+/* Library / kernel build identification, e.g. "tiergraph_b200 sm_100a". */
+const char* tg_version(void);
+
+/* ------------------------------------------------------------------ POD views
+ * Layout-identical to the reference structs so a C++ caller can pass them
+ * straight through. */
+
+/* tiering.hpp:16-25 TierLayout */
+typedef struct tg_layout {
+  uint64_t num_rows;
+  uint64_t local_boundary;
+  uint64_t multi_boundary;
+  uint32_t num_devices;
+  uint64_t feature_dim;
+  uint32_t elem_bytes;
+} tg_layout;
+
+/* tiering.hpp:51-58 TrafficReport (counters only) */
+typedef struct tg_report {
+  uint64_t local_accesses;
+  uint64_t peer_accesses;
+  uint64_t host_accesses;
+  uint64_t local_bytes;
+  uint64_t peer_bytes;
+  uint64_t host_bytes;
+} tg_report;
+
+/* tiering.hpp:29-37 Tier / Location */
+#define TG_TIER_LOCAL_HOT 0
+#define TG_TIER_INTERLEAVED 1
+#define TG_TIER_COLD_HOST 2
+typedef struct tg_location {
+  uint8_t tier;
+  uint32_t device;
+  uint64_t row_within_tier;
+} tg_location;
+
+/* ---------------------------------------------------------------- context
+ * One device + one CUDA stream + scratch memory. Mirrors the reference's
+ * process-global worker count (parallel.hpp:5-9): the device is chosen per
+ * context; tg_default_device() resolves TIERGRAPH_DEVICES like
+ * TIERGRAPH_THREADS (parallel.cpp:13-19). */
+typedef struct tg_ctx tg_ctx;
+int tg_ctx_create(int device, tg_ctx** out);
+/* Run on a caller-owned stream (e.g. torch.cuda.current_stream()). */
+int tg_ctx_create_on_stream(int device, void* cuda_stream, tg_ctx** out);
+int tg_ctx_destroy(tg_ctx* ctx);
+int tg_ctx_sync(tg_ctx* ctx);
+void* tg_ctx_stream(tg_ctx* ctx);
+int tg_ctx_device(tg_ctx* ctx);
+/* First entry of TIERGRAPH_DEVICES ("0,1,..."), else 0. */
+int tg_default_device(void);
+/* Number of devices listed in TIERGRAPH_DEVICES (>=1), or the visible count. */
+int tg_device_count(void);
+/* Launches of this library's kernels since process start (all contexts). */
+uint64_t tg_kernel_launches(void);
+
+/* ------------------------------------------------------------------ graph
+ * Device copy of a reference CsrGraph (csr_graph.hpp:22-35): offsets
+ * (n+1 x u64) and targets (e x u64), host|device. Stored narrowed to u32
+ * (requires n, e < 2^32); targets are range-checked (TG_ERR_FORMAT, message
+ * as validate_csr csr_graph.cpp:21-25). Also builds the row-group schedule
+ * used by the SpMV. */
+typedef struct tg_graph tg_graph;
+int tg_graph_create(tg_ctx* ctx, const uint64_t* offsets, const uint64_t* targets, uint64_t n,
+                    uint64_t e, tg_graph** out);
+int tg_graph_destroy(tg_graph* g);
+uint64_t tg_graph_num_nodes(const tg_graph* g);
+uint64_t tg_graph_num_edges(const tg_graph* g);
+/* Device pointers of the narrowed CSR (u32) — for peer kernels and tests. */
+const uint32_t* tg_graph_offsets32(const tg_graph* g);
+const uint32_t* tg_graph_targets32(const tg_graph* g);
+
+/* --------------------------------------------------------------- scoring
+ * scoring.hpp:32 degree_score -> out (n x f64, host|device) */
+int tg_degree_score(tg_ctx* ctx, const tg_graph* g, double* out);
+/* csr_graph.cpp:89-93 in_degrees -> out (n x u64, host|device) */
+int tg_in_degrees(tg_ctx* ctx, const tg_graph* g, uint64_t* out);
+/* scoring.hpp:40 reverse_pagerank (scoring.cpp:78-84). Bit-exact fp64. */
+int tg_reverse_pagerank(tg_ctx* ctx, const tg_graph* g, uint32_t iterations, double damp,
+                        double* out);
+/* scoring.hpp:45-46 weighted_reverse_pagerank (scoring.cpp:86-102).
+ * tid = TrainIdSet::ids (host|device), ntid >= 1 else TG_ERR_DOMAIN. */
+int tg_weighted_reverse_pagerank(tg_ctx* ctx, const tg_graph* g, uint32_t iterations,
+                                 double damp, const uint64_t* tid, uint64_t ntid, double* out);
+
+/* Row-partitioned iteration for multi-GPU: the caller owns the
+ * exchange (NCCL all-gather of `norm`). norm_in/norm_out/score_out are device
+ * vectors of length n; only rows [row_begin,row_end) are written.
+ *   tg_pagerank_prepare: in-degrees (u32, device, length n) and the initial
+ *     normalized vector for the weighted (tid!=NULL) or plain recurrence.
+ *   tg_pagerank_step: one Jacobi step over the rows; `last` writes scores
+ *     instead of the next normalized vector. */
+int tg_pagerank_prepare_async(tg_ctx* ctx, const tg_graph* g, const uint64_t* tid_dev,
+                              uint64_t ntid, uint32_t* indeg_dev, double* norm0_dev);
+int tg_pagerank_step_async(tg_ctx* ctx, const tg_graph* g, const uint32_t* indeg_dev,
+                           double damp, const double* norm_in_dev, double* norm_out_dev,
+                           double* score_out_dev, uint64_t row_begin, uint64_t row_end,
+                           int last);
+
+/* scoring.hpp:49 score_ordering (scoring.cpp:104-115): ids by descending
+ * score, ties by ascending id. scores/out host|device. TG_ERR_DOMAIN names the
+ * first non-finite or negative score. */
+int tg_score_ordering(tg_ctx* ctx, const double* scores, uint64_t n, uint64_t* out_order);
+
+/* ---------------------------------------------------------------- reorder
+ * reorder.hpp:25 permutation_from_scores (reorder.cpp:23-29). out_new_id_of
+ * (n x u64, host|device). out_order may be NULL or receives score_ordering. */
+int tg_permutation_from_scores(tg_ctx* ctx, const double* scores, uint64_t n,
+                               uint64_t* out_new_id_of, uint64_t* out_order);
+/* reorder.hpp:21 validate_permutation (reorder.cpp:10-21) */
+int tg_validate_permutation(tg_ctx* ctx, const uint64_t* perm, uint64_t n);
+/* reorder.hpp:27 invert (reorder.cpp:31-37) */
+int tg_invert(tg_ctx* ctx, const uint64_t* perm, uint64_t n, uint64_t* out);
+/* reorder.hpp:40 reorder_features (reorder.cpp:97-117): new row perm[u] = old
+ * row u. src/dst host|device, rows x row_bytes. */
+int tg_reorder_features(tg_ctx* ctx, const void* src, uint64_t rows, uint64_t row_bytes,
+                        const uint64_t* perm, uint64_t perm_len, void* dst);
+/* reorder.hpp:33 reorder_graph (reorder.cpp:39-66, Algorithm 2). Inputs and
+ * outputs host|device; out_offsets n+1, out_targets e. */
+int tg_reorder_graph(tg_ctx* ctx, const uint64_t* offsets, const uint64_t* targets, uint64_t n,
+                     uint64_t e, const uint64_t* perm, uint64_t perm_len, uint64_t* out_offsets,
+                     uint64_t* out_targets);
+
+/* ---------------------------------------------------------------- tiering
+ * Host-side scalar logic (tiering.cpp:10-98); no device work. */
+int tg_validate_layout(const tg_layout* layout);
+int tg_validate_cost_model(double local_gbps, double peer_gbps, double host_gbps);
+int tg_resolve(const tg_layout* layout, uint64_t row_id, uint32_t requesting_device,
+               tg_location* out);
+int tg_plan_layout(uint64_t num_rows, double hot_fraction, double replicated_fraction,
+                   uint32_t num_devices, uint64_t feature_dim, uint32_t elem_bytes,
+                   uint64_t per_device_budget_bytes, tg_layout* out);
+double tg_report_hit_ratio(const tg_report* r);
+double tg_report_est_transfer_seconds(const tg_report* r, double local_gbps, double peer_gbps,
+                                      double host_gbps);
+
+/* tiering.hpp:88-89 gather (tiering.cpp:100-125), accounting only, on the
+ * GPU. ids host|device; report is ACCUMULATED like the reference's. On an
+ * out-of-range id the ids before it stay accounted and TG_ERR_DOMAIN is
+ * returned, exactly like the reference's throwing loop. */
+int tg_gather_account(tg_ctx* ctx, const tg_layout* layout, const uint64_t* ids, uint64_t n,
+                      uint32_t requesting_device, tg_report* report);
+
+/* tiering.hpp:95 simulate_trace (tiering.cpp:127-162); counts host|device. */
+int tg_simulate_trace(tg_ctx* ctx, const uint64_t* counts, uint64_t n, const tg_layout* layout,
+                      tg_report* out);
+/* tiering.hpp:98-99 counts_in_row_order (tiering.cpp:164-175) */
+int tg_counts_in_row_order(tg_ctx* ctx, const uint64_t* counts, uint64_t n,
+                           const uint64_t* ordering, uint64_t m, uint64_t* out);
+/* tiering.hpp:110-117 hot_fraction_sweep (tiering.cpp:177-202). Per fraction i:
+ * out_layouts[i], out_reports[i], out_replicated[i] (all host). */
+int tg_hot_fraction_sweep(tg_ctx* ctx, const uint64_t* counts, uint64_t n,
+                          const uint64_t* ordering, const double* fractions, uint64_t nf,
+                          double replicated_fraction, uint32_t num_devices, uint64_t feature_dim,
+                          uint32_t elem_bytes, uint64_t per_device_budget_bytes,
+                          tg_layout* out_layouts, tg_report* out_reports,
+                          double* out_replicated);
+
+/* --------------------------------------------------- tiered feature store
+ * The byte-moving gather the paper describes (Listing 1;
+ * :346-353) and the reference only accounts for. One store per device
+ * (device_index in [0, num_devices)): replicated rows [0, lb) and this
+ * device's interleaved slice of [lb, mb) live in local HBM; cold rows
+ * [mb, num_rows) live in pinned, mapped host memory read by UVA zero-copy.
+ * Row ids are NEW ids (after permutation_from_scores), as resolve() takes. */
+typedef struct tg_store tg_store;
+
+#define TG_COLD_REORDERED 0u /* pinned copy of the cold rows in new-id order   */
+#define TG_COLD_INDIRECT 1u  /* register the caller's original host matrix and  */
+                             /* index it through the permutation (no host copy) */
+#define TG_COLD_PAD128 2u    /* pad cold rows to a 128 B stride (PCIe lines)    */
+
+int tg_store_create(tg_ctx* ctx, const tg_layout* layout, uint32_t device_index, uint32_t flags,
+                    tg_store** out);
+int tg_store_destroy(tg_store* s);
+/* K7 placement. features: the ORIGINAL matrix (old-id order, num_rows x
+ * row_bytes, host|device); new_id_of: NodePermutation (host|device). Fills
+ * this device's hot rows and (TG_COLD_REORDERED) the cold copy. */
+int tg_store_place(tg_store* s, const void* features, const uint64_t* new_id_of);
+/* Base of this store's local HBM region (replicated rows then the slice). */
+void* tg_store_local_base(const tg_store* s);
+uint64_t tg_store_local_rows(const tg_store* s);
+/* Point device d's slot of the combined-tensor table at a peer's local base
+ * (same-process peer pointer, or a CUDA-IPC mapping from tg_ipc_open). */
+int tg_store_set_peer(tg_store* s, uint32_t d, const void* peer_local_base);
+/* Share one cold tier between stores/processes: use `host` (mapped pinned or
+ * registered memory holding the cold rows in the store's cold format). */
+int tg_store_share_cold(tg_store* s, const tg_store* owner);
+
+/* K8: copy rows ids[0..n) (host|device) into dst (n x row_bytes, host|device)
+ * and accumulate the reference accounting into report (host). Synchronous. */
+int tg_gather_rows(tg_store* s, const uint64_t* ids, uint64_t n, void* dst, tg_report* report);
+/* Same, stream-ordered: ids_dev/dst_dev device pointers, counters_dev = 3 x
+ * u64 device accumulator {local, peer, host} accesses, err_dev = 1 x u64
+ * device word receiving min(bad index)+1 (0 = ok). No synchronisation. */
+int tg_gather_rows_async(tg_store* s, const uint64_t* ids_dev, uint64_t n, void* dst_dev,
+                         uint64_t* counters_dev, uint64_t* err_dev);
+
+/* ------------------------------------------------------------- peer memory */
+int tg_enable_peer_access(int device, int peer);
+int tg_ipc_get_handle(const void* dev_ptr, void* handle_out /* 64 bytes */);
+int tg_ipc_open_handle(tg_ctx* ctx, const void* handle /* 64 bytes */, void** dev_ptr_out);
+int tg_ipc_close_handle(void* dev_ptr);
+/* Register caller host memory as mapped pinned (cudaHostRegister). */
+int tg_host_register(void* ptr, uint64_t bytes);
+int tg_host_unregister(void* ptr);
+int tg_host_alloc(uint64_t bytes, void** out); /* cudaHostAlloc Mapped|Portable */
+int tg_host_free(void* p);
+
+/* ------------------------------------------------------------ measurement
+ * Zero-copy read bandwidth of `bytes` of mapped host memory in rows of
+ * row_bytes (random order), timed with CUDA events on the ctx stream; and a
+ * device-to-device copy for the HBM reference. Both return GB/s. */
+int tg_measure_host_read_gbps(tg_ctx* ctx, uint64_t bytes, uint64_t row_bytes, int reps,
+                              double* gbps);
+int tg_measure_hbm_copy_gbps(tg_ctx* ctx, uint64_t bytes, int reps, double* gbps);
+
+/* ------------------------------------------------ host-side input producers
+ * Not the hot path: the reference's CPU producers of the gather's id lists,
+ * restated bit-exactly in C++ (csrc/host_producers.cpp). Outputs returned
+ * through *_out pointers are malloc'ed; release them with tg_free. */
+const char* tg_host_last_error(void);
+void tg_free(void* p);
+/* scoring.hpp:24 draw_random_train_ids (scoring.cpp:22-31); out has count ids */
+int tg_draw_random_train_ids(uint64_t num_nodes, uint64_t count, uint64_t seed, uint64_t* out);
+/* csr_graph.hpp:48 transpose (csr_graph.cpp:67-80), host arrays */
+int tg_transpose_host(const uint64_t* off, const uint64_t* tgt, uint64_t n, uint64_t* t_off,
+                      uint64_t* t_tgt);
+/* One epoch of run_training_trace's schedule (sampling.cpp:106-123): shuffle
+ * tid with key {0x5348, epoch}, split into batches, expand batches
+ * [first_batch, first_batch+max_batches) with build_minibatch (sampling.cpp:56-90)
+ * over the transposed graph. Lists are concatenated: batch i is
+ * ids[off[i]..off[i+1]). threads <= 0 uses all OpenMP threads. */
+int tg_epoch_minibatches(const uint64_t* gt_off, const uint64_t* gt_tgt, uint64_t n,
+                         const uint64_t* tid, uint64_t ntid, const uint32_t* fanouts, uint32_t nf,
+                         uint64_t batch_size, uint64_t seed, uint64_t epoch, uint64_t first_batch,
+                         uint64_t max_batches, int threads, uint64_t** out_off, uint64_t* out_nb,
+                         uint64_t** out_ids);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* TG_CAPI_H_ */

@@ -1,0 +1,191 @@
+// Internal plumbing shared by the tiergraph B200 kernels: error model, the
+// per-device context (stream + scratch), host|device pointer staging, and the
+// launch counter the bench reports as gpu_launches.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <atomic>
+#include <cstdint>
+#include <cstring>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "tg_capi.h"
+
+namespace tgb {
+
+// ---------------------------------------------------------------- errors
+struct Error : std::runtime_error {
+  int code;
+  Error(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+[[noreturn]] inline void domain_error(const std::string& m) { throw Error(TG_ERR_DOMAIN, m); }
+[[noreturn]] inline void format_error(const std::string& m) { throw Error(TG_ERR_FORMAT, m); }
+
+inline void cuda_check(cudaError_t e, const char* what) {
+  if (e != cudaSuccess)
+    throw Error(TG_ERR_INTERNAL, std::string(what) + ": " + cudaGetErrorString(e));
+}
+#define TGB_CUDA(x) ::tgb::cuda_check((x), #x)
+
+extern std::atomic<uint64_t> g_launches;
+inline void count_launch(int n = 1) { g_launches.fetch_add(n, std::memory_order_relaxed); }
+// Check the launch itself (configuration errors); execution errors surface at
+// the next synchronising call.
+#define TGB_LAUNCHED()                                                 \
+  do {                                                                 \
+    ::tgb::count_launch();                                             \
+    ::tgb::cuda_check(cudaGetLastError(), "kernel launch");            \
+  } while (0)
+
+// --------------------------------------------------------------- context
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    cudaGetDevice(&prev);
+    if (prev != dev) TGB_CUDA(cudaSetDevice(dev));
+  }
+  ~DeviceGuard() {
+    int cur;
+    if (prev >= 0 && cudaGetDevice(&cur) == cudaSuccess && cur != prev) cudaSetDevice(prev);
+  }
+};
+
+enum Slot : int {
+  kScratchA = 0, kScratchB, kScratchC, kScratchD, kScratchE, kScratchF,
+  kStageIn0, kStageIn1, kStageIn2, kStageOut0, kStageOut1, kSmall, kNumSlots
+};
+
+}  // namespace tgb
+
+struct tg_ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  int num_sms = 148;
+  void* slot_ptr[tgb::kNumSlots] = {};
+  size_t slot_size[tgb::kNumSlots] = {};
+  void* pinned_small = nullptr;  // 4 KB mapped host scratch for small results
+
+  // Grow-only scratch buffer bound to a slot. Stream-ordered reuse is safe
+  // because every user of the context enqueues on `stream`.
+  void* scratch(int slot, size_t bytes) {
+    if (bytes == 0) bytes = 16;
+    if (slot_size[slot] < bytes) {
+      if (slot_ptr[slot]) {
+        tgb::cuda_check(cudaStreamSynchronize(stream), "scratch sync");
+        tgb::cuda_check(cudaFree(slot_ptr[slot]), "scratch free");
+        slot_ptr[slot] = nullptr;
+        slot_size[slot] = 0;
+      }
+      size_t sz = bytes + bytes / 8;
+      tgb::cuda_check(cudaMalloc(&slot_ptr[slot], sz), "scratch alloc");
+      slot_size[slot] = sz;
+    }
+    return slot_ptr[slot];
+  }
+  template <typename T>
+  T* scratch_t(int slot, size_t count) {
+    return static_cast<T*>(scratch(slot, count * sizeof(T)));
+  }
+  void sync() { tgb::cuda_check(cudaStreamSynchronize(stream), "stream sync"); }
+};
+
+namespace tgb {
+
+inline bool is_device_ptr(const void* p) {
+  if (!p) return false;
+  cudaPointerAttributes a;
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
+}
+
+// Device pointer to mapped pinned host memory, or nullptr if `p` is not
+// registered/pinned.
+inline void* mapped_device_ptr(const void* p) {
+  if (!p) return nullptr;
+  cudaPointerAttributes a;
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return nullptr;
+  }
+  if (a.type == cudaMemoryTypeHost) return a.devicePointer;
+  return nullptr;
+}
+
+// Read-only input that may live on the host: returns a device pointer,
+// copying into a scratch slot when needed.
+template <typename T>
+const T* dev_in(tg_ctx* ctx, const T* p, size_t count, int slot) {
+  if (count == 0) return ctx->scratch_t<T>(slot, 1);
+  if (is_device_ptr(p)) return p;
+  T* d = ctx->scratch_t<T>(slot, count);
+  TGB_CUDA(cudaMemcpyAsync(d, p, count * sizeof(T), cudaMemcpyHostToDevice, ctx->stream));
+  return d;
+}
+
+// Output that may live on the host: write into dev(), then finish() copies
+// back (and synchronises) when the destination is host memory.
+template <typename T>
+struct DevOut {
+  tg_ctx* ctx;
+  T* user;
+  size_t count;
+  T* d;
+  bool host;
+  DevOut(tg_ctx* c, T* u, size_t n, int slot) : ctx(c), user(u), count(n) {
+    host = !is_device_ptr(u);
+    d = host ? c->scratch_t<T>(slot, n ? n : 1) : u;
+  }
+  T* dev() { return d; }
+  void finish() {
+    if (host && count)
+      TGB_CUDA(cudaMemcpyAsync(user, d, count * sizeof(T), cudaMemcpyDeviceToHost, ctx->stream));
+    ctx->sync();
+  }
+};
+
+inline unsigned grid_for(uint64_t work, unsigned per_block, unsigned cap = 148u * 64u) {
+  uint64_t g = (work + per_block - 1) / per_block;
+  if (g < 1) g = 1;
+  if (g > cap) g = cap;
+  return static_cast<unsigned>(g);
+}
+
+}  // namespace tgb
+
+namespace tgb {
+// Thread-local message + exception → error-code translation for the C-ABI.
+void set_last_error(const std::string& m);
+template <typename F>
+int guard(F&& f) {
+  try {
+    f();
+    return TG_OK;
+  } catch (const Error& e) {
+    set_last_error(e.what());
+    return e.code;
+  } catch (const std::bad_alloc&) {
+    set_last_error("out of memory");
+    return TG_ERR_INTERNAL;
+  } catch (const std::exception& e) {
+    set_last_error(e.what());
+    return TG_ERR_INTERNAL;
+  }
+}
+
+__device__ __forceinline__ uint32_t warp_min_u32(uint32_t v) {
+  return __reduce_min_sync(0xffffffffu, v);
+}
+__device__ __forceinline__ uint32_t warp_max_u32(uint32_t v) {
+  return __reduce_max_sync(0xffffffffu, v);
+}
+
+// Validates a permutation (reorder.cpp:10-21); optionally writes its inverse (u32).
+void check_permutation(tg_ctx* ctx, const uint64_t* perm_dev, uint64_t n, uint32_t* inv_dev);
+}  // namespace tgb

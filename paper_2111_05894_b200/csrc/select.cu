@@ -1,0 +1,297 @@
+// Hot path A, part 2: hot-set selection — validate + key transform (K4), a
+// stable LSD radix sort of (key, id) (K5), and the permutation scatter (K6).
+//
+// Reference: proj/src/scoring.cpp:104-115 (score_ordering: reject non-finite
+// or negative scores, sort ids by score descending, ties by ascending id) and
+// proj/src/reorder.cpp:23-29 (permutation_from_scores: new_id_of[order[r]]=r).
+//
+// Key = ~bits(score) with -0.0 canonicalised to +0.0: for non-negative finite
+// doubles the IEEE bit pattern is monotone, so ascending keys = descending
+// scores, and equal scores (including +-0) share a key. A stable sort over
+// ids presented in ascending order reproduces the id tie-break exactly.
+//
+// Sort: 8-bit digits, reduce-then-scan per pass (block digit counts -> one
+// scan -> stable block-local ranking via warp __match_any_sync -> scatter).
+// One upfront pass builds all eight digit histograms; passes whose digit is
+// constant over the whole input are skipped on the device (no host sync), with
+// the ping-pong buffer choice planned on the device as well.
+#include <cuda_runtime.h>
+
+#include <string>
+
+#include "internal.cuh"
+
+namespace tgb {
+
+constexpr int kRsWarps = 8;
+constexpr int kRsIpt = 16;
+constexpr int kRsTile = kRsWarps * 32 * kRsIpt;  // 4096 items per CTA
+
+struct RadixPlan {
+  int skip[8];
+  int src[8];
+  int final_src;
+};
+
+__device__ __forceinline__ uint64_t score_key(double s) {
+  uint64_t b = static_cast<uint64_t>(__double_as_longlong(s));
+  if (b == 0x8000000000000000ull) b = 0;  // -0.0 == +0.0 (scoring.cpp:111)
+  return ~b;
+}
+
+// K4: validate (scoring.cpp:105-107), build keys/ids, and all 8 digit histograms.
+__global__ void __launch_bounds__(256) key_prep_kernel(const double* __restrict__ s, uint64_t n,
+                                                       uint64_t* __restrict__ keys,
+                                                       uint32_t* __restrict__ vals,
+                                                       uint32_t* __restrict__ hist,
+                                                       unsigned long long* bad) {
+  __shared__ uint32_t h[8][256];
+  for (int i = threadIdx.x; i < 8 * 256; i += blockDim.x) (&h[0][0])[i] = 0;
+  __syncthreads();
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    const double v = s[i];
+    if (!(isfinite(v) && v >= 0.0)) atomicMin(bad, (unsigned long long)i);
+    const uint64_t k = score_key(v);
+    keys[i] = k;
+    vals[i] = static_cast<uint32_t>(i);
+#pragma unroll
+    for (int p = 0; p < 8; ++p) atomicAdd(&h[p][(k >> (8 * p)) & 0xff], 1u);
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < 8 * 256; i += blockDim.x) {
+    const uint32_t c = (&h[0][0])[i];
+    if (c) atomicAdd(hist + i, c);
+  }
+}
+
+__global__ void plan_kernel(const uint32_t* __restrict__ hist, uint64_t n, RadixPlan* plan) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  int src = 0;
+  for (int p = 0; p < 8; ++p) {
+    bool trivial = false;
+    for (int d = 0; d < 256; ++d) trivial |= hist[p * 256 + d] == n;
+    plan->skip[p] = trivial ? 1 : 0;
+    plan->src[p] = src;
+    if (!trivial) src ^= 1;
+  }
+  plan->final_src = src;
+}
+
+__global__ void __launch_bounds__(kRsWarps * 32) digit_count_kernel(
+    const uint64_t* __restrict__ k0, const uint64_t* __restrict__ k1, uint64_t n, int pass,
+    const RadixPlan* __restrict__ plan, uint32_t* __restrict__ counts, uint32_t nblk) {
+  if (plan->skip[pass]) return;
+  const uint64_t* keys = plan->src[pass] ? k1 : k0;
+  __shared__ uint32_t h[256];
+  h[threadIdx.x] = 0;
+  __syncthreads();
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const uint64_t base = (uint64_t)blockIdx.x * kRsTile + w * (32 * kRsIpt);
+  const int shift = 8 * pass;
+#pragma unroll
+  for (int k = 0; k < kRsIpt; ++k) {
+    const uint64_t i = base + k * 32 + lane;
+    if (i < n) atomicAdd(&h[(keys[i] >> shift) & 0xff], 1u);
+  }
+  __syncthreads();
+  counts[(uint64_t)threadIdx.x * nblk + blockIdx.x] = h[threadIdx.x];
+}
+
+// Exclusive scan of the digit-major count matrix (256 x nblk) in one CTA.
+__global__ void __launch_bounds__(1024) count_scan_kernel(uint32_t* __restrict__ counts,
+                                                          uint64_t m, int pass,
+                                                          const RadixPlan* __restrict__ plan) {
+  if (plan->skip[pass]) return;
+  __shared__ uint32_t warp_tot[32];
+  const uint64_t per = (m + blockDim.x - 1) / blockDim.x;
+  const uint64_t b = threadIdx.x * per;
+  const uint64_t e = b + per < m ? b + per : m;
+  uint32_t local = 0;
+  for (uint64_t i = b; i < e; ++i) local += counts[i];
+  // block exclusive scan of `local`
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  uint32_t incl = local;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += y;
+  }
+  if (lane == 31) warp_tot[w] = incl;
+  __syncthreads();
+  if (w == 0) {
+    uint32_t t = lane < (int)(blockDim.x / 32) ? warp_tot[lane] : 0;
+    uint32_t ti = t;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, ti, o);
+      if (lane >= o) ti += y;
+    }
+    warp_tot[lane] = ti - t;
+  }
+  __syncthreads();
+  uint32_t run = warp_tot[w] + incl - local;
+  for (uint64_t i = b; i < e; ++i) {
+    const uint32_t c = counts[i];
+    counts[i] = run;
+    run += c;
+  }
+}
+
+// Stable block-local ranking (warp rounds in index order + per-warp digit
+// counters), then scatter to the scanned global offsets.
+__global__ void __launch_bounds__(kRsWarps * 32) scatter_kernel(
+    uint64_t* __restrict__ k0, uint32_t* __restrict__ v0, uint64_t* __restrict__ k1,
+    uint32_t* __restrict__ v1, uint64_t n, int pass, const RadixPlan* __restrict__ plan,
+    const uint32_t* __restrict__ offs, uint32_t nblk) {
+  if (plan->skip[pass]) return;
+  const bool from1 = plan->src[pass] != 0;
+  const uint64_t* kin = from1 ? k1 : k0;
+  const uint32_t* vin = from1 ? v1 : v0;
+  uint64_t* kout = from1 ? k0 : k1;
+  uint32_t* vout = from1 ? v0 : v1;
+  __shared__ uint32_t wcnt[kRsWarps][256];
+  __shared__ uint32_t doff[256];
+  for (int i = threadIdx.x; i < kRsWarps * 256; i += blockDim.x) (&wcnt[0][0])[i] = 0;
+  doff[threadIdx.x] = offs[(uint64_t)threadIdx.x * nblk + blockIdx.x];
+  __syncthreads();
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const uint32_t lt = (1u << lane) - 1u;
+  const uint64_t base = (uint64_t)blockIdx.x * kRsTile + w * (32 * kRsIpt);
+  const int shift = 8 * pass;
+  uint64_t key[kRsIpt];
+  uint32_t val[kRsIpt];
+  uint32_t rank[kRsIpt];
+#pragma unroll
+  for (int k = 0; k < kRsIpt; ++k) {
+    const uint64_t i = base + k * 32 + lane;
+    const bool ok = i < n;
+    key[k] = ok ? kin[i] : 0;
+    val[k] = ok ? vin[i] : 0;
+  }
+#pragma unroll
+  for (int k = 0; k < kRsIpt; ++k) {
+    const uint64_t i = base + k * 32 + lane;
+    const uint32_t d = i < n ? static_cast<uint32_t>((key[k] >> shift) & 0xff) : 256u;
+    const uint32_t peers = __match_any_sync(0xffffffffu, d);
+    const uint32_t pre = d < 256 ? wcnt[w][d] : 0;
+    __syncwarp();
+    if (d < 256 && (peers & lt) == 0) wcnt[w][d] = pre + __popc(peers);
+    __syncwarp();
+    rank[k] = pre + __popc(peers & lt);
+  }
+  __syncthreads();
+  {
+    const int d = threadIdx.x;  // 256 threads: one digit each
+    uint32_t run = 0;
+#pragma unroll
+    for (int ww = 0; ww < kRsWarps; ++ww) {
+      const uint32_t c = wcnt[ww][d];
+      wcnt[ww][d] = run;
+      run += c;
+    }
+  }
+  __syncthreads();
+#pragma unroll
+  for (int k = 0; k < kRsIpt; ++k) {
+    const uint64_t i = base + k * 32 + lane;
+    if (i < n) {
+      const uint32_t d = static_cast<uint32_t>((key[k] >> shift) & 0xff);
+      const uint32_t pos = doff[d] + wcnt[w][d] + rank[k];
+      kout[pos] = key[k];
+      vout[pos] = val[k];
+    }
+  }
+}
+
+// K6: order[r] = id, new_id_of[id] = r (reorder.cpp:27)
+__global__ void perm_kernel(const uint32_t* __restrict__ v0, const uint32_t* __restrict__ v1,
+                            const RadixPlan* __restrict__ plan, uint64_t n,
+                            uint64_t* __restrict__ order, uint64_t* __restrict__ new_id_of) {
+  const uint32_t* v = plan->final_src ? v1 : v0;
+  for (uint64_t r = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; r < n;
+       r += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t id = v[r];
+    if (order) order[r] = id;
+    if (new_id_of) new_id_of[id] = r;
+  }
+}
+
+// Sorts scores -> (order, new_id_of). Either output may be null. Device pointers.
+void sort_scores(tg_ctx* ctx, const double* scores_dev, uint64_t n, uint64_t* order_dev,
+                 uint64_t* perm_dev) {
+  if (n >= 0xffffffffull) domain_error("score_ordering: n must be < 2^32");
+  uint64_t* k0 = ctx->scratch_t<uint64_t>(kScratchA, n);
+  uint64_t* k1 = ctx->scratch_t<uint64_t>(kScratchB, n);
+  uint32_t* v0 = ctx->scratch_t<uint32_t>(kScratchC, n);
+  uint32_t* v1 = ctx->scratch_t<uint32_t>(kScratchD, n);
+  const uint32_t nblk = static_cast<uint32_t>((n + kRsTile - 1) / kRsTile);
+  // small slot layout: [bad u64][plan][hist 8x256 u32]
+  char* small = static_cast<char*>(ctx->scratch(kSmall, 64 + sizeof(RadixPlan) + 8 * 256 * 4));
+  auto* bad = reinterpret_cast<unsigned long long*>(small);
+  auto* plan = reinterpret_cast<RadixPlan*>(small + 64);
+  auto* hist = reinterpret_cast<uint32_t*>(small + 64 + sizeof(RadixPlan));
+  uint32_t* counts = ctx->scratch_t<uint32_t>(kScratchE, (uint64_t)256 * nblk);
+  TGB_CUDA(cudaMemsetAsync(bad, 0xff, 8, ctx->stream));
+  TGB_CUDA(cudaMemsetAsync(hist, 0, 8 * 256 * 4, ctx->stream));
+  key_prep_kernel<<<grid_for(n, 256, ctx->num_sms * 8), 256, 0, ctx->stream>>>(scores_dev, n, k0,
+                                                                               v0, hist, bad);
+  TGB_LAUNCHED();
+  plan_kernel<<<1, 32, 0, ctx->stream>>>(hist, n, plan);
+  TGB_LAUNCHED();
+  for (int p = 0; p < 8; ++p) {
+    digit_count_kernel<<<nblk, kRsWarps * 32, 0, ctx->stream>>>(k0, k1, n, p, plan, counts, nblk);
+    TGB_LAUNCHED();
+    count_scan_kernel<<<1, 1024, 0, ctx->stream>>>(counts, (uint64_t)256 * nblk, p, plan);
+    TGB_LAUNCHED();
+    scatter_kernel<<<nblk, kRsWarps * 32, 0, ctx->stream>>>(k0, v0, k1, v1, n, p, plan, counts,
+                                                             nblk);
+    TGB_LAUNCHED();
+  }
+  perm_kernel<<<grid_for(n, 256), 256, 0, ctx->stream>>>(v0, v1, plan, n, order_dev, perm_dev);
+  TGB_LAUNCHED();
+  unsigned long long hb = 0;
+  TGB_CUDA(cudaMemcpyAsync(&hb, bad, 8, cudaMemcpyDeviceToHost, ctx->stream));
+  ctx->sync();
+  if (hb != ~0ull)
+    domain_error("score " + std::to_string(hb) + " is not finite and >= 0");  // scoring.cpp:107
+}
+
+}  // namespace tgb
+
+using namespace tgb;
+
+extern "C" {
+
+int tg_score_ordering(tg_ctx* ctx, const double* scores, uint64_t n, uint64_t* out_order) {
+  return guard([&] {
+    if (n == 0) return;
+    DeviceGuard dg(ctx->device);
+    const double* s = dev_in(ctx, scores, n, kStageIn0);
+    DevOut<uint64_t> o(ctx, out_order, n, kStageOut0);
+    sort_scores(ctx, s, n, o.dev(), nullptr);
+    o.finish();
+  });
+}
+
+int tg_permutation_from_scores(tg_ctx* ctx, const double* scores, uint64_t n,
+                               uint64_t* out_new_id_of, uint64_t* out_order) {
+  return guard([&] {
+    if (n == 0) return;
+    DeviceGuard dg(ctx->device);
+    const double* s = dev_in(ctx, scores, n, kStageIn0);
+    DevOut<uint64_t> p(ctx, out_new_id_of, n, kStageOut0);
+    uint64_t* od = nullptr;
+    bool order_host = false;
+    if (out_order) {
+      order_host = !is_device_ptr(out_order);
+      od = order_host ? ctx->scratch_t<uint64_t>(kStageOut1, n) : out_order;
+    }
+    sort_scores(ctx, s, n, od, p.dev());
+    if (order_host)
+      TGB_CUDA(cudaMemcpyAsync(out_order, od, n * 8, cudaMemcpyDeviceToHost, ctx->stream));
+    p.finish();
+  });
+}
+
+}  // extern "C"

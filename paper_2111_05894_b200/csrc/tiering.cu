@@ -1,0 +1,1100 @@
+// Hot path B: the tier address map, placement (K7), the tiered feature gather
+// (K8) and the reference's byte accounting, plus the trace replays.
+//
+// Reference: proj/src/tiering.cpp (resolve :48-65, plan_layout :67-98,
+// gather :100-125, simulate_trace :127-162, counts_in_row_order :164-175,
+// hot_fraction_sweep :177-202) and the byte-moving gather the paper describes
+// (PAPER.md:683-709 Listing 1, :346-353): a per-row pointer from a small table
+// {local HBM, peer HBM slices, pinned host}, chosen by comparing the row id to
+// the hot boundaries.
+//
+// Address map (resolve): row r < lb            -> local replicated row r
+//                        lb <= r < mb          -> device (r-lb)%D, slot (r-lb)/D
+//                        r >= mb               -> cold row r-mb (pinned host)
+// Each device's HBM region holds its lb replicated rows followed by its slice
+// of the interleaved rows. Peers' slices are read by direct loads through
+// peer pointers (same process, cudaDeviceEnablePeerAccess) or CUDA-IPC
+// mappings (one process per GPU); cold rows by UVA zero-copy loads.
+//
+// K8 copies rows with 16-byte vector loads: a warp takes a batch of B rows
+// (B*R/16 <= 256 chunks), resolves one row per lane, then every lane issues
+// up to 8 independent 16 B loads before storing them, so each warp keeps
+// ~4 KB in flight — the queue depth the PCIe zero-copy path needs.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <map>
+#include <mutex>
+#include <string>
+
+#include "internal.cuh"
+
+struct tg_store {
+  tg_ctx* ctx = nullptr;
+  tg_layout L{};
+  uint32_t dev = 0;
+  uint32_t flags = 0;
+  uint64_t R = 0;
+  uint64_t local_rows = 0;
+  uint8_t* local = nullptr;                       // device
+  const uint8_t* inter[TG_MAX_DEVICES] = {};      // per-device interleaved slice base
+  uint8_t* cold_host = nullptr;                   // host view (owned when own_cold)
+  const uint8_t* cold_dev = nullptr;              // device view of the cold tier
+  uint64_t cold_stride = 0;
+  bool own_cold = false;
+  void* registered = nullptr;                     // caller matrix registered for INDIRECT
+  uint32_t* cold_src = nullptr;                   // INDIRECT: cold slot -> original row
+  bool own_cold_src = false;
+  const tg_store* cold_owner = nullptr;
+  bool placed = false;
+  uint64_t* counters = nullptr;                   // device: 3 x u64 + err
+};
+
+namespace tgb {
+
+// --------------------------------------------------------------- host logic
+void validate_layout(const tg_layout& l) {  // tiering.cpp:10-18
+  if (l.num_devices < 1) domain_error("layout: num_devices must be >= 1");
+  if (l.local_boundary > l.multi_boundary || l.multi_boundary > l.num_rows)
+    domain_error("layout: need 0 <= local_boundary <= multi_boundary <= num_rows, got " +
+                 std::to_string(l.local_boundary) + ", " + std::to_string(l.multi_boundary) +
+                 ", " + std::to_string(l.num_rows));
+}
+
+tg_layout plan_layout(uint64_t num_rows, double hot, double rep, uint32_t devices, uint64_t dim,
+                      uint32_t eb, uint64_t budget) {  // tiering.cpp:67-98
+  if (!(rep >= 0.0 && rep <= hot && hot <= 1.0))
+    domain_error("plan_layout: need 0 <= replicated_fraction <= hot_fraction <= 1");
+  if (devices < 1) domain_error("plan_layout: num_devices must be >= 1");
+  tg_layout l{};
+  l.num_rows = num_rows;
+  l.local_boundary = static_cast<uint64_t>(std::llround(rep * static_cast<double>(num_rows)));
+  l.multi_boundary = static_cast<uint64_t>(std::llround(hot * static_cast<double>(num_rows)));
+  l.num_devices = devices;
+  l.feature_dim = dim;
+  l.elem_bytes = eb;
+  validate_layout(l);
+  if (budget > 0) {
+    const uint64_t inter = l.multi_boundary - l.local_boundary;
+    const uint64_t per_dev = l.local_boundary + (inter + devices - 1) / devices;
+    const uint64_t required = per_dev * (dim * eb);
+    if (required > budget)
+      domain_error("layout needs " + std::to_string(required) +
+                   " bytes per device but the budget is " + std::to_string(budget));
+  }
+  return l;
+}
+
+void range_error(const tg_layout& l, uint64_t row) {  // tiering.cpp:50-52
+  domain_error("row " + std::to_string(row) + " out of range for " + std::to_string(l.num_rows) +
+               " rows");
+}
+void device_error(const tg_layout& l, uint32_t dev) {  // tiering.cpp:53-55
+  domain_error("requesting device " + std::to_string(dev) + " out of range for " +
+               std::to_string(l.num_devices) + " devices");
+}
+
+// ------------------------------------------------------------ device resolve
+struct TierMap {
+  uint64_t lb, mb, nrows;
+  uint32_t D, dev;
+};
+
+// 0 local (replicated, or interleaved on the requesting device), 1 peer, 2 host, 3 invalid.
+__device__ __forceinline__ int tier_of(const TierMap& m, uint64_t id, uint32_t* owner,
+                                       uint64_t* slot) {
+  if (id >= m.nrows) return 3;
+  if (id < m.lb) {
+    *slot = id;
+    return 0;
+  }
+  if (id < m.mb) {
+    const uint64_t off = id - m.lb;
+    uint32_t d;
+    uint64_t s;
+    if (m.D == 1) {
+      d = 0;
+      s = off;
+    } else if (off < 0xffffffffull) {  // 32-bit divide is far cheaper
+      const uint32_t o = static_cast<uint32_t>(off);
+      d = o % m.D;
+      s = o / m.D;
+    } else {
+      d = static_cast<uint32_t>(off % m.D);
+      s = off / m.D;
+    }
+    *owner = d;
+    *slot = s;
+    return d == m.dev ? 0 : 1;
+  }
+  *slot = id - m.mb;
+  return 2;
+}
+
+__device__ __forceinline__ void block_add_counters(uint64_t cl, uint64_t cp, uint64_t ch,
+                                                   uint64_t* counters) {
+  __shared__ unsigned long long sc[3];
+  if (threadIdx.x < 3) sc[threadIdx.x] = 0;
+  __syncthreads();
+  if ((threadIdx.x & 31) == 0) {
+    if (cl) atomicAdd(&sc[0], (unsigned long long)cl);
+    if (cp) atomicAdd(&sc[1], (unsigned long long)cp);
+    if (ch) atomicAdd(&sc[2], (unsigned long long)ch);
+  }
+  __syncthreads();
+  if (threadIdx.x < 3 && sc[threadIdx.x])
+    atomicAdd(reinterpret_cast<unsigned long long*>(counters) + threadIdx.x, sc[threadIdx.x]);
+}
+
+// tiering.cpp:100-125 gather(): accounting only, one id per thread.
+__global__ void __launch_bounds__(256) account_kernel(TierMap m, const uint64_t* __restrict__ ids,
+                                                      uint64_t n, uint64_t* counters,
+                                                      unsigned long long* err) {
+  uint64_t cl = 0, cp = 0, ch = 0;
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    uint32_t owner;
+    uint64_t slot;
+    const int t = tier_of(m, ids[i], &owner, &slot);
+    if (t == 3) atomicMin(err, (unsigned long long)i);
+    cl += t == 0;
+    cp += t == 1;
+    ch += t == 2;
+  }
+  // warp reduce then block
+  for (int o = 16; o; o >>= 1) {
+    cl += __shfl_xor_sync(0xffffffffu, cl, o);
+    cp += __shfl_xor_sync(0xffffffffu, cp, o);
+    ch += __shfl_xor_sync(0xffffffffu, ch, o);
+  }
+  block_add_counters(cl, cp, ch, counters);
+}
+
+// ------------------------------------------------------------- row copies
+__device__ __forceinline__ uint4 ld_stream_v4(const void* p) {
+  uint4 r;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+               : "l"(p));
+  return r;
+}
+template <typename V>
+__device__ __forceinline__ V ld_row(const V* p) {
+  return *p;
+}
+template <>
+__device__ __forceinline__ uint4 ld_row<uint4>(const uint4* p) {
+  return ld_stream_v4(p);
+}
+
+constexpr int kCopyChunks = 256;            // chunks per warp batch (8 per lane)
+constexpr int kCopyPerLane = kCopyChunks / 32;
+
+// Copies a batch of B rows: src[j]/dst[j] held by lane j (j < B, nullptr =
+// skip). C = row_bytes / sizeof(V) chunks per row; B*C <= kCopyChunks.
+template <typename V>
+__device__ __forceinline__ void copy_batch(const uint8_t* src, uint8_t* dst, uint32_t B,
+                                           uint32_t C, int lane) {
+  const uint32_t total = B * C;
+  V buf[kCopyPerLane];
+  const V* sp[kCopyPerLane];
+  V* dp[kCopyPerLane];
+#pragma unroll
+  for (int u = 0; u < kCopyPerLane; ++u) {
+    const uint32_t idx = lane + 32u * u;
+    const uint32_t row = idx < total ? idx / C : 0;
+    const uint32_t ch = idx - row * C;
+    const uint8_t* s = reinterpret_cast<const uint8_t*>(
+        __shfl_sync(0xffffffffu, reinterpret_cast<uintptr_t>(src), row));
+    uint8_t* d = reinterpret_cast<uint8_t*>(
+        __shfl_sync(0xffffffffu, reinterpret_cast<uintptr_t>(dst), row));
+    const bool ok = idx < total && s != nullptr;
+    sp[u] = ok ? reinterpret_cast<const V*>(s) + ch : nullptr;
+    dp[u] = ok ? reinterpret_cast<V*>(d) + ch : nullptr;
+  }
+#pragma unroll
+  for (int u = 0; u < kCopyPerLane; ++u)
+    if (sp[u]) buf[u] = ld_row<V>(sp[u]);
+#pragma unroll
+  for (int u = 0; u < kCopyPerLane; ++u)
+    if (dp[u]) *dp[u] = buf[u];
+}
+
+// Large rows (C > kCopyChunks): one row per warp, looped.
+template <typename V>
+__device__ __forceinline__ void copy_row_looped(const uint8_t* src, uint8_t* dst, uint64_t C,
+                                                int lane) {
+  const V* s = reinterpret_cast<const V*>(src);
+  V* d = reinterpret_cast<V*>(dst);
+  for (uint64_t c0 = 0; c0 < C; c0 += kCopyChunks) {
+    V buf[kCopyPerLane];
+#pragma unroll
+    for (int u = 0; u < kCopyPerLane; ++u) {
+      const uint64_t c = c0 + lane + 32u * u;
+      if (c < C) buf[u] = ld_row<V>(s + c);
+    }
+#pragma unroll
+    for (int u = 0; u < kCopyPerLane; ++u) {
+      const uint64_t c = c0 + lane + 32u * u;
+      if (c < C) d[c] = buf[u];
+    }
+  }
+}
+
+struct GatherTable {
+  TierMap m;
+  const uint8_t* local;
+  const uint8_t* inter[TG_MAX_DEVICES];
+  const uint8_t* cold;
+  const uint32_t* cold_src;
+  uint64_t R;
+  uint64_t cold_stride;
+};
+
+__device__ __forceinline__ const uint8_t* row_ptr(const GatherTable& t, uint64_t id, int* tier) {
+  uint32_t owner = 0;
+  uint64_t slot = 0;
+  const int k = tier_of(t.m, id, &owner, &slot);
+  *tier = k;
+  if (k == 3) return nullptr;
+  if (id < t.m.lb) return t.local + slot * t.R;
+  if (k == 2) {
+    const uint64_t row = t.cold_src ? t.cold_src[slot] : slot;
+    return t.cold + row * t.cold_stride;
+  }
+  return t.inter[owner] + slot * t.R;
+}
+
+// K8: the tiered gather. dst row i <- feature row ids[i].
+template <typename V>
+__global__ void __launch_bounds__(256) gather_kernel(GatherTable t, const uint64_t* __restrict__ ids,
+                                                     uint64_t n, uint8_t* __restrict__ dst,
+                                                     uint32_t B, uint32_t C, uint64_t* counters,
+                                                     unsigned long long* err) {
+  const int lane = threadIdx.x & 31;
+  const uint64_t warp = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
+  const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+  uint64_t cl = 0, cp = 0, ch = 0;
+  for (uint64_t b0 = warp * B; b0 < n; b0 += nwarps * B) {
+    const uint8_t* src = nullptr;
+    uint8_t* d = nullptr;
+    int tier = -1;
+    if (lane < (int)B && b0 + lane < n) {
+      src = row_ptr(t, ids[b0 + lane], &tier);
+      if (tier == 3) atomicMin(err, (unsigned long long)(b0 + lane));
+      else d = dst + (b0 + lane) * t.R;
+    }
+    cl += __popc(__ballot_sync(0xffffffffu, tier == 0));
+    cp += __popc(__ballot_sync(0xffffffffu, tier == 1));
+    ch += __popc(__ballot_sync(0xffffffffu, tier == 2));
+    if (C <= (uint32_t)kCopyChunks) {
+      copy_batch<V>(src, d, B, C, lane);
+    } else {
+      for (uint32_t j = 0; j < B; ++j) {
+        const uint8_t* s = reinterpret_cast<const uint8_t*>(
+            __shfl_sync(0xffffffffu, reinterpret_cast<uintptr_t>(src), j));
+        uint8_t* o = reinterpret_cast<uint8_t*>(
+            __shfl_sync(0xffffffffu, reinterpret_cast<uintptr_t>(d), j));
+        if (s) copy_row_looped<V>(s, o, C, lane);
+      }
+    }
+  }
+  if (lane != 0) cl = cp = ch = 0;
+  block_add_counters(cl, cp, ch, counters);
+}
+
+// Generic row mover: dst + dst_row(i)*dst_stride <- src + src_row(i)*src_stride
+// with the rows named by optional u64/u32 index arrays. Used for placement
+// (K7: hot slots and the cold copy) and reorder_features.
+struct MoveArgs {
+  const uint8_t* src;
+  uint8_t* dst;
+  uint64_t src_stride, dst_stride;
+  const uint32_t* src_idx32;  // src row = src_idx32[i] (else i)
+  const uint64_t* dst_idx64;  // dst row = dst_idx64[i] (else i)
+  uint64_t src_row_base;      // added to i before src_idx32 lookup
+  uint32_t slot_mode;         // 1: src row index from slot i of a store (see below)
+  uint64_t lb;
+  uint32_t D, dev;
+};
+
+__device__ __forceinline__ uint64_t store_slot_row(uint64_t s, uint64_t lb, uint32_t D,
+                                                   uint32_t dev) {
+  return s < lb ? s : lb + (s - lb) * D + dev;
+}
+
+template <typename V>
+__global__ void __launch_bounds__(256) move_rows_kernel(MoveArgs a, uint64_t n, uint32_t B,
+                                                        uint32_t C) {
+  const int lane = threadIdx.x & 31;
+  const uint64_t warp = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
+  const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+  for (uint64_t b0 = warp * B; b0 < n; b0 += nwarps * B) {
+    const uint8_t* s = nullptr;
+    uint8_t* d = nullptr;
+    if (lane < (int)B && b0 + lane < n) {
+      const uint64_t i = b0 + lane;
+      uint64_t k = a.src_row_base + (a.slot_mode ? store_slot_row(i, a.lb, a.D, a.dev) : i);
+      const uint64_t sr = a.src_idx32 ? a.src_idx32[k] : k;
+      const uint64_t dr = a.dst_idx64 ? a.dst_idx64[i] : i;
+      s = a.src + sr * a.src_stride;
+      d = a.dst + dr * a.dst_stride;
+    }
+    if (C <= (uint32_t)kCopyChunks) {
+      copy_batch<V>(s, d, B, C, lane);
+    } else {
+      for (uint32_t j = 0; j < B; ++j) {
+        const uint8_t* ss = reinterpret_cast<const uint8_t*>(
+            __shfl_sync(0xffffffffu, reinterpret_cast<uintptr_t>(s), j));
+        uint8_t* dd = reinterpret_cast<uint8_t*>(
+            __shfl_sync(0xffffffffu, reinterpret_cast<uintptr_t>(d), j));
+        if (ss) copy_row_looped<V>(ss, dd, C, lane);
+      }
+    }
+  }
+}
+
+// Widest vector the row size and every base/stride allow.
+int vec_width(uint64_t R, std::initializer_list<uint64_t> addrs) {
+  int w = 16;
+  while (w > 1) {
+    bool ok = R % w == 0;
+    for (uint64_t a : addrs) ok = ok && a % w == 0;
+    if (ok) break;
+    w >>= 1;
+  }
+  return w;
+}
+
+void batch_shape(uint64_t R, int w, uint32_t* B, uint32_t* C) {
+  const uint64_t c = R / w;
+  *C = static_cast<uint32_t>(c);
+  *B = c >= (uint64_t)kCopyChunks ? 1u : static_cast<uint32_t>(std::min<uint64_t>(32, kCopyChunks / c));
+}
+
+void launch_move(tg_ctx* ctx, const MoveArgs& a, uint64_t n, uint64_t R) {
+  if (n == 0 || R == 0) return;
+  const int w = vec_width(R, {reinterpret_cast<uint64_t>(a.src), reinterpret_cast<uint64_t>(a.dst),
+                             a.src_stride, a.dst_stride});
+  uint32_t B, C;
+  batch_shape(R, w, &B, &C);
+  const uint64_t warps = (n + B - 1) / B;
+  const unsigned grid = grid_for(warps * 32, 256, ctx->num_sms * 16);
+  switch (w) {
+    case 16: move_rows_kernel<uint4><<<grid, 256, 0, ctx->stream>>>(a, n, B, C); break;
+    case 8: move_rows_kernel<uint2><<<grid, 256, 0, ctx->stream>>>(a, n, B, C); break;
+    case 4: move_rows_kernel<uint32_t><<<grid, 256, 0, ctx->stream>>>(a, n, B, C); break;
+    case 2: move_rows_kernel<uint16_t><<<grid, 256, 0, ctx->stream>>>(a, n, B, C); break;
+    default: move_rows_kernel<uint8_t><<<grid, 256, 0, ctx->stream>>>(a, n, B, C); break;
+  }
+  TGB_LAUNCHED();
+}
+
+// ---------------------------------------------------------- permutation util
+__global__ void perm_check_kernel(const uint64_t* __restrict__ p, uint64_t n,
+                                  uint32_t* __restrict__ seen, uint32_t* __restrict__ inv,
+                                  unsigned long long* bad) {
+  for (uint64_t u = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; u < n;
+       u += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t v = p[u];
+    if (v >= n) {
+      atomicMin(bad, (unsigned long long)u);
+      continue;
+    }
+    if (atomicAdd(&seen[v], 1u) != 0) atomicMin(bad, (unsigned long long)u);
+    if (inv) inv[v] = static_cast<uint32_t>(u);
+  }
+}
+
+// Validates a permutation (reorder.cpp:10-21) and optionally builds its
+// inverse as u32. Throws DomainError naming the offending new id.
+void check_permutation(tg_ctx* ctx, const uint64_t* perm_dev, uint64_t n, uint32_t* inv_dev) {
+  if (n == 0) return;
+  if (n >= 0xffffffffull) domain_error("permutation: n must be < 2^32");
+  uint32_t* seen = ctx->scratch_t<uint32_t>(kScratchE, n);
+  auto* bad = ctx->scratch_t<unsigned long long>(kSmall, 1);
+  TGB_CUDA(cudaMemsetAsync(seen, 0, n * 4, ctx->stream));
+  TGB_CUDA(cudaMemsetAsync(bad, 0xff, 8, ctx->stream));
+  perm_check_kernel<<<grid_for(n, 256), 256, 0, ctx->stream>>>(perm_dev, n, seen, inv_dev, bad);
+  TGB_LAUNCHED();
+  unsigned long long hb;
+  TGB_CUDA(cudaMemcpyAsync(&hb, bad, 8, cudaMemcpyDeviceToHost, ctx->stream));
+  ctx->sync();
+  if (hb != ~0ull) {
+    // Reproduce the reference's message for the FIRST offending position.
+    uint64_t v;
+    TGB_CUDA(cudaMemcpy(&v, perm_dev + hb, 8, cudaMemcpyDeviceToHost));
+    if (v >= n) domain_error("permutation: new id " + std::to_string(v) + " out of range");
+    domain_error("permutation: new id " + std::to_string(v) + " assigned twice");
+  }
+}
+
+__global__ void u32_to_u64_kernel(const uint32_t* __restrict__ in, uint64_t* __restrict__ out,
+                                  uint64_t n) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+       i += (uint64_t)gridDim.x * blockDim.x)
+    out[i] = in[i];
+}
+
+// ------------------------------------------------------------ trace replays
+__global__ void row_order_kernel(const uint64_t* __restrict__ counts, uint64_t n,
+                                 const uint64_t* __restrict__ ordering,
+                                 uint64_t* __restrict__ out, unsigned long long* bad) {
+  for (uint64_t k = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; k < n;
+       k += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t u = ordering[k];
+    if (u >= n) {
+      atomicMin(bad, (unsigned long long)k);
+      out[k] = 0;
+    } else {
+      out[k] = counts[u];
+    }
+  }
+}
+
+constexpr int kMaxSim = 16;
+struct SimLayouts {
+  uint64_t lb[kMaxSim], mb[kMaxSim];
+  uint32_t D[kMaxSim];
+  int count;
+};
+
+// tiering.cpp:137-157 for several layouts at once; out[4*f + {local,peer,host}], out[3] total
+__global__ void __launch_bounds__(256) simulate_kernel(const uint64_t* __restrict__ counts, uint64_t n,
+                                                       SimLayouts L, unsigned long long* out) {
+  __shared__ unsigned long long acc[kMaxSim * 3 + 1];
+  for (int i = threadIdx.x; i < kMaxSim * 3 + 1; i += blockDim.x) acc[i] = 0;
+  __syncthreads();
+  uint64_t loc[kMaxSim], peer[kMaxSim], host[kMaxSim], total = 0;
+#pragma unroll
+  for (int f = 0; f < kMaxSim; ++f) loc[f] = peer[f] = host[f] = 0;
+  for (uint64_t row = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; row < n;
+       row += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t c = counts[row];
+    if (!c) continue;
+    total += c;
+#pragma unroll
+    for (int f = 0; f < kMaxSim; ++f) {
+      if (f >= L.count) break;
+      if (row < L.lb[f]) {
+        loc[f] += c;
+      } else if (row < L.mb[f]) {
+        const uint64_t D = L.D[f];
+        const uint64_t owner = (row - L.lb[f]) % D;
+        const uint64_t l = c / D + (owner < c % D ? 1 : 0);  // tiering.cpp:148
+        loc[f] += l;
+        peer[f] += c - l;
+      } else {
+        host[f] += c;
+      }
+    }
+  }
+  for (int o = 16; o; o >>= 1) total += __shfl_xor_sync(0xffffffffu, total, o);
+#pragma unroll
+  for (int f = 0; f < kMaxSim; ++f) {
+    if (f >= L.count) break;
+    for (int o = 16; o; o >>= 1) {
+      loc[f] += __shfl_xor_sync(0xffffffffu, loc[f], o);
+      peer[f] += __shfl_xor_sync(0xffffffffu, peer[f], o);
+      host[f] += __shfl_xor_sync(0xffffffffu, host[f], o);
+    }
+  }
+  if ((threadIdx.x & 31) == 0) {
+    for (int f = 0; f < L.count; ++f) {
+      if (loc[f]) atomicAdd(&acc[3 * f], (unsigned long long)loc[f]);
+      if (peer[f]) atomicAdd(&acc[3 * f + 1], (unsigned long long)peer[f]);
+      if (host[f]) atomicAdd(&acc[3 * f + 2], (unsigned long long)host[f]);
+    }
+    if (total) atomicAdd(&acc[kMaxSim * 3], (unsigned long long)total);
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < kMaxSim * 3 + 1; i += blockDim.x)
+    if (acc[i]) atomicAdd(&out[i], acc[i]);
+}
+
+// Runs simulate_trace for each layout over device counts; returns total.
+uint64_t simulate_many(tg_ctx* ctx, const uint64_t* counts_dev, uint64_t n,
+                       const std::vector<tg_layout>& layouts, std::vector<tg_report>& out) {
+  out.assign(layouts.size(), tg_report{});
+  uint64_t total = 0;
+  auto* acc = ctx->scratch_t<unsigned long long>(kSmall, kMaxSim * 3 + 1);
+  for (size_t f0 = 0; f0 < std::max<size_t>(layouts.size(), 1); f0 += kMaxSim) {
+    SimLayouts L{};
+    L.count = static_cast<int>(std::min<size_t>(kMaxSim, layouts.size() - std::min(f0, layouts.size())));
+    for (int f = 0; f < L.count; ++f) {
+      L.lb[f] = layouts[f0 + f].local_boundary;
+      L.mb[f] = layouts[f0 + f].multi_boundary;
+      L.D[f] = layouts[f0 + f].num_devices;
+    }
+    TGB_CUDA(cudaMemsetAsync(acc, 0, sizeof(unsigned long long) * (kMaxSim * 3 + 1), ctx->stream));
+    if (n) {
+      simulate_kernel<<<grid_for(n, 256, ctx->num_sms * 4), 256, 0, ctx->stream>>>(counts_dev, n, L,
+                                                                                  acc);
+      TGB_LAUNCHED();
+    }
+    unsigned long long h[kMaxSim * 3 + 1];
+    TGB_CUDA(cudaMemcpyAsync(h, acc, sizeof(h), cudaMemcpyDeviceToHost, ctx->stream));
+    ctx->sync();
+    total = h[kMaxSim * 3];
+    for (int f = 0; f < L.count; ++f) {
+      tg_report& r = out[f0 + f];
+      const uint64_t rb = layouts[f0 + f].feature_dim * layouts[f0 + f].elem_bytes;
+      r.local_accesses = h[3 * f];
+      r.peer_accesses = h[3 * f + 1];
+      r.host_accesses = h[3 * f + 2];
+      r.local_bytes = r.local_accesses * rb;  // tiering.cpp:158-160
+      r.peer_bytes = r.peer_accesses * rb;
+      r.host_bytes = r.host_accesses * rb;
+    }
+    if (layouts.empty()) break;
+  }
+  return total;
+}
+
+// Reference-counted cudaHostRegister of caller matrices, so several stores
+// (virtual devices, or a store and a later re-placement) can map the same
+// host matrix. Memory pinned outside the library is used as is.
+std::mutex g_reg_mu;
+std::map<void*, std::pair<uint64_t, int>> g_reg;
+
+const uint8_t* acquire_host_matrix(const void* p, uint64_t bytes, bool* owned) {
+  std::lock_guard<std::mutex> lk(g_reg_mu);
+  void* key = const_cast<void*>(p);
+  auto it = g_reg.find(key);
+  if (it != g_reg.end()) {
+    ++it->second.second;
+    *owned = true;
+  } else if (void* m = mapped_device_ptr(p)) {
+    *owned = false;
+    return static_cast<const uint8_t*>(m);
+  } else {
+    TGB_CUDA(cudaHostRegister(key, bytes, cudaHostRegisterMapped | cudaHostRegisterPortable));
+    g_reg[key] = {bytes, 1};
+    *owned = true;
+  }
+  void* m = nullptr;
+  TGB_CUDA(cudaHostGetDevicePointer(&m, key, 0));
+  return static_cast<const uint8_t*>(m);
+}
+
+void release_host_matrix(void* p) {
+  std::lock_guard<std::mutex> lk(g_reg_mu);
+  auto it = g_reg.find(p);
+  if (it == g_reg.end()) return;
+  if (--it->second.second == 0) {
+    cudaHostUnregister(p);
+    g_reg.erase(it);
+  }
+}
+
+void add_report(tg_report* r, uint64_t l, uint64_t p, uint64_t h, uint64_t rb) {
+  r->local_accesses += l;
+  r->peer_accesses += p;
+  r->host_accesses += h;
+  r->local_bytes += l * rb;
+  r->peer_bytes += p * rb;
+  r->host_bytes += h * rb;
+}
+
+void account(tg_ctx* ctx, const tg_layout& l, const uint64_t* ids_dev, uint64_t n, uint32_t dev,
+             uint64_t* counters3, unsigned long long* err) {
+  TierMap m{l.local_boundary, l.multi_boundary, l.num_rows, l.num_devices, dev};
+  account_kernel<<<grid_for(n, 256, ctx->num_sms * 8), 256, 0, ctx->stream>>>(m, ids_dev, n,
+                                                                              counters3, err);
+  TGB_LAUNCHED();
+}
+
+GatherTable make_table(const tg_store* s) {
+  GatherTable t{};
+  t.m = TierMap{s->L.local_boundary, s->L.multi_boundary, s->L.num_rows, s->L.num_devices, s->dev};
+  t.local = s->local;
+  for (uint32_t d = 0; d < s->L.num_devices; ++d) t.inter[d] = s->inter[d];
+  t.cold = s->cold_dev;
+  t.cold_src = s->cold_src;
+  t.R = s->R;
+  t.cold_stride = s->cold_stride;
+  return t;
+}
+
+void launch_gather(tg_store* s, const uint64_t* ids_dev, uint64_t n, void* dst_dev,
+                   uint64_t* counters3, unsigned long long* err) {
+  tg_ctx* ctx = s->ctx;
+  if (!s->placed) domain_error("tiered store: tg_store_place has not run");
+  const uint64_t inter_rows = s->L.multi_boundary - s->L.local_boundary;
+  for (uint32_t d = 0; d < s->L.num_devices && inter_rows > d; ++d)
+    if (!s->inter[d]) domain_error("tiered store: peer slice of device " + std::to_string(d) +
+                                   " is not attached (tg_store_set_peer)");
+  const GatherTable t = make_table(s);
+  uint64_t align = reinterpret_cast<uint64_t>(dst_dev) | reinterpret_cast<uint64_t>(s->local) |
+                   reinterpret_cast<uint64_t>(s->cold_dev) | s->cold_stride;
+  for (uint32_t d = 0; d < s->L.num_devices; ++d) align |= reinterpret_cast<uint64_t>(s->inter[d]);
+  const int w = vec_width(s->R, {align});
+  uint32_t B, C;
+  batch_shape(s->R, w, &B, &C);
+  const uint64_t warps = (n + B - 1) / B;
+  const unsigned grid = grid_for(warps * 32, 256, ctx->num_sms * 8);
+  auto* dst = static_cast<uint8_t*>(dst_dev);
+  switch (w) {
+    case 16: gather_kernel<uint4><<<grid, 256, 0, ctx->stream>>>(t, ids_dev, n, dst, B, C, counters3, err); break;
+    case 8: gather_kernel<uint2><<<grid, 256, 0, ctx->stream>>>(t, ids_dev, n, dst, B, C, counters3, err); break;
+    case 4: gather_kernel<uint32_t><<<grid, 256, 0, ctx->stream>>>(t, ids_dev, n, dst, B, C, counters3, err); break;
+    case 2: gather_kernel<uint16_t><<<grid, 256, 0, ctx->stream>>>(t, ids_dev, n, dst, B, C, counters3, err); break;
+    default: gather_kernel<uint8_t><<<grid, 256, 0, ctx->stream>>>(t, ids_dev, n, dst, B, C, counters3, err); break;
+  }
+  TGB_LAUNCHED();
+}
+
+}  // namespace tgb
+
+using namespace tgb;
+
+extern "C" {
+
+int tg_validate_layout(const tg_layout* layout) {
+  return guard([&] { validate_layout(*layout); });
+}
+
+int tg_validate_cost_model(double l, double p, double h) {
+  return guard([&] {  // tiering.cpp:20-23
+    if (!(l > 0.0 && p > 0.0 && h > 0.0)) domain_error("cost model: all bandwidths must be positive");
+  });
+}
+
+int tg_resolve(const tg_layout* l, uint64_t row, uint32_t dev, tg_location* out) {
+  return guard([&] {  // tiering.cpp:48-65
+    if (row >= l->num_rows) range_error(*l, row);
+    if (dev >= l->num_devices) device_error(*l, dev);
+    if (row < l->local_boundary) {
+      *out = {TG_TIER_LOCAL_HOT, 0, row};
+    } else if (row < l->multi_boundary) {
+      const uint64_t off = row - l->local_boundary;
+      *out = {TG_TIER_INTERLEAVED, static_cast<uint32_t>(off % l->num_devices), off / l->num_devices};
+    } else {
+      *out = {TG_TIER_COLD_HOST, 0, row - l->multi_boundary};
+    }
+  });
+}
+
+int tg_plan_layout(uint64_t num_rows, double hot, double rep, uint32_t devices, uint64_t dim,
+                   uint32_t eb, uint64_t budget, tg_layout* out) {
+  return guard([&] { *out = plan_layout(num_rows, hot, rep, devices, dim, eb, budget); });
+}
+
+double tg_report_hit_ratio(const tg_report* r) {  // tiering.cpp:25-29
+  const uint64_t total = r->local_accesses + r->peer_accesses + r->host_accesses;
+  if (total == 0) return 0.0;
+  return 1.0 - static_cast<double>(r->host_accesses) / static_cast<double>(total);
+}
+
+double tg_report_est_transfer_seconds(const tg_report* r, double l, double p, double h) {
+  constexpr double kGiB = 1e9;  // tiering.cpp:31-36
+  return static_cast<double>(r->local_bytes) / (l * kGiB) +
+         static_cast<double>(r->peer_bytes) / (p * kGiB) +
+         static_cast<double>(r->host_bytes) / (h * kGiB);
+}
+
+int tg_gather_account(tg_ctx* ctx, const tg_layout* layout, const uint64_t* ids, uint64_t n,
+                      uint32_t dev, tg_report* report) {
+  return guard([&] {
+    if (n == 0) return;  // the reference loop body never runs
+    DeviceGuard dg(ctx->device);
+    const uint64_t* d = dev_in(ctx, ids, n, kStageIn0);
+    auto* c = ctx->scratch_t<uint64_t>(kSmall, 4);
+    auto* err = reinterpret_cast<unsigned long long*>(c + 3);
+    TGB_CUDA(cudaMemsetAsync(c, 0, 24, ctx->stream));
+    TGB_CUDA(cudaMemsetAsync(err, 0xff, 8, ctx->stream));
+    const uint64_t rb = layout->feature_dim * layout->elem_bytes;
+    if (dev >= layout->num_devices) {
+      // resolve() range-checks the row first, then the device (tiering.cpp:50-55)
+      uint64_t id0;
+      TGB_CUDA(cudaMemcpy(&id0, d, 8, cudaMemcpyDeviceToHost));
+      if (id0 >= layout->num_rows) range_error(*layout, id0);
+      device_error(*layout, dev);
+    }
+    account(ctx, *layout, d, n, dev, c, err);
+    uint64_t h[4];
+    TGB_CUDA(cudaMemcpyAsync(h, c, 32, cudaMemcpyDeviceToHost, ctx->stream));
+    ctx->sync();
+    if (h[3] != ~0ull) {
+      // keep the prefix before the first bad id accounted, then throw
+      const uint64_t first = h[3];
+      TGB_CUDA(cudaMemsetAsync(c, 0, 24, ctx->stream));
+      if (first) account(ctx, *layout, d, first, dev, c, err);
+      TGB_CUDA(cudaMemcpyAsync(h, c, 24, cudaMemcpyDeviceToHost, ctx->stream));
+      ctx->sync();
+      add_report(report, h[0], h[1], h[2], rb);
+      uint64_t bad;
+      TGB_CUDA(cudaMemcpy(&bad, d + first, 8, cudaMemcpyDeviceToHost));
+      range_error(*layout, bad);
+    }
+    add_report(report, h[0], h[1], h[2], rb);
+  });
+}
+
+int tg_simulate_trace(tg_ctx* ctx, const uint64_t* counts, uint64_t n, const tg_layout* layout,
+                      tg_report* out) {
+  return guard([&] {  // tiering.cpp:127-162
+    validate_layout(*layout);
+    if (n != layout->num_rows)
+      domain_error("counter covers " + std::to_string(n) + " rows but the layout has " +
+                   std::to_string(layout->num_rows));
+    DeviceGuard dg(ctx->device);
+    const uint64_t* c = dev_in(ctx, counts, n, kStageIn0);
+    std::vector<tg_report> reps;
+    const uint64_t total = simulate_many(ctx, c, n, {*layout}, reps);
+    if (total == 0) domain_error("simulate_trace: counter total is zero");
+    *out = reps[0];
+  });
+}
+
+int tg_counts_in_row_order(tg_ctx* ctx, const uint64_t* counts, uint64_t n,
+                           const uint64_t* ordering, uint64_t m, uint64_t* out) {
+  return guard([&] {  // tiering.cpp:164-175
+    if (m != n) domain_error("ordering length != counter length");
+    if (n == 0) return;
+    DeviceGuard dg(ctx->device);
+    const uint64_t* c = dev_in(ctx, counts, n, kStageIn0);
+    const uint64_t* o = dev_in(ctx, ordering, n, kStageIn1);
+    DevOut<uint64_t> r(ctx, out, n, kStageOut0);
+    auto* bad = ctx->scratch_t<unsigned long long>(kSmall, 1);
+    TGB_CUDA(cudaMemsetAsync(bad, 0xff, 8, ctx->stream));
+    row_order_kernel<<<grid_for(n, 256), 256, 0, ctx->stream>>>(c, n, o, r.dev(), bad);
+    TGB_LAUNCHED();
+    unsigned long long hb;
+    TGB_CUDA(cudaMemcpyAsync(&hb, bad, 8, cudaMemcpyDeviceToHost, ctx->stream));
+    r.finish();
+    if (hb != ~0ull) domain_error("ordering id out of range");
+  });
+}
+
+int tg_hot_fraction_sweep(tg_ctx* ctx, const uint64_t* counts, uint64_t n,
+                          const uint64_t* ordering, const double* fr, uint64_t nf,
+                          double replicated, uint32_t devices, uint64_t dim, uint32_t eb,
+                          uint64_t budget, tg_layout* out_layouts, tg_report* out_reports,
+                          double* out_rep) {
+  return guard([&] {  // tiering.cpp:177-202
+    for (uint64_t i = 1; i < nf; ++i)
+      if (fr[i] < fr[i - 1]) domain_error("sweep fractions must be sorted ascending");
+    DeviceGuard dg(ctx->device);
+    // counts_in_row_order (throws before any layout is planned)
+    uint64_t* rc = ctx->scratch_t<uint64_t>(kScratchF, n ? n : 1);
+    if (n) {
+      const uint64_t* c = dev_in(ctx, counts, n, kStageIn0);
+      const uint64_t* o = dev_in(ctx, ordering, n, kStageIn1);
+      auto* bad = ctx->scratch_t<unsigned long long>(kSmall, 1);
+      TGB_CUDA(cudaMemsetAsync(bad, 0xff, 8, ctx->stream));
+      row_order_kernel<<<grid_for(n, 256), 256, 0, ctx->stream>>>(c, n, o, rc, bad);
+      TGB_LAUNCHED();
+      unsigned long long hb;
+      TGB_CUDA(cudaMemcpyAsync(&hb, bad, 8, cudaMemcpyDeviceToHost, ctx->stream));
+      ctx->sync();
+      if (hb != ~0ull) domain_error("ordering id out of range");
+    }
+    std::vector<tg_layout> lays;
+    std::vector<double> reps;
+    std::vector<tg_report> out;
+    bool total_checked = false;
+    for (uint64_t i = 0; i < nf; ++i) {
+      const double rep = std::min(replicated, fr[i]);  // :195
+      lays.push_back(plan_layout(n, fr[i], rep, devices, dim, eb, budget));
+      reps.push_back(rep);
+      if (!total_checked) {
+        // simulate_trace of the first fraction runs before the next plan_layout
+        std::vector<tg_report> first;
+        if (simulate_many(ctx, rc, n, {lays[0]}, first) == 0)
+          domain_error("simulate_trace: counter total is zero");
+        total_checked = true;
+      }
+    }
+    simulate_many(ctx, rc, n, lays, out);
+    for (uint64_t i = 0; i < nf; ++i) {
+      out_layouts[i] = lays[i];
+      out_reports[i] = out[i];
+      out_rep[i] = reps[i];
+    }
+  });
+}
+
+// --------------------------------------------------------------- the store
+int tg_store_create(tg_ctx* ctx, const tg_layout* layout, uint32_t device_index, uint32_t flags,
+                    tg_store** out) {
+  return guard([&] {
+    validate_layout(*layout);
+    if (layout->num_devices > TG_MAX_DEVICES)
+      domain_error("tiered store: at most " + std::to_string(TG_MAX_DEVICES) + " devices");
+    if (device_index >= layout->num_devices) device_error(*layout, device_index);
+    DeviceGuard dg(ctx->device);
+    auto* s = new tg_store;
+    s->ctx = ctx;
+    s->L = *layout;
+    s->dev = device_index;
+    s->flags = flags;
+    s->R = layout->feature_dim * layout->elem_bytes;
+    const uint64_t lb = layout->local_boundary, mb = layout->multi_boundary;
+    const uint64_t D = layout->num_devices;
+    const uint64_t inter = mb - lb;
+    const uint64_t mine = inter > device_index ? (inter - device_index + D - 1) / D : 0;
+    s->local_rows = lb + mine;
+    try {
+      TGB_CUDA(cudaMalloc(&s->local, std::max<uint64_t>(s->local_rows * s->R, 16)));
+      TGB_CUDA(cudaMalloc(&s->counters, 64));
+      s->inter[device_index] = s->local + lb * s->R;
+    } catch (...) {
+      tg_store_destroy(s);
+      throw;
+    }
+    *out = s;
+  });
+}
+
+int tg_store_destroy(tg_store* s) {
+  if (!s) return TG_OK;
+  DeviceGuard dg(s->ctx->device);
+  cudaFree(s->local);
+  cudaFree(s->counters);
+  if (s->own_cold && s->cold_host) cudaFreeHost(s->cold_host);
+  if (s->own_cold_src) cudaFree(s->cold_src);
+  if (s->registered) release_host_matrix(s->registered);
+  delete s;
+  return TG_OK;
+}
+
+void* tg_store_local_base(const tg_store* s) { return s ? s->local : nullptr; }
+uint64_t tg_store_local_rows(const tg_store* s) { return s ? s->local_rows : 0; }
+
+int tg_store_set_peer(tg_store* s, uint32_t d, const void* peer_local_base) {
+  return guard([&] {
+    if (d >= s->L.num_devices) device_error(s->L, d);
+    s->inter[d] = static_cast<const uint8_t*>(peer_local_base) + s->L.local_boundary * s->R;
+  });
+}
+
+int tg_store_share_cold(tg_store* s, const tg_store* owner) {
+  return guard([&] {
+    if (owner->L.num_rows != s->L.num_rows || owner->L.multi_boundary != s->L.multi_boundary ||
+        owner->R != s->R)
+      domain_error("tiered store: cold tier layouts differ");
+    s->cold_owner = owner;
+  });
+}
+
+int tg_store_place(tg_store* s, const void* features, const uint64_t* new_id_of) {
+  return guard([&] {
+    tg_ctx* ctx = s->ctx;
+    DeviceGuard dg(ctx->device);
+    const uint64_t N = s->L.num_rows, R = s->R, mb = s->L.multi_boundary;
+    if (N == 0) {
+      s->placed = true;
+      return;
+    }
+    // the permutation (validated like reorder_features, reorder.cpp:102) and its inverse
+    const uint64_t* perm = dev_in(ctx, new_id_of, N, kStageIn0);
+    uint32_t* order = ctx->scratch_t<uint32_t>(kScratchD, N);
+    check_permutation(ctx, perm, N, order);
+    // source rows: device memory, mapped pinned memory, or pageable (registered here)
+    const uint8_t* src = nullptr;
+    void* reg = nullptr;
+    if (is_device_ptr(features)) {
+      src = static_cast<const uint8_t*>(features);
+    } else {
+      bool owned = false;
+      src = acquire_host_matrix(features, N * R, &owned);
+      if (owned) reg = const_cast<void*>(features);
+    }
+    // K7a: this device's HBM rows (replicated prefix + interleaved slice)
+    MoveArgs a{};
+    a.src = src;
+    a.dst = s->local;
+    a.src_stride = R;
+    a.dst_stride = R;
+    a.src_idx32 = order;
+    a.slot_mode = 1;
+    a.lb = s->L.local_boundary;
+    a.D = s->L.num_devices;
+    a.dev = s->dev;
+    launch_move(ctx, a, s->local_rows, R);
+    // K7b: the cold tier
+    if (s->cold_owner) {
+      s->cold_dev = s->cold_owner->cold_dev;
+      s->cold_src = s->cold_owner->cold_src;
+      s->cold_stride = s->cold_owner->cold_stride;
+    } else if (s->flags & TG_COLD_INDIRECT) {
+      if (is_device_ptr(features)) domain_error("TG_COLD_INDIRECT needs the matrix in host memory");
+      const uint64_t cold = N - mb;
+      TGB_CUDA(cudaMalloc(&s->cold_src, sizeof(uint32_t) * std::max<uint64_t>(cold, 1)));
+      s->own_cold_src = true;
+      if (cold)
+        TGB_CUDA(cudaMemcpyAsync(s->cold_src, order + mb, cold * 4, cudaMemcpyDeviceToDevice,
+                                 ctx->stream));
+      s->cold_dev = src;
+      s->cold_stride = R;
+      s->registered = reg;  // keep the caller's matrix mapped for the store's lifetime
+      reg = nullptr;
+    } else {
+      const uint64_t cold = N - mb;
+      s->cold_stride = (s->flags & TG_COLD_PAD128) ? (R + 127) / 128 * 128 : R;
+      if (!s->own_cold) {
+        TGB_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&s->cold_host),
+                               std::max<uint64_t>(cold * s->cold_stride, 16),
+                               cudaHostAllocMapped | cudaHostAllocPortable));
+        s->own_cold = true;
+      }
+      void* cd = nullptr;
+      TGB_CUDA(cudaHostGetDevicePointer(&cd, s->cold_host, 0));
+      s->cold_dev = static_cast<const uint8_t*>(cd);
+      MoveArgs c{};
+      c.src = src;
+      c.dst = static_cast<uint8_t*>(cd);
+      c.src_stride = R;
+      c.dst_stride = s->cold_stride;
+      c.src_idx32 = order;
+      c.src_row_base = mb;
+      launch_move(ctx, c, cold, R);
+    }
+    ctx->sync();
+    if (reg) release_host_matrix(reg);
+    s->placed = true;
+  });
+}
+
+int tg_gather_rows_async(tg_store* s, const uint64_t* ids_dev, uint64_t n, void* dst_dev,
+                         uint64_t* counters_dev, uint64_t* err_dev) {
+  return guard([&] {
+    if (n == 0) return;
+    DeviceGuard dg(s->ctx->device);
+    launch_gather(s, ids_dev, n, dst_dev, counters_dev,
+                  reinterpret_cast<unsigned long long*>(err_dev));
+  });
+}
+
+int tg_gather_rows(tg_store* s, const uint64_t* ids, uint64_t n, void* dst, tg_report* report) {
+  return guard([&] {
+    if (n == 0) return;
+    tg_ctx* ctx = s->ctx;
+    DeviceGuard dg(ctx->device);
+    const uint64_t* d = dev_in(ctx, ids, n, kStageIn0);
+    DevOut<uint8_t> o(ctx, static_cast<uint8_t*>(dst), n * s->R, kStageOut0);
+    uint64_t* c = s->counters;
+    auto* err = reinterpret_cast<unsigned long long*>(c + 3);
+    TGB_CUDA(cudaMemsetAsync(c, 0, 24, ctx->stream));
+    TGB_CUDA(cudaMemsetAsync(err, 0xff, 8, ctx->stream));
+    launch_gather(s, d, n, o.dev(), c, err);
+    uint64_t h[4];
+    TGB_CUDA(cudaMemcpyAsync(h, c, 32, cudaMemcpyDeviceToHost, ctx->stream));
+    o.finish();
+    if (h[3] != ~0ull) {  // reference semantics: prefix accounted, then DomainError
+      const uint64_t first = h[3];
+      TGB_CUDA(cudaMemsetAsync(c, 0, 24, ctx->stream));
+      if (first) account(ctx, s->L, d, first, s->dev, c, err);
+      TGB_CUDA(cudaMemcpyAsync(h, c, 24, cudaMemcpyDeviceToHost, ctx->stream));
+      ctx->sync();
+      add_report(report, h[0], h[1], h[2], s->R);
+      uint64_t bad;
+      TGB_CUDA(cudaMemcpy(&bad, d + first, 8, cudaMemcpyDeviceToHost));
+      range_error(s->L, bad);
+    }
+    add_report(report, h[0], h[1], h[2], s->R);
+  });
+}
+
+// ------------------------------------------------------------- reorder ops
+int tg_validate_permutation(tg_ctx* ctx, const uint64_t* perm, uint64_t n) {
+  return guard([&] {
+    if (n == 0) return;
+    DeviceGuard dg(ctx->device);
+    check_permutation(ctx, dev_in(ctx, perm, n, kStageIn0), n, nullptr);
+  });
+}
+
+int tg_invert(tg_ctx* ctx, const uint64_t* perm, uint64_t n, uint64_t* out) {
+  return guard([&] {  // reorder.cpp:31-37
+    if (n == 0) return;
+    DeviceGuard dg(ctx->device);
+    const uint64_t* p = dev_in(ctx, perm, n, kStageIn0);
+    uint32_t* inv = ctx->scratch_t<uint32_t>(kScratchD, n);
+    check_permutation(ctx, p, n, inv);
+    DevOut<uint64_t> o(ctx, out, n, kStageOut0);
+    u32_to_u64_kernel<<<grid_for(n, 256), 256, 0, ctx->stream>>>(inv, o.dev(), n);
+    TGB_LAUNCHED();
+    o.finish();
+  });
+}
+
+int tg_reorder_features(tg_ctx* ctx, const void* src, uint64_t rows, uint64_t row_bytes,
+                        const uint64_t* perm, uint64_t perm_len, void* dst) {
+  return guard([&] {  // reorder.cpp:97-117
+    if (perm_len != rows)
+      domain_error("permutation length " + std::to_string(perm_len) + " != num_rows " +
+                   std::to_string(rows));
+    if (rows == 0) return;
+    DeviceGuard dg(ctx->device);
+    const uint64_t* p = dev_in(ctx, perm, rows, kStageIn0);
+    check_permutation(ctx, p, rows, nullptr);
+    const uint64_t bytes = rows * row_bytes;
+    const uint8_t* s = dev_in(ctx, static_cast<const uint8_t*>(src), bytes, kStageIn1);
+    DevOut<uint8_t> o(ctx, static_cast<uint8_t*>(dst), bytes, kStageOut0);
+    MoveArgs a{};
+    a.src = s;
+    a.dst = o.dev();
+    a.src_stride = row_bytes;
+    a.dst_stride = row_bytes;
+    a.dst_idx64 = p;  // scatter: new row perm[u] <- old row u
+    launch_move(ctx, a, rows, row_bytes);
+    o.finish();
+  });
+}
+
+// ------------------------------------------------------------- peer memory
+int tg_enable_peer_access(int device, int peer) {
+  return guard([&] {
+    DeviceGuard dg(device);
+    const cudaError_t e = cudaDeviceEnablePeerAccess(peer, 0);
+    if (e == cudaErrorPeerAccessAlreadyEnabled) {
+      cudaGetLastError();
+      return;
+    }
+    TGB_CUDA(e);
+  });
+}
+
+int tg_ipc_get_handle(const void* p, void* out) {
+  return guard([&] {
+    cudaIpcMemHandle_t h;
+    TGB_CUDA(cudaIpcGetMemHandle(&h, const_cast<void*>(p)));
+    static_assert(sizeof(h) == 64, "ipc handle size");
+    std::memcpy(out, &h, 64);
+  });
+}
+
+int tg_ipc_open_handle(tg_ctx* ctx, const void* handle, void** out) {
+  return guard([&] {
+    DeviceGuard dg(ctx->device);
+    cudaIpcMemHandle_t h;
+    std::memcpy(&h, handle, 64);
+    TGB_CUDA(cudaIpcOpenMemHandle(out, h, cudaIpcMemLazyEnablePeerAccess));
+  });
+}
+
+int tg_ipc_close_handle(void* p) {
+  return guard([&] { TGB_CUDA(cudaIpcCloseMemHandle(p)); });
+}
+
+int tg_host_register(void* p, uint64_t bytes) {
+  return guard([&] {
+    TGB_CUDA(cudaHostRegister(p, bytes, cudaHostRegisterMapped | cudaHostRegisterPortable));
+  });
+}
+int tg_host_unregister(void* p) {
+  return guard([&] { TGB_CUDA(cudaHostUnregister(p)); });
+}
+int tg_host_alloc(uint64_t bytes, void** out) {
+  return guard([&] {
+    TGB_CUDA(cudaHostAlloc(out, bytes, cudaHostAllocMapped | cudaHostAllocPortable));
+  });
+}
+int tg_host_free(void* p) {
+  return guard([&] { TGB_CUDA(cudaFreeHost(p)); });
+}
+
+}  // extern "C"

@@ -1,0 +1,75 @@
+"""Host-side producers of the hot path's inputs (not the hot path).
+
+Thin bindings of csrc/host_producers.cpp — the reference's counter-based
+train-id draw (scoring.cpp:22-31), transpose (csr_graph.cpp:67-80) and
+GraphSAGE minibatch expansion (sampling.cpp:56-90, scheduled per epoch like
+run_training_trace, sampling.cpp:106-123) — so the gather sees exactly the
+reference's sampled node-id lists.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from typing import List, Sequence
+
+import numpy as np
+
+from ._lib import LIB
+from .tiergraph import CsrGraph, DomainError, TierGraphError, TrainIdSet
+
+
+def _host_check(rc: int):
+    if rc != 0:
+        msg = LIB.tg_host_last_error().decode(errors="replace")
+        raise (DomainError if rc == 2 else TierGraphError)(msg)
+
+
+def _take(p: C.c_void_p, n: int) -> np.ndarray:
+    if n == 0:
+        LIB.tg_free(p)
+        return np.zeros(0, np.uint64)
+    a = np.ctypeslib.as_array(C.cast(p, C.POINTER(C.c_uint64)), shape=(n,)).copy()
+    LIB.tg_free(p)
+    return a
+
+
+def draw_random_train_ids(num_nodes: int, count: int, seed: int) -> TrainIdSet:
+    """scoring.hpp:24 (scoring.cpp:22-31)"""
+    out = np.empty(max(count, 1), np.uint64)
+    _host_check(LIB.tg_draw_random_train_ids(int(num_nodes), int(count), int(seed), out.ctypes.data))
+    return TrainIdSet(out[:count])
+
+
+def transpose(g: CsrGraph) -> CsrGraph:
+    """csr_graph.hpp:48 (csr_graph.cpp:67-80)"""
+    off = np.ascontiguousarray(np.asarray(g.offsets, np.uint64))
+    tgt = np.ascontiguousarray(np.asarray(g.targets, np.uint64))
+    n = len(off) - 1
+    t_off = np.empty(n + 1, np.uint64)
+    t_tgt = np.empty(max(len(tgt), 1), np.uint64)
+    _host_check(LIB.tg_transpose_host(off.ctypes.data, (tgt if len(tgt) else t_tgt).ctypes.data,
+                                      n, t_off.ctypes.data, t_tgt.ctypes.data))
+    return CsrGraph(t_off, t_tgt[:len(tgt)])
+
+
+def epoch_minibatches(gt: CsrGraph, tid, fanouts: Sequence[int], batch_size: int, seed: int,
+                      epoch: int, first_batch: int = 0, max_batches: int = 0,
+                      threads: int = 0) -> List[np.ndarray]:
+    """The sorted unique node-id list of each minibatch of one epoch, exactly
+    as run_training_trace builds them (shuffle key {0x5348, epoch}; batch b
+    expanded with BatchRng{seed, epoch, b}). `gt` is the TRANSPOSED graph."""
+    ids = np.ascontiguousarray(np.asarray(tid.ids if isinstance(tid, TrainIdSet) else tid,
+                                          np.uint64))
+    f = np.ascontiguousarray(np.asarray(list(fanouts), np.uint32))
+    off = np.ascontiguousarray(np.asarray(gt.offsets, np.uint64))
+    tgt = np.ascontiguousarray(np.asarray(gt.targets, np.uint64))
+    if len(tgt) == 0:
+        tgt = np.zeros(1, np.uint64)
+    po, nb, pi = C.c_void_p(), C.c_uint64(), C.c_void_p()
+    _host_check(LIB.tg_epoch_minibatches(off.ctypes.data, tgt.ctypes.data, len(off) - 1,
+                                         ids.ctypes.data, len(ids), f.ctypes.data, len(f),
+                                         int(batch_size), int(seed), int(epoch), int(first_batch),
+                                         int(max_batches), int(threads), C.byref(po), C.byref(nb),
+                                         C.byref(pi)))
+    o = _take(po, nb.value + 1)
+    allids = _take(pi, int(o[-1]) if len(o) else 0)
+    return [allids[o[b]:o[b + 1]] for b in range(nb.value)]

@@ -26,3 +26,17 @@ def ref():
     if r is None:
         pytest.skip("reference build oracle/_ref/libtgref.so not present")
     return r
+
+
+@pytest.fixture(scope="session")
+def tg():
+    from paper_2111_05894_b200 import tiergraph
+    return tiergraph
+
+
+@pytest.fixture(scope="session")
+def ctx(tg):
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+    return tg.default_context()

@@ -1,0 +1,217 @@
+"""GPU parity: tier accounting, trace replays and the byte-moving tiered
+gather (K7 placement + K8). Rows must be bit-exact: gathered row i ==
+reorder_features(f, perm).row(ids[i]) (reorder.cpp:97-117 composed with
+resolve tiering.cpp:48-65), and every TrafficReport must equal the
+reference's gather() (tiering.cpp:100-125) integer for integer.
+"""
+import numpy as np
+import pytest
+
+import oracle
+from tests.helpers import (RngStream, derive_stream_key, random_counter, random_graph,
+                           random_layout, random_permutation)
+
+pytestmark = pytest.mark.gpu
+
+LISTING = (16, 4, 10, 2, 8, 4)
+
+
+def checker():
+    return oracle.ref() or oracle.port()
+
+
+def test_account_known_answers(tg, ctx):  # test_tiering.cpp:124-153
+    lay = tg.TierLayout(*LISTING)
+    r = tg.TrafficReport()
+    tg.gather(lay, [0, 1, 3], 0, r)
+    assert r.host_bytes == 0 and r.local_accesses == 3 and r.local_bytes == 96
+    cold = tg.TierLayout(16, 0, 0, 2, 8, 4)
+    r = tg.TrafficReport()
+    tg.gather(cold, [0, 5, 11, 15], 1, r)
+    assert r.host_accesses == 4 and r.host_bytes == 128 and r.local_accesses + r.peer_accesses == 0
+    r = tg.TrafficReport()
+    tg.gather(lay, [2, 5, 11], 0, r)
+    assert (r.local_accesses, r.peer_accesses, r.host_accesses) == (1, 1, 1)
+    r = tg.TrafficReport()
+    tg.gather(lay, [5], 1, r)
+    assert r.local_accesses == 1
+
+
+def test_account_errors_keep_prefix(tg, ctx):
+    lay = tg.TierLayout(*LISTING)
+    ids = [1, 5, 11, 16, 2]
+    r = tg.TrafficReport(local_accesses=10)
+    with pytest.raises(tg.DomainError, match="row 16 out of range for 16 rows"):
+        tg.gather(lay, ids, 0, r)
+    want = oracle.port().gather(LISTING, ids[:3], 0, np.array([10, 0, 0, 0, 0, 0], np.uint64))
+    assert np.array_equal(r.as_array(), want)
+    with pytest.raises(tg.DomainError, match="requesting device 2"):
+        tg.gather(lay, [0], 2, tg.TrafficReport())
+    tg.gather(lay, [], 7, tg.TrafficReport())  # empty: the reference loop never resolves
+
+
+def test_account_random_layouts(tg, ctx):
+    chk = checker()
+    for i in range(40):
+        rng = RngStream(derive_stream_key(i, [0xACC7]))
+        n = 1 + rng.next_below(3000)
+        lay = random_layout(rng, n)
+        ids = np.random.default_rng(i).integers(0, n, 5000).astype(np.uint64)
+        for dev in range(lay[3]):
+            r = tg.TrafficReport()
+            tg.gather(tg.TierLayout(*lay), ids, dev, r)
+            assert np.array_equal(r.as_array(), chk.gather(lay, ids, dev))
+
+
+def test_simulate_and_sweep(tg, ctx):
+    chk = checker()
+    for i in range(30):  # acceptance.cpp:384-411
+        rng = RngStream(derive_stream_key(i, [0xB4]))
+        n = 1 + rng.next_below(2000)
+        lay = random_layout(rng, n)
+        counts = random_counter(n, i + 900, tag=0x636E, bound=25)
+        r = tg.simulate_trace(tg.make_access_counter(counts), tg.TierLayout(*lay))
+        assert np.array_equal(r.as_array(), chk.simulate_trace(counts, lay))
+        ordering = chk.score_ordering(counts.astype(np.float64))
+        assert np.array_equal(tg.counts_in_row_order(tg.make_access_counter(counts), ordering),
+                              chk.counts_in_row_order(counts, ordering))
+        fr = [0.0, 0.05, 0.1, 0.25, 0.5, 1.0]
+        rows = tg.hot_fraction_sweep(tg.make_access_counter(counts), ordering, fr, 0.1, lay[3], 8, 4)
+        lays, reps, rf = chk.hot_fraction_sweep(counts, ordering, fr, 0.1, lay[3], 8, 4)
+        for k, row in enumerate(rows):
+            assert row.layout.as_tuple() == tuple(int(x) for x in lays[k])
+            assert np.array_equal(row.report.as_array(), reps[k])
+            assert row.replicated_fraction == rf[k]
+    with pytest.raises(tg.DomainError):
+        tg.simulate_trace(tg.make_access_counter([0, 0]), tg.TierLayout(2, 0, 1, 1, 1, 4))
+    with pytest.raises(tg.DomainError):
+        tg.simulate_trace(tg.make_access_counter([1, 1, 1]), tg.TierLayout(2, 0, 1, 1, 1, 4))
+    c = tg.make_access_counter([9, 1, 4, 0, 2, 7, 3, 3, 1, 5])
+    o = tg.score_ordering(c.counts.astype(np.float64))
+    with pytest.raises(tg.DomainError):
+        tg.hot_fraction_sweep(c, o, [0.5, 0.1], 0.0, 2, 4, 4)
+    with pytest.raises(tg.DomainError, match="ordering"):
+        tg.counts_in_row_order(c, np.array([0, 1, 2, 3, 4, 5, 6, 7, 8, 99], np.uint64))
+
+
+def _virtual_devices(tg, ctx, features, perm, lay, **kw):
+    """D stores on ONE GPU wired to each other's HBM slices through the same
+    peer-pointer table real NVLink peers use (tg_store_set_peer)."""
+    D = lay.num_devices
+    stores = [tg.TieredFeatureStore(features, perm, lay, d, ctx=ctx, place=False, **kw)
+              for d in range(D)]
+    for d in range(1, D):
+        stores[d].share_cold(stores[0])
+    for s in stores:
+        s.place(features, perm)
+    for s in stores:
+        for d in range(D):
+            if d != s.device_index:
+                s.set_peer(d, stores[d].local_base)
+    return stores
+
+
+@pytest.mark.parametrize("dim,eb", [(100, 4), (128, 4), (768, 2), (9, 4), (3, 1), (1, 8), (2048, 4)])
+@pytest.mark.parametrize("cold_mode,pad", [("reordered", False), ("indirect", False),
+                                           ("reordered", True)])
+def test_store_gather_bit_exact(tg, ctx, dim, eb, cold_mode, pad):
+    chk, port = checker(), oracle.port()
+    n = 3000
+    rng = np.random.default_rng(dim * eb)
+    feat = rng.integers(0, 256, (n, dim * eb), dtype=np.uint8)
+    perm = random_permutation(n, dim)
+    reordered = port.reorder_features(feat, perm)
+    for D, hot, rep in ((1, 0.2, 0.0), (2, 0.3, 0.05), (3, 0.5, 0.1), (4, 1.0, 0.0),
+                        (6, 0.37, 0.2), (2, 0.0, 0.0)):
+        lay = tg.plan_layout(n, hot, rep, D, dim, eb)
+        stores = _virtual_devices(tg, ctx, feat, perm, lay, cold_mode=cold_mode, pad128=pad)
+        ids = np.sort(rng.choice(n, size=700, replace=False)).astype(np.uint64)
+        ids = np.concatenate([ids, rng.integers(0, n, 50).astype(np.uint64)])  # duplicates too
+        for d, s in enumerate(stores):
+            rep_ = tg.TrafficReport()
+            out = s.gather_rows(ids, report=rep_)
+            assert np.array_equal(out, reordered[ids])
+            assert np.array_equal(rep_.as_array(), chk.gather(lay.as_tuple(), ids, d))
+
+
+def test_store_errors_and_empty(tg, ctx):
+    n, dim = 100, 16
+    feat = np.arange(n * dim, dtype=np.float32).reshape(n, dim)
+    perm = random_permutation(n, 1)
+    lay = tg.plan_layout(n, 0.3, 0.1, 1, dim, 4)
+    s = tg.TieredFeatureStore(feat, perm, lay, ctx=ctx)
+    r = tg.TrafficReport()
+    assert s.gather_rows(np.zeros(0, np.uint64), report=r).shape == (0, 64)
+    with pytest.raises(tg.DomainError, match="row 100 out of range"):
+        s.gather_rows([3, 50, 100, 4], report=r)
+    assert np.array_equal(r.as_array(), oracle.port().gather(lay.as_tuple(), [3, 50], 0))
+    with pytest.raises(tg.DomainError):
+        tg.TieredFeatureStore(feat, np.zeros(n, np.uint64), lay, ctx=ctx)  # not a bijection
+    lay2 = tg.plan_layout(n, 0.5, 0.0, 2, dim, 4)
+    s2 = tg.TieredFeatureStore(feat, perm, lay2, 0, ctx=ctx)
+    with pytest.raises(tg.DomainError, match="peer slice of device 1"):
+        s2.gather_rows([60])
+    with pytest.raises(tg.DomainError):
+        tg.TieredFeatureStore(feat, perm, lay2, 2, ctx=ctx)
+
+
+def test_device_resident_inputs_and_async(tg, ctx):
+    import torch
+    n, dim = 5000, 100
+    from paper_2111_05894_b200 import synth
+    feat = synth.test_features(n, dim)
+    perm = random_permutation(n, 9)
+    lay = tg.plan_layout(n, 0.2, 0.0, 1, dim, 4)
+    dev = torch.device("cuda", ctx.device)
+    feat_d = torch.from_numpy(feat).to(dev)
+    s = tg.TieredFeatureStore(feat_d.view(torch.uint8).reshape(-1), perm, lay, ctx=ctx)
+    ids = torch.randint(0, n, (4096,), device=dev, dtype=torch.int64)
+    out = torch.empty((4096, dim * 4), dtype=torch.uint8, device=dev)
+    cnt = torch.zeros(3, dtype=torch.int64, device=dev)
+    err = torch.full((1,), -1, dtype=torch.int64, device=dev)
+    ctx.sync()
+    s.gather_rows_async(ids, out, cnt, err)
+    ctx.sync()
+    inv = oracle.port().invert(perm)
+    old = inv[ids.cpu().numpy().astype(np.uint64)]
+    want = synth.expected_rows(old, dim)
+    assert np.array_equal(out.cpu().numpy().view(np.float32), want)
+    rep = oracle.port().gather(lay.as_tuple(), ids.cpu().numpy().astype(np.uint64), 0)
+    assert cnt.cpu().tolist() == [int(rep[0]), int(rep[1]), int(rep[2])]
+    assert int(err.item()) == -1
+
+
+def test_end_to_end_reference_minibatches(tg, ctx):
+    """The whole path on a small R-MAT graph: wrpr -> permutation -> reorder
+    graph/features -> the reference's OWN sampled minibatch id lists ->
+    tiered gather; rows byte-equal and reports equal to the reference."""
+    chk = checker()
+    if chk.kind != "reference":
+        pytest.skip("needs the reference build for its minibatch lists")
+    from paper_2111_05894_b200 import producers, synth
+    n, dim = 50_000, 128
+    off, tgt = synth.rmat_graph(n, 800_000, seed=1)
+    tid = chk.draw_random_train_ids(n, n // 10, 3)
+    scores = tg.weighted_reverse_pagerank(tg.CsrGraph(off, tgt), tg.PagerankConfig(),
+                                          tg.TrainIdSet(tid))
+    assert scores.tobytes() == chk.weighted_reverse_pagerank(off, tgt, tid).tobytes()
+    perm = tg.permutation_from_scores(scores)
+    assert np.array_equal(perm.new_id_of, chk.permutation_from_scores(scores))
+    rg = tg.reorder_graph(tg.CsrGraph(off, tgt), perm)
+    ro, rt = chk.reorder_graph(off, tgt, perm.new_id_of)
+    assert np.array_equal(rg.offsets, ro) and np.array_equal(rg.targets, rt)
+    go, gt = chk.transpose(ro, rt)
+    new_tid = np.sort(perm.new_id_of[tid])
+    lists = chk.epoch_minibatches(go, gt, new_tid, [10, 15], 1024, 7, 0, max_batches=4)
+    mine = producers.epoch_minibatches(tg.CsrGraph(go, gt), new_tid, [10, 15], 1024, 7, 0,
+                                       max_batches=4)
+    assert all(np.array_equal(a, b) for a, b in zip(lists, mine))
+    feat = chk.make_test_features(n, dim)
+    reordered = chk.reorder_features(feat, perm.new_id_of)
+    lay = tg.plan_layout(n, 0.2, 0.0, 1, dim, 4)
+    store = tg.TieredFeatureStore(feat, perm, lay, ctx=ctx)
+    for ids in lists:
+        r = tg.TrafficReport()
+        out = store.gather_rows(ids, report=r)
+        assert np.array_equal(out.view(np.float32), reordered[ids])
+        assert np.array_equal(r.as_array(), chk.gather(lay.as_tuple(), ids, 0))

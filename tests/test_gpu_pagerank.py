@@ -1,0 +1,174 @@
+"""GPU parity: reverse PageRank (K1-K3) is bit-identical to the reference.
+
+Tolerance: none — scores are compared as raw IEEE-754 bytes (the hot set
+depends on exact fp64 ties). The checker is the reference build
+(oracle/_ref) when present, else the pinned C restatement (oracle/_build).
+"""
+import numpy as np
+import pytest
+
+import oracle
+from tests.helpers import RngStream, derive_stream_key, graph_from_pairs, random_graph
+
+pytestmark = pytest.mark.gpu
+
+
+def checker():
+    return oracle.ref() or oracle.port()
+
+
+def G(tg, off, tgt):
+    return tg.CsrGraph(off, tgt)
+
+
+def test_known_answers(tg, ctx):
+    port = oracle.port()
+    off, tgt = graph_from_pairs(port, 2, [(0, 1)])  # test_scoring.cpp:27-32
+    s = tg.reverse_pagerank(G(tg, off, tgt), tg.PagerankConfig(1, 0.85))
+    assert s[0] == pytest.approx(0.5, rel=1e-14) and s[1] == pytest.approx(0.075, rel=1e-14)
+    off, tgt = graph_from_pairs(port, 2, [(0, 1), (1, 0)])  # :34-41
+    for it in (1, 5, 17):
+        s = tg.reverse_pagerank(G(tg, off, tgt), tg.PagerankConfig(it, 0.85))
+        assert s[0] == s[1] and s[0] == pytest.approx(0.5, rel=1e-12)
+    off, tgt = graph_from_pairs(port, 4, [(2, 0)])  # :74-83 exact dyadic
+    s = tg.weighted_reverse_pagerank(G(tg, off, tgt), tg.PagerankConfig(1, 0.5),
+                                     tg.TrainIdSet.from_ids([0, 1], 4))
+    assert s[2] == 0.375 and s[3] == 0.125
+    off, tgt = graph_from_pairs(port, 2, [(0, 1)])  # :85-91
+    s = tg.weighted_reverse_pagerank(G(tg, off, tgt), tg.PagerankConfig(1, 0.85),
+                                     tg.TrainIdSet.from_ids([0], 2))
+    assert s[0] == pytest.approx(0.5, rel=1e-14) and s[1] == pytest.approx(0.075, rel=1e-14)
+
+
+def test_errors(tg, ctx):
+    port = oracle.port()
+    g = G(tg, *graph_from_pairs(port, 2, [(0, 1)]))
+    with pytest.raises(tg.DomainError):
+        tg.weighted_reverse_pagerank(g, tg.PagerankConfig(), tg.TrainIdSet(np.zeros(0, np.uint64)))
+    for it, d in [(0, 0.85), (1, 1.0), (1, 0.0)]:
+        with pytest.raises(tg.DomainError):
+            tg.reverse_pagerank(g, tg.PagerankConfig(it, d))
+    with pytest.raises(tg.DomainError, match="train id 7 out of range"):
+        tg.weighted_reverse_pagerank(g, tg.PagerankConfig(), tg.TrainIdSet(np.array([0, 7], np.uint64)))
+    with pytest.raises(tg.FormatError):
+        tg.reverse_pagerank(G(tg, np.array([0, 1, 1], np.uint64), np.array([5], np.uint64)))
+    # empty graph: config still validated, result empty
+    e = G(tg, np.zeros(1, np.uint64), np.zeros(0, np.uint64))
+    assert tg.reverse_pagerank(e).size == 0
+    with pytest.raises(tg.DomainError):
+        tg.reverse_pagerank(e, tg.PagerankConfig(0, 0.85))
+
+
+def test_isolated_and_edgeless(tg, ctx):
+    port = oracle.port()
+    off, tgt = graph_from_pairs(port, 10, [(0, 1), (2, 1), (3, 4)])
+    for s in (tg.reverse_pagerank(G(tg, off, tgt)),
+              tg.weighted_reverse_pagerank(G(tg, off, tgt), tg.PagerankConfig(),
+                                           tg.TrainIdSet.from_ids([0, 3], 10))):
+        assert np.all(np.isfinite(s)) and np.all(s >= 0)
+    off = np.zeros(8, np.uint64)
+    s = tg.reverse_pagerank(G(tg, off, np.zeros(0, np.uint64)))
+    assert s.tobytes() == checker().reverse_pagerank(off, np.zeros(0, np.uint64)).tobytes()
+
+
+def test_random_graphs_bit_exact(tg, ctx):
+    chk, port = checker(), oracle.port()
+    for i in range(40):  # acceptance.cpp:112-148 instance mix
+        n = 20 + (i * 37) % 481
+        off, tgt = random_graph(port, n, 0.5 + i % 8, i)
+        g = G(tg, off, tgt)
+        tid = port.draw_random_train_ids(n, max(1, n // 10), i)
+        for it in (1, 5, 20):
+            a = tg.reverse_pagerank(g, tg.PagerankConfig(it, 0.85))
+            assert a.tobytes() == chk.reverse_pagerank(off, tgt, it, 0.85).tobytes()
+            b = tg.weighted_reverse_pagerank(g, tg.PagerankConfig(it, 0.85), tg.TrainIdSet(tid))
+            assert b.tobytes() == chk.weighted_reverse_pagerank(off, tgt, tid, it, 0.85).tobytes()
+
+
+def test_all_labeled_equals_unweighted(tg, ctx):
+    port = oracle.port()
+    off, tgt = random_graph(port, 350, 3.0, 7)  # acceptance.cpp:154-162
+    g = G(tg, off, tgt)
+    a = tg.weighted_reverse_pagerank(g, tg.PagerankConfig(),
+                                     tg.TrainIdSet(np.arange(350, dtype=np.uint64)))
+    assert a.tobytes() == tg.reverse_pagerank(g).tobytes()
+
+
+def _hub_graph(n, hubs, seed):
+    """Random graph plus hub rows long enough to cross many windows and the
+    heavy-group threshold (row lengths 33..40000)."""
+    rng = np.random.default_rng(seed)
+    src = [rng.integers(0, n, 6 * n)]
+    dst = [rng.integers(0, n, 6 * n)]
+    for h, length in hubs:
+        src.append(np.full(length, h))
+        dst.append(rng.choice(n, size=length, replace=False))
+    src = np.concatenate(src).astype(np.uint64)
+    dst = np.concatenate(dst).astype(np.uint64)
+    return oracle.port().from_edge_list(n, src, dst)
+
+
+def test_long_rows_and_heavy_groups(tg, ctx):
+    chk = checker()
+    n = 60000
+    hubs = [(0, 40000), (1, 257), (31, 2049), (32, 5000), (95, 33), (1000, 20000), (59999, 3000)]
+    off, tgt = _hub_graph(n, hubs, 3)
+    g = G(tg, off, tgt)
+    tid = oracle.port().draw_random_train_ids(n, 600, 5)
+    for it in (1, 5):
+        a = tg.weighted_reverse_pagerank(g, tg.PagerankConfig(it, 0.85), tg.TrainIdSet(tid))
+        assert a.tobytes() == chk.weighted_reverse_pagerank(off, tgt, tid, it, 0.85).tobytes()
+
+
+def test_in_degrees_and_degree_score(tg, ctx):
+    port = oracle.port()
+    off, tgt = _hub_graph(20000, [(0, 15000), (7, 100)], 9)
+    g = G(tg, off, tgt)
+    assert np.array_equal(tg.in_degrees(g), port.in_degrees(off, tgt))
+    assert np.array_equal(tg.degree_score(g), port.degree_score(off))
+
+
+def test_row_partitioned_steps_equal_full_run(tg, ctx):
+    """The multi-GPU decomposition (row blocks + all-gather of `norm`) run as
+    several row ranges on one device reproduces the single run bit for bit."""
+    import torch
+    from paper_2111_05894_b200._lib import LIB
+    port = oracle.port()
+    n = 5000
+    off, tgt = _hub_graph(n, [(3, 3000), (64, 900)], 11)
+    g = G(tg, off, tgt)
+    tid = port.draw_random_train_ids(n, 400, 1)
+    want = tg.weighted_reverse_pagerank(g, tg.PagerankConfig(5, 0.85), tg.TrainIdSet(tid))
+    dev = torch.device("cuda", ctx.device)
+    tid_d = torch.as_tensor(tid.astype(np.int64), device=dev)
+    deg = torch.empty(n, dtype=torch.int32, device=dev)
+    na = torch.empty(n, dtype=torch.float64, device=dev)
+    nb = torch.empty_like(na)
+    score = torch.empty_like(na)
+    gh = g.device(ctx)
+    assert LIB.tg_pagerank_prepare_async(ctx.h, gh, tid_d.data_ptr(), len(tid),
+                                         deg.data_ptr(), na.data_ptr()) == 0
+    bounds = [0, 32 * 20, 32 * 61, 32 * 100, n]  # 4 "ranks", 32-row aligned
+    for it in range(5):
+        last = int(it == 4)
+        for r0, r1 in zip(bounds[:-1], bounds[1:]):
+            assert LIB.tg_pagerank_step_async(ctx.h, gh, deg.data_ptr(), 0.85, na.data_ptr(),
+                                              nb.data_ptr(), score.data_ptr(), r0, r1, last) == 0
+        na, nb = nb, na
+    ctx.sync()
+    assert score.cpu().numpy().tobytes() == want.tobytes()
+
+
+def test_rmat_c1_scale_bit_exact_and_hot_set(tg, ctx):
+    """C1 shape (R-MAT 1M nodes / 16M draws, 10 % train): bit-exact scores and
+    an identical hot set / permutation (the tie-break by id included)."""
+    from paper_2111_05894_b200 import synth
+    off, tgt = synth.rmat_graph(1_000_000, 16_000_000, seed=1)
+    port = oracle.port()
+    tid = port.draw_random_train_ids(1_000_000, 100_000, 3)
+    g = G(tg, off, tgt)
+    got = tg.weighted_reverse_pagerank(g, tg.PagerankConfig(), tg.TrainIdSet(tid))
+    want = port.weighted_reverse_pagerank(off, tgt, tid)
+    assert got.tobytes() == want.tobytes()
+    perm = tg.permutation_from_scores(got)
+    assert np.array_equal(perm.new_id_of, port.permutation_from_scores(want))
