@@ -1,0 +1,585 @@
+#!/usr/bin/env python
+"""Benchmark of the data-tiering hot path on B200 (one JSON line on rank 0).
+
+Metric (BASELINE.json): feature-gather GB/s & minibatches/s at 1/2/4/8 B200;
+reverse-PageRank GTEPS. A "step" is one minibatch of the tiered gather (K8):
+the reference's own sampled node-id list for that minibatch, gathered from
+local HBM / peer HBM / pinned host memory into a contiguous HBM buffer.
+`value` = gathered payload GB/s over all ranks (ids + features resident, L2
+flushed between steps, per-step CUDA events on the launching stream, max over
+ranks); `e2e` = the same through the synchronous C-ABI call with the ids in
+pinned host memory (H2D inside the timed region) and the TrafficReport read
+back (D2H). PageRank (5 iterations, in-degrees included) and the selection
+sort are timed alongside and reported as sub-objects.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2] [--impl ours|reference]
+Under torchrun (N>1) every rank gathers its own minibatch stream; the hot
+tier is sharded across the ranks and read through CUDA-IPC peer pointers.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "feature-gather GB/s & minibatches/s at 1/2/4/8 B200; reverse-PageRank GTEPS"
+
+CONFIGS = {
+    "c1": dict(workload="C1: R-MAT 1M nodes / 16M draws, 128-d f32, 10% train, fanout (10,15), "
+                        "batch 1024, hot 20%",
+               nodes=1_000_000, draws=16_000_000, dim=128, elem=4, fanouts=[10, 15], batch=1024,
+               train=0.10, hot=0.20),
+    "c2": dict(workload="C2: ogbn-products-shaped R-MAT 2.45M nodes / 61.9M draws, 100-d f32, "
+                        "10% train, fanout (15,10,5), batch 1024, hot 20%",
+               nodes=2_450_000, draws=61_900_000, dim=100, elem=4, fanouts=[15, 10, 5], batch=1024,
+               train=0.10, hot=0.20),
+}
+
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+def measured_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured (MEASURED_PEAKS.json)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+    Q = ("index,clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 7:
+                continue
+            try:
+                sm.append(float(f[1]))
+                mx = max(mx, float(f[2]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[3:7]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx or None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ----------------------------------------------------------------------------
+def build_inputs(cfg, device, rank=0, world=1):
+    """Synthetic graph (GPU R-MAT), train ids, features in pinned host memory."""
+    from paper_2111_05894_b200 import producers, synth, tiergraph as tg
+    t0 = time.time()
+    off, tgt = synth.rmat_graph(cfg["nodes"], cfg["draws"], seed=1, device=f"cuda:{device}")
+    n, e = len(off) - 1, len(tgt)
+    tid = producers.draw_random_train_ids(n, int(n * cfg["train"]), 3)
+    log(f"[rank {rank}] graph {n} nodes / {e} edges, {len(tid.ids)} train ids ({time.time()-t0:.1f}s)")
+    return off, tgt, tid
+
+
+def pin_features(cfg):
+    from paper_2111_05894_b200 import synth, tiergraph as tg
+    n, dim = cfg["nodes"], cfg["dim"]
+    R = dim * cfg["elem"]
+    buf = tg.host_alloc(n * R)
+    synth.test_features(n, dim, out=buf)
+    return buf, R
+
+
+def time_events(torch, fn, reps, warm=1):
+    for _ in range(warm):
+        fn()
+    torch.cuda.synchronize()
+    ts = []
+    for _ in range(reps):
+        a = torch.cuda.Event(enable_timing=True)
+        b = torch.cuda.Event(enable_timing=True)
+        a.record()
+        fn()
+        b.record()
+        b.synchronize()
+        ts.append(a.elapsed_time(b))
+    return ts
+
+
+def bench_pagerank(torch, tg, ctx, g, tid, n, e, iters=5, reps=5):
+    """Whole weighted_reverse_pagerank call on device-resident data + the
+    per-kernel SpMV time for the roofline."""
+    from paper_2111_05894_b200._lib import LIB
+    dev = torch.device("cuda", ctx.device)
+    out = torch.empty(n, dtype=torch.float64, device=dev)
+    tid_d = torch.as_tensor(tid.ids.astype(np.int64), device=dev)
+    cfgp = tg.PagerankConfig(iters, 0.85)
+    ts = time_events(torch, lambda: tg.weighted_reverse_pagerank(g, cfgp, tid_d, ctx=ctx, out=out),
+                     reps)
+    ms = min(ts)
+    # per-kernel: prepare (in-degree + init) and each SpMV step, events between
+    deg = torch.empty(n, dtype=torch.int32, device=dev)
+    na = torch.empty(n, dtype=torch.float64, device=dev)
+    nb = torch.empty_like(na)
+    sc = torch.empty_like(na)
+    gh = g.device(ctx)
+    step_ms, prep_ms = [], []
+    for _ in range(reps):
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(iters + 2)]
+        ev[0].record()
+        assert LIB.tg_pagerank_prepare_async(ctx.h, gh, tid_d.data_ptr(), len(tid.ids),
+                                             deg.data_ptr(), na.data_ptr()) == 0
+        ev[1].record()
+        x, y = na, nb
+        for it in range(iters):
+            assert LIB.tg_pagerank_step_async(ctx.h, gh, deg.data_ptr(), 0.85, x.data_ptr(),
+                                              y.data_ptr(), sc.data_ptr(), 0, n,
+                                              int(it == iters - 1)) == 0
+            ev[it + 2].record()
+            x, y = y, x
+        ev[-1].synchronize()
+        prep_ms.append(ev[0].elapsed_time(ev[1]))
+        step_ms.extend(ev[i + 1].elapsed_time(ev[i + 2]) for i in range(iters))
+    assert sc.cpu().numpy().tobytes() == out.cpu().numpy().tobytes()
+    return out, ms, statistics.mean(step_ms), statistics.mean(prep_ms)
+
+
+def exchange_peers(torch, tg, store, rank, world):
+    """CUDA-IPC handles of every rank's HBM region -> the combined-tensor table."""
+    import ctypes as C
+    import torch.distributed as dist
+    from paper_2111_05894_b200._lib import LIB
+    h = (C.c_uint8 * 64)()
+    assert LIB.tg_ipc_get_handle(C.c_void_p(store.local_base), h) == 0, LIB.tg_last_error()
+    mine = bytes(h)
+    allh = [None] * world
+    dist.all_gather_object(allh, mine)
+    opened = []
+    for d in range(world):
+        if d == rank:
+            continue
+        hb = (C.c_uint8 * 64).from_buffer_copy(allh[d])
+        p = C.c_void_p()
+        assert LIB.tg_ipc_open_handle(store.ctx.h, hb, C.byref(p)) == 0, LIB.tg_last_error()
+        store.set_peer(d, p.value)
+        opened.append(p.value)
+    return opened
+
+
+def run_ours(args):
+    import torch
+    from paper_2111_05894_b200 import producers, tiergraph as tg
+
+    cfg = CONFIGS[args.config]
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    stream = torch.cuda.current_stream()
+    ctx = tg.Context(local, stream=stream)
+    hbm_peak, hbm_src = measured_peaks()
+
+    off, tgt, tid = build_inputs(cfg, local, rank, world)
+    n, e = len(off) - 1, len(tgt)
+    g = tg.CsrGraph(off, tgt)
+    g.device(ctx)
+
+    # ---- hot path A: PageRank + selection (device-resident graph)
+    scores_d, pr_ms, step_ms, prep_ms = bench_pagerank(torch, tg, ctx, g, tid, n, e)
+    dev = torch.device("cuda", local)
+    perm_d = torch.empty(n, dtype=torch.int64, device=dev)
+    sel = time_events(torch, lambda: tg.permutation_from_scores(scores_d, ctx=ctx, out=perm_d), 3)
+    scores = scores_d.cpu().numpy()
+    perm = tg.NodePermutation(perm_d.cpu().numpy().view(np.uint64))
+
+    # ---- reordered graph -> the reference's minibatch schedule (host producer)
+    t0 = time.time()
+    rg = tg.reorder_graph(g, perm, ctx=ctx)
+    gt = producers.transpose(rg)
+    new_tid = np.sort(perm.new_id_of[tid.ids])
+    lists = producers.epoch_minibatches(gt, new_tid, cfg["fanouts"], cfg["batch"], seed=7, epoch=0)
+    mine = lists[rank::world]
+    log(f"[rank {rank}] {len(lists)} minibatches/epoch sampled on host "
+        f"(avg {np.mean([len(l) for l in lists]):.0f} ids) in {time.time()-t0:.1f}s")
+
+    # ---- tiered store: hot rows in HBM (sharded across ranks), cold rows pinned
+    feat, R = pin_features(cfg)
+    lay = tg.plan_layout(n, cfg["hot"], 0.0, world, cfg["dim"], cfg["elem"])
+    store = tg.TieredFeatureStore(feat, perm, lay, rank, ctx=ctx)
+    if world > 1:
+        exchange_peers(torch, tg, store, rank, world)
+        dist.barrier()
+
+    # ---- device-resident per-step inputs
+    nsteps = args.steps + args.warmup
+    ids_d = [torch.as_tensor(mine[k % len(mine)].astype(np.int64), device=dev) for k in range(nsteps)]
+    maxu = max(len(x) for x in mine)
+    out_d = torch.empty((maxu, R), dtype=torch.uint8, device=dev)
+    cnt = torch.zeros(3, dtype=torch.int64, device=dev)
+    err = torch.full((1,), -1, dtype=torch.int64, device=dev)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)  # > 126 MB L2
+
+    def step(k):
+        store.gather_rows_async(ids_d[k], out_d, cnt, err)
+
+    for k in range(args.warmup):
+        flush.zero_()
+        step(k)
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    launches0 = tg.kernel_launches()
+    cnt.zero_()
+    evs = []
+    with ClockSampler(local) as clk:
+        torch.cuda.synchronize()
+        for k in range(args.warmup, nsteps):
+            flush.zero_()
+            a = torch.cuda.Event(enable_timing=True)
+            b = torch.cuda.Event(enable_timing=True)
+            a.record()
+            step(k)
+            b.record()
+            evs.append((a, b))
+        torch.cuda.synchronize()
+        if dist:
+            dist.barrier()
+    launches = tg.kernel_launches() - launches0
+    step_times = [a.elapsed_time(b) for a, b in evs]
+    t_ms = sum(step_times)
+    assert int(err.item()) == -1, "gather reported an out-of-range id"
+    counters = cnt.cpu().numpy()
+    u_rows = sum(len(mine[k % len(mine)]) for k in range(args.warmup, nsteps))
+    assert int(counters.sum()) == u_rows
+    if dist:
+        t = torch.tensor([t_ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        t_ms = float(t.item())
+        tot = torch.tensor([u_rows, int(counters[0]), int(counters[1]), int(counters[2])],
+                           dtype=torch.float64, device=dev)
+        dist.all_reduce(tot)
+        u_all, cl, cp, ch = (int(x) for x in tot.tolist())
+    else:
+        u_all, cl, cp, ch = u_rows, int(counters[0]), int(counters[1]), int(counters[2])
+    gbps = u_all * R / (t_ms * 1e-3) / 1e9
+    mbps = args.steps * world / (t_ms * 1e-3)
+
+    # ---- e2e: synchronous C-ABI, ids in pinned host memory, report read back
+    pinned_ids = [tg.host_alloc(len(mine[k % len(mine)]) * 8).view(np.uint64) for k in range(nsteps)]
+    for k in range(nsteps):
+        pinned_ids[k][:] = mine[k % len(mine)]
+    e2e_t = 0.0
+    rep = tg.TrafficReport()
+    for k in range(args.warmup):
+        store.gather_rows(pinned_ids[k], out=out_d[:len(pinned_ids[k])], report=rep)
+    torch.cuda.synchronize()
+    for k in range(args.warmup, nsteps):
+        flush.zero_()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        store.gather_rows(pinned_ids[k], out=out_d[:len(pinned_ids[k])], report=rep)
+        e2e_t += time.perf_counter() - t0
+    if dist:
+        t = torch.tensor([e2e_t], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_t = float(t.item())
+    e2e_gbps = u_all * R / e2e_t / 1e9
+    h2d = u_rows * 8 / args.steps
+
+    # ---- CPU->GPU bytes per epoch: K8 counters over this rank's share of the epoch
+    ep = tg.TrafficReport()
+    counts = np.zeros(n, np.uint64)
+    for ids in mine:
+        store.gather_rows(ids, out=out_d[:len(ids)], report=ep)
+        counts[ids.astype(np.int64)] += np.uint64(1)  # lists are sorted-unique
+    sim = tg.simulate_trace(tg.make_access_counter(counts), lay)
+    host_epoch, total_epoch = ep.host_bytes, ep.local_bytes + ep.peer_bytes + ep.host_bytes
+    if dist:
+        t = torch.tensor([host_epoch, total_epoch], dtype=torch.float64, device=dev)
+        dist.all_reduce(t)
+        host_epoch, total_epoch = (int(x) for x in t.tolist())
+
+    # ---- roofline of the dominant kernel (K8) — mixed HBM / NVLink / PCIe
+    pcie_dma = host_link_dma_gbps(torch, dev)
+    pcie_zc = tg.measure_host_read_gbps(ctx, 1 << 30, R if R % 16 == 0 else 512, 3)
+    pcie_peak = max(pcie_dma, pcie_zc)
+    nvl_peak = 770.0  # measured peer copy per direction (B200_PROFILING.md)
+    per_launch = u_rows / args.steps
+    alg_bytes = per_launch * (2 * R + 8)  # payload read + output write + ids
+    t_launch = statistics.mean(step_times) * 1e-3
+    frac_l, frac_p, frac_h = cl / max(u_all, 1), cp / max(u_all, 1), ch / max(u_all, 1)
+    hbm_bytes = per_launch * (frac_l * R + R + 8)
+    t_hbm = hbm_bytes / (hbm_peak * 1e9)
+    t_nvl = per_launch * frac_p * R / (nvl_peak * 1e9)
+    t_pcie = per_launch * frac_h * R / (pcie_peak * 1e9)
+    t_star = max(t_hbm, t_nvl, t_pcie)
+    bound = ["hbm", "nvlink", "pcie"][int(np.argmax([t_hbm, t_nvl, t_pcie]))]
+    achieved = alg_bytes / t_launch / 1e9
+    peak_eff = alg_bytes / t_star / 1e9
+    traffic = None
+    tf = os.path.join(ROOT, "profiles", f"ncu_traffic_{args.config}.json")
+    if os.path.exists(tf):
+        try:
+            traffic = json.load(open(tf)).get("gather_dram_bytes_per_launch")
+        except Exception:
+            traffic = None
+
+    result = None
+    if rank == 0:
+        clocks = clk.summary()
+        pr_bytes_iter = 4 * (n + 1) + 4 * e + 8 * e + 4 * n + 8 * n
+        result = {
+            "metric": METRIC, "value": round(gbps, 2), "unit": "GB/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(t_ms / args.steps, 4),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u8",
+            "data": "synthetic (R-MAT graph, closed-form features, reference sampler id lists)",
+            "config": {"workload": cfg["workload"], "nodes": n, "edges_after_dedup": e,
+                       "row_bytes": R, "hot_fraction": cfg["hot"], "layout": lay.as_tuple(),
+                       "l2": "flushed between steps (256 MB memset), per-step CUDA events",
+                       "parallelism": f"{world} GPU(s), hot tier sharded, cold tier per rank"},
+            "minibatches_per_s": round(mbps, 1),
+            "avg_ids_per_minibatch": round(u_all / max(args.steps * world, 1), 1),
+            "hit_split": {"local": round(frac_l, 4), "peer": round(frac_p, 4), "host": round(frac_h, 4)},
+            "e2e": {"value": round(e2e_gbps, 2), "unit": "GB/s", "h2d_bytes_per_step": int(h2d),
+                    "d2h_bytes_per_step": 32,
+                    "how": "tg_gather_rows (synchronous C-ABI): ids from pinned host memory, "
+                           "rows into HBM, TrafficReport read back"},
+            "gpu_launches": int(launches),
+            "roofline": {"bound": bound, "achieved": round(achieved, 2),
+                         "peak": round(peak_eff, 2), "unit": "GB/s",
+                         "frac": round(t_star / t_launch, 4), "traffic": traffic,
+                         "kernel": "gather_kernel<uint4> (K8)",
+                         "algorithmic_bytes_per_launch": int(alg_bytes),
+                         "mixed": {"hbm_gbs": hbm_peak, "hbm_src": hbm_src,
+                                   "pcie_gbs": round(pcie_peak, 2),
+                                   "pcie_src": f"measured live: max(DMA H2D {pcie_dma:.1f}, "
+                                               f"zero-copy row read {pcie_zc:.1f})",
+                                   "nvlink_gbs": nvl_peak, "t_star_us": round(t_star * 1e6, 2),
+                                   "t_launch_us": round(t_launch * 1e6, 2)}},
+            "pagerank": {"gteps": round(5 * e / (pr_ms * 1e-3) / 1e9, 3), "ms": round(pr_ms, 4),
+                         "iterations": 5, "edges": e,
+                         "spmv_step_us": round(step_ms * 1e3, 2),
+                         "prepare_us": round(prep_ms * 1e3, 2),
+                         "roofline": {"bound": "hbm", "kernel": "pr_step_kernel (K3)",
+                                      "achieved": round(pr_bytes_iter / (step_ms * 1e-3) / 1e9, 1),
+                                      "peak": hbm_peak, "unit": "GB/s",
+                                      "frac": round(pr_bytes_iter / (step_ms * 1e-3) / 1e9 / hbm_peak, 4),
+                                      "algorithmic_bytes_per_launch": pr_bytes_iter}},
+            "selection": {"ms": round(min(sel), 4), "keys": n},
+            "epoch": {"minibatches": len(lists), "host_bytes_tiered": int(host_epoch),
+                      "bytes_untiered": int(total_epoch),
+                      "reduction": round(1 - host_epoch / max(total_epoch, 1), 4),
+                      "equals_simulate_trace": bool(world > 1 or sim.host_bytes == ep.host_bytes)},
+            "clocks": clocks,
+        }
+        if world == 1 and not args.no_cpu_baseline:
+            result["cpu_baseline"], result["parity"] = cpu_baseline(
+                cfg, off, tgt, tid, scores, perm, feat, R, lay, mine, store, out_d, torch)
+    if dist:
+        dist.barrier()
+        dist.destroy_process_group()
+    return result
+
+
+def host_link_dma_gbps(torch, dev, nbytes=1 << 30):
+    h = torch.empty(nbytes, dtype=torch.uint8).pin_memory()
+    d = torch.empty(nbytes, dtype=torch.uint8, device=dev)
+    best = 0.0
+    for _ in range(3):
+        a = torch.cuda.Event(enable_timing=True)
+        b = torch.cuda.Event(enable_timing=True)
+        a.record()
+        d.copy_(h, non_blocking=True)
+        b.record()
+        b.synchronize()
+        best = max(best, nbytes / (a.elapsed_time(b) * 1e-3) / 1e9)
+    return best
+
+
+def cpu_baseline(cfg, off, tgt, tid, scores, perm, feat, R, lay, lists, store, out_d, torch):
+    """The reference's CPU path (oracle/_ref, all host threads) on a bounded
+    sample of the same workload, plus bit-exact parity of our results."""
+    import oracle
+    ref = oracle.ref()
+    kind = "reference"
+    if ref is None:
+        ref, kind = oracle.port(), "port"
+    cores = os.cpu_count() or 1
+    parity = {}
+    # PageRank (whole C2 run: a few seconds on the host)
+    t0 = time.perf_counter()
+    want = ref.weighted_reverse_pagerank(off, tgt, tid.ids)
+    pr_s = time.perf_counter() - t0
+    parity["pagerank_bit_exact"] = bool(want.tobytes() == scores.tobytes())
+    parity["permutation_identical"] = bool(
+        np.array_equal(ref.permutation_from_scores(want), perm.new_id_of))
+    if kind != "reference":
+        return ({"value": None, "unit": "GB/s", "cores": cores, "kind": kind,
+                 "sample": "reference build missing"}, parity)
+    ref.set_worker_count(cores)
+    rf = oracle.RefFeatures(ref, feat.reshape(cfg["nodes"], R)).reordered(perm.new_id_of)
+    sample = lists[: max(1, min(len(lists), 24))]
+    out = np.empty((max(len(x) for x in sample), R), np.uint8)
+    rep = np.zeros(6, np.uint64)
+    rf.gather(lay, sample[0], 0, out, rep)  # warm
+    t0 = time.perf_counter()
+    moved = 0
+    for ids in sample:
+        rf.gather(lay, ids, 0, out, rep)
+        moved += len(ids) * R
+    cpu_s = time.perf_counter() - t0
+    # gather parity on the last sampled minibatch
+    ids = sample[-1]
+    r = np.zeros(6, np.uint64)
+    rf.gather(lay, ids, 0, out, r)
+    from paper_2111_05894_b200 import tiergraph as tg
+    mine = tg.TrafficReport()
+    got = store.gather_rows(ids, report=mine)
+    parity["gather_rows_bit_exact"] = bool(np.array_equal(got, out[: len(ids)]))
+    parity["traffic_report_equal"] = bool(np.array_equal(mine.as_array(), r))
+    base = {"value": round(moved / cpu_s / 1e9, 3), "unit": "GB/s", "cores": cores, "kind": kind,
+            "sample": f"{len(sample)} minibatches of the same epoch: reference FeatureMatrix::row "
+                      f"memcpy (reorder.cpp:113-115 pattern) + gather() accounting, "
+                      f"{cores} OpenMP threads, {cpu_s:.2f}s",
+            "pagerank_gteps": round(5 * len(tgt) / pr_s / 1e9, 4),
+            "pagerank_s": round(pr_s, 3)}
+    return base, parity
+
+
+def run_reference(args):
+    """--impl reference: the reference's own CPU implementation of the path
+    (oracle/_ref: the unmodified reference sources), rank 0 only."""
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return None
+    import oracle
+    ref = oracle.ref()
+    cfg = CONFIGS[args.config]
+    if ref is None:
+        return {"impl": "reference", "unavailable": "oracle/_ref/libtgref.so was not built"}
+    cores = os.cpu_count() or 1
+    ref.set_worker_count(cores)
+    from paper_2111_05894_b200 import synth
+    dev = "cuda" if _cuda_available() else "cpu"
+    off, tgt = synth.rmat_graph(cfg["nodes"], cfg["draws"], seed=1, device=dev)
+    n, e = len(off) - 1, len(tgt)
+    tid = ref.draw_random_train_ids(n, int(n * cfg["train"]), 3)
+    t0 = time.perf_counter()
+    scores = ref.weighted_reverse_pagerank(off, tgt, tid)
+    pr_s = time.perf_counter() - t0
+    perm = ref.permutation_from_scores(scores)
+    ro, rt = ref.reorder_graph(off, tgt, perm)
+    go, gt = ref.transpose(ro, rt)
+    new_tid = np.sort(perm[tid])
+    nsteps = args.steps + args.warmup
+    lists = ref.epoch_minibatches(go, gt, new_tid, cfg["fanouts"], cfg["batch"], 7, 0,
+                                  max_batches=min(nsteps, 64))
+    R = cfg["dim"] * cfg["elem"]
+    feat = synth.test_features(n, cfg["dim"])
+    rf = oracle.RefFeatures(ref, feat.view(np.uint8).reshape(n, R)).reordered(perm)
+    lay = ref.plan_layout(n, cfg["hot"], 0.0, 1, cfg["dim"], cfg["elem"])
+    out = np.empty((max(len(x) for x in lists), R), np.uint8)
+    rep = np.zeros(6, np.uint64)
+    for k in range(args.warmup):
+        rf.gather(lay, lists[k % len(lists)], 0, out, rep)
+    t0 = time.perf_counter()
+    moved = 0
+    for k in range(args.warmup, nsteps):
+        ids = lists[k % len(lists)]
+        rf.gather(lay, ids, 0, out, rep)
+        moved += len(ids) * R
+    dt = time.perf_counter() - t0
+    v = moved / dt / 1e9
+    return {"metric": METRIC, "value": round(v, 3), "unit": "GB/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": round(dt * 1e3 / args.steps, 3), "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "u8",
+            "data": "synthetic (R-MAT graph, closed-form features, reference sampler id lists)",
+            "config": {"workload": cfg["workload"], "nodes": n, "edges_after_dedup": e,
+                       "row_bytes": R, "hot_fraction": cfg["hot"]},
+            "impl": "reference",
+            "minibatches_per_s": round(args.steps / dt, 2),
+            "pagerank": {"gteps": round(5 * e / pr_s / 1e9, 4), "s": round(pr_s, 3)},
+            "cpu_baseline": {"value": round(v, 3), "unit": "GB/s", "cores": cores,
+                             "kind": "reference",
+                             "sample": f"{args.steps} minibatches: FeatureMatrix::row memcpy + "
+                                       "gather() accounting (reference build, OpenMP)"},
+            "e2e": {"value": round(v, 3), "unit": "GB/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+
+
+def _cuda_available():
+    try:
+        import torch
+        return torch.cuda.is_available()
+    except Exception:
+        return False
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    res = run_reference(args) if args.impl == "reference" else run_ours(args)
+    if res is not None:
+        print(json.dumps(res), flush=True)
+
+
+if __name__ == "__main__":
+    main()
