@@ -74,7 +74,7 @@ class ClockSampler:
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.Q}",
-                 "--format=csv,noheader,nounits", "-lms", "100"],
+                 "--format=csv,noheader,nounits", "-lms", "20"],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
@@ -223,7 +223,8 @@ def run_ours(args):
     if world > 1:
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    stream = torch.cuda.current_stream()
+    stream = torch.cuda.Stream(device=local)  # one non-default stream for torch and tiergraph
+    torch.cuda.set_stream(stream)
     ctx = tg.Context(local, stream=stream)
     hbm_peak, hbm_src = measured_peaks()
 
@@ -270,6 +271,7 @@ def run_ours(args):
     def step(k):
         store.gather_rows_async(ids_d[k], out_d, cnt, err)
 
+    clk = ClockSampler(local).__enter__()  # samples warm-up + timed region
     for k in range(args.warmup):
         flush.zero_()
         step(k)
@@ -279,7 +281,7 @@ def run_ours(args):
     launches0 = tg.kernel_launches()
     cnt.zero_()
     evs = []
-    with ClockSampler(local) as clk:
+    if True:
         torch.cuda.synchronize()
         for k in range(args.warmup, nsteps):
             flush.zero_()
@@ -292,6 +294,7 @@ def run_ours(args):
         torch.cuda.synchronize()
         if dist:
             dist.barrier()
+    clk.__exit__(None, None, None)
     launches = tg.kernel_launches() - launches0
     step_times = [a.elapsed_time(b) for a, b in evs]
     t_ms = sum(step_times)
@@ -471,10 +474,12 @@ def cpu_baseline(cfg, off, tgt, tid, scores, perm, feat, R, lay, lists, store, o
     rep = np.zeros(6, np.uint64)
     rf.gather(lay, sample[0], 0, out, rep)  # warm
     t0 = time.perf_counter()
-    moved = 0
-    for ids in sample:
-        rf.gather(lay, ids, 0, out, rep)
-        moved += len(ids) * R
+    moved, passes = 0, 0
+    while time.perf_counter() - t0 < 3.0:  # a bounded ~3 s sample of CPU work
+        for ids in sample:
+            rf.gather(lay, ids, 0, out, rep)
+            moved += len(ids) * R
+        passes += 1
     cpu_s = time.perf_counter() - t0
     # gather parity on the last sampled minibatch
     ids = sample[-1]
@@ -486,7 +491,7 @@ def cpu_baseline(cfg, off, tgt, tid, scores, perm, feat, R, lay, lists, store, o
     parity["gather_rows_bit_exact"] = bool(np.array_equal(got, out[: len(ids)]))
     parity["traffic_report_equal"] = bool(np.array_equal(mine.as_array(), r))
     base = {"value": round(moved / cpu_s / 1e9, 3), "unit": "GB/s", "cores": cores, "kind": kind,
-            "sample": f"{len(sample)} minibatches of the same epoch: reference FeatureMatrix::row "
+            "sample": f"{passes} x {len(sample)} minibatches of the same epoch: reference FeatureMatrix::row "
                       f"memcpy (reorder.cpp:113-115 pattern) + gather() accounting, "
                       f"{cores} OpenMP threads, {cpu_s:.2f}s",
             "pagerank_gteps": round(5 * len(tgt) / pr_s / 1e9, 4),
@@ -568,8 +573,8 @@ def _cuda_available():
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
-    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")

@@ -159,7 +159,7 @@ int tg_device_count(void) {
   return n;
 }
 
-static int ctx_create(int device, void* stream, tg_ctx** out) {
+static int ctx_create(int device, void* stream, bool given, tg_ctx** out) {
   return guard([&] {
     int count = 0;
     TGB_CUDA(cudaGetDeviceCount(&count));
@@ -177,7 +177,7 @@ static int ctx_create(int device, void* stream, tg_ctx** out) {
     auto* c = new tg_ctx;
     c->device = device;
     TGB_CUDA(cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, device));
-    if (stream) {
+    if (given) {  // 0 = the legacy default stream, used as is
       c->stream = static_cast<cudaStream_t>(stream);
     } else {
       TGB_CUDA(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
@@ -187,9 +187,9 @@ static int ctx_create(int device, void* stream, tg_ctx** out) {
   });
 }
 
-int tg_ctx_create(int device, tg_ctx** out) { return ctx_create(device, nullptr, out); }
+int tg_ctx_create(int device, tg_ctx** out) { return ctx_create(device, nullptr, false, out); }
 int tg_ctx_create_on_stream(int device, void* stream, tg_ctx** out) {
-  return ctx_create(device, stream, out);
+  return ctx_create(device, stream, true, out);
 }
 
 int tg_ctx_destroy(tg_ctx* c) {

@@ -22,6 +22,7 @@
 
 #include <algorithm>
 #include <string>
+#include <vector>
 
 #include "internal.cuh"
 
@@ -30,18 +31,19 @@ struct tg_graph {
   uint64_t n = 0, e = 0;
   uint32_t* off = nullptr;     // n+1, u32
   uint32_t* tgt = nullptr;     // e, u32
-  uint32_t n_groups = 0;       // ceil(n/32)
-  uint8_t* heavy_flag = nullptr;
-  uint32_t* heavy = nullptr;   // group ids with a long row
-  uint32_t n_heavy = 0;
+  uint32_t* hub = nullptr;     // rows longer than kHubLen, longest first
+  uint32_t n_hub = 0;
+  uint32_t max_row = 0;
 };
 
 namespace tgb {
 
 constexpr int kGroupRows = 32;
-constexpr uint32_t kHeavyRowLen = 2048;  // rows longer than this start first
-constexpr int kPrWin = 256;              // edges staged per warp per window
-constexpr int kPrWarps = 8;              // warps per CTA
+constexpr uint32_t kHubLen = 2048;  // longer rows: one CTA each, warp-specialised
+constexpr int kPrWin = 256;         // edges staged per warp per window (light path)
+constexpr int kPrWarps = 8;         // warps per CTA
+constexpr int kHubSlot = 512;       // doubles per ring slot (hub path)
+constexpr int kHubSlots = 8;        // ring depth
 
 // ------------------------------------------------------------ graph upload
 __global__ void narrow_offsets_kernel(const uint64_t* __restrict__ in, uint32_t* __restrict__ out,
@@ -69,18 +71,14 @@ __global__ void narrow_targets_kernel(const uint64_t* __restrict__ in, uint32_t*
   }
 }
 
-// Per 32-row group: flag it heavy when it holds a row longer than kHeavyRowLen.
-__global__ void group_schedule_kernel(const uint32_t* __restrict__ off, uint64_t n,
-                                      uint32_t n_groups, uint8_t* __restrict__ flag,
-                                      uint32_t* __restrict__ heavy, uint32_t* __restrict__ n_heavy) {
-  const uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
-  const uint32_t g = static_cast<uint32_t>(i / kGroupRows);
-  uint32_t len = 0;
-  if (i < n) len = off[i + 1] - off[i];
-  const bool h = __any_sync(0xffffffffu, len > kHeavyRowLen);
-  if ((threadIdx.x & 31) == 0 && g < n_groups) {
-    flag[g] = h ? 1 : 0;
-    if (h) heavy[atomicAdd(n_heavy, 1u)] = g;
+// Rows longer than kHubLen get a whole CTA each (hub path of K3).
+__global__ void hub_rows_kernel(const uint32_t* __restrict__ off, uint64_t n,
+                                uint32_t* __restrict__ hub, uint32_t* __restrict__ cnt) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t len = off[i + 1] - off[i];
+    if (len > kHubLen) hub[atomicAdd(cnt, 1u)] = static_cast<uint32_t>(i);
+    if (len) atomicMax(cnt + 1, len);
   }
 }
 
@@ -168,71 +166,199 @@ struct PrStepArgs {
   const double* norm_in;
   double* norm_out;
   double* score_out;
-  const uint8_t* heavy_flag;
-  const uint32_t* heavy;
-  uint32_t n_heavy;
-  uint32_t group_begin, group_end;  // groups overlapping [row_begin,row_end)
+  const uint32_t* hub;
+  uint32_t n_hub;
+  uint32_t group_begin, group_end;  // 32-row groups overlapping [row_begin,row_end)
   uint64_t row_begin, row_end;
   double base, damp;
   int last;
 };
 
-__global__ void __launch_bounds__(kPrWarps * 32) pr_step_kernel(const PrStepArgs a) {
-  __shared__ double sbuf[kPrWarps][kPrWin];
-  const int lane = threadIdx.x & 31;
-  const int wib = threadIdx.x >> 5;
-  const uint64_t gw = (uint64_t)blockIdx.x * kPrWarps + wib;
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("{\n\t.reg .b64 st;\n\tmbarrier.arrive.shared::cta.b64 st, [%0];\n\t}" ::"r"(
+                   smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tWAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
 
-  // Heavy groups first (in-range ones), then every light group in order.
-  uint32_t group;
-  if (gw < a.n_heavy) {
-    group = a.heavy[gw];
-    if (group < a.group_begin || group >= a.group_end) return;
+__device__ __forceinline__ void finish_row(const PrStepArgs& a, uint64_t r, double acc) {
+  const double nx = __dadd_rn(a.base, __dmul_rn(a.damp, acc));  // scoring.cpp:69, no FMA
+  if (a.last) {
+    a.score_out[r] = nx;
   } else {
-    const uint64_t g = a.group_begin + (gw - a.n_heavy);
-    if (g >= a.group_end) return;
-    group = static_cast<uint32_t>(g);
-    if (a.heavy_flag[group]) return;
+    const uint32_t d = a.deg[r];
+    a.norm_out[r] = __ddiv_rn(nx, static_cast<double>(d > 1u ? d : 1u));  // scoring.cpp:61
   }
+}
 
+// Serial, in-order accumulation of v[0..cnt) into acc: loads run 8 ahead of
+// the dependent DADD chain (the chain is the only serial part).
+__device__ __forceinline__ double chain_add(double acc, const double* v, uint32_t cnt) {
+  uint32_t i = 0;
+  for (; i + 8 <= cnt; i += 8) {
+    double x[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) x[k] = v[i + k];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) acc = __dadd_rn(acc, x[k]);
+  }
+  for (; i < cnt; ++i) acc = __dadd_rn(acc, v[i]);
+  return acc;
+}
+
+// Hub path: one CTA per long row. Warps 1..7 stream the row's targets and
+// gather the normalized values into a ring of shared-memory slots; lane 0 of
+// warp 0 runs the single in-order DADD chain over the ring (mbarrier
+// full/empty handshake per slot).
+__device__ void hub_row(const PrStepArgs& a, uint32_t r, double* ring, uint64_t* full,
+                        uint64_t* empty) {
+  const uint32_t beg = a.off[r], len = a.off[r + 1] - beg;
+  const uint32_t chunks = (len + kHubSlot - 1) / kHubSlot;
+  const int tid = threadIdx.x;
+  if (tid == 0) {
+    for (int s = 0; s < kHubSlots; ++s) {
+      mbar_init(&full[s], kPrWarps * 32 - 32);
+      mbar_init(&empty[s], 1);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  if (tid < 32) {
+    if (tid == 0) {
+      double acc = 0.0;  // scoring.cpp:67
+      for (uint32_t c = 0; c < chunks; ++c) {
+        const uint32_t s = c % kHubSlots;
+        mbar_wait(&full[s], (c / kHubSlots) & 1);
+        const uint32_t cnt = min(kHubSlot, len - c * kHubSlot);
+        acc = chain_add(acc, ring + s * kHubSlot, cnt);  // scoring.cpp:68, in order
+        mbar_arrive(&empty[s]);
+      }
+      finish_row(a, r, acc);
+    }
+  } else {
+    const int lt = tid - 32;
+    constexpr int kLoaders = kPrWarps * 32 - 32;
+    constexpr int kPer = (kHubSlot + kLoaders - 1) / kLoaders;
+    for (uint32_t c = 0; c < chunks; ++c) {
+      const uint32_t s = c % kHubSlots;
+      if (c >= kHubSlots) mbar_wait(&empty[s], ((c / kHubSlots) - 1) & 1);
+      const uint32_t base = beg + c * kHubSlot;
+      const uint32_t cnt = min(kHubSlot, len - c * kHubSlot);
+      uint32_t t[kPer];
+#pragma unroll
+      for (int k = 0; k < kPer; ++k) {
+        const uint32_t j = lt + k * kLoaders;
+        t[k] = j < cnt ? __ldg(a.tgt + base + j) : 0u;
+      }
+#pragma unroll
+      for (int k = 0; k < kPer; ++k) {
+        const uint32_t j = lt + k * kLoaders;
+        if (j < cnt) ring[s * kHubSlot + j] = __ldg(a.norm_in + t[k]);
+      }
+      mbar_arrive(&full[s]);
+    }
+  }
+}
+
+// Light path: a warp owns 32 consecutive rows; rows are processed in runs of
+// consecutive non-hub rows whose edges are contiguous. A run's edges stream
+// through 256-edge windows: coalesced target loads and value gathers staged
+// in shared memory (the next window's loads in flight while the lanes run the
+// current window's chains), then each lane adds its own row's slice in order.
+__device__ void light_group(const PrStepArgs& a, uint32_t group, double* buf) {
+  const int lane = threadIdx.x & 31;
   const uint64_t r = (uint64_t)group * kGroupRows + lane;
-  const bool valid = r >= a.row_begin && r < a.row_end;
+  const bool in_range = r >= a.row_begin && r < a.row_end;
   uint32_t beg = 0, end = 0;
-  if (valid) {
+  if (in_range) {
     beg = a.off[r];
     end = a.off[r + 1];
   }
-  const uint32_t span_b = warp_min_u32(valid ? beg : 0xffffffffu);
-  const uint32_t span_e = warp_max_u32(valid ? end : 0u);
-  if (span_b == 0xffffffffu) return;  // uniform across the warp
-
+  const bool hub = in_range && end - beg > kHubLen;
+  const bool mine = in_range && !hub;
+  const uint32_t hub_mask = __ballot_sync(0xffffffffu, hub);
+  const uint32_t mine_mask = __ballot_sync(0xffffffffu, mine);
   double acc = 0.0;  // scoring.cpp:67
-  double* buf = sbuf[wib];
-  for (uint32_t wb = span_b; wb < span_e; wb += kPrWin) {
-    uint32_t t[kPrWin / 32];
+  uint32_t todo = mine_mask;
+  while (todo) {
+    // run = lanes [first, stop) with no hub row in between
+    const int first = __ffs(todo) - 1;
+    const uint32_t later_hubs = hub_mask & ~((2u << first) - 1u);
+    const int stop = later_hubs ? __ffs(later_hubs) - 1 : 32;
+    const uint32_t run = todo & (stop == 32 ? ~0u : ((1u << stop) - 1u));
+    todo &= ~run;
+    const int last_lane = 31 - __clz(run);
+    const uint32_t span_b = __shfl_sync(0xffffffffu, beg, first);
+    const uint32_t span_e = __shfl_sync(0xffffffffu, end, last_lane);
+    const bool in_run = (run >> lane) & 1u;
+    constexpr int K = kPrWin / 32;
+    uint32_t t1[K];
+    double v[K];
+    // prologue: window 0 values, window 1 targets
 #pragma unroll
-    for (int k = 0; k < kPrWin / 32; ++k) {
-      const uint32_t e = wb + k * 32 + lane;
-      t[k] = e < span_e ? __ldg(a.tgt + e) : 0xffffffffu;
+    for (int k = 0; k < K; ++k) {
+      const uint32_t e = span_b + k * 32 + lane;
+      t1[k] = e < span_e ? __ldg(a.tgt + e) : 0xffffffffu;
     }
 #pragma unroll
-    for (int k = 0; k < kPrWin / 32; ++k)
-      buf[k * 32 + lane] = t[k] != 0xffffffffu ? __ldg(a.norm_in + t[k]) : 0.0;
-    __syncwarp();
-    const uint32_t lo = beg > wb ? beg : wb;
-    const uint32_t hi = end < wb + kPrWin ? end : wb + kPrWin;
-    for (uint32_t e = lo; e < hi; ++e) acc = __dadd_rn(acc, buf[e - wb]);  // :68, in order
-    __syncwarp();
-  }
-  if (valid) {
-    const double nx = __dadd_rn(a.base, __dmul_rn(a.damp, acc));  // :69, no FMA
-    if (a.last) {
-      a.score_out[r] = nx;
-    } else {
-      const uint32_t d = a.deg[r];
-      a.norm_out[r] = __ddiv_rn(nx, static_cast<double>(d > 1u ? d : 1u));  // :61
+    for (int k = 0; k < K; ++k) v[k] = t1[k] != 0xffffffffu ? __ldg(a.norm_in + t1[k]) : 0.0;
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      const uint32_t e = span_b + kPrWin + k * 32 + lane;
+      t1[k] = e < span_e ? __ldg(a.tgt + e) : 0xffffffffu;
+    }
+    for (uint32_t wb = span_b; wb < span_e; wb += kPrWin) {
+#pragma unroll
+      for (int k = 0; k < K; ++k) buf[k * 32 + lane] = v[k];
+      __syncwarp();
+      // next window's gathers and the one after's targets go in flight now
+      double vn[K];
+#pragma unroll
+      for (int k = 0; k < K; ++k) vn[k] = t1[k] != 0xffffffffu ? __ldg(a.norm_in + t1[k]) : 0.0;
+#pragma unroll
+      for (int k = 0; k < K; ++k) {
+        const uint32_t e = wb + 2 * kPrWin + k * 32 + lane;
+        t1[k] = e < span_e ? __ldg(a.tgt + e) : 0xffffffffu;
+      }
+      if (in_run) {
+        const uint32_t lo = beg > wb ? beg : wb;
+        const uint32_t hi = end < wb + kPrWin ? end : wb + kPrWin;
+        if (hi > lo) acc = chain_add(acc, buf + (lo - wb), hi - lo);  // in order
+      }
+      __syncwarp();
+#pragma unroll
+      for (int k = 0; k < K; ++k) v[k] = vn[k];
     }
   }
+  if (mine) finish_row(a, r, acc);
+}
+
+__global__ void __launch_bounds__(kPrWarps * 32) pr_step_kernel(const PrStepArgs a) {
+  __shared__ __align__(16) double smem[kHubSlots * kHubSlot];  // 32 KB: hub ring / light windows
+  __shared__ uint64_t bars[2 * kHubSlots];
+  static_assert(kPrWarps * kPrWin <= kHubSlots * kHubSlot, "light windows must fit");
+  if (blockIdx.x < a.n_hub) {  // hub CTAs first: their chains start earliest
+    const uint32_t r = a.hub[blockIdx.x];
+    if (r >= a.row_begin && r < a.row_end) hub_row(a, r, smem, bars, bars + kHubSlots);
+    return;
+  }
+  const int w = threadIdx.x >> 5;
+  const uint64_t g = a.group_begin + (uint64_t)(blockIdx.x - a.n_hub) * kPrWarps + w;
+  if (g >= a.group_end) return;
+  light_group(a, static_cast<uint32_t>(g), smem + w * kPrWin);
 }
 
 unsigned long long read_flag(tg_ctx* ctx, unsigned long long* dflag) {
@@ -251,8 +377,10 @@ void compute_indeg(tg_ctx* ctx, const tg_graph* g, uint32_t* deg) {
 }
 
 // Prepares deg + norm0 for the weighted (tid != nullptr) or plain recurrence.
+// Out-of-range train ids set *bad (min index) and are skipped; the caller
+// checks it after the run (no synchronisation here).
 void pagerank_prepare(tg_ctx* ctx, const tg_graph* g, const uint64_t* tid_dev, uint64_t ntid,
-                      uint32_t* deg, double* norm0) {
+                      uint32_t* deg, double* norm0, unsigned long long* bad) {
   const uint64_t n = g->n;
   compute_indeg(ctx, g, deg);
   const double init = 1.0 / static_cast<double>(n);  // scoring.cpp:96
@@ -262,16 +390,8 @@ void pagerank_prepare(tg_ctx* ctx, const tg_graph* g, const uint64_t* tid_dev, u
     weight = static_cast<double>(n) / static_cast<double>(ntid);  // scoring.cpp:94-95
     mult = ctx->scratch_t<uint32_t>(kScratchF, n);
     TGB_CUDA(cudaMemsetAsync(mult, 0, sizeof(uint32_t) * n, ctx->stream));
-    auto* bad = ctx->scratch_t<unsigned long long>(kSmall, 1);
-    TGB_CUDA(cudaMemsetAsync(bad, 0xff, sizeof(unsigned long long), ctx->stream));
     train_mult_kernel<<<grid_for(ntid, 256), 256, 0, ctx->stream>>>(tid_dev, ntid, n, mult, bad);
     TGB_LAUNCHED();
-    const unsigned long long b = read_flag(ctx, bad);
-    if (b != ~0ull) {
-      uint64_t id = 0;
-      TGB_CUDA(cudaMemcpy(&id, tid_dev + b, sizeof(id), cudaMemcpyDeviceToHost));
-      domain_error("train id " + std::to_string(id) + " out of range");  // scoring.cpp:98
-    }
   }
   pr_init_kernel<<<grid_for(n, 256), 256, 0, ctx->stream>>>(deg, mult, n, init, weight, norm0);
   TGB_LAUNCHED();
@@ -288,9 +408,8 @@ void pagerank_step(tg_ctx* ctx, const tg_graph* g, const uint32_t* deg, double d
   a.norm_in = nin;
   a.norm_out = nout;
   a.score_out = sout;
-  a.heavy_flag = g->heavy_flag;
-  a.heavy = g->heavy;
-  a.n_heavy = g->n_heavy;
+  a.hub = g->hub;
+  a.n_hub = g->n_hub;
   a.group_begin = static_cast<uint32_t>(rb / kGroupRows);
   a.group_end = static_cast<uint32_t>((re + kGroupRows - 1) / kGroupRows);
   a.row_begin = rb;
@@ -298,8 +417,8 @@ void pagerank_step(tg_ctx* ctx, const tg_graph* g, const uint32_t* deg, double d
   a.base = (1.0 - damp) / static_cast<double>(g->n);  // scoring.cpp:53
   a.damp = damp;
   a.last = last;
-  const uint64_t warps = a.n_heavy + (a.group_end - a.group_begin);
-  const unsigned grid = static_cast<unsigned>((warps + kPrWarps - 1) / kPrWarps);
+  const uint64_t light = (a.group_end - a.group_begin + kPrWarps - 1) / kPrWarps;
+  const unsigned grid = static_cast<unsigned>(a.n_hub + light);
   pr_step_kernel<<<grid, kPrWarps * 32, 0, ctx->stream>>>(a);
   TGB_LAUNCHED();
 }
@@ -325,13 +444,22 @@ void run_pagerank(tg_ctx* ctx, const tg_graph* g, uint32_t iterations, double da
   double* na = ctx->scratch_t<double>(kScratchB, n);
   double* nb = ctx->scratch_t<double>(kScratchC, n);
   DevOut<double> o(ctx, out, n, kStageOut0);
-  pagerank_prepare(ctx, g, tid_dev, ntid, deg, na);
+  auto* bad = ctx->scratch_t<unsigned long long>(kSmall, 1);
+  if (weighted) TGB_CUDA(cudaMemsetAsync(bad, 0xff, 8, ctx->stream));
+  pagerank_prepare(ctx, g, tid_dev, ntid, deg, na, bad);
   for (uint32_t it = 0; it < iterations; ++it) {
     const bool last = it + 1 == iterations;
     pagerank_step(ctx, g, deg, damp, na, nb, o.dev(), 0, n, last ? 1 : 0);
     std::swap(na, nb);
   }
+  unsigned long long hb = ~0ull;
+  if (weighted) TGB_CUDA(cudaMemcpyAsync(&hb, bad, 8, cudaMemcpyDeviceToHost, ctx->stream));
   o.finish();
+  if (hb != ~0ull) {
+    uint64_t id = 0;
+    TGB_CUDA(cudaMemcpy(&id, tid_dev + hb, sizeof(id), cudaMemcpyDeviceToHost));
+    domain_error("train id " + std::to_string(id) + " out of range");  // scoring.cpp:98
+  }
 }
 
 }  // namespace tgb
@@ -383,21 +511,34 @@ int tg_graph_create(tg_ctx* ctx, const uint64_t* offsets, const uint64_t* target
                      " (need offsets[0]==0, monotone, offsets[num_nodes]==num_edges)");
       if (hb[1] != ~0ull)
         format_error("csr: target out of range at edge " + std::to_string(hb[1]));
-      // row-group schedule
-      g->n_groups = static_cast<uint32_t>((n + kGroupRows - 1) / kGroupRows);
-      TGB_CUDA(cudaMalloc(&g->heavy_flag, std::max<uint32_t>(g->n_groups, 1)));
-      TGB_CUDA(cudaMalloc(&g->heavy, sizeof(uint32_t) * (std::max<uint32_t>(g->n_groups, 1) + 1)));
-      uint32_t* cnt = g->heavy + std::max<uint32_t>(g->n_groups, 1);
-      TGB_CUDA(cudaMemsetAsync(cnt, 0, sizeof(uint32_t), ctx->stream));
+      // hub rows (one CTA each in K3), longest first
+      TGB_CUDA(cudaMalloc(&g->hub, sizeof(uint32_t) * (std::max<uint64_t>(n, 1) + 2)));
+      uint32_t* cnt = g->hub + std::max<uint64_t>(n, 1);
+      TGB_CUDA(cudaMemsetAsync(cnt, 0, 2 * sizeof(uint32_t), ctx->stream));
       if (n) {
-        group_schedule_kernel<<<static_cast<unsigned>((uint64_t(g->n_groups) * 32 + 255) / 256), 256,
-                                0, ctx->stream>>>(g->off, n, g->n_groups, g->heavy_flag, g->heavy,
-                                                  cnt);
+        hub_rows_kernel<<<grid_for(n, 256), 256, 0, ctx->stream>>>(g->off, n, g->hub, cnt);
         TGB_LAUNCHED();
       }
-      TGB_CUDA(cudaMemcpyAsync(&g->n_heavy, cnt, sizeof(uint32_t), cudaMemcpyDeviceToHost,
-                               ctx->stream));
+      uint32_t hc[2];
+      TGB_CUDA(cudaMemcpyAsync(hc, cnt, sizeof(hc), cudaMemcpyDeviceToHost, ctx->stream));
       ctx->sync();
+      g->n_hub = hc[0];
+      g->max_row = hc[1];
+      if (g->n_hub) {
+        std::vector<uint32_t> rows(g->n_hub), offs(n + 1);
+        TGB_CUDA(cudaMemcpy(rows.data(), g->hub, 4 * rows.size(), cudaMemcpyDeviceToHost));
+        std::vector<std::pair<uint32_t, uint32_t>> lens;
+        for (uint32_t r : rows) {
+          uint32_t o2[2];
+          TGB_CUDA(cudaMemcpy(o2, g->off + r, 8, cudaMemcpyDeviceToHost));
+          lens.push_back({o2[1] - o2[0], r});
+        }
+        std::sort(lens.begin(), lens.end(), [](auto x, auto y) {
+          return x.first != y.first ? x.first > y.first : x.second < y.second;
+        });
+        for (size_t i = 0; i < lens.size(); ++i) rows[i] = lens[i].second;
+        TGB_CUDA(cudaMemcpy(g->hub, rows.data(), 4 * rows.size(), cudaMemcpyHostToDevice));
+      }
     } catch (...) {
       tg_graph_destroy(g);
       throw;
@@ -410,8 +551,7 @@ int tg_graph_destroy(tg_graph* g) {
   if (!g) return TG_OK;
   cudaFree(g->off);
   cudaFree(g->tgt);
-  cudaFree(g->heavy_flag);
-  cudaFree(g->heavy);
+  cudaFree(g->hub);
   delete g;
   return TG_OK;
 }
@@ -461,7 +601,9 @@ int tg_pagerank_prepare_async(tg_ctx* ctx, const tg_graph* g, const uint64_t* ti
     if (tid_dev && ntid == 0) domain_error("weighted reverse pagerank needs a non-empty train id set");
     if (!g->n) return;
     DeviceGuard dg(ctx->device);
-    pagerank_prepare(ctx, g, tid_dev, ntid, indeg_dev, norm0_dev);
+    // train ids must be in range here (the synchronous entry points check them)
+    auto* bad = ctx->scratch_t<unsigned long long>(kSmall, 1);
+    pagerank_prepare(ctx, g, tid_dev, ntid, indeg_dev, norm0_dev, bad);
   });
 }
 

@@ -276,7 +276,12 @@ __global__ void __launch_bounds__(256) gather_kernel(GatherTable t, const uint64
   const uint64_t warp = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
   const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
   uint64_t cl = 0, cp = 0, ch = 0;
-  for (uint64_t b0 = warp * B; b0 < n; b0 += nwarps * B) {
+  // Batches run from the END of the id list: minibatch lists are sorted, so
+  // the cold (highest) ids go first and their PCIe latency overlaps the
+  // HBM-resident rows that follow.
+  const uint64_t nb = (n + B - 1) / B;
+  for (uint64_t k = warp; k < nb; k += nwarps) {
+    const uint64_t b0 = (nb - 1 - k) * B;
     const uint8_t* src = nullptr;
     uint8_t* d = nullptr;
     int tier = -1;
