@@ -211,6 +211,9 @@ typedef struct tg_store tg_store;
 #define TG_COLD_INDIRECT 1u  /* register the caller's original host matrix and  */
                              /* index it through the permutation (no host copy) */
 #define TG_COLD_PAD128 2u    /* pad cold rows to a 128 B stride (PCIe lines)    */
+#define TG_GATHER_BULK 4u    /* K8 via TMA bulk copies (cp.async.bulk) staged   */
+                             /* through shared memory                            */
+#define TG_GATHER_L2PF 8u    /* K8 LDG path with the L2::256B prefetch hint      */
 
 int tg_store_create(tg_ctx* ctx, const tg_layout* layout, uint32_t device_index, uint32_t flags,
                     tg_store** out);

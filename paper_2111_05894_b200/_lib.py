@@ -21,6 +21,8 @@ TG_MAX_DEVICES = 16
 TG_COLD_REORDERED = 0
 TG_COLD_INDIRECT = 1
 TG_COLD_PAD128 = 2
+TG_GATHER_BULK = 4
+TG_GATHER_L2PF = 8
 
 
 class TgLayout(C.Structure):

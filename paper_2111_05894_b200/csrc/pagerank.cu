@@ -34,6 +34,7 @@ struct tg_graph {
   uint32_t* hub = nullptr;     // rows longer than kHubLen, longest first
   uint32_t n_hub = 0;
   uint32_t max_row = 0;
+  uint32_t* indeg = nullptr;   // in_degrees (csr_graph.cpp:89-93), built with the device graph
 };
 
 namespace tgb {
@@ -208,12 +209,21 @@ __device__ __forceinline__ void finish_row(const PrStepArgs& a, uint64_t r, doub
 // the dependent DADD chain (the chain is the only serial part).
 __device__ __forceinline__ double chain_add(double acc, const double* v, uint32_t cnt) {
   uint32_t i = 0;
-  for (; i + 8 <= cnt; i += 8) {
-    double x[8];
+  if (cnt >= 16) {
+    double x[8], y[8];
 #pragma unroll
-    for (int k = 0; k < 8; ++k) x[k] = v[i + k];
+    for (int k = 0; k < 8; ++k) x[k] = v[k];
+    for (; i + 16 <= cnt; i += 8) {
+#pragma unroll
+      for (int k = 0; k < 8; ++k) y[k] = v[i + 8 + k];  // next 8 in flight
+#pragma unroll
+      for (int k = 0; k < 8; ++k) acc = __dadd_rn(acc, x[k]);
+#pragma unroll
+      for (int k = 0; k < 8; ++k) x[k] = y[k];
+    }
 #pragma unroll
     for (int k = 0; k < 8; ++k) acc = __dadd_rn(acc, x[k]);
+    i += 8;
   }
   for (; i < cnt; ++i) acc = __dadd_rn(acc, v[i]);
   return acc;
@@ -382,7 +392,8 @@ void compute_indeg(tg_ctx* ctx, const tg_graph* g, uint32_t* deg) {
 void pagerank_prepare(tg_ctx* ctx, const tg_graph* g, const uint64_t* tid_dev, uint64_t ntid,
                       uint32_t* deg, double* norm0, unsigned long long* bad) {
   const uint64_t n = g->n;
-  compute_indeg(ctx, g, deg);
+  if (deg != g->indeg)
+    TGB_CUDA(cudaMemcpyAsync(deg, g->indeg, 4 * n, cudaMemcpyDeviceToDevice, ctx->stream));
   const double init = 1.0 / static_cast<double>(n);  // scoring.cpp:96
   double weight = 1.0;
   uint32_t* mult = nullptr;
@@ -440,7 +451,7 @@ void run_pagerank(tg_ctx* ctx, const tg_graph* g, uint32_t iterations, double da
   if (n == 0) return;
   DeviceGuard dg(ctx->device);
   const uint64_t* tid_dev = weighted ? dev_in(ctx, tid, ntid, kStageIn0) : nullptr;
-  uint32_t* deg = ctx->scratch_t<uint32_t>(kScratchA, n);
+  uint32_t* deg = g->indeg;  // cached with the device graph
   double* na = ctx->scratch_t<double>(kScratchB, n);
   double* nb = ctx->scratch_t<double>(kScratchC, n);
   DevOut<double> o(ctx, out, n, kStageOut0);
@@ -539,6 +550,9 @@ int tg_graph_create(tg_ctx* ctx, const uint64_t* offsets, const uint64_t* target
         for (size_t i = 0; i < lens.size(); ++i) rows[i] = lens[i].second;
         TGB_CUDA(cudaMemcpy(g->hub, rows.data(), 4 * rows.size(), cudaMemcpyHostToDevice));
       }
+      TGB_CUDA(cudaMalloc(&g->indeg, sizeof(uint32_t) * std::max<uint64_t>(n, 1)));
+      compute_indeg(ctx, g, g->indeg);
+      ctx->sync();
     } catch (...) {
       tg_graph_destroy(g);
       throw;
@@ -552,6 +566,7 @@ int tg_graph_destroy(tg_graph* g) {
   cudaFree(g->off);
   cudaFree(g->tgt);
   cudaFree(g->hub);
+  cudaFree(g->indeg);
   delete g;
   return TG_OK;
 }
@@ -577,7 +592,7 @@ int tg_in_degrees(tg_ctx* ctx, const tg_graph* g, uint64_t* out) {
     if (!g->n) return;
     DeviceGuard dg(ctx->device);
     uint32_t* deg = ctx->scratch_t<uint32_t>(kScratchA, g->n);
-    compute_indeg(ctx, g, deg);
+    compute_indeg(ctx, g, deg);  // recomputed on purpose: this is the in_degrees() API
     DevOut<uint64_t> o(ctx, out, g->n, kStageOut0);
     widen_u32_kernel<<<grid_for(g->n, 256), 256, 0, ctx->stream>>>(deg, o.dev(), g->n);
     TGB_LAUNCHED();

@@ -179,13 +179,25 @@ __device__ __forceinline__ uint4 ld_stream_v4(const void* p) {
                : "l"(p));
   return r;
 }
-template <typename V>
+__device__ __forceinline__ uint4 ld_l2pf_v4(const void* p) {
+  uint4 r;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::256B.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+               : "l"(p));
+  return r;
+}
+// PF: ask L2 to fetch the surrounding 256 B sector group (TG_GATHER_L2PF).
+template <typename V, bool PF = false>
 __device__ __forceinline__ V ld_row(const V* p) {
   return *p;
 }
 template <>
-__device__ __forceinline__ uint4 ld_row<uint4>(const uint4* p) {
+__device__ __forceinline__ uint4 ld_row<uint4, false>(const uint4* p) {
   return ld_stream_v4(p);
+}
+template <>
+__device__ __forceinline__ uint4 ld_row<uint4, true>(const uint4* p) {
+  return ld_l2pf_v4(p);
 }
 
 constexpr int kCopyChunks = 256;            // chunks per warp batch (8 per lane)
@@ -193,7 +205,7 @@ constexpr int kCopyPerLane = kCopyChunks / 32;
 
 // Copies a batch of B rows: src[j]/dst[j] held by lane j (j < B, nullptr =
 // skip). C = row_bytes / sizeof(V) chunks per row; B*C <= kCopyChunks.
-template <typename V>
+template <typename V, bool PF = false>
 __device__ __forceinline__ void copy_batch(const uint8_t* src, uint8_t* dst, uint32_t B,
                                            uint32_t C, int lane) {
   const uint32_t total = B * C;
@@ -215,7 +227,7 @@ __device__ __forceinline__ void copy_batch(const uint8_t* src, uint8_t* dst, uin
   }
 #pragma unroll
   for (int u = 0; u < kCopyPerLane; ++u)
-    if (sp[u]) buf[u] = ld_row<V>(sp[u]);
+    if (sp[u]) buf[u] = ld_row<V, PF>(sp[u]);
 #pragma unroll
   for (int u = 0; u < kCopyPerLane; ++u)
     if (dp[u]) *dp[u] = buf[u];
@@ -267,7 +279,7 @@ __device__ __forceinline__ const uint8_t* row_ptr(const GatherTable& t, uint64_t
 }
 
 // K8: the tiered gather. dst row i <- feature row ids[i].
-template <typename V>
+template <typename V, bool PF = false>
 __global__ void __launch_bounds__(256) gather_kernel(GatherTable t, const uint64_t* __restrict__ ids,
                                                      uint64_t n, uint8_t* __restrict__ dst,
                                                      uint32_t B, uint32_t C, uint64_t* counters,
@@ -294,7 +306,7 @@ __global__ void __launch_bounds__(256) gather_kernel(GatherTable t, const uint64
     cp += __popc(__ballot_sync(0xffffffffu, tier == 1));
     ch += __popc(__ballot_sync(0xffffffffu, tier == 2));
     if (C <= (uint32_t)kCopyChunks) {
-      copy_batch<V>(src, d, B, C, lane);
+      copy_batch<V, PF>(src, d, B, C, lane);
     } else {
       for (uint32_t j = 0; j < B; ++j) {
         const uint8_t* s = reinterpret_cast<const uint8_t*>(
@@ -305,6 +317,109 @@ __global__ void __launch_bounds__(256) gather_kernel(GatherTable t, const uint64
       }
     }
   }
+  if (lane != 0) cl = cp = ch = 0;
+  block_add_counters(cl, cp, ch, counters);
+}
+
+// K8, TMA bulk-copy variant (TG_GATHER_BULK): each warp stages a batch of
+// rows in shared memory with one cp.async.bulk per row (global/host-mapped ->
+// smem, completion on an mbarrier), then writes them out with bulk stores
+// (smem -> HBM). The copy engine issues whole-row requests, which is what
+// the PCIe zero-copy path prefers. Two staging buffers per warp: the loads of
+// batch k+1 are in flight while batch k drains.
+constexpr int kBulkWarps = 8;
+constexpr int kBulkStage = 6144;  // bytes per staging buffer (x2 per warp)
+
+__device__ __forceinline__ void bulk_g2s(uint32_t smem_dst, const void* src, uint32_t bytes,
+                                         uint32_t mbar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+      ::"r"(smem_dst), "l"(src), "r"(bytes), "r"(mbar)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_s2g(void* dst, uint32_t smem_src, uint32_t bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst),
+               "r"(smem_src), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_commit() {
+  asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+}
+template <int N>
+__device__ __forceinline__ void bulk_wait_read() {
+  asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
+}
+__device__ __forceinline__ void mbar_init_s(uint32_t bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
+  asm volatile("{\n\t.reg .b64 st;\n\tmbarrier.arrive.expect_tx.shared::cta.b64 st, [%0], %1;\n\t}"
+               ::"r"(bar), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait_s(uint32_t bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tWAITB_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAITB_%=;\n\t}" ::"r"(bar),
+      "r"(parity)
+      : "memory");
+}
+
+__global__ void __launch_bounds__(kBulkWarps * 32) gather_bulk_kernel(
+    GatherTable t, const uint64_t* __restrict__ ids, uint64_t n, uint8_t* __restrict__ dst,
+    uint32_t B, uint32_t Rpad, uint64_t* counters, unsigned long long* err) {
+  extern __shared__ __align__(128) uint8_t bulk_smem[];  // [warps][2][kBulkStage]
+  __shared__ __align__(8) uint64_t bars[kBulkWarps][2];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const uint32_t bar0 = static_cast<uint32_t>(__cvta_generic_to_shared(&bars[w][0]));
+  const uint32_t bar1 = static_cast<uint32_t>(__cvta_generic_to_shared(&bars[w][1]));
+  const uint32_t s0 =
+      static_cast<uint32_t>(__cvta_generic_to_shared(bulk_smem + (2 * w) * kBulkStage));
+  const uint32_t s1 = s0 + kBulkStage;
+  if (lane == 0) {
+    mbar_init_s(bar0, 1);
+    mbar_init_s(bar1, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncwarp();
+  const uint64_t warp = (uint64_t)blockIdx.x * kBulkWarps + w;
+  const uint64_t nwarps = (uint64_t)gridDim.x * kBulkWarps;
+  const uint64_t nb = (n + B - 1) / B;
+  const uint32_t R = static_cast<uint32_t>(t.R);
+  uint64_t cl = 0, cp = 0, ch = 0;
+  uint32_t phase[2] = {0, 0};
+  // in-flight batch state (one per buffer)
+  int buf = 0;
+  for (uint64_t k = warp; k < nb; k += nwarps) {
+    const uint64_t b0 = (nb - 1 - k) * B;  // cold (highest ids) first
+    const uint32_t bar = buf ? bar1 : bar0;
+    const uint32_t sb = buf ? s1 : s0;
+    // the buffer we are about to fill was stored from two batches ago
+    bulk_wait_read<1>();
+    __syncwarp();
+    const uint8_t* src = nullptr;
+    int tier = -1;
+    if (lane < (int)B && b0 + lane < n) {
+      src = row_ptr(t, ids[b0 + lane], &tier);
+      if (tier == 3) atomicMin(err, (unsigned long long)(b0 + lane));
+    }
+    cl += __popc(__ballot_sync(0xffffffffu, tier == 0));
+    cp += __popc(__ballot_sync(0xffffffffu, tier == 1));
+    ch += __popc(__ballot_sync(0xffffffffu, tier == 2));
+    const uint32_t nrows = __popc(__ballot_sync(0xffffffffu, src != nullptr));
+    if (lane == 0) mbar_expect_tx(bar, nrows * R);
+    __syncwarp();
+    if (src) bulk_g2s(sb + lane * Rpad, src, R, bar);
+    // drain the OTHER buffer's batch (issued last iteration) while this one loads
+    mbar_wait_s(bar, phase[buf]);
+    phase[buf] ^= 1;
+    if (src) bulk_s2g(dst + (b0 + lane) * t.R, sb + lane * Rpad, R);
+    bulk_commit();
+    buf ^= 1;
+  }
+  bulk_wait_read<0>();
+  asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
   if (lane != 0) cl = cp = ch = 0;
   block_add_counters(cl, cp, ch, counters);
 }
@@ -635,11 +750,33 @@ void launch_gather(tg_store* s, const uint64_t* ids_dev, uint64_t n, void* dst_d
                    reinterpret_cast<uint64_t>(s->cold_dev) | s->cold_stride;
   for (uint32_t d = 0; d < s->L.num_devices; ++d) align |= reinterpret_cast<uint64_t>(s->inter[d]);
   const int w = vec_width(s->R, {align});
+  auto* dst = static_cast<uint8_t*>(dst_dev);
+  if ((s->flags & TG_GATHER_BULK) && w == 16 && s->R <= (uint64_t)kBulkStage) {
+    const uint32_t Rpad = static_cast<uint32_t>(s->R);
+    const uint32_t B = std::min<uint32_t>(32, kBulkStage / Rpad);
+    const uint64_t warps = (n + B - 1) / B;
+    const unsigned grid = grid_for(warps * 32, kBulkWarps * 32, ctx->num_sms * 2);
+    constexpr int kSmem = kBulkWarps * 2 * kBulkStage;
+    static bool attr = false;
+    if (!attr) {
+      TGB_CUDA(cudaFuncSetAttribute(gather_bulk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    kSmem));
+      attr = true;
+    }
+    gather_bulk_kernel<<<grid, kBulkWarps * 32, kSmem, ctx->stream>>>(t, ids_dev, n, dst, B, Rpad,
+                                                                      counters3, err);
+    TGB_LAUNCHED();
+    return;
+  }
   uint32_t B, C;
   batch_shape(s->R, w, &B, &C);
   const uint64_t warps = (n + B - 1) / B;
   const unsigned grid = grid_for(warps * 32, 256, ctx->num_sms * 8);
-  auto* dst = static_cast<uint8_t*>(dst_dev);
+  if ((s->flags & TG_GATHER_L2PF) && w == 16) {
+    gather_kernel<uint4, true><<<grid, 256, 0, ctx->stream>>>(t, ids_dev, n, dst, B, C, counters3, err);
+    TGB_LAUNCHED();
+    return;
+  }
   switch (w) {
     case 16: gather_kernel<uint4><<<grid, 256, 0, ctx->stream>>>(t, ids_dev, n, dst, B, C, counters3, err); break;
     case 8: gather_kernel<uint2><<<grid, 256, 0, ctx->stream>>>(t, ids_dev, n, dst, B, C, counters3, err); break;

@@ -19,8 +19,8 @@ from typing import Iterable, Optional, Sequence
 
 import numpy as np
 
-from ._lib import (LIB, TG_COLD_INDIRECT, TG_COLD_PAD128, TG_COLD_REORDERED, TgLayout,
-                   TgLocation, TgReport)
+from ._lib import (LIB, TG_COLD_INDIRECT, TG_COLD_PAD128, TG_COLD_REORDERED, TG_GATHER_BULK,
+                   TG_GATHER_L2PF, TgLayout, TgLocation, TgReport)
 
 __all__ = [
     "TierGraphError", "DomainError", "FormatError", "IoError", "Context", "default_context",
@@ -601,13 +601,14 @@ class TieredFeatureStore:
 
     def __init__(self, features, perm, layout: TierLayout, device_index: int = 0, *,
                  ctx: Context = None, cold_mode: str = "reordered", pad128: bool = False,
-                 place: bool = True):
+                 gather_mode: str = "ldg", place: bool = True):
         self.ctx = _ctx(ctx)
         self.layout = layout
         self.device_index = device_index
         flags = {"reordered": TG_COLD_REORDERED, "indirect": TG_COLD_INDIRECT}[cold_mode]
         if pad128:
             flags |= TG_COLD_PAD128
+        flags |= {"ldg": 0, "bulk": TG_GATHER_BULK, "l2pf": TG_GATHER_L2PF}[gather_mode]
         h = C.c_void_p()
         _check(LIB.tg_store_create(self.ctx.h, C.byref(layout._c()), int(device_index), flags,
                                    C.byref(h)))
