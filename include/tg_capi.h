@@ -4,7 +4,7 @@
  * Plain pointers and sizes only (no torch, no STL). Every entry point names the
  * reference interface it replaces (reference = arXiv 2111.05894 `tiergraph`,
  * files under proj/include/tiergraph and proj/src). The C++ drop-in headers in
- * include/tiergraph/*.hpp are implemented on top of these calls, and the
+ * include/tiergraph/tiergraph.hpp is implemented on top of these calls, and the
  * Python host mirror (paper_2111_05894_b200/tiergraph.py) binds them with
  * ctypes; INTEGRATION.md shows the bindings.
  *
