@@ -60,57 +60,64 @@ def measured_peaks():
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
-    Q = ("index,clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
-         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-         "clocks_event_reasons.sw_power_cap")
+    """SM clock + throttle reasons sampled through NVML every ~2 ms while the
+    timed region runs (the recipe's nvidia-smi clocks line, without the
+    nvidia-smi start-up latency that would miss a sub-second region)."""
+    REASONS = {0x8: "hw_slowdown", 0x40: "hw_thermal_slowdown", 0x20: "sw_thermal_slowdown",
+               0x4: "sw_power_cap", 0x80: "hw_power_brake_slowdown"}
 
     def __init__(self, device: int):
         self.device = device
-        self.proc = None
-        self.lines = []
+        self.samples = []
+        self.stop = threading.Event()
+        self.t = None
+        self.max_mhz = None
 
     def __enter__(self):
         try:
-            self.proc = subprocess.Popen(
-                ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.Q}",
-                 "--format=csv,noheader,nounits", "-lms", "20"],
-                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self.t = threading.Thread(target=self._read, daemon=True)
+            import pynvml as nv
+            nv.nvmlInit()
+            h = nv.nvmlDeviceGetHandleByIndex(self.device)
+            self.max_mhz = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
+            get_reasons = getattr(nv, "nvmlDeviceGetCurrentClocksEventReasons", None) or \
+                nv.nvmlDeviceGetCurrentClocksThrottleReasons
+
+            def run():
+                while not self.stop.is_set():
+                    try:
+                        self.samples.append((time.perf_counter(),
+                                             nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM),
+                                             int(get_reasons(h))))
+                    except Exception:
+                        pass
+                    time.sleep(0.002)
+            self.t = threading.Thread(target=run, daemon=True)
             self.t.start()
-        except Exception:
-            self.proc = None
+            t0 = time.perf_counter()
+            while not self.samples and time.perf_counter() - t0 < 2.0:
+                time.sleep(0.001)
+        except Exception as e:  # no NVML: report no samples
+            log(f"clock sampler unavailable: {e}")
         return self
 
-    def _read(self):
-        for line in self.proc.stdout:
-            self.lines.append(line.strip())
-
     def __exit__(self, *exc):
-        if self.proc:
-            self.proc.terminate()
-            try:
-                self.proc.wait(timeout=5)
-            except Exception:
-                self.proc.kill()
+        self.stop.set()
+        if self.t:
+            self.t.join(timeout=2)
 
-    def summary(self):
-        sm, mx, reasons = [], 0.0, set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for ln in self.lines:
-            f = [x.strip() for x in ln.split(",")]
-            if len(f) < 7:
-                continue
-            try:
-                sm.append(float(f[1]))
-                mx = max(mx, float(f[2]))
-            except ValueError:
-                continue
-            for nm, v in zip(names, f[3:7]):
-                if v.lower() == "active":
+    def summary(self, t_begin=None, t_end=None):
+        win = [x for x in self.samples
+               if (t_begin is None or x[0] >= t_begin) and (t_end is None or x[0] <= t_end)]
+        if len(win) < 3:
+            win = self.samples
+        reasons = set()
+        for _, _, m in win:
+            for bit, nm in self.REASONS.items():
+                if m & bit:
                     reasons.add(nm)
-        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx or None,
-                "reasons": sorted(reasons), "samples": len(sm)}
+        sm = [c for _, c, _ in win]
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(reasons), "samples": len(win), "source": "NVML, 2 ms poll"}
 
 
 # ----------------------------------------------------------------------------
@@ -283,6 +290,7 @@ def run_ours(args):
     evs = []
     if True:
         torch.cuda.synchronize()
+        t_begin = time.perf_counter()
         for k in range(args.warmup, nsteps):
             flush.zero_()
             a = torch.cuda.Event(enable_timing=True)
@@ -292,6 +300,7 @@ def run_ours(args):
             b.record()
             evs.append((a, b))
         torch.cuda.synchronize()
+        t_end = time.perf_counter()
         if dist:
             dist.barrier()
     clk.__exit__(None, None, None)
@@ -377,7 +386,7 @@ def run_ours(args):
 
     result = None
     if rank == 0:
-        clocks = clk.summary()
+        clocks = clk.summary(t_begin, t_end)
         pr_bytes_iter = 4 * (n + 1) + 4 * e + 8 * e + 4 * n + 8 * n
         result = {
             "metric": METRIC, "value": round(gbps, 2), "unit": "GB/s", "n_gpus": world,

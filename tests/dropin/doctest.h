@@ -4,7 +4,7 @@
 // (proj/tests/test_{scoring,reorder,tiering}.cpp) are written against doctest,
 // whose header is not shipped with the reference (proj/.gitignore:2) and is not
 // installed here. This file implements exactly the subset those suites use —
-// TEST_CASE, CHECK, REQUIRE, CHECK_THROWS_AS, CHECK_THROWS_WITH_AS,
+// TEST_SUITE_BEGIN/END, TEST_CASE, CHECK, REQUIRE, CHECK_THROWS_AS, CHECK_THROWS_WITH_AS,
 // doctest::Approx(.epsilon), doctest::Contains — so they can be compiled
 // unchanged against the B200 drop-in library (oracle/Makefile, target dropin).
 //
@@ -136,6 +136,10 @@ inline int run_all(int argc, char** argv) {
                                                                  &fn);                 \
   static void fn()
 #define TEST_CASE(name) DOCTEST_CASE_(DOCTEST_CAT(doctest_case_, __COUNTER__), name)
+
+// Suites are only grouping labels here.
+#define TEST_SUITE_BEGIN(name) static_assert(true, name)
+#define TEST_SUITE_END() static_assert(true, "")
 
 #define CHECK(...) doctest::detail::check(static_cast<bool>(__VA_ARGS__), __FILE__, __LINE__, #__VA_ARGS__, false)
 #define REQUIRE(...) doctest::detail::check(static_cast<bool>(__VA_ARGS__), __FILE__, __LINE__, #__VA_ARGS__, true)
