@@ -1,0 +1,77 @@
+"""Summarise ncu captures for profiles/ (run here, on the CPU box).
+
+  python scripts/ncu_summary.py launches <launches.csv>            -> per-kernel share table
+  python scripts/ncu_summary.py full <report.ncu-rep> [name]        -> key metrics per launch
+Prints markdown; `full` also prints one JSON line with the DRAM traffic per launch.
+"""
+import collections
+import csv
+import io
+import json
+import subprocess
+import sys
+
+KEYS = [
+    "gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
+    "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed",
+    "lts__t_bytes.sum", "lts__t_sectors_aperture_sysmem.sum",
+    "sm__throughput.avg.pct_of_peak_sustained_elapsed",
+    "sm__warps_active.avg.pct_of_peak_sustained_active", "launch__registers_per_thread",
+    "launch__grid_size", "launch__block_size", "launch__occupancy_limit_registers",
+    "smsp__average_warps_issue_stalled_long_scoreboard_per_issue_active.ratio",
+    "smsp__thread_inst_executed_per_inst_executed.ratio",
+]
+
+SCALE = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "usecond": 1e-6, "msecond": 1e-3,
+         "nsecond": 1e-9, "second": 1}
+
+
+def launches(path):
+    rows = list(csv.reader(open(path)))
+    hi = [i for i, r in enumerate(rows) if "Kernel Name" in r][0]
+    h = rows[hi]
+    ki, vi, ui = h.index("Kernel Name"), h.index("Metric Value"), h.index("Metric Unit")
+    agg = collections.defaultdict(lambda: [0, 0.0])
+    for r in rows[hi + 1:]:
+        if len(r) <= vi:
+            continue
+        v = float(r[vi].replace(",", "")) * SCALE.get(r[ui], 1e-9)
+        name = r[ki].split("(")[0]
+        agg[name][0] += 1
+        agg[name][1] += v
+    tot = sum(a[1] for a in agg.values())
+    print("| kernel | launches | total us | share | avg us |\n|---|---|---|---|---|")
+    for k, (c, t) in sorted(agg.items(), key=lambda x: -x[1][1]):
+        print(f"| `{k[:70]}` | {c} | {t*1e6:.1f} | {t/tot*100:.1f}% | {t/c*1e6:.2f} |")
+
+
+def full(path, name=None):
+    out = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True,
+                         text=True, check=True).stdout
+    rows = list(csv.reader(io.StringIO(out)))
+    h, units = rows[0], rows[1]
+    print(f"report `{path.split('/')[-1]}`\n")
+    print("| metric | " + " | ".join(f"launch {i}" for i in range(len(rows) - 2)) + " |")
+    print("|---" * (len(rows) - 1) + "|")
+    kn = h.index("Kernel Name")
+    print("| kernel | " + " | ".join(f"`{r[kn].split('(')[0]}`" for r in rows[2:]) + " |")
+    dram = []
+    for k in KEYS:
+        if k not in h:
+            continue
+        i = h.index(k)
+        print(f"| {k} | " + " | ".join(f"{r[i]} {units[i]}" for r in rows[2:]) + " |")
+    ir, iw = h.index("dram__bytes_read.sum"), h.index("dram__bytes_write.sum")
+    for r in rows[2:]:
+        dram.append(float(r[ir]) * SCALE[units[ir]] + float(r[iw]) * SCALE[units[iw]])
+    print()
+    print(json.dumps({"report": path.split("/")[-1], "kernel": name,
+                      "dram_bytes_per_launch": [int(x) for x in dram],
+                      "dram_bytes_per_launch_mean": int(sum(dram) / len(dram))}))
+
+
+if __name__ == "__main__":
+    if sys.argv[1] == "launches":
+        launches(sys.argv[2])
+    else:
+        full(sys.argv[2], sys.argv[3] if len(sys.argv) > 3 else None)
