@@ -214,6 +214,7 @@ typedef struct tg_store tg_store;
 #define TG_GATHER_BULK 4u    /* K8 via TMA bulk copies (cp.async.bulk) staged   */
                              /* through shared memory                            */
 #define TG_GATHER_L2PF 8u    /* K8 LDG path with the L2::256B prefetch hint      */
+#define TG_GATHER_SPREAD 16u /* K8: deal consecutive batches across CTAs         */
 
 int tg_store_create(tg_ctx* ctx, const tg_layout* layout, uint32_t device_index, uint32_t flags,
                     tg_store** out);

@@ -23,6 +23,7 @@ TG_COLD_INDIRECT = 1
 TG_COLD_PAD128 = 2
 TG_GATHER_BULK = 4
 TG_GATHER_L2PF = 8
+TG_GATHER_SPREAD = 16
 
 
 class TgLayout(C.Structure):

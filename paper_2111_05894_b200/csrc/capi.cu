@@ -198,6 +198,12 @@ int tg_ctx_destroy(tg_ctx* c) {
   cudaStreamSynchronize(c->stream);
   for (int i = 0; i < kNumSlots; ++i)
     if (c->slot_ptr[i]) cudaFree(c->slot_ptr[i]);
+  if (c->aux) {
+    cudaStreamSynchronize(c->aux);
+    cudaStreamDestroy(c->aux);
+    cudaEventDestroy(c->ev_fork);
+    cudaEventDestroy(c->ev_join);
+  }
   if (c->own_stream) cudaStreamDestroy(c->stream);
   delete c;
   return TG_OK;

@@ -68,6 +68,26 @@ struct tg_ctx {
   void* slot_ptr[tgb::kNumSlots] = {};
   size_t slot_size[tgb::kNumSlots] = {};
   void* pinned_small = nullptr;  // 4 KB mapped host scratch for small results
+  // Fork-join side stream (concurrent kernels inside one stream-ordered call).
+  cudaStream_t aux = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+
+  // Work enqueued on `aux` between fork() and join() runs concurrently with
+  // `stream` and is ordered after everything before fork() and before
+  // everything after join() (event edges; also valid under graph capture).
+  void fork() {
+    if (!aux) {
+      tgb::cuda_check(cudaStreamCreateWithFlags(&aux, cudaStreamNonBlocking), "aux stream");
+      tgb::cuda_check(cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming), "event");
+      tgb::cuda_check(cudaEventCreateWithFlags(&ev_join, cudaEventDisableTiming), "event");
+    }
+    tgb::cuda_check(cudaEventRecord(ev_fork, stream), "fork record");
+    tgb::cuda_check(cudaStreamWaitEvent(aux, ev_fork, 0), "fork wait");
+  }
+  void join() {
+    tgb::cuda_check(cudaEventRecord(ev_join, aux), "join record");
+    tgb::cuda_check(cudaStreamWaitEvent(stream, ev_join, 0), "join wait");
+  }
 
   // Grow-only scratch buffer bound to a slot. Stream-ordered reuse is safe
   // because every user of the context enqueues on `stream`.
@@ -188,4 +208,8 @@ __device__ __forceinline__ uint32_t warp_max_u32(uint32_t v) {
 
 // Validates a permutation (reorder.cpp:10-21); optionally writes its inverse (u32).
 void check_permutation(tg_ctx* ctx, const uint64_t* perm_dev, uint64_t n, uint32_t* inv_dev);
+// Rows [rb, re) of a u32 CSR ordered by length descending, ties by id (K3's
+// schedule). Stream-ordered; uses private temporaries, not scratch slots.
+void sort_rows_by_length(tg_ctx* ctx, const uint32_t* off, uint64_t rb, uint64_t re,
+                         uint32_t* order_dev);
 }  // namespace tgb

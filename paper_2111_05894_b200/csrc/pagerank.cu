@@ -31,20 +31,28 @@ struct tg_graph {
   uint64_t n = 0, e = 0;
   uint32_t* off = nullptr;     // n+1, u32
   uint32_t* tgt = nullptr;     // e, u32
-  uint32_t* hub = nullptr;     // rows longer than kHubLen, longest first
-  uint32_t n_hub = 0;
-  uint32_t max_row = 0;
   uint32_t* indeg = nullptr;   // in_degrees (csr_graph.cpp:89-93), built with the device graph
+  // K3 schedules: rows of [rb, re) by length descending (ties by id), split
+  // into the three row classes. [0, n) is built with the graph; row ranges
+  // of a partitioned (multi-GPU) run are built on first use.
+  struct Sched {
+    uint64_t rb, re;
+    uint32_t* order;
+    uint32_t nA, nB;  // order[0,nA): len > kLenA; [nA,nB): kLenB < len <= kLenA
+  };
+  std::vector<Sched> scheds;
 };
 
 namespace tgb {
 
-constexpr int kGroupRows = 32;
-constexpr uint32_t kHubLen = 2048;  // longer rows: one CTA each, warp-specialised
-constexpr int kPrWin = 256;         // edges staged per warp per window (light path)
-constexpr int kPrWarps = 8;         // warps per CTA
-constexpr int kHubSlot = 512;       // doubles per ring slot (hub path)
-constexpr int kHubSlots = 8;        // ring depth
+// K3 row classes (rows sorted by length at graph upload):
+//   A  len > kLenA          one CTA per row, exact parallel evaluation of the chain
+//   B  kLenB < len <= kLenA one warp per row: lanes stage 256-edge windows, lane 0 chains
+//   C  len <= kLenB         one thread per row (a warp's rows have near-equal lengths)
+constexpr uint32_t kLenA = 4096;
+constexpr uint32_t kLenB = 512;
+constexpr int kPrWin = 256;         // edges staged per warp per window (class B)
+constexpr int kPrWarps = 8;         // warps per CTA (classes B, C)
 
 // ------------------------------------------------------------ graph upload
 __global__ void narrow_offsets_kernel(const uint64_t* __restrict__ in, uint32_t* __restrict__ out,
@@ -72,14 +80,21 @@ __global__ void narrow_targets_kernel(const uint64_t* __restrict__ in, uint32_t*
   }
 }
 
-// Rows longer than kHubLen get a whole CTA each (hub path of K3).
-__global__ void hub_rows_kernel(const uint32_t* __restrict__ off, uint64_t n,
-                                uint32_t* __restrict__ hub, uint32_t* __restrict__ cnt) {
-  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
-       i += (uint64_t)gridDim.x * blockDim.x) {
-    const uint32_t len = off[i + 1] - off[i];
-    if (len > kHubLen) hub[atomicAdd(cnt, 1u)] = static_cast<uint32_t>(i);
-    if (len) atomicMax(cnt + 1, len);
+// Class boundaries of a length-sorted schedule (one thread; binary search).
+__global__ void class_bounds_kernel(const uint32_t* __restrict__ off,
+                                    const uint32_t* __restrict__ order, uint64_t m,
+                                    uint32_t* __restrict__ out) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  const uint32_t lim[2] = {kLenA, kLenB};
+  for (int c = 0; c < 2; ++c) {  // first index whose length is <= lim[c]
+    uint64_t lo = 0, hi = m;
+    while (lo < hi) {
+      const uint64_t mid = (lo + hi) / 2;
+      const uint32_t r = order[mid];
+      if (off[r + 1] - off[r] > lim[c]) lo = mid + 1;
+      else hi = mid;
+    }
+    out[c] = static_cast<uint32_t>(lo);
   }
 }
 
@@ -167,9 +182,9 @@ struct PrStepArgs {
   const double* norm_in;
   double* norm_out;
   double* score_out;
-  const uint32_t* hub;
-  uint32_t n_hub;
-  uint32_t group_begin, group_end;  // 32-row groups overlapping [row_begin,row_end)
+  const uint32_t* order;   // the range's rows by length, descending
+  uint32_t nA, nB, m;      // class boundaries in `order`, range size
+  uint32_t b_ctas;         // CTAs of class B (then class C)
   uint64_t row_begin, row_end;
   double base, damp;
   int last;
@@ -229,146 +244,389 @@ __device__ __forceinline__ double chain_add(double acc, const double* v, uint32_
   return acc;
 }
 
-// Hub path: one CTA per long row. Warps 1..7 stream the row's targets and
-// gather the normalized values into a ring of shared-memory slots; lane 0 of
-// warp 0 runs the single in-order DADD chain over the ring (mbarrier
-// full/empty handshake per slot).
-__device__ void hub_row(const PrStepArgs& a, uint32_t r, double* ring, uint64_t* full,
-                        uint64_t* empty) {
-  const uint32_t beg = a.off[r], len = a.off[r + 1] - beg;
-  const uint32_t chunks = (len + kHubSlot - 1) / kHubSlot;
-  const int tid = threadIdx.x;
-  if (tid == 0) {
-    for (int s = 0; s < kHubSlots; ++s) {
-      mbar_init(&full[s], kPrWarps * 32 - 32);
-      mbar_init(&empty[s], 1);
-    }
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  __syncthreads();
-  if (tid < 32) {
-    if (tid == 0) {
-      double acc = 0.0;  // scoring.cpp:67
-      for (uint32_t c = 0; c < chunks; ++c) {
-        const uint32_t s = c % kHubSlots;
-        mbar_wait(&full[s], (c / kHubSlots) & 1);
-        const uint32_t cnt = min(kHubSlot, len - c * kHubSlot);
-        acc = chain_add(acc, ring + s * kHubSlot, cnt);  // scoring.cpp:68, in order
-        mbar_arrive(&empty[s]);
-      }
-      finish_row(a, r, acc);
-    }
-  } else {
-    const int lt = tid - 32;
-    constexpr int kLoaders = kPrWarps * 32 - 32;
-    constexpr int kPer = (kHubSlot + kLoaders - 1) / kLoaders;
-    for (uint32_t c = 0; c < chunks; ++c) {
-      const uint32_t s = c % kHubSlots;
-      if (c >= kHubSlots) mbar_wait(&empty[s], ((c / kHubSlots) - 1) & 1);
-      const uint32_t base = beg + c * kHubSlot;
-      const uint32_t cnt = min(kHubSlot, len - c * kHubSlot);
-      uint32_t t[kPer];
-#pragma unroll
-      for (int k = 0; k < kPer; ++k) {
-        const uint32_t j = lt + k * kLoaders;
-        t[k] = j < cnt ? __ldg(a.tgt + base + j) : 0u;
-      }
-#pragma unroll
-      for (int k = 0; k < kPer; ++k) {
-        const uint32_t j = lt + k * kLoaders;
-        if (j < cnt) ring[s * kHubSlot + j] = __ldg(a.norm_in + t[k]);
-      }
-      mbar_arrive(&full[s]);
-    }
-  }
+// Hub path: one CTA per long row, with the row's strictly sequential sum
+//   acc = 0; for w in row: acc = RN(acc + norm[w])          (scoring.cpp:66-68)
+// evaluated EXACTLY, but in parallel, instead of as one serial DADD chain
+// (the chain costs 8 cycles per edge: 450 us for the 77k-edge row at C2).
+//
+// Why this is exact: all addends are finite and >= 0, so acc never decreases.
+// While acc stays inside one binade [2^E, 2^(E+1)) its grid step is
+// u = 2^(E-52), acc = m*u with integer m in [2^52, 2^53), and
+//   RN(m*u + x) = (m + X + t)*u,  X = floor(x/u),  f = x/u - X,
+//   t = 1 if f > 1/2, or f == 1/2 and (m + X) is odd (ties to even), else 0,
+// as long as the result stays below 2^(E+1) (m + X + t <= 2^53). So inside a
+// binade each addend contributes an integer increment that depends on the
+// running m only through its parity. An increment is a pair (d0, d1) — the
+// increment for incoming parity 0 and 1 — and pairs compose associatively:
+//   (F then G).d[p] = F.d[p] + G.d[p ^ (F.d[p] & 1)].
+// A block-wide scan of these pairs gives m after every addend. The first
+// addend that would leave the binade (m >= 2^53) is added with a real
+// __dadd_rn; the pass then restarts from the next addend in the new binade.
+// acc crosses a binade only O(log(sum / first)) times per row, mostly in its
+// first elements, so a 2048-element tile takes one or two passes.
+constexpr int kHubT = 8;                          // addends per thread per tile
+constexpr int kHubWarps = 16;                     // 512-thread CTA per hub row
+constexpr int kHubThreads = kHubWarps * 32;
+constexpr int kHubTile = kHubThreads * kHubT;     // 4096 addends, 32 KB of smem
+constexpr long long kTop = 1ll << 53;
+constexpr int kHubSerial = 256;                   // serial prefix at a row start
+
+struct QPair {
+  long long d0, d1;
+};
+
+__device__ __forceinline__ QPair q_compose(const QPair f, const QPair g) {
+  QPair c;  // saturate at 2^53: anything beyond only has to read as "crossed"
+  c.d0 = f.d0 >= kTop ? kTop : min(kTop, f.d0 + ((f.d0 & 1) ? g.d1 : g.d0));
+  c.d1 = f.d1 >= kTop ? kTop : min(kTop, f.d1 + ((f.d1 & 1) ? g.d0 : g.d1));
+  return c;
 }
 
-// Light path: a warp owns 32 consecutive rows; rows are processed in runs of
-// consecutive non-hub rows whose edges are contiguous. A run's edges stream
-// through 256-edge windows: coalesced target loads and value gathers staged
-// in shared memory (the next window's loads in flight while the lanes run the
-// current window's chains), then each lane adds its own row's slice in order.
-__device__ void light_group(const PrStepArgs& a, uint32_t group, double* buf) {
+__device__ __forceinline__ QPair q_shfl_up(const QPair v, int o) {
+  QPair r;
+  r.d0 = __shfl_up_sync(0xffffffffu, v.d0, o);
+  r.d1 = __shfl_up_sync(0xffffffffu, v.d1, o);
+  return r;
+}
+
+// x * 2^k exactly. Fast path: x normal and the result normal, so only the
+// exponent field moves. Otherwise two multiplications by normal powers of two
+// (an underflow only happens for x/u < 2^-1000, where "f < 1/2" is still
+// decided correctly; an overflow saturates to "crossed").
+__device__ __forceinline__ double scale_pow2(double x, int k) {
+  const long long xb = __double_as_longlong(x);
+  const int ex = static_cast<int>(xb >> 52);  // x >= 0
+  if (ex != 0 && ex + k > 0 && ex + k < 2047)
+    return __longlong_as_double(xb + (static_cast<long long>(k) << 52));
+  const int k1 = k / 2, k2 = k - k1;
+  const double f1 = __longlong_as_double(static_cast<long long>(k1 + 1023) << 52);
+  const double f2 = __longlong_as_double(static_cast<long long>(k2 + 1023) << 52);
+  return __dmul_rn(__dmul_rn(x, f1), f2);
+}
+
+// The increment pair of addend x in the binade with grid step 2^(E-52).
+// X = floor(x/u) and f = x/u - X without int<->fp conversions: for
+// 0 <= sc < 2^52, sc + 2^52 rounded toward zero is exactly 2^52 + floor(sc).
+__device__ __forceinline__ QPair q_of(double x, int E) {
+  const double sc = scale_pow2(x, 52 - E);
+  constexpr double k2p52 = 4503599627370496.0;
+  if (!(sc < 2.0 * k2p52)) return QPair{kTop, kTop};  // >= 2^53, inf or NaN
+  long long X;
+  double f;
+  if (sc < k2p52) {
+    const double y = __dadd_rz(sc, k2p52);
+    X = __double_as_longlong(y) & ((1ll << 52) - 1);
+    f = __dsub_rn(sc, __dsub_rn(y, k2p52));  // exact
+  } else {
+    X = (__double_as_longlong(sc) & ((1ll << 52) - 1)) | (1ll << 52);  // sc is an integer
+    f = 0.0;
+  }
+  const bool up = f > 0.5, tie = f == 0.5;
+  const long long odd = X & 1;
+  return QPair{X + ((up || (tie && odd)) ? 1 : 0), X + ((up || (tie && !odd)) ? 1 : 0)};
+}
+
+// Tie-free fast path: the increment of x when no addend of the pass sits
+// exactly on a half-step (then the parity of m never matters and the pairs
+// collapse to one integer). *tie reports a half-step; kTop = "crossed".
+__device__ __forceinline__ long long q_single(double x, int E, bool* tie) {
+  const double sc = scale_pow2(x, 52 - E);
+  constexpr double k2p52 = 4503599627370496.0;
+  if (!(sc < 2.0 * k2p52)) return kTop;
+  if (sc >= k2p52) return (__double_as_longlong(sc) & ((1ll << 52) - 1)) | (1ll << 52);
+  const double y = __dadd_rz(sc, k2p52);
+  const double f = __dsub_rn(sc, __dsub_rn(y, k2p52));
+  *tie |= f == 0.5;
+  return (__double_as_longlong(y) & ((1ll << 52) - 1)) + (f > 0.5 ? 1 : 0);
+}
+
+__device__ __forceinline__ long long sat_add(long long a, long long b) {
+  return min(a + b, kTop);  // a, b <= 2^53: no overflow
+}
+
+struct HubShared {
+  QPair wagg[kHubWarps];  // per-warp totals, then their exclusive prefixes
+  long long wsum[kHubWarps];  // tie-free path: the same for plain increments
+  long long wsum_tot;
+  QPair wtot;             // block total
+  int wfirst[kHubWarps];  // per-warp first crossing
+  double acc;
+};
+
+// Class A: one CTA per row longer than kLenA.
+__global__ void __launch_bounds__(kHubThreads) pr_hub_kernel(const PrStepArgs a) {
+  extern __shared__ __align__(16) double xs[];  // [kHubTile]
+  __shared__ HubShared sh;
+  const uint32_t r = a.order[blockIdx.x];  // class A
+  const uint32_t beg = a.off[r], len = a.off[r + 1] - beg;
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  double acc = 0.0;  // scoring.cpp:67 — identical in every thread
+  // software pipeline: this thread's 8 addends of the next tile
+  double x_next[kHubT];
+  auto load_tile = [&](uint32_t base) {
+    uint32_t t[kHubT];
+#pragma unroll
+    for (int k = 0; k < kHubT; ++k) {
+      const uint32_t j = base + tid * kHubT + k;
+      t[k] = j < len ? __ldg(a.tgt + beg + j) : 0u;
+    }
+#pragma unroll
+    for (int k = 0; k < kHubT; ++k) {
+      const uint32_t j = base + tid * kHubT + k;
+      x_next[k] = j < len ? __ldg(a.norm_in + t[k]) : 0.0;
+    }
+  };
+  load_tile(0);
+  for (uint32_t base = 0; base < len; base += kHubTile) {
+    const int cnt = static_cast<int>(len - base < (uint32_t)kHubTile ? len - base : (uint32_t)kHubTile);
+    double x[kHubT];
+#pragma unroll
+    for (int k = 0; k < kHubT; ++k) {
+      x[k] = x_next[k];
+      xs[tid * kHubT + k] = x[k];
+    }
+    if (base + kHubTile < len) load_tile(base + kHubTile);  // next tile in flight
+    __syncthreads();
+    int k0 = 0;  // first addend of this tile not yet in acc
+    while (k0 < cnt) {
+      if (acc == 0.0) {
+        // Row start (or an all-zero prefix): acc crosses binades every few
+        // addends here, so one thread runs the plain chain over the next 256.
+        if (tid == 0) {
+          const int stop = k0 + kHubSerial < cnt ? k0 + kHubSerial : cnt;
+          double s0 = 0.0;
+          for (int j = k0; j < stop; ++j) s0 = __dadd_rn(s0, xs[j]);  // scoring.cpp:68
+          sh.acc = s0;
+        }
+        __syncthreads();
+        acc = sh.acc;
+        k0 = k0 + kHubSerial < cnt ? k0 + kHubSerial : cnt;
+        __syncthreads();
+        continue;
+      }
+      const long long bits = __double_as_longlong(acc);
+      const int ef = static_cast<int>(bits >> 52);
+      const int E = ef ? ef - 1023 : -1022;
+      const long long m0 = (bits & ((1ll << 52) - 1)) | (ef ? (1ll << 52) : 0ll);
+      const int p0 = static_cast<int>(m0 & 1);
+      const long long room = kTop - m0;  // crossing when the increment reaches it
+      int mine = kHubTile;
+      long long before = 0;  // increment before this thread's first crossing
+      int jc = kHubTile;
+      long long total = 0;
+      // ---- tie-free fast path: plain saturating int64 prefix sums
+      bool tie = false;
+      long long inc[kHubT];
+      long long run1 = 0;
+#pragma unroll
+      for (int k = 0; k < kHubT; ++k) {
+        const int j = tid * kHubT + k;
+        if (j >= k0 && j < cnt) run1 = sat_add(run1, q_single(x[k], E, &tie));
+        inc[k] = run1;
+      }
+      long long v1 = run1;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const long long y = __shfl_up_sync(0xffffffffu, v1, o);
+        if (lane >= o) v1 = sat_add(y, v1);
+      }
+      if (lane == 31) sh.wsum[w] = v1;
+      const bool any_tie = __syncthreads_or(tie);
+      if (!any_tie) {
+        if (w == 0) {
+          long long vi = lane < kHubWarps ? sh.wsum[lane] : 0;
+#pragma unroll
+          for (int o = 1; o < 32; o <<= 1) {
+            const long long y = __shfl_up_sync(0xffffffffu, vi, o);
+            if (lane >= o) vi = sat_add(y, vi);
+          }
+          long long ex = __shfl_up_sync(0xffffffffu, vi, 1);
+          if (lane == 0) ex = 0;
+          if (lane < kHubWarps) sh.wsum[lane] = ex;
+          if (lane == kHubWarps - 1) sh.wsum_tot = vi;
+        }
+        __syncthreads();
+        long long ex1 = __shfl_up_sync(0xffffffffu, v1, 1);
+        if (lane == 0) ex1 = 0;
+        const long long pre1 = sat_add(sh.wsum[w], ex1);
+#pragma unroll
+        for (int k = 0; k < kHubT; ++k) {
+          const int j = tid * kHubT + k;
+          const long long c = sat_add(pre1, inc[k]);
+          if (mine == kHubTile && j >= k0 && j < cnt && c >= room) {
+            mine = j;
+            before = k ? sat_add(pre1, inc[k - 1]) : pre1;
+          }
+        }
+        total = sh.wsum_tot;
+      } else {
+      // ---- general path: parity-dependent increment pairs (ties to even)
+      QPair run{0, 0};
+#pragma unroll
+      for (int k = 0; k < kHubT; ++k) {
+        const int j = tid * kHubT + k;
+        if (j >= k0 && j < cnt) run = q_compose(run, q_of(x[k], E));
+      }
+      // warp inclusive scan, then warp 0 scans the warp totals
+      QPair v = run;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const QPair y = q_shfl_up(v, o);
+        if (lane >= o) v = q_compose(y, v);
+      }
+      if (lane == 31) sh.wagg[w] = v;
+      __syncthreads();
+      if (w == 0) {
+        const QPair t = lane < kHubWarps ? sh.wagg[lane] : QPair{0, 0};
+        QPair vi = t;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const QPair y = q_shfl_up(vi, o);
+          if (lane >= o) vi = q_compose(y, vi);
+        }
+        QPair ex = q_shfl_up(vi, 1);
+        if (lane == 0) ex = QPair{0, 0};
+        if (lane < kHubWarps) sh.wagg[lane] = ex;
+        if (lane == kHubWarps - 1) sh.wtot = vi;
+      }
+      __syncthreads();
+      QPair excl = q_shfl_up(v, 1);
+      if (lane == 0) excl = QPair{0, 0};
+      const QPair pre = q_compose(sh.wagg[w], excl);
+      // m after each addend; this thread's first addend that leaves the binade
+      {
+        QPair c = pre;
+#pragma unroll
+        for (int k = 0; k < kHubT; ++k) {
+          const int j = tid * kHubT + k;
+          if (mine == kHubTile && j >= k0 && j < cnt) {
+            const long long b = p0 ? c.d1 : c.d0;
+            c = q_compose(c, q_of(x[k], E));
+            if ((p0 ? c.d1 : c.d0) >= room) {
+              mine = j;
+              before = b;
+            }
+          }
+        }
+      }
+      total = p0 ? sh.wtot.d1 : sh.wtot.d0;
+      }
+      // first crossing: crossings are monotone in the addend index, so it is
+      // the lowest crossing lane of the lowest warp that has one
+      const unsigned cm = __ballot_sync(0xffffffffu, mine < kHubTile);
+      const int first_mine = __shfl_sync(0xffffffffu, mine, cm ? __ffs(cm) - 1 : 0);
+      if (lane == 0) sh.wfirst[w] = cm ? first_mine : kHubTile;
+      __syncthreads();
+#pragma unroll
+      for (int ww = 0; ww < kHubWarps; ++ww) jc = min(jc, sh.wfirst[ww]);
+      const double u = (E - 52) >= -1022
+                           ? __longlong_as_double(static_cast<long long>(E - 52 + 1023) << 52)
+                           : __longlong_as_double(1ll << (E - 52 + 1074));
+      if (jc == kHubTile) {
+        // no crossing: acc = (m0 + total) * u exactly; every thread computes it
+        acc = __dmul_rn(static_cast<double>(m0 + total), u);
+        k0 = cnt;
+      } else {
+        // the owner of addend jc: exact value before it, then one real DADD
+        if (mine == jc) {
+          const double prev = __dmul_rn(static_cast<double>(m0 + before), u);
+          sh.acc = __dadd_rn(prev, xs[jc]);  // scoring.cpp:68
+        }
+        __syncthreads();
+        acc = sh.acc;
+        k0 = jc + 1;
+      }
+      __syncthreads();
+    }
+  }
+  if (tid == 0) finish_row(a, r, acc);
+}
+
+// Class B: one warp per row. Lanes stream the row's targets in 256-edge
+// windows (coalesced), gather the normalized values into shared memory (the
+// next window's gathers and the window after's targets in flight), and lane
+// 0 adds each window in storage order.
+__device__ __forceinline__ void warp_row(const PrStepArgs& a, uint32_t r, double* buf) {
   const int lane = threadIdx.x & 31;
-  const uint64_t r = (uint64_t)group * kGroupRows + lane;
-  const bool in_range = r >= a.row_begin && r < a.row_end;
-  uint32_t beg = 0, end = 0;
-  if (in_range) {
-    beg = a.off[r];
-    end = a.off[r + 1];
+  const uint32_t beg = a.off[r], len = a.off[r + 1] - beg;
+  constexpr int K = kPrWin / 32;
+  uint32_t t1[K];
+  double v[K];
+#pragma unroll
+  for (int k = 0; k < K; ++k) {
+    const uint32_t e = k * 32 + lane;
+    t1[k] = e < len ? __ldg(a.tgt + beg + e) : 0xffffffffu;
   }
-  const bool hub = in_range && end - beg > kHubLen;
-  const bool mine = in_range && !hub;
-  const uint32_t hub_mask = __ballot_sync(0xffffffffu, hub);
-  const uint32_t mine_mask = __ballot_sync(0xffffffffu, mine);
+#pragma unroll
+  for (int k = 0; k < K; ++k) v[k] = t1[k] != 0xffffffffu ? __ldg(a.norm_in + t1[k]) : 0.0;
+#pragma unroll
+  for (int k = 0; k < K; ++k) {
+    const uint32_t e = kPrWin + k * 32 + lane;
+    t1[k] = e < len ? __ldg(a.tgt + beg + e) : 0xffffffffu;
+  }
   double acc = 0.0;  // scoring.cpp:67
-  uint32_t todo = mine_mask;
-  while (todo) {
-    // run = lanes [first, stop) with no hub row in between
-    const int first = __ffs(todo) - 1;
-    const uint32_t later_hubs = hub_mask & ~((2u << first) - 1u);
-    const int stop = later_hubs ? __ffs(later_hubs) - 1 : 32;
-    const uint32_t run = todo & (stop == 32 ? ~0u : ((1u << stop) - 1u));
-    todo &= ~run;
-    const int last_lane = 31 - __clz(run);
-    const uint32_t span_b = __shfl_sync(0xffffffffu, beg, first);
-    const uint32_t span_e = __shfl_sync(0xffffffffu, end, last_lane);
-    const bool in_run = (run >> lane) & 1u;
-    constexpr int K = kPrWin / 32;
-    uint32_t t1[K];
-    double v[K];
-    // prologue: window 0 values, window 1 targets
+  for (uint32_t wb = 0; wb < len; wb += kPrWin) {
+#pragma unroll
+    for (int k = 0; k < K; ++k) buf[k * 32 + lane] = v[k];
+    __syncwarp();
+    double vn[K];
+#pragma unroll
+    for (int k = 0; k < K; ++k) vn[k] = t1[k] != 0xffffffffu ? __ldg(a.norm_in + t1[k]) : 0.0;
 #pragma unroll
     for (int k = 0; k < K; ++k) {
-      const uint32_t e = span_b + k * 32 + lane;
-      t1[k] = e < span_e ? __ldg(a.tgt + e) : 0xffffffffu;
+      const uint32_t e = wb + 2 * kPrWin + k * 32 + lane;
+      t1[k] = e < len ? __ldg(a.tgt + beg + e) : 0xffffffffu;
     }
+    if (lane == 0) acc = chain_add(acc, buf, len - wb < (uint32_t)kPrWin ? len - wb : kPrWin);
+    __syncwarp();
 #pragma unroll
-    for (int k = 0; k < K; ++k) v[k] = t1[k] != 0xffffffffu ? __ldg(a.norm_in + t1[k]) : 0.0;
-#pragma unroll
-    for (int k = 0; k < K; ++k) {
-      const uint32_t e = span_b + kPrWin + k * 32 + lane;
-      t1[k] = e < span_e ? __ldg(a.tgt + e) : 0xffffffffu;
-    }
-    for (uint32_t wb = span_b; wb < span_e; wb += kPrWin) {
-#pragma unroll
-      for (int k = 0; k < K; ++k) buf[k * 32 + lane] = v[k];
-      __syncwarp();
-      // next window's gathers and the one after's targets go in flight now
-      double vn[K];
-#pragma unroll
-      for (int k = 0; k < K; ++k) vn[k] = t1[k] != 0xffffffffu ? __ldg(a.norm_in + t1[k]) : 0.0;
-#pragma unroll
-      for (int k = 0; k < K; ++k) {
-        const uint32_t e = wb + 2 * kPrWin + k * 32 + lane;
-        t1[k] = e < span_e ? __ldg(a.tgt + e) : 0xffffffffu;
-      }
-      if (in_run) {
-        const uint32_t lo = beg > wb ? beg : wb;
-        const uint32_t hi = end < wb + kPrWin ? end : wb + kPrWin;
-        if (hi > lo) acc = chain_add(acc, buf + (lo - wb), hi - lo);  // in order
-      }
-      __syncwarp();
-#pragma unroll
-      for (int k = 0; k < K; ++k) v[k] = vn[k];
-    }
+    for (int k = 0; k < K; ++k) v[k] = vn[k];
   }
-  if (mine) finish_row(a, r, acc);
+  if (lane == 0) finish_row(a, r, acc);
+}
+
+// Class C: one thread per row of at most kLenB edges, in storage order. A
+// warp's 32 rows have near-equal lengths (length-sorted schedule), so the
+// lanes stay converged; 8 gathers per lane are in flight per step.
+__device__ __forceinline__ void thread_row(const PrStepArgs& a, uint32_t r) {
+  const uint32_t beg = a.off[r], len = a.off[r + 1] - beg;
+  const uint32_t* t = a.tgt + beg;
+  double acc = 0.0;  // scoring.cpp:67
+  uint32_t k = 0;
+  for (; k + 8 <= len; k += 8) {
+    uint32_t ti[8];
+    double v[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) ti[q] = __ldg(t + k + q);
+#pragma unroll
+    for (int q = 0; q < 8; ++q) v[q] = __ldg(a.norm_in + ti[q]);
+#pragma unroll
+    for (int q = 0; q < 8; ++q) acc = __dadd_rn(acc, v[q]);
+  }
+  if (k < len) {
+    uint32_t ti[8];
+    double v[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) ti[q] = k + q < len ? __ldg(t + k + q) : 0u;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) v[q] = k + q < len ? __ldg(a.norm_in + ti[q]) : 0.0;
+#pragma unroll
+    for (int q = 0; q < 8; ++q)
+      if (k + q < len) acc = __dadd_rn(acc, v[q]);
+  }
+  finish_row(a, r, acc);
 }
 
 __global__ void __launch_bounds__(kPrWarps * 32) pr_step_kernel(const PrStepArgs a) {
-  __shared__ __align__(16) double smem[kHubSlots * kHubSlot];  // 32 KB: hub ring / light windows
-  __shared__ uint64_t bars[2 * kHubSlots];
-  static_assert(kPrWarps * kPrWin <= kHubSlots * kHubSlot, "light windows must fit");
-  if (blockIdx.x < a.n_hub) {  // hub CTAs first: their chains start earliest
-    const uint32_t r = a.hub[blockIdx.x];
-    if (r >= a.row_begin && r < a.row_end) hub_row(a, r, smem, bars, bars + kHubSlots);
-    return;
+  __shared__ __align__(16) double smem[kPrWarps * kPrWin];  // 16 KB: class B windows
+  if (blockIdx.x < a.b_ctas) {
+    const int w = threadIdx.x >> 5;
+    const uint64_t i = a.nA + (uint64_t)blockIdx.x * kPrWarps + w;
+    if (i < a.nB) warp_row(a, a.order[i], smem + w * kPrWin);
+  } else {
+    const uint64_t i = a.nB + (uint64_t)(blockIdx.x - a.b_ctas) * blockDim.x + threadIdx.x;
+    if (i < a.m) thread_row(a, a.order[i]);
   }
-  const int w = threadIdx.x >> 5;
-  const uint64_t g = a.group_begin + (uint64_t)(blockIdx.x - a.n_hub) * kPrWarps + w;
-  if (g >= a.group_end) return;
-  light_group(a, static_cast<uint32_t>(g), smem + w * kPrWin);
 }
 
 unsigned long long read_flag(tg_ctx* ctx, unsigned long long* dflag) {
@@ -408,10 +666,30 @@ void pagerank_prepare(tg_ctx* ctx, const tg_graph* g, const uint64_t* tid_dev, u
   TGB_LAUNCHED();
 }
 
+const tg_graph::Sched& schedule(tg_ctx* ctx, const tg_graph* g, uint64_t rb, uint64_t re) {
+  auto& v = const_cast<tg_graph*>(g)->scheds;
+  for (const auto& sc : v)
+    if (sc.rb == rb && sc.re == re) return sc;
+  tg_graph::Sched sc{rb, re, nullptr, 0, 0};
+  TGB_CUDA(cudaMalloc(&sc.order, sizeof(uint32_t) * std::max<uint64_t>(re - rb, 1) + 8));
+  sort_rows_by_length(ctx, g->off, rb, re, sc.order);
+  uint32_t* bounds = sc.order + std::max<uint64_t>(re - rb, 1);
+  class_bounds_kernel<<<1, 32, 0, ctx->stream>>>(g->off, sc.order, re - rb, bounds);
+  TGB_LAUNCHED();
+  uint32_t hb[2];
+  TGB_CUDA(cudaMemcpyAsync(hb, bounds, sizeof(hb), cudaMemcpyDeviceToHost, ctx->stream));
+  ctx->sync();  // once per (graph, range)
+  sc.nA = hb[0];
+  sc.nB = hb[1];
+  v.push_back(sc);
+  return v.back();
+}
+
 void pagerank_step(tg_ctx* ctx, const tg_graph* g, const uint32_t* deg, double damp,
                    const double* nin, double* nout, double* sout, uint64_t rb, uint64_t re,
                    int last) {
   if (re <= rb) return;
+  const tg_graph::Sched& sc = schedule(ctx, g, rb, re);
   PrStepArgs a;
   a.off = g->off;
   a.tgt = g->tgt;
@@ -419,19 +697,35 @@ void pagerank_step(tg_ctx* ctx, const tg_graph* g, const uint32_t* deg, double d
   a.norm_in = nin;
   a.norm_out = nout;
   a.score_out = sout;
-  a.hub = g->hub;
-  a.n_hub = g->n_hub;
-  a.group_begin = static_cast<uint32_t>(rb / kGroupRows);
-  a.group_end = static_cast<uint32_t>((re + kGroupRows - 1) / kGroupRows);
+  a.order = sc.order;
+  a.nA = sc.nA;
+  a.nB = sc.nB;
+  a.m = static_cast<uint32_t>(re - rb);
+  a.b_ctas = (sc.nB - sc.nA + kPrWarps - 1) / kPrWarps;
   a.row_begin = rb;
   a.row_end = re;
   a.base = (1.0 - damp) / static_cast<double>(g->n);  // scoring.cpp:53
   a.damp = damp;
   a.last = last;
-  const uint64_t light = (a.group_end - a.group_begin + kPrWarps - 1) / kPrWarps;
-  const unsigned grid = static_cast<unsigned>(a.n_hub + light);
-  pr_step_kernel<<<grid, kPrWarps * 32, 0, ctx->stream>>>(a);
-  TGB_LAUNCHED();
+  const uint64_t c_ctas = (a.m - sc.nB + kPrWarps * 32 - 1) / (kPrWarps * 32);
+  if (sc.nA) {
+    // class A on the side stream, concurrently with classes B and C
+    static bool attr[TG_MAX_DEVICES] = {};  // a function attribute is per device
+    if (!attr[ctx->device % TG_MAX_DEVICES]) {
+      TGB_CUDA(cudaFuncSetAttribute(pr_hub_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    kHubTile * 8));
+      attr[ctx->device % TG_MAX_DEVICES] = true;
+    }
+    ctx->fork();
+    pr_hub_kernel<<<sc.nA, kHubThreads, kHubTile * 8, ctx->aux>>>(a);
+    TGB_LAUNCHED();
+  }
+  const unsigned grid = static_cast<unsigned>(a.b_ctas + c_ctas);
+  if (grid) {
+    pr_step_kernel<<<grid, kPrWarps * 32, 0, ctx->stream>>>(a);
+    TGB_LAUNCHED();
+  }
+  if (sc.nA) ctx->join();
 }
 
 void check_config(uint32_t iterations, double damp) {  // scoring.cpp:42-47
@@ -522,34 +816,7 @@ int tg_graph_create(tg_ctx* ctx, const uint64_t* offsets, const uint64_t* target
                      " (need offsets[0]==0, monotone, offsets[num_nodes]==num_edges)");
       if (hb[1] != ~0ull)
         format_error("csr: target out of range at edge " + std::to_string(hb[1]));
-      // hub rows (one CTA each in K3), longest first
-      TGB_CUDA(cudaMalloc(&g->hub, sizeof(uint32_t) * (std::max<uint64_t>(n, 1) + 2)));
-      uint32_t* cnt = g->hub + std::max<uint64_t>(n, 1);
-      TGB_CUDA(cudaMemsetAsync(cnt, 0, 2 * sizeof(uint32_t), ctx->stream));
-      if (n) {
-        hub_rows_kernel<<<grid_for(n, 256), 256, 0, ctx->stream>>>(g->off, n, g->hub, cnt);
-        TGB_LAUNCHED();
-      }
-      uint32_t hc[2];
-      TGB_CUDA(cudaMemcpyAsync(hc, cnt, sizeof(hc), cudaMemcpyDeviceToHost, ctx->stream));
-      ctx->sync();
-      g->n_hub = hc[0];
-      g->max_row = hc[1];
-      if (g->n_hub) {
-        std::vector<uint32_t> rows(g->n_hub), offs(n + 1);
-        TGB_CUDA(cudaMemcpy(rows.data(), g->hub, 4 * rows.size(), cudaMemcpyDeviceToHost));
-        std::vector<std::pair<uint32_t, uint32_t>> lens;
-        for (uint32_t r : rows) {
-          uint32_t o2[2];
-          TGB_CUDA(cudaMemcpy(o2, g->off + r, 8, cudaMemcpyDeviceToHost));
-          lens.push_back({o2[1] - o2[0], r});
-        }
-        std::sort(lens.begin(), lens.end(), [](auto x, auto y) {
-          return x.first != y.first ? x.first > y.first : x.second < y.second;
-        });
-        for (size_t i = 0; i < lens.size(); ++i) rows[i] = lens[i].second;
-        TGB_CUDA(cudaMemcpy(g->hub, rows.data(), 4 * rows.size(), cudaMemcpyHostToDevice));
-      }
+      if (n) schedule(ctx, g, 0, n);  // K3 schedule of the whole graph
       TGB_CUDA(cudaMalloc(&g->indeg, sizeof(uint32_t) * std::max<uint64_t>(n, 1)));
       compute_indeg(ctx, g, g->indeg);
       ctx->sync();
@@ -565,7 +832,7 @@ int tg_graph_destroy(tg_graph* g) {
   if (!g) return TG_OK;
   cudaFree(g->off);
   cudaFree(g->tgt);
-  cudaFree(g->hub);
+  for (auto& sc : g->scheds) cudaFree(sc.order);
   cudaFree(g->indeg);
   delete g;
   return TG_OK;

@@ -217,6 +217,84 @@ __global__ void perm_kernel(const uint32_t* __restrict__ v0, const uint32_t* __r
   }
 }
 
+// K3 schedule: keys = ~len (u32 in a u64 key) of rows [rb, rb+m), vals = the
+// row's offset in the range. Ascending keys = descending lengths; the sort is
+// stable, so equal lengths keep ascending ids.
+__global__ void __launch_bounds__(256) rowlen_key_kernel(const uint32_t* __restrict__ off,
+                                                         uint64_t rb, uint64_t m,
+                                                         uint64_t* __restrict__ keys,
+                                                         uint32_t* __restrict__ vals,
+                                                         uint32_t* __restrict__ hist) {
+  __shared__ uint32_t h[4][256];
+  for (int i = threadIdx.x; i < 4 * 256; i += blockDim.x) (&h[0][0])[i] = 0;
+  __syncthreads();
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < m;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t k = ~(off[rb + i + 1] - off[rb + i]);
+    keys[i] = k;
+    vals[i] = static_cast<uint32_t>(i);
+#pragma unroll
+    for (int p = 0; p < 4; ++p) atomicAdd(&h[p][(k >> (8 * p)) & 0xff], 1u);
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < 4 * 256; i += blockDim.x) {
+    const uint32_t c = (&h[0][0])[i];
+    if (c) atomicAdd(hist + i, c);
+  }
+  // digits 4..7 of every key are 0: one full bin each
+  if (blockIdx.x == 0)
+    for (int p = 4 + threadIdx.x; p < 8; p += blockDim.x) hist[p * 256] = static_cast<uint32_t>(m);
+}
+
+__global__ void order_out_kernel(const uint32_t* __restrict__ v0, const uint32_t* __restrict__ v1,
+                                 const RadixPlan* __restrict__ plan, uint64_t rb, uint64_t m,
+                                 uint32_t* __restrict__ order) {
+  const uint32_t* v = plan->final_src ? v1 : v0;
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < m;
+       i += (uint64_t)gridDim.x * blockDim.x)
+    order[i] = static_cast<uint32_t>(rb + v[i]);
+}
+
+void sort_rows_by_length(tg_ctx* ctx, const uint32_t* off, uint64_t rb, uint64_t re,
+                         uint32_t* order_dev) {
+  const uint64_t m = re - rb;
+  if (m == 0) return;
+  const uint32_t nblk = static_cast<uint32_t>((m + kRsTile - 1) / kRsTile);
+  // private temporaries (stream-ordered allocations): callers may hold the
+  // context's scratch slots across this call
+  const size_t bytes = 2 * 8 * m + 2 * 4 * m + 4ull * 256 * nblk + 64 + sizeof(RadixPlan) +
+                       8 * 256 * 4 + 256;
+  char* base = nullptr;
+  TGB_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&base), bytes, ctx->stream));
+  auto align = [](char* p) { return reinterpret_cast<char*>((reinterpret_cast<uintptr_t>(p) + 15) & ~uintptr_t(15)); };
+  char* p = base;
+  uint64_t* k0 = reinterpret_cast<uint64_t*>(p); p = align(p + 8 * m);
+  uint64_t* k1 = reinterpret_cast<uint64_t*>(p); p = align(p + 8 * m);
+  uint32_t* v0 = reinterpret_cast<uint32_t*>(p); p = align(p + 4 * m);
+  uint32_t* v1 = reinterpret_cast<uint32_t*>(p); p = align(p + 4 * m);
+  uint32_t* counts = reinterpret_cast<uint32_t*>(p); p = align(p + 4ull * 256 * nblk);
+  auto* plan = reinterpret_cast<RadixPlan*>(p); p = align(p + sizeof(RadixPlan));
+  uint32_t* hist = reinterpret_cast<uint32_t*>(p);
+  TGB_CUDA(cudaMemsetAsync(hist, 0, 8 * 256 * 4, ctx->stream));
+  rowlen_key_kernel<<<grid_for(m, 256, ctx->num_sms * 8), 256, 0, ctx->stream>>>(off, rb, m, k0,
+                                                                                v0, hist);
+  TGB_LAUNCHED();
+  plan_kernel<<<1, 32, 0, ctx->stream>>>(hist, m, plan);
+  TGB_LAUNCHED();
+  for (int pass = 0; pass < 4; ++pass) {  // digits 4..7 are constant: planned as skipped
+    digit_count_kernel<<<nblk, kRsWarps * 32, 0, ctx->stream>>>(k0, k1, m, pass, plan, counts, nblk);
+    TGB_LAUNCHED();
+    count_scan_kernel<<<1, 1024, 0, ctx->stream>>>(counts, (uint64_t)256 * nblk, pass, plan);
+    TGB_LAUNCHED();
+    scatter_kernel<<<nblk, kRsWarps * 32, 0, ctx->stream>>>(k0, v0, k1, v1, m, pass, plan, counts,
+                                                             nblk);
+    TGB_LAUNCHED();
+  }
+  order_out_kernel<<<grid_for(m, 256), 256, 0, ctx->stream>>>(v0, v1, plan, rb, m, order_dev);
+  TGB_LAUNCHED();
+  TGB_CUDA(cudaFreeAsync(base, ctx->stream));
+}
+
 // Sorts scores -> (order, new_id_of). Either output may be null. Device pointers.
 void sort_scores(tg_ctx* ctx, const double* scores_dev, uint64_t n, uint64_t* order_dev,
                  uint64_t* perm_dev) {

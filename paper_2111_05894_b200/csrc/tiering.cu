@@ -283,9 +283,12 @@ template <typename V, bool PF = false>
 __global__ void __launch_bounds__(256) gather_kernel(GatherTable t, const uint64_t* __restrict__ ids,
                                                      uint64_t n, uint8_t* __restrict__ dst,
                                                      uint32_t B, uint32_t C, uint64_t* counters,
-                                                     unsigned long long* err) {
+                                                     unsigned long long* err, uint32_t spread) {
   const int lane = threadIdx.x & 31;
-  const uint64_t warp = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
+  // spread: consecutive batches go to different CTAs (so the cold batches,
+  // taken first, are issued from every SM rather than the first few CTAs)
+  const uint64_t warp = spread ? (threadIdx.x >> 5) * (uint64_t)gridDim.x + blockIdx.x
+                               : (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
   const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
   uint64_t cl = 0, cp = 0, ch = 0;
   // Batches run from the END of the id list: minibatch lists are sorted, so
@@ -368,7 +371,7 @@ __device__ __forceinline__ void mbar_wait_s(uint32_t bar, uint32_t parity) {
 
 __global__ void __launch_bounds__(kBulkWarps * 32) gather_bulk_kernel(
     GatherTable t, const uint64_t* __restrict__ ids, uint64_t n, uint8_t* __restrict__ dst,
-    uint32_t B, uint32_t Rpad, uint64_t* counters, unsigned long long* err) {
+    uint32_t B, uint32_t Rpad, uint64_t* counters, unsigned long long* err, uint32_t spread) {
   extern __shared__ __align__(128) uint8_t bulk_smem[];  // [warps][2][kBulkStage]
   __shared__ __align__(8) uint64_t bars[kBulkWarps][2];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
@@ -383,7 +386,8 @@ __global__ void __launch_bounds__(kBulkWarps * 32) gather_bulk_kernel(
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncwarp();
-  const uint64_t warp = (uint64_t)blockIdx.x * kBulkWarps + w;
+  const uint64_t warp = spread ? (uint64_t)w * gridDim.x + blockIdx.x
+                               : (uint64_t)blockIdx.x * kBulkWarps + w;
   const uint64_t nwarps = (uint64_t)gridDim.x * kBulkWarps;
   const uint64_t nb = (n + B - 1) / B;
   const uint32_t R = static_cast<uint32_t>(t.R);
@@ -746,6 +750,7 @@ void launch_gather(tg_store* s, const uint64_t* ids_dev, uint64_t n, void* dst_d
     if (!s->inter[d]) domain_error("tiered store: peer slice of device " + std::to_string(d) +
                                    " is not attached (tg_store_set_peer)");
   const GatherTable t = make_table(s);
+  const uint32_t spread = (s->flags & TG_GATHER_SPREAD) ? 1u : 0u;
   uint64_t align = reinterpret_cast<uint64_t>(dst_dev) | reinterpret_cast<uint64_t>(s->local) |
                    reinterpret_cast<uint64_t>(s->cold_dev) | s->cold_stride;
   for (uint32_t d = 0; d < s->L.num_devices; ++d) align |= reinterpret_cast<uint64_t>(s->inter[d]);
@@ -757,14 +762,14 @@ void launch_gather(tg_store* s, const uint64_t* ids_dev, uint64_t n, void* dst_d
     const uint64_t warps = (n + B - 1) / B;
     const unsigned grid = grid_for(warps * 32, kBulkWarps * 32, ctx->num_sms * 2);
     constexpr int kSmem = kBulkWarps * 2 * kBulkStage;
-    static bool attr = false;
-    if (!attr) {
+    static bool attr[TG_MAX_DEVICES] = {};  // a function attribute is per device
+    if (!attr[ctx->device % TG_MAX_DEVICES]) {
       TGB_CUDA(cudaFuncSetAttribute(gather_bulk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     kSmem));
-      attr = true;
+      attr[ctx->device % TG_MAX_DEVICES] = true;
     }
     gather_bulk_kernel<<<grid, kBulkWarps * 32, kSmem, ctx->stream>>>(t, ids_dev, n, dst, B, Rpad,
-                                                                      counters3, err);
+                                                                      counters3, err, spread);
     TGB_LAUNCHED();
     return;
   }
@@ -773,16 +778,16 @@ void launch_gather(tg_store* s, const uint64_t* ids_dev, uint64_t n, void* dst_d
   const uint64_t warps = (n + B - 1) / B;
   const unsigned grid = grid_for(warps * 32, 256, ctx->num_sms * 8);
   if ((s->flags & TG_GATHER_L2PF) && w == 16) {
-    gather_kernel<uint4, true><<<grid, 256, 0, ctx->stream>>>(t, ids_dev, n, dst, B, C, counters3, err);
+    gather_kernel<uint4, true><<<grid, 256, 0, ctx->stream>>>(t, ids_dev, n, dst, B, C, counters3, err, spread);
     TGB_LAUNCHED();
     return;
   }
   switch (w) {
-    case 16: gather_kernel<uint4><<<grid, 256, 0, ctx->stream>>>(t, ids_dev, n, dst, B, C, counters3, err); break;
-    case 8: gather_kernel<uint2><<<grid, 256, 0, ctx->stream>>>(t, ids_dev, n, dst, B, C, counters3, err); break;
-    case 4: gather_kernel<uint32_t><<<grid, 256, 0, ctx->stream>>>(t, ids_dev, n, dst, B, C, counters3, err); break;
-    case 2: gather_kernel<uint16_t><<<grid, 256, 0, ctx->stream>>>(t, ids_dev, n, dst, B, C, counters3, err); break;
-    default: gather_kernel<uint8_t><<<grid, 256, 0, ctx->stream>>>(t, ids_dev, n, dst, B, C, counters3, err); break;
+    case 16: gather_kernel<uint4><<<grid, 256, 0, ctx->stream>>>(t, ids_dev, n, dst, B, C, counters3, err, spread); break;
+    case 8: gather_kernel<uint2><<<grid, 256, 0, ctx->stream>>>(t, ids_dev, n, dst, B, C, counters3, err, spread); break;
+    case 4: gather_kernel<uint32_t><<<grid, 256, 0, ctx->stream>>>(t, ids_dev, n, dst, B, C, counters3, err, spread); break;
+    case 2: gather_kernel<uint16_t><<<grid, 256, 0, ctx->stream>>>(t, ids_dev, n, dst, B, C, counters3, err, spread); break;
+    default: gather_kernel<uint8_t><<<grid, 256, 0, ctx->stream>>>(t, ids_dev, n, dst, B, C, counters3, err, spread); break;
   }
   TGB_LAUNCHED();
 }

@@ -20,7 +20,7 @@ from typing import Iterable, Optional, Sequence
 import numpy as np
 
 from ._lib import (LIB, TG_COLD_INDIRECT, TG_COLD_PAD128, TG_COLD_REORDERED, TG_GATHER_BULK,
-                   TG_GATHER_L2PF, TgLayout, TgLocation, TgReport)
+                   TG_GATHER_L2PF, TG_GATHER_SPREAD, TgLayout, TgLocation, TgReport)
 
 __all__ = [
     "TierGraphError", "DomainError", "FormatError", "IoError", "Context", "default_context",
@@ -608,7 +608,10 @@ class TieredFeatureStore:
         flags = {"reordered": TG_COLD_REORDERED, "indirect": TG_COLD_INDIRECT}[cold_mode]
         if pad128:
             flags |= TG_COLD_PAD128
-        flags |= {"ldg": 0, "bulk": TG_GATHER_BULK, "l2pf": TG_GATHER_L2PF}[gather_mode]
+        # gather_mode: "ldg" | "bulk" | "l2pf", optionally "+spread"
+        for tok in gather_mode.split("+"):
+            flags |= {"ldg": 0, "bulk": TG_GATHER_BULK, "l2pf": TG_GATHER_L2PF,
+                      "spread": TG_GATHER_SPREAD}[tok]
         h = C.c_void_p()
         _check(LIB.tg_store_create(self.ctx.h, C.byref(layout._c()), int(device_index), flags,
                                    C.byref(h)))

@@ -42,7 +42,7 @@ def main():
     ref_out = None
     for hot in (cfg["hot"], 0.0, 1.0):
         lay = tg.plan_layout(n, hot, 0.0, 1, cfg["dim"], cfg["elem"])
-        for mode in ("ldg", "l2pf", "bulk"):
+        for mode in ("ldg", "ldg+spread", "bulk", "bulk+spread"):
             for pad in (False, True):
                 st = tg.TieredFeatureStore(feat, perm, lay, ctx=ctx, gather_mode=mode, pad128=pad)
                 out = torch.empty((maxu, R), dtype=torch.uint8, device=dev)
@@ -67,7 +67,7 @@ def main():
                 if ref_out is None or mode == "ldg" and not pad:
                     ref_out = check
                 ok = np.array_equal(check, ref_out)
-                print(f"hot={hot:.2f} mode={mode:5s} pad128={pad!s:5s} "
+                print(f"hot={hot:.2f} mode={mode:11s} pad128={pad!s:5s} "
                       f"avg {np.mean(ms)*1e3:8.1f} us  min {np.min(ms)*1e3:8.1f} us  "
                       f"{u * R / (sum(ms) * 1e-3) / 1e9:8.1f} GB/s  match={ok}", flush=True)
                 st.close()

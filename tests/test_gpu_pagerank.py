@@ -172,3 +172,24 @@ def test_rmat_c1_scale_bit_exact_and_hot_set(tg, ctx):
     assert got.tobytes() == want.tobytes()
     perm = tg.permutation_from_scores(got)
     assert np.array_equal(perm.new_id_of, port.permutation_from_scores(want))
+
+
+def test_hub_rows_with_tie_prone_addends(tg, ctx):
+    """Hub rows (> 2048 edges, the parallel exact-chain path) whose addends are
+    all equal or few-valued, so the running sum hits round-half-even ties and
+    binade crossings at many points: still bit-identical to the serial sum."""
+    chk = checker()
+    port = oracle.port()
+    n = 3 * 2 ** 15
+    src = [np.zeros(60000, np.uint64), np.ones(n - 60001, np.uint64),
+           np.full(5000, 2, np.uint64)]
+    dst = [np.arange(1, 60001, dtype=np.uint64), np.arange(60001, n, dtype=np.uint64),
+           np.random.default_rng(4).choice(n, 5000, replace=False).astype(np.uint64)]
+    off, tgt = port.from_edge_list(n, np.concatenate(src), np.concatenate(dst))
+    g = G(tg, off, tgt)
+    for tid in (np.arange(0, n, 3, dtype=np.uint64), np.arange(n, dtype=np.uint64)):
+        for it in (1, 2, 5):
+            a = tg.weighted_reverse_pagerank(g, tg.PagerankConfig(it, 0.85), tg.TrainIdSet(tid))
+            assert a.tobytes() == chk.weighted_reverse_pagerank(off, tgt, tid, it, 0.85).tobytes()
+    a = tg.reverse_pagerank(g, tg.PagerankConfig(3, 0.5))
+    assert a.tobytes() == chk.reverse_pagerank(off, tgt, 3, 0.5).tobytes()
