@@ -77,7 +77,11 @@ struct tg_ctx {
   // everything after join() (event edges; also valid under graph capture).
   void fork() {
     if (!aux) {
-      tgb::cuda_check(cudaStreamCreateWithFlags(&aux, cudaStreamNonBlocking), "aux stream");
+      // highest priority: the side stream carries the critical-path work
+      // (e.g. K3's longest rows), so its CTAs are scheduled first
+      int lo = 0, hi = 0;
+      tgb::cuda_check(cudaDeviceGetStreamPriorityRange(&lo, &hi), "priority range");
+      tgb::cuda_check(cudaStreamCreateWithPriority(&aux, cudaStreamNonBlocking, hi), "aux stream");
       tgb::cuda_check(cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming), "event");
       tgb::cuda_check(cudaEventCreateWithFlags(&ev_join, cudaEventDisableTiming), "event");
     }

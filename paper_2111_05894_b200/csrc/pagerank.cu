@@ -542,47 +542,58 @@ __global__ void __launch_bounds__(kHubThreads) pr_hub_kernel(const PrStepArgs a)
   if (tid == 0) finish_row(a, r, acc);
 }
 
-// Class B: one warp per row. Lanes stream the row's targets in 256-edge
-// windows (coalesced), gather the normalized values into shared memory (the
-// next window's gathers and the window after's targets in flight), and lane
-// 0 adds each window in storage order.
-__device__ __forceinline__ void warp_row(const PrStepArgs& a, uint32_t r, double* buf) {
-  const int lane = threadIdx.x & 31;
-  const uint32_t beg = a.off[r], len = a.off[r + 1] - beg;
-  constexpr int K = kPrWin / 32;
+// Class B: 8 lanes per row (4 rows per warp, near-equal lengths). The 8
+// lanes stream their row's targets in 64-edge windows (32 B coalesced per
+// row), gather the normalized values into shared memory with the next
+// window's gathers and the window after's targets in flight, and the group's
+// first lane adds each window in storage order — 4 chains per warp.
+constexpr int kBLanes = 8;
+constexpr int kBWin = kBLanes * 8;  // 64 edges per window
+__device__ __forceinline__ void group_row(const PrStepArgs& a, int64_t i, double* buf) {
+  const int lane = threadIdx.x & 31, sl = lane & (kBLanes - 1);
+  const bool has = i < static_cast<int64_t>(a.nB);
+  const uint32_t r = has ? a.order[i] : 0u;
+  const uint32_t beg = has ? a.off[r] : 0u;
+  const uint32_t len = has ? a.off[r + 1] - beg : 0u;
+  constexpr int K = kBWin / kBLanes;  // 8 per lane per window
   uint32_t t1[K];
   double v[K];
 #pragma unroll
   for (int k = 0; k < K; ++k) {
-    const uint32_t e = k * 32 + lane;
+    const uint32_t e = k * kBLanes + sl;
     t1[k] = e < len ? __ldg(a.tgt + beg + e) : 0xffffffffu;
   }
 #pragma unroll
   for (int k = 0; k < K; ++k) v[k] = t1[k] != 0xffffffffu ? __ldg(a.norm_in + t1[k]) : 0.0;
 #pragma unroll
   for (int k = 0; k < K; ++k) {
-    const uint32_t e = kPrWin + k * 32 + lane;
+    const uint32_t e = kBWin + k * kBLanes + sl;
     t1[k] = e < len ? __ldg(a.tgt + beg + e) : 0xffffffffu;
   }
-  double acc = 0.0;  // scoring.cpp:67
-  for (uint32_t wb = 0; wb < len; wb += kPrWin) {
+  // the warp loops until its longest row is done (lengths are near-equal)
+  uint32_t wmax = len;
 #pragma unroll
-    for (int k = 0; k < K; ++k) buf[k * 32 + lane] = v[k];
+  for (int o = 16; o; o >>= 1) wmax = max(wmax, __shfl_xor_sync(0xffffffffu, wmax, o));
+  double acc = 0.0;  // scoring.cpp:67
+  for (uint32_t wb = 0; wb < wmax; wb += kBWin) {
+#pragma unroll
+    for (int k = 0; k < K; ++k) buf[k * kBLanes + sl] = v[k];
     __syncwarp();
     double vn[K];
 #pragma unroll
     for (int k = 0; k < K; ++k) vn[k] = t1[k] != 0xffffffffu ? __ldg(a.norm_in + t1[k]) : 0.0;
 #pragma unroll
     for (int k = 0; k < K; ++k) {
-      const uint32_t e = wb + 2 * kPrWin + k * 32 + lane;
+      const uint32_t e = wb + 2 * kBWin + k * kBLanes + sl;
       t1[k] = e < len ? __ldg(a.tgt + beg + e) : 0xffffffffu;
     }
-    if (lane == 0) acc = chain_add(acc, buf, len - wb < (uint32_t)kPrWin ? len - wb : kPrWin);
+    if (sl == 0 && wb < len)
+      acc = chain_add(acc, buf, len - wb < (uint32_t)kBWin ? len - wb : kBWin);  // in order
     __syncwarp();
 #pragma unroll
     for (int k = 0; k < K; ++k) v[k] = vn[k];
   }
-  if (lane == 0) finish_row(a, r, acc);
+  if (has && sl == 0) finish_row(a, r, acc);
 }
 
 // Class C: one thread per row of at most kLenB edges, in storage order. A
@@ -593,11 +604,14 @@ __device__ __forceinline__ void thread_row(const PrStepArgs& a, uint32_t r) {
   const uint32_t* t = a.tgt + beg;
   double acc = 0.0;  // scoring.cpp:67
   uint32_t k = 0;
+  // peel to a 16 B boundary, then two 16 B target loads per 8 edges
+  const uint32_t peel = min(len, (4u - (beg & 3u)) & 3u);
+  for (; k < peel; ++k) acc = __dadd_rn(acc, __ldg(a.norm_in + __ldg(t + k)));
   for (; k + 8 <= len; k += 8) {
-    uint32_t ti[8];
+    const uint4 q0 = __ldg(reinterpret_cast<const uint4*>(t + k));
+    const uint4 q1 = __ldg(reinterpret_cast<const uint4*>(t + k + 4));
+    const uint32_t ti[8] = {q0.x, q0.y, q0.z, q0.w, q1.x, q1.y, q1.z, q1.w};
     double v[8];
-#pragma unroll
-    for (int q = 0; q < 8; ++q) ti[q] = __ldg(t + k + q);
 #pragma unroll
     for (int q = 0; q < 8; ++q) v[q] = __ldg(a.norm_in + ti[q]);
 #pragma unroll
@@ -618,11 +632,11 @@ __device__ __forceinline__ void thread_row(const PrStepArgs& a, uint32_t r) {
 }
 
 __global__ void __launch_bounds__(kPrWarps * 32) pr_step_kernel(const PrStepArgs a) {
-  __shared__ __align__(16) double smem[kPrWarps * kPrWin];  // 16 KB: class B windows
+  __shared__ __align__(16) double smem[kPrWarps * 32 / kBLanes * kBWin];  // 16 KB: class B windows
   if (blockIdx.x < a.b_ctas) {
-    const int w = threadIdx.x >> 5;
-    const uint64_t i = a.nA + (uint64_t)blockIdx.x * kPrWarps + w;
-    if (i < a.nB) warp_row(a, a.order[i], smem + w * kPrWin);
+    const int g = threadIdx.x / kBLanes;  // row group within the CTA
+    const int64_t i = a.nA + (int64_t)blockIdx.x * (kPrWarps * 32 / kBLanes) + g;
+    group_row(a, i, smem + g * kBWin);
   } else {
     const uint64_t i = a.nB + (uint64_t)(blockIdx.x - a.b_ctas) * blockDim.x + threadIdx.x;
     if (i < a.m) thread_row(a, a.order[i]);
@@ -701,7 +715,8 @@ void pagerank_step(tg_ctx* ctx, const tg_graph* g, const uint32_t* deg, double d
   a.nA = sc.nA;
   a.nB = sc.nB;
   a.m = static_cast<uint32_t>(re - rb);
-  a.b_ctas = (sc.nB - sc.nA + kPrWarps - 1) / kPrWarps;
+  constexpr uint32_t kRowsPerCta = kPrWarps * 32 / kBLanes;
+  a.b_ctas = (sc.nB - sc.nA + kRowsPerCta - 1) / kRowsPerCta;
   a.row_begin = rb;
   a.row_end = re;
   a.base = (1.0 - damp) / static_cast<double>(g->n);  // scoring.cpp:53
