@@ -32,7 +32,9 @@ struct TieredStoreOptions {
   // permutation (no second host copy, PAPER.md:659-668 cudaHostRegister).
   bool cold_indirect = false;
   // Pad cold rows to a 128-byte stride (whole PCIe read requests).
-  bool pad128 = false;
+  bool pad128 = true;
+  // K8 through TMA bulk copies staged in shared memory (else 16 B loads).
+  bool bulk = true;
 };
 
 class TieredFeatureStore {

@@ -1,0 +1,117 @@
+"""Multi-GPU reverse PageRank: row-partitioned K3 + all-gather of `norm`.
+
+SURVEY §8(e): each rank owns one contiguous block of rows. Every Jacobi step
+(reference `run_iterations`, scoring.cpp:50-74) computes `norm_out` (or, on
+the last step, the scores) for the rank's rows only, then the blocks are
+exchanged with one all-gather (NCCL over NVLink/NVSwitch on GPUs) so every
+rank holds the full `norm` vector for the next step. A row's sum never
+leaves its rank, so the result is bit-identical to the single-GPU run and to
+the reference for any number of ranks (the reference's guarantee for any
+worker count, parallel.hpp:5-7).
+
+The driver is written against a small "stepper" interface so that the
+partitioning and exchange logic runs unchanged over gloo in the CPU tests
+(tests/test_distributed.py); the product stepper, `DeviceStepper`, launches
+this library's kernels through the C-ABI (tg_pagerank_prepare_async /
+tg_pagerank_step_async) and has no CPU path.
+"""
+from __future__ import annotations
+
+import math
+from typing import Optional, Tuple
+
+import numpy as np
+
+
+def row_blocks(n: int, world: int) -> Tuple[int, list]:
+    """Equal row blocks, block r = [r*chunk, min(n, (r+1)*chunk)). Equal sizes
+    let the exchange be one in-place all_gather_into_tensor (padding < world
+    rows)."""
+    chunk = max(1, math.ceil(n / max(world, 1)))
+    return chunk, [(min(n, r * chunk), min(n, (r + 1) * chunk)) for r in range(world)]
+
+
+class DeviceStepper:
+    """K1-K3 of one rank on its GPU, through the C-ABI."""
+
+    def __init__(self, g, ctx):
+        import torch
+        from . import tiergraph as tg
+        self.torch = torch
+        self.tg = tg
+        self.ctx = ctx
+        self.g = g
+        self.gh = g.device(ctx)
+        self.n = g.num_nodes()
+        self.dev = torch.device("cuda", ctx.device)
+        self.deg = torch.empty(max(self.n, 1), dtype=torch.int32, device=self.dev)
+
+    def alloc(self, count: int):
+        return self.torch.empty(count, dtype=self.torch.float64, device=self.dev)
+
+    def prepare(self, tid_dev, ntid: int, norm0) -> None:
+        from ._lib import LIB
+        self.tg._check(LIB.tg_pagerank_prepare_async(
+            self.ctx.h, self.gh, tid_dev.data_ptr() if tid_dev is not None else None, ntid,
+            self.deg.data_ptr(), norm0.data_ptr()))
+
+    def step(self, damp: float, nin, nout, sout, rb: int, re: int, last: bool) -> None:
+        from ._lib import LIB
+        self.tg._check(LIB.tg_pagerank_step_async(
+            self.ctx.h, self.gh, self.deg.data_ptr(), float(damp), nin.data_ptr(),
+            nout.data_ptr(), sout.data_ptr(), int(rb), int(re), int(last)))
+
+    def sync(self) -> None:
+        self.ctx.sync()
+
+
+def reverse_pagerank_partitioned(stepper, n: int, iterations: int, damp: float, tid=None,
+                                 ntid: int = 0, group=None):
+    """Runs the recurrence with rows split over the ranks of `group` and
+    returns the full score vector (length n) on every rank.
+
+    `tid` (a device tensor of train ids, or None for the unweighted
+    recurrence) must be the same on every rank.
+    """
+    import torch.distributed as dist
+    if iterations < 1:
+        from .tiergraph import DomainError
+        raise DomainError("pagerank: iterations must be >= 1")  # scoring.cpp:43-44
+    world = dist.get_world_size(group) if dist.is_initialized() else 1
+    rank = dist.get_rank(group) if dist.is_initialized() else 0
+    chunk, blocks = row_blocks(n, world)
+    rb, re = blocks[rank]
+    padded = chunk * world
+    a = stepper.alloc(padded)
+    b = stepper.alloc(padded)
+    scores = stepper.alloc(padded)
+    # norm0 for every row (cheap, identical on every rank: no exchange needed)
+    stepper.prepare(tid, ntid, a)
+    x, y = a, b
+    for it in range(iterations):
+        last = it + 1 == iterations
+        stepper.step(damp, x, y, scores, rb, re, last)
+        out = scores if last else y
+        if world > 1:
+            stepper.sync()  # the step must land before the collective reads it
+            dist.all_gather_into_tensor(out, out[rank * chunk:(rank + 1) * chunk], group=group)
+        x, y = y, x
+    stepper.sync()
+    return scores[:n]
+
+
+def weighted_reverse_pagerank_multi(g, cfg, tid, ctx=None, group=None):
+    """scoring.hpp:45-46 on all ranks of `group` (one GPU per rank)."""
+    import torch
+    from . import tiergraph as tg
+    ctx = ctx or tg.default_context()
+    ids = tid.ids if isinstance(tid, tg.TrainIdSet) else tid
+    if ids is None or len(ids) == 0:
+        raise tg.DomainError("weighted reverse pagerank needs a non-empty train id set; "
+                             "use reverse_pagerank when no nodes are labeled")  # scoring.cpp:89-91
+    if not (0.0 < cfg.damp < 1.0):
+        raise tg.DomainError(f"pagerank: damp must lie in (0,1), got {cfg.damp}")
+    st = DeviceStepper(g, ctx)
+    tid_d = torch.as_tensor(np.asarray(ids, np.uint64).astype(np.int64), device=st.dev)
+    return reverse_pagerank_partitioned(st, g.num_nodes(), cfg.iterations, cfg.damp, tid_d,
+                                        len(ids), group)

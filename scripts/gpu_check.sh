@@ -14,6 +14,6 @@ timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --lo
    python bench.py --steps 20 --warmup 3 --no-cpu-baseline > $O/bench_ncu.log 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:gather -s 5 -c 2 \
    -o $O/gather python bench.py --steps 10 --warmup 3 --no-cpu-baseline > $O/ncu_gather.log 2>&1
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:pr_step -s 5 -c 2 \
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:pr_ -s 6 -c 2 \
    -o $O/prstep python bench.py --steps 5 --warmup 3 --no-cpu-baseline > $O/ncu_pr.log 2>&1
 ls -la $O

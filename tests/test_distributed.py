@@ -1,0 +1,124 @@
+"""The multi-GPU decomposition, exercised over gloo on CPU (world_size 2 and 3).
+
+paper_2111_05894_b200/distributed.py partitions the rows, runs one step per
+rank and exchanges `norm` blocks with all_gather_into_tensor. Here the same
+driver runs with a CPU stepper that restates the reference arithmetic
+(scoring.cpp:59-70: IEEE division, left-to-right row sums, separately rounded
+update — test infrastructure only), and the gathered scores must be
+bit-identical to the reference build / C restatement for every rank count.
+The GPU stepper is covered by tests/test_gpu_pagerank.py
+(row-partitioned steps) and by the single-GPU multi-rank run below.
+"""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+import oracle
+from paper_2111_05894_b200 import distributed as D
+
+
+class CpuStepper:
+    def __init__(self, off, tgt):
+        self.off = off.astype(np.int64)
+        self.tgt = tgt.astype(np.int64)
+        self.n = len(off) - 1
+        self.deg = np.bincount(self.tgt, minlength=self.n).astype(np.int64)
+
+    def alloc(self, count):
+        return torch.zeros(count, dtype=torch.float64)
+
+    def prepare(self, tid, ntid, norm0):
+        n = self.n
+        s = [1.0 / n] * n  # scoring.cpp:96
+        if tid is not None:
+            w = n / ntid  # scoring.cpp:94-95
+            for i in tid.tolist():
+                s[i] = s[i] * w
+        for j in range(n):
+            norm0[j] = s[j] / max(int(self.deg[j]), 1)  # :59-61
+
+    def step(self, damp, nin, nout, sout, rb, re, last):
+        base = (1.0 - damp) / self.n  # :53
+        x = nin.tolist()
+        for r in range(rb, re):
+            acc = 0.0
+            for w in self.tgt[self.off[r]:self.off[r + 1]]:
+                acc += x[w]  # :66-68, in storage order
+            nx = base + damp * acc  # :69 (two roundings, no FMA)
+            if last:
+                sout[r] = nx
+            else:
+                nout[r] = nx / max(int(self.deg[r]), 1)
+
+    def sync(self):
+        pass
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, off, tgt, tid, iters, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        st = CpuStepper(off, tgt)
+        t = None if tid is None else torch.as_tensor(tid.astype(np.int64))
+        out = D.reverse_pagerank_partitioned(st, len(off) - 1, iters, 0.85, t,
+                                             0 if tid is None else len(tid))
+        q.put((rank, out.numpy().tobytes()))
+    finally:
+        dist.destroy_process_group()
+
+
+def _run(world, off, tgt, tid, iters):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, off, tgt, tid, iters, q))
+             for r in range(world)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=300) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    return res
+
+
+def test_row_blocks_cover_and_pad():
+    for n in (0, 1, 5, 31, 32, 1000, 1001):
+        for world in (1, 2, 3, 8):
+            chunk, blocks = D.row_blocks(n, world)
+            assert chunk * world >= n and (n == 0 or chunk * world - n < world)
+            rows = [r for b in blocks for r in range(*b)]
+            assert rows == list(range(n))
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_partitioned_pagerank_over_gloo_is_bit_exact(world):
+    port = oracle.port()
+    chk = oracle.ref() or port
+    n = 157
+    rng = np.random.default_rng(world)
+    src = np.concatenate([rng.integers(0, n, 900), np.zeros(120, np.int64)]).astype(np.uint64)
+    dst = np.concatenate([rng.integers(0, n, 900), rng.integers(0, n, 120)]).astype(np.uint64)
+    off, tgt = port.from_edge_list(n, src, dst)
+    tid = port.draw_random_train_ids(n, 30, 7)
+    for iters in (1, 5):
+        res = _run(world, off, tgt, tid, iters)
+        want = chk.weighted_reverse_pagerank(off, tgt, tid, iters, 0.85).tobytes()
+        assert all(v == want for v in res.values()), f"world={world} iters={iters}"
+    res = _run(world, off, tgt, None, 3)
+    want = chk.reverse_pagerank(off, tgt, 3, 0.85).tobytes()
+    assert all(v == want for v in res.values())

@@ -114,7 +114,8 @@ def _virtual_devices(tg, ctx, features, perm, lay, **kw):
 @pytest.mark.parametrize("dim,eb", [(100, 4), (128, 4), (768, 2), (9, 4), (3, 1), (1, 8), (2048, 4)])
 @pytest.mark.parametrize("cold_mode,pad", [("reordered", False), ("indirect", False),
                                            ("reordered", True)])
-def test_store_gather_bit_exact(tg, ctx, dim, eb, cold_mode, pad):
+@pytest.mark.parametrize("mode", ["ldg", "bulk", "bulk+spread", "l2pf+spread"])
+def test_store_gather_bit_exact(tg, ctx, dim, eb, cold_mode, pad, mode):
     chk, port = checker(), oracle.port()
     n = 3000
     rng = np.random.default_rng(dim * eb)
@@ -124,7 +125,8 @@ def test_store_gather_bit_exact(tg, ctx, dim, eb, cold_mode, pad):
     for D, hot, rep in ((1, 0.2, 0.0), (2, 0.3, 0.05), (3, 0.5, 0.1), (4, 1.0, 0.0),
                         (6, 0.37, 0.2), (2, 0.0, 0.0)):
         lay = tg.plan_layout(n, hot, rep, D, dim, eb)
-        stores = _virtual_devices(tg, ctx, feat, perm, lay, cold_mode=cold_mode, pad128=pad)
+        stores = _virtual_devices(tg, ctx, feat, perm, lay, cold_mode=cold_mode, pad128=pad,
+                                  gather_mode=mode)
         ids = np.sort(rng.choice(n, size=700, replace=False)).astype(np.uint64)
         ids = np.concatenate([ids, rng.integers(0, n, 50).astype(np.uint64)])  # duplicates too
         for d, s in enumerate(stores):

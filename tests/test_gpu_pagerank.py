@@ -193,3 +193,17 @@ def test_hub_rows_with_tie_prone_addends(tg, ctx):
             assert a.tobytes() == chk.weighted_reverse_pagerank(off, tgt, tid, it, 0.85).tobytes()
     a = tg.reverse_pagerank(g, tg.PagerankConfig(3, 0.5))
     assert a.tobytes() == chk.reverse_pagerank(off, tgt, 3, 0.5).tobytes()
+
+
+def test_partitioned_driver_single_rank_on_device(tg, ctx):
+    """distributed.weighted_reverse_pagerank_multi (DeviceStepper) without a
+    process group equals the single call bit for bit."""
+    from paper_2111_05894_b200 import distributed as D
+    port = oracle.port()
+    n = 20000
+    off, tgt = _hub_graph(n, [(0, 9000), (5, 3000)], 21)
+    g = G(tg, off, tgt)
+    tid = port.draw_random_train_ids(n, 2000, 4)
+    want = tg.weighted_reverse_pagerank(g, tg.PagerankConfig(), tg.TrainIdSet(tid))
+    got = D.weighted_reverse_pagerank_multi(g, tg.PagerankConfig(), tg.TrainIdSet(tid), ctx=ctx)
+    assert got.cpu().numpy().tobytes() == want.tobytes()
