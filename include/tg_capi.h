@@ -283,6 +283,26 @@ int tg_epoch_minibatches(const uint64_t* gt_off, const uint64_t* gt_tgt, uint64_
                          uint64_t max_batches, int threads, uint64_t** out_off, uint64_t* out_nb,
                          uint64_t** out_ids);
 
+/* ------------------------------------------- GPU minibatch sampling (§8f)
+ * sampling.cpp:35-90 build_minibatch on the device, bit-identical member
+ * lists. `gt` is the TRANSPOSED graph (row v = in-neighbours of v, rows in
+ * the reference transpose's order, csr_graph.cpp:67-80), uploaded with
+ * tg_graph_create. The sampler owns per-node stamp arrays (2 x 4n bytes).
+ * tg_sample_minibatch: seeds (host|device, ns >= 1, < n) expanded through
+ * fanouts[0..nf) with BatchRng{rng_seed, epoch, batch}; writes the sorted
+ * unique members to out (host|device, capacity cap) and their count to
+ * *out_n (also set when cap is too small, with TG_ERR_DOMAIN). */
+typedef struct tg_sampler tg_sampler;
+int tg_sampler_create(tg_ctx* ctx, const tg_graph* gt, tg_sampler** out);
+int tg_sampler_destroy(tg_sampler* s);
+int tg_sample_minibatch(tg_sampler* s, const uint64_t* seeds, uint64_t ns, const uint32_t* fanouts,
+                        uint32_t nf, uint64_t rng_seed, uint64_t epoch, uint64_t batch,
+                        uint64_t* out, uint64_t cap, uint64_t* out_n);
+/* sampling.cpp:106-109: the epoch's shuffled train-id order (Fisher-Yates,
+ * key {0x5348, epoch}); batch b is order[b*batch_size ..). Host arrays. */
+int tg_epoch_order(const uint64_t* tid, uint64_t ntid, uint64_t rng_seed, uint64_t epoch,
+                   uint64_t* out);
+
 #ifdef __cplusplus
 }
 #endif

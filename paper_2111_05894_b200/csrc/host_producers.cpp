@@ -180,6 +180,15 @@ int tg_transpose_host(const uint64_t* off, const uint64_t* tgt, uint64_t n, uint
   return TG_OK;
 }
 
+int tg_epoch_order(const uint64_t* tid, uint64_t ntid, uint64_t seed, uint64_t epoch,
+                   uint64_t* out) {
+  std::memcpy(out, tid, sizeof(uint64_t) * ntid);
+  const uint64_t sc[2] = {0x5348ull, epoch};  // sampling.cpp:108
+  Rng sh{stream_key(seed, sc, 2)};
+  for (size_t i = ntid; i > 1; --i) std::swap(out[i - 1], out[sh.below(i)]);  // rng.hpp:67-73
+  return TG_OK;
+}
+
 int tg_epoch_minibatches(const uint64_t* gt_off, const uint64_t* gt_tgt, uint64_t n,
                          const uint64_t* tid, uint64_t ntid, const uint32_t* fanouts, uint32_t nf,
                          uint64_t batch_size, uint64_t seed, uint64_t epoch, uint64_t first_batch,

@@ -1,0 +1,345 @@
+// GPU GraphSAGE minibatch expansion — SURVEY §8(f) row 1, the producer of
+// the tiered gather's node-id lists, moved onto the device.
+//
+// Reference: proj/src/sampling.cpp:35-90 (BatchRng streams,
+// sample_in_neighbors, build_minibatch) over proj/include/tiergraph/rng.hpp
+// (mix64, derive_stream_key, counter-based RngStream, Lemire next_below) and
+// proj/src/rng.cpp:8-40 (Floyd's k-subset).
+//
+// Bit-identical member lists by construction: every node's draws come from
+// its own stream keyed by (seed, 0x534D, epoch, batch, layer, node), so the
+// SET a node samples does not depend on the order frontier nodes are
+// visited. The device therefore needs no sorts:
+//   * a layer's frontier is the de-duplicated set of the previous layer's
+//     samples: a per-node stamp array (atomicExch(stamp) != stamp admits a
+//     node once per layer) appends it to the next frontier in any order;
+//   * the members (seeds + every frontier) carry a per-minibatch stamp, and
+//     the final sorted unique list is a compaction of the stamped nodes in
+//     node-id order — sorted for free.
+// One thread per frontier node runs Floyd's algorithm exactly as rng.cpp does
+// (membership among the picks already emitted; the reference switches from a
+// linear scan to a hash set above 64 picks, which yields the same set).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "internal.cuh"
+
+namespace tgb {
+
+__device__ __forceinline__ uint64_t dmix64(uint64_t x) {  // rng.hpp:13-18
+  x += 0x9E3779B97F4A7C15ull;
+  x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ull;
+  x = (x ^ (x >> 27)) * 0x94D049BB133111EBull;
+  return x ^ (x >> 31);
+}
+
+struct DevRng {  // rng.hpp:32-59
+  uint64_t s;
+  __device__ uint64_t next() { return dmix64(s++); }
+  __device__ uint64_t below(uint64_t bound) {  // Lemire multiply-shift with rejection
+    uint64_t x = next();
+    uint64_t lo = x * bound, hi = __umul64hi(x, bound);
+    if (lo < bound) {
+      const uint64_t t = (0 - bound) % bound;
+      while (lo < t) {
+        x = next();
+        lo = x * bound;
+        hi = __umul64hi(x, bound);
+      }
+    }
+    return hi;
+  }
+};
+
+struct SampleArgs {
+  const uint32_t* off;  // transposed graph (row v = in-neighbours of v)
+  const uint32_t* tgt;
+  const uint32_t* frontier;
+  uint32_t f;
+  uint32_t fanout;
+  uint64_t key_base;  // mix64(seed ^ IV) folded with {0x534D, epoch, batch, layer}
+  uint32_t* picks;    // f x fanout scratch for Floyd's membership test
+  uint32_t* layer_mark;
+  uint32_t layer_stamp;
+  uint32_t* member_mark;
+  uint32_t member_stamp;
+  uint32_t* next;
+  uint32_t* next_count;
+};
+
+__device__ __forceinline__ void admit(const SampleArgs& a, uint32_t u) {
+  if (atomicExch(a.layer_mark + u, a.layer_stamp) != a.layer_stamp) {
+    a.next[atomicAdd(a.next_count, 1u)] = u;
+    a.member_mark[u] = a.member_stamp;
+  }
+}
+
+// sampling.cpp:39-54 + rng.cpp:8-40 for one frontier node per thread.
+__global__ void __launch_bounds__(256) sample_layer_kernel(const SampleArgs a) {
+  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= a.f) return;
+  const uint32_t v = a.frontier[i];
+  const uint32_t b = a.off[v], deg = a.off[v + 1] - b;
+  if (deg <= a.fanout) {  // all in-neighbours
+    for (uint32_t p = 0; p < deg; ++p) admit(a, a.tgt[b + p]);
+    return;
+  }
+  DevRng rng{dmix64(a.key_base ^ dmix64(v))};  // derive_stream_key(..., node)
+  uint32_t* picks = a.picks + static_cast<uint64_t>(i) * a.fanout;
+  uint32_t cnt = 0;
+  for (uint64_t j = deg - a.fanout; j < deg; ++j) {
+    const uint32_t t = static_cast<uint32_t>(rng.below(j + 1));
+    bool seen = false;
+    for (uint32_t q = 0; q < cnt; ++q) seen |= picks[q] == t;
+    const uint32_t p = seen ? static_cast<uint32_t>(j) : t;
+    picks[cnt++] = p;
+    admit(a, a.tgt[b + p]);
+  }
+}
+
+__global__ void seed_kernel(const uint64_t* __restrict__ seeds, uint64_t ns, uint64_t n,
+                            uint32_t* layer_mark, uint32_t stamp, uint32_t* member_mark,
+                            uint32_t mstamp, uint32_t* frontier, uint32_t* count,
+                            unsigned long long* bad) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < ns;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t s = seeds[i];
+    if (s >= n) {
+      atomicMin(bad, (unsigned long long)i);
+      continue;
+    }
+    const uint32_t u = static_cast<uint32_t>(s);
+    if (atomicExch(layer_mark + u, stamp) != stamp) {
+      frontier[atomicAdd(count, 1u)] = u;
+      member_mark[u] = mstamp;
+    }
+  }
+}
+
+// members = stamped nodes in id order: per-block counts, then positions.
+constexpr int kCompactBlock = 1024;
+__global__ void __launch_bounds__(kCompactBlock) member_count_kernel(const uint32_t* __restrict__ mark,
+                                                                     uint64_t n, uint32_t stamp,
+                                                                     uint32_t* __restrict__ counts) {
+  const uint64_t i = blockIdx.x * (uint64_t)kCompactBlock + threadIdx.x;
+  const int c = __syncthreads_count(i < n && mark[i] == stamp);
+  if (threadIdx.x == 0) counts[blockIdx.x] = c;
+}
+
+__global__ void __launch_bounds__(1024) count_prefix_kernel(uint32_t* __restrict__ counts,
+                                                            uint32_t m, uint32_t* total) {
+  __shared__ uint32_t part[1024];
+  const uint32_t per = (m + 1023) / 1024;
+  const uint32_t b = threadIdx.x * per, e = min(m, b + per);
+  uint32_t s = 0;
+  for (uint32_t i = b; i < e; ++i) s += counts[i];
+  part[threadIdx.x] = s;
+  __syncthreads();
+  for (int o = 1; o < 1024; o <<= 1) {
+    const uint32_t y = threadIdx.x >= o ? part[threadIdx.x - o] : 0;
+    __syncthreads();
+    part[threadIdx.x] += y;
+    __syncthreads();
+  }
+  uint32_t run = part[threadIdx.x] - s;
+  for (uint32_t i = b; i < e; ++i) {
+    const uint32_t c = counts[i];
+    counts[i] = run;
+    run += c;
+  }
+  if (threadIdx.x == 1023) *total = part[1023];
+}
+
+__global__ void __launch_bounds__(kCompactBlock) member_write_kernel(const uint32_t* __restrict__ mark,
+                                                                     uint64_t n, uint32_t stamp,
+                                                                     const uint32_t* __restrict__ base,
+                                                                     uint64_t* __restrict__ out) {
+  __shared__ uint32_t wsum[kCompactBlock / 32];
+  const uint64_t i = blockIdx.x * (uint64_t)kCompactBlock + threadIdx.x;
+  const bool on = i < n && mark[i] == stamp;
+  const unsigned bal = __ballot_sync(0xffffffffu, on);
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  if (lane == 0) wsum[w] = __popc(bal);
+  __syncthreads();
+  uint32_t before = 0;
+  for (int k = 0; k < w; ++k) before += wsum[k];
+  if (on) out[base[blockIdx.x] + before + __popc(bal & ((1u << lane) - 1u))] = i;
+}
+
+uint64_t host_mix64(uint64_t x) {
+  x += 0x9E3779B97F4A7C15ull;
+  x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ull;
+  x = (x ^ (x >> 27)) * 0x94D049BB133111EBull;
+  return x ^ (x >> 31);
+}
+
+}  // namespace tgb
+
+using namespace tgb;
+
+struct tg_sampler {
+  tg_ctx* ctx = nullptr;
+  const uint32_t* off = nullptr;
+  const uint32_t* tgt = nullptr;
+  uint64_t n = 0;
+  uint32_t* layer_mark = nullptr;   // n
+  uint32_t* member_mark = nullptr;  // n
+  uint32_t* buf[2] = {nullptr, nullptr};
+  uint64_t buf_cap = 0;
+  uint32_t* picks = nullptr;
+  uint64_t picks_cap = 0;
+  uint32_t* small = nullptr;  // counters
+  uint32_t* blk = nullptr;    // compaction block counts
+  uint32_t stamp = 0;
+};
+
+namespace {
+
+void ensure(uint32_t** p, uint64_t* cap, uint64_t want) {
+  if (*cap >= want) return;
+  cudaFree(*p);
+  *p = nullptr;
+  want = std::max<uint64_t>(want, 1024);
+  TGB_CUDA(cudaMalloc(p, sizeof(uint32_t) * want));
+  *cap = want;
+}
+
+uint32_t next_stamp(tg_sampler* s) {
+  if (s->stamp >= 0xFFFFFFF0u) {  // wrap: forget every old stamp
+    TGB_CUDA(cudaMemsetAsync(s->layer_mark, 0, 4 * s->n, s->ctx->stream));
+    TGB_CUDA(cudaMemsetAsync(s->member_mark, 0, 4 * s->n, s->ctx->stream));
+    s->stamp = 0;
+  }
+  return ++s->stamp;
+}
+
+}  // namespace
+
+extern "C" {
+
+int tg_sampler_create(tg_ctx* ctx, const tg_graph* gt, tg_sampler** out) {
+  return guard([&] {
+    if (!ctx || !gt || !out) domain_error("tg_sampler_create: null argument");
+    DeviceGuard dg(ctx->device);
+    auto* s = new tg_sampler;
+    s->ctx = ctx;
+    s->n = tg_graph_num_nodes(gt);
+    s->off = tg_graph_offsets32(gt);
+    s->tgt = tg_graph_targets32(gt);
+    try {
+      TGB_CUDA(cudaMalloc(&s->layer_mark, 4 * std::max<uint64_t>(s->n, 1)));
+      TGB_CUDA(cudaMalloc(&s->member_mark, 4 * std::max<uint64_t>(s->n, 1)));
+      TGB_CUDA(cudaMemsetAsync(s->layer_mark, 0, 4 * std::max<uint64_t>(s->n, 1), ctx->stream));
+      TGB_CUDA(cudaMemsetAsync(s->member_mark, 0, 4 * std::max<uint64_t>(s->n, 1), ctx->stream));
+      TGB_CUDA(cudaMalloc(&s->small, 64));
+      const uint64_t nblk = (s->n + kCompactBlock - 1) / kCompactBlock;
+      TGB_CUDA(cudaMalloc(&s->blk, 4 * std::max<uint64_t>(nblk, 1)));
+    } catch (...) {
+      tg_sampler_destroy(s);
+      throw;
+    }
+    *out = s;
+  });
+}
+
+int tg_sampler_destroy(tg_sampler* s) {
+  if (!s) return TG_OK;
+  DeviceGuard dg(s->ctx->device);
+  cudaStreamSynchronize(s->ctx->stream);
+  cudaFree(s->layer_mark);
+  cudaFree(s->member_mark);
+  cudaFree(s->buf[0]);
+  cudaFree(s->buf[1]);
+  cudaFree(s->picks);
+  cudaFree(s->small);
+  cudaFree(s->blk);
+  delete s;
+  return TG_OK;
+}
+
+int tg_sample_minibatch(tg_sampler* s, const uint64_t* seeds, uint64_t ns, const uint32_t* fanouts,
+                        uint32_t nf, uint64_t rng_seed, uint64_t epoch, uint64_t batch,
+                        uint64_t* out, uint64_t cap, uint64_t* out_n) {
+  return guard([&] {
+    // validate_fanouts, sampling.cpp:18-25; build_minibatch :59-62
+    if (nf == 0) domain_error("fanouts must be non-empty");
+    if (nf > 5)
+      domain_error("fanout depth " + std::to_string(nf) + " exceeds the supported maximum of 5");
+    for (uint32_t l = 0; l < nf; ++l)
+      if (fanouts[l] < 1) domain_error("every fanout must be >= 1");
+    if (ns == 0) domain_error("build_minibatch: seeds must be non-empty");
+    tg_ctx* ctx = s->ctx;
+    DeviceGuard dg(ctx->device);
+    const uint64_t n = s->n;
+    const uint64_t* sd = dev_in(ctx, seeds, ns, kStageIn0);
+    // frontier buffers: a frontier never exceeds n nodes
+    uint64_t cap0 = s->buf_cap;
+    ensure(&s->buf[0], &cap0, n + 1);
+    uint64_t cap1 = s->buf_cap;
+    ensure(&s->buf[1], &cap1, n + 1);
+    s->buf_cap = std::min(cap0, cap1);
+    uint32_t* cnt = s->small;  // [0] frontier count, [1] member total
+    auto* bad = reinterpret_cast<unsigned long long*>(s->small + 4);
+    TGB_CUDA(cudaMemsetAsync(cnt, 0, 8, ctx->stream));
+    TGB_CUDA(cudaMemsetAsync(bad, 0xff, 8, ctx->stream));
+    const uint32_t mstamp = next_stamp(s);
+    uint32_t lstamp = next_stamp(s);
+    seed_kernel<<<grid_for(ns, 256), 256, 0, ctx->stream>>>(sd, ns, n, s->layer_mark, lstamp,
+                                                           s->member_mark, mstamp, s->buf[0], cnt,
+                                                           bad);
+    TGB_LAUNCHED();
+    uint32_t hc[6];
+    TGB_CUDA(cudaMemcpyAsync(hc, s->small, 24, cudaMemcpyDeviceToHost, ctx->stream));
+    ctx->sync();
+    unsigned long long hb;
+    std::memcpy(&hb, hc + 4, 8);
+    if (hb != ~0ull) {
+      uint64_t v = 0;
+      TGB_CUDA(cudaMemcpy(&v, sd + hb, 8, cudaMemcpyDeviceToHost));
+      domain_error("seed " + std::to_string(v) + " out of range");  // sampling.cpp:61-62
+    }
+    uint32_t f = hc[0];
+    const uint64_t key0 = host_mix64(rng_seed ^ 0x6A09E667F3BCC908ull);  // rng.hpp:23-28
+    int cur = 0;
+    for (uint32_t layer = 0; layer < nf && f > 0; ++layer) {
+      const uint32_t k = fanouts[layer];
+      uint64_t key = key0;
+      const uint64_t coords[4] = {0x534Dull, epoch, batch, layer};  // sampling.cpp:35-37
+      for (uint64_t c : coords) key = host_mix64(key ^ host_mix64(c));
+      ensure(&s->picks, &s->picks_cap, static_cast<uint64_t>(f) * k);
+      lstamp = next_stamp(s);
+      TGB_CUDA(cudaMemsetAsync(cnt, 0, 4, ctx->stream));
+      SampleArgs a{s->off, s->tgt, s->buf[cur], f, k, key, s->picks, s->layer_mark, lstamp,
+                   s->member_mark, mstamp, s->buf[cur ^ 1], cnt};
+      sample_layer_kernel<<<(f + 255) / 256, 256, 0, ctx->stream>>>(a);
+      TGB_LAUNCHED();
+      TGB_CUDA(cudaMemcpyAsync(&f, cnt, 4, cudaMemcpyDeviceToHost, ctx->stream));
+      ctx->sync();
+      cur ^= 1;
+    }
+    // members, sorted by id
+    const uint64_t nblk = (n + kCompactBlock - 1) / kCompactBlock;
+    member_count_kernel<<<nblk, kCompactBlock, 0, ctx->stream>>>(s->member_mark, n, mstamp, s->blk);
+    TGB_LAUNCHED();
+    count_prefix_kernel<<<1, 1024, 0, ctx->stream>>>(s->blk, static_cast<uint32_t>(nblk), cnt + 1);
+    TGB_LAUNCHED();
+    uint32_t total = 0;
+    TGB_CUDA(cudaMemcpyAsync(&total, cnt + 1, 4, cudaMemcpyDeviceToHost, ctx->stream));
+    ctx->sync();
+    *out_n = total;
+    if (total > cap)
+      domain_error("tg_sample_minibatch: " + std::to_string(total) +
+                   " members exceed the output capacity " + std::to_string(cap));
+    DevOut<uint64_t> o(ctx, out, total, kStageOut0);
+    member_write_kernel<<<nblk, kCompactBlock, 0, ctx->stream>>>(s->member_mark, n, mstamp, s->blk,
+                                                                 o.dev());
+    TGB_LAUNCHED();
+    o.finish();
+  });
+}
+
+}  // extern "C"

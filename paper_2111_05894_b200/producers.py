@@ -73,3 +73,55 @@ def epoch_minibatches(gt: CsrGraph, tid, fanouts: Sequence[int], batch_size: int
     o = _take(po, nb.value + 1)
     allids = _take(pi, int(o[-1]) if len(o) else 0)
     return [allids[o[b]:o[b + 1]] for b in range(nb.value)]
+
+
+def epoch_order(tid, seed: int, epoch: int) -> np.ndarray:
+    """sampling.cpp:106-109: this epoch's shuffled train ids; batch b is
+    order[b*batch_size : (b+1)*batch_size]."""
+    ids = np.ascontiguousarray(np.asarray(tid.ids if isinstance(tid, TrainIdSet) else tid,
+                                          np.uint64))
+    out = np.empty(max(len(ids), 1), np.uint64)
+    _host_check(LIB.tg_epoch_order(ids.ctypes.data if len(ids) else out.ctypes.data, len(ids),
+                                   int(seed), int(epoch), out.ctypes.data))
+    return out[:len(ids)]
+
+
+class GpuSampler:
+    """build_minibatch (sampling.cpp:56-90) on the GPU, bit-identical member
+    lists (csrc/sampling.cu). `gt` is the TRANSPOSED graph (producers.transpose)."""
+
+    def __init__(self, gt: CsrGraph, ctx=None):
+        from . import tiergraph as tg
+        self.tg = tg
+        self.ctx = ctx or tg.default_context()
+        self.gt = gt
+        self.n = gt.num_nodes()
+        h = C.c_void_p()
+        tg._check(LIB.tg_sampler_create(self.ctx.h, gt.device(self.ctx), C.byref(h)))
+        self.h = h
+
+    def minibatch(self, seeds, fanouts: Sequence[int], seed: int, epoch: int, batch: int,
+                  out=None):
+        """Sorted unique member ids (numpy u64, or into a device tensor `out`,
+        returning the member count)."""
+        tg = self.tg
+        sd = tg._u64(seeds)
+        fo = np.ascontiguousarray(np.asarray(list(fanouts), np.uint32))
+        cnt = C.c_uint64()
+        dst = out if out is not None else np.empty(max(self.n, 1), np.uint64)
+        tg._check(LIB.tg_sample_minibatch(self.h, tg._nonempty(sd, np.uint64), tg._len(sd),
+                                          fo.ctypes.data if len(fo) else None, len(fo),
+                                          int(seed), int(epoch), int(batch), tg._ptr(dst),
+                                          tg._len(dst), C.byref(cnt)))
+        return int(cnt.value) if out is not None else dst[:cnt.value].copy()
+
+    def close(self):
+        if getattr(self, "h", None):
+            LIB.tg_sampler_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

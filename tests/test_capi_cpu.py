@@ -116,3 +116,16 @@ def test_host_producers_match_reference(ref):
                 assert np.array_equal(a, b)
     with pytest.raises(tg.DomainError):
         producers.draw_random_train_ids(10, 11, 0)
+
+
+def test_epoch_order_matches_reference_shuffle():
+    """producers.epoch_order = the reference's per-epoch Fisher-Yates
+    (sampling.cpp:106-109, rng.hpp:67-73), checked on the oracle."""
+    import oracle
+    from paper_2111_05894_b200 import producers
+    port = oracle.port()
+    chk = oracle.ref() or port
+    tid = port.draw_random_train_ids(10_000, 1_234, 9)
+    for epoch in (0, 1, 7):
+        key = chk.derive_stream_key(7, [0x5348, epoch])
+        assert np.array_equal(producers.epoch_order(tid, 7, epoch), port.shuffle(key, tid))
