@@ -283,9 +283,24 @@ def run_ours(args):
     rg = tg.reorder_graph(g, perm, ctx=ctx)
     gt = producers.transpose(rg)
     new_tid = np.sort(perm.new_id_of[tid.ids])
-    lists = producers.epoch_minibatches(gt, new_tid, cfg["fanouts"], cfg["batch"], seed=7, epoch=0)
+    # the epoch's minibatch id lists, sampled on the GPU (csrc/sampling.cu,
+    # bit-identical to the reference's build_minibatch); spot-checked against
+    # the host restatement
+    sampler = producers.GpuSampler(tg.CsrGraph(gt.offsets, gt.targets), ctx=ctx)
+    order = producers.epoch_order(new_tid, 7, 0)
+    B = cfg["batch"]
+    nbat = (len(order) + B - 1) // B
+    sampler.minibatch(order[:B], cfg["fanouts"], 7, 0, 0)  # warm
+    torch.cuda.synchronize()
+    t_s = time.perf_counter()
+    lists = [sampler.minibatch(order[b * B:(b + 1) * B], cfg["fanouts"], 7, 0, b)
+             for b in range(nbat)]
+    sample_s = time.perf_counter() - t_s
+    host_check = producers.epoch_minibatches(gt, new_tid, cfg["fanouts"], B, seed=7, epoch=0,
+                                             max_batches=2)
+    sampler_ok = all(np.array_equal(a, b) for a, b in zip(host_check, lists))
     mine = lists[rank::world]
-    log(f"[rank {rank}] {len(lists)} minibatches/epoch sampled on host "
+    log(f"[rank {rank}] {len(lists)} minibatches/epoch sampled on the GPU "
         f"(avg {np.mean([len(l) for l in lists]):.0f} ids) in {time.time()-t0:.1f}s")
 
     # ---- tiered store: hot rows in HBM (sharded across ranks), cold rows pinned
@@ -465,6 +480,10 @@ def run_ours(args):
                                       "frac": round(pr_bytes_iter / (step_ms * 1e-3) / 1e9 / hbm_peak, 4),
                                       "algorithmic_bytes_per_launch": pr_bytes_iter}},
             "selection": {"ms": round(min(sel), 4), "keys": n},
+            "sampling": {"minibatches_per_s": round(nbat / sample_s, 1), "minibatches": nbat,
+                         "how": "GPU build_minibatch (csrc/sampling.cu), one epoch, host-timed "
+                                "incl. per-layer syncs",
+                         "matches_host_restatement": bool(sampler_ok)},
             "epoch": {"minibatches": len(lists), "host_bytes_tiered": int(host_epoch),
                       "bytes_untiered": int(total_epoch),
                       "reduction": round(1 - host_epoch / max(total_epoch, 1), 4),
@@ -473,7 +492,8 @@ def run_ours(args):
         }
         if world == 1 and not args.no_cpu_baseline:
             result["cpu_baseline"], result["parity"] = cpu_baseline(
-                cfg, off, tgt, tid, scores, perm, feat, R, lay, mine, store, out_d, torch)
+                cfg, off, tgt, tid, scores, perm, feat, R, lay, mine, store, out_d, torch,
+                gt=gt, new_tid=new_tid, gpu_lists=lists)
     if dist:
         dist.barrier()
         dist.destroy_process_group()
@@ -495,7 +515,8 @@ def host_link_dma_gbps(torch, dev, nbytes=1 << 30):
     return best
 
 
-def cpu_baseline(cfg, off, tgt, tid, scores, perm, feat, R, lay, lists, store, out_d, torch):
+def cpu_baseline(cfg, off, tgt, tid, scores, perm, feat, R, lay, lists, store, out_d, torch,
+                 gt=None, new_tid=None, gpu_lists=None):
     """The reference's CPU path (oracle/_ref, all host threads) on a bounded
     sample of the same workload, plus bit-exact parity of our results."""
     import oracle
@@ -537,12 +558,22 @@ def cpu_baseline(cfg, off, tgt, tid, scores, perm, feat, R, lay, lists, store, o
     mine = tg.TrafficReport()
     got = store.gather_rows(ids, report=mine)
     parity["gather_rows_bit_exact"] = bool(np.array_equal(got, out[: len(ids)]))
+    if gt is not None:
+        # the reference's own sampler on the host cores, and parity of the GPU sampler
+        go_, gt_ = np.asarray(gt.offsets), np.asarray(gt.targets)
+        t0 = time.perf_counter()
+        ref_lists = ref.epoch_minibatches(go_, gt_, new_tid, cfg["fanouts"], cfg["batch"], 7, 0,
+                                          max_batches=32)
+        samp_s = time.perf_counter() - t0
+        parity["gpu_sampler_bit_exact"] = bool(all(np.array_equal(a, b)
+                                                   for a, b in zip(ref_lists, gpu_lists)))
     parity["traffic_report_equal"] = bool(np.array_equal(mine.as_array(), r))
     base = {"value": round(moved / cpu_s / 1e9, 3), "unit": "GB/s", "cores": cores, "kind": kind,
             "sample": f"{passes} x {len(sample)} minibatches of the same epoch: reference FeatureMatrix::row "
                       f"memcpy (reorder.cpp:113-115 pattern) + gather() accounting, "
                       f"{cores} OpenMP threads, {cpu_s:.2f}s",
             "pagerank_gteps": round(5 * len(tgt) / pr_s / 1e9, 4),
+            "sampling_minibatches_per_s": round(32 / samp_s, 2) if gt is not None else None,
             "pagerank_s": round(pr_s, 3)}
     return base, parity
 

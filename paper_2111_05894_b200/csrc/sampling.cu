@@ -72,7 +72,10 @@ struct SampleArgs {
 };
 
 __device__ __forceinline__ void admit(const SampleArgs& a, uint32_t u) {
-  if (atomicExch(a.layer_mark + u, a.layer_stamp) != a.layer_stamp) {
+  // a plain L2 read first: hot nodes are drawn by many threads per layer,
+  // and only the first needs the atomic (a stale read just costs one)
+  if (__ldcg(a.layer_mark + u) != a.layer_stamp &&
+      atomicExch(a.layer_mark + u, a.layer_stamp) != a.layer_stamp) {
     a.next[atomicAdd(a.next_count, 1u)] = u;
     a.member_mark[u] = a.member_stamp;
   }
