@@ -1120,7 +1120,10 @@ int tg_gather_rows(tg_store* s, const uint64_t* ids, uint64_t n, void* dst, tg_r
     if (n == 0) return;
     tg_ctx* ctx = s->ctx;
     DeviceGuard dg(ctx->device);
-    const uint64_t* d = dev_in(ctx, ids, n, kStageIn0);
+    // ids in pinned, mapped host memory are read in place (UVA zero-copy,
+    // overlapping the gather) instead of being staged by a separate copy
+    const void* mapped = mapped_device_ptr(ids);
+    const uint64_t* d = mapped ? static_cast<const uint64_t*>(mapped) : dev_in(ctx, ids, n, kStageIn0);
     DevOut<uint8_t> o(ctx, static_cast<uint8_t*>(dst), n * s->R, kStageOut0);
     uint64_t* c = s->counters;
     auto* err = reinterpret_cast<unsigned long long*>(c + 3);
