@@ -269,6 +269,11 @@ def run_ours(args):
     scores_d, pr_ms, step_ms, prep_ms = bench_pagerank(torch, tg, ctx, g, tid, n, e)
     indeg_out = torch.empty(n, dtype=torch.int64, device=torch.device("cuda", local))
     indeg_ms = min(time_events(torch, lambda: tg.in_degrees(g, ctx=ctx, out=indeg_out), 3))
+    import ctypes as _C
+    from paper_2111_05894_b200._lib import LIB as _LIB
+    floor_us = _C.c_double()
+    assert _LIB.tg_measure_gather_floor_us(ctx.h, g.device(ctx), 5, _C.byref(floor_us)) == 0
+    floor_us = floor_us.value
     pr_multi = None
     if world > 1:
         pr_multi = bench_pagerank_multi(torch, tg, ctx, g, tid, scores_d, dist)
@@ -478,7 +483,14 @@ def run_ours(args):
                                       "achieved": round(pr_bytes_iter / (step_ms * 1e-3) / 1e9, 1),
                                       "peak": hbm_peak, "unit": "GB/s",
                                       "frac": round(pr_bytes_iter / (step_ms * 1e-3) / 1e9 / hbm_peak, 4),
-                                      "algorithmic_bytes_per_launch": pr_bytes_iter}},
+                                      "algorithmic_bytes_per_launch": pr_bytes_iter},
+                         "gather_floor": {
+                             "us": round(floor_us, 2),
+                             "frac": round(floor_us / (step_ms * 1e3), 4),
+                             "what": "the same E gathers norm[targets[e]] streamed over the same "
+                                     "u32 CSR with no summation-order constraint "
+                                     "(tg_measure_gather_floor_us): the memory-system floor of "
+                                     "a K3 step on this graph; frac = floor / K3 step"}},
             "selection": {"ms": round(min(sel), 4), "keys": n},
             "sampling": {"minibatches_per_s": round(nbat / sample_s, 1), "minibatches": nbat,
                          "how": "GPU build_minibatch (csrc/sampling.cu), one epoch, host-timed "

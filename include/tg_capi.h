@@ -260,6 +260,9 @@ int tg_host_free(void* p);
 int tg_measure_host_read_gbps(tg_ctx* ctx, uint64_t bytes, uint64_t row_bytes, int reps,
                               double* gbps);
 int tg_measure_hbm_copy_gbps(tg_ctx* ctx, uint64_t bytes, int reps, double* gbps);
+/* The memory-system floor of one K3 step on graph g: the same E gathers
+ * x[targets[e]] with no summation-order constraint (best of reps, us). */
+int tg_measure_gather_floor_us(tg_ctx* ctx, const tg_graph* g, int reps, double* us);
 
 /* ------------------------------------------------ host-side input producers
  * Not the hot path: the reference's CPU producers of the gather's id lists,

@@ -116,6 +116,7 @@ SIGNATURES = {
     "tg_transpose_host": (I32, [vp, vp, U64, vp, vp]),
     "tg_epoch_minibatches": (I32, [vp, vp, U64, vp, U64, vp, U32, U64, U64, U64, U64, U64, I32,
                                    C.POINTER(vp), C.POINTER(U64), C.POINTER(vp)]),
+    "tg_measure_gather_floor_us": (I32, [vp, vp, I32, C.POINTER(D)]),
     "tg_sampler_create": (I32, [vp, vp, C.POINTER(vp)]),
     "tg_sampler_destroy": (I32, [vp]),
     "tg_sample_minibatch": (I32, [vp, vp, U64, vp, U32, U64, U64, U64, vp, U64, C.POINTER(U64)]),

@@ -265,7 +265,7 @@ __device__ __forceinline__ double chain_add(double acc, const double* v, uint32_
 // acc crosses a binade only O(log(sum / first)) times per row, mostly in its
 // first elements, so a 2048-element tile takes one or two passes.
 constexpr int kHubT = 8;                          // addends per thread per tile
-constexpr int kHubWarps = 16;                     // 512-thread CTA per hub row
+constexpr int kHubWarps = 8;                      // 256-thread CTA per hub row
 constexpr int kHubThreads = kHubWarps * 32;
 constexpr int kHubTile = kHubThreads * kHubT;     // 4096 addends, 32 KB of smem
 constexpr long long kTop = 1ll << 53;
@@ -643,6 +643,24 @@ __global__ void __launch_bounds__(kPrWarps * 32) pr_step_kernel(const PrStepArgs
   }
 }
 
+// The memory-system floor of one K3 step on this graph: the same E gathers
+// x[tgt[e]] streamed over the same u32 targets, summed with no ordering
+// constraint (one partial per thread). K3 / this = distance to the floor.
+__global__ void __launch_bounds__(256) gather_floor_kernel(const uint32_t* __restrict__ tgt,
+                                                           uint64_t e, const double* __restrict__ x,
+                                                           double* __restrict__ sink) {
+  double acc = 0.0;
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+  for (; i + 3 * stride < e; i += 4 * stride) {
+    const uint32_t a = __ldg(tgt + i), b = __ldg(tgt + i + stride), c = __ldg(tgt + i + 2 * stride),
+                   d = __ldg(tgt + i + 3 * stride);
+    acc += __ldg(x + a) + __ldg(x + b) + __ldg(x + c) + __ldg(x + d);
+  }
+  for (; i < e; i += stride) acc += __ldg(x + __ldg(tgt + i));
+  if (acc == -1.0) sink[0] = acc;  // never true: keeps the loads alive
+}
+
 unsigned long long read_flag(tg_ctx* ctx, unsigned long long* dflag) {
   unsigned long long h = 0;
   TGB_CUDA(cudaMemcpyAsync(&h, dflag, sizeof(h), cudaMemcpyDeviceToHost, ctx->stream));
@@ -840,6 +858,31 @@ int tg_graph_create(tg_ctx* ctx, const uint64_t* offsets, const uint64_t* target
       throw;
     }
     *out = g;
+  });
+}
+
+int tg_measure_gather_floor_us(tg_ctx* ctx, const tg_graph* g, int reps, double* us) {
+  return guard([&] {
+    DeviceGuard dg(ctx->device);
+    double* x = ctx->scratch_t<double>(kScratchA, std::max<uint64_t>(g->n, 1) + 1);
+    TGB_CUDA(cudaMemsetAsync(x, 0, 8 * (g->n + 1), ctx->stream));
+    cudaEvent_t a, b;
+    TGB_CUDA(cudaEventCreate(&a));
+    TGB_CUDA(cudaEventCreate(&b));
+    float best = 1e30f;
+    for (int r = 0; r <= std::max(reps, 1); ++r) {
+      TGB_CUDA(cudaEventRecord(a, ctx->stream));
+      gather_floor_kernel<<<ctx->num_sms * 16, 256, 0, ctx->stream>>>(g->tgt, g->e, x, x + g->n);
+      TGB_LAUNCHED();
+      TGB_CUDA(cudaEventRecord(b, ctx->stream));
+      TGB_CUDA(cudaEventSynchronize(b));
+      float ms = 0;
+      TGB_CUDA(cudaEventElapsedTime(&ms, a, b));
+      if (r && ms < best) best = ms;  // first run warms
+    }
+    cudaEventDestroy(a);
+    cudaEventDestroy(b);
+    *us = best * 1e3;
   });
 }
 
