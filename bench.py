@@ -409,6 +409,35 @@ def run_ours(args):
         dist.all_reduce(t)
         host_epoch, total_epoch = (int(x) for x in t.tolist())
 
+    # ---- C5: cache-ratio sweep of CPU->GPU bytes per epoch (replicated vs
+    # sharded hot tier, 1/2/4/8 devices) from the whole epoch's access counter
+    # (all ranks' minibatches), replayed on the GPU by hot_fraction_sweep
+    # (tiering.cpp:177-202); the identity ordering is the score ordering
+    # because rows are already in new-id order.
+    sweep = None
+    if rank == 0:
+        all_counts = np.zeros(n, np.uint64)
+        for ids in lists:
+            all_counts[ids.astype(np.int64)] += np.uint64(1)
+        acc = tg.make_access_counter(all_counts)
+        ident = np.arange(n, dtype=np.uint64)
+        fr = [0.0, 0.05, 0.1, 0.2, 0.25, 0.5, 1.0]
+        sweep = {"fractions": fr, "epoch_minibatches": len(lists), "row_bytes": R}
+        sweep["note"] = ("per-GPU HBM budget = fraction x N x row_bytes; replicated keeps the "
+                         "same hot set on every GPU, sharded spreads min(1, D x fraction) of "
+                         "the rows over D GPUs at the same per-GPU budget")
+        for D in (1, 2, 4, 8):
+            for mode in ("replicated", "sharded"):
+                eff = fr if mode == "replicated" else [min(1.0, D * f) for f in fr]
+                rep = 1.0 if mode == "replicated" else 0.0
+                rows = tg.hot_fraction_sweep(acc, ident, eff, rep, D, cfg["dim"], cfg["elem"],
+                                             ctx=ctx)
+                host = [r.report.host_bytes for r in rows]
+                sweep[f"{mode}_D{D}"] = {
+                    "hot_fraction": eff, "host_bytes": host,
+                    "reduction_vs_untiered": [round(1 - h / max(host[0], 1), 4) for h in host],
+                    "peer_bytes": [r.report.peer_bytes for r in rows]}
+
     # ---- roofline of the dominant kernel (K8) — mixed HBM / NVLink / PCIe
     pcie_dma = host_link_dma_gbps(torch, dev)
     pcie_zc = tg.measure_host_read_gbps(ctx, 1 << 30, R if R % 16 == 0 else 512, 3)
@@ -500,6 +529,7 @@ def run_ours(args):
                       "bytes_untiered": int(total_epoch),
                       "reduction": round(1 - host_epoch / max(total_epoch, 1), 4),
                       "equals_simulate_trace": bool(world > 1 or sim.host_bytes == ep.host_bytes)},
+            "epoch_sweep": sweep,
             "clocks": clocks,
         }
         if world == 1 and not args.no_cpu_baseline:
