@@ -301,6 +301,20 @@ int tg_sampler_destroy(tg_sampler* s);
 int tg_sample_minibatch(tg_sampler* s, const uint64_t* seeds, uint64_t ns, const uint32_t* fanouts,
                         uint32_t nf, uint64_t rng_seed, uint64_t epoch, uint64_t batch,
                         uint64_t* out, uint64_t cap, uint64_t* out_n);
+/* Same, also returning every individual draw (build_minibatch's raw_draws,
+ * sampling.hpp:48-55: each seed once as given, then every sampled node; order
+ * unspecified, multiset deterministic) into raw (host|device, raw_cap). */
+int tg_sample_minibatch_raw(tg_sampler* s, const uint64_t* seeds, uint64_t ns,
+                            const uint32_t* fanouts, uint32_t nf, uint64_t rng_seed,
+                            uint64_t epoch, uint64_t batch, uint64_t* out, uint64_t cap,
+                            uint64_t* out_n, uint64_t* raw, uint64_t raw_cap, uint64_t* raw_n);
+/* sampling.cpp:92-140 run_training_trace on the device: per epoch the seeded
+ * shuffle, then every batch expanded; counts (n x u64, host|device) get one
+ * per unique member per batch (dedup_per_batch) or one per raw access. The
+ * sampler's graph is the TRANSPOSED graph; tid is a TrainIdSet (sorted). */
+int tg_sampler_trace(tg_sampler* s, const uint64_t* tid, uint64_t ntid, const uint32_t* fanouts,
+                     uint32_t nf, uint64_t batch_size, uint64_t epochs, uint64_t rng_seed,
+                     int dedup_per_batch, uint64_t* counts);
 /* sampling.cpp:106-109: the epoch's shuffled train-id order (Fisher-Yates,
  * key {0x5348, epoch}); batch b is order[b*batch_size ..). Host arrays. */
 int tg_epoch_order(const uint64_t* tid, uint64_t ntid, uint64_t rng_seed, uint64_t epoch,

@@ -121,6 +121,9 @@ SIGNATURES = {
     "tg_sampler_destroy": (I32, [vp]),
     "tg_sample_minibatch": (I32, [vp, vp, U64, vp, U32, U64, U64, U64, vp, U64, C.POINTER(U64)]),
     "tg_epoch_order": (I32, [vp, U64, U64, U64, vp]),
+    "tg_sample_minibatch_raw": (I32, [vp, vp, U64, vp, U32, U64, U64, U64, vp, U64,
+                                      C.POINTER(U64), vp, U64, C.POINTER(U64)]),
+    "tg_sampler_trace": (I32, [vp, vp, U64, vp, U32, U64, U64, U64, I32, vp]),
 }
 
 

@@ -69,15 +69,31 @@ struct SampleArgs {
   uint32_t member_stamp;
   uint32_t* next;
   uint32_t* next_count;
+  // optional outputs (run_training_trace, raw_draws; sampling.cpp:56-140)
+  unsigned long long* counts;  // per-node access counts, or null
+  int count_raw;               // 1: one per draw; 0: one per new minibatch member
+  uint64_t* raw;               // every draw, or null
+  unsigned long long* raw_n;
+  uint64_t raw_cap;
 };
 
 __device__ __forceinline__ void admit(const SampleArgs& a, uint32_t u) {
+  if (a.raw) {
+    const unsigned long long k = atomicAdd(a.raw_n, 1ull);
+    if (k < a.raw_cap) a.raw[k] = u;
+  }
+  if (a.counts && a.count_raw) atomicAdd(a.counts + u, 1ull);
   // a plain L2 read first: hot nodes are drawn by many threads per layer,
   // and only the first needs the atomic (a stale read just costs one)
   if (__ldcg(a.layer_mark + u) != a.layer_stamp &&
       atomicExch(a.layer_mark + u, a.layer_stamp) != a.layer_stamp) {
     a.next[atomicAdd(a.next_count, 1u)] = u;
-    a.member_mark[u] = a.member_stamp;
+    if (a.counts && !a.count_raw) {
+      if (atomicExch(a.member_mark + u, a.member_stamp) != a.member_stamp)
+        atomicAdd(a.counts + u, 1ull);
+    } else {
+      a.member_mark[u] = a.member_stamp;
+    }
   }
 }
 
@@ -107,7 +123,8 @@ __global__ void __launch_bounds__(256) sample_layer_kernel(const SampleArgs a) {
 __global__ void seed_kernel(const uint64_t* __restrict__ seeds, uint64_t ns, uint64_t n,
                             uint32_t* layer_mark, uint32_t stamp, uint32_t* member_mark,
                             uint32_t mstamp, uint32_t* frontier, uint32_t* count,
-                            unsigned long long* bad) {
+                            unsigned long long* bad, unsigned long long* counts, int count_raw,
+                            uint64_t* raw, unsigned long long* raw_n, uint64_t raw_cap) {
   for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < ns;
        i += (uint64_t)gridDim.x * blockDim.x) {
     const uint64_t s = seeds[i];
@@ -116,9 +133,15 @@ __global__ void seed_kernel(const uint64_t* __restrict__ seeds, uint64_t ns, uin
       continue;
     }
     const uint32_t u = static_cast<uint32_t>(s);
+    if (raw) {  // each seed once, as given (sampling.cpp:70)
+      const unsigned long long k = atomicAdd(raw_n, 1ull);
+      if (k < raw_cap) raw[k] = u;
+    }
+    if (counts && count_raw) atomicAdd(counts + u, 1ull);
     if (atomicExch(layer_mark + u, stamp) != stamp) {
       frontier[atomicAdd(count, 1u)] = u;
       member_mark[u] = mstamp;
+      if (counts && !count_raw) atomicAdd(counts + u, 1ull);
     }
   }
 }
@@ -264,84 +287,199 @@ int tg_sampler_destroy(tg_sampler* s) {
   return TG_OK;
 }
 
-int tg_sample_minibatch(tg_sampler* s, const uint64_t* seeds, uint64_t ns, const uint32_t* fanouts,
-                        uint32_t nf, uint64_t rng_seed, uint64_t epoch, uint64_t batch,
-                        uint64_t* out, uint64_t cap, uint64_t* out_n) {
-  return guard([&] {
-    // validate_fanouts, sampling.cpp:18-25; build_minibatch :59-62
-    if (nf == 0) domain_error("fanouts must be non-empty");
-    if (nf > 5)
-      domain_error("fanout depth " + std::to_string(nf) + " exceeds the supported maximum of 5");
-    for (uint32_t l = 0; l < nf; ++l)
-      if (fanouts[l] < 1) domain_error("every fanout must be >= 1");
-    if (ns == 0) domain_error("build_minibatch: seeds must be non-empty");
-    tg_ctx* ctx = s->ctx;
-    DeviceGuard dg(ctx->device);
-    const uint64_t n = s->n;
-    const uint64_t* sd = dev_in(ctx, seeds, ns, kStageIn0);
-    // frontier buffers: a frontier never exceeds n nodes
-    uint64_t cap0 = s->buf_cap;
-    ensure(&s->buf[0], &cap0, n + 1);
-    uint64_t cap1 = s->buf_cap;
-    ensure(&s->buf[1], &cap1, n + 1);
-    s->buf_cap = std::min(cap0, cap1);
-    uint32_t* cnt = s->small;  // [0] frontier count, [1] member total
-    auto* bad = reinterpret_cast<unsigned long long*>(s->small + 4);
-    TGB_CUDA(cudaMemsetAsync(cnt, 0, 8, ctx->stream));
-    TGB_CUDA(cudaMemsetAsync(bad, 0xff, 8, ctx->stream));
-    const uint32_t mstamp = next_stamp(s);
-    uint32_t lstamp = next_stamp(s);
-    seed_kernel<<<grid_for(ns, 256), 256, 0, ctx->stream>>>(sd, ns, n, s->layer_mark, lstamp,
-                                                           s->member_mark, mstamp, s->buf[0], cnt,
-                                                           bad);
+}  // extern "C"
+
+namespace {
+
+struct ExpandOut {
+  unsigned long long* counts = nullptr;  // device, n
+  int count_raw = 0;
+  uint64_t* raw = nullptr;  // device
+  uint64_t raw_cap = 0;
+};
+
+void check_fanouts(const uint32_t* fanouts, uint32_t nf) {  // sampling.cpp:18-25
+  if (nf == 0) domain_error("fanouts must be non-empty");
+  if (nf > 5)
+    domain_error("fanout depth " + std::to_string(nf) + " exceeds the supported maximum of 5");
+  for (uint32_t l = 0; l < nf; ++l)
+    if (fanouts[l] < 1) domain_error("every fanout must be >= 1");
+}
+
+// build_minibatch (sampling.cpp:56-90) on the device; returns the member stamp.
+// The raw-draw count (when requested) is left in s->small[6..7].
+uint32_t expand(tg_sampler* s, const uint64_t* sd, uint64_t ns, const uint32_t* fanouts, uint32_t nf,
+                uint64_t rng_seed, uint64_t epoch, uint64_t batch, const ExpandOut& o) {
+  if (ns == 0) domain_error("build_minibatch: seeds must be non-empty");
+  tg_ctx* ctx = s->ctx;
+  const uint64_t n = s->n;
+  uint64_t cap0 = s->buf_cap;
+  ensure(&s->buf[0], &cap0, n + 1);
+  uint64_t cap1 = s->buf_cap;
+  ensure(&s->buf[1], &cap1, n + 1);
+  s->buf_cap = std::min(cap0, cap1);
+  uint32_t* cnt = s->small;  // [0] frontier count, [1] member total, [4..5] bad, [6..7] raw n
+  auto* bad = reinterpret_cast<unsigned long long*>(s->small + 4);
+  auto* raw_n = reinterpret_cast<unsigned long long*>(s->small + 6);
+  TGB_CUDA(cudaMemsetAsync(cnt, 0, 8, ctx->stream));
+  TGB_CUDA(cudaMemsetAsync(bad, 0xff, 8, ctx->stream));
+  TGB_CUDA(cudaMemsetAsync(raw_n, 0, 8, ctx->stream));
+  const uint32_t mstamp = next_stamp(s);
+  uint32_t lstamp = next_stamp(s);
+  seed_kernel<<<grid_for(ns, 256), 256, 0, ctx->stream>>>(sd, ns, n, s->layer_mark, lstamp,
+                                                         s->member_mark, mstamp, s->buf[0], cnt,
+                                                         bad, o.counts, o.count_raw, o.raw, raw_n,
+                                                         o.raw_cap);
+  TGB_LAUNCHED();
+  uint32_t hc[6];
+  TGB_CUDA(cudaMemcpyAsync(hc, s->small, 24, cudaMemcpyDeviceToHost, ctx->stream));
+  ctx->sync();
+  unsigned long long hb;
+  std::memcpy(&hb, hc + 4, 8);
+  if (hb != ~0ull) {
+    uint64_t v = 0;
+    TGB_CUDA(cudaMemcpy(&v, sd + hb, 8, cudaMemcpyDeviceToHost));
+    domain_error("seed " + std::to_string(v) + " out of range");  // sampling.cpp:61-62
+  }
+  uint32_t f = hc[0];
+  const uint64_t key0 = host_mix64(rng_seed ^ 0x6A09E667F3BCC908ull);  // rng.hpp:23-28
+  int cur = 0;
+  for (uint32_t layer = 0; layer < nf && f > 0; ++layer) {
+    const uint32_t k = fanouts[layer];
+    uint64_t key = key0;
+    const uint64_t coords[4] = {0x534Dull, epoch, batch, layer};  // sampling.cpp:35-37
+    for (uint64_t c : coords) key = host_mix64(key ^ host_mix64(c));
+    ensure(&s->picks, &s->picks_cap, static_cast<uint64_t>(f) * k);
+    lstamp = next_stamp(s);
+    TGB_CUDA(cudaMemsetAsync(cnt, 0, 4, ctx->stream));
+    SampleArgs a{s->off, s->tgt, s->buf[cur], f, k, key, s->picks, s->layer_mark, lstamp,
+                 s->member_mark, mstamp, s->buf[cur ^ 1], cnt, o.counts, o.count_raw, o.raw,
+                 raw_n, o.raw_cap};
+    sample_layer_kernel<<<(f + 255) / 256, 256, 0, ctx->stream>>>(a);
     TGB_LAUNCHED();
-    uint32_t hc[6];
-    TGB_CUDA(cudaMemcpyAsync(hc, s->small, 24, cudaMemcpyDeviceToHost, ctx->stream));
+    TGB_CUDA(cudaMemcpyAsync(&f, cnt, 4, cudaMemcpyDeviceToHost, ctx->stream));
     ctx->sync();
-    unsigned long long hb;
-    std::memcpy(&hb, hc + 4, 8);
-    if (hb != ~0ull) {
-      uint64_t v = 0;
-      TGB_CUDA(cudaMemcpy(&v, sd + hb, 8, cudaMemcpyDeviceToHost));
-      domain_error("seed " + std::to_string(v) + " out of range");  // sampling.cpp:61-62
-    }
-    uint32_t f = hc[0];
-    const uint64_t key0 = host_mix64(rng_seed ^ 0x6A09E667F3BCC908ull);  // rng.hpp:23-28
-    int cur = 0;
-    for (uint32_t layer = 0; layer < nf && f > 0; ++layer) {
-      const uint32_t k = fanouts[layer];
-      uint64_t key = key0;
-      const uint64_t coords[4] = {0x534Dull, epoch, batch, layer};  // sampling.cpp:35-37
-      for (uint64_t c : coords) key = host_mix64(key ^ host_mix64(c));
-      ensure(&s->picks, &s->picks_cap, static_cast<uint64_t>(f) * k);
-      lstamp = next_stamp(s);
-      TGB_CUDA(cudaMemsetAsync(cnt, 0, 4, ctx->stream));
-      SampleArgs a{s->off, s->tgt, s->buf[cur], f, k, key, s->picks, s->layer_mark, lstamp,
-                   s->member_mark, mstamp, s->buf[cur ^ 1], cnt};
-      sample_layer_kernel<<<(f + 255) / 256, 256, 0, ctx->stream>>>(a);
-      TGB_LAUNCHED();
-      TGB_CUDA(cudaMemcpyAsync(&f, cnt, 4, cudaMemcpyDeviceToHost, ctx->stream));
-      ctx->sync();
-      cur ^= 1;
-    }
-    // members, sorted by id
-    const uint64_t nblk = (n + kCompactBlock - 1) / kCompactBlock;
-    member_count_kernel<<<nblk, kCompactBlock, 0, ctx->stream>>>(s->member_mark, n, mstamp, s->blk);
-    TGB_LAUNCHED();
-    count_prefix_kernel<<<1, 1024, 0, ctx->stream>>>(s->blk, static_cast<uint32_t>(nblk), cnt + 1);
-    TGB_LAUNCHED();
-    uint32_t total = 0;
-    TGB_CUDA(cudaMemcpyAsync(&total, cnt + 1, 4, cudaMemcpyDeviceToHost, ctx->stream));
-    ctx->sync();
-    *out_n = total;
-    if (total > cap)
-      domain_error("tg_sample_minibatch: " + std::to_string(total) +
-                   " members exceed the output capacity " + std::to_string(cap));
+    cur ^= 1;
+  }
+  return mstamp;
+}
+
+uint64_t compact_members(tg_sampler* s, uint32_t mstamp, uint64_t* out, uint64_t cap) {
+  tg_ctx* ctx = s->ctx;
+  const uint64_t n = s->n;
+  uint32_t* cnt = s->small;
+  const uint64_t nblk = (n + kCompactBlock - 1) / kCompactBlock;
+  member_count_kernel<<<nblk, kCompactBlock, 0, ctx->stream>>>(s->member_mark, n, mstamp, s->blk);
+  TGB_LAUNCHED();
+  count_prefix_kernel<<<1, 1024, 0, ctx->stream>>>(s->blk, static_cast<uint32_t>(nblk), cnt + 1);
+  TGB_LAUNCHED();
+  uint32_t total = 0;
+  TGB_CUDA(cudaMemcpyAsync(&total, cnt + 1, 4, cudaMemcpyDeviceToHost, ctx->stream));
+  ctx->sync();
+  if (total <= cap) {
     DevOut<uint64_t> o(ctx, out, total, kStageOut0);
     member_write_kernel<<<nblk, kCompactBlock, 0, ctx->stream>>>(s->member_mark, n, mstamp, s->blk,
                                                                  o.dev());
     TGB_LAUNCHED();
     o.finish();
+  }
+  return total;
+}
+
+}  // namespace
+
+extern "C" {
+
+int tg_sample_minibatch(tg_sampler* s, const uint64_t* seeds, uint64_t ns, const uint32_t* fanouts,
+                        uint32_t nf, uint64_t rng_seed, uint64_t epoch, uint64_t batch,
+                        uint64_t* out, uint64_t cap, uint64_t* out_n) {
+  return guard([&] {
+    check_fanouts(fanouts, nf);
+    if (ns == 0) domain_error("build_minibatch: seeds must be non-empty");
+    DeviceGuard dg(s->ctx->device);
+    const uint64_t* sd = dev_in(s->ctx, seeds, ns, kStageIn0);
+    const uint32_t mstamp = expand(s, sd, ns, fanouts, nf, rng_seed, epoch, batch, ExpandOut{});
+    const uint64_t total = compact_members(s, mstamp, out, cap);
+    *out_n = total;
+    if (total > cap)
+      domain_error("tg_sample_minibatch: " + std::to_string(total) +
+                   " members exceed the output capacity " + std::to_string(cap));
+  });
+}
+
+int tg_sample_minibatch_raw(tg_sampler* s, const uint64_t* seeds, uint64_t ns,
+                            const uint32_t* fanouts, uint32_t nf, uint64_t rng_seed,
+                            uint64_t epoch, uint64_t batch, uint64_t* out, uint64_t cap,
+                            uint64_t* out_n, uint64_t* raw, uint64_t raw_cap, uint64_t* raw_n) {
+  return guard([&] {
+    check_fanouts(fanouts, nf);
+    if (ns == 0) domain_error("build_minibatch: seeds must be non-empty");
+    tg_ctx* ctx = s->ctx;
+    DeviceGuard dg(ctx->device);
+    const uint64_t* sd = dev_in(ctx, seeds, ns, kStageIn0);
+    uint64_t* rd = ctx->scratch_t<uint64_t>(kStageOut1, std::max<uint64_t>(raw_cap, 1));
+    ExpandOut o;
+    o.raw = rd;
+    o.raw_cap = raw_cap;
+    const uint32_t mstamp = expand(s, sd, ns, fanouts, nf, rng_seed, epoch, batch, o);
+    unsigned long long rn = 0;
+    TGB_CUDA(cudaMemcpyAsync(&rn, s->small + 6, 8, cudaMemcpyDeviceToHost, ctx->stream));
+    ctx->sync();
+    *raw_n = rn;
+    const uint64_t total = compact_members(s, mstamp, out, cap);
+    *out_n = total;
+    if (total > cap || rn > raw_cap)
+      domain_error("tg_sample_minibatch_raw: output capacity exceeded");
+    if (rn) {
+      if (is_device_ptr(raw)) {
+        TGB_CUDA(cudaMemcpyAsync(raw, rd, 8 * rn, cudaMemcpyDeviceToDevice, ctx->stream));
+      } else {
+        TGB_CUDA(cudaMemcpyAsync(raw, rd, 8 * rn, cudaMemcpyDeviceToHost, ctx->stream));
+      }
+      ctx->sync();
+    }
+  });
+}
+
+int tg_sampler_trace(tg_sampler* s, const uint64_t* tid, uint64_t ntid, const uint32_t* fanouts,
+                     uint32_t nf, uint64_t batch_size, uint64_t epochs, uint64_t rng_seed,
+                     int dedup_per_batch, uint64_t* counts) {
+  return guard([&] {
+    // run_training_trace, sampling.cpp:92-140 (tid already validated by the caller's
+    // TrainIdSet; ids are range-checked here)
+    check_fanouts(fanouts, nf);
+    if (ntid == 0) domain_error("run_training_trace: train id set is empty");
+    if (batch_size < 1) domain_error("batch_size must be >= 1");
+    if (epochs < 1) domain_error("epochs must be >= 1");
+    tg_ctx* ctx = s->ctx;
+    DeviceGuard dg(ctx->device);
+    const uint64_t n = s->n;
+    std::vector<uint64_t> order(ntid);
+    if (is_device_ptr(tid)) {
+      TGB_CUDA(cudaMemcpy(order.data(), tid, 8 * ntid, cudaMemcpyDeviceToHost));
+    } else {
+      std::memcpy(order.data(), tid, 8 * ntid);
+    }
+    for (uint64_t id : order)
+      if (id >= n) domain_error("train id " + std::to_string(id) + " out of range");
+    const std::vector<uint64_t> ids = order;
+    DevOut<uint64_t> c(ctx, counts, n, kStageOut0);
+    TGB_CUDA(cudaMemsetAsync(c.dev(), 0, 8 * std::max<uint64_t>(n, 1), ctx->stream));
+    ExpandOut o;
+    o.counts = reinterpret_cast<unsigned long long*>(c.dev());
+    o.count_raw = dedup_per_batch ? 0 : 1;
+    uint64_t* dorder = ctx->scratch_t<uint64_t>(kStageIn1, ntid);
+    for (uint64_t epoch = 0; epoch < epochs; ++epoch) {
+      tg_epoch_order(ids.data(), ntid, rng_seed, epoch, order.data());  // sampling.cpp:106-109
+      TGB_CUDA(cudaMemcpyAsync(dorder, order.data(), 8 * ntid, cudaMemcpyHostToDevice,
+                               ctx->stream));
+      const uint64_t nb = (ntid + batch_size - 1) / batch_size;
+      for (uint64_t b = 0; b < nb; ++b) {
+        const uint64_t beg = b * batch_size, len = std::min(batch_size, ntid - beg);
+        expand(s, dorder + beg, len, fanouts, nf, rng_seed, epoch, b, o);
+      }
+    }
+    c.finish();
   });
 }
 

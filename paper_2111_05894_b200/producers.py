@@ -115,6 +115,39 @@ class GpuSampler:
                                           tg._len(dst), C.byref(cnt)))
         return int(cnt.value) if out is not None else dst[:cnt.value].copy()
 
+    def minibatch_raw(self, seeds, fanouts: Sequence[int], seed: int, epoch: int, batch: int):
+        """(members, raw draws) — build_minibatch with raw_draws (sampling.hpp:48-55);
+        the raw draws come back sorted (their order is unspecified)."""
+        tg = self.tg
+        sd = tg._u64(seeds)
+        fo = np.ascontiguousarray(np.asarray(list(fanouts), np.uint32))
+        cap = self.n
+        raw_cap = len(sd) + sum(int(f) for f in fanouts) * self.n
+        raw_cap = min(raw_cap, 1 << 24)
+        out = np.empty(max(cap, 1), np.uint64)
+        raw = np.empty(max(raw_cap, 1), np.uint64)
+        cnt, rn = C.c_uint64(), C.c_uint64()
+        tg._check(LIB.tg_sample_minibatch_raw(self.h, tg._nonempty(sd, np.uint64), tg._len(sd),
+                                              fo.ctypes.data if len(fo) else None, len(fo),
+                                              int(seed), int(epoch), int(batch), out.ctypes.data,
+                                              cap, C.byref(cnt), raw.ctypes.data, raw_cap,
+                                              C.byref(rn)))
+        return out[:cnt.value].copy(), np.sort(raw[:rn.value])
+
+    def trace(self, tid, fanouts: Sequence[int], batch_size: int, epochs: int, seed: int,
+              dedup_per_batch: bool = True, out=None):
+        """run_training_trace (sampling.cpp:92-140) on the device: per-node
+        access counts (numpy u64, or into the device tensor `out`)."""
+        tg = self.tg
+        ids = tg._u64(tid.ids if isinstance(tid, TrainIdSet) else tid)
+        fo = np.ascontiguousarray(np.asarray(list(fanouts), np.uint32))
+        dst = out if out is not None else np.empty(max(self.n, 1), np.uint64)
+        tg._check(LIB.tg_sampler_trace(self.h, tg._nonempty(ids, np.uint64), tg._len(ids),
+                                       fo.ctypes.data if len(fo) else None, len(fo),
+                                       int(batch_size), int(epochs), int(seed),
+                                       int(bool(dedup_per_batch)), tg._ptr(dst)))
+        return dst if out is not None else dst[:self.n]
+
     def close(self):
         if getattr(self, "h", None):
             LIB.tg_sampler_destroy(self.h)

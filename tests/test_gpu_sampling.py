@@ -77,3 +77,43 @@ def test_rmat_c1_shape_minibatches(tg, ctx):
     s = producers.GpuSampler(tg.CsrGraph(go, gt), ctx=ctx)
     for b, w in enumerate(want):
         assert np.array_equal(s.minibatch(order[b * 1024:(b + 1) * 1024], [10, 15], 7, 0, b), w)
+
+
+@pytest.mark.parametrize("dedup", [True, False])
+def test_training_trace_counts_bit_exact(tg, ctx, dedup):
+    """run_training_trace (sampling.cpp:92-140) on the GPU: identical per-node
+    access counts, with and without per-batch de-duplication, over 2 epochs."""
+    from paper_2111_05894_b200 import producers
+    ref = oracle.ref()
+    if ref is None:
+        pytest.skip("needs the reference build for run_training_trace")
+    n = 4000
+    off, tgt = _graph(n, 11, hubs=[(0, 2000), (3, 70)])
+    go, gt = ref.transpose(off, tgt)
+    tid = oracle.port().draw_random_train_ids(n, 700, 5)
+    want = ref.run_training_trace(off, tgt, tid, [5, 10, 3], 50, 2, 9, dedup)
+    s = producers.GpuSampler(tg.CsrGraph(go, gt), ctx=ctx)
+    got = s.trace(tid, [5, 10, 3], 50, 2, 9, dedup)
+    assert np.array_equal(got, want)
+
+
+def test_raw_draws_multiset(tg, ctx):
+    """raw_draws: each seed once as given plus every draw — its multiset summed
+    over an epoch equals the reference's raw-access trace counts."""
+    from paper_2111_05894_b200 import producers
+    ref = oracle.ref()
+    if ref is None:
+        pytest.skip("needs the reference build for run_training_trace")
+    n = 3000
+    off, tgt = _graph(n, 12, hubs=[(1, 1500)])
+    go, gt = ref.transpose(off, tgt)
+    tid = oracle.port().draw_random_train_ids(n, 300, 6)
+    want = ref.run_training_trace(off, tgt, tid, [4, 7], 64, 1, 3, False)
+    s = producers.GpuSampler(tg.CsrGraph(go, gt), ctx=ctx)
+    order = producers.epoch_order(tid, 3, 0)
+    counts = np.zeros(n, np.uint64)
+    for b in range((len(order) + 63) // 64):
+        mem, raw = s.minibatch_raw(order[b * 64:(b + 1) * 64], [4, 7], 3, 0, b)
+        assert np.array_equal(mem, np.unique(raw))
+        np.add.at(counts, raw.astype(np.int64), np.uint64(1))
+    assert np.array_equal(counts, want)
