@@ -19,6 +19,7 @@
 #pragma once
 
 #include <cstdint>
+#include <initializer_list>
 #include <span>
 #include <stdexcept>
 #include <string>
@@ -122,13 +123,96 @@ CsrGraph reorder_graph(const CsrGraph& g, const NodePermutation& perm);
 CsrGraph sequential_reorder_oracle(const CsrGraph& g, const NodePermutation& perm);
 FeatureMatrix reorder_features(const FeatureMatrix& f, const NodePermutation& perm);
 
-// ------------------------------------------------------------- sampling
-// The one sampling type the tiering API consumes (reference sampling.hpp:31-34).
+// --------------------------------------------------------- graph helpers
+// reference csr_graph.hpp:48 — canonical transpose (host; standalone library
+// only, a drop-in build keeps the reference's csr_graph.cpp).
+CsrGraph transpose(const CsrGraph& g);
+
+// ------------------------------------------------------------------- rng
+// reference rng.hpp:13-73: splitmix64, stream keys and the counter-based
+// stream the samplers draw from (header-only there, restated here).
+constexpr std::uint64_t mix64(std::uint64_t x) {
+  x += 0x9E3779B97F4A7C15ull;
+  x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ull;
+  x = (x ^ (x >> 27)) * 0x94D049BB133111EBull;
+  return x ^ (x >> 31);
+}
+
+inline std::uint64_t derive_stream_key(std::uint64_t seed,
+                                       std::initializer_list<std::uint64_t> coords) {
+  std::uint64_t key = mix64(seed ^ 0x6A09E667F3BCC908ull);
+  for (const std::uint64_t c : coords) key = mix64(key ^ mix64(c));
+  return key;
+}
+
+class RngStream {
+ public:
+  explicit RngStream(std::uint64_t key) : counter_(key) {}
+  std::uint64_t next_u64() { return mix64(counter_++); }
+  // uniform in [0, bound): Lemire's multiply-shift, rejecting the biased low part
+  std::uint64_t next_below(std::uint64_t bound) {
+    unsigned __int128 prod = static_cast<unsigned __int128>(next_u64()) * bound;
+    if (static_cast<std::uint64_t>(prod) < bound) {
+      const std::uint64_t floor = (0 - bound) % bound;
+      while (static_cast<std::uint64_t>(prod) < floor)
+        prod = static_cast<unsigned __int128>(next_u64()) * bound;
+    }
+    return static_cast<std::uint64_t>(prod >> 64);
+  }
+  double next_unit() { return static_cast<double>(next_u64() >> 11) * 0x1.0p-53; }
+
+ private:
+  std::uint64_t counter_;
+};
+
+// reference rng.cpp:8-40 (Floyd's k-subset; standalone library only).
+void sample_index_subset(RngStream& rng, std::uint64_t population, std::uint64_t k,
+                         std::vector<std::uint64_t>& out);
+
+template <typename T>
+void shuffle_in_place(RngStream& rng, std::vector<T>& items) {  // rng.hpp:67-73
+  for (std::size_t i = items.size(); i > 1; --i)
+    std::swap(items[i - 1], items[static_cast<std::size_t>(rng.next_below(i))]);
+}
+
+// -------------------------------------------------------------- sampling
+// reference sampling.hpp:12-72. build_minibatch and run_training_trace run on
+// the GPU (csrc/sampling.cu, bit-identical); sample_in_neighbors (one node,
+// a caller-owned stream) and cumulative_access_curve stay on the host.
+struct FanoutSpec {
+  std::vector<std::uint32_t> fanouts;
+};
+void validate_fanouts(const FanoutSpec& spec);
+
+struct TraceConfig {
+  std::uint64_t batch_size = 1000;
+  std::uint64_t epochs = 1;
+  std::uint64_t rng_seed = 0;
+  bool dedup_per_batch = true;
+};
+
 struct AccessCounter {
   std::vector<std::uint64_t> counts;
   std::uint64_t total = 0;
 };
 AccessCounter make_access_counter(std::vector<std::uint64_t> counts);
+
+struct BatchRng {
+  std::uint64_t rng_seed = 0;
+  std::uint64_t epoch = 0;
+  std::uint64_t batch_index = 0;
+  RngStream stream(std::uint32_t layer, NodeId node) const;
+};
+
+std::vector<NodeId> sample_in_neighbors(const CsrGraph& gt, NodeId node, std::uint32_t fanout,
+                                        RngStream& rng);
+std::vector<NodeId> build_minibatch(const CsrGraph& gt, std::span<const NodeId> seeds,
+                                    const FanoutSpec& fanouts, const BatchRng& rng,
+                                    std::vector<NodeId>* raw_draws = nullptr);
+AccessCounter run_training_trace(const CsrGraph& g, const TrainIdSet& tid,
+                                 const FanoutSpec& fanouts, const TraceConfig& cfg);
+std::vector<double> cumulative_access_curve(const AccessCounter& counter,
+                                            std::span<const NodeId> ordering);
 
 // -------------------------------------------------------------- tiering
 // reference tiering.hpp:16-121.

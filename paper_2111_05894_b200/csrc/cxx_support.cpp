@@ -2,6 +2,7 @@
 // library needs so that tiergraph.hpp is self-sufficient. A drop-in build
 // against the reference headers links the reference's own csr_graph.cpp,
 // feature_matrix.cpp and sampling.cpp instead, and does not compile this file.
+#include <algorithm>
 #include <string>
 #include <utility>
 #include <vector>
@@ -29,12 +30,34 @@ void validate_features(const FeatureMatrix& f) {
                       " bytes, expected " + std::to_string(want));
 }
 
-// sampling.cpp:27-33 — total is the sum of the counts.
-AccessCounter make_access_counter(std::vector<std::uint64_t> counts) {
-  AccessCounter c;
-  for (const std::uint64_t v : counts) c.total += v;
-  c.counts = std::move(counts);
-  return c;
+// csr_graph.cpp:67-80 — canonical transpose, host (the restatement in
+// csrc/host_producers.cpp: rows in ascending source order).
+CsrGraph transpose(const CsrGraph& g) {
+  const uint64_t n = g.num_nodes();
+  CsrGraph t;
+  t.offsets.assign(n + 1, 0);
+  t.targets.resize(g.num_edges());
+  if (n == 0) return t;
+  static const uint64_t kNone = 0;
+  uint64_t scratch = 0;
+  b200::check(tg_transpose_host(g.offsets.data(), g.targets.empty() ? &kNone : g.targets.data(),
+                                n, t.offsets.data(), t.targets.empty() ? &scratch : t.targets.data()));
+  return t;
+}
+
+// rng.cpp:8-40 — Floyd's k-subset: draw t in [0, j] for j = pop-k .. pop-1 and
+// take t unless already taken, else j.
+void sample_index_subset(RngStream& rng, std::uint64_t population, std::uint64_t k,
+                         std::vector<std::uint64_t>& out) {
+  out.clear();
+  if (k >= population) {
+    for (std::uint64_t i = 0; i < population; ++i) out.push_back(i);
+    return;
+  }
+  for (std::uint64_t j = population - k; j < population; ++j) {
+    const std::uint64_t t = rng.next_below(j + 1);
+    out.push_back(std::find(out.begin(), out.end(), t) == out.end() ? t : j);
+  }
 }
 
 }  // namespace tiergraph
