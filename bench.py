@@ -487,7 +487,7 @@ def run_ours(args):
             "roofline": {"bound": bound, "achieved": round(achieved, 2),
                          "peak": round(peak_eff, 2), "unit": "GB/s",
                          "frac": round(t_star / t_launch, 4), "traffic": traffic,
-                         "kernel": "gather_kernel<uint4> (K8)",
+                         "kernel": "gather_bulk_kernel (K8: TMA bulk copies, 128 B-padded cold tier)",
                          "algorithmic_bytes_per_launch": int(alg_bytes),
                          "mixed": {"hbm_gbs": hbm_peak, "hbm_src": hbm_src,
                                    "pcie_gbs": round(pcie_peak, 2),
