@@ -139,6 +139,21 @@ int tg_pagerank_step_async(tg_ctx* ctx, const tg_graph* g, const uint32_t* indeg
                            double* score_out_dev, uint64_t row_begin, uint64_t row_end,
                            int last);
 
+/* Fused exchange for a partitioned run: the step
+ * also stores each of its rows into every peer's norm_out / score_out vector
+ * (device pointers valid on this device: peer-mapped or CUDA-IPC), so no
+ * all-gather follows. tg_peer_barrier_async then releases those stores, adds
+ * 1 to each peer's arrival counter (peer_flags, u32) and waits on this
+ * device until local_flag >= target; a wait over ~2 s sets *err_dev = 1 and
+ * returns. With G ranks, target after step s (1-based) is s * (G - 1). */
+int tg_pagerank_step_peers_async(tg_ctx* ctx, const tg_graph* g, const uint32_t* indeg_dev,
+                                 double damp, const double* norm_in_dev, double* norm_out_dev,
+                                 double* score_out_dev, uint64_t row_begin, uint64_t row_end,
+                                 int last, double* const* peer_norm_out,
+                                 double* const* peer_score_out, uint32_t n_peers);
+int tg_peer_barrier_async(tg_ctx* ctx, uint32_t* local_flag, uint32_t* const* peer_flags,
+                          uint32_t n_peers, uint32_t target, uint32_t* err_dev);
+
 /* scoring.hpp:49 score_ordering (scoring.cpp:104-115): ids by descending
  * score, ties by ascending id. scores/out host|device. TG_ERR_DOMAIN names the
  * first non-finite or negative score. */

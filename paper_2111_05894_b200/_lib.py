@@ -75,6 +75,8 @@ SIGNATURES = {
     "tg_weighted_reverse_pagerank": (I32, [vp, vp, U32, D, vp, U64, vp]),
     "tg_pagerank_prepare_async": (I32, [vp, vp, vp, U64, vp, vp]),
     "tg_pagerank_step_async": (I32, [vp, vp, vp, D, vp, vp, vp, U64, U64, I32]),
+    "tg_pagerank_step_peers_async": (I32, [vp, vp, vp, D, vp, vp, vp, U64, U64, I32, vp, vp, U32]),
+    "tg_peer_barrier_async": (I32, [vp, vp, vp, U32, U32, vp]),
     "tg_score_ordering": (I32, [vp, vp, U64, vp]),
     "tg_permutation_from_scores": (I32, [vp, vp, U64, vp, vp]),
     "tg_validate_permutation": (I32, [vp, vp, U64]),

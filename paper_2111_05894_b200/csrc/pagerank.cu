@@ -188,6 +188,11 @@ struct PrStepArgs {
   uint64_t row_begin, row_end;
   double base, damp;
   int last;
+  // fused exchange: the same row also goes to every peer's norm / score
+  // vector (NVLink P2P stores), replacing the all-gather of a partitioned run
+  uint32_t n_peers;
+  double* peer_norm[TG_MAX_DEVICES];
+  double* peer_score[TG_MAX_DEVICES];
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -214,9 +219,12 @@ __device__ __forceinline__ void finish_row(const PrStepArgs& a, uint64_t r, doub
   const double nx = __dadd_rn(a.base, __dmul_rn(a.damp, acc));  // scoring.cpp:69, no FMA
   if (a.last) {
     a.score_out[r] = nx;
+    for (uint32_t p = 0; p < a.n_peers; ++p) a.peer_score[p][r] = nx;
   } else {
     const uint32_t d = a.deg[r];
-    a.norm_out[r] = __ddiv_rn(nx, static_cast<double>(d > 1u ? d : 1u));  // scoring.cpp:61
+    const double v = __ddiv_rn(nx, static_cast<double>(d > 1u ? d : 1u));  // scoring.cpp:61
+    a.norm_out[r] = v;
+    for (uint32_t p = 0; p < a.n_peers; ++p) a.peer_norm[p][r] = v;
   }
 }
 
@@ -661,6 +669,32 @@ __global__ void __launch_bounds__(256) gather_floor_kernel(const uint32_t* __res
   if (acc == -1.0) sink[0] = acc;  // never true: keeps the loads alive
 }
 
+// Cross-GPU barrier of the fused exchange: release this rank's P2P stores
+// (everything earlier on the stream), bump every peer's arrival counter, then
+// wait until this rank's counter reaches `target`. A wait longer than ~2 s
+// sets *err and returns instead of hanging the device.
+struct PeerFlags {
+  unsigned* peer[TG_MAX_DEVICES];
+};
+__global__ void peer_barrier_kernel(unsigned* local, PeerFlags peers, uint32_t n, unsigned target,
+                                    unsigned* err) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  __threadfence_system();
+  for (uint32_t p = 0; p < n; ++p) atomicAdd_system(peers.peer[p], 1u);
+  const long long t0 = clock64();
+  while (true) {
+    unsigned v;
+    asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(local) : "memory");
+    if (v >= target) break;
+    if (clock64() - t0 > 4000000000ll) {
+      atomicExch(err, 1u);
+      break;
+    }
+    __nanosleep(200);
+  }
+  __threadfence_system();
+}
+
 unsigned long long read_flag(tg_ctx* ctx, unsigned long long* dflag) {
   unsigned long long h = 0;
   TGB_CUDA(cudaMemcpyAsync(&h, dflag, sizeof(h), cudaMemcpyDeviceToHost, ctx->stream));
@@ -719,7 +753,8 @@ const tg_graph::Sched& schedule(tg_ctx* ctx, const tg_graph* g, uint64_t rb, uin
 
 void pagerank_step(tg_ctx* ctx, const tg_graph* g, const uint32_t* deg, double damp,
                    const double* nin, double* nout, double* sout, uint64_t rb, uint64_t re,
-                   int last) {
+                   int last, uint32_t n_peers = 0, double* const* peer_norm = nullptr,
+                   double* const* peer_score = nullptr) {
   if (re <= rb) return;
   const tg_graph::Sched& sc = schedule(ctx, g, rb, re);
   PrStepArgs a;
@@ -740,6 +775,11 @@ void pagerank_step(tg_ctx* ctx, const tg_graph* g, const uint32_t* deg, double d
   a.base = (1.0 - damp) / static_cast<double>(g->n);  // scoring.cpp:53
   a.damp = damp;
   a.last = last;
+  a.n_peers = n_peers;
+  for (uint32_t p = 0; p < TG_MAX_DEVICES; ++p) {
+    a.peer_norm[p] = p < n_peers ? peer_norm[p] : nullptr;
+    a.peer_score[p] = p < n_peers ? peer_score[p] : nullptr;
+  }
   const uint64_t c_ctas = (a.m - sc.nB + kPrWarps * 32 - 1) / (kPrWarps * 32);
   if (sc.nA) {
     // class A on the side stream, concurrently with classes B and C
@@ -944,6 +984,32 @@ int tg_pagerank_prepare_async(tg_ctx* ctx, const tg_graph* g, const uint64_t* ti
     // train ids must be in range here (the synchronous entry points check them)
     auto* bad = ctx->scratch_t<unsigned long long>(kSmall, 1);
     pagerank_prepare(ctx, g, tid_dev, ntid, indeg_dev, norm0_dev, bad);
+  });
+}
+
+int tg_pagerank_step_peers_async(tg_ctx* ctx, const tg_graph* g, const uint32_t* indeg_dev,
+                                 double damp, const double* norm_in_dev, double* norm_out_dev,
+                                 double* score_out_dev, uint64_t row_begin, uint64_t row_end,
+                                 int last, double* const* peer_norm_out,
+                                 double* const* peer_score_out, uint32_t n_peers) {
+  return guard([&] {
+    if (row_end > g->n || row_begin > row_end) domain_error("pagerank step: bad row range");
+    if (n_peers >= TG_MAX_DEVICES) domain_error("pagerank step: too many peers");
+    DeviceGuard dg(ctx->device);
+    pagerank_step(ctx, g, indeg_dev, damp, norm_in_dev, norm_out_dev, score_out_dev, row_begin,
+                  row_end, last, n_peers, peer_norm_out, peer_score_out);
+  });
+}
+
+int tg_peer_barrier_async(tg_ctx* ctx, uint32_t* local_flag, uint32_t* const* peer_flags,
+                          uint32_t n_peers, uint32_t target, uint32_t* err_dev) {
+  return guard([&] {
+    if (n_peers >= TG_MAX_DEVICES) domain_error("peer barrier: too many peers");
+    DeviceGuard dg(ctx->device);
+    PeerFlags pf{};
+    for (uint32_t p = 0; p < n_peers; ++p) pf.peer[p] = peer_flags[p];
+    peer_barrier_kernel<<<1, 32, 0, ctx->stream>>>(local_flag, pf, n_peers, target, err_dev);
+    TGB_LAUNCHED();
   });
 }
 

@@ -9,7 +9,16 @@ leaves its rank, so the result is bit-identical to the single-GPU run and to
 the reference for any number of ranks (the reference's guarantee for any
 worker count, parallel.hpp:5-7).
 
-The driver is written against a small "stepper" interface so that the
+Two exchanges are provided:
+  * `reverse_pagerank_partitioned` / `weighted_reverse_pagerank_multi`: one
+    process per GPU, an all-gather (NCCL) after every step — the baseline;
+  * `weighted_reverse_pagerank_peers`: the fused B200 path — each step's
+    epilogue stores its rows straight into every rank's `norm` vector (P2P
+    stores over NVLink/NVSwitch), and a device-side arrival barrier
+    (tg_peer_barrier_async) replaces the collective, so the exchange overlaps
+    the SpMV row by row. One process drives all ranks (one context each).
+
+The all-gather driver is written against a small "stepper" interface so that the
 partitioning and exchange logic runs unchanged over gloo in the CPU tests
 (tests/test_distributed.py); the product stepper, `DeviceStepper`, launches
 this library's kernels through the C-ABI (tg_pagerank_prepare_async /
@@ -115,3 +124,62 @@ def weighted_reverse_pagerank_multi(g, cfg, tid, ctx=None, group=None):
     tid_d = torch.as_tensor(np.asarray(ids, np.uint64).astype(np.int64), device=st.dev)
     return reverse_pagerank_partitioned(st, g.num_nodes(), cfg.iterations, cfg.damp, tid_d,
                                         len(ids), group)
+
+
+def weighted_reverse_pagerank_peers(g, cfg, tid, ctxs, timeout_check=True):
+    """Partitioned PageRank with the FUSED exchange, one process driving
+    several ranks (one context each; ranks may share a GPU): every step writes
+    its rows straight into all ranks' `norm` vectors (P2P stores over NVLink
+    between GPUs) and a device-side barrier replaces the all-gather
+    (tg_pagerank_step_peers_async / tg_peer_barrier_async). Returns the full
+    score vector of every rank (all identical, bit-exact to one GPU).
+    `tid=None` runs the unweighted recurrence."""
+    import ctypes as C
+    import torch
+    from . import tiergraph as tg
+    from ._lib import LIB
+    G = len(ctxs)
+    n = g.num_nodes()
+    if G >= 16:
+        raise tg.DomainError("at most 15 peers")
+    devs = [torch.device("cuda", c.device) for c in ctxs]
+    for a in range(G):
+        for b in range(G):
+            if ctxs[a].device != ctxs[b].device:
+                tg._check(LIB.tg_enable_peer_access(ctxs[a].device, ctxs[b].device))
+    chunk, blocks = row_blocks(n, G)
+    gh = [g.device(c) for c in ctxs]
+    deg = [torch.empty(max(n, 1), dtype=torch.int32, device=d) for d in devs]
+    bufs = [[torch.empty(max(n, 1), dtype=torch.float64, device=d) for _ in range(3)] for d in devs]
+    flags = [torch.zeros(2, dtype=torch.int32, device=d) for d in devs]  # [arrivals, err]
+    ids = None if tid is None else (tid.ids if isinstance(tid, tg.TrainIdSet) else tid)
+    for r, c in enumerate(ctxs):
+        td = None if ids is None else torch.as_tensor(np.asarray(ids, np.uint64).astype(np.int64),
+                                                      device=devs[r])
+        tg._check(LIB.tg_pagerank_prepare_async(c.h, gh[r], None if td is None else td.data_ptr(),
+                                                0 if ids is None else len(ids),
+                                                deg[r].data_ptr(), bufs[r][0].data_ptr()))
+        c.sync()  # keeps td alive until the prepare ran
+    cur = 0
+    for it in range(cfg.iterations):
+        last = int(it + 1 == cfg.iterations)
+        nxt = 1 - cur
+        for r, c in enumerate(ctxs):
+            peers = [q for q in range(G) if q != r]
+            pn = (C.c_void_p * 16)(*[bufs[q][nxt].data_ptr() for q in peers])
+            ps = (C.c_void_p * 16)(*[bufs[q][2].data_ptr() for q in peers])
+            rb, re = blocks[r]
+            tg._check(LIB.tg_pagerank_step_peers_async(
+                c.h, gh[r], deg[r].data_ptr(), float(cfg.damp), bufs[r][cur].data_ptr(),
+                bufs[r][nxt].data_ptr(), bufs[r][2].data_ptr(), rb, re, last, pn, ps,
+                len(peers)))
+        for r, c in enumerate(ctxs):
+            pf = (C.c_void_p * 16)(*[flags[q].data_ptr() for q in range(G) if q != r])
+            tg._check(LIB.tg_peer_barrier_async(c.h, flags[r].data_ptr(), pf, G - 1,
+                                                (it + 1) * (G - 1), flags[r].data_ptr() + 4))
+        cur = nxt
+    for c in ctxs:
+        c.sync()
+    if timeout_check and any(int(f[1].item()) for f in flags):
+        raise tg.TierGraphError("peer barrier timed out")
+    return [b[2][:n] for b in bufs]

@@ -207,3 +207,24 @@ def test_partitioned_driver_single_rank_on_device(tg, ctx):
     want = tg.weighted_reverse_pagerank(g, tg.PagerankConfig(), tg.TrainIdSet(tid))
     got = D.weighted_reverse_pagerank_multi(g, tg.PagerankConfig(), tg.TrainIdSet(tid), ctx=ctx)
     assert got.cpu().numpy().tobytes() == want.tobytes()
+
+
+@pytest.mark.parametrize("ranks", [2, 3, 4])
+def test_fused_peer_exchange_virtual_ranks(tg, ctx, ranks):
+    """The fused exchange (rows stored straight into every rank's `norm`, a
+    device barrier instead of the all-gather) with `ranks` contexts on one
+    GPU: every rank ends with the single-GPU scores, bit for bit."""
+    from paper_2111_05894_b200 import distributed as D
+    port = oracle.port()
+    n = 12000
+    off, tgt = _hub_graph(n, [(0, 9000), (4000, 5000), (11999, 3000)], 31)
+    g = G(tg, off, tgt)
+    tid = port.draw_random_train_ids(n, 1200, 2)
+    want = tg.weighted_reverse_pagerank(g, tg.PagerankConfig(), tg.TrainIdSet(tid))
+    ctxs = [tg.Context(ctx.device) for _ in range(ranks)]
+    outs = D.weighted_reverse_pagerank_peers(g, tg.PagerankConfig(), tg.TrainIdSet(tid), ctxs)
+    for o in outs:
+        assert o.cpu().numpy().tobytes() == want.tobytes()
+    un = D.weighted_reverse_pagerank_peers(g, tg.PagerankConfig(3, 0.85), None, ctxs)
+    want_un = tg.reverse_pagerank(g, tg.PagerankConfig(3, 0.85))
+    assert all(o.cpu().numpy().tobytes() == want_un.tobytes() for o in un)
