@@ -99,3 +99,20 @@ def expected_rows(old_ids: np.ndarray, dim: int) -> np.ndarray:
     """Closed-form rows for old ids (to verify gathers without a second copy)."""
     base = (mix64_np(np.asarray(old_ids, np.uint64)) >> np.uint64(40)).astype(np.float32)
     return base[:, None] + np.arange(dim, dtype=np.float32)[None, :]
+
+
+def test_features_pinned_gpu(num_rows: int, dim: int, out: np.ndarray, device="cuda",
+                             rows_per_chunk=1 << 21):
+    """The same closed-form f32 fill as test_features, computed on the GPU and
+    copied chunk by chunk into `out` (a pinned host buffer of num_rows*dim*4
+    bytes) — for the papers100M-shaped matrix (57 GB) a numpy fill is minutes."""
+    import torch
+    dst = torch.from_numpy(out.reshape(-1).view(np.float32)).view(num_rows, dim)
+    cols = torch.arange(dim, dtype=torch.float32, device=device)
+    for r0 in range(0, num_rows, rows_per_chunk):
+        r1 = min(num_rows, r0 + rows_per_chunk)
+        r = torch.arange(r0, r1, dtype=torch.int64, device=device)
+        base = ((mix64_torch(r) >> 40) & ((1 << 24) - 1)).to(torch.float32)
+        dst[r0:r1].copy_(base[:, None] + cols[None, :])
+    torch.cuda.synchronize()
+    return out
