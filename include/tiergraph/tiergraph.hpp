@@ -3,11 +3,12 @@
 // Same namespace, type layouts and signatures as the reference C++ toolkit
 // (arXiv 2111.05894 `tiergraph`, proj/include/tiergraph/*.hpp) for the part
 // of it on the data-tiering hot path: scoring (hot-set prediction), reorder
-// (permutation and row layout) and tiering (address map, accounting, replay).
-// Every function runs on the GPU through the C-ABI in tg_capi.h; the bodies
-// live in paper_2111_05894_b200/csrc/cxx_api.cpp, which compiles unchanged
-// against either this header or the reference's own headers (that second
-// build is the drop-in proof).
+// (permutation and row layout), tiering (address map, accounting, replay),
+// and the sampler that produces the gather's id lists. The computations run
+// on the GPU through the C-ABI in tg_capi.h; the bodies live in
+// paper_2111_05894_b200/csrc/cxx_api.cpp and cxx_sampling.cpp, which compile
+// unchanged against either this header or the reference's own headers (that
+// second build is the drop-in proof).
 //
 // The per-subsystem header names of the reference (tiergraph/scoring.hpp, ...)
 // exist in this directory as forwarders to this file.

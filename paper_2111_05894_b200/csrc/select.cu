@@ -95,47 +95,52 @@ __global__ void __launch_bounds__(kRsWarps * 32) digit_count_kernel(
     if (i < n) atomicAdd(&h[(keys[i] >> shift) & 0xff], 1u);
   }
   __syncthreads();
-  counts[(uint64_t)threadIdx.x * nblk + blockIdx.x] = h[threadIdx.x];
+  counts[(uint64_t)blockIdx.x * 256 + threadIdx.x] = h[threadIdx.x];  // block-major
 }
 
-// Exclusive scan of the digit-major count matrix (256 x nblk) in one CTA.
+// Per-digit exclusive scan over the blocks: CTA d scans column d of the
+// block-major count matrix [nblk][256] in place and leaves the digit's total
+// in totals[d]. (The digit bases are an exclusive scan of the 256 totals,
+// done by every scatter CTA in its prologue.)
 __global__ void __launch_bounds__(1024) count_scan_kernel(uint32_t* __restrict__ counts,
-                                                          uint64_t m, int pass,
-                                                          const RadixPlan* __restrict__ plan) {
+                                                          uint32_t nblk, int pass,
+                                                          const RadixPlan* __restrict__ plan,
+                                                          uint32_t* __restrict__ totals) {
   if (plan->skip[pass]) return;
   __shared__ uint32_t warp_tot[32];
-  const uint64_t per = (m + blockDim.x - 1) / blockDim.x;
-  const uint64_t b = threadIdx.x * per;
-  const uint64_t e = b + per < m ? b + per : m;
-  uint32_t local = 0;
-  for (uint64_t i = b; i < e; ++i) local += counts[i];
-  // block exclusive scan of `local`
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  uint32_t incl = local;
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
-    if (lane >= o) incl += y;
-  }
-  if (lane == 31) warp_tot[w] = incl;
+  __shared__ uint32_t carry;
+  const int d = blockIdx.x, lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  if (threadIdx.x == 0) carry = 0;
   __syncthreads();
-  if (w == 0) {
-    uint32_t t = lane < (int)(blockDim.x / 32) ? warp_tot[lane] : 0;
-    uint32_t ti = t;
+  for (uint32_t b0 = 0; b0 < nblk; b0 += blockDim.x) {
+    const uint32_t b = b0 + threadIdx.x;
+    const uint32_t c = b < nblk ? counts[(uint64_t)b * 256 + d] : 0u;
+    uint32_t incl = c;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
-      const uint32_t y = __shfl_up_sync(0xffffffffu, ti, o);
-      if (lane >= o) ti += y;
+      const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += y;
     }
-    warp_tot[lane] = ti - t;
+    if (lane == 31) warp_tot[w] = incl;
+    __syncthreads();
+    if (w == 0) {
+      const uint32_t t = lane < (int)(blockDim.x / 32) ? warp_tot[lane] : 0u;
+      uint32_t ti = t;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, ti, o);
+        if (lane >= o) ti += y;
+      }
+      warp_tot[lane] = ti - t;
+    }
+    __syncthreads();
+    const uint32_t base = carry;
+    if (b < nblk) counts[(uint64_t)b * 256 + d] = base + warp_tot[w] + incl - c;
+    __syncthreads();
+    if (threadIdx.x == blockDim.x - 1) carry = base + warp_tot[w] + incl;
+    __syncthreads();
   }
-  __syncthreads();
-  uint32_t run = warp_tot[w] + incl - local;
-  for (uint64_t i = b; i < e; ++i) {
-    const uint32_t c = counts[i];
-    counts[i] = run;
-    run += c;
-  }
+  if (threadIdx.x == 0) totals[d] = carry;
 }
 
 // Stable block-local ranking (warp rounds in index order + per-warp digit
@@ -143,7 +148,7 @@ __global__ void __launch_bounds__(1024) count_scan_kernel(uint32_t* __restrict__
 __global__ void __launch_bounds__(kRsWarps * 32) scatter_kernel(
     uint64_t* __restrict__ k0, uint32_t* __restrict__ v0, uint64_t* __restrict__ k1,
     uint32_t* __restrict__ v1, uint64_t n, int pass, const RadixPlan* __restrict__ plan,
-    const uint32_t* __restrict__ offs, uint32_t nblk) {
+    const uint32_t* __restrict__ offs, uint32_t nblk, const uint32_t* __restrict__ totals) {
   if (plan->skip[pass]) return;
   const bool from1 = plan->src[pass] != 0;
   const uint64_t* kin = from1 ? k1 : k0;
@@ -153,7 +158,22 @@ __global__ void __launch_bounds__(kRsWarps * 32) scatter_kernel(
   __shared__ uint32_t wcnt[kRsWarps][256];
   __shared__ uint32_t doff[256];
   for (int i = threadIdx.x; i < kRsWarps * 256; i += blockDim.x) (&wcnt[0][0])[i] = 0;
-  doff[threadIdx.x] = offs[(uint64_t)threadIdx.x * nblk + blockIdx.x];
+  {  // digit base (exclusive scan of the 256 totals) + this block's column prefix
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const uint32_t t = totals[threadIdx.x];
+    uint32_t incl = t;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += y;
+    }
+    __shared__ uint32_t wt[kRsWarps];
+    if (lane == 31) wt[w] = incl;
+    __syncthreads();
+    uint32_t before = 0;
+    for (int k = 0; k < w; ++k) before += wt[k];
+    doff[threadIdx.x] = before + incl - t + offs[(uint64_t)blockIdx.x * 256 + threadIdx.x];
+  }
   __syncthreads();
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const uint32_t lt = (1u << lane) - 1u;
@@ -263,7 +283,7 @@ void sort_rows_by_length(tg_ctx* ctx, const uint32_t* off, uint64_t rb, uint64_t
   // private temporaries (stream-ordered allocations): callers may hold the
   // context's scratch slots across this call
   const size_t bytes = 2 * 8 * m + 2 * 4 * m + 4ull * 256 * nblk + 64 + sizeof(RadixPlan) +
-                       8 * 256 * 4 + 256;
+                       8 * 256 * 4 + 256 * 4 + 256;
   char* base = nullptr;
   TGB_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&base), bytes, ctx->stream));
   auto align = [](char* p) { return reinterpret_cast<char*>((reinterpret_cast<uintptr_t>(p) + 15) & ~uintptr_t(15)); };
@@ -274,7 +294,8 @@ void sort_rows_by_length(tg_ctx* ctx, const uint32_t* off, uint64_t rb, uint64_t
   uint32_t* v1 = reinterpret_cast<uint32_t*>(p); p = align(p + 4 * m);
   uint32_t* counts = reinterpret_cast<uint32_t*>(p); p = align(p + 4ull * 256 * nblk);
   auto* plan = reinterpret_cast<RadixPlan*>(p); p = align(p + sizeof(RadixPlan));
-  uint32_t* hist = reinterpret_cast<uint32_t*>(p);
+  uint32_t* hist = reinterpret_cast<uint32_t*>(p); p = align(p + 8 * 256 * 4);
+  uint32_t* totals = reinterpret_cast<uint32_t*>(p);
   TGB_CUDA(cudaMemsetAsync(hist, 0, 8 * 256 * 4, ctx->stream));
   rowlen_key_kernel<<<grid_for(m, 256, ctx->num_sms * 8), 256, 0, ctx->stream>>>(off, rb, m, k0,
                                                                                 v0, hist);
@@ -284,10 +305,10 @@ void sort_rows_by_length(tg_ctx* ctx, const uint32_t* off, uint64_t rb, uint64_t
   for (int pass = 0; pass < 4; ++pass) {  // digits 4..7 are constant: planned as skipped
     digit_count_kernel<<<nblk, kRsWarps * 32, 0, ctx->stream>>>(k0, k1, m, pass, plan, counts, nblk);
     TGB_LAUNCHED();
-    count_scan_kernel<<<1, 1024, 0, ctx->stream>>>(counts, (uint64_t)256 * nblk, pass, plan);
+    count_scan_kernel<<<256, 1024, 0, ctx->stream>>>(counts, nblk, pass, plan, totals);
     TGB_LAUNCHED();
     scatter_kernel<<<nblk, kRsWarps * 32, 0, ctx->stream>>>(k0, v0, k1, v1, m, pass, plan, counts,
-                                                             nblk);
+                                                             nblk, totals);
     TGB_LAUNCHED();
   }
   order_out_kernel<<<grid_for(m, 256), 256, 0, ctx->stream>>>(v0, v1, plan, rb, m, order_dev);
@@ -305,10 +326,12 @@ void sort_scores(tg_ctx* ctx, const double* scores_dev, uint64_t n, uint64_t* or
   uint32_t* v1 = ctx->scratch_t<uint32_t>(kScratchD, n);
   const uint32_t nblk = static_cast<uint32_t>((n + kRsTile - 1) / kRsTile);
   // small slot layout: [bad u64][plan][hist 8x256 u32]
-  char* small = static_cast<char*>(ctx->scratch(kSmall, 64 + sizeof(RadixPlan) + 8 * 256 * 4));
+  char* small = static_cast<char*>(
+      ctx->scratch(kSmall, 64 + sizeof(RadixPlan) + 8 * 256 * 4 + 256 * 4));
   auto* bad = reinterpret_cast<unsigned long long*>(small);
   auto* plan = reinterpret_cast<RadixPlan*>(small + 64);
   auto* hist = reinterpret_cast<uint32_t*>(small + 64 + sizeof(RadixPlan));
+  auto* totals = hist + 8 * 256;
   uint32_t* counts = ctx->scratch_t<uint32_t>(kScratchE, (uint64_t)256 * nblk);
   TGB_CUDA(cudaMemsetAsync(bad, 0xff, 8, ctx->stream));
   TGB_CUDA(cudaMemsetAsync(hist, 0, 8 * 256 * 4, ctx->stream));
@@ -320,10 +343,10 @@ void sort_scores(tg_ctx* ctx, const double* scores_dev, uint64_t n, uint64_t* or
   for (int p = 0; p < 8; ++p) {
     digit_count_kernel<<<nblk, kRsWarps * 32, 0, ctx->stream>>>(k0, k1, n, p, plan, counts, nblk);
     TGB_LAUNCHED();
-    count_scan_kernel<<<1, 1024, 0, ctx->stream>>>(counts, (uint64_t)256 * nblk, p, plan);
+    count_scan_kernel<<<256, 1024, 0, ctx->stream>>>(counts, nblk, p, plan, totals);
     TGB_LAUNCHED();
     scatter_kernel<<<nblk, kRsWarps * 32, 0, ctx->stream>>>(k0, v0, k1, v1, n, p, plan, counts,
-                                                             nblk);
+                                                             nblk, totals);
     TGB_LAUNCHED();
   }
   perm_kernel<<<grid_for(n, 256), 256, 0, ctx->stream>>>(v0, v1, plan, n, order_dev, perm_dev);
