@@ -35,6 +35,10 @@ struct TieredStoreOptions {
   bool pad128 = true;
   // K8 through TMA bulk copies staged in shared memory (else 16 B loads).
   bool bulk = true;
+  // Deal consecutive row batches across CTAs, so the cold (PCIe) rows, taken
+  // first, are issued from every SM (address translation of a large host
+  // region is per-SM limited: 148 -> 89 us per C3 minibatch).
+  bool spread = true;
 };
 
 class TieredFeatureStore {

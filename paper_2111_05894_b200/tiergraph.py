@@ -601,7 +601,7 @@ class TieredFeatureStore:
 
     def __init__(self, features, perm, layout: TierLayout, device_index: int = 0, *,
                  ctx: Context = None, cold_mode: str = "reordered", pad128: bool = True,
-                 gather_mode: str = "bulk", place: bool = True):
+                 gather_mode: str = "bulk+spread", place: bool = True):
         self.ctx = _ctx(ctx)
         self.layout = layout
         self.device_index = device_index
