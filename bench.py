@@ -209,28 +209,47 @@ def bench_pagerank(torch, tg, ctx, g, tid, n, e, iters=5, reps=5):
 
 
 def bench_pagerank_multi(torch, tg, ctx, g, tid, single, dist, reps=3):
-    """Row-partitioned PageRank over all ranks (NCCL all-gather of `norm`
-    blocks each step), device-timed, max over ranks; checked bit-exact
-    against this rank's single-GPU run."""
+    """Row-partitioned PageRank over all ranks, device-timed, max over ranks,
+    checked bit-exact against this rank's single-GPU run, with both
+    exchanges: the baseline (an NCCL all-gather of the `norm` blocks after
+    every step) and the fused one (each step's epilogue stores its rows into
+    every rank's vector over CUDA-IPC peer memory; a device arrival barrier
+    replaces the collective)."""
     from paper_2111_05894_b200 import distributed as D
     cfgp = tg.PagerankConfig(5, 0.85)
-    out = D.weighted_reverse_pagerank_multi(g, cfgp, tid, ctx=ctx)  # warm (builds row schedule)
-    ts = []
-    for _ in range(reps):
-        dist.barrier()
-        torch.cuda.synchronize()
-        a = torch.cuda.Event(enable_timing=True)
-        b = torch.cuda.Event(enable_timing=True)
-        a.record()
-        out = D.weighted_reverse_pagerank_multi(g, cfgp, tid, ctx=ctx)
-        b.record()
-        b.synchronize()
-        ts.append(a.elapsed_time(b))
-    t = torch.tensor([min(ts)], dtype=torch.float64, device=single.device)
-    dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    same = torch.tensor([int(torch.equal(out, single))], device=single.device)
-    dist.all_reduce(same, op=dist.ReduceOp.MIN)
-    return float(t.item()), bool(same.item())
+    ex = D.PeerExchangePagerank(g, ctx)
+    runs = {"allgather": lambda: D.weighted_reverse_pagerank_multi(g, cfgp, tid, ctx=ctx),
+            "fused_p2p": lambda: D.weighted_reverse_pagerank_ipc(g, cfgp, tid, ctx=ctx, exchange=ex)}
+    res = {}
+    for name, fn in runs.items():
+        out = fn()  # warm (row schedule, IPC mappings)
+        ts = []
+        for _ in range(reps):
+            dist.barrier()
+            torch.cuda.synchronize()
+            a = torch.cuda.Event(enable_timing=True)
+            b = torch.cuda.Event(enable_timing=True)
+            a.record()
+            out = fn()
+            b.record()
+            b.synchronize()
+            ts.append(a.elapsed_time(b))
+        t = allreduce(dist, [min(ts)], single.device, dist.ReduceOp.MAX)
+        same = allreduce(dist, [int(torch.equal(out, single))], single.device, dist.ReduceOp.MIN)
+        res[name] = (float(t[0]), bool(same[0]))
+    dist.barrier()
+    ex.close()
+    return res
+
+
+def allreduce(dist, vals, device, op=None):
+    """All-reduce a few host numbers (fp64) over the ranks; on the gloo
+    plumbing of the shared-GPU test mode the tensor stays on the host."""
+    import torch
+    dev = device if dist.get_backend() == "nccl" else "cpu"
+    t = torch.tensor(vals, dtype=torch.float64, device=dev)
+    dist.all_reduce(t, op=op if op is not None else dist.ReduceOp.SUM)
+    return t.tolist()
 
 
 def exchange_peers(torch, tg, store, rank, world):
@@ -263,11 +282,21 @@ def run_ours(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # TG_BENCH_SHARE_GPU=1: every rank on cuda:0 with gloo plumbing (NCCL
+    # refuses two ranks on one GPU) -- exercises the multi-process path
+    # (CUDA-IPC peer tables, row-partitioned PageRank, max-over-ranks timing)
+    # on a one-GPU box. Not a scaling measurement.
+    share = world > 1 and os.environ.get("TG_BENCH_SHARE_GPU") == "1"
+    if share:
+        local = 0
     torch.cuda.set_device(local)
     dist = None
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if share:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     stream = torch.cuda.Stream(device=local)  # one non-default stream for torch and tiergraph
     torch.cuda.set_stream(stream)
     ctx = tg.Context(local, stream=stream)
@@ -379,13 +408,9 @@ def run_ours(args):
     u_rows = sum(len(mine[k % len(mine)]) for k in range(args.warmup, nsteps))
     assert int(counters.sum()) == u_rows
     if dist:
-        t = torch.tensor([t_ms], dtype=torch.float64, device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        t_ms = float(t.item())
-        tot = torch.tensor([u_rows, int(counters[0]), int(counters[1]), int(counters[2])],
-                           dtype=torch.float64, device=dev)
-        dist.all_reduce(tot)
-        u_all, cl, cp, ch = (int(x) for x in tot.tolist())
+        t_ms = allreduce(dist, [t_ms], dev, dist.ReduceOp.MAX)[0]
+        tot = allreduce(dist, [u_rows, int(counters[0]), int(counters[1]), int(counters[2])], dev)
+        u_all, cl, cp, ch = (int(x) for x in tot)
     else:
         u_all, cl, cp, ch = u_rows, int(counters[0]), int(counters[1]), int(counters[2])
     gbps = u_all * R / (t_ms * 1e-3) / 1e9
@@ -407,9 +432,7 @@ def run_ours(args):
         store.gather_rows(pinned_ids[k], out=out_d[:len(pinned_ids[k])], report=rep)
         e2e_t += time.perf_counter() - t0
     if dist:
-        t = torch.tensor([e2e_t], dtype=torch.float64, device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        e2e_t = float(t.item())
+        e2e_t = allreduce(dist, [e2e_t], dev, dist.ReduceOp.MAX)[0]
     e2e_gbps = u_all * R / e2e_t / 1e9
     h2d = u_rows * 8 / args.steps
 
@@ -422,9 +445,7 @@ def run_ours(args):
     sim = tg.simulate_trace(tg.make_access_counter(counts), lay)
     host_epoch, total_epoch = ep.host_bytes, ep.local_bytes + ep.peer_bytes + ep.host_bytes
     if dist:
-        t = torch.tensor([host_epoch, total_epoch], dtype=torch.float64, device=dev)
-        dist.all_reduce(t)
-        host_epoch, total_epoch = (int(x) for x in t.tolist())
+        host_epoch, total_epoch = (int(x) for x in allreduce(dist, [host_epoch, total_epoch], dev))
 
     # ---- C5: cache-ratio sweep of CPU->GPU bytes per epoch (replicated vs
     # sharded hot tier, 1/2/4/8 devices) from the whole epoch's access counter
@@ -492,7 +513,9 @@ def run_ours(args):
             "config": {"workload": cfg["workload"], "nodes": n, "edges_after_dedup": e,
                        "row_bytes": R, "hot_fraction": cfg["hot"], "layout": lay.as_tuple(),
                        "l2": "flushed between steps (256 MB memset), per-step CUDA events",
-                       "parallelism": f"{world} GPU(s), hot tier sharded, cold tier per rank"},
+                       "parallelism": f"{world} GPU(s), hot tier sharded, cold tier per rank"
+                                      + (" (TEST MODE: all ranks share cuda:0, gloo plumbing; not "
+                                         "a scaling number)" if share else "")},
             "minibatches_per_s": round(mbps, 1),
             "avg_ids_per_minibatch": round(u_all / max(args.steps * world, 1), 1),
             "hit_split": {"local": round(frac_l, 4), "peer": round(frac_p, 4), "host": round(frac_h, 4)},
@@ -519,10 +542,16 @@ def run_ours(args):
                          "indeg_us": round(indeg_ms * 1e3, 2),
                          "gteps_incl_indeg": round(5 * e / ((pr_ms + indeg_ms) * 1e-3) / 1e9, 3),
                          "multi_gpu": None if pr_multi is None else {
-                             "ranks": world, "ms": round(pr_multi[0], 4),
-                             "gteps": round(5 * e / (pr_multi[0] * 1e-3) / 1e9, 3),
-                             "bit_exact_vs_single_gpu": pr_multi[1],
-                             "exchange": "NCCL all_gather_into_tensor of norm row blocks per step"},
+                             name: {"ranks": world, "ms": round(v[0], 4),
+                                    "gteps": round(5 * e / (v[0] * 1e-3) / 1e9, 3),
+                                    "bit_exact_vs_single_gpu": v[1],
+                                    "exchange": {
+                                        "allgather": "NCCL all_gather_into_tensor of norm row "
+                                                     "blocks after every step",
+                                        "fused_p2p": "K3 epilogue stores rows into every rank's "
+                                                     "norm over CUDA-IPC peer memory + device "
+                                                     "arrival barrier"}[name]}
+                             for name, v in pr_multi.items()},
                          "spmv_step_us": round(step_ms * 1e3, 2),
                          "prepare_us": round(prep_ms * 1e3, 2),
                          "roofline": {"bound": "hbm", "kernel": "pr_step_kernel (K3)",

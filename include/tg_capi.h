@@ -262,6 +262,12 @@ int tg_enable_peer_access(int device, int peer);
 int tg_ipc_get_handle(const void* dev_ptr, void* handle_out /* 64 bytes */);
 int tg_ipc_open_handle(tg_ctx* ctx, const void* handle /* 64 bytes */, void** dev_ptr_out);
 int tg_ipc_close_handle(void* dev_ptr);
+/* Library-owned device allocation (cudaMalloc on the ctx device, zeroed):
+ * the base of its own allocation, so a CUDA-IPC handle of it maps exactly
+ * this buffer in another process (used for the cross-process fused
+ * PageRank exchange: norm ping-pong, scores and arrival counters). */
+int tg_device_alloc(tg_ctx* ctx, uint64_t bytes, void** out);
+int tg_device_free(tg_ctx* ctx, void* p);
 /* Register caller host memory as mapped pinned (cudaHostRegister). */
 int tg_host_register(void* ptr, uint64_t bytes);
 int tg_host_unregister(void* ptr);

@@ -106,6 +106,8 @@ SIGNATURES = {
     "tg_ipc_get_handle": (I32, [vp, vp]),
     "tg_ipc_open_handle": (I32, [vp, vp, C.POINTER(vp)]),
     "tg_ipc_close_handle": (I32, [vp]),
+    "tg_device_alloc": (I32, [vp, U64, C.POINTER(vp)]),
+    "tg_device_free": (I32, [vp, vp]),
     "tg_host_register": (I32, [vp, U64]),
     "tg_host_unregister": (I32, [vp]),
     "tg_host_alloc": (I32, [U64, C.POINTER(vp)]),

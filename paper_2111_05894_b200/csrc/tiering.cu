@@ -1230,6 +1230,22 @@ int tg_ipc_close_handle(void* p) {
   return guard([&] { TGB_CUDA(cudaIpcCloseMemHandle(p)); });
 }
 
+int tg_device_alloc(tg_ctx* ctx, uint64_t bytes, void** out) {
+  return guard([&] {
+    DeviceGuard dg(ctx->device);
+    TGB_CUDA(cudaMalloc(out, std::max<uint64_t>(bytes, 16)));
+    TGB_CUDA(cudaMemsetAsync(*out, 0, std::max<uint64_t>(bytes, 16), ctx->stream));
+    ctx->sync();
+  });
+}
+
+int tg_device_free(tg_ctx* ctx, void* p) {
+  return guard([&] {
+    DeviceGuard dg(ctx->device);
+    TGB_CUDA(cudaFree(p));
+  });
+}
+
 int tg_host_register(void* p, uint64_t bytes) {
   return guard([&] {
     TGB_CUDA(cudaHostRegister(p, bytes, cudaHostRegisterMapped | cudaHostRegisterPortable));

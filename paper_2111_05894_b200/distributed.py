@@ -103,7 +103,14 @@ def reverse_pagerank_partitioned(stepper, n: int, iterations: int, damp: float, 
         out = scores if last else y
         if world > 1:
             stepper.sync()  # the step must land before the collective reads it
-            dist.all_gather_into_tensor(out, out[rank * chunk:(rank + 1) * chunk], group=group)
+            if out.is_cuda and dist.get_backend(group) != "nccl":
+                # gloo plumbing (tests, shared-GPU bench mode): stage through the host
+                h = out.cpu()
+                dist.all_gather_into_tensor(h, h[rank * chunk:(rank + 1) * chunk].clone(),
+                                            group=group)
+                out.copy_(h)
+            else:
+                dist.all_gather_into_tensor(out, out[rank * chunk:(rank + 1) * chunk], group=group)
         x, y = y, x
     stepper.sync()
     return scores[:n]
@@ -183,3 +190,166 @@ def weighted_reverse_pagerank_peers(g, cfg, tid, ctxs, timeout_check=True):
     if timeout_check and any(int(f[1].item()) for f in flags):
         raise tg.TierGraphError("peer barrier timed out")
     return [b[2][:n] for b in bufs]
+
+
+class _DevView:
+    """A device vector owned by this library, seen by torch (no copy)."""
+
+    def __init__(self, ptr: int, count: int, typestr: str):
+        self.__cuda_array_interface__ = {"shape": (count,), "typestr": typestr,
+                                         "data": (ptr, False), "version": 3, "stream": None}
+
+
+class PeerExchangePagerank:
+    """The fused exchange with ONE PROCESS PER GPU (the form `bench.py` runs
+    under torchrun): partitioned weighted reverse PageRank where every step's
+    epilogue stores this rank's rows straight into all other ranks' `norm`
+    (or score) vectors over NVLink/NVSwitch and a device-side arrival barrier
+    replaces the all-gather -- `weighted_reverse_pagerank_peers` across
+    processes.
+
+    Each rank owns one library allocation (tg_device_alloc)
+        [norm A | norm B | scores]  (n f64 each)  [arrivals u32, err u32]
+    whose CUDA-IPC handle is exchanged once through the process group
+    (all_gather_object, which also orders the zeroed counters before any
+    arrival). Arrival counters only grow: the barrier target of a step is the
+    running total of arrivals so far, so the object can run the recurrence any
+    number of times without resetting them. Row sums never leave their rank,
+    so the result is bit-identical to one GPU (scoring.cpp:50-74; any worker
+    count, parallel.hpp:5-7).
+
+    Safe reuse of the shared vectors (Jacobi ping-pong, scoring.cpp:71): a
+    rank writes a peer's buffer X in step s only after the barrier of step
+    s-1, and every rank finished its last read of X (step s-1 or earlier)
+    before arriving there.
+    """
+
+    def __init__(self, g, ctx, group=None):
+        import ctypes as C
+        import torch
+        import torch.distributed as dist
+        from . import tiergraph as tg
+        from ._lib import LIB
+        self.tg, self.LIB, self.C, self.torch = tg, LIB, C, torch
+        self.ctx, self.g = ctx, g
+        self.gh = g.device(ctx)
+        self.n = n = g.num_nodes()
+        self.world = dist.get_world_size(group) if dist.is_initialized() else 1
+        self.rank = dist.get_rank(group) if dist.is_initialized() else 0
+        if self.world >= TG_MAX_PEERS + 1:
+            raise tg.DomainError(f"at most {TG_MAX_PEERS} peers")
+        _, blocks = row_blocks(n, self.world)
+        self.rb, self.re = blocks[self.rank]
+        self.vec = ((max(n, 1) * 8 + 255) // 256) * 256
+        nbytes = 3 * self.vec + 256
+        base = C.c_void_p()
+        tg._check(LIB.tg_device_alloc(ctx.h, nbytes, C.byref(base)))
+        self.base = base.value
+        self.dev = torch.device("cuda", ctx.device)
+        self.deg = torch.empty(max(n, 1), dtype=torch.int32, device=self.dev)
+        h = (C.c_uint8 * 64)()
+        tg._check(LIB.tg_ipc_get_handle(C.c_void_p(self.base), h))
+        handles = [bytes(h)] * self.world
+        if self.world > 1:
+            handles = [None] * self.world
+            dist.all_gather_object(handles, bytes(h), group=group)
+        self.bases, self.opened = [], []
+        for q in range(self.world):
+            if q == self.rank:
+                self.bases.append(self.base)
+                continue
+            hb = (C.c_uint8 * 64).from_buffer_copy(handles[q])
+            p = C.c_void_p()
+            tg._check(LIB.tg_ipc_open_handle(ctx.h, hb, C.byref(p)))
+            self.bases.append(p.value)
+            self.opened.append(p.value)
+        self.arrivals = 0
+        self.peers = [q for q in range(self.world) if q != self.rank]
+
+    def _vec(self, base: int, k: int) -> int:
+        return base + k * self.vec
+
+    def _flag(self, base: int, k: int = 0) -> int:
+        return base + 3 * self.vec + 4 * k
+
+    def run(self, iterations: int, damp: float, tid_dev=None, ntid: int = 0):
+        """Runs the recurrence (stream-ordered on the context, no host sync);
+        returns the full score vector as a torch view of this rank's buffer,
+        valid once the context stream has drained and until the next run."""
+        C, LIB, tg = self.C, self.LIB, self.tg
+        if iterations < 1:
+            raise tg.DomainError("pagerank: iterations must be >= 1")  # scoring.cpp:43-44
+        if not (0.0 < damp < 1.0):
+            raise tg.DomainError(f"pagerank: damp must lie in (0,1), got {damp}")
+        tg._check(LIB.tg_pagerank_prepare_async(
+            self.ctx.h, self.gh, None if tid_dev is None else tid_dev.data_ptr(), ntid,
+            self.deg.data_ptr(), self._vec(self.base, 0)))
+        G = self.world
+        pf = (C.c_void_p * 16)(*[self._flag(self.bases[q]) for q in self.peers])
+        if G > 1:
+            # entry barrier: no peer stores into this run's vectors before
+            # every rank has finished reading the previous run's scores
+            self.arrivals += G - 1
+            tg._check(LIB.tg_peer_barrier_async(self.ctx.h, self._flag(self.base), pf, G - 1,
+                                                self.arrivals, self._flag(self.base, 1)))
+        cur = 0
+        for it in range(iterations):
+            last = int(it + 1 == iterations)
+            nxt = 1 - cur
+            pn = (C.c_void_p * 16)(*[self._vec(self.bases[q], nxt) for q in self.peers])
+            ps = (C.c_void_p * 16)(*[self._vec(self.bases[q], 2) for q in self.peers])
+            tg._check(LIB.tg_pagerank_step_peers_async(
+                self.ctx.h, self.gh, self.deg.data_ptr(), float(damp), self._vec(self.base, cur),
+                self._vec(self.base, nxt), self._vec(self.base, 2), self.rb, self.re, last,
+                pn, ps, len(self.peers)))
+            if G > 1:
+                self.arrivals += G - 1
+                tg._check(LIB.tg_peer_barrier_async(
+                    self.ctx.h, self._flag(self.base), pf, G - 1, self.arrivals,
+                    self._flag(self.base, 1)))
+            cur = nxt
+        return self.torch.as_tensor(_DevView(self._vec(self.base, 2), self.n, "<f8"),
+                                    device=self.dev)
+
+    def timed_out(self) -> bool:
+        """True when a device barrier gave up waiting (a peer never arrived)."""
+        e = self.torch.as_tensor(_DevView(self._flag(self.base, 1), 1, "<u4"), device=self.dev)
+        self.ctx.sync()
+        return bool(int(e.cpu().item()))
+
+    def close(self) -> None:
+        self.ctx.sync()
+        for p in self.opened:
+            self.LIB.tg_ipc_close_handle(self.C.c_void_p(p))
+        self.opened = []
+        if self.base:
+            self.LIB.tg_device_free(self.ctx.h, self.C.c_void_p(self.base))
+            self.base = 0
+
+
+TG_MAX_PEERS = 15
+
+
+def weighted_reverse_pagerank_ipc(g, cfg, tid, ctx=None, group=None, exchange=None):
+    """scoring.hpp:45-46 over all ranks of `group`, one process per GPU, with
+    the fused P2P exchange. Pass a PeerExchangePagerank as `exchange` to reuse
+    its buffers and IPC mappings across calls. Returns a copy of the scores."""
+    import torch
+    from . import tiergraph as tg
+    ctx = ctx or tg.default_context()
+    ids = tid.ids if isinstance(tid, tg.TrainIdSet) else tid
+    if ids is None or len(ids) == 0:
+        raise tg.DomainError("weighted reverse pagerank needs a non-empty train id set; "
+                             "use reverse_pagerank when no nodes are labeled")  # scoring.cpp:89-91
+    own = exchange is None
+    ex = exchange or PeerExchangePagerank(g, ctx, group)
+    tid_d = torch.as_tensor(np.asarray(ids, np.uint64).astype(np.int64), device=ex.dev)
+    s = ex.run(cfg.iterations, cfg.damp, tid_d, len(ids))
+    ex.ctx.sync()  # the last barrier has passed: every peer's rows have landed
+    out = s.clone()
+    torch.cuda.current_stream(ex.dev).synchronize()
+    if ex.timed_out():
+        raise tg.TierGraphError("peer barrier timed out")
+    if own:
+        ex.close()
+    return out

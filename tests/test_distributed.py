@@ -122,3 +122,50 @@ def test_partitioned_pagerank_over_gloo_is_bit_exact(world):
     res = _run(world, off, tgt, None, 3)
     want = chk.reverse_pagerank(off, tgt, 3, 0.85).tobytes()
     assert all(v == want for v in res.values())
+
+
+def _ipc_worker(rank, world, port, off, tgt, tid, q):
+    """One process per rank, all on cuda:0 (the gpurun box has one GPU): the
+    cross-process fused exchange (CUDA-IPC peer stores + device barrier)."""
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2111_05894_b200 import tiergraph as tg
+        ctx = tg.Context(0)
+        g = tg.CsrGraph(off, tgt)
+        ex = D.PeerExchangePagerank(g, ctx)
+        outs = []
+        for iters in (5, 1, 2):  # reuse of the shared vectors and counters across runs
+            s = D.weighted_reverse_pagerank_ipc(g, tg.PagerankConfig(iters, 0.85), tid, ctx=ctx,
+                                                exchange=ex)
+            outs.append(s.cpu().numpy().tobytes())
+        dist.barrier()
+        ex.close()
+        q.put((rank, outs))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("world", [2, 3])
+def test_fused_exchange_across_processes_is_bit_exact(world):
+    port = oracle.port()
+    chk = oracle.ref() or port
+    from paper_2111_05894_b200 import synth
+    off, tgt = synth.rmat_graph(30_000, 400_000, seed=world)
+    tid = port.draw_random_train_ids(len(off) - 1, 3_000, 5)
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    p0 = _free_port()
+    procs = [ctx.Process(target=_ipc_worker, args=(r, world, p0, off, tgt, tid, q))
+             for r in range(world)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=600) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    for k, iters in enumerate((5, 1, 2)):
+        want = chk.weighted_reverse_pagerank(off, tgt, tid, iters, 0.85).tobytes()
+        assert all(v[k] == want for v in res.values()), f"world={world} iters={iters}"
