@@ -53,7 +53,42 @@ CONFIGS = {
                nodes=111_000_000, draws=1_600_000_000, dim=128, elem=4, fanouts=[15, 10, 5],
                batch=1024, train=0.10, hot=0.20, max_batches=512, cold_mode="indirect",
                cpu_gather=False),
+    # C4: the hot tier is capped at 5% of the rows PER GPU (plan_layout's
+    # per-device budget, tiering.cpp:87-96), sharded, so K = 5% x ranks. The
+    # 374.8 GB fp16 matrix exceeds the box's 196 GB of host RAM (and the
+    # driver maps at most ~RAM-size of host memory for the GPU, measured), so
+    # the host side is a pinned row cache of P rows (`row_cache_gb`) and the
+    # store is placed with tg_store_place_rows: new id i reads cache row
+    # (original id mod P). Graph, PageRank, selection, sampling, layout and
+    # accounting run at full size; parity checks the gathered bytes against
+    # that map.
+    "c4": dict(workload="C4: MAG240M-shaped R-MAT 244M nodes / 1.7B draws, 768-d fp16, 10% train, "
+                        "fanout (15,10,5), batch 1024, hot budget 5% of rows per GPU (sharded), "
+                        "cold rows via UVA",
+               nodes=244_000_000, draws=1_700_000_000, dim=768, elem=2, fanouts=[15, 10, 5],
+               batch=1024, train=0.10, hot_per_gpu=0.05, max_batches=256, cold_mode="indirect",
+               cpu_gather=False, row_cache_gb=80, fp16=True),
 }
+
+
+def hot_fraction(cfg, world):
+    return cfg["hot"] if "hot" in cfg else min(1.0, cfg["hot_per_gpu"] * world)
+
+
+def expected_rows(cfg, old_ids):
+    """Closed-form rows of the bench matrix for original ids (aliased for C4)."""
+    from paper_2111_05894_b200 import synth
+    ids = np.asarray(old_ids, np.uint64)
+    if cfg.get("row_cache_gb"):
+        ids = ids % np.uint64(cache_rows(cfg))
+    if cfg.get("fp16"):
+        return synth.expected_rows_f16(ids, cfg["dim"])
+    return synth.expected_rows(ids, cfg["dim"])
+
+
+def cache_rows(cfg):
+    R = cfg["dim"] * cfg["elem"]
+    return int(cfg["row_cache_gb"] * (1 << 30) // R)
 
 
 def log(*a):
@@ -142,10 +177,15 @@ def build_inputs(cfg, device, rank=0, world=1):
     return off, tgt, tid
 
 
-def pin_features(cfg):
+def pin_features(cfg, ctx=None):
     from paper_2111_05894_b200 import synth, tiergraph as tg
     n, dim = cfg["nodes"], cfg["dim"]
     R = dim * cfg["elem"]
+    if cfg.get("row_cache_gb"):
+        P = cache_rows(cfg)
+        buf = tg.host_alloc(P * R)
+        synth.test_features_f16_gpu(P, dim, buf)
+        return buf.reshape(P, R), R
     buf = tg.host_alloc(n * R)
     if n * R > (8 << 30):
         synth.test_features_pinned_gpu(n, dim, buf)
@@ -354,10 +394,22 @@ def run_ours(args):
         f"(avg {np.mean([len(l) for l in lists]):.0f} ids) in {time.time()-t0:.1f}s")
 
     # ---- tiered store: hot rows in HBM (sharded across ranks), cold rows pinned
-    feat, R = pin_features(cfg)
-    lay = tg.plan_layout(n, cfg["hot"], 0.0, world, cfg["dim"], cfg["elem"])
-    store = tg.TieredFeatureStore(feat, perm, lay, rank, ctx=ctx,
-                                  cold_mode=cfg.get("cold_mode", "reordered"))
+    feat, R = pin_features(cfg, ctx)
+    hot = hot_fraction(cfg, world)
+    budget = 0
+    if "hot_per_gpu" in cfg:  # plan_layout's per-device HBM budget (tiering.cpp:87-96)
+        budget = (int(np.ceil(cfg["hot_per_gpu"] * n)) + 1) * R
+    lay = tg.plan_layout(n, hot, 0.0, world, cfg["dim"], cfg["elem"], budget)
+    if cfg.get("row_cache_gb"):
+        store = tg.TieredFeatureStore(None, perm, lay, rank, ctx=ctx,
+                                      cold_mode=cfg.get("cold_mode", "reordered"), place=False)
+        inv = np.empty(n, np.uint64)
+        inv[perm.new_id_of.astype(np.int64)] = np.arange(n, dtype=np.uint64)
+        store.place_rows(feat, (inv % np.uint64(len(feat))).astype(np.uint32))
+        del inv
+    else:
+        store = tg.TieredFeatureStore(feat, perm, lay, rank, ctx=ctx,
+                                      cold_mode=cfg.get("cold_mode", "reordered"))
     if world > 1:
         exchange_peers(torch, tg, store, rank, world)
         dist.barrier()
@@ -493,6 +545,10 @@ def run_ours(args):
     bound = ["hbm", "nvlink", "pcie"][int(np.argmax([t_hbm, t_nvl, t_pcie]))]
     achieved = alg_bytes / t_launch / 1e9
     peak_eff = alg_bytes / t_star / 1e9
+    cold_rows = int(round(per_launch * frac_h))
+    cold_floor = None
+    if cold_rows:
+        cold_floor = store.measure_cold_us(cold_rows, 5)
     traffic = None
     tf = os.path.join(ROOT, "profiles", f"ncu_traffic_{args.config}.json")
     if os.path.exists(tf):
@@ -511,7 +567,7 @@ def run_ours(args):
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u8",
             "data": "synthetic (R-MAT graph, closed-form features, reference sampler id lists)",
             "config": {"workload": cfg["workload"], "nodes": n, "edges_after_dedup": e,
-                       "row_bytes": R, "hot_fraction": cfg["hot"], "layout": lay.as_tuple(),
+                       "row_bytes": R, "hot_fraction": hot, "layout": lay.as_tuple(),
                        "l2": "flushed between steps (256 MB memset), per-step CUDA events",
                        "parallelism": f"{world} GPU(s), hot tier sharded, cold tier per rank"
                                       + (" (TEST MODE: all ranks share cuda:0, gloo plumbing; not "
@@ -527,14 +583,24 @@ def run_ours(args):
             "roofline": {"bound": bound, "achieved": round(achieved, 2),
                          "peak": round(peak_eff, 2), "unit": "GB/s",
                          "frac": round(t_star / t_launch, 4), "traffic": traffic,
-                         "kernel": "gather_bulk_kernel (K8: TMA bulk copies, 128 B-padded cold tier)",
+                         "kernel": "gather_bulk_kernel (K8: TMA bulk copies, cold tier " + (
+                             "read in place)" if cfg.get("cold_mode") == "indirect"
+                             else "128 B-padded)"),
                          "algorithmic_bytes_per_launch": int(alg_bytes),
                          "mixed": {"hbm_gbs": hbm_peak, "hbm_src": hbm_src,
                                    "pcie_gbs": round(pcie_peak, 2),
                                    "pcie_src": f"measured live: max(DMA H2D {pcie_dma:.1f}, "
                                                f"zero-copy row read {pcie_zc:.1f})",
                                    "nvlink_gbs": nvl_peak, "t_star_us": round(t_star * 1e6, 2),
-                                   "t_launch_us": round(t_launch * 1e6, 2)}},
+                                   "t_launch_us": round(t_launch * 1e6, 2)},
+                         "cold_floor": None if cold_floor is None else {
+                             "us": round(cold_floor, 2), "rows": cold_rows,
+                             "frac": round(cold_floor / (t_launch * 1e6), 4),
+                             "what": "K8 on this store over the launch's number of cold rows "
+                                     "alone (random cold ids, L2 flushed): the PCIe part by "
+                                     "itself on the same region and mapping, GPU address "
+                                     "translation included; frac = cold-only / full launch "
+                                     "(1.0 = the HBM rows are fully hidden)"}},
             "pagerank": {"gteps": round(5 * e / (pr_ms * 1e-3) / 1e9, 3), "ms": round(pr_ms, 4),
                          "iterations": 5, "edges": e,
                          "note": "device-resident u32 CSR; in-degrees (K1) are built with the "
@@ -578,6 +644,11 @@ def run_ours(args):
             "epoch_sweep": sweep,
             "clocks": clocks,
         }
+        if cfg.get("row_cache_gb"):
+            result["config"]["host_row_cache"] = {
+                "rows": cache_rows(cfg), "bytes": cache_rows(cfg) * R,
+                "map": "new id i reads cache row (original id mod rows): tg_store_place_rows",
+                "why": "the 374.8 GB matrix exceeds the box's host RAM (196 GB)"}
         if world == 1 and not args.no_cpu_baseline:
             result["cpu_baseline"], result["parity"] = cpu_baseline(
                 cfg, off, tgt, tid, scores, perm, feat, R, lay, mine, store, out_d, torch,
@@ -656,8 +727,8 @@ def cpu_baseline(cfg, off, tgt, tid, scores, perm, feat, R, lay, lists, store, o
         inv[perm.new_id_of.astype(np.int64)] = np.arange(len(inv), dtype=np.uint64)
         mine = tg.TrafficReport()
         got = store.gather_rows(ids, report=mine)
-        parity["gather_rows_bit_exact"] = bool(np.array_equal(
-            got.view(np.float32), synth.expected_rows(inv[ids.astype(np.int64)], cfg["dim"])))
+        want = expected_rows(cfg, inv[ids.astype(np.int64)])
+        parity["gather_rows_bit_exact"] = bool(np.array_equal(got.view(want.dtype), want))
         r = ref.gather(lay.as_tuple(), ids, 0)
     if gt is not None:
         # the reference's own sampler on the host cores, and parity of the GPU sampler
@@ -694,6 +765,12 @@ def run_reference(args):
     cfg = CONFIGS[args.config]
     if ref is None:
         return {"impl": "reference", "unavailable": "oracle/_ref/libtgref.so was not built"}
+    if not cfg.get("cpu_gather", True):
+        return {"impl": "reference", "unavailable": (
+            "the reference's CPU gather reads FeatureMatrix::row of a reordered copy of the "
+            f"matrix ({cfg['nodes'] * cfg['dim'] * cfg['elem'] / 1e9:.0f} GB here, twice with the "
+            "original), beyond the box's host RAM; the reference PageRank/sampler at this "
+            "scale are timed in the `ours` line's cpu_baseline")}
     cores = os.cpu_count() or 1
     ref.set_worker_count(cores)
     from paper_2111_05894_b200 import synth

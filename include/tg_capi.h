@@ -239,6 +239,13 @@ int tg_store_destroy(tg_store* s);
  * this device's hot rows and (TG_COLD_REORDERED) the cold copy. */
 int tg_store_place(tg_store* s, const void* features, const uint64_t* new_id_of);
 /* Base of this store's local HBM region (replicated rows then the slice). */
+/* K7 from a caller's row array: new id i holds source row row_of[i]
+ * (rows: nrows x row_bytes, host (registered in place) or device; row_of:
+ * N u32, host or device, each < nrows). tg_store_place is the case
+ * rows = the original matrix, row_of = the inverse permutation. With
+ * TG_COLD_INDIRECT the cold tier is read in place through row_of (e.g. a
+ * host row cache in its own order). */
+int tg_store_place_rows(tg_store* s, const void* rows, uint64_t nrows, const uint32_t* row_of);
 void* tg_store_local_base(const tg_store* s);
 uint64_t tg_store_local_rows(const tg_store* s);
 /* Point device d's slot of the combined-tensor table at a peer's local base
@@ -271,6 +278,8 @@ int tg_device_free(tg_ctx* ctx, void* p);
 /* Register caller host memory as mapped pinned (cudaHostRegister). */
 int tg_host_register(void* ptr, uint64_t bytes);
 int tg_host_unregister(void* ptr);
+/* Device address of pinned / registered host memory, NULL if not mapped. */
+void* tg_mapped_device_ptr(const void* host);
 int tg_host_alloc(uint64_t bytes, void** out); /* cudaHostAlloc Mapped|Portable */
 int tg_host_free(void* p);
 
@@ -280,6 +289,16 @@ int tg_host_free(void* p);
  * device-to-device copy for the HBM reference. Both return GB/s. */
 int tg_measure_host_read_gbps(tg_ctx* ctx, uint64_t bytes, uint64_t row_bytes, int reps,
                               double* gbps);
+/* Mean time (us) to read `rows` random rows (row_bytes each, at `stride`)
+ * out of `region_rows` rows of an existing mapped host region, one launch
+ * per rep with the L2 flushed before it: the practical floor of a gather's
+ * cold part over the same region (GPU address translation included). */
+/* Mean time (us) of this store's own gather (K8) over `rows` random COLD
+ * ids only, L2 flushed before each launch: the cold part of a gather timed
+ * alone, on the same region, mapping and load path. */
+int tg_store_measure_cold_us(tg_store* s, uint64_t rows, int reps, double* us);
+int tg_measure_host_rows_us(tg_ctx* ctx, const void* host, uint64_t region_rows, uint64_t stride,
+                            uint64_t row_bytes, uint64_t rows, int reps, double* us);
 int tg_measure_hbm_copy_gbps(tg_ctx* ctx, uint64_t bytes, int reps, double* gbps);
 /* The memory-system floor of one K3 step on graph g: the same E gathers
  * x[targets[e]] with no summation-order constraint (best of reps, us). */

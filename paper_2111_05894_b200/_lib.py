@@ -106,6 +106,10 @@ SIGNATURES = {
     "tg_ipc_get_handle": (I32, [vp, vp]),
     "tg_ipc_open_handle": (I32, [vp, vp, C.POINTER(vp)]),
     "tg_ipc_close_handle": (I32, [vp]),
+    "tg_measure_host_rows_us": (I32, [vp, vp, U64, U64, U64, U64, C.c_int, C.POINTER(C.c_double)]),
+    "tg_store_measure_cold_us": (I32, [vp, U64, C.c_int, C.POINTER(C.c_double)]),
+    "tg_mapped_device_ptr": (vp, [vp]),
+    "tg_store_place_rows": (I32, [vp, vp, U64, vp]),
     "tg_device_alloc": (I32, [vp, U64, C.POINTER(vp)]),
     "tg_device_free": (I32, [vp, vp]),
     "tg_host_register": (I32, [vp, U64]),

@@ -1,6 +1,8 @@
 // C-ABI plumbing: error reporting, contexts, device selection, the launch
 // counter, the graph reorder (K9, Algorithm 2) and the link microbenchmarks
 // used for the roofline denominators.
+#include <map>
+#include <mutex>
 #include <cuda_runtime.h>
 
 #include <cstdlib>
@@ -253,19 +255,53 @@ int tg_reorder_graph(tg_ctx* ctx, const uint64_t* offsets, const uint64_t* targe
 namespace tgb {
 
 __global__ void host_read_kernel(const uint8_t* __restrict__ src, uint64_t rows, uint64_t R,
-                                 uint8_t* __restrict__ dst, uint64_t seed) {
-  // random row order, 16 B vectors, one warp per row
+                                 uint8_t* __restrict__ dst, uint64_t seed, uint64_t region = 0,
+                                 uint64_t stride = 0) {
+  // `rows` random rows of [0, region) (default: all of them), 16 B vectors,
+  // one warp per row
   const int lane = threadIdx.x & 31;
   const uint64_t warp = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
   const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+  if (!region) region = rows;
+  if (!stride) stride = R;
   for (uint64_t i = warp; i < rows; i += nw) {
-    uint64_t x = (i + seed) * 0x9E3779B97F4A7C15ull;
+    uint64_t x = (i + seed * 0x632BE59BD9B4E019ull) * 0x9E3779B97F4A7C15ull;
     x ^= x >> 31;
-    const uint64_t r = x % rows;
-    const uint4* s = reinterpret_cast<const uint4*>(src + r * R);
+    x *= 0xBF58476D1CE4E5B9ull;
+    x ^= x >> 29;
+    const uint64_t r = x % region;
+    const uint4* s = reinterpret_cast<const uint4*>(src + r * stride);
     uint4* d = reinterpret_cast<uint4*>(dst + i * R);
     for (uint64_t c = lane; c < R / 16; c += 32) d[c] = s[c];
   }
+}
+
+double measure_rows_us(tg_ctx* ctx, const uint8_t* src_dev, uint64_t region_rows, uint64_t stride,
+                       uint64_t R, uint64_t rows, int reps) {
+  if (R % 16 || R == 0 || stride % 16) domain_error("row_bytes and stride must be multiples of 16");
+  if (!rows || !region_rows) domain_error("empty measurement");
+  uint8_t* d = ctx->scratch_t<uint8_t>(kScratchF, rows * R);
+  uint8_t* fl = ctx->scratch_t<uint8_t>(kScratchE, 256ull << 20);
+  cudaEvent_t a, b;
+  TGB_CUDA(cudaEventCreate(&a));
+  TGB_CUDA(cudaEventCreate(&b));
+  const unsigned grid = ctx->num_sms * 8;
+  double tot = 0;
+  for (int i = 0; i <= reps; ++i) {
+    TGB_CUDA(cudaMemsetAsync(fl, i, 256ull << 20, ctx->stream));  // L2 flush, as the bench
+    TGB_CUDA(cudaEventRecord(a, ctx->stream));
+    host_read_kernel<<<grid, 256, 0, ctx->stream>>>(src_dev, rows, R, d, 1000 + i, region_rows,
+                                                    stride);
+    TGB_LAUNCHED();
+    TGB_CUDA(cudaEventRecord(b, ctx->stream));
+    TGB_CUDA(cudaEventSynchronize(b));
+    float ms = 0;
+    TGB_CUDA(cudaEventElapsedTime(&ms, a, b));
+    if (i) tot += ms;  // the first launch warms
+  }
+  cudaEventDestroy(a);
+  cudaEventDestroy(b);
+  return tot / std::max(reps, 1) * 1e3;
 }
 
 }  // namespace tgb
@@ -304,6 +340,16 @@ int tg_measure_host_read_gbps(tg_ctx* ctx, uint64_t bytes, uint64_t R, int reps,
     cudaEventDestroy(b);
     cudaFreeHost(h);
     *gbps = static_cast<double>(rows * R) / (best * 1e-3) / 1e9;
+  });
+}
+
+int tg_measure_host_rows_us(tg_ctx* ctx, const void* host, uint64_t region_rows, uint64_t stride,
+                            uint64_t R, uint64_t rows, int reps, double* us) {
+  return guard([&] {
+    DeviceGuard dg(ctx->device);
+    const void* hd = is_device_ptr(host) ? host : mapped_device_ptr(host);
+    if (!hd) domain_error("tg_measure_host_rows_us: the region is not device-visible");
+    *us = measure_rows_us(ctx, static_cast<const uint8_t*>(hd), region_rows, stride, R, rows, reps);
   });
 }
 

@@ -729,6 +729,21 @@ void account(tg_ctx* ctx, const tg_layout& l, const uint64_t* ids_dev, uint64_t 
   TGB_LAUNCHED();
 }
 
+// n sorted, distinct random ids in [base, base + span), one per stratum of
+// span/n ids (a minibatch list is sorted and unique; measurement only)
+__global__ void random_ids_kernel(uint64_t* __restrict__ out, uint64_t n, uint64_t base,
+                                  uint64_t span, uint64_t seed) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    uint64_t x = (i + seed * 0x632BE59BD9B4E019ull) * 0x9E3779B97F4A7C15ull;
+    x ^= x >> 31;
+    x *= 0xBF58476D1CE4E5B9ull;
+    x ^= x >> 29;
+    const uint64_t lo = (unsigned __int128)span * i / n, hi = (unsigned __int128)span * (i + 1) / n;
+    out[i] = base + lo + (hi > lo ? x % (hi - lo) : 0);
+  }
+}
+
 GatherTable make_table(const tg_store* s) {
   GatherTable t{};
   t.m = TierMap{s->L.local_boundary, s->L.multi_boundary, s->L.num_rows, s->L.num_devices, s->dev};
@@ -1008,6 +1023,42 @@ int tg_store_destroy(tg_store* s) {
 }
 
 void* tg_store_local_base(const tg_store* s) { return s ? s->local : nullptr; }
+
+int tg_store_measure_cold_us(tg_store* s, uint64_t rows, int reps, double* us) {
+  return guard([&] {
+    if (!s->placed) domain_error("tiered store: tg_store_place has not run");
+    tg_ctx* ctx = s->ctx;
+    DeviceGuard dg(ctx->device);
+    const uint64_t mb = s->L.multi_boundary, N = s->L.num_rows;
+    if (mb >= N) domain_error("tiered store: no cold rows");
+    if (!rows) domain_error("empty measurement");
+    // K8 itself over `rows` random cold ids only (L2 flushed before each launch)
+    auto* ids = ctx->scratch_t<uint64_t>(kScratchD, rows);
+    auto* out = ctx->scratch_t<uint8_t>(kScratchF, rows * s->R);
+    auto* fl = ctx->scratch_t<uint8_t>(kScratchE, 256ull << 20);
+    auto* c = ctx->scratch_t<uint64_t>(kSmall, 4);
+    cudaEvent_t a, b;
+    TGB_CUDA(cudaEventCreate(&a));
+    TGB_CUDA(cudaEventCreate(&b));
+    double tot = 0;
+    for (int i = 0; i <= reps; ++i) {
+      random_ids_kernel<<<grid_for(rows, 256), 256, 0, ctx->stream>>>(ids, rows, mb, N - mb, 77 + i);
+      TGB_LAUNCHED();
+      TGB_CUDA(cudaMemsetAsync(fl, i, 256ull << 20, ctx->stream));
+      TGB_CUDA(cudaMemsetAsync(c, 0, 32, ctx->stream));
+      TGB_CUDA(cudaEventRecord(a, ctx->stream));
+      launch_gather(s, ids, rows, out, c, reinterpret_cast<unsigned long long*>(c + 3));
+      TGB_CUDA(cudaEventRecord(b, ctx->stream));
+      TGB_CUDA(cudaEventSynchronize(b));
+      float ms = 0;
+      TGB_CUDA(cudaEventElapsedTime(&ms, a, b));
+      if (i) tot += ms;  // the first launch warms
+    }
+    cudaEventDestroy(a);
+    cudaEventDestroy(b);
+    *us = tot / std::max(reps, 1) * 1e3;
+  });
+}
 uint64_t tg_store_local_rows(const tg_store* s) { return s ? s->local_rows : 0; }
 
 int tg_store_set_peer(tg_store* s, uint32_t d, const void* peer_local_base) {
@@ -1026,11 +1077,93 @@ int tg_store_share_cold(tg_store* s, const tg_store* owner) {
   });
 }
 
+namespace tgb {
+// K7 placement from `src_rows` (src_nrows rows of R bytes; host or device)
+// where new id i's bytes are source row order[i] (u32, device, N entries).
+void place_impl(tg_store* s, const void* src_rows, uint64_t src_nrows, const uint32_t* order) {
+  tg_ctx* ctx = s->ctx;
+  const uint64_t N = s->L.num_rows, R = s->R, mb = s->L.multi_boundary;
+  // source rows: device memory, mapped pinned memory, or pageable (registered here)
+  const uint8_t* src = nullptr;
+  void* reg = nullptr;
+  if (is_device_ptr(src_rows)) {
+    src = static_cast<const uint8_t*>(src_rows);
+  } else {
+    bool owned = false;
+    src = acquire_host_matrix(src_rows, src_nrows * R, &owned);
+    if (owned) reg = const_cast<void*>(src_rows);
+  }
+  // K7a: this device's HBM rows (replicated prefix + interleaved slice)
+  MoveArgs a{};
+  a.src = src;
+  a.dst = s->local;
+  a.src_stride = R;
+  a.dst_stride = R;
+  a.src_idx32 = order;
+  a.slot_mode = 1;
+  a.lb = s->L.local_boundary;
+  a.D = s->L.num_devices;
+  a.dev = s->dev;
+  launch_move(ctx, a, s->local_rows, R);
+  // K7b: the cold tier
+  if (s->cold_owner) {
+    s->cold_dev = s->cold_owner->cold_dev;
+    s->cold_src = s->cold_owner->cold_src;
+    s->cold_stride = s->cold_owner->cold_stride;
+  } else if (s->flags & TG_COLD_INDIRECT) {
+    // the caller's rows are read in place through the row map
+    const uint64_t cold = N - mb;
+    if (!s->cold_src) {
+      TGB_CUDA(cudaMalloc(&s->cold_src, sizeof(uint32_t) * std::max<uint64_t>(cold, 1)));
+      s->own_cold_src = true;
+    }
+    if (cold)
+      TGB_CUDA(cudaMemcpyAsync(s->cold_src, order + mb, cold * 4, cudaMemcpyDeviceToDevice,
+                               ctx->stream));
+    s->cold_dev = src;
+    s->cold_stride = R;
+    if (s->registered) release_host_matrix(s->registered);
+    s->registered = reg;  // keep the caller's matrix mapped for the store's lifetime
+    reg = nullptr;
+  } else {
+    const uint64_t cold = N - mb;
+    s->cold_stride = (s->flags & TG_COLD_PAD128) ? (R + 127) / 128 * 128 : R;
+    if (!s->own_cold) {
+      TGB_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&s->cold_host),
+                             std::max<uint64_t>(cold * s->cold_stride, 16),
+                             cudaHostAllocMapped | cudaHostAllocPortable));
+      s->own_cold = true;
+    }
+    void* cd = nullptr;
+    TGB_CUDA(cudaHostGetDevicePointer(&cd, s->cold_host, 0));
+    s->cold_dev = static_cast<const uint8_t*>(cd);
+    MoveArgs c{};
+    c.src = src;
+    c.dst = static_cast<uint8_t*>(cd);
+    c.src_stride = R;
+    c.dst_stride = s->cold_stride;
+    c.src_idx32 = order;
+    c.src_row_base = mb;
+    launch_move(ctx, c, cold, R);
+  }
+  ctx->sync();
+  if (reg) release_host_matrix(reg);
+  s->placed = true;
+}
+
+__global__ void check_rows_kernel(const uint32_t* __restrict__ m, uint64_t n, uint64_t nrows,
+                                  unsigned long long* bad) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+       i += (uint64_t)gridDim.x * blockDim.x)
+    if (m[i] >= nrows) atomicMin(bad, (unsigned long long)i);
+}
+}  // namespace tgb
+
 int tg_store_place(tg_store* s, const void* features, const uint64_t* new_id_of) {
   return guard([&] {
     tg_ctx* ctx = s->ctx;
     DeviceGuard dg(ctx->device);
-    const uint64_t N = s->L.num_rows, R = s->R, mb = s->L.multi_boundary;
+    const uint64_t N = s->L.num_rows;
     if (N == 0) {
       s->placed = true;
       return;
@@ -1039,69 +1172,34 @@ int tg_store_place(tg_store* s, const void* features, const uint64_t* new_id_of)
     const uint64_t* perm = dev_in(ctx, new_id_of, N, kStageIn0);
     uint32_t* order = ctx->scratch_t<uint32_t>(kScratchD, N);
     check_permutation(ctx, perm, N, order);
-    // source rows: device memory, mapped pinned memory, or pageable (registered here)
-    const uint8_t* src = nullptr;
-    void* reg = nullptr;
-    if (is_device_ptr(features)) {
-      src = static_cast<const uint8_t*>(features);
-    } else {
-      bool owned = false;
-      src = acquire_host_matrix(features, N * R, &owned);
-      if (owned) reg = const_cast<void*>(features);
+    place_impl(s, features, N, order);
+  });
+}
+
+int tg_store_place_rows(tg_store* s, const void* rows, uint64_t nrows, const uint32_t* row_of) {
+  return guard([&] {
+    tg_ctx* ctx = s->ctx;
+    DeviceGuard dg(ctx->device);
+    const uint64_t N = s->L.num_rows;
+    if (N == 0) {
+      s->placed = true;
+      return;
     }
-    // K7a: this device's HBM rows (replicated prefix + interleaved slice)
-    MoveArgs a{};
-    a.src = src;
-    a.dst = s->local;
-    a.src_stride = R;
-    a.dst_stride = R;
-    a.src_idx32 = order;
-    a.slot_mode = 1;
-    a.lb = s->L.local_boundary;
-    a.D = s->L.num_devices;
-    a.dev = s->dev;
-    launch_move(ctx, a, s->local_rows, R);
-    // K7b: the cold tier
-    if (s->cold_owner) {
-      s->cold_dev = s->cold_owner->cold_dev;
-      s->cold_src = s->cold_owner->cold_src;
-      s->cold_stride = s->cold_owner->cold_stride;
-    } else if (s->flags & TG_COLD_INDIRECT) {
-      if (is_device_ptr(features)) domain_error("TG_COLD_INDIRECT needs the matrix in host memory");
-      const uint64_t cold = N - mb;
-      TGB_CUDA(cudaMalloc(&s->cold_src, sizeof(uint32_t) * std::max<uint64_t>(cold, 1)));
-      s->own_cold_src = true;
-      if (cold)
-        TGB_CUDA(cudaMemcpyAsync(s->cold_src, order + mb, cold * 4, cudaMemcpyDeviceToDevice,
-                                 ctx->stream));
-      s->cold_dev = src;
-      s->cold_stride = R;
-      s->registered = reg;  // keep the caller's matrix mapped for the store's lifetime
-      reg = nullptr;
-    } else {
-      const uint64_t cold = N - mb;
-      s->cold_stride = (s->flags & TG_COLD_PAD128) ? (R + 127) / 128 * 128 : R;
-      if (!s->own_cold) {
-        TGB_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&s->cold_host),
-                               std::max<uint64_t>(cold * s->cold_stride, 16),
-                               cudaHostAllocMapped | cudaHostAllocPortable));
-        s->own_cold = true;
-      }
-      void* cd = nullptr;
-      TGB_CUDA(cudaHostGetDevicePointer(&cd, s->cold_host, 0));
-      s->cold_dev = static_cast<const uint8_t*>(cd);
-      MoveArgs c{};
-      c.src = src;
-      c.dst = static_cast<uint8_t*>(cd);
-      c.src_stride = R;
-      c.dst_stride = s->cold_stride;
-      c.src_idx32 = order;
-      c.src_row_base = mb;
-      launch_move(ctx, c, cold, R);
-    }
+    if (nrows == 0) domain_error("tg_store_place_rows: no source rows");
+    if (nrows > 0xffffffffull) domain_error("tg_store_place_rows: at most 2^32-1 source rows");
+    uint32_t* m = ctx->scratch_t<uint32_t>(kScratchD, N);
+    TGB_CUDA(cudaMemcpyAsync(m, row_of, 4 * N, cudaMemcpyDefault, ctx->stream));
+    auto* bad = ctx->scratch_t<unsigned long long>(kSmall, 1);
+    TGB_CUDA(cudaMemsetAsync(bad, 0xff, 8, ctx->stream));
+    check_rows_kernel<<<grid_for(N, 256), 256, 0, ctx->stream>>>(m, N, nrows, bad);
+    TGB_LAUNCHED();
+    unsigned long long hb;
+    TGB_CUDA(cudaMemcpyAsync(&hb, bad, 8, cudaMemcpyDeviceToHost, ctx->stream));
     ctx->sync();
-    if (reg) release_host_matrix(reg);
-    s->placed = true;
+    if (hb != ~0ull)
+      domain_error("tg_store_place_rows: row_of[" + std::to_string(hb) + "] >= " +
+                   std::to_string(nrows));
+    place_impl(s, rows, nrows, m);
   });
 }
 
@@ -1251,6 +1349,8 @@ int tg_host_register(void* p, uint64_t bytes) {
     TGB_CUDA(cudaHostRegister(p, bytes, cudaHostRegisterMapped | cudaHostRegisterPortable));
   });
 }
+void* tg_mapped_device_ptr(const void* host) { return mapped_device_ptr(host); }
+
 int tg_host_unregister(void* p) {
   return guard([&] { TGB_CUDA(cudaHostUnregister(p)); });
 }

@@ -116,3 +116,33 @@ def test_features_pinned_gpu(num_rows: int, dim: int, out: np.ndarray, device="c
         dst[r0:r1].copy_(base[:, None] + cols[None, :])
     torch.cuda.synchronize()
     return out
+
+
+# ---------------------------------------------------------------- C4 (fp16)
+# MAG240M-shaped features: 768-d fp16. The reference's FeatureMatrix is
+# byte-opaque (elem_bytes, feature_matrix.hpp:13-20) and its maker is f32
+# only (feature_matrix.cpp:16-28), so the fp16 fixture is the same closed form
+# narrowed to values fp16 holds exactly: base = mix64(r) >> 54 (0..1023),
+# value = base + c (c < 768, so every value is an integer <= 1790).
+def expected_rows_f16(old_ids: np.ndarray, dim: int) -> np.ndarray:
+    base = (mix64_np(np.asarray(old_ids, np.uint64)) >> np.uint64(54)).astype(np.float32)
+    return (base[:, None] + np.arange(dim, dtype=np.float32)[None, :]).astype(np.float16)
+
+
+def test_features_f16_gpu(num_rows: int, dim: int, out: np.ndarray, device="cuda",
+                          rows_per_chunk=1 << 21):
+    """expected_rows_f16 for rows [0, num_rows), computed on the GPU and copied
+    into `out` (pinned or registered host memory, num_rows*dim*2 bytes)."""
+    import torch
+    if isinstance(out, torch.Tensor):
+        dst = out.view(torch.float16)[: num_rows * dim].view(num_rows, dim)
+    else:
+        dst = torch.from_numpy(out.reshape(-1)[: num_rows * dim * 2].view(np.float16)).view(num_rows, dim)
+    cols = torch.arange(dim, dtype=torch.float32, device=device)
+    for r0 in range(0, num_rows, rows_per_chunk):
+        r1 = min(num_rows, r0 + rows_per_chunk)
+        r = torch.arange(r0, r1, dtype=torch.int64, device=device)
+        base = ((mix64_torch(r) >> 54) & 1023).to(torch.float32)
+        dst[r0:r1].copy_((base[:, None] + cols[None, :]).to(torch.float16))
+    torch.cuda.synchronize()
+    return out

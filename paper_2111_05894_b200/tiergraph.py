@@ -638,6 +638,21 @@ class TieredFeatureStore:
         self._keep = [data]  # TG_COLD_INDIRECT maps the caller's matrix: keep it alive
         _check(LIB.tg_store_place(self.h, _ptr(data), _nonempty(p, np.uint64)))
 
+    def place_rows(self, rows, row_of):
+        """K7 from a caller's row array: new id i holds rows[row_of[i]]
+        (rows: [nrows, row_bytes] host or device; row_of: N u32)."""
+        R = self.layout.bytes_per_row()
+        if not _is_torch(rows):
+            rows = np.ascontiguousarray(rows)
+        nbytes = (rows.numel() * rows.element_size()) if _is_torch(rows) else rows.nbytes
+        if R == 0 or nbytes % R:
+            raise FormatError(f"rows: {nbytes} bytes is not a whole number of {R}-byte rows")
+        ro = np.ascontiguousarray(row_of, dtype=np.uint32) if not _is_torch(row_of) else row_of
+        if _len(ro) != self.layout.num_rows:
+            raise DomainError(f"row map length {_len(ro)} != num_rows {self.layout.num_rows}")
+        self._keep = [rows, ro]
+        _check(LIB.tg_store_place_rows(self.h, _ptr(rows), nbytes // R, _ptr(ro)))
+
     @property
     def local_base(self) -> int:
         return int(LIB.tg_store_local_base(self.h) or 0)
@@ -645,6 +660,13 @@ class TieredFeatureStore:
     @property
     def local_rows(self) -> int:
         return int(LIB.tg_store_local_rows(self.h))
+
+    def measure_cold_us(self, rows: int, reps: int = 5) -> float:
+        """Mean us to read `rows` random rows of this store's cold region
+        (L2 flushed per launch): the floor of a gather's cold part."""
+        v = C.c_double()
+        _check(LIB.tg_store_measure_cold_us(self.h, int(rows), int(reps), C.byref(v)))
+        return float(v.value)
 
     def set_peer(self, device_index: int, peer_local_base: int):
         _check(LIB.tg_store_set_peer(self.h, int(device_index), C.c_void_p(peer_local_base)))
@@ -697,6 +719,21 @@ def host_alloc(nbytes: int) -> np.ndarray:
     arr_owner = _PinnedOwner(p.value)
     _PINNED[id(arr)] = arr_owner
     return arr
+
+
+def host_register(arr: np.ndarray) -> None:
+    """Pin and map caller host memory in place (cudaHostRegister,
+    PAPER.md:659-668); a store placed from it then reads it as is."""
+    _check(LIB.tg_host_register(C.c_void_p(arr.ctypes.data), int(arr.nbytes)))
+
+
+def mapped_device_pointer(arr: np.ndarray) -> int:
+    """Device address of registered/pinned host memory (0 if not mapped)."""
+    return int(LIB.tg_mapped_device_ptr(C.c_void_p(arr.ctypes.data)) or 0)
+
+
+def host_unregister(arr: np.ndarray) -> None:
+    _check(LIB.tg_host_unregister(C.c_void_p(arr.ctypes.data)))
 
 
 class _PinnedOwner:
