@@ -228,3 +228,25 @@ def test_fused_peer_exchange_virtual_ranks(tg, ctx, ranks):
     un = D.weighted_reverse_pagerank_peers(g, tg.PagerankConfig(3, 0.85), None, ctxs)
     want_un = tg.reverse_pagerank(g, tg.PagerankConfig(3, 0.85))
     assert all(o.cpu().numpy().tobytes() == want_un.tobytes() for o in un)
+
+
+@pytest.mark.parametrize("n,draws", [(200_000, 5_000_000), (1_500_000, 6_000_000)])
+def test_in_degrees_partitioned_count(tg, ctx, n, draws):
+    """K1 on graphs with >= 4M edges (R-MAT hubs; 
+    scan / scatter, then per-bucket shared-memory counts; the hub buckets
+    are split over several CTAs) equals csr_graph.cpp:89-93 exactly."""
+    from paper_2111_05894_b200 import synth
+    off, tgt = synth.rmat_graph(n, draws, seed=11)
+    assert len(tgt) >= 1 << 22
+    want = np.bincount(tgt.astype(np.int64), minlength=n).astype(np.uint64)
+    g = tg.CsrGraph(off, tgt)
+    assert np.array_equal(tg.in_degrees(g, ctx=ctx), want)
+    # a hub id holding more than one count item (> 2^20 edges) and an empty tail
+    tgt2 = np.sort(np.concatenate([np.zeros(1_500_000, np.uint64),
+                                   np.random.default_rng(1).integers(0, n // 2, 3_000_000)
+                                   .astype(np.uint64)]))
+    off2 = np.zeros(n + 1, np.uint64)
+    off2[1:] = len(tgt2)  # one row holds every edge (unsorted rows are fine for K1)
+    g2 = tg.CsrGraph(off2, tgt2)
+    want2 = np.bincount(tgt2.astype(np.int64), minlength=n).astype(np.uint64)
+    assert np.array_equal(tg.in_degrees(g2, ctx=ctx), want2)
