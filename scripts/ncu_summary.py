@@ -2,6 +2,11 @@
 
   python scripts/ncu_summary.py launches <launches.csv>            -> per-kernel share table
   python scripts/ncu_summary.py full <report.ncu-rep> [name]        -> key metrics per launch
+  python scripts/ncu_summary.py memory <metrics.csv> [hbm_peak] [pcie_peak]
+        -> per kernel: launches, avg us, HBM / PCIe (sysmem) / NVLink (peer) GB/s
+           achieved per launch vs the peaks (the csv of an ncu --metrics run with
+           gpu__time_duration.sum, dram__bytes_read.sum, dram__bytes_write.sum,
+           lts__t_sectors_aperture_sysmem.sum, lts__t_sectors_aperture_peer.sum)
 Prints markdown; `full` also prints one JSON line with the DRAM traffic per launch.
 """
 import collections
@@ -70,8 +75,47 @@ def full(path, name=None):
                       "dram_bytes_per_launch_mean": int(sum(dram) / len(dram))}))
 
 
+def memory(path, hbm_peak=6543.4, pcie_peak=55.4):
+    rows = list(csv.reader(open(path)))
+    hi = [i for i, r in enumerate(rows) if "Kernel Name" in r][0]
+    h = rows[hi]
+    ki, ni, vi, ui = (h.index("Kernel Name"), h.index("Metric Name"), h.index("Metric Value"),
+                      h.index("Metric Unit"))
+    idi = h.index("ID")
+    launches_ = collections.defaultdict(dict)
+    names = {}
+    for r in rows[hi + 1:]:
+        if len(r) <= vi:
+            continue
+        v = float(r[vi].replace(",", "")) * SCALE.get(r[ui], 1.0)
+        if r[ni].startswith("lts__t_sectors"):
+            v = float(r[vi].replace(",", "")) * 32  # sectors -> bytes
+        launches_[r[idi]][r[ni]] = v
+        names[r[idi]] = r[ki].split("(")[0].replace("void ", "")
+    agg = collections.defaultdict(lambda: collections.defaultdict(float))
+    for lid, m in launches_.items():
+        a = agg[names[lid]]
+        a["n"] += 1
+        a["t"] += m.get("gpu__time_duration.sum", 0.0)
+        a["hbm"] += m.get("dram__bytes_read.sum", 0.0) + m.get("dram__bytes_write.sum", 0.0)
+        a["sys"] += m.get("lts__t_sectors_aperture_sysmem.sum", 0.0)
+        a["peer"] += m.get("lts__t_sectors_aperture_peer.sum", 0.0)
+    print(f"| kernel | launches | avg us | HBM GB/s (of {hbm_peak:.0f}) | PCIe sysmem GB/s "
+          f"(of {pcie_peak:.1f}) | NVLink peer GB/s |")
+    print("|---|---|---|---|---|---|")
+    for k, a in sorted(agg.items(), key=lambda x: -x[1]["t"]):
+        t = a["t"]
+        if t <= 0:
+            continue
+        hb, sy, pe = a["hbm"] / t / 1e9, a["sys"] / t / 1e9, a["peer"] / t / 1e9
+        print(f"| `{k[:60]}` | {int(a['n'])} | {t / a['n'] * 1e6:.1f} | {hb:.0f} "
+              f"({hb / hbm_peak:.2f}) | {sy:.1f} ({sy / pcie_peak:.2f}) | {pe:.1f} |")
+
+
 if __name__ == "__main__":
     if sys.argv[1] == "launches":
         launches(sys.argv[2])
+    elif sys.argv[1] == "memory":
+        memory(sys.argv[2], *[float(x) for x in sys.argv[3:5]])
     else:
         full(sys.argv[2], sys.argv[3] if len(sys.argv) > 3 else None)
