@@ -264,6 +264,13 @@ int tg_gather_rows(tg_store* s, const uint64_t* ids, uint64_t n, void* dst, tg_r
 int tg_gather_rows_async(tg_store* s, const uint64_t* ids_dev, uint64_t n, void* dst_dev,
                          uint64_t* counters_dev, uint64_t* err_dev);
 
+/* Measurement of the synchronous path exactly as a C/C++ caller sees it:
+ * k calls of tg_gather_rows (ids[i]: counts[i] host ids each, into dst),
+ * each timed with steady_clock around the call; with flush_l2 a 256 MB
+ * device memset runs (untimed) before every call. *seconds = the sum. */
+int tg_time_gather_rows(tg_store* s, const uint64_t* const* ids, const uint64_t* counts, uint64_t k,
+                        void* dst, int flush_l2, tg_report* report, double* seconds);
+
 /* ------------------------------------------------------------- peer memory */
 int tg_enable_peer_access(int device, int peer);
 int tg_ipc_get_handle(const void* dev_ptr, void* handle_out /* 64 bytes */);

@@ -24,6 +24,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <chrono>
 #include <map>
 #include <mutex>
 #include <string>
@@ -49,6 +50,7 @@ struct tg_store {
   const tg_store* cold_owner = nullptr;
   bool placed = false;
   uint64_t* counters = nullptr;                   // device: 3 x u64 + err
+  uint64_t* result_host = nullptr;                // pinned: the counters read back
 };
 
 namespace tgb {
@@ -1015,6 +1017,7 @@ int tg_store_destroy(tg_store* s) {
   DeviceGuard dg(s->ctx->device);
   cudaFree(s->local);
   cudaFree(s->counters);
+  if (s->result_host) cudaFreeHost(s->result_host);
   if (s->own_cold && s->cold_host) cudaFreeHost(s->cold_host);
   if (s->own_cold_src) cudaFree(s->cold_src);
   if (s->registered) release_host_matrix(s->registered);
@@ -1228,7 +1231,9 @@ int tg_gather_rows(tg_store* s, const uint64_t* ids, uint64_t n, void* dst, tg_r
     TGB_CUDA(cudaMemsetAsync(c, 0, 24, ctx->stream));
     TGB_CUDA(cudaMemsetAsync(err, 0xff, 8, ctx->stream));
     launch_gather(s, d, n, o.dev(), c, err);
-    uint64_t h[4];
+    if (!s->result_host)
+      TGB_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&s->result_host), 64, cudaHostAllocDefault));
+    uint64_t* h = s->result_host;
     TGB_CUDA(cudaMemcpyAsync(h, c, 32, cudaMemcpyDeviceToHost, ctx->stream));
     o.finish();
     if (h[3] != ~0ull) {  // reference semantics: prefix accounted, then DomainError
@@ -1243,6 +1248,28 @@ int tg_gather_rows(tg_store* s, const uint64_t* ids, uint64_t n, void* dst, tg_r
       range_error(s->L, bad);
     }
     add_report(report, h[0], h[1], h[2], s->R);
+  });
+}
+
+int tg_time_gather_rows(tg_store* s, const uint64_t* const* ids, const uint64_t* counts, uint64_t k,
+                        void* dst, int flush_l2, tg_report* report, double* seconds) {
+  return guard([&] {
+    tg_ctx* ctx = s->ctx;
+    DeviceGuard dg(ctx->device);
+    uint8_t* fl = flush_l2 ? ctx->scratch_t<uint8_t>(kScratchE, 256ull << 20) : nullptr;
+    double tot = 0.0;
+    for (uint64_t i = 0; i < k; ++i) {
+      if (fl) {
+        TGB_CUDA(cudaMemsetAsync(fl, static_cast<int>(i & 0xff), 256ull << 20, ctx->stream));
+        ctx->sync();
+      }
+      const auto t0 = std::chrono::steady_clock::now();
+      const int rc = tg_gather_rows(s, ids[i], counts[i], dst, report);
+      const auto t1 = std::chrono::steady_clock::now();
+      if (rc) throw Error(rc, tg_last_error());
+      tot += std::chrono::duration<double>(t1 - t0).count();
+    }
+    *seconds = tot;
   });
 }
 

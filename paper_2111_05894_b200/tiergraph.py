@@ -692,6 +692,24 @@ class TieredFeatureStore:
                 report._load(r)
         return out
 
+    def time_gather_rows(self, id_lists, out, report: TrafficReport = None,
+                         flush_l2: bool = True) -> float:
+        """Seconds spent in len(id_lists) synchronous tg_gather_rows calls,
+        timed inside the library around each call (no Python in the timed
+        region); ids are host arrays (pinned ones are read in place)."""
+        lists = [np.ascontiguousarray(x, dtype=np.uint64) for x in id_lists]
+        ptrs = (C.c_void_p * len(lists))(*[x.ctypes.data for x in lists])
+        cnts = (C.c_uint64 * len(lists))(*[len(x) for x in lists])
+        r = (report or TrafficReport())._c()
+        sec = C.c_double()
+        try:
+            _check(LIB.tg_time_gather_rows(self.h, ptrs, cnts, len(lists), _ptr(out),
+                                           int(flush_l2), C.byref(r), C.byref(sec)))
+        finally:
+            if report is not None:
+                report._load(r)
+        return float(sec.value)
+
     def gather_rows_async(self, ids_dev, out_dev, counters_dev, err_dev):
         """Stream-ordered K8 on device tensors (no synchronisation)."""
         _check(LIB.tg_gather_rows_async(self.h, _ptr(ids_dev), _len(ids_dev), _ptr(out_dev),

@@ -249,3 +249,25 @@ def test_place_rows_from_a_row_cache(tg, ctx, cold_mode):
         st.place_rows(rows, np.full(n, P, np.uint32))
     # the cold part timed alone (measurement helper) runs on the placed store
     assert st.measure_cold_us(100, 2) > 0
+
+
+def test_time_gather_rows_matches_gather_rows(tg, ctx):
+    """tg_time_gather_rows (the bench's e2e timer) runs the public
+    tg_gather_rows per list: same bytes, same accumulated report."""
+    chk = checker()
+    n, dim = 4000, 32
+    rng = np.random.default_rng(9)
+    perm = rng.permutation(n).astype(np.uint64)
+    feat = rng.integers(0, 256, (n, dim * 4), dtype=np.uint8)
+    lay = tg.plan_layout(n, 0.25, 0.0, 1, dim, 4)
+    st = tg.TieredFeatureStore(feat, tg.NodePermutation(perm), lay, ctx=ctx)
+    lists = [np.unique(rng.integers(0, n, 700)).astype(np.uint64) for _ in range(4)]
+    out = np.zeros((max(len(x) for x in lists), dim * 4), np.uint8)
+    rep = tg.TrafficReport()
+    sec = st.time_gather_rows(lists, out, rep)
+    assert sec > 0
+    want = np.zeros(6, np.uint64)
+    for x in lists:
+        want = chk.gather(lay.as_tuple(), x, 0, want)
+    assert np.array_equal(rep.as_array(), want)
+    assert np.array_equal(out[:len(lists[-1])], st.gather_rows(lists[-1]))
