@@ -12,7 +12,7 @@ timeout 900 python bench.py > $O/bench_c2.json 2> $O/bench_c2.err
 timeout 600 python bench.py --impl reference --steps 20 --warmup 3 > $O/bench_c2_ref.json 2> $O/bench_c2_ref.err
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $O/launches.csv \
    python bench.py --steps 20 --warmup 3 --no-cpu-baseline > $O/bench_ncu.log 2>&1
-timeout 1200 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum,lts__t_sectors_aperture_sysmem.sum,lts__t_sectors_aperture_peer.sum \
+timeout 1200 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum,syslts__t_sectors_aperture_sysmem_lookup_miss.sum,syslts__t_sectors_aperture_peer_lookup_miss.sum \
    --clock-control none --csv --log-file $O/kernel_memory.csv \
    python bench.py --steps 5 --warmup 3 --no-cpu-baseline > $O/bench_ncu_mem.log 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:gather -s 5 -c 2 \

@@ -6,7 +6,9 @@
         -> per kernel: launches, avg us, HBM / PCIe (sysmem) / NVLink (peer) GB/s
            achieved per launch vs the peaks (the csv of an ncu --metrics run with
            gpu__time_duration.sum, dram__bytes_read.sum, dram__bytes_write.sum,
-           lts__t_sectors_aperture_sysmem.sum, lts__t_sectors_aperture_peer.sum)
+           syslts__t_sectors_aperture_sysmem_lookup_miss.sum,
+           syslts__t_sectors_aperture_peer_lookup_miss.sum: sectors of 32 B read from
+           host memory / peer GPUs through the system L2 slice)
 Prints markdown; `full` also prints one JSON line with the DRAM traffic per launch.
 """
 import collections
@@ -19,7 +21,9 @@ import sys
 KEYS = [
     "gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
     "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed",
-    "lts__t_bytes.sum", "lts__t_sectors_aperture_sysmem.sum",
+    "lts__t_bytes.sum", "pcie__read_bytes.sum.per_second", "pcie__write_bytes.sum.per_second",
+    "syslts__t_sectors_aperture_sysmem_lookup_miss.sum",
+    "syslts__t_sectors_aperture_peer_lookup_miss.sum",
     "sm__throughput.avg.pct_of_peak_sustained_elapsed",
     "sm__warps_active.avg.pct_of_peak_sustained_active", "launch__registers_per_thread",
     "launch__grid_size", "launch__block_size", "launch__occupancy_limit_registers",
@@ -28,7 +32,7 @@ KEYS = [
 ]
 
 SCALE = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "usecond": 1e-6, "msecond": 1e-3,
-         "nsecond": 1e-9, "second": 1}
+         "nsecond": 1e-9, "second": 1, "ns": 1e-9, "us": 1e-6, "ms": 1e-3, "s": 1}
 
 
 def launches(path):
@@ -85,10 +89,10 @@ def memory(path, hbm_peak=6543.4, pcie_peak=55.4):
     launches_ = collections.defaultdict(dict)
     names = {}
     for r in rows[hi + 1:]:
-        if len(r) <= vi:
+        if len(r) <= vi or r[vi] in ("n/a", ""):
             continue
         v = float(r[vi].replace(",", "")) * SCALE.get(r[ui], 1.0)
-        if r[ni].startswith("lts__t_sectors"):
+        if "t_sectors" in r[ni]:
             v = float(r[vi].replace(",", "")) * 32  # sectors -> bytes
         launches_[r[idi]][r[ni]] = v
         names[r[idi]] = r[ki].split("(")[0].replace("void ", "")
@@ -98,8 +102,8 @@ def memory(path, hbm_peak=6543.4, pcie_peak=55.4):
         a["n"] += 1
         a["t"] += m.get("gpu__time_duration.sum", 0.0)
         a["hbm"] += m.get("dram__bytes_read.sum", 0.0) + m.get("dram__bytes_write.sum", 0.0)
-        a["sys"] += m.get("lts__t_sectors_aperture_sysmem.sum", 0.0)
-        a["peer"] += m.get("lts__t_sectors_aperture_peer.sum", 0.0)
+        a["sys"] += m.get("syslts__t_sectors_aperture_sysmem_lookup_miss.sum", 0.0)
+        a["peer"] += m.get("syslts__t_sectors_aperture_peer_lookup_miss.sum", 0.0)
     print(f"| kernel | launches | avg us | HBM GB/s (of {hbm_peak:.0f}) | PCIe sysmem GB/s "
           f"(of {pcie_peak:.1f}) | NVLink peer GB/s |")
     print("|---|---|---|---|---|---|")
