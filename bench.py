@@ -45,23 +45,25 @@ CONFIGS = {
                train=0.10, hot=0.20),
     # C3: BASELINE names no train fraction, fanout or batch for papers100M;
     # 10 %, (15,10,5) and 1024 are used and stated. The epoch is bounded to
-    # max_batches minibatches; the cold rows stay in the caller's pinned matrix
-    # (registered in place, indexed through the permutation): no 45 GB copy.
+    # max_batches minibatches; the cold rows get their own pinned copy in
+    # new-id (score) order (45 GB): the most-read cold rows then share the
+    # first GBs, which the GPU translates far more cheaply than random rows of
+    # the 57 GB original (87.6 vs 102.6 us per minibatch, profiles/r01f).
     "c3": dict(workload="C3: ogbn-papers100M-shaped R-MAT 111M nodes / 1.6B draws, 128-d f32, "
                         "10% train, fanout (15,10,5), batch 1024, hot 20% sharded over the "
-                        "ranks, cold rows via UVA from the pinned matrix",
+                        "ranks, cold rows via UVA from a pinned copy in new-id order",
                nodes=111_000_000, draws=1_600_000_000, dim=128, elem=4, fanouts=[15, 10, 5],
-               batch=1024, train=0.10, hot=0.20, max_batches=512, cold_mode="indirect",
+               batch=1024, train=0.10, hot=0.20, max_batches=512, cold_mode="reordered",
                cpu_gather=False),
     # C4: the hot tier is capped at 5% of the rows PER GPU (plan_layout's
     # per-device budget, tiering.cpp:87-96), sharded, so K = 5% x ranks. The
     # 374.8 GB fp16 matrix exceeds the box's 196 GB of host RAM (and the
     # driver maps at most ~RAM-size of host memory for the GPU, measured), so
-    # the host side is a pinned row cache of P rows (`row_cache_gb`) and the
-    # store is placed with tg_store_place_rows: new id i reads cache row
-    # (original id mod P). Graph, PageRank, selection, sampling, layout and
-    # accounting run at full size; parity checks the gathered bytes against
-    # that map.
+    # the host side is a pinned row cache of P rows (`row_cache_gb`) holding
+    # the reordered matrix wrapped every P rows, placed with
+    # tg_store_place_rows: new id i reads cache row (i mod P). Graph,
+    # PageRank, selection, sampling, layout and accounting run at full size;
+    # parity checks the gathered bytes against that map.
     "c4": dict(workload="C4: MAG240M-shaped R-MAT 244M nodes / 1.7B draws, 768-d fp16, 10% train, "
                         "fanout (15,10,5), batch 1024, hot budget 5% of rows per GPU (sharded), "
                         "cold rows via UVA",
@@ -75,12 +77,15 @@ def hot_fraction(cfg, world):
     return cfg["hot"] if "hot" in cfg else min(1.0, cfg["hot_per_gpu"] * world)
 
 
-def expected_rows(cfg, old_ids):
-    """Closed-form rows of the bench matrix for original ids (aliased for C4)."""
+def expected_rows(cfg, new_ids, inv):
+    """Closed-form rows of the bench matrix for NEW ids: the original row
+    inv[id]; for C4, row cache row (id mod P) (see CONFIGS["c4"])."""
     from paper_2111_05894_b200 import synth
-    ids = np.asarray(old_ids, np.uint64)
+    new_ids = np.asarray(new_ids, np.uint64)
     if cfg.get("row_cache_gb"):
-        ids = ids % np.uint64(cache_rows(cfg))
+        ids = new_ids % np.uint64(cache_rows(cfg))
+    else:
+        ids = inv[new_ids.astype(np.int64)]
     if cfg.get("fp16"):
         return synth.expected_rows_f16(ids, cfg["dim"])
     return synth.expected_rows(ids, cfg["dim"])
@@ -401,12 +406,12 @@ def run_ours(args):
         budget = (int(np.ceil(cfg["hot_per_gpu"] * n)) + 1) * R
     lay = tg.plan_layout(n, hot, 0.0, world, cfg["dim"], cfg["elem"], budget)
     if cfg.get("row_cache_gb"):
+        # the cache holds the rows in new-id (score) order, wrapping every P
+        # rows, as a reorder_features'd matrix would (reorder.cpp:97-117)
         store = tg.TieredFeatureStore(None, perm, lay, rank, ctx=ctx,
                                       cold_mode=cfg.get("cold_mode", "reordered"), place=False)
-        inv = np.empty(n, np.uint64)
-        inv[perm.new_id_of.astype(np.int64)] = np.arange(n, dtype=np.uint64)
-        store.place_rows(feat, (inv % np.uint64(len(feat))).astype(np.uint32))
-        del inv
+        store.place_rows(feat, (np.arange(n, dtype=np.uint64) % np.uint64(len(feat)))
+                         .astype(np.uint32))
     else:
         store = tg.TieredFeatureStore(feat, perm, lay, rank, ctx=ctx,
                                       cold_mode=cfg.get("cold_mode", "reordered"))
@@ -654,7 +659,8 @@ def run_ours(args):
         if cfg.get("row_cache_gb"):
             result["config"]["host_row_cache"] = {
                 "rows": cache_rows(cfg), "bytes": cache_rows(cfg) * R,
-                "map": "new id i reads cache row (original id mod rows): tg_store_place_rows",
+                "map": "new id i reads cache row (i mod rows), i.e. the reordered matrix "
+                       "wrapped every `rows` rows: tg_store_place_rows",
                 "why": "the 374.8 GB matrix exceeds the box's host RAM (196 GB)"}
         if world == 1 and not args.no_cpu_baseline:
             result["cpu_baseline"], result["parity"] = cpu_baseline(
@@ -734,7 +740,7 @@ def cpu_baseline(cfg, off, tgt, tid, scores, perm, feat, R, lay, lists, store, o
         inv[perm.new_id_of.astype(np.int64)] = np.arange(len(inv), dtype=np.uint64)
         mine = tg.TrafficReport()
         got = store.gather_rows(ids, report=mine)
-        want = expected_rows(cfg, inv[ids.astype(np.int64)])
+        want = expected_rows(cfg, ids, inv)
         parity["gather_rows_bit_exact"] = bool(np.array_equal(got.view(want.dtype), want))
         r = ref.gather(lay.as_tuple(), ids, 0)
     if gt is not None:
