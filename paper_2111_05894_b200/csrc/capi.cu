@@ -202,9 +202,12 @@ int tg_ctx_destroy(tg_ctx* c) {
     if (c->slot_ptr[i]) cudaFree(c->slot_ptr[i]);
   if (c->aux) {
     cudaStreamSynchronize(c->aux);
+    cudaStreamSynchronize(c->aux2);
     cudaStreamDestroy(c->aux);
+    cudaStreamDestroy(c->aux2);
     cudaEventDestroy(c->ev_fork);
     cudaEventDestroy(c->ev_join);
+    cudaEventDestroy(c->ev_join2);
   }
   if (c->own_stream) cudaStreamDestroy(c->stream);
   delete c;

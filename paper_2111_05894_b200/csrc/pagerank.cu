@@ -53,6 +53,9 @@ constexpr uint32_t kLenA = 4096;
 constexpr uint32_t kLenB = 512;
 constexpr int kPrWin = 256;         // edges staged per warp per window (class B)
 constexpr int kPrWarps = 8;         // warps per CTA (classes B, C)
+#ifndef TG_PR_C_MINB
+#define TG_PR_C_MINB 5              // class C CTAs per SM (caps its registers)
+#endif
 
 // ------------------------------------------------------------ graph upload
 __global__ void narrow_offsets_kernel(const uint64_t* __restrict__ in, uint32_t* __restrict__ out,
@@ -612,18 +615,36 @@ __device__ __forceinline__ void thread_row(const PrStepArgs& a, uint32_t r) {
   const uint32_t* t = a.tgt + beg;
   double acc = 0.0;  // scoring.cpp:67
   uint32_t k = 0;
-  // peel to a 16 B boundary, then two 16 B target loads per 8 edges
+  // peel to a 16 B boundary (its loads independent of each other), then two
+  // 16 B target loads per 8 edges, the next group's targets in flight
   const uint32_t peel = min(len, (4u - (beg & 3u)) & 3u);
-  for (; k < peel; ++k) acc = __dadd_rn(acc, __ldg(a.norm_in + __ldg(t + k)));
-  for (; k + 8 <= len; k += 8) {
-    const uint4 q0 = __ldg(reinterpret_cast<const uint4*>(t + k));
-    const uint4 q1 = __ldg(reinterpret_cast<const uint4*>(t + k + 4));
-    const uint32_t ti[8] = {q0.x, q0.y, q0.z, q0.w, q1.x, q1.y, q1.z, q1.w};
-    double v[8];
+  if (peel) {
+    uint32_t ti[3];
+    double v[3];
 #pragma unroll
-    for (int q = 0; q < 8; ++q) v[q] = __ldg(a.norm_in + ti[q]);
+    for (int q = 0; q < 3; ++q) ti[q] = q < (int)peel ? __ldg(t + q) : 0u;
 #pragma unroll
-    for (int q = 0; q < 8; ++q) acc = __dadd_rn(acc, v[q]);
+    for (int q = 0; q < 3; ++q) v[q] = q < (int)peel ? __ldg(a.norm_in + ti[q]) : 0.0;
+#pragma unroll
+    for (int q = 0; q < 3; ++q)
+      if (q < (int)peel) acc = __dadd_rn(acc, v[q]);
+    k = peel;
+  }
+  if (k + 8 <= len) {
+    uint4 q0 = __ldg(reinterpret_cast<const uint4*>(t + k));
+    uint4 q1 = __ldg(reinterpret_cast<const uint4*>(t + k + 4));
+    for (; k + 8 <= len; k += 8) {
+      const uint32_t ti[8] = {q0.x, q0.y, q0.z, q0.w, q1.x, q1.y, q1.z, q1.w};
+      if (k + 16 <= len) {
+        q0 = __ldg(reinterpret_cast<const uint4*>(t + k + 8));
+        q1 = __ldg(reinterpret_cast<const uint4*>(t + k + 12));
+      }
+      double v[8];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) v[q] = __ldg(a.norm_in + ti[q]);
+#pragma unroll
+      for (int q = 0; q < 8; ++q) acc = __dadd_rn(acc, v[q]);
+    }
   }
   if (k < len) {
     uint32_t ti[8];
@@ -639,16 +660,18 @@ __device__ __forceinline__ void thread_row(const PrStepArgs& a, uint32_t r) {
   finish_row(a, r, acc);
 }
 
-__global__ void __launch_bounds__(kPrWarps * 32) pr_step_kernel(const PrStepArgs a) {
+// Classes B and C are separate kernels so that class C (most rows, short
+// chains, latency-bound gathers) runs at its own, higher occupancy.
+__global__ void __launch_bounds__(kPrWarps * 32) pr_rows_b_kernel(const PrStepArgs a) {
   __shared__ __align__(16) double smem[kPrWarps * 32 / kBLanes * kBWin];  // 16 KB: class B windows
-  if (blockIdx.x < a.b_ctas) {
-    const int g = threadIdx.x / kBLanes;  // row group within the CTA
-    const int64_t i = a.nA + (int64_t)blockIdx.x * (kPrWarps * 32 / kBLanes) + g;
-    group_row(a, i, smem + g * kBWin);
-  } else {
-    const uint64_t i = a.nB + (uint64_t)(blockIdx.x - a.b_ctas) * blockDim.x + threadIdx.x;
-    if (i < a.m) thread_row(a, a.order[i]);
-  }
+  const int g = threadIdx.x / kBLanes;  // row group within the CTA
+  const int64_t i = a.nA + (int64_t)blockIdx.x * (kPrWarps * 32 / kBLanes) + g;
+  group_row(a, i, smem + g * kBWin);
+}
+
+__global__ void __launch_bounds__(kPrWarps * 32, TG_PR_C_MINB) pr_step_kernel(const PrStepArgs a) {
+  const uint64_t i = a.nB + (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < a.m) thread_row(a, a.order[i]);
 }
 
 // The memory-system floor of one K3 step on this graph: the same E gathers
@@ -793,12 +816,17 @@ void pagerank_step(tg_ctx* ctx, const tg_graph* g, const uint32_t* deg, double d
     pr_hub_kernel<<<sc.nA, kHubThreads, kHubTile * 8, ctx->aux>>>(a);
     TGB_LAUNCHED();
   }
-  const unsigned grid = static_cast<unsigned>(a.b_ctas + c_ctas);
-  if (grid) {
-    pr_step_kernel<<<grid, kPrWarps * 32, 0, ctx->stream>>>(a);
+  if (a.b_ctas) {
+    // class B on the second side stream: its chains are long, start them early
+    if (!sc.nA) ctx->fork();
+    pr_rows_b_kernel<<<a.b_ctas, kPrWarps * 32, 0, ctx->aux2>>>(a);
     TGB_LAUNCHED();
   }
-  if (sc.nA) ctx->join();
+  if (c_ctas) {
+    pr_step_kernel<<<static_cast<unsigned>(c_ctas), kPrWarps * 32, 0, ctx->stream>>>(a);
+    TGB_LAUNCHED();
+  }
+  if (sc.nA || a.b_ctas) ctx->join();
 }
 
 void check_config(uint32_t iterations, double damp) {  // scoring.cpp:42-47
