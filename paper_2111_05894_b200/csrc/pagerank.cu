@@ -53,9 +53,6 @@ constexpr uint32_t kLenA = 4096;
 constexpr uint32_t kLenB = 512;
 constexpr int kPrWin = 256;         // edges staged per warp per window (class B)
 constexpr int kPrWarps = 8;         // warps per CTA (classes B, C)
-#ifndef TG_PR_C_MINB
-#define TG_PR_C_MINB 5              // class C CTAs per SM (caps its registers)
-#endif
 
 // ------------------------------------------------------------ graph upload
 __global__ void narrow_offsets_kernel(const uint64_t* __restrict__ in, uint32_t* __restrict__ out,
@@ -660,18 +657,16 @@ __device__ __forceinline__ void thread_row(const PrStepArgs& a, uint32_t r) {
   finish_row(a, r, acc);
 }
 
-// Classes B and C are separate kernels so that class C (most rows, short
-// chains, latency-bound gathers) runs at its own, higher occupancy.
-__global__ void __launch_bounds__(kPrWarps * 32) pr_rows_b_kernel(const PrStepArgs a) {
+__global__ void __launch_bounds__(kPrWarps * 32) pr_step_kernel(const PrStepArgs a) {
   __shared__ __align__(16) double smem[kPrWarps * 32 / kBLanes * kBWin];  // 16 KB: class B windows
-  const int g = threadIdx.x / kBLanes;  // row group within the CTA
-  const int64_t i = a.nA + (int64_t)blockIdx.x * (kPrWarps * 32 / kBLanes) + g;
-  group_row(a, i, smem + g * kBWin);
-}
-
-__global__ void __launch_bounds__(kPrWarps * 32, TG_PR_C_MINB) pr_step_kernel(const PrStepArgs a) {
-  const uint64_t i = a.nB + (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < a.m) thread_row(a, a.order[i]);
+  if (blockIdx.x < a.b_ctas) {
+    const int g = threadIdx.x / kBLanes;  // row group within the CTA
+    const int64_t i = a.nA + (int64_t)blockIdx.x * (kPrWarps * 32 / kBLanes) + g;
+    group_row(a, i, smem + g * kBWin);
+  } else {
+    const uint64_t i = a.nB + (uint64_t)(blockIdx.x - a.b_ctas) * blockDim.x + threadIdx.x;
+    if (i < a.m) thread_row(a, a.order[i]);
+  }
 }
 
 // The memory-system floor of one K3 step on this graph: the same E gathers
@@ -816,17 +811,13 @@ void pagerank_step(tg_ctx* ctx, const tg_graph* g, const uint32_t* deg, double d
     pr_hub_kernel<<<sc.nA, kHubThreads, kHubTile * 8, ctx->aux>>>(a);
     TGB_LAUNCHED();
   }
-  if (a.b_ctas) {
-    // class B on the second side stream: its chains are long, start them early
-    if (!sc.nA) ctx->fork();
-    pr_rows_b_kernel<<<a.b_ctas, kPrWarps * 32, 0, ctx->aux2>>>(a);
+  const unsigned grid = static_cast<unsigned>(a.b_ctas + c_ctas);
+  if (grid) {
+    // classes B (first CTAs: long chains start early) and C in one grid
+    pr_step_kernel<<<grid, kPrWarps * 32, 0, ctx->stream>>>(a);
     TGB_LAUNCHED();
   }
-  if (c_ctas) {
-    pr_step_kernel<<<static_cast<unsigned>(c_ctas), kPrWarps * 32, 0, ctx->stream>>>(a);
-    TGB_LAUNCHED();
-  }
-  if (sc.nA || a.b_ctas) ctx->join();
+  if (sc.nA) ctx->join();
 }
 
 void check_config(uint32_t iterations, double damp) {  // scoring.cpp:42-47

@@ -775,7 +775,12 @@ void launch_gather(tg_store* s, const uint64_t* ids_dev, uint64_t n, void* dst_d
   auto* dst = static_cast<uint8_t*>(dst_dev);
   if ((s->flags & TG_GATHER_BULK) && w == 16 && s->R <= (uint64_t)kBulkStage) {
     const uint32_t Rpad = static_cast<uint32_t>(s->R);
-    const uint32_t B = std::min<uint32_t>(32, kBulkStage / Rpad);
+    // rows per warp batch: as many as a staging buffer holds, but small
+    // enough that a short list still spreads over every SM (each SM's TMA
+    // and address translation serve its own batches)
+    const uint64_t all_warps = static_cast<uint64_t>(ctx->num_sms) * 2 * kBulkWarps;
+    const uint32_t B = static_cast<uint32_t>(std::max<uint64_t>(
+        1, std::min<uint64_t>({32, kBulkStage / Rpad, (n + all_warps - 1) / all_warps})));
     const uint64_t warps = (n + B - 1) / B;
     const unsigned grid = grid_for(warps * 32, kBulkWarps * 32, ctx->num_sms * 2);
     constexpr int kSmem = kBulkWarps * 2 * kBulkStage;
