@@ -50,7 +50,8 @@ struct tg_store {
   const tg_store* cold_owner = nullptr;
   bool placed = false;
   uint64_t* counters = nullptr;                   // device: 3 x u64 + err
-  uint64_t* result_host = nullptr;                // pinned: the counters read back
+  uint64_t* result_host = nullptr;                // mapped pinned: the counters read back
+  uint64_t* result_dev = nullptr;                 // its device address
 };
 
 namespace tgb {
@@ -264,7 +265,37 @@ struct GatherTable {
   const uint32_t* cold_src;
   uint64_t R;
   uint64_t cold_stride;
+  // synchronous C-ABI path: the last CTA to finish copies {counters, err} to
+  // mapped pinned host memory and re-arms them (no memset / D2H copy calls)
+  uint64_t* fin_host;
+  unsigned* fin_done;
 };
+
+__device__ __forceinline__ void gather_finalize(const GatherTable& t, uint64_t* counters,
+                                                unsigned long long* err) {
+  if (!t.fin_host) return;
+  __syncthreads();  // this CTA's counter atomics are issued
+  if (threadIdx.x == 0) {
+    __threadfence();
+    const unsigned ticket = atomicAdd(t.fin_done, 1u);
+    if (ticket == gridDim.x - 1) {
+      __threadfence();
+      volatile uint64_t* c = counters;
+      volatile unsigned long long* e = err;
+      volatile uint64_t* h = t.fin_host;
+      h[0] = c[0];
+      h[1] = c[1];
+      h[2] = c[2];
+      h[3] = e[0];
+      c[0] = 0;
+      c[1] = 0;
+      c[2] = 0;
+      e[0] = ~0ull;
+      *reinterpret_cast<volatile unsigned*>(t.fin_done) = 0u;
+      __threadfence_system();
+    }
+  }
+}
 
 __device__ __forceinline__ const uint8_t* row_ptr(const GatherTable& t, uint64_t id, int* tier) {
   uint32_t owner = 0;
@@ -324,6 +355,7 @@ __global__ void __launch_bounds__(256) gather_kernel(GatherTable t, const uint64
   }
   if (lane != 0) cl = cp = ch = 0;
   block_add_counters(cl, cp, ch, counters);
+  gather_finalize(t, counters, err);
 }
 
 // K8, TMA bulk-copy variant (TG_GATHER_BULK): each warp stages a batch of
@@ -428,6 +460,7 @@ __global__ void __launch_bounds__(kBulkWarps * 32) gather_bulk_kernel(
   asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
   if (lane != 0) cl = cp = ch = 0;
   block_add_counters(cl, cp, ch, counters);
+  gather_finalize(t, counters, err);
 }
 
 // Generic row mover: dst + dst_row(i)*dst_stride <- src + src_row(i)*src_stride
@@ -759,14 +792,18 @@ GatherTable make_table(const tg_store* s) {
 }
 
 void launch_gather(tg_store* s, const uint64_t* ids_dev, uint64_t n, void* dst_dev,
-                   uint64_t* counters3, unsigned long long* err) {
+                   uint64_t* counters3, unsigned long long* err, bool finalize = false) {
   tg_ctx* ctx = s->ctx;
   if (!s->placed) domain_error("tiered store: tg_store_place has not run");
   const uint64_t inter_rows = s->L.multi_boundary - s->L.local_boundary;
   for (uint32_t d = 0; d < s->L.num_devices && inter_rows > d; ++d)
     if (!s->inter[d]) domain_error("tiered store: peer slice of device " + std::to_string(d) +
                                    " is not attached (tg_store_set_peer)");
-  const GatherTable t = make_table(s);
+  GatherTable t = make_table(s);
+  if (finalize) {
+    t.fin_host = s->result_dev;
+    t.fin_done = reinterpret_cast<unsigned*>(s->counters + 4);
+  }
   const uint32_t spread = (s->flags & TG_GATHER_SPREAD) ? 1u : 0u;
   uint64_t align = reinterpret_cast<uint64_t>(dst_dev) | reinterpret_cast<uint64_t>(s->local) |
                    reinterpret_cast<uint64_t>(s->cold_dev) | s->cold_stride;
@@ -1008,6 +1045,14 @@ int tg_store_create(tg_ctx* ctx, const tg_layout* layout, uint32_t device_index,
     try {
       TGB_CUDA(cudaMalloc(&s->local, std::max<uint64_t>(s->local_rows * s->R, 16)));
       TGB_CUDA(cudaMalloc(&s->counters, 64));
+      // [0..2] counters, [3] first bad index (~0 = none), [4] CTA ticket
+      TGB_CUDA(cudaMemsetAsync(s->counters, 0, 64, ctx->stream));
+      TGB_CUDA(cudaMemsetAsync(s->counters + 3, 0xff, 8, ctx->stream));
+      TGB_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&s->result_host), 64, cudaHostAllocMapped));
+      void* rd = nullptr;
+      TGB_CUDA(cudaHostGetDevicePointer(&rd, s->result_host, 0));
+      s->result_dev = static_cast<uint64_t*>(rd);
+      ctx->sync();
       s->inter[device_index] = s->local + lb * s->R;
     } catch (...) {
       tg_store_destroy(s);
@@ -1231,21 +1276,18 @@ int tg_gather_rows(tg_store* s, const uint64_t* ids, uint64_t n, void* dst, tg_r
     const void* mapped = mapped_device_ptr(ids);
     const uint64_t* d = mapped ? static_cast<const uint64_t*>(mapped) : dev_in(ctx, ids, n, kStageIn0);
     DevOut<uint8_t> o(ctx, static_cast<uint8_t*>(dst), n * s->R, kStageOut0);
-    uint64_t* c = s->counters;
+    uint64_t* c = s->counters;  // armed: zero counters, err = ~0 (re-armed by the kernel)
     auto* err = reinterpret_cast<unsigned long long*>(c + 3);
-    TGB_CUDA(cudaMemsetAsync(c, 0, 24, ctx->stream));
-    TGB_CUDA(cudaMemsetAsync(err, 0xff, 8, ctx->stream));
-    launch_gather(s, d, n, o.dev(), c, err);
-    if (!s->result_host)
-      TGB_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&s->result_host), 64, cudaHostAllocDefault));
-    uint64_t* h = s->result_host;
-    TGB_CUDA(cudaMemcpyAsync(h, c, 32, cudaMemcpyDeviceToHost, ctx->stream));
-    o.finish();
+    launch_gather(s, d, n, o.dev(), c, err, /*finalize=*/true);
+    o.finish();  // stream sync: the last CTA's host stores are visible
+    volatile uint64_t* hv = s->result_host;
+    uint64_t h[4] = {hv[0], hv[1], hv[2], hv[3]};
     if (h[3] != ~0ull) {  // reference semantics: prefix accounted, then DomainError
       const uint64_t first = h[3];
       TGB_CUDA(cudaMemsetAsync(c, 0, 24, ctx->stream));
       if (first) account(ctx, s->L, d, first, s->dev, c, err);
       TGB_CUDA(cudaMemcpyAsync(h, c, 24, cudaMemcpyDeviceToHost, ctx->stream));
+      TGB_CUDA(cudaMemsetAsync(c, 0, 24, ctx->stream));  // re-arm for the next call
       ctx->sync();
       add_report(report, h[0], h[1], h[2], s->R);
       uint64_t bad;
