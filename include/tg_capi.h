@@ -271,6 +271,20 @@ int tg_gather_rows_async(tg_store* s, const uint64_t* ids_dev, uint64_t n, void*
 int tg_time_gather_rows(tg_store* s, const uint64_t* const* ids, const uint64_t* counts, uint64_t k,
                         void* dst, int flush_l2, tg_report* report, double* seconds);
 
+/* ----------------------------------------------- containers into the tiers
+ * the reference's binary containers (io.hpp:14-22) read
+ * straight into device memory through pinned double-buffered staging, with
+ * the reference's header errors (io.cpp:65-75, 95-110, 163-180: bad magic /
+ * unsupported version / truncated -> TG_ERR_FORMAT; cannot open -> TG_ERR_IO).
+ * tg_graph_load_csrg replaces load_csr (io.cpp:95-116) + tg_graph_create:
+ * no u64 host copy of the CSR is made. tg_store_place_feat replaces
+ * load_features (io.cpp:163-181) + reorder_features + tg_store_place: the
+ * file's rows go to this device's HBM slots and the store's own pinned cold
+ * tier by the permutation (new_id_of: host or device), without the N x R
+ * matrix in host memory. The store must not be TG_COLD_INDIRECT. */
+int tg_graph_load_csrg(tg_ctx* ctx, const char* path, tg_graph** out);
+int tg_store_place_feat(tg_store* s, const char* path, const uint64_t* new_id_of);
+
 /* ------------------------------------------------------------- peer memory */
 int tg_enable_peer_access(int device, int peer);
 int tg_ipc_get_handle(const void* dev_ptr, void* handle_out /* 64 bytes */);

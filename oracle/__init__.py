@@ -49,6 +49,10 @@ class FormatError(OracleError):
     """Reference FormatError (types.hpp:20-23)."""
 
 
+class IoError(OracleError, OSError):
+    """Reference IoError (types.hpp:13-16)."""
+
+
 def _raise(rc: int, msg: str = ""):
     if rc == 0:
         return
@@ -56,6 +60,8 @@ def _raise(rc: int, msg: str = ""):
         raise DomainError(msg)
     if rc == 3:
         raise FormatError(msg)
+    if rc == 4:
+        raise IoError(msg)
     raise OracleError(f"rc={rc}: {msg}")
 
 
@@ -387,6 +393,11 @@ class RefOracle:
                                               C.POINTER(vp), C.POINTER(U64), C.POINTER(vp)]),
             "tgref_run_training_trace": (I32, [vp, u64p, U64, u32p, U32, U64, U64, U64, I32, u64p]),
             "tgref_mix64": (U64, [U64]),
+            "tgref_save_csr": (I32, [vp, C.c_char_p]),
+            "tgref_load_csr": (I32, [C.c_char_p, C.POINTER(vp)]),
+            "tgref_save_features": (I32, [vp, C.c_char_p]),
+            "tgref_load_features": (I32, [C.c_char_p, C.POINTER(vp)]),
+            "tgref_save_perm": (I32, [u64p, U64, C.c_char_p]),
             "tgref_derive_stream_key": (U64, [U64, u64p, U32]),
         }
         for name, (res, args) in sig.items():
@@ -408,6 +419,38 @@ class RefOracle:
 
     def set_worker_count(self, n):
         self.L.tgref_set_worker_count(int(n))
+
+    # io.cpp containers ----------------------------------------------------
+    def save_csr(self, off, tgt, path):
+        g = self.graph(off, tgt)
+        self._chk(self.L.tgref_save_csr(g.h, str(path).encode()))
+
+    def load_csr(self, path):
+        """(offsets, targets) read by the reference; raises its error."""
+        h = C.c_void_p()
+        self._chk(self.L.tgref_load_csr(str(path).encode(), C.byref(h)))
+        return self._export(_RefGraph(self, h.value).h)
+
+    def save_features(self, data, rows, dim, elem_bytes, path):
+        data = np.ascontiguousarray(data).reshape(-1).view(np.uint8)
+        h = self.L.tgref_features_create(data.ctypes.data, rows, dim, elem_bytes)
+        try:
+            self._chk(self.L.tgref_save_features(h, str(path).encode()))
+        finally:
+            self.L.tgref_features_destroy(h)
+
+    def load_features_error(self, path):
+        """The reference's load_features() outcome: None or (code, message)."""
+        h = C.c_void_p()
+        rc = self.L.tgref_load_features(str(path).encode(), C.byref(h))
+        if rc:
+            return rc, self.L.tgref_last_error().decode()
+        self.L.tgref_features_destroy(h)
+        return None
+
+    def save_perm(self, perm, path):
+        p = _u64(perm)
+        self._chk(self.L.tgref_save_perm(p, len(p), str(path).encode()))
 
     # graph handles -------------------------------------------------------
     def graph(self, off, tgt):

@@ -22,6 +22,7 @@
 
 #include "tiergraph/csr_graph.hpp"
 #include "tiergraph/feature_matrix.hpp"
+#include "tiergraph/io.hpp"
 #include "tiergraph/parallel.hpp"
 #include "tiergraph/reorder.hpp"
 #include "tiergraph/rng.hpp"
@@ -528,6 +529,41 @@ uint64_t tgref_derive_stream_key(uint64_t seed, const uint64_t* coords, uint32_t
       h = tg::derive_stream_key(seed, {coords[0], coords[1], coords[2], coords[3], coords[4]});
   }
   return h;
+}
+
+// io.cpp: the binary containers (golden files for the device loaders)
+int tgref_save_csr(void* h, const char* path) {
+  return guard([&] { tg::save_csr(static_cast<RefGraph*>(h)->g, path); });
+}
+int tgref_load_csr(const char* path, void** out_graph) {
+  return guard([&] {
+    auto* h = new RefGraph;
+    try {
+      h->g = tg::load_csr(path);
+    } catch (...) {
+      delete h;
+      throw;
+    }
+    *out_graph = h;
+  });
+}
+int tgref_save_features(void* h, const char* path) {
+  return guard([&] { tg::save_features(static_cast<RefFeatures*>(h)->f, path); });
+}
+int tgref_load_features(const char* path, void** out) {
+  return guard([&] {
+    auto* h = new RefFeatures;
+    try {
+      h->f = tg::load_features(path);
+    } catch (...) {
+      delete h;
+      throw;
+    }
+    *out = h;
+  });
+}
+int tgref_save_perm(const uint64_t* perm, uint64_t n, const char* path) {
+  return guard([&] { tg::save_u64_vector(std::vector<uint64_t>(perm, perm + n), "PERM", path); });
 }
 
 }  // extern "C"

@@ -25,6 +25,7 @@
 #include <vector>
 
 #include "internal.cuh"
+#include "store_internal.cuh"
 
 struct tg_graph {
   tg_ctx* ctx = nullptr;
@@ -861,6 +862,38 @@ void run_pagerank(tg_ctx* ctx, const tg_graph* g, uint32_t iterations, double da
 
 }  // namespace tgb
 
+namespace tgb {
+void graph_from_device(tg_ctx* ctx, const uint64_t* doff, uint32_t* tgt, uint64_t n, uint64_t e,
+                       tg_graph** out) {
+  auto* g = new tg_graph;
+  g->ctx = ctx;
+  g->n = n;
+  g->e = e;
+  g->tgt = tgt;  // owned from here on
+  try {
+    TGB_CUDA(cudaMalloc(&g->off, sizeof(uint32_t) * (n + 1)));
+    auto* bad = ctx->scratch_t<unsigned long long>(kSmall, 2);
+    TGB_CUDA(cudaMemsetAsync(bad, 0xff, sizeof(unsigned long long), ctx->stream));
+    narrow_offsets_kernel<<<grid_for(n + 1, 256), 256, 0, ctx->stream>>>(doff, g->off, n, e, bad);
+    TGB_LAUNCHED();
+    unsigned long long hb;
+    TGB_CUDA(cudaMemcpyAsync(&hb, bad, sizeof(hb), cudaMemcpyDeviceToHost, ctx->stream));
+    ctx->sync();
+    if (hb != ~0ull)
+      format_error("csr: offsets invalid at index " + std::to_string(hb) +
+                   " (need offsets[0]==0, monotone, offsets[num_nodes]==num_edges)");
+    if (n) schedule(ctx, g, 0, n);  // K3 schedule of the whole graph
+    TGB_CUDA(cudaMalloc(&g->indeg, sizeof(uint32_t) * std::max<uint64_t>(n, 1)));
+    compute_indeg(ctx, g, g->indeg);
+    ctx->sync();
+  } catch (...) {
+    tg_graph_destroy(g);
+    throw;
+  }
+  *out = g;
+}
+}  // namespace tgb
+
 using namespace tgb;
 
 extern "C" {
@@ -872,18 +905,11 @@ int tg_graph_create(tg_ctx* ctx, const uint64_t* offsets, const uint64_t* target
     if (n >= 0xffffffffull || e >= 0xffffffffull)
       domain_error("tg_graph_create: n and e must be < 2^32 for the u32 device layout");
     DeviceGuard dg(ctx->device);
-    auto* g = new tg_graph;
-    g->ctx = ctx;
-    g->n = n;
-    g->e = e;
+    uint32_t* tgt = nullptr;
+    TGB_CUDA(cudaMalloc(&tgt, sizeof(uint32_t) * std::max<uint64_t>(e, 1)));
     try {
-      TGB_CUDA(cudaMalloc(&g->off, sizeof(uint32_t) * (n + 1)));
-      TGB_CUDA(cudaMalloc(&g->tgt, sizeof(uint32_t) * std::max<uint64_t>(e, 1)));
       auto* bad = ctx->scratch_t<unsigned long long>(kSmall, 2);
-      TGB_CUDA(cudaMemsetAsync(bad, 0xff, 2 * sizeof(unsigned long long), ctx->stream));
-      const uint64_t* doff = dev_in(ctx, offsets, n + 1, kStageIn0);
-      narrow_offsets_kernel<<<grid_for(n + 1, 256), 256, 0, ctx->stream>>>(doff, g->off, n, e, bad);
-      TGB_LAUNCHED();
+      TGB_CUDA(cudaMemsetAsync(bad + 1, 0xff, sizeof(unsigned long long), ctx->stream));
       // targets: straight from device memory, or in 32M-entry chunks from the host
       const bool tdev = is_device_ptr(targets);
       const uint64_t chunk = tdev ? std::max<uint64_t>(e, 1) : (32ull << 20);
@@ -896,27 +922,20 @@ int tg_graph_create(tg_ctx* ctx, const uint64_t* offsets, const uint64_t* target
                                    ctx->stream));
           src = st;
         }
-        narrow_targets_kernel<<<grid_for(cnt, 256), 256, 0, ctx->stream>>>(src, g->tgt + base, cnt,
+        narrow_targets_kernel<<<grid_for(cnt, 256), 256, 0, ctx->stream>>>(src, tgt + base, cnt,
                                                                            base, n, bad + 1);
         TGB_LAUNCHED();
       }
-      unsigned long long hb[2];
-      TGB_CUDA(cudaMemcpyAsync(hb, bad, sizeof(hb), cudaMemcpyDeviceToHost, ctx->stream));
+      unsigned long long hb;
+      TGB_CUDA(cudaMemcpyAsync(&hb, bad + 1, sizeof(hb), cudaMemcpyDeviceToHost, ctx->stream));
       ctx->sync();
-      if (hb[0] != ~0ull)
-        format_error("csr: offsets invalid at index " + std::to_string(hb[0]) +
-                     " (need offsets[0]==0, monotone, offsets[num_nodes]==num_edges)");
-      if (hb[1] != ~0ull)
-        format_error("csr: target out of range at edge " + std::to_string(hb[1]));
-      if (n) schedule(ctx, g, 0, n);  // K3 schedule of the whole graph
-      TGB_CUDA(cudaMalloc(&g->indeg, sizeof(uint32_t) * std::max<uint64_t>(n, 1)));
-      compute_indeg(ctx, g, g->indeg);
-      ctx->sync();
+      if (hb != ~0ull) format_error("csr: target out of range at edge " + std::to_string(hb));
     } catch (...) {
-      tg_graph_destroy(g);
+      cudaFree(tgt);
       throw;
     }
-    *out = g;
+    const uint64_t* doff = dev_in(ctx, offsets, n + 1, kStageIn0);
+    graph_from_device(ctx, doff, tgt, n, e, out);
   });
 }
 

@@ -31,28 +31,7 @@
 
 #include "internal.cuh"
 
-struct tg_store {
-  tg_ctx* ctx = nullptr;
-  tg_layout L{};
-  uint32_t dev = 0;
-  uint32_t flags = 0;
-  uint64_t R = 0;
-  uint64_t local_rows = 0;
-  uint8_t* local = nullptr;                       // device
-  const uint8_t* inter[TG_MAX_DEVICES] = {};      // per-device interleaved slice base
-  uint8_t* cold_host = nullptr;                   // host view (owned when own_cold)
-  const uint8_t* cold_dev = nullptr;              // device view of the cold tier
-  uint64_t cold_stride = 0;
-  bool own_cold = false;
-  void* registered = nullptr;                     // caller matrix registered for INDIRECT
-  uint32_t* cold_src = nullptr;                   // INDIRECT: cold slot -> original row
-  bool own_cold_src = false;
-  const tg_store* cold_owner = nullptr;
-  bool placed = false;
-  uint64_t* counters = nullptr;                   // device: 3 x u64 + err
-  uint64_t* result_host = nullptr;                // mapped pinned: the counters read back
-  uint64_t* result_dev = nullptr;                 // its device address
-};
+#include "store_internal.cuh"
 
 namespace tgb {
 
@@ -1130,7 +1109,24 @@ int tg_store_share_cold(tg_store* s, const tg_store* owner) {
   });
 }
 
+}  // extern "C"
+
 namespace tgb {
+const uint8_t* ensure_cold_tier(tg_store* s) {
+  const uint64_t cold = s->L.num_rows - s->L.multi_boundary;
+  s->cold_stride = (s->flags & TG_COLD_PAD128) ? (s->R + 127) / 128 * 128 : s->R;
+  if (!s->own_cold) {
+    TGB_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&s->cold_host),
+                           std::max<uint64_t>(cold * s->cold_stride, 16),
+                           cudaHostAllocMapped | cudaHostAllocPortable));
+    s->own_cold = true;
+  }
+  void* cd = nullptr;
+  TGB_CUDA(cudaHostGetDevicePointer(&cd, s->cold_host, 0));
+  s->cold_dev = static_cast<const uint8_t*>(cd);
+  return s->cold_dev;
+}
+
 // K7 placement from `src_rows` (src_nrows rows of R bytes; host or device)
 // where new id i's bytes are source row order[i] (u32, device, N entries).
 void place_impl(tg_store* s, const void* src_rows, uint64_t src_nrows, const uint32_t* order) {
@@ -1180,16 +1176,8 @@ void place_impl(tg_store* s, const void* src_rows, uint64_t src_nrows, const uin
     reg = nullptr;
   } else {
     const uint64_t cold = N - mb;
-    s->cold_stride = (s->flags & TG_COLD_PAD128) ? (R + 127) / 128 * 128 : R;
-    if (!s->own_cold) {
-      TGB_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&s->cold_host),
-                             std::max<uint64_t>(cold * s->cold_stride, 16),
-                             cudaHostAllocMapped | cudaHostAllocPortable));
-      s->own_cold = true;
-    }
-    void* cd = nullptr;
-    TGB_CUDA(cudaHostGetDevicePointer(&cd, s->cold_host, 0));
-    s->cold_dev = static_cast<const uint8_t*>(cd);
+    ensure_cold_tier(s);
+    void* cd = const_cast<uint8_t*>(s->cold_dev);
     MoveArgs c{};
     c.src = src;
     c.dst = static_cast<uint8_t*>(cd);
@@ -1211,6 +1199,8 @@ __global__ void check_rows_kernel(const uint32_t* __restrict__ m, uint64_t n, ui
     if (m[i] >= nrows) atomicMin(bad, (unsigned long long)i);
 }
 }  // namespace tgb
+
+extern "C" {
 
 int tg_store_place(tg_store* s, const void* features, const uint64_t* new_id_of) {
   return guard([&] {

@@ -159,6 +159,44 @@ def default_context() -> Context:
 
 
 # ------------------------------------------------------------ data types
+class DeviceCsrGraph:
+    """A CsrGraph that exists only on the device (tg_graph_load_csrg): the
+    same calls accept it wherever they take a CsrGraph bound to `ctx`."""
+
+    def __init__(self, ctx: "Context", h):
+        self._ctx, self._h = ctx, h
+
+    def num_nodes(self) -> int:
+        return int(LIB.tg_graph_num_nodes(self._h))
+
+    def num_edges(self) -> int:
+        return int(LIB.tg_graph_num_edges(self._h))
+
+    def device(self, ctx: "Context"):
+        if ctx is not self._ctx:
+            raise DomainError("this graph lives on another context")
+        return self._h
+
+    def release(self):
+        if self._h:
+            LIB.tg_graph_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.release()
+        except Exception:
+            pass
+
+
+def load_csr_device(path, *, ctx: "Context" = None) -> DeviceCsrGraph:
+    """io.hpp:26 load_csr, straight into the device layout (CSRG v1)."""
+    c = _ctx(ctx)
+    h = C.c_void_p()
+    _check(LIB.tg_graph_load_csrg(c.h, str(path).encode(), C.byref(h)))
+    return DeviceCsrGraph(c, h)
+
+
 class CsrGraph:
     """csr_graph.hpp:22-35. Row u = targets[offsets[u]:offsets[u+1]] (out-neighbors).
 
@@ -637,6 +675,15 @@ class TieredFeatureStore:
             raise DomainError(f"permutation length {_len(p)} != num_rows {self.layout.num_rows}")
         self._keep = [data]  # TG_COLD_INDIRECT maps the caller's matrix: keep it alive
         _check(LIB.tg_store_place(self.h, _ptr(data), _nonempty(p, np.uint64)))
+
+    def place_file(self, path, perm):
+        """K7 straight from a FEAT v1 file (io.hpp:35): rows to this device's
+        HBM slots and the pinned cold tier, no N x R host copy."""
+        p = _perm(perm)
+        if _len(p) != self.layout.num_rows:
+            raise DomainError(f"permutation length {_len(p)} != num_rows {self.layout.num_rows}")
+        self._keep = [p]
+        _check(LIB.tg_store_place_feat(self.h, str(path).encode(), _nonempty(p, np.uint64)))
 
     def place_rows(self, rows, row_of):
         """K7 from a caller's row array: new id i holds rows[row_of[i]]
