@@ -373,7 +373,13 @@ def run_ours(args):
     # ---- reordered graph -> the reference's minibatch schedule (host producer)
     t0 = time.time()
     rg = tg.reorder_graph(g, perm, ctx=ctx)
-    gt = producers.transpose(rg)
+    gt = tg.transpose(rg, ctx=ctx)  # on the device (csr_graph.cpp:67-80)
+    transpose_ok = None
+    if world == 1 and not args.no_cpu_baseline and cfg.get("cpu_gather", True):
+        import oracle  # checker only: the reference's transpose of the same graph
+        chk = oracle.ref() or oracle.port()
+        t_off, t_tgt = chk.transpose(rg.offsets, rg.targets)
+        transpose_ok = bool(np.array_equal(t_off, gt.offsets) and np.array_equal(t_tgt, gt.targets))
     del rg
     new_tid = np.sort(perm.new_id_of[tid.ids])
     # the epoch's minibatch id lists, sampled on the GPU (csrc/sampling.cu,
@@ -682,6 +688,8 @@ def run_ours(args):
             result["cpu_baseline"], result["parity"] = cpu_baseline(
                 cfg, off, tgt, tid, scores, perm, feat, R, lay, mine, store, out_d, torch,
                 gt=gt, new_tid=new_tid, gpu_lists=lists)
+            if transpose_ok is not None:
+                result["parity"]["transpose_identical"] = transpose_ok
     if dist:
         dist.barrier()
         dist.destroy_process_group()

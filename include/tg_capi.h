@@ -271,6 +271,13 @@ int tg_gather_rows_async(tg_store* s, const uint64_t* ids_dev, uint64_t n, void*
 int tg_time_gather_rows(tg_store* s, const uint64_t* const* ids, const uint64_t* counts, uint64_t k,
                         void* dst, int flush_l2, tg_report* report, double* seconds);
 
+/* csr_graph.hpp:48 transpose (csr_graph.cpp:67-80) on the device: a stable
+ * radix sort of the edges by target in CSR order, so every transposed row
+ * lists its sources ascending, bit-identical to the reference. Inputs and
+ * outputs host or device; n, e < 2^32. */
+int tg_transpose(tg_ctx* ctx, const uint64_t* offsets, const uint64_t* targets, uint64_t n,
+                 uint64_t e, uint64_t* out_offsets, uint64_t* out_targets);
+
 /* ----------------------------------------------- containers into the tiers
  * the reference's binary containers (io.hpp:14-22) read
  * straight into device memory through pinned double-buffered staging, with

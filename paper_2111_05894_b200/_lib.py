@@ -113,6 +113,7 @@ SIGNATURES = {
     "tg_time_gather_rows": (I32, [vp, vp, vp, U64, vp, C.c_int, vp, C.POINTER(C.c_double)]),
     "tg_graph_load_csrg": (I32, [vp, C.c_char_p, C.POINTER(vp)]),
     "tg_store_place_feat": (I32, [vp, C.c_char_p, vp]),
+    "tg_transpose": (I32, [vp, vp, vp, U64, U64, vp, vp]),
     "tg_device_alloc": (I32, [vp, U64, C.POINTER(vp)]),
     "tg_device_free": (I32, [vp, vp]),
     "tg_host_register": (I32, [vp, U64]),

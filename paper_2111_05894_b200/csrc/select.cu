@@ -358,11 +358,143 @@ void sort_scores(tg_ctx* ctx, const double* scores_dev, uint64_t n, uint64_t* or
     domain_error("score " + std::to_string(hb) + " is not finite and >= 0");  // scoring.cpp:107
 }
 
+// ------------------------------------------------------------- transpose
+// csr_graph.cpp:67-80: row v of the transpose lists the sources u of the
+// edges (u, v), ascending ("walking sources in ascending order leaves every
+// transposed row sorted"). On the device: a STABLE radix sort of the edges by
+// target, presented in CSR (= ascending source) order, carrying the source
+// as the value; the transposed offsets are the key boundaries.
+__global__ void __launch_bounds__(256) edge_keys_kernel(const uint64_t* __restrict__ off,
+                                                        const uint64_t* __restrict__ tgt,
+                                                        uint64_t n, uint64_t* __restrict__ keys,
+                                                        uint32_t* __restrict__ vals,
+                                                        uint32_t* __restrict__ hist) {
+  __shared__ uint32_t h[4][256];
+  for (int i = threadIdx.x; i < 4 * 256; i += blockDim.x) (&h[0][0])[i] = 0;
+  __syncthreads();
+  // one warp per source row: coalesced over the row's edges
+  const int lane = threadIdx.x & 31;
+  const uint64_t warp = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
+  const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+  for (uint64_t u = warp; u < n; u += nw) {
+    for (uint64_t i = off[u] + lane; i < off[u + 1]; i += 32) {
+      const uint64_t k = tgt[i];
+      keys[i] = k;
+      vals[i] = static_cast<uint32_t>(u);
+#pragma unroll
+      for (int p = 0; p < 4; ++p) atomicAdd(&h[p][(k >> (8 * p)) & 0xff], 1u);
+    }
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < 4 * 256; i += blockDim.x) {
+    const uint32_t c = (&h[0][0])[i];
+    if (c) atomicAdd(hist + i, c);
+  }
+}
+
+__global__ void key_range_check_kernel(const uint64_t* __restrict__ tgt, uint64_t e, uint64_t n,
+                                       uint32_t* __restrict__ hist, unsigned long long* bad) {
+  // targets < n < 2^32, so digits 4..7 are 0: one full bin each; range check
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < e;
+       i += (uint64_t)gridDim.x * blockDim.x)
+    if (tgt[i] >= n) atomicMin(bad, (unsigned long long)i);
+  if (blockIdx.x == 0)
+    for (int p = 4 + threadIdx.x; p < 8; p += blockDim.x) hist[p * 256] = static_cast<uint32_t>(e);
+}
+
+// t_off[v] = first sorted position with key >= v; t_tgt[i] = source (u64)
+__global__ void transpose_out_kernel(const uint64_t* __restrict__ k0, const uint64_t* __restrict__ k1,
+                                     const uint32_t* __restrict__ v0, const uint32_t* __restrict__ v1,
+                                     const RadixPlan* __restrict__ plan, uint64_t n, uint64_t e,
+                                     uint64_t* __restrict__ t_off, uint64_t* __restrict__ t_tgt) {
+  const uint64_t* k = plan->final_src ? k1 : k0;
+  const uint32_t* v = plan->final_src ? v1 : v0;
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i <= e;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t hi = i < e ? k[i] : n;          // rows (prev, hi] start at i
+    const uint64_t lo = i ? k[i - 1] + 1 : 0;
+    for (uint64_t r = lo; r <= hi && r <= n; ++r) t_off[r] = i;
+    if (i < e) t_tgt[i] = v[i];
+  }
+}
+
+void transpose_device(tg_ctx* ctx, const uint64_t* off, const uint64_t* tgt, uint64_t n, uint64_t e,
+                      uint64_t* t_off, uint64_t* t_tgt) {
+  if (n >= 0xffffffffull || e >= 0xffffffffull)
+    domain_error("transpose: n and e must be < 2^32 on the device");
+  if (e == 0) {
+    TGB_CUDA(cudaMemsetAsync(t_off, 0, 8 * (n + 1), ctx->stream));
+    return;
+  }
+  const uint32_t nblk = static_cast<uint32_t>((e + kRsTile - 1) / kRsTile);
+  const size_t bytes = 2 * 8 * e + 2 * 4 * e + 4ull * 256 * nblk + 64 + sizeof(RadixPlan) +
+                       8 * 256 * 4 + 256 * 4 + 256;
+  char* base = nullptr;
+  TGB_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&base), bytes, ctx->stream));
+  auto align = [](char* p) { return reinterpret_cast<char*>((reinterpret_cast<uintptr_t>(p) + 15) & ~uintptr_t(15)); };
+  char* p = base;
+  uint64_t* k0 = reinterpret_cast<uint64_t*>(p); p = align(p + 8 * e);
+  uint64_t* k1 = reinterpret_cast<uint64_t*>(p); p = align(p + 8 * e);
+  uint32_t* v0 = reinterpret_cast<uint32_t*>(p); p = align(p + 4 * e);
+  uint32_t* v1 = reinterpret_cast<uint32_t*>(p); p = align(p + 4 * e);
+  uint32_t* counts = reinterpret_cast<uint32_t*>(p); p = align(p + 4ull * 256 * nblk);
+  auto* bad = reinterpret_cast<unsigned long long*>(p); p = align(p + 64);
+  auto* plan = reinterpret_cast<RadixPlan*>(p); p = align(p + sizeof(RadixPlan));
+  uint32_t* hist = reinterpret_cast<uint32_t*>(p); p = align(p + 8 * 256 * 4);
+  uint32_t* totals = reinterpret_cast<uint32_t*>(p);
+  TGB_CUDA(cudaMemsetAsync(hist, 0, 8 * 256 * 4, ctx->stream));
+  TGB_CUDA(cudaMemsetAsync(bad, 0xff, 8, ctx->stream));
+  key_range_check_kernel<<<grid_for(e, 256, ctx->num_sms * 8), 256, 0, ctx->stream>>>(tgt, e, n,
+                                                                                      hist, bad);
+  TGB_LAUNCHED();
+  unsigned long long hb;
+  TGB_CUDA(cudaMemcpyAsync(&hb, bad, 8, cudaMemcpyDeviceToHost, ctx->stream));
+  ctx->sync();
+  if (hb != ~0ull) {
+    cudaFreeAsync(base, ctx->stream);
+    format_error("csr: target out of range at edge " + std::to_string(hb));
+  }
+  edge_keys_kernel<<<grid_for(n * 32, 256, ctx->num_sms * 16), 256, 0, ctx->stream>>>(off, tgt, n, k0,
+                                                                                     v0, hist);
+  TGB_LAUNCHED();
+  plan_kernel<<<1, 32, 0, ctx->stream>>>(hist, e, plan);
+  TGB_LAUNCHED();
+  for (int pass = 0; pass < 4; ++pass) {  // digits 4..7 are constant: planned as skipped
+    digit_count_kernel<<<nblk, kRsWarps * 32, 0, ctx->stream>>>(k0, k1, e, pass, plan, counts, nblk);
+    TGB_LAUNCHED();
+    count_scan_kernel<<<256, 1024, 0, ctx->stream>>>(counts, nblk, pass, plan, totals);
+    TGB_LAUNCHED();
+    scatter_kernel<<<nblk, kRsWarps * 32, 0, ctx->stream>>>(k0, v0, k1, v1, e, pass, plan, counts,
+                                                             nblk, totals);
+    TGB_LAUNCHED();
+  }
+  transpose_out_kernel<<<grid_for(e + 1, 256, ctx->num_sms * 16), 256, 0, ctx->stream>>>(
+      k0, k1, v0, v1, plan, n, e, t_off, t_tgt);
+  TGB_LAUNCHED();
+  TGB_CUDA(cudaFreeAsync(base, ctx->stream));
+}
+
 }  // namespace tgb
 
 using namespace tgb;
 
 extern "C" {
+
+int tg_transpose(tg_ctx* ctx, const uint64_t* offsets, const uint64_t* targets, uint64_t n,
+                 uint64_t e, uint64_t* out_offsets, uint64_t* out_targets) {
+  return guard([&] {  // csr_graph.cpp:67-80
+    DeviceGuard dg(ctx->device);
+    const uint64_t* off = dev_in(ctx, offsets, n + 1, kStageIn0);
+    const uint64_t* tgt = dev_in(ctx, targets, e, kStageIn1);
+    DevOut<uint64_t> oo(ctx, out_offsets, n + 1, kStageOut0);
+    DevOut<uint64_t> ot(ctx, out_targets, e, kStageOut1);
+    transpose_device(ctx, off, tgt, n, e, oo.dev(), ot.dev());
+    if (oo.host)
+      TGB_CUDA(cudaMemcpyAsync(out_offsets, oo.dev(), 8 * (n + 1), cudaMemcpyDeviceToHost,
+                               ctx->stream));
+    ot.finish();
+  });
+}
 
 int tg_score_ordering(tg_ctx* ctx, const double* scores, uint64_t n, uint64_t* out_order) {
   return guard([&] {

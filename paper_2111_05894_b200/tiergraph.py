@@ -528,6 +528,17 @@ def reorder_graph(g: CsrGraph, perm, *, ctx: Context = None) -> CsrGraph:
     return CsrGraph(oo, ot[:e])
 
 
+def transpose(g: CsrGraph, *, ctx: Context = None) -> CsrGraph:
+    """csr_graph.hpp:48 (csr_graph.cpp:67-80), on the device."""
+    c = _ctx(ctx)
+    n, e = g.num_nodes(), g.num_edges()
+    oo = np.empty(n + 1, np.uint64)
+    ot = np.empty(max(e, 1), np.uint64)
+    _check(LIB.tg_transpose(c.h, _ptr(g.offsets), _nonempty(g.targets, np.uint64), n, e, _ptr(oo),
+                            _ptr(ot)))
+    return CsrGraph(oo, ot[:e])
+
+
 def reorder_features(f: FeatureMatrix, perm, *, ctx: Context = None) -> FeatureMatrix:
     """reorder.hpp:40 (reorder.cpp:97-117): new row perm[u] = old row u."""
     c = _ctx(ctx)
