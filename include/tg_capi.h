@@ -380,6 +380,16 @@ int tg_sample_minibatch_raw(tg_sampler* s, const uint64_t* seeds, uint64_t ns,
  * shuffle, then every batch expanded; counts (n x u64, host|device) get one
  * per unique member per batch (dedup_per_batch) or one per raw access. The
  * sampler's graph is the TRANSPOSED graph; tid is a TrainIdSet (sorted). */
+/* Many minibatches of one epoch in one call, no host round trip between
+ * them: batch b (first_batch <= b < first_batch + nbatches) expands seeds
+ * order[b*B, (b+1)*B) with BatchRng{rng_seed, epoch, b} (sampling.cpp:35-37,
+ * 106-115). Members of batch k go to out_members[out_offsets[k],
+ * out_offsets[k+1]) (sorted unique); out_offsets has nbatches + 1 entries.
+ * Outputs host or device; cap = out_members entries. */
+int tg_sample_batches(tg_sampler* s, const uint64_t* order, uint64_t n_order, uint64_t batch_size,
+                      uint64_t first_batch, uint64_t nbatches, const uint32_t* fanouts,
+                      uint32_t nf, uint64_t rng_seed, uint64_t epoch, uint64_t* out_members,
+                      uint64_t cap, uint64_t* out_offsets);
 int tg_sampler_trace(tg_sampler* s, const uint64_t* tid, uint64_t ntid, const uint32_t* fanouts,
                      uint32_t nf, uint64_t batch_size, uint64_t epochs, uint64_t rng_seed,
                      int dedup_per_batch, uint64_t* counts);

@@ -114,6 +114,7 @@ SIGNATURES = {
     "tg_graph_load_csrg": (I32, [vp, C.c_char_p, C.POINTER(vp)]),
     "tg_store_place_feat": (I32, [vp, C.c_char_p, vp]),
     "tg_transpose": (I32, [vp, vp, vp, U64, U64, vp, vp]),
+    "tg_sample_batches": (I32, [vp, vp, U64, U64, U64, U64, vp, U32, U64, U64, vp, U64, vp]),
     "tg_device_alloc": (I32, [vp, U64, C.POINTER(vp)]),
     "tg_device_free": (I32, [vp, vp]),
     "tg_host_register": (I32, [vp, U64]),

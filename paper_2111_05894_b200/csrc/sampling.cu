@@ -59,14 +59,13 @@ struct SampleArgs {
   const uint32_t* off;  // transposed graph (row v = in-neighbours of v)
   const uint32_t* tgt;
   const uint32_t* frontier;
-  uint32_t f;
+  const uint32_t* f_dev;  // frontier size, written by the previous launch (no host round trip)
   uint32_t fanout;
   uint64_t key_base;  // mix64(seed ^ IV) folded with {0x534D, epoch, batch, layer}
   uint32_t* picks;    // f x fanout scratch for Floyd's membership test
   uint32_t* layer_mark;
   uint32_t layer_stamp;
-  uint32_t* member_mark;
-  uint32_t member_stamp;
+  uint32_t* member_bits;  // one bit per node: a member of this minibatch
   uint32_t* next;
   uint32_t* next_count;
   // optional outputs (run_training_trace, raw_draws; sampling.cpp:56-140)
@@ -85,44 +84,145 @@ __device__ __forceinline__ void admit(const SampleArgs& a, uint32_t u) {
   if (a.counts && a.count_raw) atomicAdd(a.counts + u, 1ull);
   // a plain L2 read first: hot nodes are drawn by many threads per layer,
   // and only the first needs the atomic (a stale read just costs one)
-  if (__ldcg(a.layer_mark + u) != a.layer_stamp &&
-      atomicExch(a.layer_mark + u, a.layer_stamp) != a.layer_stamp) {
-    a.next[atomicAdd(a.next_count, 1u)] = u;
-    if (a.counts && !a.count_raw) {
-      if (atomicExch(a.member_mark + u, a.member_stamp) != a.member_stamp)
-        atomicAdd(a.counts + u, 1ull);
-    } else {
-      a.member_mark[u] = a.member_stamp;
+  // the lanes calling here together (all of them reach the ballot below)
+  const unsigned act = __activemask();
+  bool fresh = false;
+  if (__ldcg(a.layer_mark + u) != a.layer_stamp)
+    fresh = atomicExch(a.layer_mark + u, a.layer_stamp) != a.layer_stamp;
+  // append to the next frontier with one atomic per warp: every new node of
+  // the layer hits the same counter
+  const unsigned m = __ballot_sync(act, fresh);
+  if (!m) return;
+  const int lane = threadIdx.x & 31, leader = __ffs(m) - 1;
+  uint32_t base = 0;
+  if (lane == leader) base = atomicAdd(a.next_count, static_cast<uint32_t>(__popc(m)));
+  base = __shfl_sync(act, base, leader);
+  if (fresh) {
+    a.next[base + __popc(m & ((1u << lane) - 1u))] = u;
+    const uint32_t bit = 1u << (u & 31);
+    if ((__ldcg(a.member_bits + (u >> 5)) & bit) == 0 &&
+        (atomicOr(a.member_bits + (u >> 5), bit) & bit) == 0 && a.counts && !a.count_raw)
+      atomicAdd(a.counts + u, 1ull);
+  }
+}
+
+// admit() for up to K draws of one thread at once, phase by phase so the
+// memory operations of different draws are in flight together: mark reads,
+// then the claiming exchanges, then one warp-aggregated append for all of
+// them, then the member bits. Draw order within the thread is preserved in
+// the raw list and the per-node counts are order-independent.
+template <int K>
+__device__ __forceinline__ void admit_batch(const SampleArgs& a, const uint32_t (&u)[K],
+                                            uint32_t nvalid) {
+  if (a.raw || a.counts) {
+#pragma unroll
+    for (int q = 0; q < K; ++q) {
+      if ((uint32_t)q >= nvalid) continue;
+      if (a.raw) {
+        const unsigned long long k = atomicAdd(a.raw_n, 1ull);
+        if (k < a.raw_cap) a.raw[k] = u[q];
+      }
+      if (a.counts && a.count_raw) atomicAdd(a.counts + u[q], 1ull);
     }
+  }
+  uint32_t seen[K];
+#pragma unroll
+  for (int q = 0; q < K; ++q) seen[q] = (uint32_t)q < nvalid ? __ldcg(a.layer_mark + u[q]) : a.layer_stamp;
+  uint32_t fresh = 0;  // bit q: draw q claimed its node for the next frontier
+#pragma unroll
+  for (int q = 0; q < K; ++q)
+    if (seen[q] != a.layer_stamp && atomicExch(a.layer_mark + u[q], a.layer_stamp) != a.layer_stamp)
+      fresh |= 1u << q;
+  // one append for the whole warp: exclusive scan of the lanes' fresh counts
+  const unsigned act = __activemask();
+  const int lane = threadIdx.x & 31;
+  const uint32_t mine = __popc(fresh);  // <= K <= 16: five bits
+  const uint32_t total = __reduce_add_sync(act, mine);
+  if (!total) return;
+  // exclusive prefix over the active lanes below this one, bit by bit
+  const uint32_t below = act & ((1u << lane) - 1u);
+  uint32_t excl = 0;
+#pragma unroll
+  for (int k = 0; k < 5; ++k)
+    excl += static_cast<uint32_t>(__popc(__ballot_sync(act, (mine >> k) & 1u) & below)) << k;
+  const int top = 31 - __clz(act);
+  uint32_t base = 0;
+  if (lane == top) base = atomicAdd(a.next_count, total);
+  base = __shfl_sync(act, base, top);
+  uint32_t pos = base + excl;
+#pragma unroll
+  for (int q = 0; q < K; ++q)
+    if (fresh & (1u << q)) a.next[pos++] = u[q];
+#pragma unroll
+  for (int q = 0; q < K; ++q) {
+    if (!(fresh & (1u << q))) continue;
+    const uint32_t bit = 1u << (u[q] & 31);
+    if ((atomicOr(a.member_bits + (u[q] >> 5), bit) & bit) == 0 && a.counts && !a.count_raw)
+      atomicAdd(a.counts + u[q], 1ull);
   }
 }
 
 // sampling.cpp:39-54 + rng.cpp:8-40 for one frontier node per thread.
+// Fanouts up to kRegK keep Floyd's picks in registers and split each node's
+// work into: all draws (ALU only), then all neighbour loads (independent, in
+// flight together), then the admits -- one memory round trip per phase
+// instead of one per draw.
+constexpr uint32_t kRegK = 16;
 __global__ void __launch_bounds__(256) sample_layer_kernel(const SampleArgs a) {
-  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= a.f) return;
-  const uint32_t v = a.frontier[i];
-  const uint32_t b = a.off[v], deg = a.off[v + 1] - b;
-  if (deg <= a.fanout) {  // all in-neighbours
-    for (uint32_t p = 0; p < deg; ++p) admit(a, a.tgt[b + p]);
-    return;
-  }
-  DevRng rng{dmix64(a.key_base ^ dmix64(v))};  // derive_stream_key(..., node)
-  uint32_t* picks = a.picks + static_cast<uint64_t>(i) * a.fanout;
-  uint32_t cnt = 0;
-  for (uint64_t j = deg - a.fanout; j < deg; ++j) {
-    const uint32_t t = static_cast<uint32_t>(rng.below(j + 1));
-    bool seen = false;
-    for (uint32_t q = 0; q < cnt; ++q) seen |= picks[q] == t;
-    const uint32_t p = seen ? static_cast<uint32_t>(j) : t;
-    picks[cnt++] = p;
-    admit(a, a.tgt[b + p]);
+  const uint32_t f = *a.f_dev;  // written by the previous launch: no host round trip
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < f; i += gridDim.x * blockDim.x) {
+    const uint32_t v = a.frontier[i];
+    const uint32_t b = a.off[v], deg = a.off[v + 1] - b;
+    if (deg <= a.fanout) {  // all in-neighbours
+      uint32_t p = 0;
+      for (; p + kRegK <= deg; p += kRegK) {
+        uint32_t u[kRegK];
+#pragma unroll
+        for (uint32_t q = 0; q < kRegK; ++q) u[q] = a.tgt[b + p + q];
+        admit_batch<kRegK>(a, u, kRegK);
+      }
+      uint32_t u[kRegK];
+#pragma unroll
+      for (uint32_t q = 0; q < kRegK; ++q) u[q] = p + q < deg ? a.tgt[b + p + q] : 0u;
+      admit_batch<kRegK>(a, u, deg - p);
+      continue;
+    }
+    DevRng rng{dmix64(a.key_base ^ dmix64(v))};  // derive_stream_key(..., node)
+    if (a.fanout <= kRegK) {
+      uint32_t pk[kRegK];
+#pragma unroll
+      for (uint32_t jj = 0; jj < kRegK; ++jj) {
+        if (jj < a.fanout) {
+          const uint64_t j = deg - a.fanout + jj;
+          const uint32_t t = static_cast<uint32_t>(rng.below(j + 1));
+          bool seen = false;
+#pragma unroll
+          for (uint32_t q = 0; q < kRegK; ++q) seen |= q < jj && pk[q] == t;
+          pk[jj] = seen ? static_cast<uint32_t>(j) : t;
+        }
+      }
+      uint32_t u[kRegK];
+#pragma unroll
+      for (uint32_t q = 0; q < kRegK; ++q) u[q] = q < a.fanout ? a.tgt[b + pk[q]] : 0u;
+      admit_batch<kRegK>(a, u, a.fanout);  // draw order, as the reference emits them
+      continue;
+    }
+    uint32_t* picks = a.picks + static_cast<uint64_t>(i) * a.fanout;
+    uint32_t cnt = 0;
+    for (uint64_t j = deg - a.fanout; j < deg; ++j) {
+      const uint32_t t = static_cast<uint32_t>(rng.below(j + 1));
+      bool seen = false;
+      for (uint32_t q = 0; q < cnt; ++q) seen |= picks[q] == t;
+      const uint32_t p = seen ? static_cast<uint32_t>(j) : t;
+      picks[cnt++] = p;
+      admit(a, a.tgt[b + p]);
+    }
   }
 }
 
 __global__ void seed_kernel(const uint64_t* __restrict__ seeds, uint64_t ns, uint64_t n,
-                            uint32_t* layer_mark, uint32_t stamp, uint32_t* member_mark,
-                            uint32_t mstamp, uint32_t* frontier, uint32_t* count,
+                            uint32_t* layer_mark, uint32_t stamp, uint32_t* member_bits,
+                            uint32_t* frontier, uint32_t* count,
                             unsigned long long* bad, unsigned long long* counts, int count_raw,
                             uint64_t* raw, unsigned long long* raw_n, uint64_t raw_cap) {
   for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < ns;
@@ -140,20 +240,42 @@ __global__ void seed_kernel(const uint64_t* __restrict__ seeds, uint64_t ns, uin
     if (counts && count_raw) atomicAdd(counts + u, 1ull);
     if (atomicExch(layer_mark + u, stamp) != stamp) {
       frontier[atomicAdd(count, 1u)] = u;
-      member_mark[u] = mstamp;
+      atomicOr(member_bits + (u >> 5), 1u << (u & 31));  // the bitmap is clear per minibatch
       if (counts && !count_raw) atomicAdd(counts + u, 1ull);
     }
   }
 }
 
-// members = stamped nodes in id order: per-block counts, then positions.
+// members = set bits in node-id order: per-block popcounts (1024 words =
+// 32,768 nodes per block), then positions. Reads N/8 bytes per minibatch.
 constexpr int kCompactBlock = 1024;
-__global__ void __launch_bounds__(kCompactBlock) member_count_kernel(const uint32_t* __restrict__ mark,
-                                                                     uint64_t n, uint32_t stamp,
+__device__ __forceinline__ uint32_t block_excl_sum(uint32_t v, uint32_t* total) {
+  __shared__ uint32_t ws[kCompactBlock / 32];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  uint32_t x = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) ws[w] = x;
+  __syncthreads();
+  uint32_t before = 0, tot = 0;
+  for (int k = 0; k < kCompactBlock / 32; ++k) {
+    if (k < w) before += ws[k];
+    tot += ws[k];
+  }
+  *total = tot;
+  return before + x - v;
+}
+
+__global__ void __launch_bounds__(kCompactBlock) member_count_kernel(const uint32_t* __restrict__ bits,
+                                                                     uint64_t nwords,
                                                                      uint32_t* __restrict__ counts) {
   const uint64_t i = blockIdx.x * (uint64_t)kCompactBlock + threadIdx.x;
-  const int c = __syncthreads_count(i < n && mark[i] == stamp);
-  if (threadIdx.x == 0) counts[blockIdx.x] = c;
+  uint32_t tot;
+  block_excl_sum(i < nwords ? __popc(bits[i]) : 0u, &tot);
+  if (threadIdx.x == 0) counts[blockIdx.x] = tot;
 }
 
 __global__ void __launch_bounds__(1024) count_prefix_kernel(uint32_t* __restrict__ counts,
@@ -180,20 +302,27 @@ __global__ void __launch_bounds__(1024) count_prefix_kernel(uint32_t* __restrict
   if (threadIdx.x == 1023) *total = part[1023];
 }
 
-__global__ void __launch_bounds__(kCompactBlock) member_write_kernel(const uint32_t* __restrict__ mark,
-                                                                     uint64_t n, uint32_t stamp,
+__global__ void __launch_bounds__(kCompactBlock) member_write_kernel(const uint32_t* __restrict__ bits,
+                                                                     uint64_t nwords,
                                                                      const uint32_t* __restrict__ base,
-                                                                     uint64_t* __restrict__ out) {
-  __shared__ uint32_t wsum[kCompactBlock / 32];
+                                                                     uint64_t* __restrict__ out,
+                                                                     const uint64_t* out_base,
+                                                                     uint64_t cap) {
   const uint64_t i = blockIdx.x * (uint64_t)kCompactBlock + threadIdx.x;
-  const bool on = i < n && mark[i] == stamp;
-  const unsigned bal = __ballot_sync(0xffffffffu, on);
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  if (lane == 0) wsum[w] = __popc(bal);
-  __syncthreads();
-  uint32_t before = 0;
-  for (int k = 0; k < w; ++k) before += wsum[k];
-  if (on) out[base[blockIdx.x] + before + __popc(bal & ((1u << lane) - 1u))] = i;
+  uint32_t word = i < nwords ? bits[i] : 0u, tot;
+  uint64_t pos = (out_base ? *out_base : 0) + base[blockIdx.x] + block_excl_sum(__popc(word), &tot);
+  while (word) {
+    const int b = __ffs(word) - 1;
+    if (pos < cap) out[pos] = i * 32 + b;
+    ++pos;
+    word &= word - 1;
+  }
+}
+
+// after minibatch k: offsets[k + 1] = offsets[k] + its member total
+__global__ void advance_offset_kernel(const uint32_t* __restrict__ total, uint64_t* offsets,
+                                      uint64_t k) {
+  if (threadIdx.x == 0 && blockIdx.x == 0) offsets[k + 1] = offsets[k] + *total;
 }
 
 uint64_t host_mix64(uint64_t x) {
@@ -213,7 +342,8 @@ struct tg_sampler {
   const uint32_t* tgt = nullptr;
   uint64_t n = 0;
   uint32_t* layer_mark = nullptr;   // n
-  uint32_t* member_mark = nullptr;  // n
+  uint32_t* member_bits = nullptr;  // ceil(n / 32)
+  uint64_t nwords = 0;
   uint32_t* buf[2] = {nullptr, nullptr};
   uint64_t buf_cap = 0;
   uint32_t* picks = nullptr;
@@ -237,7 +367,6 @@ void ensure(uint32_t** p, uint64_t* cap, uint64_t want) {
 uint32_t next_stamp(tg_sampler* s) {
   if (s->stamp >= 0xFFFFFFF0u) {  // wrap: forget every old stamp
     TGB_CUDA(cudaMemsetAsync(s->layer_mark, 0, 4 * s->n, s->ctx->stream));
-    TGB_CUDA(cudaMemsetAsync(s->member_mark, 0, 4 * s->n, s->ctx->stream));
     s->stamp = 0;
   }
   return ++s->stamp;
@@ -258,11 +387,12 @@ int tg_sampler_create(tg_ctx* ctx, const tg_graph* gt, tg_sampler** out) {
     s->tgt = tg_graph_targets32(gt);
     try {
       TGB_CUDA(cudaMalloc(&s->layer_mark, 4 * std::max<uint64_t>(s->n, 1)));
-      TGB_CUDA(cudaMalloc(&s->member_mark, 4 * std::max<uint64_t>(s->n, 1)));
+      s->nwords = std::max<uint64_t>((s->n + 31) / 32, 1);
+      TGB_CUDA(cudaMalloc(&s->member_bits, 4 * s->nwords));
       TGB_CUDA(cudaMemsetAsync(s->layer_mark, 0, 4 * std::max<uint64_t>(s->n, 1), ctx->stream));
-      TGB_CUDA(cudaMemsetAsync(s->member_mark, 0, 4 * std::max<uint64_t>(s->n, 1), ctx->stream));
-      TGB_CUDA(cudaMalloc(&s->small, 64));
-      const uint64_t nblk = (s->n + kCompactBlock - 1) / kCompactBlock;
+      TGB_CUDA(cudaMemsetAsync(s->member_bits, 0, 4 * s->nwords, ctx->stream));
+      TGB_CUDA(cudaMalloc(&s->small, 256));
+      const uint64_t nblk = (s->nwords + kCompactBlock - 1) / kCompactBlock;
       TGB_CUDA(cudaMalloc(&s->blk, 4 * std::max<uint64_t>(nblk, 1)));
     } catch (...) {
       tg_sampler_destroy(s);
@@ -277,7 +407,7 @@ int tg_sampler_destroy(tg_sampler* s) {
   DeviceGuard dg(s->ctx->device);
   cudaStreamSynchronize(s->ctx->stream);
   cudaFree(s->layer_mark);
-  cudaFree(s->member_mark);
+  cudaFree(s->member_bits);
   cudaFree(s->buf[0]);
   cudaFree(s->buf[1]);
   cudaFree(s->picks);
@@ -306,9 +436,16 @@ void check_fanouts(const uint32_t* fanouts, uint32_t nf) {  // sampling.cpp:18-2
     if (fanouts[l] < 1) domain_error("every fanout must be >= 1");
 }
 
-// build_minibatch (sampling.cpp:56-90) on the device; returns the member stamp.
-// The raw-draw count (when requested) is left in s->small[6..7].
-uint32_t expand(tg_sampler* s, const uint64_t* sd, uint64_t ns, const uint32_t* fanouts, uint32_t nf,
+// Small device counters: [0] seed frontier size, [1 + l] layer l's new
+// frontier size, [8] member total; u64 [5] first bad seed index, u64 [6] raw
+// draws (as u32 indices 10..13).
+constexpr int kSmallBad = 10, kSmallRaw = 12, kSmallTotal = 8;
+
+// build_minibatch (sampling.cpp:56-90) on the device, stream-ordered with no
+// host round trip: every layer's grid covers an upper bound of its frontier
+// and the kernel reads the actual size from the device. Returns an upper
+// bound of the member count.
+uint64_t expand(tg_sampler* s, const uint64_t* sd, uint64_t ns, const uint32_t* fanouts, uint32_t nf,
                 uint64_t rng_seed, uint64_t epoch, uint64_t batch, const ExpandOut& o) {
   if (ns == 0) domain_error("build_minibatch: seeds must be non-empty");
   tg_ctx* ctx = s->ctx;
@@ -318,30 +455,21 @@ uint32_t expand(tg_sampler* s, const uint64_t* sd, uint64_t ns, const uint32_t* 
   uint64_t cap1 = s->buf_cap;
   ensure(&s->buf[1], &cap1, n + 1);
   s->buf_cap = std::min(cap0, cap1);
-  uint32_t* cnt = s->small;  // [0] frontier count, [1] member total, [4..5] bad, [6..7] raw n
-  auto* bad = reinterpret_cast<unsigned long long*>(s->small + 4);
-  auto* raw_n = reinterpret_cast<unsigned long long*>(s->small + 6);
-  TGB_CUDA(cudaMemsetAsync(cnt, 0, 8, ctx->stream));
+  uint32_t* cnt = s->small;
+  auto* bad = reinterpret_cast<unsigned long long*>(s->small + kSmallBad);
+  auto* raw_n = reinterpret_cast<unsigned long long*>(s->small + kSmallRaw);
+  TGB_CUDA(cudaMemsetAsync(cnt, 0, 4 * 10, ctx->stream));
   TGB_CUDA(cudaMemsetAsync(bad, 0xff, 8, ctx->stream));
   TGB_CUDA(cudaMemsetAsync(raw_n, 0, 8, ctx->stream));
-  const uint32_t mstamp = next_stamp(s);
+  TGB_CUDA(cudaMemsetAsync(s->member_bits, 0, 4 * s->nwords, ctx->stream));
   uint32_t lstamp = next_stamp(s);
   seed_kernel<<<grid_for(ns, 256), 256, 0, ctx->stream>>>(sd, ns, n, s->layer_mark, lstamp,
-                                                         s->member_mark, mstamp, s->buf[0], cnt,
-                                                         bad, o.counts, o.count_raw, o.raw, raw_n,
+                                                         s->member_bits, s->buf[0], cnt, bad,
+                                                         o.counts, o.count_raw, o.raw, raw_n,
                                                          o.raw_cap);
   TGB_LAUNCHED();
-  uint32_t hc[6];
-  TGB_CUDA(cudaMemcpyAsync(hc, s->small, 24, cudaMemcpyDeviceToHost, ctx->stream));
-  ctx->sync();
-  unsigned long long hb;
-  std::memcpy(&hb, hc + 4, 8);
-  if (hb != ~0ull) {
-    uint64_t v = 0;
-    TGB_CUDA(cudaMemcpy(&v, sd + hb, 8, cudaMemcpyDeviceToHost));
-    domain_error("seed " + std::to_string(v) + " out of range");  // sampling.cpp:61-62
-  }
-  uint32_t f = hc[0];
+  uint64_t f = std::min<uint64_t>(ns, n);  // frontier bound
+  uint64_t members = f;
   const uint64_t key0 = host_mix64(rng_seed ^ 0x6A09E667F3BCC908ull);  // rng.hpp:23-28
   int cur = 0;
   for (uint32_t layer = 0; layer < nf && f > 0; ++layer) {
@@ -349,41 +477,66 @@ uint32_t expand(tg_sampler* s, const uint64_t* sd, uint64_t ns, const uint32_t* 
     uint64_t key = key0;
     const uint64_t coords[4] = {0x534Dull, epoch, batch, layer};  // sampling.cpp:35-37
     for (uint64_t c : coords) key = host_mix64(key ^ host_mix64(c));
-    ensure(&s->picks, &s->picks_cap, static_cast<uint64_t>(f) * k);
+    if (f * k > (1ull << 28)) {
+      // a huge bound (wide fanouts on a big graph): size the picks by the
+      // actual frontier instead (one host round trip)
+      uint32_t hf = 0;
+      TGB_CUDA(cudaMemcpyAsync(&hf, cnt + layer, 4, cudaMemcpyDeviceToHost, ctx->stream));
+      ctx->sync();
+      f = hf;
+    }
+    ensure(&s->picks, &s->picks_cap, std::max<uint64_t>(f * k, 1));
     lstamp = next_stamp(s);
-    TGB_CUDA(cudaMemsetAsync(cnt, 0, 4, ctx->stream));
-    SampleArgs a{s->off, s->tgt, s->buf[cur], f, k, key, s->picks, s->layer_mark, lstamp,
-                 s->member_mark, mstamp, s->buf[cur ^ 1], cnt, o.counts, o.count_raw, o.raw,
+    SampleArgs a{s->off, s->tgt, s->buf[cur], cnt + layer, k, key, s->picks, s->layer_mark, lstamp,
+                 s->member_bits, s->buf[cur ^ 1], cnt + layer + 1, o.counts, o.count_raw, o.raw,
                  raw_n, o.raw_cap};
-    sample_layer_kernel<<<(f + 255) / 256, 256, 0, ctx->stream>>>(a);
+    sample_layer_kernel<<<grid_for(f, 256, ctx->num_sms * 16), 256, 0, ctx->stream>>>(a);
     TGB_LAUNCHED();
-    TGB_CUDA(cudaMemcpyAsync(&f, cnt, 4, cudaMemcpyDeviceToHost, ctx->stream));
-    ctx->sync();
+    f = std::min<uint64_t>(n, f * k);
+    members += f;
     cur ^= 1;
   }
-  return mstamp;
+  return std::min<uint64_t>(members, n);
 }
 
-uint64_t compact_members(tg_sampler* s, uint32_t mstamp, uint64_t* out, uint64_t cap) {
+// The stamped members in id order into out_dev (device, >= bound entries);
+// the total is left in s->small[kSmallTotal]. No host round trip.
+void compact_members(tg_sampler* s, uint64_t* out_dev, const uint64_t* out_base = nullptr,
+                     uint64_t cap = ~0ull) {
   tg_ctx* ctx = s->ctx;
-  const uint64_t n = s->n;
-  uint32_t* cnt = s->small;
-  const uint64_t nblk = (n + kCompactBlock - 1) / kCompactBlock;
-  member_count_kernel<<<nblk, kCompactBlock, 0, ctx->stream>>>(s->member_mark, n, mstamp, s->blk);
+  const uint64_t nblk = (s->nwords + kCompactBlock - 1) / kCompactBlock;
+  member_count_kernel<<<nblk, kCompactBlock, 0, ctx->stream>>>(s->member_bits, s->nwords, s->blk);
   TGB_LAUNCHED();
-  count_prefix_kernel<<<1, 1024, 0, ctx->stream>>>(s->blk, static_cast<uint32_t>(nblk), cnt + 1);
+  count_prefix_kernel<<<1, 1024, 0, ctx->stream>>>(s->blk, static_cast<uint32_t>(nblk),
+                                                   s->small + kSmallTotal);
   TGB_LAUNCHED();
-  uint32_t total = 0;
-  TGB_CUDA(cudaMemcpyAsync(&total, cnt + 1, 4, cudaMemcpyDeviceToHost, ctx->stream));
-  ctx->sync();
-  if (total <= cap) {
-    DevOut<uint64_t> o(ctx, out, total, kStageOut0);
-    member_write_kernel<<<nblk, kCompactBlock, 0, ctx->stream>>>(s->member_mark, n, mstamp, s->blk,
-                                                                 o.dev());
-    TGB_LAUNCHED();
-    o.finish();
+  member_write_kernel<<<nblk, kCompactBlock, 0, ctx->stream>>>(s->member_bits, s->nwords, s->blk,
+                                                               out_dev, out_base, cap);
+  TGB_LAUNCHED();
+}
+
+struct SmallOut {
+  uint32_t total;
+  unsigned long long bad, raw_n;
+};
+
+SmallOut read_small(tg_sampler* s) {
+  uint32_t h[16];
+  TGB_CUDA(cudaMemcpyAsync(h, s->small, sizeof(h), cudaMemcpyDeviceToHost, s->ctx->stream));
+  s->ctx->sync();
+  SmallOut r;
+  r.total = h[kSmallTotal];
+  std::memcpy(&r.bad, h + kSmallBad, 8);
+  std::memcpy(&r.raw_n, h + kSmallRaw, 8);
+  return r;
+}
+
+void check_seeds(tg_sampler* s, const uint64_t* sd, const SmallOut& r) {
+  if (r.bad != ~0ull) {
+    uint64_t v = 0;
+    TGB_CUDA(cudaMemcpy(&v, sd + r.bad, 8, cudaMemcpyDeviceToHost));
+    domain_error("seed " + std::to_string(v) + " out of range");  // sampling.cpp:61-62
   }
-  return total;
 }
 
 }  // namespace
@@ -396,14 +549,22 @@ int tg_sample_minibatch(tg_sampler* s, const uint64_t* seeds, uint64_t ns, const
   return guard([&] {
     check_fanouts(fanouts, nf);
     if (ns == 0) domain_error("build_minibatch: seeds must be non-empty");
-    DeviceGuard dg(s->ctx->device);
-    const uint64_t* sd = dev_in(s->ctx, seeds, ns, kStageIn0);
-    const uint32_t mstamp = expand(s, sd, ns, fanouts, nf, rng_seed, epoch, batch, ExpandOut{});
-    const uint64_t total = compact_members(s, mstamp, out, cap);
-    *out_n = total;
-    if (total > cap)
-      domain_error("tg_sample_minibatch: " + std::to_string(total) +
+    tg_ctx* ctx = s->ctx;
+    DeviceGuard dg(ctx->device);
+    const uint64_t* sd = dev_in(ctx, seeds, ns, kStageIn0);
+    const uint64_t bound = expand(s, sd, ns, fanouts, nf, rng_seed, epoch, batch, ExpandOut{});
+    uint64_t* md = ctx->scratch_t<uint64_t>(kStageOut1, std::max<uint64_t>(bound, 1));
+    compact_members(s, md);
+    const SmallOut r = read_small(s);  // the one host round trip
+    check_seeds(s, sd, r);
+    *out_n = r.total;
+    if (r.total > cap)
+      domain_error("tg_sample_minibatch: " + std::to_string(r.total) +
                    " members exceed the output capacity " + std::to_string(cap));
+    if (r.total) {
+      TGB_CUDA(cudaMemcpyAsync(out, md, 8ull * r.total, cudaMemcpyDefault, ctx->stream));
+      ctx->sync();
+    }
   });
 }
 
@@ -417,27 +578,65 @@ int tg_sample_minibatch_raw(tg_sampler* s, const uint64_t* seeds, uint64_t ns,
     tg_ctx* ctx = s->ctx;
     DeviceGuard dg(ctx->device);
     const uint64_t* sd = dev_in(ctx, seeds, ns, kStageIn0);
-    uint64_t* rd = ctx->scratch_t<uint64_t>(kStageOut1, std::max<uint64_t>(raw_cap, 1));
+    uint64_t* rd = ctx->scratch_t<uint64_t>(kStageOut0, std::max<uint64_t>(raw_cap, 1));
     ExpandOut o;
     o.raw = rd;
     o.raw_cap = raw_cap;
-    const uint32_t mstamp = expand(s, sd, ns, fanouts, nf, rng_seed, epoch, batch, o);
-    unsigned long long rn = 0;
-    TGB_CUDA(cudaMemcpyAsync(&rn, s->small + 6, 8, cudaMemcpyDeviceToHost, ctx->stream));
-    ctx->sync();
-    *raw_n = rn;
-    const uint64_t total = compact_members(s, mstamp, out, cap);
-    *out_n = total;
-    if (total > cap || rn > raw_cap)
+    const uint64_t bound = expand(s, sd, ns, fanouts, nf, rng_seed, epoch, batch, o);
+    uint64_t* md = ctx->scratch_t<uint64_t>(kStageOut1, std::max<uint64_t>(bound, 1));
+    compact_members(s, md);
+    const SmallOut r = read_small(s);
+    check_seeds(s, sd, r);
+    *raw_n = r.raw_n;
+    *out_n = r.total;
+    if (r.total > cap || r.raw_n > raw_cap)
       domain_error("tg_sample_minibatch_raw: output capacity exceeded");
-    if (rn) {
-      if (is_device_ptr(raw)) {
-        TGB_CUDA(cudaMemcpyAsync(raw, rd, 8 * rn, cudaMemcpyDeviceToDevice, ctx->stream));
-      } else {
-        TGB_CUDA(cudaMemcpyAsync(raw, rd, 8 * rn, cudaMemcpyDeviceToHost, ctx->stream));
-      }
-      ctx->sync();
+    if (r.total) TGB_CUDA(cudaMemcpyAsync(out, md, 8ull * r.total, cudaMemcpyDefault, ctx->stream));
+    if (r.raw_n) TGB_CUDA(cudaMemcpyAsync(raw, rd, 8ull * r.raw_n, cudaMemcpyDefault, ctx->stream));
+    ctx->sync();
+  });
+}
+
+int tg_sample_batches(tg_sampler* s, const uint64_t* order, uint64_t n_order, uint64_t batch_size,
+                      uint64_t first_batch, uint64_t nbatches, const uint32_t* fanouts,
+                      uint32_t nf, uint64_t rng_seed, uint64_t epoch, uint64_t* out_members,
+                      uint64_t cap, uint64_t* out_offsets) {
+  return guard([&] {
+    // run_training_trace's batching (sampling.cpp:106-115): batch b's seeds are
+    // order[b*B, (b+1)*B), expanded by build_minibatch with BatchRng{seed, epoch, b}
+    check_fanouts(fanouts, nf);
+    if (batch_size < 1) domain_error("batch_size must be >= 1");
+    const uint64_t nb_all = (n_order + batch_size - 1) / batch_size;
+    if (first_batch + nbatches > nb_all)
+      domain_error("batches [" + std::to_string(first_batch) + ", " +
+                   std::to_string(first_batch + nbatches) + ") exceed the " +
+                   std::to_string(nb_all) + " batches of the order");
+    tg_ctx* ctx = s->ctx;
+    DeviceGuard dg(ctx->device);
+    const uint64_t* od = dev_in(ctx, order, n_order, kStageIn1);
+    DevOut<uint64_t> offs(ctx, out_offsets, nbatches + 1, kStageOut0);
+    TGB_CUDA(cudaMemsetAsync(offs.dev(), 0, 8, ctx->stream));
+    uint64_t* md = out_members;
+    const bool host_out = !is_device_ptr(out_members);
+    if (host_out) md = ctx->scratch_t<uint64_t>(kScratchA, std::max<uint64_t>(cap, 1));
+    for (uint64_t k = 0; k < nbatches; ++k) {
+      const uint64_t b = first_batch + k;
+      const uint64_t beg = b * batch_size, len = std::min(batch_size, n_order - beg);
+      expand(s, od + beg, len, fanouts, nf, rng_seed, epoch, b, ExpandOut{});
+      compact_members(s, md, offs.dev() + k, cap);
+      advance_offset_kernel<<<1, 32, 0, ctx->stream>>>(s->small + kSmallTotal, offs.dev(), k);
+      TGB_LAUNCHED();
     }
+    uint64_t total = 0;
+    TGB_CUDA(cudaMemcpyAsync(&total, offs.dev() + nbatches, 8, cudaMemcpyDeviceToHost, ctx->stream));
+    const SmallOut r = read_small(s);  // syncs
+    if (r.bad != ~0ull) domain_error("seed out of range in the batch order");
+    if (total > cap)
+      domain_error("tg_sample_batches: " + std::to_string(total) +
+                   " members exceed the output capacity " + std::to_string(cap));
+    if (host_out && total)
+      TGB_CUDA(cudaMemcpyAsync(out_members, md, 8 * total, cudaMemcpyDeviceToHost, ctx->stream));
+    offs.finish();
   });
 }
 

@@ -99,6 +99,17 @@ class GpuSampler:
         h = C.c_void_p()
         tg._check(LIB.tg_sampler_create(self.ctx.h, gt.device(self.ctx), C.byref(h)))
         self.h = h
+        self._pinned = None  # reusable pinned output (members of one minibatch)
+
+    def _out_buffer(self, ns: int, fanouts) -> np.ndarray:
+        bound, layer = ns, ns
+        for f in fanouts:
+            layer = min(self.n, layer * int(f))
+            bound += layer
+        bound = max(1, min(bound, self.n))
+        if self._pinned is None or len(self._pinned) < bound:
+            self._pinned = self.tg.host_alloc(8 * bound).view(np.uint64)
+        return self._pinned
 
     def minibatch(self, seeds, fanouts: Sequence[int], seed: int, epoch: int, batch: int,
                   out=None):
@@ -108,12 +119,59 @@ class GpuSampler:
         sd = tg._u64(seeds)
         fo = np.ascontiguousarray(np.asarray(list(fanouts), np.uint32))
         cnt = C.c_uint64()
-        dst = out if out is not None else np.empty(max(self.n, 1), np.uint64)
+        dst = out if out is not None else self._out_buffer(len(sd), fanouts)
         tg._check(LIB.tg_sample_minibatch(self.h, tg._nonempty(sd, np.uint64), tg._len(sd),
                                           fo.ctypes.data if len(fo) else None, len(fo),
                                           int(seed), int(epoch), int(batch), tg._ptr(dst),
                                           tg._len(dst), C.byref(cnt)))
         return int(cnt.value) if out is not None else dst[:cnt.value].copy()
+
+    def batches(self, order, fanouts: Sequence[int], batch_size: int, seed: int, epoch: int,
+                first_batch: int = 0, nbatches: int = None, device: bool = False):
+        """Member lists of batches [first_batch, first_batch + nbatches) of an
+        epoch whose shuffled train ids are `order` (epoch_order), expanded on
+        the device back to back with one host round trip in total. With
+        device=True returns (the concatenated member lists as a CUDA int64
+        tensor, the u64 offsets) without copying them to the host; the tensor
+        is reused by the next call."""
+        tg = self.tg
+        od = tg._u64(order)
+        nb_all = (len(od) + batch_size - 1) // batch_size
+        if nbatches is None:
+            nbatches = nb_all - first_batch
+        fo = np.ascontiguousarray(np.asarray(list(fanouts), np.uint32))
+        per, layer = batch_size, batch_size
+        for f in fanouts:
+            layer = min(self.n, layer * int(f))
+            per += layer
+        cap = max(1, nbatches * min(per, self.n))
+        md = self._device_buffer(cap)
+        offs = np.empty(nbatches + 1, np.uint64)
+        tg._check(LIB.tg_sample_batches(self.h, tg._nonempty(od, np.uint64), len(od), batch_size,
+                                        first_batch, nbatches,
+                                        fo.ctypes.data if len(fo) else None, len(fo), int(seed),
+                                        int(epoch), md.data_ptr(), cap, offs.ctypes.data))
+        if device:
+            return md, offs
+        total = int(offs[-1])
+        host = self._host_buffer(total)
+        host_t = self._torch.from_numpy(host[:total].view(np.int64))
+        host_t.copy_(md[:total])  # pinned: one DMA
+        allm = host[:total].copy()
+        return [allm[int(offs[k]):int(offs[k + 1])] for k in range(nbatches)]
+
+    def _device_buffer(self, cap: int):
+        import torch
+        self._torch = torch
+        if getattr(self, "_dbuf", None) is None or self._dbuf.numel() < cap:
+            self._dbuf = torch.empty(cap, dtype=torch.int64,
+                                     device=torch.device("cuda", self.ctx.device))
+        return self._dbuf
+
+    def _host_buffer(self, n: int) -> np.ndarray:
+        if getattr(self, "_hbuf", None) is None or len(self._hbuf) < n:
+            self._hbuf = self.tg.host_alloc(8 * max(n, 1)).view(np.uint64)
+        return self._hbuf
 
     def minibatch_raw(self, seeds, fanouts: Sequence[int], seed: int, epoch: int, batch: int):
         """(members, raw draws) — build_minibatch with raw_draws (sampling.hpp:48-55);

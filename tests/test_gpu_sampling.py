@@ -117,3 +117,24 @@ def test_raw_draws_multiset(tg, ctx):
         assert np.array_equal(mem, np.unique(raw))
         np.add.at(counts, raw.astype(np.int64), np.uint64(1))
     assert np.array_equal(counts, want)
+
+
+@pytest.mark.parametrize("fanouts", [[10, 15], [15, 10, 5], [100, 3]])
+def test_sample_batches_back_to_back(tg, ctx, fanouts):
+    """tg_sample_batches (one host round trip for many minibatches) gives the
+    reference's epoch lists, from any first batch, incl. a short last batch."""
+    from paper_2111_05894_b200 import producers
+    chk = checker()
+    n = 6000
+    off, tgt = _graph(n, 7, hubs=[(0, 3000), (9, 400)])
+    go, gt = chk.transpose(off, tgt)
+    tid = oracle.port().draw_random_train_ids(n, 1000, 5)  # 16 batches of 64, the last 40
+    want = chk.epoch_minibatches(go, gt, tid, fanouts, 64, 11, 2, max_batches=16)
+    order = producers.epoch_order(tid, 11, 2)
+    s = producers.GpuSampler(tg.CsrGraph(go, gt), ctx=ctx)
+    got = s.batches(order, fanouts, 64, 11, 2)
+    assert len(got) == 16 and all(np.array_equal(a, b) for a, b in zip(got, want))
+    mid = s.batches(order, fanouts, 64, 11, 2, first_batch=5, nbatches=4)
+    assert all(np.array_equal(a, b) for a, b in zip(mid, want[5:9]))
+    with pytest.raises(tg.DomainError, match="exceed"):
+        s.batches(order, fanouts, 64, 11, 2, first_batch=15, nbatches=2)
