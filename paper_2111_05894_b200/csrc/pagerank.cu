@@ -40,6 +40,7 @@ struct tg_graph {
     uint64_t rb, re;
     uint32_t* order;
     uint32_t nA, nB;  // order[0,nA): len > kLenA; [nA,nB): kLenB < len <= kLenA
+    uint32_t nLong;   // order[0,nLong): len > kHubLong (512-thread class-A CTAs)
   };
   std::vector<Sched> scheds;
 };
@@ -52,6 +53,10 @@ namespace tgb {
 //   C  len <= kLenB         one thread per row (a warp's rows have near-equal lengths)
 constexpr uint32_t kLenA = 4096;
 constexpr uint32_t kLenB = 512;
+// class-A CTAs: 256 threads x 8 addends (2,048 per tile); 512 x 8 for rows
+// longer than kHubLong (half the tiles on the critical path; 1024 x 4 was
+// measured no faster for the 77k-edge C2 row: 158 vs 151 us)
+constexpr uint32_t kHubLong = 16384;
 constexpr int kPrWin = 256;         // edges staged per warp per window (class B)
 constexpr int kPrWarps = 8;         // warps per CTA (classes B, C)
 
@@ -86,8 +91,8 @@ __global__ void class_bounds_kernel(const uint32_t* __restrict__ off,
                                     const uint32_t* __restrict__ order, uint64_t m,
                                     uint32_t* __restrict__ out) {
   if (threadIdx.x != 0 || blockIdx.x != 0) return;
-  const uint32_t lim[2] = {kLenA, kLenB};
-  for (int c = 0; c < 2; ++c) {  // first index whose length is <= lim[c]
+  const uint32_t lim[3] = {kLenA, kLenB, kHubLong};
+  for (int c = 0; c < 3; ++c) {  // first index whose length is <= lim[c]
     uint64_t lo = 0, hi = m;
     while (lo < hi) {
       const uint64_t mid = (lo + hi) / 2;
@@ -273,10 +278,6 @@ __device__ __forceinline__ double chain_add(double acc, const double* v, uint32_
 // __dadd_rn; the pass then restarts from the next addend in the new binade.
 // acc crosses a binade only O(log(sum / first)) times per row, mostly in its
 // first elements, so a 2048-element tile takes one or two passes.
-constexpr int kHubT = 8;                          // addends per thread per tile
-constexpr int kHubWarps = 8;                      // 256-thread CTA per hub row
-constexpr int kHubThreads = kHubWarps * 32;
-constexpr int kHubTile = kHubThreads * kHubT;     // 4096 addends, 32 KB of smem
 constexpr long long kTop = 1ll << 53;
 constexpr int kHubSerial = 256;                   // serial prefix at a row start
 
@@ -353,20 +354,26 @@ __device__ __forceinline__ long long sat_add(long long a, long long b) {
   return min(a + b, kTop);  // a, b <= 2^53: no overflow
 }
 
+template <int W>
 struct HubShared {
-  QPair wagg[kHubWarps];  // per-warp totals, then their exclusive prefixes
-  long long wsum[kHubWarps];  // tie-free path: the same for plain increments
+  QPair wagg[W];  // per-warp totals, then their exclusive prefixes
+  long long wsum[W];  // tie-free path: the same for plain increments
   long long wsum_tot;
   QPair wtot;             // block total
-  int wfirst[kHubWarps];  // per-warp first crossing
+  int wfirst[W];  // per-warp first crossing
   double acc;
 };
 
 // Class A: one CTA per row longer than kLenA.
-__global__ void __launch_bounds__(kHubThreads) pr_hub_kernel(const PrStepArgs a) {
+template <int W, int T>
+__global__ void __launch_bounds__(W * 32) pr_hub_kernel(const PrStepArgs a, uint32_t row0) {
+  constexpr int kHubWarps = W;
+  constexpr int kHubThreads = W * 32;
+  constexpr int kHubT = T;
+  constexpr int kHubTile = kHubThreads * kHubT;
   extern __shared__ __align__(16) double xs[];  // [kHubTile]
-  __shared__ HubShared sh;
-  const uint32_t r = a.order[blockIdx.x];  // class A
+  __shared__ HubShared<W> sh;
+  const uint32_t r = a.order[row0 + blockIdx.x];  // class A
   const uint32_t beg = a.off[r], len = a.off[r + 1] - beg;
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   double acc = 0.0;  // scoring.cpp:67 — identical in every thread
@@ -755,17 +762,18 @@ const tg_graph::Sched& schedule(tg_ctx* ctx, const tg_graph* g, uint64_t rb, uin
   auto& v = const_cast<tg_graph*>(g)->scheds;
   for (const auto& sc : v)
     if (sc.rb == rb && sc.re == re) return sc;
-  tg_graph::Sched sc{rb, re, nullptr, 0, 0};
-  TGB_CUDA(cudaMalloc(&sc.order, sizeof(uint32_t) * std::max<uint64_t>(re - rb, 1) + 8));
+  tg_graph::Sched sc{rb, re, nullptr, 0, 0, 0};
+  TGB_CUDA(cudaMalloc(&sc.order, sizeof(uint32_t) * std::max<uint64_t>(re - rb, 1) + 16));
   sort_rows_by_length(ctx, g->off, rb, re, sc.order);
   uint32_t* bounds = sc.order + std::max<uint64_t>(re - rb, 1);
   class_bounds_kernel<<<1, 32, 0, ctx->stream>>>(g->off, sc.order, re - rb, bounds);
   TGB_LAUNCHED();
-  uint32_t hb[2];
+  uint32_t hb[3];
   TGB_CUDA(cudaMemcpyAsync(hb, bounds, sizeof(hb), cudaMemcpyDeviceToHost, ctx->stream));
   ctx->sync();  // once per (graph, range)
   sc.nA = hb[0];
   sc.nB = hb[1];
+  sc.nLong = hb[2];
   v.push_back(sc);
   return v.back();
 }
@@ -801,16 +809,26 @@ void pagerank_step(tg_ctx* ctx, const tg_graph* g, const uint32_t* deg, double d
   }
   const uint64_t c_ctas = (a.m - sc.nB + kPrWarps * 32 - 1) / (kPrWarps * 32);
   if (sc.nA) {
-    // class A on the side stream, concurrently with classes B and C
+    // class A on the side streams, concurrently with classes B and C: the
+    // longest rows (> kHubLong) with 512-thread CTAs, the rest with 256
     static bool attr[TG_MAX_DEVICES] = {};  // a function attribute is per device
     if (!attr[ctx->device % TG_MAX_DEVICES]) {
-      TGB_CUDA(cudaFuncSetAttribute(pr_hub_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    kHubTile * 8));
+      TGB_CUDA(cudaFuncSetAttribute(pr_hub_kernel<16, 8>,
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize, 16 * 32 * 8 * 8));
+      TGB_CUDA(cudaFuncSetAttribute(pr_hub_kernel<8, 8>,
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize, 8 * 32 * 8 * 8));
       attr[ctx->device % TG_MAX_DEVICES] = true;
     }
     ctx->fork();
-    pr_hub_kernel<<<sc.nA, kHubThreads, kHubTile * 8, ctx->aux>>>(a);
-    TGB_LAUNCHED();
+    const uint32_t nl = sc.nLong;
+    if (nl) {
+      pr_hub_kernel<16, 8><<<nl, 16 * 32, 16 * 32 * 8 * 8, ctx->aux>>>(a, 0);
+      TGB_LAUNCHED();
+    }
+    if (sc.nA > nl) {
+      pr_hub_kernel<8, 8><<<sc.nA - nl, 8 * 32, 8 * 32 * 8 * 8, ctx->aux2>>>(a, nl);
+      TGB_LAUNCHED();
+    }
   }
   const unsigned grid = static_cast<unsigned>(a.b_ctas + c_ctas);
   if (grid) {

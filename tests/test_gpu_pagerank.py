@@ -111,7 +111,8 @@ def _hub_graph(n, hubs, seed):
 def test_long_rows_and_heavy_groups(tg, ctx):
     chk = checker()
     n = 60000
-    hubs = [(0, 40000), (1, 257), (31, 2049), (32, 5000), (95, 33), (1000, 20000), (59999, 3000)]
+    hubs = [(0, 40000), (1, 257), (31, 2049), (32, 5000), (95, 33), (1000, 20000), (59999, 3000),
+            (2, 45000), (3, 58000)]
     off, tgt = _hub_graph(n, hubs, 3)
     g = G(tg, off, tgt)
     tid = oracle.port().draw_random_train_ids(n, 600, 5)
