@@ -53,9 +53,10 @@ namespace tgb {
 //   C  len <= kLenB         one thread per row (a warp's rows have near-equal lengths)
 constexpr uint32_t kLenA = 4096;
 constexpr uint32_t kLenB = 512;
-// class-A CTAs: 256 threads x 8 addends (2,048 per tile); 512 x 8 for rows
-// longer than kHubLong (half the tiles on the critical path; 1024 x 4 was
-// measured no faster for the 77k-edge C2 row: 158 vs 151 us)
+// class-A CTAs: 256 threads x 8 addends (2,048 per tile); 512 x 8 for the
+// rows longer than kHubLong and a quarter of the longest row (half the tiles
+// on the critical path; 1024 x 4 was measured no faster for the 77k-edge C2
+// row: 158 vs 151 us)
 constexpr uint32_t kHubLong = 16384;
 constexpr int kPrWin = 256;         // edges staged per warp per window (class B)
 constexpr int kPrWarps = 8;         // warps per CTA (classes B, C)
@@ -91,7 +92,10 @@ __global__ void class_bounds_kernel(const uint32_t* __restrict__ off,
                                     const uint32_t* __restrict__ order, uint64_t m,
                                     uint32_t* __restrict__ out) {
   if (threadIdx.x != 0 || blockIdx.x != 0) return;
-  const uint32_t lim[3] = {kLenA, kLenB, kHubLong};
+  // 512-thread class-A CTAs only for the few rows that set the critical
+  // path: longer than kHubLong AND than a quarter of the longest row
+  const uint32_t longest = m ? off[order[0] + 1] - off[order[0]] : 0u;
+  const uint32_t lim[3] = {kLenA, kLenB, max(kHubLong, longest / 4)};
   for (int c = 0; c < 3; ++c) {  // first index whose length is <= lim[c]
     uint64_t lo = 0, hi = m;
     while (lo < hi) {

@@ -408,8 +408,17 @@ __global__ void __launch_bounds__(kBulkWarps * 32) gather_bulk_kernel(
   uint32_t phase[2] = {0, 0};
   // in-flight batch state (one per buffer)
   int buf = 0;
+  // the next batch's ids are loaded one batch ahead (ids may sit in host
+  // memory, read in place: their PCIe latency then overlaps this batch)
+  auto id_of = [&](uint64_t k) -> uint64_t {
+    const uint64_t i = (nb - 1 - k) * B + lane;
+    return (k < nb && lane < (int)B && i < n) ? ids[i] : 0ull;
+  };
+  uint64_t id_next = id_of(warp);
   for (uint64_t k = warp; k < nb; k += nwarps) {
     const uint64_t b0 = (nb - 1 - k) * B;  // cold (highest ids) first
+    const uint64_t id = id_next;
+    id_next = id_of(k + nwarps);
     const uint32_t bar = buf ? bar1 : bar0;
     const uint32_t sb = buf ? s1 : s0;
     // the buffer we are about to fill was stored from two batches ago
@@ -418,7 +427,7 @@ __global__ void __launch_bounds__(kBulkWarps * 32) gather_bulk_kernel(
     const uint8_t* src = nullptr;
     int tier = -1;
     if (lane < (int)B && b0 + lane < n) {
-      src = row_ptr(t, ids[b0 + lane], &tier);
+      src = row_ptr(t, id, &tier);
       if (tier == 3) atomicMin(err, (unsigned long long)(b0 + lane));
     }
     cl += __popc(__ballot_sync(0xffffffffu, tier == 0));
