@@ -560,10 +560,13 @@ def run_ours(args):
     alg_bytes = per_launch * (2 * R + 8)  # payload read + output write + ids
     t_launch = statistics.mean(step_times) * 1e-3
     frac_l, frac_p, frac_h = cl / max(u_all, 1), cp / max(u_all, 1), ch / max(u_all, 1)
-    hbm_bytes = per_launch * (frac_l * R + R + 8)
+    # a split cold row crosses PCIe as its whole 128 B lines (Hc bytes) and
+    # reads its remainder from HBM (TG_COLD_SPLIT_TAIL)
+    Hc = store.cold_host_bytes
+    hbm_bytes = per_launch * (frac_l * R + frac_h * (R - Hc) + R + 8)
     t_hbm = hbm_bytes / (hbm_peak * 1e9)
     t_nvl = per_launch * frac_p * R / (nvl_peak * 1e9)
-    t_pcie = per_launch * frac_h * R / (pcie_peak * 1e9)
+    t_pcie = per_launch * frac_h * Hc / (pcie_peak * 1e9)
     t_star = max(t_hbm, t_nvl, t_pcie)
     bound = ["hbm", "nvlink", "pcie"][int(np.argmax([t_hbm, t_nvl, t_pcie]))]
     achieved = alg_bytes / t_launch / 1e9
@@ -626,7 +629,10 @@ def run_ours(args):
                          "frac": round(t_star / t_launch, 4), "traffic": traffic,
                          "kernel": "gather_bulk_kernel (K8: TMA bulk copies, cold tier " + (
                              "read in place)" if cfg.get("cold_mode") == "indirect"
-                             else "128 B-padded)"),
+                             else "128 B-padded)" if Hc == R
+                             else f"split: {Hc} B of whole lines per row over PCIe, the last "
+                                  f"{R - Hc} B from HBM)"),
+                         "cold_bytes_over_pcie_per_row": int(Hc),
                          "algorithmic_bytes_per_launch": int(alg_bytes),
                          "mixed": {"hbm_gbs": hbm_peak, "hbm_src": hbm_src,
                                    "pcie_gbs": round(pcie_peak, 2),

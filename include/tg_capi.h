@@ -230,6 +230,10 @@ typedef struct tg_store tg_store;
                              /* through shared memory                            */
 #define TG_GATHER_L2PF 8u    /* K8 LDG path with the L2::256B prefetch hint      */
 #define TG_GATHER_SPREAD 16u /* K8: deal consecutive batches across CTAs         */
+#define TG_COLD_SPLIT_TAIL 32u /* TG_COLD_REORDERED with R % 128 != 0: keep each  */
+                             /* cold row's whole 128 B lines in host memory and */
+                             /* the R mod 128 remainder in HBM (one PCIe read   */
+                             /* request fewer per cold row)                      */
 
 int tg_store_create(tg_ctx* ctx, const tg_layout* layout, uint32_t device_index, uint32_t flags,
                     tg_store** out);
@@ -248,6 +252,9 @@ int tg_store_place(tg_store* s, const void* features, const uint64_t* new_id_of)
 int tg_store_place_rows(tg_store* s, const void* rows, uint64_t nrows, const uint32_t* row_of);
 void* tg_store_local_base(const tg_store* s);
 uint64_t tg_store_local_rows(const tg_store* s);
+/* Bytes of each cold row read over PCIe (row_bytes, or its whole 128 B lines
+ * under TG_COLD_SPLIT_TAIL once placed). */
+uint64_t tg_store_cold_host_bytes(const tg_store* s);
 /* Point device d's slot of the combined-tensor table at a peer's local base
  * (same-process peer pointer, or a CUDA-IPC mapping from tg_ipc_open). */
 int tg_store_set_peer(tg_store* s, uint32_t d, const void* peer_local_base);

@@ -33,6 +33,10 @@ struct TieredStoreOptions {
   bool cold_indirect = false;
   // Pad cold rows to a 128-byte stride (whole PCIe read requests).
   bool pad128 = true;
+  // Rows whose size is not a multiple of 128 B: keep each cold row's whole
+  // 128 B lines in host memory and the remainder in HBM (one PCIe read
+  // request fewer per cold row: C2's 400 B rows read as 384 + 16).
+  bool split_tail = true;
   // K8 through TMA bulk copies staged in shared memory (else 16 B loads).
   bool bulk = true;
   // Deal consecutive row batches across CTAs, so the cold (PCIe) rows, taken

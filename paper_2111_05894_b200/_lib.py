@@ -24,6 +24,7 @@ TG_COLD_PAD128 = 2
 TG_GATHER_BULK = 4
 TG_GATHER_L2PF = 8
 TG_GATHER_SPREAD = 16
+TG_COLD_SPLIT_TAIL = 32
 
 
 class TgLayout(C.Structure):
@@ -98,6 +99,7 @@ SIGNATURES = {
     "tg_store_place": (I32, [vp, vp, vp]),
     "tg_store_local_base": (vp, [vp]),
     "tg_store_local_rows": (U64, [vp]),
+    "tg_store_cold_host_bytes": (U64, [vp]),
     "tg_store_set_peer": (I32, [vp, U32, vp]),
     "tg_store_share_cold": (I32, [vp, vp]),
     "tg_gather_rows": (I32, [vp, vp, U64, vp, PR]),

@@ -58,6 +58,7 @@ TieredFeatureStore::TieredFeatureStore(const FeatureMatrix& features, const Node
                     layout.num_devices, layout.feature_dim, layout.elem_bytes};
   const std::uint32_t flags = (opts.cold_indirect ? TG_COLD_INDIRECT : TG_COLD_REORDERED) |
                               (opts.pad128 ? TG_COLD_PAD128 : 0u) |
+                              (opts.split_tail ? TG_COLD_SPLIT_TAIL : 0u) |
                               (opts.bulk ? TG_GATHER_BULK : 0u) |
                               (opts.spread ? TG_GATHER_SPREAD : 0u);
   static const std::uint64_t kNoRow = 0;

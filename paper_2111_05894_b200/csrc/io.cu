@@ -135,7 +135,7 @@ __global__ void __launch_bounds__(256) place_chunk_kernel(const uint8_t* __restr
                                                           const uint64_t* __restrict__ new_id_of,
                                                           uint8_t* local, uint8_t* cold, uint64_t cs,
                                                           uint64_t lb, uint64_t mb, uint32_t D,
-                                                          uint32_t dev) {
+                                                          uint32_t dev, uint8_t* tail, uint64_t H) {
   const int lane = threadIdx.x & 31;
   const uint64_t warp = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
   const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
@@ -143,6 +143,17 @@ __global__ void __launch_bounds__(256) place_chunk_kernel(const uint8_t* __restr
   for (uint64_t i = warp; i < cnt; i += nw) {
     const uint64_t p = new_id_of[r0 + i];
     uint8_t* d;
+    const V* s = reinterpret_cast<const V*>(src + i * R);
+    if (p >= mb && H) {  // TG_COLD_SPLIT_TAIL: whole lines to the host row, the rest to HBM
+      V* dh = reinterpret_cast<V*>(cold + (p - mb) * cs);
+      V* dt = reinterpret_cast<V*>(tail + (p - mb) * (R - H));
+      const uint64_t Hc = H / sizeof(V);
+      for (uint64_t c = lane; c < C; c += 32) {
+        if (c < Hc) dh[c] = s[c];
+        else dt[c - Hc] = s[c];
+      }
+      continue;
+    }
     if (p < lb) {
       d = local + p * R;
     } else if (p < mb) {
@@ -152,7 +163,6 @@ __global__ void __launch_bounds__(256) place_chunk_kernel(const uint8_t* __restr
     } else {
       d = cold + (p - mb) * cs;
     }
-    const V* s = reinterpret_cast<const V*>(src + i * R);
     V* dv = reinterpret_cast<V*>(d);
     for (uint64_t c = lane; c < C; c += 32) dv[c] = s[c];
   }
@@ -269,12 +279,14 @@ int tg_store_place_feat(tg_store* s, const char* path, const uint64_t* new_id_of
         if (w == 16)
           place_chunk_kernel<uint4><<<grid, 256, 0, ctx->stream>>>(st.dev[b], r0, cnt, R, perm,
                                                                    s->local, cold, s->cold_stride,
-                                                                   lb, mb, s->L.num_devices, s->dev);
+                                                                   lb, mb, s->L.num_devices, s->dev,
+                                                                   s->cold_tail, s->cold_head);
         else
           place_chunk_kernel<uint8_t><<<grid, 256, 0, ctx->stream>>>(st.dev[b], r0, cnt, R, perm,
                                                                      s->local, cold, s->cold_stride,
                                                                      lb, mb, s->L.num_devices,
-                                                                     s->dev);
+                                                                     s->dev, s->cold_tail,
+                                                                     s->cold_head);
         TGB_LAUNCHED();
         st.release(b);
       }

@@ -18,6 +18,11 @@ struct tg_store {
   uint8_t* cold_host = nullptr;                   // host view (owned when own_cold)
   const uint8_t* cold_dev = nullptr;              // device view of the cold tier
   uint64_t cold_stride = 0;
+  // TG_COLD_SPLIT_TAIL: the host row holds cold_head bytes (whole 128 B
+  // lines); the remaining R - cold_head bytes of each cold row sit in HBM
+  uint64_t cold_head = 0;                         // 0: the whole row is in host memory
+  uint8_t* cold_tail = nullptr;                   // device, (N-mb) x (R - cold_head)
+  bool own_cold_tail = false;
   bool own_cold = false;
   void* registered = nullptr;                     // caller matrix registered for INDIRECT
   uint32_t* cold_src = nullptr;                   // INDIRECT: cold slot -> original row

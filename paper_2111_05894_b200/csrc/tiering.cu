@@ -187,9 +187,11 @@ constexpr int kCopyPerLane = kCopyChunks / 32;
 
 // Copies a batch of B rows: src[j]/dst[j] held by lane j (j < B, nullptr =
 // skip). C = row_bytes / sizeof(V) chunks per row; B*C <= kCopyChunks.
+// tail/Hc: a split cold row's chunks [Hc, C) come from `tail` (per lane, or null).
 template <typename V, bool PF = false>
 __device__ __forceinline__ void copy_batch(const uint8_t* src, uint8_t* dst, uint32_t B,
-                                           uint32_t C, int lane) {
+                                           uint32_t C, int lane, const uint8_t* tail = nullptr,
+                                           uint32_t Hc = 0) {
   const uint32_t total = B * C;
   V buf[kCopyPerLane];
   const V* sp[kCopyPerLane];
@@ -203,8 +205,12 @@ __device__ __forceinline__ void copy_batch(const uint8_t* src, uint8_t* dst, uin
         __shfl_sync(0xffffffffu, reinterpret_cast<uintptr_t>(src), row));
     uint8_t* d = reinterpret_cast<uint8_t*>(
         __shfl_sync(0xffffffffu, reinterpret_cast<uintptr_t>(dst), row));
+    const uint8_t* tl = reinterpret_cast<const uint8_t*>(
+        __shfl_sync(0xffffffffu, reinterpret_cast<uintptr_t>(tail), row));
     const bool ok = idx < total && s != nullptr;
-    sp[u] = ok ? reinterpret_cast<const V*>(s) + ch : nullptr;
+    sp[u] = !ok ? nullptr
+                : (tl && ch >= Hc) ? reinterpret_cast<const V*>(tl) + (ch - Hc)
+                                   : reinterpret_cast<const V*>(s) + ch;
     dp[u] = ok ? reinterpret_cast<V*>(d) + ch : nullptr;
   }
 #pragma unroll
@@ -218,15 +224,17 @@ __device__ __forceinline__ void copy_batch(const uint8_t* src, uint8_t* dst, uin
 // Large rows (C > kCopyChunks): one row per warp, looped.
 template <typename V>
 __device__ __forceinline__ void copy_row_looped(const uint8_t* src, uint8_t* dst, uint64_t C,
-                                                int lane) {
+                                                int lane, const uint8_t* tail = nullptr,
+                                                uint64_t Hc = 0) {
   const V* s = reinterpret_cast<const V*>(src);
+  const V* tl = reinterpret_cast<const V*>(tail);
   V* d = reinterpret_cast<V*>(dst);
   for (uint64_t c0 = 0; c0 < C; c0 += kCopyChunks) {
     V buf[kCopyPerLane];
 #pragma unroll
     for (int u = 0; u < kCopyPerLane; ++u) {
       const uint64_t c = c0 + lane + 32u * u;
-      if (c < C) buf[u] = ld_row<V>(s + c);
+      if (c < C) buf[u] = ld_row<V>((tl && c >= Hc) ? tl + (c - Hc) : s + c);
     }
 #pragma unroll
     for (int u = 0; u < kCopyPerLane; ++u) {
@@ -242,8 +250,10 @@ struct GatherTable {
   const uint8_t* inter[TG_MAX_DEVICES];
   const uint8_t* cold;
   const uint32_t* cold_src;
+  const uint8_t* cold_tail;  // TG_COLD_SPLIT_TAIL: bytes [cold_head, R) of cold rows, in HBM
   uint64_t R;
   uint64_t cold_stride;
+  uint64_t cold_head;
   // synchronous C-ABI path: the last CTA to finish copies {counters, err} to
   // mapped pinned host memory and re-arms them (no memset / D2H copy calls)
   uint64_t* fin_host;
@@ -276,15 +286,19 @@ __device__ __forceinline__ void gather_finalize(const GatherTable& t, uint64_t* 
   }
 }
 
-__device__ __forceinline__ const uint8_t* row_ptr(const GatherTable& t, uint64_t id, int* tier) {
+// *tail: for a split cold row, where its bytes [cold_head, R) live (else null)
+__device__ __forceinline__ const uint8_t* row_ptr(const GatherTable& t, uint64_t id, int* tier,
+                                                  const uint8_t** tail) {
   uint32_t owner = 0;
   uint64_t slot = 0;
   const int k = tier_of(t.m, id, &owner, &slot);
   *tier = k;
+  *tail = nullptr;
   if (k == 3) return nullptr;
   if (id < t.m.lb) return t.local + slot * t.R;
   if (k == 2) {
     const uint64_t row = t.cold_src ? t.cold_src[slot] : slot;
+    if (t.cold_tail) *tail = t.cold_tail + row * (t.R - t.cold_head);
     return t.cold + row * t.cold_stride;
   }
   return t.inter[owner] + slot * t.R;
@@ -310,25 +324,29 @@ __global__ void __launch_bounds__(256) gather_kernel(GatherTable t, const uint64
   for (uint64_t k = warp; k < nb; k += nwarps) {
     const uint64_t b0 = (nb - 1 - k) * B;
     const uint8_t* src = nullptr;
+    const uint8_t* tail = nullptr;
     uint8_t* d = nullptr;
     int tier = -1;
     if (lane < (int)B && b0 + lane < n) {
-      src = row_ptr(t, ids[b0 + lane], &tier);
+      src = row_ptr(t, ids[b0 + lane], &tier, &tail);
       if (tier == 3) atomicMin(err, (unsigned long long)(b0 + lane));
       else d = dst + (b0 + lane) * t.R;
     }
     cl += __popc(__ballot_sync(0xffffffffu, tier == 0));
     cp += __popc(__ballot_sync(0xffffffffu, tier == 1));
     ch += __popc(__ballot_sync(0xffffffffu, tier == 2));
+    const uint32_t Hc = static_cast<uint32_t>(t.cold_head / sizeof(V));
     if (C <= (uint32_t)kCopyChunks) {
-      copy_batch<V, PF>(src, d, B, C, lane);
+      copy_batch<V, PF>(src, d, B, C, lane, tail, Hc);
     } else {
       for (uint32_t j = 0; j < B; ++j) {
         const uint8_t* s = reinterpret_cast<const uint8_t*>(
             __shfl_sync(0xffffffffu, reinterpret_cast<uintptr_t>(src), j));
+        const uint8_t* tl = reinterpret_cast<const uint8_t*>(
+            __shfl_sync(0xffffffffu, reinterpret_cast<uintptr_t>(tail), j));
         uint8_t* o = reinterpret_cast<uint8_t*>(
             __shfl_sync(0xffffffffu, reinterpret_cast<uintptr_t>(d), j));
-        if (s) copy_row_looped<V>(s, o, C, lane);
+        if (s) copy_row_looped<V>(s, o, C, lane, tl, Hc);
       }
     }
   }
@@ -425,9 +443,10 @@ __global__ void __launch_bounds__(kBulkWarps * 32) gather_bulk_kernel(
     bulk_wait_read<1>();
     __syncwarp();
     const uint8_t* src = nullptr;
+    const uint8_t* tail = nullptr;
     int tier = -1;
     if (lane < (int)B && b0 + lane < n) {
-      src = row_ptr(t, id, &tier);
+      src = row_ptr(t, id, &tier, &tail);
       if (tier == 3) atomicMin(err, (unsigned long long)(b0 + lane));
     }
     cl += __popc(__ballot_sync(0xffffffffu, tier == 0));
@@ -436,7 +455,13 @@ __global__ void __launch_bounds__(kBulkWarps * 32) gather_bulk_kernel(
     const uint32_t nrows = __popc(__ballot_sync(0xffffffffu, src != nullptr));
     if (lane == 0) mbar_expect_tx(bar, nrows * R);
     __syncwarp();
-    if (src) bulk_g2s(sb + lane * Rpad, src, R, bar);
+    if (tail) {  // split cold row: whole lines over PCIe, the remainder from HBM
+      const uint32_t H = static_cast<uint32_t>(t.cold_head);
+      bulk_g2s(sb + lane * Rpad, src, H, bar);
+      bulk_g2s(sb + lane * Rpad + H, tail, R - H, bar);
+    } else if (src) {
+      bulk_g2s(sb + lane * Rpad, src, R, bar);
+    }
     // drain the OTHER buffer's batch (issued last iteration) while this one loads
     mbar_wait_s(bar, phase[buf]);
     phase[buf] ^= 1;
@@ -774,8 +799,10 @@ GatherTable make_table(const tg_store* s) {
   for (uint32_t d = 0; d < s->L.num_devices; ++d) t.inter[d] = s->inter[d];
   t.cold = s->cold_dev;
   t.cold_src = s->cold_src;
+  t.cold_tail = s->cold_head ? s->cold_tail : nullptr;
   t.R = s->R;
   t.cold_stride = s->cold_stride;
+  t.cold_head = s->cold_head;
   return t;
 }
 
@@ -795,6 +822,8 @@ void launch_gather(tg_store* s, const uint64_t* ids_dev, uint64_t n, void* dst_d
   const uint32_t spread = (s->flags & TG_GATHER_SPREAD) ? 1u : 0u;
   uint64_t align = reinterpret_cast<uint64_t>(dst_dev) | reinterpret_cast<uint64_t>(s->local) |
                    reinterpret_cast<uint64_t>(s->cold_dev) | s->cold_stride;
+  if (s->cold_head)
+    align |= reinterpret_cast<uint64_t>(s->cold_tail) | s->cold_head | (s->R - s->cold_head);
   for (uint32_t d = 0; d < s->L.num_devices; ++d) align |= reinterpret_cast<uint64_t>(s->inter[d]);
   const int w = vec_width(s->R, {align});
   auto* dst = static_cast<uint8_t*>(dst_dev);
@@ -1058,6 +1087,7 @@ int tg_store_destroy(tg_store* s) {
   if (s->result_host) cudaFreeHost(s->result_host);
   if (s->own_cold && s->cold_host) cudaFreeHost(s->cold_host);
   if (s->own_cold_src) cudaFree(s->cold_src);
+  if (s->own_cold_tail) cudaFree(s->cold_tail);
   if (s->registered) release_host_matrix(s->registered);
   delete s;
   return TG_OK;
@@ -1101,6 +1131,9 @@ int tg_store_measure_cold_us(tg_store* s, uint64_t rows, int reps, double* us) {
   });
 }
 uint64_t tg_store_local_rows(const tg_store* s) { return s ? s->local_rows : 0; }
+uint64_t tg_store_cold_host_bytes(const tg_store* s) {
+  return s ? (s->cold_head ? s->cold_head : s->R) : 0;
+}
 
 int tg_store_set_peer(tg_store* s, uint32_t d, const void* peer_local_base) {
   return guard([&] {
@@ -1124,6 +1157,17 @@ namespace tgb {
 const uint8_t* ensure_cold_tier(tg_store* s) {
   const uint64_t cold = s->L.num_rows - s->L.multi_boundary;
   s->cold_stride = (s->flags & TG_COLD_PAD128) ? (s->R + 127) / 128 * 128 : s->R;
+  s->cold_head = 0;
+  if ((s->flags & TG_COLD_SPLIT_TAIL) && s->R > 128 && s->R % 128 && s->R % 16 == 0) {
+    // whole 128 B lines in host memory (packed: every row starts on a line),
+    // the R mod 128 remainder of every cold row in HBM
+    s->cold_head = s->R / 128 * 128;
+    s->cold_stride = s->cold_head;
+    if (!s->own_cold_tail) {
+      TGB_CUDA(cudaMalloc(&s->cold_tail, std::max<uint64_t>(cold * (s->R - s->cold_head), 16)));
+      s->own_cold_tail = true;
+    }
+  }
   if (!s->own_cold) {
     TGB_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&s->cold_host),
                            std::max<uint64_t>(cold * s->cold_stride, 16),
@@ -1168,6 +1212,8 @@ void place_impl(tg_store* s, const void* src_rows, uint64_t src_nrows, const uin
     s->cold_dev = s->cold_owner->cold_dev;
     s->cold_src = s->cold_owner->cold_src;
     s->cold_stride = s->cold_owner->cold_stride;
+    s->cold_head = s->cold_owner->cold_head;
+    s->cold_tail = s->cold_owner->cold_tail;
   } else if (s->flags & TG_COLD_INDIRECT) {
     // the caller's rows are read in place through the row map
     const uint64_t cold = N - mb;
@@ -1180,6 +1226,7 @@ void place_impl(tg_store* s, const void* src_rows, uint64_t src_nrows, const uin
                                ctx->stream));
     s->cold_dev = src;
     s->cold_stride = R;
+    s->cold_head = 0;
     if (s->registered) release_host_matrix(s->registered);
     s->registered = reg;  // keep the caller's matrix mapped for the store's lifetime
     reg = nullptr;
@@ -1194,7 +1241,15 @@ void place_impl(tg_store* s, const void* src_rows, uint64_t src_nrows, const uin
     c.dst_stride = s->cold_stride;
     c.src_idx32 = order;
     c.src_row_base = mb;
-    launch_move(ctx, c, cold, R);
+    const uint64_t H = s->cold_head ? s->cold_head : R;
+    launch_move(ctx, c, cold, H);
+    if (s->cold_head) {  // the remainders into HBM
+      MoveArgs t = c;
+      t.src = src + H;
+      t.dst = s->cold_tail;
+      t.dst_stride = R - H;
+      launch_move(ctx, t, cold, R - H);
+    }
   }
   ctx->sync();
   if (reg) release_host_matrix(reg);

@@ -19,7 +19,8 @@ from typing import Iterable, Optional, Sequence
 
 import numpy as np
 
-from ._lib import (LIB, TG_COLD_INDIRECT, TG_COLD_PAD128, TG_COLD_REORDERED, TG_GATHER_BULK,
+from ._lib import (LIB, TG_COLD_INDIRECT, TG_COLD_PAD128, TG_COLD_REORDERED, TG_COLD_SPLIT_TAIL,
+                   TG_GATHER_BULK,
                    TG_GATHER_L2PF, TG_GATHER_SPREAD, TgLayout, TgLocation, TgReport)
 
 __all__ = [
@@ -650,13 +651,15 @@ class TieredFeatureStore:
 
     def __init__(self, features, perm, layout: TierLayout, device_index: int = 0, *,
                  ctx: Context = None, cold_mode: str = "reordered", pad128: bool = True,
-                 gather_mode: str = "bulk+spread", place: bool = True):
+                 split_tail: bool = True, gather_mode: str = "bulk+spread", place: bool = True):
         self.ctx = _ctx(ctx)
         self.layout = layout
         self.device_index = device_index
         flags = {"reordered": TG_COLD_REORDERED, "indirect": TG_COLD_INDIRECT}[cold_mode]
         if pad128:
             flags |= TG_COLD_PAD128
+        if split_tail:  # whole 128 B lines of each cold row in host memory, the rest in HBM
+            flags |= TG_COLD_SPLIT_TAIL
         # gather_mode: "ldg" | "bulk" | "l2pf", optionally "+spread"
         for tok in gather_mode.split("+"):
             flags |= {"ldg": 0, "bulk": TG_GATHER_BULK, "l2pf": TG_GATHER_L2PF,
@@ -718,6 +721,12 @@ class TieredFeatureStore:
     @property
     def local_rows(self) -> int:
         return int(LIB.tg_store_local_rows(self.h))
+
+    @property
+    def cold_host_bytes(self) -> int:
+        """Bytes of each cold row that cross PCIe (row_bytes, or its whole
+        128 B lines when the remainder is kept in HBM)."""
+        return int(LIB.tg_store_cold_host_bytes(self.h))
 
     def measure_cold_us(self, rows: int, reps: int = 5) -> float:
         """Mean us to read `rows` random rows of this store's cold region

@@ -111,11 +111,17 @@ def _virtual_devices(tg, ctx, features, perm, lay, **kw):
     return stores
 
 
-@pytest.mark.parametrize("dim,eb", [(100, 4), (128, 4), (768, 2), (9, 4), (3, 1), (1, 8), (2048, 4)])
-@pytest.mark.parametrize("cold_mode,pad", [("reordered", False), ("indirect", False),
-                                           ("reordered", True)])
+@pytest.mark.parametrize("dim,eb", [(100, 4), (128, 4), (768, 2), (9, 4), (3, 1), (1, 8), (2048, 4),
+                                    (36, 4), (300, 4), (1100, 4)])
+@pytest.mark.parametrize("cold_mode,pad,split", [("reordered", False, False), ("indirect", False, False),
+                                                 ("reordered", True, False), ("reordered", True, True),
+                                                 ("reordered", False, True)])
 @pytest.mark.parametrize("mode", ["ldg", "bulk", "bulk+spread", "l2pf+spread"])
-def test_store_gather_bit_exact(tg, ctx, dim, eb, cold_mode, pad, mode):
+def test_store_gather_bit_exact(tg, ctx, dim, eb, cold_mode, pad, split, mode):
+    """Rows byte-exact vs reorder_features (reorder.cpp:97-117) and the report
+    equal to gather() (tiering.cpp:100-125) for every cold-tier format: split
+    cold rows (TG_COLD_SPLIT_TAIL: 400 B -> 384 host + 16 HBM, 144 -> 128+16,
+    1200 -> 1152+48, 4400 -> 4352+48 on the looped LDG path) included."""
     chk, port = checker(), oracle.port()
     n = 3000
     rng = np.random.default_rng(dim * eb)
@@ -126,7 +132,7 @@ def test_store_gather_bit_exact(tg, ctx, dim, eb, cold_mode, pad, mode):
                         (6, 0.37, 0.2), (2, 0.0, 0.0)):
         lay = tg.plan_layout(n, hot, rep, D, dim, eb)
         stores = _virtual_devices(tg, ctx, feat, perm, lay, cold_mode=cold_mode, pad128=pad,
-                                  gather_mode=mode)
+                                  split_tail=split, gather_mode=mode)
         ids = np.sort(rng.choice(n, size=700, replace=False)).astype(np.uint64)
         ids = np.concatenate([ids, rng.integers(0, n, 50).astype(np.uint64)])  # duplicates too
         for d, s in enumerate(stores):

@@ -80,9 +80,10 @@ def test_csrg_header_errors_match_reference(tg, ctx, refo, tmp_path):
         tg.load_csr_device(bad, ctx=ctx)
 
 
+@pytest.mark.parametrize("dim", [20, 100])
 @pytest.mark.parametrize("D,rep,hot", [(1, 0.0, 0.25), (3, 0.1, 0.6)])
-def test_feat_into_store(tg, ctx, refo, tmp_path, D, rep, hot):
-    n, dim, eb = 3001, 20, 4
+def test_feat_into_store(tg, ctx, refo, tmp_path, D, rep, hot, dim):
+    n, eb = 3001, 4
     rng = np.random.default_rng(D)
     feat = rng.integers(0, 256, (n, dim * eb), dtype=np.uint8)
     path = tmp_path / "f.feat"
