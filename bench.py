@@ -422,12 +422,14 @@ def run_ours(args):
         # the cache holds the rows in new-id (score) order, wrapping every P
         # rows, as a reorder_features'd matrix would (reorder.cpp:97-117)
         store = tg.TieredFeatureStore(None, perm, lay, rank, ctx=ctx,
-                                      cold_mode=cfg.get("cold_mode", "reordered"), place=False)
+                                      cold_mode=cfg.get("cold_mode", "reordered"), place=False,
+                                      gather_mode=args.gather_mode)
         store.place_rows(feat, (np.arange(n, dtype=np.uint64) % np.uint64(len(feat)))
                          .astype(np.uint32))
     else:
         store = tg.TieredFeatureStore(feat, perm, lay, rank, ctx=ctx,
-                                      cold_mode=cfg.get("cold_mode", "reordered"))
+                                      cold_mode=cfg.get("cold_mode", "reordered"),
+                                      gather_mode=args.gather_mode)
     if world > 1:
         exchange_peers(torch, tg, store, rank, world)
         dist.barrier()
@@ -610,6 +612,7 @@ def run_ours(args):
             "data": "synthetic (R-MAT graph, closed-form features, reference sampler id lists)",
             "config": {"workload": cfg["workload"], "nodes": n, "edges_after_dedup": e,
                        "row_bytes": R, "hot_fraction": hot, "layout": lay.as_tuple(),
+                       "gather_mode": args.gather_mode,
                        "l2": "flushed between steps (256 MB memset), per-step CUDA events",
                        "parallelism": f"{world} GPU(s), hot tier sharded, cold tier per rank"
                                       + (" (TEST MODE: all ranks share cuda:0, gloo plumbing; not "
@@ -890,6 +893,8 @@ def main():
     ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--gather-mode", default="bulk+spread+dynamic",
+                    help="K8 variant: ldg | bulk | l2pf, with +spread / +dynamic")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

@@ -234,6 +234,8 @@ typedef struct tg_store tg_store;
                              /* cold row's whole 128 B lines in host memory and */
                              /* the R mod 128 remainder in HBM (one PCIe read   */
                              /* request fewer per cold row)                      */
+#define TG_GATHER_DYNAMIC 64u /* K8 bulk: after one statically spread round,     */
+                             /* warps claim batches from a device counter        */
 
 int tg_store_create(tg_ctx* ctx, const tg_layout* layout, uint32_t device_index, uint32_t flags,
                     tg_store** out);

@@ -25,6 +25,7 @@ TG_GATHER_BULK = 4
 TG_GATHER_L2PF = 8
 TG_GATHER_SPREAD = 16
 TG_COLD_SPLIT_TAIL = 32
+TG_GATHER_DYNAMIC = 64
 
 
 class TgLayout(C.Structure):

@@ -60,7 +60,8 @@ TieredFeatureStore::TieredFeatureStore(const FeatureMatrix& features, const Node
                               (opts.pad128 ? TG_COLD_PAD128 : 0u) |
                               (opts.split_tail ? TG_COLD_SPLIT_TAIL : 0u) |
                               (opts.bulk ? TG_GATHER_BULK : 0u) |
-                              (opts.spread ? TG_GATHER_SPREAD : 0u);
+                              (opts.spread ? TG_GATHER_SPREAD : 0u) |
+                              (opts.dynamic ? TG_GATHER_DYNAMIC : 0u);
   static const std::uint64_t kNoRow = 0;
   static const std::uint8_t kNoByte = 0;
   const void* src = features.data.empty() ? &kNoByte : features.data.data();

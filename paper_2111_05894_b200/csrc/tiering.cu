@@ -258,7 +258,25 @@ struct GatherTable {
   // mapped pinned host memory and re-arms them (no memset / D2H copy calls)
   uint64_t* fin_host;
   unsigned* fin_done;
+  // TG_GATHER_DYNAMIC: after the first (statically spread) round, warps claim
+  // batches from this counter, so a warp waiting on a cold (PCIe) batch does
+  // not hold HBM batches behind it; the last CTA re-arms it
+  unsigned long long* claim;
+  unsigned* claim_done;
 };
+
+__device__ __forceinline__ void claim_finalize(const GatherTable& t) {
+  if (!t.claim) return;
+  __syncthreads();  // every warp of this CTA has made its last claim
+  if (threadIdx.x == 0) {
+    __threadfence();
+    if (atomicAdd(t.claim_done, 1u) == gridDim.x - 1) {
+      *reinterpret_cast<volatile unsigned long long*>(t.claim) = 0ull;
+      *reinterpret_cast<volatile unsigned*>(t.claim_done) = 0u;
+      __threadfence();
+    }
+  }
+}
 
 __device__ __forceinline__ void gather_finalize(const GatherTable& t, uint64_t* counters,
                                                 unsigned long long* err) {
@@ -432,11 +450,22 @@ __global__ void __launch_bounds__(kBulkWarps * 32) gather_bulk_kernel(
     const uint64_t i = (nb - 1 - k) * B + lane;
     return (k < nb && lane < (int)B && i < n) ? ids[i] : 0ull;
   };
-  uint64_t id_next = id_of(warp);
-  for (uint64_t k = warp; k < nb; k += nwarps) {
+  // first round static (spread over the SMs: it holds the cold batches of a
+  // sorted list), then dynamic claims (TG_GATHER_DYNAMIC) or the static stride
+  auto next_of = [&](uint64_t k) -> uint64_t {
+    if (!t.claim) return k + nwarps;
+    unsigned long long c = 0;
+    if (lane == 0) c = atomicAdd(t.claim, 1ull);
+    return nwarps + __shfl_sync(0xffffffffu, c, 0);
+  };
+  uint64_t k_next = warp;
+  uint64_t id_next = id_of(k_next);
+  while (k_next < nb) {
+    const uint64_t k = k_next;
     const uint64_t b0 = (nb - 1 - k) * B;  // cold (highest ids) first
     const uint64_t id = id_next;
-    id_next = id_of(k + nwarps);
+    k_next = next_of(k);
+    id_next = id_of(k_next);
     const uint32_t bar = buf ? bar1 : bar0;
     const uint32_t sb = buf ? s1 : s0;
     // the buffer we are about to fill was stored from two batches ago
@@ -474,6 +503,7 @@ __global__ void __launch_bounds__(kBulkWarps * 32) gather_bulk_kernel(
   if (lane != 0) cl = cp = ch = 0;
   block_add_counters(cl, cp, ch, counters);
   gather_finalize(t, counters, err);
+  claim_finalize(t);
 }
 
 // Generic row mover: dst + dst_row(i)*dst_stride <- src + src_row(i)*src_stride
@@ -818,6 +848,10 @@ void launch_gather(tg_store* s, const uint64_t* ids_dev, uint64_t n, void* dst_d
   if (finalize) {
     t.fin_host = s->result_dev;
     t.fin_done = reinterpret_cast<unsigned*>(s->counters + 4);
+  }
+  if (s->flags & TG_GATHER_DYNAMIC) {  // store-owned, zero between launches
+    t.claim = reinterpret_cast<unsigned long long*>(s->counters + 5);
+    t.claim_done = reinterpret_cast<unsigned*>(s->counters + 6);
   }
   const uint32_t spread = (s->flags & TG_GATHER_SPREAD) ? 1u : 0u;
   uint64_t align = reinterpret_cast<uint64_t>(dst_dev) | reinterpret_cast<uint64_t>(s->local) |

@@ -20,7 +20,7 @@ from typing import Iterable, Optional, Sequence
 import numpy as np
 
 from ._lib import (LIB, TG_COLD_INDIRECT, TG_COLD_PAD128, TG_COLD_REORDERED, TG_COLD_SPLIT_TAIL,
-                   TG_GATHER_BULK,
+                   TG_GATHER_BULK, TG_GATHER_DYNAMIC,
                    TG_GATHER_L2PF, TG_GATHER_SPREAD, TgLayout, TgLocation, TgReport)
 
 __all__ = [
@@ -651,7 +651,8 @@ class TieredFeatureStore:
 
     def __init__(self, features, perm, layout: TierLayout, device_index: int = 0, *,
                  ctx: Context = None, cold_mode: str = "reordered", pad128: bool = True,
-                 split_tail: bool = True, gather_mode: str = "bulk+spread", place: bool = True):
+                 split_tail: bool = True, gather_mode: str = "bulk+spread+dynamic",
+                 place: bool = True):
         self.ctx = _ctx(ctx)
         self.layout = layout
         self.device_index = device_index
@@ -663,7 +664,7 @@ class TieredFeatureStore:
         # gather_mode: "ldg" | "bulk" | "l2pf", optionally "+spread"
         for tok in gather_mode.split("+"):
             flags |= {"ldg": 0, "bulk": TG_GATHER_BULK, "l2pf": TG_GATHER_L2PF,
-                      "spread": TG_GATHER_SPREAD}[tok]
+                      "spread": TG_GATHER_SPREAD, "dynamic": TG_GATHER_DYNAMIC}[tok]
         h = C.c_void_p()
         _check(LIB.tg_store_create(self.ctx.h, C.byref(layout._c()), int(device_index), flags,
                                    C.byref(h)))

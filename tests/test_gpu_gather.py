@@ -116,7 +116,7 @@ def _virtual_devices(tg, ctx, features, perm, lay, **kw):
 @pytest.mark.parametrize("cold_mode,pad,split", [("reordered", False, False), ("indirect", False, False),
                                                  ("reordered", True, False), ("reordered", True, True),
                                                  ("reordered", False, True)])
-@pytest.mark.parametrize("mode", ["ldg", "bulk", "bulk+spread", "l2pf+spread"])
+@pytest.mark.parametrize("mode", ["ldg", "bulk", "bulk+spread", "l2pf+spread", "bulk+spread+dynamic"])
 def test_store_gather_bit_exact(tg, ctx, dim, eb, cold_mode, pad, split, mode):
     """Rows byte-exact vs reorder_features (reorder.cpp:97-117) and the report
     equal to gather() (tiering.cpp:100-125) for every cold-tier format: split
@@ -140,6 +140,38 @@ def test_store_gather_bit_exact(tg, ctx, dim, eb, cold_mode, pad, split, mode):
             out = s.gather_rows(ids, report=rep_)
             assert np.array_equal(out, reordered[ids])
             assert np.array_equal(rep_.as_array(), chk.gather(lay.as_tuple(), ids, d))
+
+
+@pytest.mark.parametrize("mode", ["bulk+spread+dynamic", "bulk+dynamic"])
+def test_dynamic_claims_rearm_between_launches(tg, ctx, mode):
+    """TG_GATHER_DYNAMIC: the store's claim counter is re-armed by the last
+    CTA of every launch, so back-to-back gathers of different lengths (sync
+    and stream-ordered) each copy every row exactly once."""
+    import torch
+    n, dim = 20000, 100
+    rng = np.random.default_rng(5)
+    feat = rng.integers(0, 256, (n, dim * 4), dtype=np.uint8)
+    perm = random_permutation(n, 3)
+    reordered = oracle.port().reorder_features(feat, perm)
+    lay = tg.plan_layout(n, 0.2, 0.0, 1, dim, 4)
+    st = tg.TieredFeatureStore(feat, perm, lay, ctx=ctx, gather_mode=mode)
+    chk = checker()
+    for size in (1, 31, 5000, 19000, 700, 12000):
+        ids = np.sort(rng.choice(n, size=size, replace=False)).astype(np.uint64)
+        rep_ = tg.TrafficReport()
+        out = st.gather_rows(ids, report=rep_)
+        assert np.array_equal(out, reordered[ids])
+        assert np.array_equal(rep_.as_array(), chk.gather(lay.as_tuple(), ids, 0))
+    dev = torch.device("cuda", ctx.device)
+    lists = [np.sort(rng.choice(n, size=s_, replace=False)).astype(np.uint64)
+             for s_ in (9000, 300, 15000)]
+    cnt = torch.zeros(3, dtype=torch.int64, device=dev)
+    err = torch.full((1,), -1, dtype=torch.int64, device=dev)
+    for ids in lists:
+        out = torch.empty((len(ids), dim * 4), dtype=torch.uint8, device=dev)
+        st.gather_rows_async(torch.as_tensor(ids.astype(np.int64), device=dev), out, cnt, err)
+        torch.cuda.synchronize()
+        assert np.array_equal(out.cpu().numpy(), reordered[ids])
 
 
 def test_store_errors_and_empty(tg, ctx):
