@@ -15,10 +15,12 @@ timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --lo
 timeout 1200 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum,syslts__t_sectors_aperture_sysmem_lookup_miss.sum,syslts__t_sectors_aperture_peer_lookup_miss.sum \
    --clock-control none --csv --log-file $O/kernel_memory.csv \
    python bench.py --steps 5 --warmup 3 --no-cpu-baseline > $O/bench_ncu_mem.log 2>&1
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:gather -s 5 -c 2 \
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:gather_bulk -s 5 -c 2 \
    -o $O/gather python bench.py --steps 10 --warmup 3 --no-cpu-baseline > $O/ncu_gather.log 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:pr_ -s 6 -c 2 \
    -o $O/prstep python bench.py --steps 5 --warmup 3 --no-cpu-baseline > $O/ncu_pr.log 2>&1
 timeout 1800 python bench.py --config c3 --steps 100 --warmup 5 > $O/bench_c3.json 2> $O/bench_c3.err
+timeout 1500 ncu --set full --clock-control none --import-source on -k regex:gather_bulk -s 5 -c 2 \
+   -o $O/gather_c3 python bench.py --config c3 --steps 10 --warmup 3 --no-cpu-baseline > $O/ncu_gather_c3.log 2>&1
 timeout 2400 python bench.py --config c4 --steps 100 --warmup 5 > $O/bench_c4.json 2> $O/bench_c4.err
 ls -la $O
