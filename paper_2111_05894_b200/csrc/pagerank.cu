@@ -701,33 +701,36 @@ __device__ __forceinline__ void thread_row(const PrStepArgs& a, uint32_t r,
 
 // Classes B and C with the hot columns in shared memory: one persistent
 // 768-thread CTA per SM copies norm_in of the hot nodes into shared memory
-// once per step, then claims work units from a counter (class-B units of 96
-// rows first: the longest rows start early; then class-C units of 768 rows).
-// Claims, not a static stride: CTAs on the SMs that class A holds start late
-// and only take what is left.
+// once per step; then every WARP claims work on its own (no CTA barriers:
+// the loads stay in flight across units), kHotChunk units per claim. A unit
+// is 4 class-B rows (8 lanes each) or 32 class-C rows (a thread each); the
+// class-B units come first (the longest rows start early). Claims, not a
+// static stride: CTAs on the SMs that class A holds start late and only take
+// what is left.
+constexpr uint32_t kHotChunk = 4;
 __global__ void __launch_bounds__(kHotThreads, 1) pr_step_hot_kernel(const PrStepArgs a,
                                                                      uint32_t b_units,
                                                                      uint32_t c_units,
                                                                      unsigned* claim) {
   extern __shared__ __align__(16) double hsm[];  // [kHotThreads/kBLanes * kBWin] windows, then hot
-  double* win = hsm;
   double* hot = hsm + kHotThreads / kBLanes * kBWin;
   for (uint32_t k = threadIdx.x; k < a.nhot; k += kHotThreads) hot[k] = __ldg(a.norm_in + a.hot_ids[k]);
   __syncthreads();
-  constexpr uint32_t kRowsB = kHotThreads / kBLanes;
-  const int g = threadIdx.x / kBLanes;
-  __shared__ uint32_t unit;
+  const int lane = threadIdx.x & 31;
+  double* win = hsm + (threadIdx.x / kBLanes) * kBWin;  // this lane group's window
+  const uint32_t total = b_units + c_units;
   while (true) {
-    __syncthreads();  // everyone has read the previous unit
-    if (threadIdx.x == 0) unit = atomicAdd(claim, 1u);
-    __syncthreads();
-    const uint32_t u = unit;
-    if (u >= b_units + c_units) break;
-    if (u < b_units) {
-      group_row<true>(a, a.nA + (int64_t)u * kRowsB + g, win + g * kBWin, hot);
-    } else {
-      const uint64_t i = a.nB + (uint64_t)(u - b_units) * kHotThreads + threadIdx.x;
-      if (i < a.m) thread_row<true>(a, a.order[i], hot);
+    unsigned base = 0;
+    if (lane == 0) base = atomicAdd(claim, kHotChunk);
+    base = __shfl_sync(0xffffffffu, base, 0);
+    if (base >= total) break;
+    for (uint32_t u = base; u < base + kHotChunk && u < total; ++u) {
+      if (u < b_units) {
+        group_row<true>(a, a.nA + (int64_t)u * (32 / kBLanes) + lane / kBLanes, win, hot);
+      } else {
+        const uint64_t i = a.nB + (uint64_t)(u - b_units) * 32 + lane;
+        if (i < a.m) thread_row<true>(a, a.order[i], hot);
+      }
     }
   }
 }
@@ -1014,9 +1017,9 @@ void pagerank_step(tg_ctx* ctx, const tg_graph* g, const uint32_t* deg, double d
   }
   const unsigned grid = static_cast<unsigned>(a.b_ctas + c_ctas);
   if (grid && g->tgt_tag) {
-    constexpr uint32_t kRowsB = kHotThreads / kBLanes;
+    constexpr uint32_t kRowsB = 32 / kBLanes;  // class-B rows per warp unit
     const uint32_t bu = (sc.nB - sc.nA + kRowsB - 1) / kRowsB;
-    const uint32_t cu = static_cast<uint32_t>((a.m - sc.nB + kHotThreads - 1) / kHotThreads);
+    const uint32_t cu = static_cast<uint32_t>((a.m - sc.nB + 31) / 32);
     const int smem = (kHotThreads / kBLanes * kBWin + kHotCols) * 8;
     static bool hattr[TG_MAX_DEVICES] = {};
     if (!hattr[ctx->device % TG_MAX_DEVICES]) {
@@ -1024,7 +1027,7 @@ void pagerank_step(tg_ctx* ctx, const tg_graph* g, const uint32_t* deg, double d
                                     smem));
       hattr[ctx->device % TG_MAX_DEVICES] = true;
     }
-    const unsigned pg = std::min<unsigned>(ctx->num_sms, bu + cu);
+    const unsigned pg = std::min<unsigned>(ctx->num_sms, (bu + cu + 23) / 24);
     auto* claim = ctx->scratch_t<unsigned>(kClaim, 1);
     TGB_CUDA(cudaMemsetAsync(claim, 0, 4, ctx->stream));
     pr_step_hot_kernel<<<pg, kHotThreads, smem, ctx->stream>>>(a, bu, cu, claim);
