@@ -111,10 +111,6 @@ uint64_t tg_graph_num_edges(const tg_graph* g);
 /* Device pointers of the narrowed CSR (u32) — for peer kernels and tests. */
 const uint32_t* tg_graph_offsets32(const tg_graph* g);
 const uint32_t* tg_graph_targets32(const tg_graph* g);
-/* Number of K3 hot columns: the highest in-degree nodes (at most 16384) whose
- * normalized values classes B/C read from shared memory (0 = off: n >= 2^31,
- * no edges, or TIERGRAPH_PR_HOT_COLUMNS=0 when the graph was created). */
-uint32_t tg_graph_hot_columns(const tg_graph* g);
 
 /* --------------------------------------------------------------- scoring
  * scoring.hpp:32 degree_score -> out (n x f64, host|device) */

@@ -69,7 +69,6 @@ SIGNATURES = {
     "tg_graph_destroy": (I32, [vp]),
     "tg_graph_num_nodes": (U64, [vp]),
     "tg_graph_num_edges": (U64, [vp]),
-    "tg_graph_hot_columns": (U32, [vp]),
     "tg_graph_offsets32": (vp, [vp]),
     "tg_graph_targets32": (vp, [vp]),
     "tg_degree_score": (I32, [vp, vp, vp]),

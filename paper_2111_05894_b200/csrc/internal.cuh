@@ -55,7 +55,7 @@ struct DeviceGuard {
 
 enum Slot : int {
   kScratchA = 0, kScratchB, kScratchC, kScratchD, kScratchE, kScratchF,
-  kStageIn0, kStageIn1, kStageIn2, kStageOut0, kStageOut1, kSmall, kClaim, kNumSlots
+  kStageIn0, kStageIn1, kStageIn2, kStageOut0, kStageOut1, kSmall, kNumSlots
 };
 
 }  // namespace tgb

@@ -21,7 +21,6 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
-#include <cstdlib>
 #include <string>
 #include <vector>
 
@@ -44,13 +43,6 @@ struct tg_graph {
     uint32_t nLong;   // order[0,nLong): len > kHubLong (512-thread class-A CTAs)
   };
   std::vector<Sched> scheds;
-  // K3 hot columns: the (at most kHotCols) nodes with the highest in-degree.
-  // Classes B and C read their normalized values from a shared-memory copy:
-  // tgt_tag[e] = 0x80000000 | slot for an edge into hot node hot_ids[slot],
-  // else tgt[e]. Built with the graph (n < 2^31); null when disabled.
-  uint32_t* tgt_tag = nullptr;
-  uint32_t* hot_ids = nullptr;
-  uint32_t nhot = 0;
 };
 
 namespace tgb {
@@ -68,13 +60,6 @@ constexpr uint32_t kLenB = 512;
 constexpr uint32_t kHubLong = 16384;
 constexpr int kPrWin = 256;         // edges staged per warp per window (class B)
 constexpr int kPrWarps = 8;         // warps per CTA (classes B, C)
-
-// A class-B/C CTA keeps this many hot-column values in shared memory (128 KB).
-// On R-MAT graphs the 16k highest in-degrees take ~45 % of all edges (C2), so
-// nearly half the norm gathers leave the L1 sector pipeline, the K3 floor.
-constexpr uint32_t kHotCols = 16384;
-constexpr uint32_t kHotTag = 0x80000000u;
-constexpr int kHotThreads = 768;  // persistent class-B/C CTA: 24 warps, one per SM
 
 // ------------------------------------------------------------ graph upload
 __global__ void narrow_offsets_kernel(const uint64_t* __restrict__ in, uint32_t* __restrict__ out,
@@ -203,9 +188,6 @@ __global__ void pr_init_kernel(const uint32_t* __restrict__ deg, const uint32_t*
 struct PrStepArgs {
   const uint32_t* off;
   const uint32_t* tgt;
-  const uint32_t* tgt_bc;   // classes B/C: tgt, or tgt_tag with hot columns
-  const uint32_t* hot_ids;  // hot column slot -> node (nhot of them)
-  uint32_t nhot;
   const uint32_t* deg;
   const double* norm_in;
   double* norm_out;
@@ -587,17 +569,7 @@ __global__ void __launch_bounds__(W * 32) pr_hub_kernel(const PrStepArgs a, uint
 // first lane adds each window in storage order — 4 chains per warp.
 constexpr int kBLanes = 8;
 constexpr int kBWin = kBLanes * 8;  // 64 edges per window
-// norm_in[t] for a class-B/C edge: a tagged hot column reads the CTA's
-// shared-memory copy (bit-identical values), anything else L1/L2.
-template <bool HOT>
-__device__ __forceinline__ double ld_norm(const PrStepArgs& a, const double* hot, uint32_t t) {
-  if constexpr (HOT) return (t & kHotTag) ? hot[t & ~kHotTag] : __ldg(a.norm_in + t);
-  else return __ldg(a.norm_in + t);
-}
-
-template <bool HOT = false>
-__device__ __forceinline__ void group_row(const PrStepArgs& a, int64_t i, double* buf,
-                                          const double* hot = nullptr) {
+__device__ __forceinline__ void group_row(const PrStepArgs& a, int64_t i, double* buf) {
   const int lane = threadIdx.x & 31, sl = lane & (kBLanes - 1);
   const bool has = i < static_cast<int64_t>(a.nB);
   const uint32_t r = has ? a.order[i] : 0u;
@@ -609,14 +581,14 @@ __device__ __forceinline__ void group_row(const PrStepArgs& a, int64_t i, double
 #pragma unroll
   for (int k = 0; k < K; ++k) {
     const uint32_t e = k * kBLanes + sl;
-    t1[k] = e < len ? __ldg(a.tgt_bc + beg + e) : 0xffffffffu;
+    t1[k] = e < len ? __ldg(a.tgt + beg + e) : 0xffffffffu;
   }
 #pragma unroll
-  for (int k = 0; k < K; ++k) v[k] = t1[k] != 0xffffffffu ? ld_norm<HOT>(a, hot, t1[k]) : 0.0;
+  for (int k = 0; k < K; ++k) v[k] = t1[k] != 0xffffffffu ? __ldg(a.norm_in + t1[k]) : 0.0;
 #pragma unroll
   for (int k = 0; k < K; ++k) {
     const uint32_t e = kBWin + k * kBLanes + sl;
-    t1[k] = e < len ? __ldg(a.tgt_bc + beg + e) : 0xffffffffu;
+    t1[k] = e < len ? __ldg(a.tgt + beg + e) : 0xffffffffu;
   }
   // the warp loops until its longest row is done (lengths are near-equal)
   uint32_t wmax = len;
@@ -629,11 +601,11 @@ __device__ __forceinline__ void group_row(const PrStepArgs& a, int64_t i, double
     __syncwarp();
     double vn[K];
 #pragma unroll
-    for (int k = 0; k < K; ++k) vn[k] = t1[k] != 0xffffffffu ? ld_norm<HOT>(a, hot, t1[k]) : 0.0;
+    for (int k = 0; k < K; ++k) vn[k] = t1[k] != 0xffffffffu ? __ldg(a.norm_in + t1[k]) : 0.0;
 #pragma unroll
     for (int k = 0; k < K; ++k) {
       const uint32_t e = wb + 2 * kBWin + k * kBLanes + sl;
-      t1[k] = e < len ? __ldg(a.tgt_bc + beg + e) : 0xffffffffu;
+      t1[k] = e < len ? __ldg(a.tgt + beg + e) : 0xffffffffu;
     }
     if (sl == 0 && wb < len)
       acc = chain_add(acc, buf, len - wb < (uint32_t)kBWin ? len - wb : kBWin);  // in order
@@ -647,11 +619,9 @@ __device__ __forceinline__ void group_row(const PrStepArgs& a, int64_t i, double
 // Class C: one thread per row of at most kLenB edges, in storage order. A
 // warp's 32 rows have near-equal lengths (length-sorted schedule), so the
 // lanes stay converged; 8 gathers per lane are in flight per step.
-template <bool HOT = false>
-__device__ __forceinline__ void thread_row(const PrStepArgs& a, uint32_t r,
-                                           const double* hot = nullptr) {
+__device__ __forceinline__ void thread_row(const PrStepArgs& a, uint32_t r) {
   const uint32_t beg = a.off[r], len = a.off[r + 1] - beg;
-  const uint32_t* t = a.tgt_bc + beg;
+  const uint32_t* t = a.tgt + beg;
   double acc = 0.0;  // scoring.cpp:67
   uint32_t k = 0;
   // peel to a 16 B boundary (its loads independent of each other), then two
@@ -663,7 +633,7 @@ __device__ __forceinline__ void thread_row(const PrStepArgs& a, uint32_t r,
 #pragma unroll
     for (int q = 0; q < 3; ++q) ti[q] = q < (int)peel ? __ldg(t + q) : 0u;
 #pragma unroll
-    for (int q = 0; q < 3; ++q) v[q] = q < (int)peel ? ld_norm<HOT>(a, hot, ti[q]) : 0.0;
+    for (int q = 0; q < 3; ++q) v[q] = q < (int)peel ? __ldg(a.norm_in + ti[q]) : 0.0;
 #pragma unroll
     for (int q = 0; q < 3; ++q)
       if (q < (int)peel) acc = __dadd_rn(acc, v[q]);
@@ -680,7 +650,7 @@ __device__ __forceinline__ void thread_row(const PrStepArgs& a, uint32_t r,
       }
       double v[8];
 #pragma unroll
-      for (int q = 0; q < 8; ++q) v[q] = ld_norm<HOT>(a, hot, ti[q]);
+      for (int q = 0; q < 8; ++q) v[q] = __ldg(a.norm_in + ti[q]);
 #pragma unroll
       for (int q = 0; q < 8; ++q) acc = __dadd_rn(acc, v[q]);
     }
@@ -691,48 +661,12 @@ __device__ __forceinline__ void thread_row(const PrStepArgs& a, uint32_t r,
 #pragma unroll
     for (int q = 0; q < 8; ++q) ti[q] = k + q < len ? __ldg(t + k + q) : 0u;
 #pragma unroll
-    for (int q = 0; q < 8; ++q) v[q] = k + q < len ? ld_norm<HOT>(a, hot, ti[q]) : 0.0;
+    for (int q = 0; q < 8; ++q) v[q] = k + q < len ? __ldg(a.norm_in + ti[q]) : 0.0;
 #pragma unroll
     for (int q = 0; q < 8; ++q)
       if (k + q < len) acc = __dadd_rn(acc, v[q]);
   }
   finish_row(a, r, acc);
-}
-
-// Classes B and C with the hot columns in shared memory: one persistent
-// 768-thread CTA per SM copies norm_in of the hot nodes into shared memory
-// once per step; then every WARP claims work on its own (no CTA barriers:
-// the loads stay in flight across units), kHotChunk units per claim. A unit
-// is 4 class-B rows (8 lanes each) or 32 class-C rows (a thread each); the
-// class-B units come first (the longest rows start early). Claims, not a
-// static stride: CTAs on the SMs that class A holds start late and only take
-// what is left.
-constexpr uint32_t kHotChunk = 4;
-__global__ void __launch_bounds__(kHotThreads, 1) pr_step_hot_kernel(const PrStepArgs a,
-                                                                     uint32_t b_units,
-                                                                     uint32_t c_units,
-                                                                     unsigned* claim) {
-  extern __shared__ __align__(16) double hsm[];  // [kHotThreads/kBLanes * kBWin] windows, then hot
-  double* hot = hsm + kHotThreads / kBLanes * kBWin;
-  for (uint32_t k = threadIdx.x; k < a.nhot; k += kHotThreads) hot[k] = __ldg(a.norm_in + a.hot_ids[k]);
-  __syncthreads();
-  const int lane = threadIdx.x & 31;
-  double* win = hsm + (threadIdx.x / kBLanes) * kBWin;  // this lane group's window
-  const uint32_t total = b_units + c_units;
-  while (true) {
-    unsigned base = 0;
-    if (lane == 0) base = atomicAdd(claim, kHotChunk);
-    base = __shfl_sync(0xffffffffu, base, 0);
-    if (base >= total) break;
-    for (uint32_t u = base; u < base + kHotChunk && u < total; ++u) {
-      if (u < b_units) {
-        group_row<true>(a, a.nA + (int64_t)u * (32 / kBLanes) + lane / kBLanes, win, hot);
-      } else {
-        const uint64_t i = a.nB + (uint64_t)(u - b_units) * 32 + lane;
-        if (i < a.m) thread_row<true>(a, a.order[i], hot);
-      }
-    }
-  }
 }
 
 __global__ void __launch_bounds__(kPrWarps * 32) pr_step_kernel(const PrStepArgs a) {
@@ -798,118 +732,6 @@ unsigned long long read_flag(tg_ctx* ctx, unsigned long long* dflag) {
   return h;
 }
 
-// ---------------------------------------------------- K3 hot-column setup
-// The hot set is every node whose in-degree reaches a threshold T, the
-// smallest T that keeps it within kHotCols: a log2 histogram, then a linear
-// one inside the boundary bucket. Slot order is irrelevant to the results
-// (the shared-memory values are copies of norm_in).
-__global__ void indeg_log2_hist_kernel(const uint32_t* __restrict__ deg, uint64_t n,
-                                       unsigned* __restrict__ cnt) {
-  __shared__ unsigned h[32];
-  if (threadIdx.x < 32) h[threadIdx.x] = 0;
-  __syncthreads();
-  for (uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; j < n;
-       j += (uint64_t)gridDim.x * blockDim.x) {
-    const uint32_t d = deg[j];
-    if (d) atomicAdd(&h[31 - __clz(d)], 1u);
-  }
-  __syncthreads();
-  if (threadIdx.x < 32 && h[threadIdx.x]) atomicAdd(&cnt[threadIdx.x], h[threadIdx.x]);
-}
-__global__ void indeg_lin_hist_kernel(const uint32_t* __restrict__ deg, uint64_t n, uint32_t lo,
-                                      uint32_t shift, uint32_t nbins, unsigned* __restrict__ cnt) {
-  for (uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; j < n;
-       j += (uint64_t)gridDim.x * blockDim.x) {
-    const uint32_t d = deg[j];
-    if (d >= lo && d - lo < (nbins << shift)) atomicAdd(&cnt[(d - lo) >> shift], 1u);
-  }
-}
-__global__ void hot_select_kernel(const uint32_t* __restrict__ deg, uint64_t n, uint32_t T,
-                                  uint32_t* __restrict__ hot_ids, uint32_t* __restrict__ slot_of,
-                                  unsigned* __restrict__ cnt) {
-  for (uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; j < n;
-       j += (uint64_t)gridDim.x * blockDim.x) {
-    if (deg[j] >= T) {
-      const unsigned sl = atomicAdd(cnt, 1u);
-      hot_ids[sl] = static_cast<uint32_t>(j);
-      slot_of[j] = sl;
-    }
-  }
-}
-__global__ void tag_targets_kernel(const uint32_t* __restrict__ tgt, uint64_t e,
-                                   const uint32_t* __restrict__ slot_of, uint32_t* __restrict__ out) {
-  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < e;
-       i += (uint64_t)gridDim.x * blockDim.x) {
-    const uint32_t t = tgt[i];
-    const uint32_t sl = slot_of[t];
-    out[i] = sl != 0xffffffffu ? (kHotTag | sl) : t;
-  }
-}
-
-bool hot_columns_enabled() {
-  const char* v = std::getenv("TIERGRAPH_PR_HOT_COLUMNS");
-  return !(v && v[0] == '0');
-}
-
-// Builds g->tgt_tag / hot_ids / nhot (needs g->indeg). No-op for n >= 2^31,
-// an edgeless graph, or TIERGRAPH_PR_HOT_COLUMNS=0.
-void build_hot_columns(tg_ctx* ctx, tg_graph* g) {
-  const uint64_t n = g->n, e = g->e;
-  if (n == 0 || e == 0 || n >= (uint64_t)kHotTag || !hot_columns_enabled()) return;
-  auto* cnt = ctx->scratch_t<unsigned>(kSmall, 4096 + 1);
-  TGB_CUDA(cudaMemsetAsync(cnt, 0, 32 * 4, ctx->stream));
-  indeg_log2_hist_kernel<<<grid_for(n, 256), 256, 0, ctx->stream>>>(g->indeg, n, cnt);
-  TGB_LAUNCHED();
-  unsigned h[32];
-  TGB_CUDA(cudaMemcpyAsync(h, cnt, sizeof(h), cudaMemcpyDeviceToHost, ctx->stream));
-  ctx->sync();
-  uint64_t cum = 0;
-  uint32_t T = 1;
-  int B = -1;
-  for (int b = 31; b >= 0; --b) {
-    if (cum + h[b] <= kHotCols) {
-      cum += h[b];
-      if (h[b]) T = 1u << b;
-    } else {
-      B = b;
-      break;
-    }
-  }
-  if (B >= 0) {  // refine inside [2^B, 2^(B+1))
-    const uint32_t lo = 1u << B;
-    const uint32_t nb = std::min<uint32_t>(lo, 4096);
-    uint32_t shift = 0;
-    while ((nb << shift) < lo) ++shift;
-    TGB_CUDA(cudaMemsetAsync(cnt, 0, nb * 4, ctx->stream));
-    indeg_lin_hist_kernel<<<grid_for(n, 256), 256, 0, ctx->stream>>>(g->indeg, n, lo, shift, nb, cnt);
-    TGB_LAUNCHED();
-    std::vector<unsigned> h2(nb);
-    TGB_CUDA(cudaMemcpyAsync(h2.data(), cnt, nb * 4, cudaMemcpyDeviceToHost, ctx->stream));
-    ctx->sync();
-    T = lo << 1;
-    for (int b = static_cast<int>(nb) - 1; b >= 0; --b) {
-      if (cum + h2[b] > kHotCols) break;
-      cum += h2[b];
-      T = lo + (static_cast<uint32_t>(b) << shift);
-    }
-  }
-  if (cum == 0) return;
-  uint32_t* slot_of = nullptr;
-  TGB_CUDA(cudaMalloc(&g->hot_ids, sizeof(uint32_t) * cum));
-  TGB_CUDA(cudaMalloc(&g->tgt_tag, sizeof(uint32_t) * e));
-  TGB_CUDA(cudaMalloc(&slot_of, sizeof(uint32_t) * n));
-  TGB_CUDA(cudaMemsetAsync(slot_of, 0xff, sizeof(uint32_t) * n, ctx->stream));
-  TGB_CUDA(cudaMemsetAsync(cnt, 0, 4, ctx->stream));
-  hot_select_kernel<<<grid_for(n, 256), 256, 0, ctx->stream>>>(g->indeg, n, T, g->hot_ids, slot_of,
-                                                               cnt);
-  TGB_LAUNCHED();
-  tag_targets_kernel<<<grid_for(e, 256), 256, 0, ctx->stream>>>(g->tgt, e, slot_of, g->tgt_tag);
-  TGB_LAUNCHED();
-  ctx->sync();
-  cudaFree(slot_of);
-  g->nhot = static_cast<uint32_t>(cum);
-}
-
 void compute_indeg(tg_ctx* ctx, const tg_graph* g, uint32_t* deg) {
   TGB_CUDA(cudaMemsetAsync(deg, 0, sizeof(uint32_t) * std::max<uint64_t>(g->n, 1), ctx->stream));
   if (g->e == 0) return;
@@ -969,9 +791,6 @@ void pagerank_step(tg_ctx* ctx, const tg_graph* g, const uint32_t* deg, double d
   PrStepArgs a;
   a.off = g->off;
   a.tgt = g->tgt;
-  a.tgt_bc = g->tgt_tag ? g->tgt_tag : g->tgt;
-  a.hot_ids = g->hot_ids;
-  a.nhot = g->tgt_tag ? g->nhot : 0;
   a.deg = deg;
   a.norm_in = nin;
   a.norm_out = nout;
@@ -1016,23 +835,7 @@ void pagerank_step(tg_ctx* ctx, const tg_graph* g, const uint32_t* deg, double d
     }
   }
   const unsigned grid = static_cast<unsigned>(a.b_ctas + c_ctas);
-  if (grid && g->tgt_tag) {
-    constexpr uint32_t kRowsB = 32 / kBLanes;  // class-B rows per warp unit
-    const uint32_t bu = (sc.nB - sc.nA + kRowsB - 1) / kRowsB;
-    const uint32_t cu = static_cast<uint32_t>((a.m - sc.nB + 31) / 32);
-    const int smem = (kHotThreads / kBLanes * kBWin + kHotCols) * 8;
-    static bool hattr[TG_MAX_DEVICES] = {};
-    if (!hattr[ctx->device % TG_MAX_DEVICES]) {
-      TGB_CUDA(cudaFuncSetAttribute(pr_step_hot_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    smem));
-      hattr[ctx->device % TG_MAX_DEVICES] = true;
-    }
-    const unsigned pg = std::min<unsigned>(ctx->num_sms, (bu + cu + 23) / 24);
-    auto* claim = ctx->scratch_t<unsigned>(kClaim, 1);
-    TGB_CUDA(cudaMemsetAsync(claim, 0, 4, ctx->stream));
-    pr_step_hot_kernel<<<pg, kHotThreads, smem, ctx->stream>>>(a, bu, cu, claim);
-    TGB_LAUNCHED();
-  } else if (grid) {
+  if (grid) {
     // classes B (first CTAs: long chains start early) and C in one grid
     pr_step_kernel<<<grid, kPrWarps * 32, 0, ctx->stream>>>(a);
     TGB_LAUNCHED();
@@ -1105,7 +908,6 @@ void graph_from_device(tg_ctx* ctx, const uint64_t* doff, uint32_t* tgt, uint64_
     TGB_CUDA(cudaMalloc(&g->indeg, sizeof(uint32_t) * std::max<uint64_t>(n, 1)));
     compute_indeg(ctx, g, g->indeg);
     ctx->sync();
-    build_hot_columns(ctx, g);
   } catch (...) {
     tg_graph_destroy(g);
     throw;
@@ -1190,15 +992,12 @@ int tg_graph_destroy(tg_graph* g) {
   cudaFree(g->tgt);
   for (auto& sc : g->scheds) cudaFree(sc.order);
   cudaFree(g->indeg);
-  cudaFree(g->tgt_tag);
-  cudaFree(g->hot_ids);
   delete g;
   return TG_OK;
 }
 
 uint64_t tg_graph_num_nodes(const tg_graph* g) { return g ? g->n : 0; }
 uint64_t tg_graph_num_edges(const tg_graph* g) { return g ? g->e : 0; }
-uint32_t tg_graph_hot_columns(const tg_graph* g) { return g && g->tgt_tag ? g->nhot : 0; }
 const uint32_t* tg_graph_offsets32(const tg_graph* g) { return g ? g->off : nullptr; }
 const uint32_t* tg_graph_targets32(const tg_graph* g) { return g ? g->tgt : nullptr; }
 

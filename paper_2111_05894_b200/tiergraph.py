@@ -173,10 +173,6 @@ class DeviceCsrGraph:
     def num_edges(self) -> int:
         return int(LIB.tg_graph_num_edges(self._h))
 
-    def hot_columns(self, ctx: "Context" = None) -> int:
-        """K3 hot columns held in shared memory (tg_graph_hot_columns)."""
-        return int(LIB.tg_graph_hot_columns(self._h))
-
     def device(self, ctx: "Context"):
         if ctx is not self._ctx:
             raise DomainError("this graph lives on another context")
@@ -236,10 +232,6 @@ class CsrGraph:
                                        self.num_nodes(), self.num_edges(), C.byref(h)))
             self._dev[key] = (ctx, h)
         return self._dev[key][1]
-
-    def hot_columns(self, ctx: Context = None) -> int:
-        """K3 hot columns of this graph's device copy (tg_graph_hot_columns)."""
-        return int(LIB.tg_graph_hot_columns(self.device(_ctx(ctx))))
 
     def release(self):
         for ctx, h in self._dev.values():

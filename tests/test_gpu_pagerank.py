@@ -175,36 +175,6 @@ def test_rmat_c1_scale_bit_exact_and_hot_set(tg, ctx):
     assert np.array_equal(perm.new_id_of, port.permutation_from_scores(want))
 
 
-@pytest.mark.parametrize("n,draws", [(3000, 40000), (200_000, 3_000_000), (60_000, 60_000)])
-def test_hot_columns_bit_exact(tg, ctx, monkeypatch, n, draws):
-    """K3 hot columns (classes B/C read the highest in-degree nodes' values
-    from shared memory): bit-identical to the reference and to the same run
-    with them disabled. Cases: every node hot (n < 16384), a skewed R-MAT
-    with the threshold inside a log2 bucket, and a flat graph (many nodes
-    tie at the threshold, so fewer than 16384 are taken)."""
-    from paper_2111_05894_b200 import synth
-    off, tgt = synth.rmat_graph(n, draws, seed=n)
-    port = oracle.port()
-    tid = port.draw_random_train_ids(n, max(1, n // 10), 3)
-    want = checker().weighted_reverse_pagerank(off, tgt, tid)
-    g_on = G(tg, off, tgt)
-    nhot = g_on.hot_columns(ctx)
-    assert 0 < nhot <= 16384
-    got = tg.weighted_reverse_pagerank(g_on, tg.PagerankConfig(), tg.TrainIdSet(tid), ctx=ctx)
-    assert got.tobytes() == want.tobytes()
-    monkeypatch.setenv("TIERGRAPH_PR_HOT_COLUMNS", "0")
-    g_off = G(tg, off, tgt)
-    assert g_off.hot_columns(ctx) == 0
-    got0 = tg.weighted_reverse_pagerank(g_off, tg.PagerankConfig(), tg.TrainIdSet(tid), ctx=ctx)
-    assert got0.tobytes() == want.tobytes()
-    deg = np.bincount(tgt.astype(np.int64), minlength=n)
-    if np.count_nonzero(deg) <= 16384:
-        assert nhot == np.count_nonzero(deg)
-    else:  # the threshold keeps every node at or above it, and no more than 16384
-        srt = np.sort(deg)[::-1]
-        assert srt[nhot - 1] > srt[nhot] or nhot == np.count_nonzero(deg)
-
-
 def test_hub_rows_with_tie_prone_addends(tg, ctx):
     """Hub rows (> 2048 edges, the parallel exact-chain path) whose addends are
     all equal or few-valued, so the running sum hits round-half-even ties and
