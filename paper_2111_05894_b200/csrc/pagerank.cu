@@ -21,6 +21,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <string>
 #include <vector>
 
@@ -569,6 +570,9 @@ __global__ void __launch_bounds__(W * 32) pr_hub_kernel(const PrStepArgs a, uint
 // first lane adds each window in storage order — 4 chains per warp.
 constexpr int kBLanes = 8;
 constexpr int kBWin = kBLanes * 8;  // 64 edges per window
+// a group's window buffer stride: one double of padding puts the four chain
+// lanes of a warp (one per group) on different banks (ncu: 4-way conflicts)
+constexpr int kBStride = kBWin + 1;
 __device__ __forceinline__ void group_row(const PrStepArgs& a, int64_t i, double* buf) {
   const int lane = threadIdx.x & 31, sl = lane & (kBLanes - 1);
   const bool has = i < static_cast<int64_t>(a.nB);
@@ -670,11 +674,11 @@ __device__ __forceinline__ void thread_row(const PrStepArgs& a, uint32_t r) {
 }
 
 __global__ void __launch_bounds__(kPrWarps * 32) pr_step_kernel(const PrStepArgs a) {
-  __shared__ __align__(16) double smem[kPrWarps * 32 / kBLanes * kBWin];  // 16 KB: class B windows
+  __shared__ __align__(16) double smem[kPrWarps * 32 / kBLanes * kBStride];  // 16.6 KB: class B windows
   if (blockIdx.x < a.b_ctas) {
     const int g = threadIdx.x / kBLanes;  // row group within the CTA
     const int64_t i = a.nA + (int64_t)blockIdx.x * (kPrWarps * 32 / kBLanes) + g;
-    group_row(a, i, smem + g * kBWin);
+    group_row(a, i, smem + g * kBStride);
   } else {
     const uint64_t i = a.nB + (uint64_t)(blockIdx.x - a.b_ctas) * blockDim.x + threadIdx.x;
     if (i < a.m) thread_row(a, a.order[i]);
