@@ -22,6 +22,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -351,6 +352,14 @@ struct tg_sampler {
   uint32_t* small = nullptr;  // counters
   uint32_t* blk = nullptr;    // compaction block counts
   uint32_t stamp = 0;
+  // the stream this sampler state works on: the context's, or a lane's own
+  cudaStream_t stream = nullptr;
+  // tg_sample_batches lanes: independent sampler states (stamps, member
+  // bits, frontiers) on their own streams, so consecutive minibatches expand
+  // concurrently; lane 0 is this object. Created on first use.
+  std::vector<tg_sampler*> lanes;
+  bool is_lane = false;
+  cudaEvent_t ev = nullptr;  // lane: its last batch's compaction is done
 };
 
 namespace {
@@ -366,15 +375,36 @@ void ensure(uint32_t** p, uint64_t* cap, uint64_t want) {
 
 uint32_t next_stamp(tg_sampler* s) {
   if (s->stamp >= 0xFFFFFFF0u) {  // wrap: forget every old stamp
-    TGB_CUDA(cudaMemsetAsync(s->layer_mark, 0, 4 * s->n, s->ctx->stream));
+    TGB_CUDA(cudaMemsetAsync(s->layer_mark, 0, 4 * s->n, s->stream));
     s->stamp = 0;
   }
   return ++s->stamp;
 }
 
+// Concurrent sampler states for tg_sample_batches (TIERGRAPH_SAMPLER_LANES,
+// default 4).
+uint32_t sampler_lanes() {
+  const char* v = std::getenv("TIERGRAPH_SAMPLER_LANES");
+  const int n = v ? std::atoi(v) : 4;
+  return static_cast<uint32_t>(std::max(1, std::min(n, 16)));
+}
+
+// Per-state device buffers (layer stamps, member bits, counters).
+void sampler_alloc(tg_sampler* s) {
+  TGB_CUDA(cudaMalloc(&s->layer_mark, 4 * std::max<uint64_t>(s->n, 1)));
+  s->nwords = std::max<uint64_t>((s->n + 31) / 32, 1);
+  TGB_CUDA(cudaMalloc(&s->member_bits, 4 * s->nwords));
+  TGB_CUDA(cudaMemsetAsync(s->layer_mark, 0, 4 * std::max<uint64_t>(s->n, 1), s->stream));
+  TGB_CUDA(cudaMemsetAsync(s->member_bits, 0, 4 * s->nwords, s->stream));
+  TGB_CUDA(cudaMalloc(&s->small, 256));
+  const uint64_t nblk = (s->nwords + kCompactBlock - 1) / kCompactBlock;
+  TGB_CUDA(cudaMalloc(&s->blk, 4 * std::max<uint64_t>(nblk, 1)));
+}
+
 }  // namespace
 
 extern "C" {
+int tg_sampler_destroy(tg_sampler* s);
 
 int tg_sampler_create(tg_ctx* ctx, const tg_graph* gt, tg_sampler** out) {
   return guard([&] {
@@ -382,18 +412,12 @@ int tg_sampler_create(tg_ctx* ctx, const tg_graph* gt, tg_sampler** out) {
     DeviceGuard dg(ctx->device);
     auto* s = new tg_sampler;
     s->ctx = ctx;
+    s->stream = ctx->stream;
     s->n = tg_graph_num_nodes(gt);
     s->off = tg_graph_offsets32(gt);
     s->tgt = tg_graph_targets32(gt);
     try {
-      TGB_CUDA(cudaMalloc(&s->layer_mark, 4 * std::max<uint64_t>(s->n, 1)));
-      s->nwords = std::max<uint64_t>((s->n + 31) / 32, 1);
-      TGB_CUDA(cudaMalloc(&s->member_bits, 4 * s->nwords));
-      TGB_CUDA(cudaMemsetAsync(s->layer_mark, 0, 4 * std::max<uint64_t>(s->n, 1), ctx->stream));
-      TGB_CUDA(cudaMemsetAsync(s->member_bits, 0, 4 * s->nwords, ctx->stream));
-      TGB_CUDA(cudaMalloc(&s->small, 256));
-      const uint64_t nblk = (s->nwords + kCompactBlock - 1) / kCompactBlock;
-      TGB_CUDA(cudaMalloc(&s->blk, 4 * std::max<uint64_t>(nblk, 1)));
+      sampler_alloc(s);
     } catch (...) {
       tg_sampler_destroy(s);
       throw;
@@ -405,7 +429,10 @@ int tg_sampler_create(tg_ctx* ctx, const tg_graph* gt, tg_sampler** out) {
 int tg_sampler_destroy(tg_sampler* s) {
   if (!s) return TG_OK;
   DeviceGuard dg(s->ctx->device);
-  cudaStreamSynchronize(s->ctx->stream);
+  cudaStreamSynchronize(s->stream);
+  for (tg_sampler* l : s->lanes) tg_sampler_destroy(l);
+  if (s->is_lane) cudaStreamDestroy(s->stream);
+  if (s->ev) cudaEventDestroy(s->ev);
   cudaFree(s->layer_mark);
   cudaFree(s->member_bits);
   cudaFree(s->buf[0]);
@@ -458,12 +485,12 @@ uint64_t expand(tg_sampler* s, const uint64_t* sd, uint64_t ns, const uint32_t* 
   uint32_t* cnt = s->small;
   auto* bad = reinterpret_cast<unsigned long long*>(s->small + kSmallBad);
   auto* raw_n = reinterpret_cast<unsigned long long*>(s->small + kSmallRaw);
-  TGB_CUDA(cudaMemsetAsync(cnt, 0, 4 * 10, ctx->stream));
-  TGB_CUDA(cudaMemsetAsync(bad, 0xff, 8, ctx->stream));
-  TGB_CUDA(cudaMemsetAsync(raw_n, 0, 8, ctx->stream));
-  TGB_CUDA(cudaMemsetAsync(s->member_bits, 0, 4 * s->nwords, ctx->stream));
+  TGB_CUDA(cudaMemsetAsync(cnt, 0, 4 * 10, s->stream));
+  TGB_CUDA(cudaMemsetAsync(bad, 0xff, 8, s->stream));
+  TGB_CUDA(cudaMemsetAsync(raw_n, 0, 8, s->stream));
+  TGB_CUDA(cudaMemsetAsync(s->member_bits, 0, 4 * s->nwords, s->stream));
   uint32_t lstamp = next_stamp(s);
-  seed_kernel<<<grid_for(ns, 256), 256, 0, ctx->stream>>>(sd, ns, n, s->layer_mark, lstamp,
+  seed_kernel<<<grid_for(ns, 256), 256, 0, s->stream>>>(sd, ns, n, s->layer_mark, lstamp,
                                                          s->member_bits, s->buf[0], cnt, bad,
                                                          o.counts, o.count_raw, o.raw, raw_n,
                                                          o.raw_cap);
@@ -481,8 +508,8 @@ uint64_t expand(tg_sampler* s, const uint64_t* sd, uint64_t ns, const uint32_t* 
       // a huge bound (wide fanouts on a big graph): size the picks by the
       // actual frontier instead (one host round trip)
       uint32_t hf = 0;
-      TGB_CUDA(cudaMemcpyAsync(&hf, cnt + layer, 4, cudaMemcpyDeviceToHost, ctx->stream));
-      ctx->sync();
+      TGB_CUDA(cudaMemcpyAsync(&hf, cnt + layer, 4, cudaMemcpyDeviceToHost, s->stream));
+      TGB_CUDA(cudaStreamSynchronize(s->stream));
       f = hf;
     }
     ensure(&s->picks, &s->picks_cap, std::max<uint64_t>(f * k, 1));
@@ -490,7 +517,7 @@ uint64_t expand(tg_sampler* s, const uint64_t* sd, uint64_t ns, const uint32_t* 
     SampleArgs a{s->off, s->tgt, s->buf[cur], cnt + layer, k, key, s->picks, s->layer_mark, lstamp,
                  s->member_bits, s->buf[cur ^ 1], cnt + layer + 1, o.counts, o.count_raw, o.raw,
                  raw_n, o.raw_cap};
-    sample_layer_kernel<<<grid_for(f, 256, ctx->num_sms * 16), 256, 0, ctx->stream>>>(a);
+    sample_layer_kernel<<<grid_for(f, 256, ctx->num_sms * 16), 256, 0, s->stream>>>(a);
     TGB_LAUNCHED();
     f = std::min<uint64_t>(n, f * k);
     members += f;
@@ -505,12 +532,12 @@ void compact_members(tg_sampler* s, uint64_t* out_dev, const uint64_t* out_base 
                      uint64_t cap = ~0ull) {
   tg_ctx* ctx = s->ctx;
   const uint64_t nblk = (s->nwords + kCompactBlock - 1) / kCompactBlock;
-  member_count_kernel<<<nblk, kCompactBlock, 0, ctx->stream>>>(s->member_bits, s->nwords, s->blk);
+  member_count_kernel<<<nblk, kCompactBlock, 0, s->stream>>>(s->member_bits, s->nwords, s->blk);
   TGB_LAUNCHED();
-  count_prefix_kernel<<<1, 1024, 0, ctx->stream>>>(s->blk, static_cast<uint32_t>(nblk),
+  count_prefix_kernel<<<1, 1024, 0, s->stream>>>(s->blk, static_cast<uint32_t>(nblk),
                                                    s->small + kSmallTotal);
   TGB_LAUNCHED();
-  member_write_kernel<<<nblk, kCompactBlock, 0, ctx->stream>>>(s->member_bits, s->nwords, s->blk,
+  member_write_kernel<<<nblk, kCompactBlock, 0, s->stream>>>(s->member_bits, s->nwords, s->blk,
                                                                out_dev, out_base, cap);
   TGB_LAUNCHED();
 }
@@ -522,8 +549,8 @@ struct SmallOut {
 
 SmallOut read_small(tg_sampler* s) {
   uint32_t h[16];
-  TGB_CUDA(cudaMemcpyAsync(h, s->small, sizeof(h), cudaMemcpyDeviceToHost, s->ctx->stream));
-  s->ctx->sync();
+  TGB_CUDA(cudaMemcpyAsync(h, s->small, sizeof(h), cudaMemcpyDeviceToHost, s->stream));
+  TGB_CUDA(cudaStreamSynchronize(s->stream));
   SmallOut r;
   r.total = h[kSmallTotal];
   std::memcpy(&r.bad, h + kSmallBad, 8);
@@ -619,18 +646,46 @@ int tg_sample_batches(tg_sampler* s, const uint64_t* order, uint64_t n_order, ui
     uint64_t* md = out_members;
     const bool host_out = !is_device_ptr(out_members);
     if (host_out) md = ctx->scratch_t<uint64_t>(kScratchA, std::max<uint64_t>(cap, 1));
+    // Lanes: batch k expands on lane k % L, each lane a sampler state on its
+    // own stream, so L minibatches expand at once (one expansion is a chain
+    // of small latency-bound kernels). The compactions stay in batch order:
+    // batch k's waits for batch k-1's (its output offset is k-1's end).
+    const uint32_t L = static_cast<uint32_t>(std::min<uint64_t>(sampler_lanes(), std::max<uint64_t>(nbatches, 1)));
+    while (s->lanes.size() + 1 < L) {
+      auto* l = new tg_sampler;
+      l->ctx = ctx;
+      l->n = s->n;
+      l->off = s->off;
+      l->tgt = s->tgt;
+      l->is_lane = true;
+      s->lanes.push_back(l);
+      TGB_CUDA(cudaStreamCreateWithFlags(&l->stream, cudaStreamNonBlocking));
+      TGB_CUDA(cudaEventCreateWithFlags(&l->ev, cudaEventDisableTiming));
+      sampler_alloc(l);
+    }
+    if (!s->ev) TGB_CUDA(cudaEventCreateWithFlags(&s->ev, cudaEventDisableTiming));
+    auto lane = [&](uint64_t k) { return k % L == 0 ? s : s->lanes[k % L - 1]; };
+    // inputs ready (order, offsets[0]) before any lane starts
+    TGB_CUDA(cudaEventRecord(s->ev, ctx->stream));
+    for (uint32_t i = 1; i < L; ++i) TGB_CUDA(cudaStreamWaitEvent(s->lanes[i - 1]->stream, s->ev, 0));
     for (uint64_t k = 0; k < nbatches; ++k) {
+      tg_sampler* ls = lane(k);
       const uint64_t b = first_batch + k;
       const uint64_t beg = b * batch_size, len = std::min(batch_size, n_order - beg);
-      expand(s, od + beg, len, fanouts, nf, rng_seed, epoch, b, ExpandOut{});
-      compact_members(s, md, offs.dev() + k, cap);
-      advance_offset_kernel<<<1, 32, 0, ctx->stream>>>(s->small + kSmallTotal, offs.dev(), k);
+      expand(ls, od + beg, len, fanouts, nf, rng_seed, epoch, b, ExpandOut{});
+      if (k > 0 && L > 1) TGB_CUDA(cudaStreamWaitEvent(ls->stream, lane(k - 1)->ev, 0));
+      compact_members(ls, md, offs.dev() + k, cap);
+      advance_offset_kernel<<<1, 32, 0, ls->stream>>>(ls->small + kSmallTotal, offs.dev(), k);
       TGB_LAUNCHED();
+      if (L > 1) TGB_CUDA(cudaEventRecord(ls->ev, ls->stream));
     }
+    for (uint32_t i = 1; i < L; ++i) TGB_CUDA(cudaStreamWaitEvent(ctx->stream, s->lanes[i - 1]->ev, 0));
     uint64_t total = 0;
     TGB_CUDA(cudaMemcpyAsync(&total, offs.dev() + nbatches, 8, cudaMemcpyDeviceToHost, ctx->stream));
-    const SmallOut r = read_small(s);  // syncs
-    if (r.bad != ~0ull) domain_error("seed out of range in the batch order");
+    bool bad = false;
+    for (uint32_t i = 0; i < L; ++i) bad |= read_small(i ? s->lanes[i - 1] : s).bad != ~0ull;
+    ctx->sync();
+    if (bad) domain_error("seed out of range in the batch order");
     if (total > cap)
       domain_error("tg_sample_batches: " + std::to_string(total) +
                    " members exceed the output capacity " + std::to_string(cap));

@@ -119,11 +119,16 @@ def test_raw_draws_multiset(tg, ctx):
     assert np.array_equal(counts, want)
 
 
+@pytest.mark.parametrize("lanes", ["1", "3", None, "7"])
 @pytest.mark.parametrize("fanouts", [[10, 15], [15, 10, 5], [100, 3]])
-def test_sample_batches_back_to_back(tg, ctx, fanouts):
+def test_sample_batches_back_to_back(tg, ctx, monkeypatch, fanouts, lanes):
     """tg_sample_batches (one host round trip for many minibatches) gives the
-    reference's epoch lists, from any first batch, incl. a short last batch."""
+    reference's epoch lists, from any first batch, incl. a short last batch,
+    with any number of concurrent sampler lanes (TIERGRAPH_SAMPLER_LANES;
+    default 4): batch k expands on lane k % L, compactions stay in order."""
     from paper_2111_05894_b200 import producers
+    if lanes is not None:
+        monkeypatch.setenv("TIERGRAPH_SAMPLER_LANES", lanes)
     chk = checker()
     n = 6000
     off, tgt = _graph(n, 7, hubs=[(0, 3000), (9, 400)])
@@ -136,5 +141,8 @@ def test_sample_batches_back_to_back(tg, ctx, fanouts):
     assert len(got) == 16 and all(np.array_equal(a, b) for a, b in zip(got, want))
     mid = s.batches(order, fanouts, 64, 11, 2, first_batch=5, nbatches=4)
     assert all(np.array_equal(a, b) for a, b in zip(mid, want[5:9]))
+    md, offs = s.batches(order, fanouts, 64, 11, 2, device=True)  # left in HBM
+    allm = md[:int(offs[-1])].cpu().numpy().view(np.uint64)
+    assert all(np.array_equal(allm[int(offs[k]):int(offs[k + 1])], want[k]) for k in range(16))
     with pytest.raises(tg.DomainError, match="exceed"):
         s.batches(order, fanouts, 64, 11, 2, first_batch=15, nbatches=2)
