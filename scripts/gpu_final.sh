@@ -23,4 +23,7 @@ timeout 1800 python bench.py --config c3 --steps 100 --warmup 5 > $O/bench_c3.js
 timeout 1500 ncu --set full --clock-control none --import-source on -k regex:gather_bulk -s 5 -c 2 \
    -o $O/gather_c3 python bench.py --config c3 --steps 10 --warmup 3 --no-cpu-baseline > $O/ncu_gather_c3.log 2>&1
 timeout 2400 python bench.py --config c4 --steps 100 --warmup 5 > $O/bench_c4.json 2> $O/bench_c4.err
+timeout 600 python -m pytest tests/test_distributed.py -x -q -m gpu > $O/pytest_distributed.log 2>&1; echo "rc=$?" >> $O/pytest_distributed.log
+TG_BENCH_SHARE_GPU=1 timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 29511 bench.py --gpus 2 --config c1 --steps 20 --warmup 3 > $O/bench_c1_2ranks_shared_gpu.json 2> $O/bench_c1_2ranks_shared_gpu.err
+echo "rc=$?" >> $O/bench_c1_2ranks_shared_gpu.err
 ls -la $O
