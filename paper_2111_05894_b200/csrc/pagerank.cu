@@ -371,7 +371,10 @@ struct HubShared {
 
 // Class A: one CTA per row longer than kLenA.
 template <int W, int T>
-__global__ void __launch_bounds__(W * 32) pr_hub_kernel(const PrStepArgs a, uint32_t row0) {
+// at most 80 registers: a 512-thread class-A CTA (16 warps x 2,560 registers)
+// then leaves room on its SM for one class-B/C CTA (8 x 2,560), which 90
+// registers (3,072 per warp) did not
+__global__ void __maxnreg__(80) pr_hub_kernel(const PrStepArgs a, uint32_t row0) {
   constexpr int kHubWarps = W;
   constexpr int kHubThreads = W * 32;
   constexpr int kHubT = T;
