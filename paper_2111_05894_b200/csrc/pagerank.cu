@@ -91,12 +91,12 @@ __global__ void narrow_targets_kernel(const uint64_t* __restrict__ in, uint32_t*
 // Class boundaries of a length-sorted schedule (one thread; binary search).
 __global__ void class_bounds_kernel(const uint32_t* __restrict__ off,
                                     const uint32_t* __restrict__ order, uint64_t m,
-                                    uint32_t* __restrict__ out) {
+                                    uint32_t len_a, uint32_t len_b, uint32_t* __restrict__ out) {
   if (threadIdx.x != 0 || blockIdx.x != 0) return;
   // 512-thread class-A CTAs only for the few rows that set the critical
   // path: longer than kHubLong AND than a quarter of the longest row
   const uint32_t longest = m ? off[order[0] + 1] - off[order[0]] : 0u;
-  const uint32_t lim[3] = {kLenA, kLenB, max(kHubLong, longest / 4)};
+  const uint32_t lim[3] = {len_a, len_b, max(max(kHubLong, len_a), longest / 4)};
   for (int c = 0; c < 3; ++c) {  // first index whose length is <= lim[c]
     uint64_t lo = 0, hi = m;
     while (lo < hi) {
@@ -777,7 +777,13 @@ const tg_graph::Sched& schedule(tg_ctx* ctx, const tg_graph* g, uint64_t rb, uin
   TGB_CUDA(cudaMalloc(&sc.order, sizeof(uint32_t) * std::max<uint64_t>(re - rb, 1) + 16));
   sort_rows_by_length(ctx, g->off, rb, re, sc.order);
   uint32_t* bounds = sc.order + std::max<uint64_t>(re - rb, 1);
-  class_bounds_kernel<<<1, 32, 0, ctx->stream>>>(g->off, sc.order, re - rb, bounds);
+  // TIERGRAPH_PR_LENA / _LENB override the class boundaries (experiments)
+  const char* ea = std::getenv("TIERGRAPH_PR_LENA");
+  const char* eb = std::getenv("TIERGRAPH_PR_LENB");
+  const uint32_t la = ea ? static_cast<uint32_t>(std::atoi(ea)) : kLenA;
+  const uint32_t lbn = eb ? static_cast<uint32_t>(std::atoi(eb)) : kLenB;
+  class_bounds_kernel<<<1, 32, 0, ctx->stream>>>(g->off, sc.order, re - rb, la, std::min(lbn, la),
+                                                 bounds);
   TGB_LAUNCHED();
   uint32_t hb[3];
   TGB_CUDA(cudaMemcpyAsync(hb, bounds, sizeof(hb), cudaMemcpyDeviceToHost, ctx->stream));
