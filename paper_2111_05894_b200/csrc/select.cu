@@ -144,7 +144,10 @@ __global__ void __launch_bounds__(1024) count_scan_kernel(uint32_t* __restrict__
 }
 
 // Stable block-local ranking (warp rounds in index order + per-warp digit
-// counters), then scatter to the scanned global offsets.
+// counters). The tile is then reordered by digit in shared memory and written
+// out in that order, so consecutive threads store consecutive positions of a
+// digit's run (coalesced) instead of 32 unrelated runs per store.
+constexpr int kRsScatterSmem = kRsTile * (8 + 4);  // staged keys + values
 __global__ void __launch_bounds__(kRsWarps * 32) scatter_kernel(
     uint64_t* __restrict__ k0, uint32_t* __restrict__ v0, uint64_t* __restrict__ k1,
     uint32_t* __restrict__ v1, uint64_t n, int pass, const RadixPlan* __restrict__ plan,
@@ -155,8 +158,12 @@ __global__ void __launch_bounds__(kRsWarps * 32) scatter_kernel(
   const uint32_t* vin = from1 ? v1 : v0;
   uint64_t* kout = from1 ? k0 : k1;
   uint32_t* vout = from1 ? v0 : v1;
+  extern __shared__ __align__(16) uint8_t rs_smem[];
+  uint64_t* skey = reinterpret_cast<uint64_t*>(rs_smem);
+  uint32_t* sval = reinterpret_cast<uint32_t*>(rs_smem + kRsTile * 8);
   __shared__ uint32_t wcnt[kRsWarps][256];
   __shared__ uint32_t doff[256];
+  __shared__ uint32_t tstart[256];
   for (int i = threadIdx.x; i < kRsWarps * 256; i += blockDim.x) (&wcnt[0][0])[i] = 0;
   {  // digit base (exclusive scan of the 256 totals) + this block's column prefix
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
@@ -210,6 +217,19 @@ __global__ void __launch_bounds__(kRsWarps * 32) scatter_kernel(
       wcnt[ww][d] = run;
       run += c;
     }
+    // the digit's start within the tile: exclusive scan of the tile totals
+    uint32_t incl = run;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += y;
+    }
+    __shared__ uint32_t st[kRsWarps];
+    if (lane == 31) st[w] = incl;
+    __syncthreads();
+    uint32_t before = 0;
+    for (int k = 0; k < w; ++k) before += st[k];
+    tstart[d] = before + incl - run;
   }
   __syncthreads();
 #pragma unroll
@@ -217,11 +237,35 @@ __global__ void __launch_bounds__(kRsWarps * 32) scatter_kernel(
     const uint64_t i = base + k * 32 + lane;
     if (i < n) {
       const uint32_t d = static_cast<uint32_t>((key[k] >> shift) & 0xff);
-      const uint32_t pos = doff[d] + wcnt[w][d] + rank[k];
-      kout[pos] = key[k];
-      vout[pos] = val[k];
+      const uint32_t lp = tstart[d] + wcnt[w][d] + rank[k];
+      skey[lp] = key[k];
+      sval[lp] = val[k];
     }
   }
+  __syncthreads();
+  const uint64_t t0 = (uint64_t)blockIdx.x * kRsTile;
+  const uint32_t tn = static_cast<uint32_t>(n - t0 < (uint64_t)kRsTile ? n - t0 : kRsTile);
+  for (uint32_t j = threadIdx.x; j < tn; j += blockDim.x) {
+    const uint64_t kk = skey[j];
+    const uint32_t d = static_cast<uint32_t>((kk >> shift) & 0xff);
+    const uint32_t pos = doff[d] + (j - tstart[d]);
+    kout[pos] = kk;
+    vout[pos] = sval[j];
+  }
+}
+
+// Launches scatter_kernel with its staged tile (dynamic shared memory).
+void launch_scatter(tg_ctx* ctx, uint64_t* k0, uint32_t* v0, uint64_t* k1, uint32_t* v1,
+                    uint64_t n, int pass, const RadixPlan* plan, const uint32_t* counts,
+                    uint32_t nblk, const uint32_t* totals) {
+  static bool attr[TG_MAX_DEVICES] = {};
+  if (!attr[ctx->device % TG_MAX_DEVICES]) {
+    TGB_CUDA(cudaFuncSetAttribute(scatter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  kRsScatterSmem));
+    attr[ctx->device % TG_MAX_DEVICES] = true;
+  }
+  scatter_kernel<<<nblk, kRsWarps * 32, kRsScatterSmem, ctx->stream>>>(k0, v0, k1, v1, n, pass,
+                                                                       plan, counts, nblk, totals);
 }
 
 // K6: order[r] = id, new_id_of[id] = r (reorder.cpp:27)
@@ -307,8 +351,7 @@ void sort_rows_by_length(tg_ctx* ctx, const uint32_t* off, uint64_t rb, uint64_t
     TGB_LAUNCHED();
     count_scan_kernel<<<256, 1024, 0, ctx->stream>>>(counts, nblk, pass, plan, totals);
     TGB_LAUNCHED();
-    scatter_kernel<<<nblk, kRsWarps * 32, 0, ctx->stream>>>(k0, v0, k1, v1, m, pass, plan, counts,
-                                                             nblk, totals);
+    launch_scatter(ctx, k0, v0, k1, v1, m, pass, plan, counts, nblk, totals);
     TGB_LAUNCHED();
   }
   order_out_kernel<<<grid_for(m, 256), 256, 0, ctx->stream>>>(v0, v1, plan, rb, m, order_dev);
@@ -345,8 +388,7 @@ void sort_scores(tg_ctx* ctx, const double* scores_dev, uint64_t n, uint64_t* or
     TGB_LAUNCHED();
     count_scan_kernel<<<256, 1024, 0, ctx->stream>>>(counts, nblk, p, plan, totals);
     TGB_LAUNCHED();
-    scatter_kernel<<<nblk, kRsWarps * 32, 0, ctx->stream>>>(k0, v0, k1, v1, n, p, plan, counts,
-                                                             nblk, totals);
+    launch_scatter(ctx, k0, v0, k1, v1, n, p, plan, counts, nblk, totals);
     TGB_LAUNCHED();
   }
   perm_kernel<<<grid_for(n, 256), 256, 0, ctx->stream>>>(v0, v1, plan, n, order_dev, perm_dev);
@@ -464,8 +506,7 @@ void transpose_device(tg_ctx* ctx, const uint64_t* off, const uint64_t* tgt, uin
     TGB_LAUNCHED();
     count_scan_kernel<<<256, 1024, 0, ctx->stream>>>(counts, nblk, pass, plan, totals);
     TGB_LAUNCHED();
-    scatter_kernel<<<nblk, kRsWarps * 32, 0, ctx->stream>>>(k0, v0, k1, v1, e, pass, plan, counts,
-                                                             nblk, totals);
+    launch_scatter(ctx, k0, v0, k1, v1, e, pass, plan, counts, nblk, totals);
     TGB_LAUNCHED();
   }
   transpose_out_kernel<<<grid_for(e + 1, 256, ctx->num_sms * 16), 256, 0, ctx->stream>>>(
