@@ -23,6 +23,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cmath>
 #include <chrono>
 #include <map>
@@ -867,8 +868,13 @@ void launch_gather(tg_store* s, const uint64_t* ids_dev, uint64_t n, void* dst_d
     // enough that a short list still spreads over every SM (each SM's TMA
     // and address translation serve its own batches)
     const uint64_t all_warps = static_cast<uint64_t>(ctx->num_sms) * 2 * kBulkWarps;
+    // TIERGRAPH_GATHER_ROWS_PER_WARP caps the batch (experiments)
+    static const uint64_t cap_b = [] {
+      const char* v = std::getenv("TIERGRAPH_GATHER_ROWS_PER_WARP");
+      return v ? std::max<uint64_t>(1, std::strtoull(v, nullptr, 10)) : 32ull;
+    }();
     const uint32_t B = static_cast<uint32_t>(std::max<uint64_t>(
-        1, std::min<uint64_t>({32, kBulkStage / Rpad, (n + all_warps - 1) / all_warps})));
+        1, std::min<uint64_t>({cap_b, kBulkStage / Rpad, (n + all_warps - 1) / all_warps})));
     const uint64_t warps = (n + B - 1) / B;
     const unsigned grid = grid_for(warps * 32, kBulkWarps * 32, ctx->num_sms * 2);
     constexpr int kSmem = kBulkWarps * 2 * kBulkStage;
