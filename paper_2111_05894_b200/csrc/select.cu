@@ -148,7 +148,7 @@ __global__ void __launch_bounds__(1024) count_scan_kernel(uint32_t* __restrict__
 // out in that order, so consecutive threads store consecutive positions of a
 // digit's run (coalesced) instead of 32 unrelated runs per store.
 constexpr int kRsScatterSmem = kRsTile * (8 + 4);  // staged keys + values
-__global__ void __launch_bounds__(kRsWarps * 32) scatter_kernel(
+__global__ void __launch_bounds__(kRsWarps * 32, 3) scatter_kernel(
     uint64_t* __restrict__ k0, uint32_t* __restrict__ v0, uint64_t* __restrict__ k1,
     uint32_t* __restrict__ v1, uint64_t n, int pass, const RadixPlan* __restrict__ plan,
     const uint32_t* __restrict__ offs, uint32_t nblk, const uint32_t* __restrict__ totals) {
