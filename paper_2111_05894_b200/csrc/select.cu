@@ -65,15 +65,22 @@ __global__ void __launch_bounds__(256) key_prep_kernel(const double* __restrict_
   }
 }
 
-__global__ void plan_kernel(const uint32_t* __restrict__ hist, uint64_t n, RadixPlan* plan) {
-  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+// One 256-thread CTA: thread d checks digit value d of every pass (a pass
+// whose histogram holds all n keys in one bucket is skipped).
+__global__ void __launch_bounds__(256) plan_kernel(const uint32_t* __restrict__ hist, uint64_t n,
+                                                   RadixPlan* plan) {
+  __shared__ int trivial[8];
+  for (int p = 0; p < 8; ++p) {
+    const int t = __syncthreads_or(hist[p * 256 + threadIdx.x] == n);
+    if (threadIdx.x == 0) trivial[p] = t;
+  }
+  __syncthreads();
+  if (threadIdx.x != 0) return;
   int src = 0;
   for (int p = 0; p < 8; ++p) {
-    bool trivial = false;
-    for (int d = 0; d < 256; ++d) trivial |= hist[p * 256 + d] == n;
-    plan->skip[p] = trivial ? 1 : 0;
+    plan->skip[p] = trivial[p] ? 1 : 0;
     plan->src[p] = src;
-    if (!trivial) src ^= 1;
+    if (!trivial[p]) src ^= 1;
   }
   plan->final_src = src;
 }
@@ -344,7 +351,7 @@ void sort_rows_by_length(tg_ctx* ctx, const uint32_t* off, uint64_t rb, uint64_t
   rowlen_key_kernel<<<grid_for(m, 256, ctx->num_sms * 8), 256, 0, ctx->stream>>>(off, rb, m, k0,
                                                                                 v0, hist);
   TGB_LAUNCHED();
-  plan_kernel<<<1, 32, 0, ctx->stream>>>(hist, m, plan);
+  plan_kernel<<<1, 256, 0, ctx->stream>>>(hist, m, plan);
   TGB_LAUNCHED();
   for (int pass = 0; pass < 4; ++pass) {  // digits 4..7 are constant: planned as skipped
     digit_count_kernel<<<nblk, kRsWarps * 32, 0, ctx->stream>>>(k0, k1, m, pass, plan, counts, nblk);
@@ -381,7 +388,7 @@ void sort_scores(tg_ctx* ctx, const double* scores_dev, uint64_t n, uint64_t* or
   key_prep_kernel<<<grid_for(n, 256, ctx->num_sms * 8), 256, 0, ctx->stream>>>(scores_dev, n, k0,
                                                                                v0, hist, bad);
   TGB_LAUNCHED();
-  plan_kernel<<<1, 32, 0, ctx->stream>>>(hist, n, plan);
+  plan_kernel<<<1, 256, 0, ctx->stream>>>(hist, n, plan);
   TGB_LAUNCHED();
   for (int p = 0; p < 8; ++p) {
     digit_count_kernel<<<nblk, kRsWarps * 32, 0, ctx->stream>>>(k0, k1, n, p, plan, counts, nblk);
@@ -499,7 +506,7 @@ void transpose_device(tg_ctx* ctx, const uint64_t* off, const uint64_t* tgt, uin
   edge_keys_kernel<<<grid_for(n * 32, 256, ctx->num_sms * 16), 256, 0, ctx->stream>>>(off, tgt, n, k0,
                                                                                      v0, hist);
   TGB_LAUNCHED();
-  plan_kernel<<<1, 32, 0, ctx->stream>>>(hist, e, plan);
+  plan_kernel<<<1, 256, 0, ctx->stream>>>(hist, e, plan);
   TGB_LAUNCHED();
   for (int pass = 0; pass < 4; ++pass) {  // digits 4..7 are constant: planned as skipped
     digit_count_kernel<<<nblk, kRsWarps * 32, 0, ctx->stream>>>(k0, k1, e, pass, plan, counts, nblk);
