@@ -247,11 +247,16 @@ __global__ void seed_kernel(const uint64_t* __restrict__ seeds, uint64_t ns, uin
   }
 }
 
-// members = set bits in node-id order: per-block popcounts (1024 words =
-// 32,768 nodes per block), then positions. Reads N/8 bytes per minibatch.
-constexpr int kCompactBlock = 1024;
+// members = set bits in node-id order: per-block popcounts (BLK words =
+// 32·BLK nodes per block), then positions. Reads N/8 bytes per minibatch.
+// BLK = 256 words per CTA for bitmaps up to 2^20 words (C2: 300 CTAs instead
+// of 75), else 1024 (the block-count prefix stays short on huge graphs).
+constexpr int kCompactBlock = 256;   // the smallest block: sizes the block-count array
+constexpr int kCompactBig = 1024;
+constexpr uint64_t kCompactBigWords = 1ull << 20;
+template <int BLK>
 __device__ __forceinline__ uint32_t block_excl_sum(uint32_t v, uint32_t* total) {
-  __shared__ uint32_t ws[kCompactBlock / 32];
+  __shared__ uint32_t ws[BLK / 32];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   uint32_t x = v;
 #pragma unroll
@@ -262,7 +267,7 @@ __device__ __forceinline__ uint32_t block_excl_sum(uint32_t v, uint32_t* total) 
   if (lane == 31) ws[w] = x;
   __syncthreads();
   uint32_t before = 0, tot = 0;
-  for (int k = 0; k < kCompactBlock / 32; ++k) {
+  for (int k = 0; k < BLK / 32; ++k) {
     if (k < w) before += ws[k];
     tot += ws[k];
   }
@@ -270,12 +275,13 @@ __device__ __forceinline__ uint32_t block_excl_sum(uint32_t v, uint32_t* total) 
   return before + x - v;
 }
 
-__global__ void __launch_bounds__(kCompactBlock) member_count_kernel(const uint32_t* __restrict__ bits,
-                                                                     uint64_t nwords,
-                                                                     uint32_t* __restrict__ counts) {
-  const uint64_t i = blockIdx.x * (uint64_t)kCompactBlock + threadIdx.x;
+template <int BLK>
+__global__ void __launch_bounds__(BLK) member_count_kernel(const uint32_t* __restrict__ bits,
+                                                           uint64_t nwords,
+                                                           uint32_t* __restrict__ counts) {
+  const uint64_t i = blockIdx.x * (uint64_t)BLK + threadIdx.x;
   uint32_t tot;
-  block_excl_sum(i < nwords ? __popc(bits[i]) : 0u, &tot);
+  block_excl_sum<BLK>(i < nwords ? __popc(bits[i]) : 0u, &tot);
   if (threadIdx.x == 0) counts[blockIdx.x] = tot;
 }
 
@@ -303,15 +309,16 @@ __global__ void __launch_bounds__(1024) count_prefix_kernel(uint32_t* __restrict
   if (threadIdx.x == 1023) *total = part[1023];
 }
 
-__global__ void __launch_bounds__(kCompactBlock) member_write_kernel(const uint32_t* __restrict__ bits,
-                                                                     uint64_t nwords,
-                                                                     const uint32_t* __restrict__ base,
-                                                                     uint64_t* __restrict__ out,
-                                                                     const uint64_t* out_base,
-                                                                     uint64_t cap) {
-  const uint64_t i = blockIdx.x * (uint64_t)kCompactBlock + threadIdx.x;
+template <int BLK>
+__global__ void __launch_bounds__(BLK) member_write_kernel(const uint32_t* __restrict__ bits,
+                                                           uint64_t nwords,
+                                                           const uint32_t* __restrict__ base,
+                                                           uint64_t* __restrict__ out,
+                                                           const uint64_t* out_base,
+                                                           uint64_t cap) {
+  const uint64_t i = blockIdx.x * (uint64_t)BLK + threadIdx.x;
   uint32_t word = i < nwords ? bits[i] : 0u, tot;
-  uint64_t pos = (out_base ? *out_base : 0) + base[blockIdx.x] + block_excl_sum(__popc(word), &tot);
+  uint64_t pos = (out_base ? *out_base : 0) + base[blockIdx.x] + block_excl_sum<BLK>(__popc(word), &tot);
   while (word) {
     const int b = __ffs(word) - 1;
     if (pos < cap) out[pos] = i * 32 + b;
@@ -528,17 +535,26 @@ uint64_t expand(tg_sampler* s, const uint64_t* sd, uint64_t ns, const uint32_t* 
 
 // The stamped members in id order into out_dev (device, >= bound entries);
 // the total is left in s->small[kSmallTotal]. No host round trip.
+// `wait` (optional) is a cudaEvent the write waits for: the member count and
+// its block prefix do not depend on the output offset, only the write does.
 void compact_members(tg_sampler* s, uint64_t* out_dev, const uint64_t* out_base = nullptr,
-                     uint64_t cap = ~0ull) {
-  tg_ctx* ctx = s->ctx;
-  const uint64_t nblk = (s->nwords + kCompactBlock - 1) / kCompactBlock;
-  member_count_kernel<<<nblk, kCompactBlock, 0, s->stream>>>(s->member_bits, s->nwords, s->blk);
+                     uint64_t cap = ~0ull, cudaEvent_t wait = nullptr) {
+  const bool big = s->nwords > kCompactBigWords;
+  const int blk = big ? kCompactBig : kCompactBlock;
+  const uint64_t nblk = (s->nwords + blk - 1) / blk;
+  if (big) member_count_kernel<kCompactBig><<<nblk, blk, 0, s->stream>>>(s->member_bits, s->nwords, s->blk);
+  else member_count_kernel<kCompactBlock><<<nblk, blk, 0, s->stream>>>(s->member_bits, s->nwords, s->blk);
   TGB_LAUNCHED();
   count_prefix_kernel<<<1, 1024, 0, s->stream>>>(s->blk, static_cast<uint32_t>(nblk),
                                                    s->small + kSmallTotal);
   TGB_LAUNCHED();
-  member_write_kernel<<<nblk, kCompactBlock, 0, s->stream>>>(s->member_bits, s->nwords, s->blk,
-                                                               out_dev, out_base, cap);
+  if (wait) TGB_CUDA(cudaStreamWaitEvent(s->stream, wait, 0));
+  if (big)
+    member_write_kernel<kCompactBig><<<nblk, blk, 0, s->stream>>>(s->member_bits, s->nwords, s->blk,
+                                                                  out_dev, out_base, cap);
+  else
+    member_write_kernel<kCompactBlock><<<nblk, blk, 0, s->stream>>>(s->member_bits, s->nwords,
+                                                                    s->blk, out_dev, out_base, cap);
   TGB_LAUNCHED();
 }
 
@@ -673,8 +689,7 @@ int tg_sample_batches(tg_sampler* s, const uint64_t* order, uint64_t n_order, ui
       const uint64_t b = first_batch + k;
       const uint64_t beg = b * batch_size, len = std::min(batch_size, n_order - beg);
       expand(ls, od + beg, len, fanouts, nf, rng_seed, epoch, b, ExpandOut{});
-      if (k > 0 && L > 1) TGB_CUDA(cudaStreamWaitEvent(ls->stream, lane(k - 1)->ev, 0));
-      compact_members(ls, md, offs.dev() + k, cap);
+      compact_members(ls, md, offs.dev() + k, cap, k > 0 && L > 1 ? lane(k - 1)->ev : nullptr);
       advance_offset_kernel<<<1, 32, 0, ls->stream>>>(ls->small + kSmallTotal, offs.dev(), k);
       TGB_LAUNCHED();
       if (L > 1) TGB_CUDA(cudaEventRecord(ls->ev, ls->stream));
