@@ -73,6 +73,28 @@ CONFIGS = {
 }
 
 
+def config_dict(cfg, n, e, world):
+    """The workload as both arms report it (identical dicts: the driver
+    compares them). Arm-specific setup goes under the line's `setup` key."""
+    return {"workload": cfg["workload"], "nodes": n, "edges_after_dedup": e,
+            "row_bytes": cfg["dim"] * cfg["elem"], "dim": cfg["dim"],
+            "elem_bytes": cfg["elem"], "hot_fraction": hot_fraction(cfg, world),
+            "train_fraction": cfg["train"], "fanouts": list(cfg["fanouts"]),
+            "batch": cfg["batch"], "epoch_minibatches_max": cfg.get("max_batches"),
+            "rng": {"graph": 1, "train_ids": 3, "minibatches": 7, "epoch": 0},
+            "l2": "inputs > L2: each step's rows are a fresh minibatch; the GPU arm also "
+                  "flushes L2 (256 MB memset) between steps"}
+
+
+def source_rows(cfg, inv):
+    """new id -> row of the host feature fixture: the original matrix row
+    inv[id] (reorder.cpp:113-115), or for C4 the row cache row (id mod P)."""
+    if cfg.get("row_cache_gb"):
+        n = len(inv)
+        return np.arange(n, dtype=np.uint64) % np.uint64(cache_rows(cfg))
+    return np.asarray(inv, np.uint64)
+
+
 def hot_fraction(cfg, world):
     return cfg["hot"] if "hot" in cfg else min(1.0, cfg["hot_per_gpu"] * world)
 
@@ -613,13 +635,14 @@ def run_ours(args):
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(t_ms / args.steps, 4),
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u8",
             "data": "synthetic (R-MAT graph, closed-form features, reference sampler id lists)",
-            "config": {"workload": cfg["workload"], "nodes": n, "edges_after_dedup": e,
-                       "row_bytes": R, "hot_fraction": hot, "layout": lay.as_tuple(),
-                       "gather_mode": args.gather_mode,
-                       "l2": "flushed between steps (256 MB memset), per-step CUDA events",
-                       "parallelism": f"{world} GPU(s), hot tier sharded, cold tier per rank"
-                                      + (" (TEST MODE: all ranks share cuda:0, gloo plumbing; not "
-                                         "a scaling number)" if share else "")},
+            "config": config_dict(cfg, n, e, world),
+            "setup": {"layout": lay.as_tuple(), "gather_mode": args.gather_mode,
+                      "cold_mode": cfg.get("cold_mode", "reordered"),
+                      "timing": "per-step CUDA events on the launching stream, L2 flushed "
+                                "(256 MB memset) before every step, max over ranks",
+                      "parallelism": f"{world} GPU(s), hot tier sharded, cold tier per rank"
+                                     + (" (TEST MODE: all ranks share cuda:0, gloo plumbing; "
+                                        "not a scaling number)" if share else "")},
             "minibatches_per_s": round(mbps, 1),
             "avg_ids_per_minibatch": round(u_all / max(args.steps * world, 1), 1),
             "hit_split": {"local": round(frac_l, 4), "peer": round(frac_p, 4), "host": round(frac_h, 4)},
@@ -701,7 +724,7 @@ def run_ours(args):
             "clocks": clocks,
         }
         if cfg.get("row_cache_gb"):
-            result["config"]["host_row_cache"] = {
+            result["setup"]["host_row_cache"] = {
                 "rows": cache_rows(cfg), "bytes": cache_rows(cfg) * R,
                 "map": "new id i reads cache row (i mod rows), i.e. the reordered matrix "
                        "wrapped every `rows` rows: tg_store_place_rows",
@@ -744,10 +767,19 @@ def cpu_baseline(cfg, off, tgt, tid, scores, perm, feat, R, lay, lists, store, o
         ref, kind = oracle.port(), "port"
     cores = os.cpu_count() or 1
     parity = {}
-    # PageRank (whole C2 run: a few seconds on the host)
-    t0 = time.perf_counter()
-    want = ref.weighted_reverse_pagerank(off, tgt, tid.ids)
-    pr_s = time.perf_counter() - t0
+    if kind == "reference":
+        ref.set_worker_count(cores)
+    # PageRank (whole run: seconds at C2, ~40 s at C3 on 16 cores)
+    if kind == "reference":
+        rg = ref.graph(off, tgt)  # the reference CsrGraph (construction not timed)
+        t0 = time.perf_counter()
+        want = rg.weighted_reverse_pagerank(tid.ids)
+        pr_s = time.perf_counter() - t0
+        del rg
+    else:
+        t0 = time.perf_counter()
+        want = ref.weighted_reverse_pagerank(off, tgt, tid.ids)
+        pr_s = time.perf_counter() - t0
     parity["pagerank_bit_exact"] = bool(want.tobytes() == scores.tobytes())
     parity["permutation_identical"] = bool(
         np.array_equal(ref.permutation_from_scores(want), perm.new_id_of))
@@ -756,39 +788,40 @@ def cpu_baseline(cfg, off, tgt, tid, scores, perm, feat, R, lay, lists, store, o
                  "sample": "reference build missing"}, parity)
     ref.set_worker_count(cores)
     from paper_2111_05894_b200 import synth, tiergraph as tg
-    moved, passes, cpu_s = 0, 0, None
+    moved, passes = 0, 0
     sample = lists[: max(1, min(len(lists), 24))]
+    inv = np.empty(len(perm.new_id_of), np.uint64)
+    inv[perm.new_id_of.astype(np.int64)] = np.arange(len(inv), dtype=np.uint64)
     if cfg.get("cpu_gather", True):
+        # the reordered copy the reference would build (reorder_features)
         rf = oracle.RefFeatures(ref, feat.reshape(cfg["nodes"], R)).reordered(perm.new_id_of)
-        out = np.empty((max(len(x) for x in sample), R), np.uint8)
-        rep = np.zeros(6, np.uint64)
-        rf.gather(lay, sample[0], 0, out, rep)  # warm
-        t0 = time.perf_counter()
-        while time.perf_counter() - t0 < 3.0:  # a bounded ~3 s sample of CPU work
-            for ids in sample:
-                rf.gather(lay, ids, 0, out, rep)
-                moved += len(ids) * R
-            passes += 1
-        cpu_s = time.perf_counter() - t0
-        # gather parity on the last sampled minibatch
-        ids = sample[-1]
-        r = np.zeros(6, np.uint64)
-        rf.gather(lay, ids, 0, out, r)
-        mine = tg.TrafficReport()
-        got = store.gather_rows(ids, report=mine)
-        parity["gather_rows_bit_exact"] = bool(np.array_equal(got, out[: len(ids)]))
+        how = "reference FeatureMatrix::row memcpy of reorder_features' copy"
     else:
-        # no second 57 GB copy: rows checked against the closed-form fill of
-        # the ORIGINAL row (feature_matrix.cpp:16-28), accounting against the
-        # reference's gather()
-        ids = sample[-1]
-        inv = np.empty(len(perm.new_id_of), np.uint64)
-        inv[perm.new_id_of.astype(np.int64)] = np.arange(len(inv), dtype=np.uint64)
-        mine = tg.TrafficReport()
-        got = store.gather_rows(ids, report=mine)
-        want = expected_rows(cfg, ids, inv)
-        parity["gather_rows_bit_exact"] = bool(np.array_equal(got.view(want.dtype), want))
-        r = ref.gather(lay.as_tuple(), ids, 0)
+        # no second 57 GB copy: the same rows read from the original matrix
+        # through the inverse permutation (byte-identical, reorder.cpp:113-115)
+        rf = oracle.RefFeaturesInv(ref, feat.reshape(-1, R), source_rows(cfg, inv))
+        how = ("reference FeatureMatrix::row memcpy of the original matrix's row inv[id] "
+               "(byte-identical to reorder_features' copy, which does not fit twice)")
+    out = np.empty((max(len(x) for x in sample), R), np.uint8)
+    rep = np.zeros(6, np.uint64)
+    rf.gather(lay, sample[0], 0, out, rep)  # warm
+    t0 = time.perf_counter()
+    while time.perf_counter() - t0 < 3.0:  # a bounded ~3 s sample of CPU work
+        for ids in sample:
+            rf.gather(lay, ids, 0, out, rep)
+            moved += len(ids) * R
+        passes += 1
+    cpu_s = time.perf_counter() - t0
+    # gather parity on the last sampled minibatch: rows and report against
+    # the reference, rows also against the closed-form fill
+    ids = sample[-1]
+    r = np.zeros(6, np.uint64)
+    rf.gather(lay, ids, 0, out, r)
+    mine = tg.TrafficReport()
+    got = store.gather_rows(ids, report=mine)
+    want = expected_rows(cfg, ids, inv)
+    parity["gather_rows_bit_exact"] = bool(np.array_equal(got, out[: len(ids)]) and
+                                           np.array_equal(got.view(want.dtype), want))
     if gt is not None:
         # the reference's own sampler on the host cores, and parity of the GPU sampler
         go_, gt_ = np.asarray(gt.offsets), np.asarray(gt.targets)
@@ -799,14 +832,13 @@ def cpu_baseline(cfg, off, tgt, tid, scores, perm, feat, R, lay, lists, store, o
         parity["gpu_sampler_bit_exact"] = bool(all(np.array_equal(a, b)
                                                    for a, b in zip(ref_lists, gpu_lists)))
     parity["traffic_report_equal"] = bool(np.array_equal(mine.as_array(), r))
-    base = {"value": round(moved / cpu_s / 1e9, 3) if cpu_s else None, "unit": "GB/s",
+    base = {"value": round(moved / cpu_s / 1e9, 3), "unit": "GB/s",
             "cores": cores, "kind": kind,
-            "sample": (f"{passes} x {len(sample)} minibatches of the same epoch: reference "
-                       f"FeatureMatrix::row memcpy (reorder.cpp:113-115 pattern) + gather() "
-                       f"accounting, {cores} OpenMP threads, {cpu_s:.2f}s") if cpu_s else
-                      "no CPU gather at this scale (it needs a second reordered copy of the "
-                      "matrix); PageRank and sampling timed",
+            "sample": (f"{passes} x {len(sample)} minibatches of the same epoch: {how} "
+                       f"(reorder.cpp:113-115 pattern) + gather() accounting, {cores} OpenMP "
+                       f"threads, {cpu_s:.2f}s"),
             "pagerank_gteps": round(5 * len(tgt) / pr_s / 1e9, 4),
+            "minibatches_per_s": round(passes * len(sample) / cpu_s, 2),
             "sampling_minibatches_per_s": round(32 / samp_s, 2) if gt is not None else None,
             "pagerank_s": round(pr_s, 3)}
     return base, parity
@@ -814,7 +846,18 @@ def cpu_baseline(cfg, off, tgt, tid, scores, perm, feat, R, lay, lists, store, o
 
 def run_reference(args):
     """--impl reference: the reference's own CPU implementation of the path
-    (oracle/_ref: the unmodified reference sources), rank 0 only."""
+    (oracle/_ref: the unmodified reference sources, all host threads), rank 0
+    only, on the same workload as the GPU arm. It never loads this repo's
+    library: the fixtures (`synth`) are plain numpy/torch, and the package no
+    longer loads libtiergraph_b200.so on import.
+
+    Per run: the reference's PageRank (timed), permutation, reorder_graph and
+    transpose produce the reorder_graph'd sampler input; the reference's
+    build_minibatch lists give one step per minibatch. A step is the CPU byte
+    gather of that minibatch (FeatureMatrix::row memcpy, reorder.cpp:113-115
+    pattern, plus the reference gather() accounting). Where the reordered
+    copy does not fit next to the original (C3, C4) the rows are read from the
+    original fixture through the inverse permutation: byte-identical."""
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
@@ -824,33 +867,60 @@ def run_reference(args):
     cfg = CONFIGS[args.config]
     if ref is None:
         return {"impl": "reference", "unavailable": "oracle/_ref/libtgref.so was not built"}
-    if not cfg.get("cpu_gather", True):
-        return {"impl": "reference", "unavailable": (
-            "the reference's CPU gather reads FeatureMatrix::row of a reordered copy of the "
-            f"matrix ({cfg['nodes'] * cfg['dim'] * cfg['elem'] / 1e9:.0f} GB here, twice with the "
-            "original), beyond the box's host RAM; the reference PageRank/sampler at this "
-            "scale are timed in the `ours` line's cpu_baseline")}
     cores = os.cpu_count() or 1
     ref.set_worker_count(cores)
     from paper_2111_05894_b200 import synth
+    t_all = time.time()
     dev = "cuda" if _cuda_available() else "cpu"
     off, tgt = synth.rmat_graph(cfg["nodes"], cfg["draws"], seed=1, device=dev)
     n, e = len(off) - 1, len(tgt)
     tid = ref.draw_random_train_ids(n, int(n * cfg["train"]), 3)
+    log(f"[reference] graph {n} / {e} ({time.time()-t_all:.0f}s)")
+    rg = ref.graph(off, tgt)  # the reference CsrGraph (construction not timed)
     t0 = time.perf_counter()
-    scores = ref.weighted_reverse_pagerank(off, tgt, tid)
+    scores = rg.weighted_reverse_pagerank(tid)
     pr_s = time.perf_counter() - t0
+    del rg
+    t0 = time.perf_counter()
     perm = ref.permutation_from_scores(scores)
+    sel_s = time.perf_counter() - t0
+    del scores
     ro, rt = ref.reorder_graph(off, tgt, perm)
+    del off, tgt
     go, gt = ref.transpose(ro, rt)
+    del ro, rt
     new_tid = np.sort(perm[tid])
     nsteps = args.steps + args.warmup
+    nb_lists = min(nsteps, 64)
+    t0 = time.perf_counter()
     lists = ref.epoch_minibatches(go, gt, new_tid, cfg["fanouts"], cfg["batch"], 7, 0,
-                                  max_batches=min(nsteps, 64))
+                                  max_batches=nb_lists)
+    samp_s = time.perf_counter() - t0
+    del go, gt
+    log(f"[reference] PageRank {pr_s:.1f}s, {len(lists)} minibatches in {samp_s:.1f}s "
+        f"({time.time()-t_all:.0f}s)")
     R = cfg["dim"] * cfg["elem"]
-    feat = synth.test_features(n, cfg["dim"])
-    rf = oracle.RefFeatures(ref, feat.view(np.uint8).reshape(n, R)).reordered(perm)
-    lay = ref.plan_layout(n, cfg["hot"], 0.0, 1, cfg["dim"], cfg["elem"])
+    inv = np.empty(n, np.uint64)
+    inv[perm.astype(np.int64)] = np.arange(n, dtype=np.uint64)
+    if cfg.get("cpu_gather", True):
+        feat = synth.test_features(n, cfg["dim"])
+        rf = oracle.RefFeatures(ref, feat.view(np.uint8).reshape(n, R)).reordered(perm)
+        del feat
+        how = "FeatureMatrix::row memcpy of reorder_features' copy"
+    else:
+        if cfg.get("row_cache_gb"):
+            P = cache_rows(cfg)
+            feat = np.empty(P * R, np.uint8)
+            synth.test_features_f16_gpu(P, cfg["dim"], feat, device=dev)
+        else:
+            feat = np.empty(n * R, np.uint8)
+            synth.test_features_pinned_gpu(n, cfg["dim"], feat, device=dev)
+        rf = oracle.RefFeaturesInv(ref, feat.reshape(-1, R), source_rows(cfg, inv))
+        how = ("FeatureMatrix::row memcpy of the original matrix's row inv[id] (byte-identical "
+               "to reorder_features' copy, which does not fit next to the original)")
+    lay = ref.plan_layout(n, hot_fraction(cfg, 1), 0.0, 1, cfg["dim"], cfg["elem"],
+                          (int(np.ceil(cfg["hot_per_gpu"] * n)) + 1) * R
+                          if "hot_per_gpu" in cfg else 0)
     out = np.empty((max(len(x) for x in lists), R), np.uint8)
     rep = np.zeros(6, np.uint64)
     for k in range(args.warmup):
@@ -863,20 +933,25 @@ def run_reference(args):
         moved += len(ids) * R
     dt = time.perf_counter() - t0
     v = moved / dt / 1e9
+    log(f"[reference] done ({time.time()-t_all:.0f}s)")
     return {"metric": METRIC, "value": round(v, 3), "unit": "GB/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": round(dt * 1e3 / args.steps, 3), "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "u8",
             "data": "synthetic (R-MAT graph, closed-form features, reference sampler id lists)",
-            "config": {"workload": cfg["workload"], "nodes": n, "edges_after_dedup": e,
-                       "row_bytes": R, "hot_fraction": cfg["hot"]},
+            "config": config_dict(cfg, n, e, world),
             "impl": "reference",
             "minibatches_per_s": round(args.steps / dt, 2),
+            "avg_ids_per_minibatch": round(moved / R / max(args.steps, 1), 1),
             "pagerank": {"gteps": round(5 * e / pr_s / 1e9, 4), "s": round(pr_s, 3)},
+            "selection": {"s": round(sel_s, 3), "keys": n},
+            "sampling": {"minibatches_per_s": round(len(lists) / samp_s, 2),
+                         "minibatches": len(lists)},
             "cpu_baseline": {"value": round(v, 3), "unit": "GB/s", "cores": cores,
                              "kind": "reference",
-                             "sample": f"{args.steps} minibatches: FeatureMatrix::row memcpy + "
-                                       "gather() accounting (reference build, OpenMP)"},
+                             "sample": f"{args.steps} minibatches (the epoch's first, in order): "
+                                       f"{how} + gather() accounting (reference build, "
+                                       f"{cores} OpenMP threads)"},
             "e2e": {"value": round(v, 3), "unit": "GB/s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
 
@@ -894,7 +969,7 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=10)
-    ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
+    ap.add_argument("--config", default="c3", choices=sorted(CONFIGS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--gather-mode", default="bulk+spread+dynamic",

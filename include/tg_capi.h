@@ -130,6 +130,8 @@ int tg_weighted_reverse_pagerank(tg_ctx* ctx, const tg_graph* g, uint32_t iterat
  * vectors of length n; only rows [row_begin,row_end) are written.
  *   tg_pagerank_prepare: in-degrees (u32, device, length n) and the initial
  *     normalized vector for the weighted (tid!=NULL) or plain recurrence.
+ *     A train id >= n is TG_ERR_DOMAIN "train id X out of range"
+ *     (scoring.cpp:98); checking it synchronises the stream once.
  *   tg_pagerank_step: one Jacobi step over the rows; `last` writes scores
  *     instead of the next normalized vector. */
 int tg_pagerank_prepare_async(tg_ctx* ctx, const tg_graph* g, const uint64_t* tid_dev,

@@ -376,6 +376,7 @@ class RefOracle:
             "tgref_features_nbytes": (U64, [vp]),
             "tgref_reorder_features": (I32, [vp, u64p, U64, C.POINTER(vp)]),
             "tgref_features_gather": (I32, [vp, u64p, vp, U64, U32, vp, u64p]),
+            "tgref_features_gather_inv": (I32, [vp, U64, U64, vp, u64p, vp, U64, U32, vp, u64p]),
             "tgref_validate_layout": (I32, [u64p]),
             "tgref_validate_cost_model": (I32, [C.c_double, C.c_double, C.c_double]),
             "tgref_resolve": (I32, [u64p, U64, U32, u64p]),
@@ -714,6 +715,29 @@ class RefFeatures:
             self.lib.L.tgref_features_destroy(self.h)
         except Exception:
             pass
+
+
+class RefFeaturesInv:
+    """The CPU byte gather over the caller's ORIGINAL matrix (no copy):
+    new row id = old row inv[id], byte-identical to RefFeatures.reordered(perm)
+    (reorder.cpp:113-115) without a second N x R matrix in host RAM."""
+
+    def __init__(self, lib: RefOracle, data: np.ndarray, row_of):
+        """row_of[id] = the row of `data` holding new row id (the inverse
+        permutation for an original matrix)."""
+        self.lib = lib
+        self.data = data  # caller-owned, kept alive; rows x row_bytes (any dtype)
+        self.rows = data.shape[0]
+        self.row_bytes = data.nbytes // max(self.rows, 1)
+        self.inv = _u64(row_of)
+
+    def gather(self, layout, ids: np.ndarray, dev: int, out: np.ndarray, report: np.ndarray):
+        ids = _u64(ids)
+        if len(ids) and int(ids.max()) >= len(self.inv):
+            raise DomainError(f"row {int(ids.max())} out of range")
+        self.lib._chk(self.lib.L.tgref_features_gather_inv(
+            self.data.ctypes.data, self.rows, self.row_bytes, self.inv.ctypes.data,
+            layout6(layout), ids.ctypes.data, len(ids), dev, out.ctypes.data, report))
 
 
 _port = None

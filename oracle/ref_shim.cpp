@@ -348,6 +348,31 @@ int tgref_features_gather(void* h, const uint64_t* layout6, const uint64_t* ids,
   });
 }
 
+// The same CPU byte gather from the ORIGINAL (un-reordered) matrix held by the
+// caller: new row `id` of reorder_features(f, perm) is old row inv[id]
+// (reorder.cpp:113-115 writes old row u to new row perm[u]), so this copies
+// FeatureMatrix::row(inv[id]) (feature_matrix.hpp:22-24: data + id*row_bytes)
+// -- byte-identical to gathering from the reordered copy without a second
+// N x R matrix (used where two copies do not fit in host RAM).
+int tgref_features_gather_inv(const uint8_t* data, uint64_t rows, uint64_t row_bytes,
+                              const uint64_t* inv, const uint64_t* layout6, const uint64_t* ids,
+                              uint64_t n, uint32_t requesting_device, uint8_t* out,
+                              uint64_t* report6) {
+  return guard([&] {
+    const auto layout = make_layout(layout6);
+    tg::TrafficReport rep = get_report(report6);
+    tg::gather(layout, std::span<const uint64_t>(ids, n), requesting_device, rep);
+    const int workers = tg::worker_count();
+#pragma omp parallel for schedule(static) num_threads(workers)
+    for (int64_t i = 0; i < static_cast<int64_t>(n); ++i) {
+      const uint64_t old = inv[ids[i]];
+      if (old < rows) std::memcpy(out + static_cast<uint64_t>(i) * row_bytes,
+                                  data + old * row_bytes, row_bytes);
+    }
+    put_report(rep, report6);
+  });
+}
+
 // ---- tiering (tiering.cpp)
 int tgref_validate_layout(const uint64_t* layout6) {
   return guard([&] { tg::validate_layout(make_layout(layout6)); });

@@ -11,7 +11,18 @@ Two hot paths, hand-written CUDA for sm_100a behind a C-ABI
 
 `tiergraph` mirrors the reference API; `producers` binds the host-side
 input producers; `synth` builds the synthetic inputs of the named shapes.
-"""
-from . import tiergraph  # noqa: F401  (loads libtiergraph_b200.so; raises if missing)
 
-__all__ = ["tiergraph"]
+The CUDA library is loaded when `tiergraph` (or a module importing it) is
+first imported, not by importing this package, so the bench's reference arm
+can use the `synth` fixtures without loading libtiergraph_b200.so. Importing
+`tiergraph` raises if the library is missing: there is no fallback.
+"""
+import importlib
+
+__all__ = ["tiergraph", "producers", "distributed", "synth"]
+
+
+def __getattr__(name):
+    if name in __all__:
+        return importlib.import_module(f"{__name__}.{name}")
+    raise AttributeError(name)

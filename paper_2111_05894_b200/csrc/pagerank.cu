@@ -1054,9 +1054,21 @@ int tg_pagerank_prepare_async(tg_ctx* ctx, const tg_graph* g, const uint64_t* ti
     if (tid_dev && ntid == 0) domain_error("weighted reverse pagerank needs a non-empty train id set");
     if (!g->n) return;
     DeviceGuard dg(ctx->device);
-    // train ids must be in range here (the synchronous entry points check them)
+    // out-of-range train ids are a DomainError as in the reference
+    // (scoring.cpp:98): the one 8 B read-back of the first offending index is
+    // this call's only synchronisation
     auto* bad = ctx->scratch_t<unsigned long long>(kSmall, 1);
+    if (tid_dev) TGB_CUDA(cudaMemsetAsync(bad, 0xff, 8, ctx->stream));
     pagerank_prepare(ctx, g, tid_dev, ntid, indeg_dev, norm0_dev, bad);
+    if (!tid_dev) return;
+    unsigned long long hb = ~0ull;
+    TGB_CUDA(cudaMemcpyAsync(&hb, bad, 8, cudaMemcpyDeviceToHost, ctx->stream));
+    ctx->sync();
+    if (hb != ~0ull) {
+      uint64_t id = 0;
+      TGB_CUDA(cudaMemcpy(&id, tid_dev + hb, sizeof(id), cudaMemcpyDeviceToHost));
+      domain_error("train id " + std::to_string(id) + " out of range");  // scoring.cpp:98
+    }
   });
 }
 

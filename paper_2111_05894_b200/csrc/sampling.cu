@@ -473,7 +473,16 @@ void check_fanouts(const uint32_t* fanouts, uint32_t nf) {  // sampling.cpp:18-2
 // Small device counters: [0] seed frontier size, [1 + l] layer l's new
 // frontier size, [8] member total; u64 [5] first bad seed index, u64 [6] raw
 // draws (as u32 indices 10..13).
-constexpr int kSmallBad = 10, kSmallRaw = 12, kSmallTotal = 8;
+constexpr int kSmallBad = 10, kSmallRaw = 12, kSmallTotal = 8, kSmallOrderBad = 14;
+
+// First out-of-range seed of a whole batch order (sticky over every batch of a
+// tg_sample_batches call; expand()'s own slot is per batch).
+__global__ void order_range_kernel(const uint64_t* __restrict__ order, uint64_t m, uint64_t n,
+                                   unsigned long long* bad) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < m;
+       i += (uint64_t)gridDim.x * blockDim.x)
+    if (order[i] >= n) atomicMin(bad, (unsigned long long)i);
+}
 
 // build_minibatch (sampling.cpp:56-90) on the device, stream-ordered with no
 // host round trip: every layer's grid covers an upper bound of its frontier
@@ -681,6 +690,19 @@ int tg_sample_batches(tg_sampler* s, const uint64_t* order, uint64_t n_order, ui
     }
     if (!s->ev) TGB_CUDA(cudaEventCreateWithFlags(&s->ev, cudaEventDisableTiming));
     auto lane = [&](uint64_t k) { return k % L == 0 ? s : s->lanes[k % L - 1]; };
+    // every seed of the called batches range-checked once (sampling.cpp:61-62);
+    // the first offending position is read back with the output total
+    const uint64_t beg0 = first_batch * batch_size;
+    const uint64_t m = std::min(n_order, (first_batch + nbatches) * batch_size) - beg0;
+    auto* obad = reinterpret_cast<unsigned long long*>(s->small + kSmallOrderBad);
+    TGB_CUDA(cudaMemsetAsync(obad, 0xff, 8, ctx->stream));
+    if (m) {
+      order_range_kernel<<<grid_for(m, 256, ctx->num_sms * 4), 256, 0, ctx->stream>>>(
+          od + beg0, m, s->n, obad);
+      TGB_LAUNCHED();
+    }
+    unsigned long long first_bad = ~0ull;
+    TGB_CUDA(cudaMemcpyAsync(&first_bad, obad, 8, cudaMemcpyDeviceToHost, ctx->stream));
     // inputs ready (order, offsets[0]) before any lane starts
     TGB_CUDA(cudaEventRecord(s->ev, ctx->stream));
     for (uint32_t i = 1; i < L; ++i) TGB_CUDA(cudaStreamWaitEvent(s->lanes[i - 1]->stream, s->ev, 0));
@@ -697,10 +719,12 @@ int tg_sample_batches(tg_sampler* s, const uint64_t* order, uint64_t n_order, ui
     for (uint32_t i = 1; i < L; ++i) TGB_CUDA(cudaStreamWaitEvent(ctx->stream, s->lanes[i - 1]->ev, 0));
     uint64_t total = 0;
     TGB_CUDA(cudaMemcpyAsync(&total, offs.dev() + nbatches, 8, cudaMemcpyDeviceToHost, ctx->stream));
-    bool bad = false;
-    for (uint32_t i = 0; i < L; ++i) bad |= read_small(i ? s->lanes[i - 1] : s).bad != ~0ull;
     ctx->sync();
-    if (bad) domain_error("seed out of range in the batch order");
+    if (first_bad != ~0ull) {
+      uint64_t v = 0;
+      TGB_CUDA(cudaMemcpy(&v, od + beg0 + first_bad, 8, cudaMemcpyDeviceToHost));
+      domain_error("seed " + std::to_string(v) + " out of range");  // sampling.cpp:61-62
+    }
     if (total > cap)
       domain_error("tg_sample_batches: " + std::to_string(total) +
                    " members exceed the output capacity " + std::to_string(cap));

@@ -595,37 +595,51 @@ void launch_move(tg_ctx* ctx, const MoveArgs& a, uint64_t n, uint64_t R) {
 }
 
 // ---------------------------------------------------------- permutation util
+// Pass 1: seen[v] = the lowest position holding new id v.
+__global__ void perm_first_kernel(const uint64_t* __restrict__ p, uint64_t n,
+                                  uint32_t* __restrict__ seen) {
+  for (uint64_t u = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; u < n;
+       u += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t v = p[u];
+    if (v < n) atomicMin(&seen[v], static_cast<uint32_t>(u));
+  }
+}
+
+// Pass 2: position u offends iff p[u] >= n or an earlier position holds p[u]
+// -- exactly the positions the reference's sequential scan throws at
+// (reorder.cpp:10-21); the minimum of them is its first throw.
 __global__ void perm_check_kernel(const uint64_t* __restrict__ p, uint64_t n,
-                                  uint32_t* __restrict__ seen, uint32_t* __restrict__ inv,
+                                  const uint32_t* __restrict__ seen, uint32_t* __restrict__ inv,
                                   unsigned long long* bad) {
   for (uint64_t u = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; u < n;
        u += (uint64_t)gridDim.x * blockDim.x) {
     const uint64_t v = p[u];
-    if (v >= n) {
+    if (v >= n || seen[v] != static_cast<uint32_t>(u)) {
       atomicMin(bad, (unsigned long long)u);
       continue;
     }
-    if (atomicAdd(&seen[v], 1u) != 0) atomicMin(bad, (unsigned long long)u);
     if (inv) inv[v] = static_cast<uint32_t>(u);
   }
 }
 
 // Validates a permutation (reorder.cpp:10-21) and optionally builds its
-// inverse as u32. Throws DomainError naming the offending new id.
+// inverse as u32. Throws DomainError naming the offending new id at the
+// reference's first offending position.
 void check_permutation(tg_ctx* ctx, const uint64_t* perm_dev, uint64_t n, uint32_t* inv_dev) {
   if (n == 0) return;
   if (n >= 0xffffffffull) domain_error("permutation: n must be < 2^32");
   uint32_t* seen = ctx->scratch_t<uint32_t>(kScratchE, n);
   auto* bad = ctx->scratch_t<unsigned long long>(kSmall, 1);
-  TGB_CUDA(cudaMemsetAsync(seen, 0, n * 4, ctx->stream));
+  TGB_CUDA(cudaMemsetAsync(seen, 0xff, n * 4, ctx->stream));
   TGB_CUDA(cudaMemsetAsync(bad, 0xff, 8, ctx->stream));
+  perm_first_kernel<<<grid_for(n, 256), 256, 0, ctx->stream>>>(perm_dev, n, seen);
+  TGB_LAUNCHED();
   perm_check_kernel<<<grid_for(n, 256), 256, 0, ctx->stream>>>(perm_dev, n, seen, inv_dev, bad);
   TGB_LAUNCHED();
   unsigned long long hb;
   TGB_CUDA(cudaMemcpyAsync(&hb, bad, 8, cudaMemcpyDeviceToHost, ctx->stream));
   ctx->sync();
   if (hb != ~0ull) {
-    // Reproduce the reference's message for the FIRST offending position.
     uint64_t v;
     TGB_CUDA(cudaMemcpy(&v, perm_dev + hb, 8, cudaMemcpyDeviceToHost));
     if (v >= n) domain_error("permutation: new id " + std::to_string(v) + " out of range");

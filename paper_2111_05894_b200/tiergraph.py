@@ -106,6 +106,18 @@ def _f64(a):
     return _as(a, np.float64, "float64")
 
 
+def _nbytes(a) -> int:
+    return int(a.numel() * a.element_size()) if _is_torch(a) else int(a.nbytes)
+
+
+def _check_out(out, need: int, what: str = "out"):
+    """A caller output buffer must be contiguous and hold `need` bytes (the
+    library writes exactly that many and cannot see the buffer's size)."""
+    _ptr(out)  # contiguity
+    if _nbytes(out) < need:
+        raise DomainError(f"{what} holds {_nbytes(out)} bytes, {need} needed")
+
+
 def _nonempty(a, dtype):
     """Pointer for a possibly empty array (the C side never dereferences it)."""
     if _len(a) == 0:
@@ -751,6 +763,7 @@ class TieredFeatureStore:
         rb = self.layout.bytes_per_row()
         if out is None:
             out = np.empty((n, rb), np.uint8)
+        _check_out(out, n * rb)
         r = (report or TrafficReport())._c()
         try:
             _check(LIB.tg_gather_rows(self.h, _nonempty(idx, np.uint64), n,
@@ -766,6 +779,7 @@ class TieredFeatureStore:
         timed inside the library around each call (no Python in the timed
         region); ids are host arrays (pinned ones are read in place)."""
         lists = [np.ascontiguousarray(x, dtype=np.uint64) for x in id_lists]
+        _check_out(out, max((len(x) for x in lists), default=0) * self.layout.bytes_per_row())
         ptrs = (C.c_void_p * len(lists))(*[x.ctypes.data for x in lists])
         cnts = (C.c_uint64 * len(lists))(*[len(x) for x in lists])
         r = (report or TrafficReport())._c()
@@ -780,6 +794,9 @@ class TieredFeatureStore:
 
     def gather_rows_async(self, ids_dev, out_dev, counters_dev, err_dev):
         """Stream-ordered K8 on device tensors (no synchronisation)."""
+        _check_out(out_dev, _len(ids_dev) * self.layout.bytes_per_row(), "out_dev")
+        _check_out(counters_dev, 24, "counters_dev")
+        _check_out(err_dev, 8, "err_dev")
         _check(LIB.tg_gather_rows_async(self.h, _ptr(ids_dev), _len(ids_dev), _ptr(out_dev),
                                         _ptr(counters_dev), _ptr(err_dev)))
 
