@@ -86,6 +86,10 @@ int tg_ctx_create(int device, tg_ctx** out);
 /* Run on a caller-owned stream (e.g. torch.cuda.current_stream()). */
 int tg_ctx_create_on_stream(int device, void* cuda_stream, tg_ctx** out);
 int tg_ctx_destroy(tg_ctx* ctx);
+/* Stream-ordered copy of `bytes` between any two UVA addresses (device, peer
+ * or CUDA-IPC mapped, pinned host): the contiguous block push of a
+ * partitioned PageRank exchange (copy engines over NVLink). */
+int tg_memcpy_async(tg_ctx* ctx, void* dst, const void* src, uint64_t bytes);
 int tg_ctx_sync(tg_ctx* ctx);
 void* tg_ctx_stream(tg_ctx* ctx);
 int tg_ctx_device(tg_ctx* ctx);
@@ -125,6 +129,13 @@ int tg_reverse_pagerank(tg_ctx* ctx, const tg_graph* g, uint32_t iterations, dou
 int tg_weighted_reverse_pagerank(tg_ctx* ctx, const tg_graph* g, uint32_t iterations,
                                  double damp, const uint64_t* tid, uint64_t ntid, double* out);
 
+/* The same, with phase_ms[0] = the device time of the prepare (K2) and
+ * phase_ms[1 + i] = that of step i (K3), CUDA events on the context stream
+ * (measurement entry point; phase_ms has iterations + 1 entries). */
+int tg_weighted_reverse_pagerank_timed(tg_ctx* ctx, const tg_graph* g, uint32_t iterations,
+                                       double damp, const uint64_t* tid, uint64_t ntid,
+                                       double* out, double* phase_ms);
+
 /* Row-partitioned iteration for multi-GPU: the caller owns the
  * exchange (NCCL all-gather of `norm`). norm_in/norm_out/score_out are device
  * vectors of length n; only rows [row_begin,row_end) are written.
@@ -140,6 +151,49 @@ int tg_pagerank_step_async(tg_ctx* ctx, const tg_graph* g, const uint32_t* indeg
                            double damp, const double* norm_in_dev, double* norm_out_dev,
                            double* score_out_dev, uint64_t row_begin, uint64_t row_end,
                            int last);
+
+/* ----------------------------------------------- partitioned (multi-GPU) K1/K3
+ * SURVEY §8e. Edge-balanced contiguous row blocks: bounds[0..parts] with
+ * bounds[r] = the first row whose offset reaches ceil(r*E/parts) (host
+ * offsets, n+1 values). */
+int tg_row_blocks(const uint64_t* offsets, uint64_t n, uint32_t parts, uint64_t* bounds);
+/* A ROW-BLOCK graph: rows [row_begin, row_end) only (one rank's shard).
+ * offsets: the whole graph's n+1 (host|device); targets: the whole array
+ * (host|device), of which only the block's edges are uploaded. Its in-degrees
+ * count the block's edges only (the K1 shard; sum them over the ranks).
+ * Valid with tg_pagerank_step_async over sub-ranges of the block,
+ * tg_in_degrees_u32_async and tg_measure_gather_floor_us; whole-graph calls
+ * (PageRank, degree_score, sampler, transpose) return TG_ERR_DOMAIN. */
+int tg_graph_create_rows(tg_ctx* ctx, const uint64_t* offsets, const uint64_t* targets,
+                         uint64_t n, uint64_t e, uint64_t row_begin, uint64_t row_end,
+                         tg_graph** out);
+int tg_graph_row_range(const tg_graph* g, uint64_t* row_begin, uint64_t* row_end);
+/* In-degrees over the edges g holds (u32, device, length n), stream-ordered. */
+int tg_in_degrees_u32_async(tg_ctx* ctx, const tg_graph* g, uint32_t* out_dev);
+/* norm0 (device, length n) from FINAL in-degrees indeg_dev (e.g. the summed
+ * shards); tid_dev NULL = unweighted. Train ids >= n: TG_ERR_DOMAIN (one
+ * synchronisation). */
+int tg_pagerank_init_async(tg_ctx* ctx, uint64_t n, const uint64_t* tid_dev, uint64_t ntid,
+                           const uint32_t* indeg_dev, double* norm0_dev);
+
+/* Partitioned PageRank over several devices of ONE process (what the C++
+ * drop-in runs when TIERGRAPH_DEVICES lists several devices). Each device
+ * holds one edge-balanced row block; K1 is sharded and summed over the devices
+ * once; each K3 step pushes every device's block of the next vector to the
+ * others as one contiguous peer copy per peer (copy engines over NVLink).
+ * Bit-identical to one device for any device count. ctxs: distinct contexts
+ * (devices may repeat: virtual devices on one GPU). */
+typedef struct tg_mgraph tg_mgraph;
+int tg_mgraph_create(tg_ctx* const* ctxs, uint32_t ndev, const uint64_t* offsets,
+                     const uint64_t* targets, uint64_t n, uint64_t e, tg_mgraph** out);
+int tg_mgraph_destroy(tg_mgraph* m);
+/* bounds[ndev+1], edges[ndev] per block, indeg_ms = sharded K1 + reduction. */
+int tg_mgraph_info(const tg_mgraph* m, uint64_t* bounds, uint64_t* edges, double* indeg_ms);
+int tg_mgraph_in_degrees(tg_mgraph* m, uint64_t* out);
+/* weighted != 0: scoring.cpp:86-102 with tid (host|device); else :78-84.
+ * out: n f64 (host or device of the first context). */
+int tg_mgraph_pagerank(tg_mgraph* m, uint32_t iterations, double damp, const uint64_t* tid,
+                       uint64_t ntid, int weighted, double* out);
 
 /* Fused exchange for a partitioned run: the step
  * also stores each of its rows into every peer's norm_out / score_out vector
@@ -340,8 +394,15 @@ int tg_measure_host_rows_us(tg_ctx* ctx, const void* host, uint64_t region_rows,
                             uint64_t row_bytes, uint64_t rows, int reps, double* us);
 int tg_measure_hbm_copy_gbps(tg_ctx* ctx, uint64_t bytes, int reps, double* gbps);
 /* The memory-system floor of one K3 step on graph g: the same E gathers
- * x[targets[e]] with no summation-order constraint (best of reps, us). */
+ * x[targets[e]] with no summation-order constraint (best of reps, us), in
+ * the labelling K3 runs on (the relabelled twin when enabled; reps < 0:
+ * |reps| repetitions in g's own labelling). */
 int tg_measure_gather_floor_us(tg_ctx* ctx, const tg_graph* g, int reps, double* us);
+/* K3 relabelling: whether the PageRank entry points run on g's
+ * twin renumbered by in-degree (TIERGRAPH_PR_RELABEL=0|1, default: when the
+ * norm vector exceeds half of L2), building it now if so; build_ms = the
+ * one-time device time of that build. Results are bit-identical either way. */
+int tg_pagerank_relabel_info(tg_ctx* ctx, const tg_graph* g, int* relabelled, double* build_ms);
 
 /* ------------------------------------------------ host-side input producers
  * Not the hot path: the reference's CPU producers of the gather's id lists,

@@ -60,6 +60,7 @@ SIGNATURES = {
     "tg_ctx_create_on_stream": (I32, [I32, vp, C.POINTER(vp)]),
     "tg_ctx_destroy": (I32, [vp]),
     "tg_ctx_sync": (I32, [vp]),
+    "tg_memcpy_async": (I32, [vp, vp, vp, U64]),
     "tg_ctx_stream": (vp, [vp]),
     "tg_ctx_device": (I32, [vp]),
     "tg_default_device": (I32, []),
@@ -133,6 +134,18 @@ SIGNATURES = {
     "tg_epoch_minibatches": (I32, [vp, vp, U64, vp, U64, vp, U32, U64, U64, U64, U64, U64, I32,
                                    C.POINTER(vp), C.POINTER(U64), C.POINTER(vp)]),
     "tg_measure_gather_floor_us": (I32, [vp, vp, I32, C.POINTER(D)]),
+    "tg_weighted_reverse_pagerank_timed": (I32, [vp, vp, U32, D, vp, U64, vp, vp]),
+    "tg_row_blocks": (I32, [vp, U64, U32, vp]),
+    "tg_graph_create_rows": (I32, [vp, vp, vp, U64, U64, U64, U64, C.POINTER(vp)]),
+    "tg_graph_row_range": (I32, [vp, C.POINTER(U64), C.POINTER(U64)]),
+    "tg_in_degrees_u32_async": (I32, [vp, vp, vp]),
+    "tg_pagerank_init_async": (I32, [vp, U64, vp, U64, vp, vp]),
+    "tg_mgraph_create": (I32, [vp, U32, vp, vp, U64, U64, C.POINTER(vp)]),
+    "tg_mgraph_destroy": (I32, [vp]),
+    "tg_mgraph_info": (I32, [vp, vp, vp, C.POINTER(D)]),
+    "tg_mgraph_in_degrees": (I32, [vp, vp]),
+    "tg_mgraph_pagerank": (I32, [vp, U32, D, vp, U64, I32, vp]),
+    "tg_pagerank_relabel_info": (I32, [vp, vp, C.POINTER(I32), C.POINTER(D)]),
     "tg_sampler_create": (I32, [vp, vp, C.POINTER(vp)]),
     "tg_sampler_destroy": (I32, [vp]),
     "tg_sample_minibatch": (I32, [vp, vp, U64, vp, U32, U64, U64, U64, vp, U64, C.POINTER(U64)]),

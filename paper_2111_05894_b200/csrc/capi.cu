@@ -214,6 +214,14 @@ int tg_ctx_destroy(tg_ctx* c) {
   return TG_OK;
 }
 
+int tg_memcpy_async(tg_ctx* c, void* dst, const void* src, uint64_t bytes) {
+  return guard([&] {
+    if (!bytes) return;
+    DeviceGuard dg(c->device);
+    TGB_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDefault, c->stream));
+  });
+}
+
 int tg_ctx_sync(tg_ctx* c) {
   return guard([&] { c->sync(); });
 }

@@ -221,6 +221,10 @@ void check_permutation(tg_ctx* ctx, const uint64_t* perm_dev, uint64_t n, uint32
 // schedule). Stream-ordered; uses private temporaries, not scratch slots.
 void sort_rows_by_length(tg_ctx* ctx, const uint32_t* off, uint64_t rb, uint64_t re,
                          uint32_t* order_dev);
+// Ids [0, n) ordered by val[id] descending, ties by id (stable radix sort).
+void sort_ids_by_value_desc(tg_ctx* ctx, const uint32_t* val, uint64_t n, uint32_t* order_dev);
+// In-place exclusive prefix sum of n u64 values (device).
+void exclusive_scan_u64(tg_ctx* ctx, uint64_t* data, uint64_t n);
 // Mean us to read `rows` random rows of [0, region_rows) (R bytes at
 // `stride`) from device-visible memory, L2 flushed before each launch.
 double measure_rows_us(tg_ctx* ctx, const uint8_t* src_dev, uint64_t region_rows, uint64_t stride,

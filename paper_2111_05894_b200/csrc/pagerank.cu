@@ -26,25 +26,8 @@
 #include <vector>
 
 #include "internal.cuh"
+#include "pagerank_internal.cuh"
 #include "store_internal.cuh"
-
-struct tg_graph {
-  tg_ctx* ctx = nullptr;
-  uint64_t n = 0, e = 0;
-  uint32_t* off = nullptr;     // n+1, u32
-  uint32_t* tgt = nullptr;     // e, u32
-  uint32_t* indeg = nullptr;   // in_degrees (csr_graph.cpp:89-93), built with the device graph
-  // K3 schedules: rows of [rb, re) by length descending (ties by id), split
-  // into the three row classes. [0, n) is built with the graph; row ranges
-  // of a partitioned (multi-GPU) run are built on first use.
-  struct Sched {
-    uint64_t rb, re;
-    uint32_t* order;
-    uint32_t nA, nB;  // order[0,nA): len > kLenA; [nA,nB): kLenB < len <= kLenA
-    uint32_t nLong;   // order[0,nLong): len > kHubLong (512-thread class-A CTAs)
-  };
-  std::vector<Sched> scheds;
-};
 
 namespace tgb {
 
@@ -161,12 +144,49 @@ __global__ void degree_score_kernel(const uint32_t* __restrict__ off, uint64_t n
 // Train-id multiplicities (a TrainIdSet normally holds unique ids, but the
 // reference multiplies once per listed id, scoring.cpp:97-100).
 __global__ void train_mult_kernel(const uint64_t* __restrict__ tid, uint64_t ntid, uint64_t n,
+                                  const uint32_t* __restrict__ relabel,
                                   uint32_t* __restrict__ mult, unsigned long long* bad) {
   for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < ntid;
        i += (uint64_t)gridDim.x * blockDim.x) {
     const uint64_t id = tid[i];
     if (id >= n) atomicMin(bad, (unsigned long long)i);
-    else atomicAdd(&mult[id], 1u);
+    else atomicAdd(&mult[relabel ? relabel[id] : id], 1u);
+  }
+}
+
+// ------------------------------------------------------- K3 relabel twin
+__global__ void twin_lens_kernel(const uint32_t* __restrict__ off, const uint32_t* __restrict__ old_of,
+                                 const uint32_t* __restrict__ indeg, uint64_t n,
+                                 uint64_t* __restrict__ lens, uint32_t* __restrict__ new_of,
+                                 uint32_t* __restrict__ indeg_tw) {
+  for (uint64_t v = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; v < n;
+       v += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t u = old_of[v];
+    lens[v] = off[u + 1] - off[u];
+    new_of[u] = static_cast<uint32_t>(v);
+    indeg_tw[v] = indeg[u];
+  }
+}
+
+__global__ void narrow_u64_kernel(const uint64_t* __restrict__ in, uint32_t* __restrict__ out,
+                                  uint64_t n) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+       i += (uint64_t)gridDim.x * blockDim.x)
+    out[i] = static_cast<uint32_t>(in[i]);
+}
+
+// one warp per twin row: copy old row old_of[v] with targets renamed
+__global__ void twin_rows_kernel(const uint32_t* __restrict__ off, const uint32_t* __restrict__ tgt,
+                                 const uint32_t* __restrict__ old_of,
+                                 const uint32_t* __restrict__ new_of, uint64_t n,
+                                 const uint32_t* __restrict__ off_tw, uint32_t* __restrict__ tgt_tw) {
+  const int lane = threadIdx.x & 31;
+  const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+  for (uint64_t v = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5; v < n; v += nw) {
+    const uint32_t u = old_of[v];
+    const uint32_t b = off[u], len = off[u + 1] - b;
+    uint32_t* dst = tgt_tw + off_tw[v];
+    for (uint32_t i = lane; i < len; i += 32) dst[i] = new_of[__ldcs(tgt + b + i)];
   }
 }
 
@@ -199,6 +219,7 @@ struct PrStepArgs {
   uint64_t row_begin, row_end;
   double base, damp;
   int last;
+  const uint32_t* score_index;  // last step: score of row r goes to score_out[score_index[r]]
   // fused exchange: the same row also goes to every peer's norm / score
   // vector (NVLink P2P stores), replacing the all-gather of a partitioned run
   uint32_t n_peers;
@@ -229,7 +250,7 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
 __device__ __forceinline__ void finish_row(const PrStepArgs& a, uint64_t r, double acc) {
   const double nx = __dadd_rn(a.base, __dmul_rn(a.damp, acc));  // scoring.cpp:69, no FMA
   if (a.last) {
-    a.score_out[r] = nx;
+    a.score_out[a.score_index ? a.score_index[r] : r] = nx;
     for (uint32_t p = 0; p < a.n_peers; ++p) a.peer_score[p][r] = nx;
   } else {
     const uint32_t d = a.deg[r];
@@ -750,11 +771,13 @@ void compute_indeg(tg_ctx* ctx, const tg_graph* g, uint32_t* deg) {
 // Prepares deg + norm0 for the weighted (tid != nullptr) or plain recurrence.
 // Out-of-range train ids set *bad (min index) and are skipped; the caller
 // checks it after the run (no synchronisation here).
-void pagerank_prepare(tg_ctx* ctx, const tg_graph* g, const uint64_t* tid_dev, uint64_t ntid,
-                      uint32_t* deg, double* norm0, unsigned long long* bad) {
-  const uint64_t n = g->n;
-  if (deg != g->indeg)
-    TGB_CUDA(cudaMemcpyAsync(deg, g->indeg, 4 * n, cudaMemcpyDeviceToDevice, ctx->stream));
+// norm0[j] = score0[j] / max(deg[j],1) from final in-degrees `deg` (K2).
+// Out-of-range train ids set *bad (min index) and are skipped; the caller
+// checks it after the run (no synchronisation here). `relabel` maps train ids
+// into a relabelled twin's ids.
+void pagerank_init(tg_ctx* ctx, uint64_t n, const uint64_t* tid_dev, uint64_t ntid,
+                   const uint32_t* deg, double* norm0, unsigned long long* bad,
+                   const uint32_t* relabel) {
   const double init = 1.0 / static_cast<double>(n);  // scoring.cpp:96
   double weight = 1.0;
   uint32_t* mult = nullptr;
@@ -762,11 +785,25 @@ void pagerank_prepare(tg_ctx* ctx, const tg_graph* g, const uint64_t* tid_dev, u
     weight = static_cast<double>(n) / static_cast<double>(ntid);  // scoring.cpp:94-95
     mult = ctx->scratch_t<uint32_t>(kScratchF, n);
     TGB_CUDA(cudaMemsetAsync(mult, 0, sizeof(uint32_t) * n, ctx->stream));
-    train_mult_kernel<<<grid_for(ntid, 256), 256, 0, ctx->stream>>>(tid_dev, ntid, n, mult, bad);
+    train_mult_kernel<<<grid_for(ntid, 256), 256, 0, ctx->stream>>>(tid_dev, ntid, n, relabel,
+                                                                     mult, bad);
     TGB_LAUNCHED();
   }
   pr_init_kernel<<<grid_for(n, 256), 256, 0, ctx->stream>>>(deg, mult, n, init, weight, norm0);
   TGB_LAUNCHED();
+}
+
+// The same from a whole graph's cached in-degrees (copied into deg when deg
+// is not the graph's own array).
+void pagerank_prepare(tg_ctx* ctx, const tg_graph* g, const uint64_t* tid_dev, uint64_t ntid,
+                      uint32_t* deg, double* norm0, unsigned long long* bad,
+                      const uint32_t* relabel = nullptr) {
+  if (!whole_graph(g))
+    domain_error("pagerank prepare: a row-block graph holds partial in-degrees; sum them "
+                 "over the blocks and use tg_pagerank_init_async");
+  if (deg != g->indeg)
+    TGB_CUDA(cudaMemcpyAsync(deg, g->indeg, 4 * g->n, cudaMemcpyDeviceToDevice, ctx->stream));
+  pagerank_init(ctx, g->n, tid_dev, ntid, deg, norm0, bad, relabel);
 }
 
 const tg_graph::Sched& schedule(tg_ctx* ctx, const tg_graph* g, uint64_t rb, uint64_t re) {
@@ -797,9 +834,13 @@ const tg_graph::Sched& schedule(tg_ctx* ctx, const tg_graph* g, uint64_t rb, uin
 
 void pagerank_step(tg_ctx* ctx, const tg_graph* g, const uint32_t* deg, double damp,
                    const double* nin, double* nout, double* sout, uint64_t rb, uint64_t re,
-                   int last, uint32_t n_peers = 0, double* const* peer_norm = nullptr,
-                   double* const* peer_score = nullptr) {
+                   int last, uint32_t n_peers, double* const* peer_norm,
+                   double* const* peer_score, const uint32_t* score_index) {
   if (re <= rb) return;
+  if (rb < g->rb || re > g->re)
+    domain_error("pagerank step: rows [" + std::to_string(rb) + ", " + std::to_string(re) +
+                 ") are not held by this graph (rows [" + std::to_string(g->rb) + ", " +
+                 std::to_string(g->re) + "))");
   const tg_graph::Sched& sc = schedule(ctx, g, rb, re);
   PrStepArgs a;
   a.off = g->off;
@@ -819,6 +860,7 @@ void pagerank_step(tg_ctx* ctx, const tg_graph* g, const uint32_t* deg, double d
   a.base = (1.0 - damp) / static_cast<double>(g->n);  // scoring.cpp:53
   a.damp = damp;
   a.last = last;
+  a.score_index = score_index;
   a.n_peers = n_peers;
   for (uint32_t p = 0; p < TG_MAX_DEVICES; ++p) {
     a.peer_norm[p] = p < n_peers ? peer_norm[p] : nullptr;
@@ -856,6 +898,76 @@ void pagerank_step(tg_ctx* ctx, const tg_graph* g, const uint32_t* deg, double d
   if (sc.nA) ctx->join();
 }
 
+// TIERGRAPH_PR_RELABEL: "0" never, "1" always, default: when the norm vector
+// (8 B per node) is larger than half of L2, i.e. when K3's random gathers
+// miss L2 (C3/C4), not at C1/C2 where the whole vector stays resident.
+bool relabel_wanted(const tg_ctx* ctx, const tg_graph* g) {
+  if (!whole_graph(g)) return false;
+  if (const char* e = std::getenv("TIERGRAPH_PR_RELABEL")) return e[0] == '1';
+  int l2 = 0;
+  cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, ctx->device);
+  return g->n > 1 && 8.0 * static_cast<double>(g->n) > 0.5 * static_cast<double>(l2);
+}
+
+// Builds g->twin (see tg_graph). One-time per graph: a radix sort of N keys,
+// a scan, and one pass over the targets (12E + 24N bytes).
+const tg_graph* relabel_twin(tg_ctx* ctx, const tg_graph* gc) {
+  auto* g = const_cast<tg_graph*>(gc);
+  if (g->twin || g->twin_tried) return g->twin;
+  g->twin_tried = true;
+  if (!relabel_wanted(ctx, g)) return nullptr;
+  const uint64_t n = g->n, e = g->e;
+  cudaEvent_t ev0, ev1;
+  TGB_CUDA(cudaEventCreate(&ev0));
+  TGB_CUDA(cudaEventCreate(&ev1));
+  TGB_CUDA(cudaEventRecord(ev0, ctx->stream));
+  auto* t = new tg_graph;
+  t->ctx = ctx;
+  t->n = n;
+  t->e = e;
+  uint64_t* lens = nullptr;
+  try {
+    TGB_CUDA(cudaMalloc(&g->old_of, 4 * n));
+    TGB_CUDA(cudaMalloc(&g->new_of, 4 * n));
+    TGB_CUDA(cudaMalloc(&t->off, 4 * (n + 1)));
+    TGB_CUDA(cudaMalloc(&t->tgt, 4 * std::max<uint64_t>(e, 1)));
+    TGB_CUDA(cudaMalloc(&t->indeg, 4 * n));
+    TGB_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&lens), 8 * (n + 1), ctx->stream));
+    sort_ids_by_value_desc(ctx, g->indeg, n, g->old_of);
+    twin_lens_kernel<<<grid_for(n, 256), 256, 0, ctx->stream>>>(g->off, g->old_of, g->indeg, n,
+                                                                lens, g->new_of, t->indeg);
+    TGB_LAUNCHED();
+    TGB_CUDA(cudaMemsetAsync(lens + n, 0, 8, ctx->stream));
+    exclusive_scan_u64(ctx, lens, n + 1);
+    narrow_u64_kernel<<<grid_for(n + 1, 256), 256, 0, ctx->stream>>>(lens, t->off, n + 1);
+    TGB_LAUNCHED();
+    TGB_CUDA(cudaFreeAsync(lens, ctx->stream));
+    lens = nullptr;
+    if (e) {
+      twin_rows_kernel<<<grid_for(n * 32, 256, ctx->num_sms * 16), 256, 0, ctx->stream>>>(
+          g->off, g->tgt, g->old_of, g->new_of, n, t->off, t->tgt);
+      TGB_LAUNCHED();
+    }
+    schedule(ctx, t, 0, n);
+    TGB_CUDA(cudaEventRecord(ev1, ctx->stream));
+    TGB_CUDA(cudaEventSynchronize(ev1));
+    TGB_CUDA(cudaEventElapsedTime(&g->twin_ms, ev0, ev1));
+  } catch (...) {
+    if (lens) cudaFree(lens);
+    tg_graph_destroy(t);
+    cudaFree(g->old_of);
+    cudaFree(g->new_of);
+    g->old_of = g->new_of = nullptr;
+    cudaEventDestroy(ev0);
+    cudaEventDestroy(ev1);
+    throw;
+  }
+  cudaEventDestroy(ev0);
+  cudaEventDestroy(ev1);
+  g->twin = t;
+  return t;
+}
+
 void check_config(uint32_t iterations, double damp) {  // scoring.cpp:42-47
   if (iterations < 1) domain_error("pagerank: iterations must be >= 1");
   if (!(damp > 0.0 && damp < 1.0))
@@ -863,7 +975,8 @@ void check_config(uint32_t iterations, double damp) {  // scoring.cpp:42-47
 }
 
 void run_pagerank(tg_ctx* ctx, const tg_graph* g, uint32_t iterations, double damp,
-                  const uint64_t* tid, uint64_t ntid, bool weighted, double* out) {
+                  const uint64_t* tid, uint64_t ntid, bool weighted, double* out,
+                  double* phase_ms = nullptr) {
   check_config(iterations, damp);
   if (weighted && ntid == 0)
     domain_error(
@@ -871,19 +984,46 @@ void run_pagerank(tg_ctx* ctx, const tg_graph* g, uint32_t iterations, double da
         "use reverse_pagerank when no nodes are labeled");  // scoring.cpp:89-91
   const uint64_t n = g ? g->n : 0;
   if (n == 0) return;
+  if (!whole_graph(g))
+    domain_error("pagerank: this graph holds only rows [" + std::to_string(g->rb) + ", " +
+                 std::to_string(g->re) + "); run the partitioned entry points");
   DeviceGuard dg(ctx->device);
   const uint64_t* tid_dev = weighted ? dev_in(ctx, tid, ntid, kStageIn0) : nullptr;
-  uint32_t* deg = g->indeg;  // cached with the device graph
+  // the relabelled twin when enabled (bit-identical results; scores are
+  // written back to the original ids by the last step's epilogue)
+  const tg_graph* tw = relabel_twin(ctx, g);
+  const tg_graph* run = tw ? tw : g;
+  uint32_t* deg = run->indeg;  // cached with the device graph
   double* na = ctx->scratch_t<double>(kScratchB, n);
   double* nb = ctx->scratch_t<double>(kScratchC, n);
   DevOut<double> o(ctx, out, n, kStageOut0);
   auto* bad = ctx->scratch_t<unsigned long long>(kSmall, 1);
   if (weighted) TGB_CUDA(cudaMemsetAsync(bad, 0xff, 8, ctx->stream));
-  pagerank_prepare(ctx, g, tid_dev, ntid, deg, na, bad);
+  // phase_ms (optional, [iterations + 1]): device time of the prepare and of
+  // every step, CUDA events on the stream
+  std::vector<cudaEvent_t> ev;
+  if (phase_ms) {
+    ev.resize(iterations + 2);
+    for (auto& x : ev) TGB_CUDA(cudaEventCreate(&x));
+    TGB_CUDA(cudaEventRecord(ev[0], ctx->stream));
+  }
+  pagerank_prepare(ctx, run, tid_dev, ntid, deg, na, bad, tw ? g->new_of : nullptr);
+  if (phase_ms) TGB_CUDA(cudaEventRecord(ev[1], ctx->stream));
   for (uint32_t it = 0; it < iterations; ++it) {
     const bool last = it + 1 == iterations;
-    pagerank_step(ctx, g, deg, damp, na, nb, o.dev(), 0, n, last ? 1 : 0);
+    pagerank_step(ctx, run, deg, damp, na, nb, o.dev(), 0, n, last ? 1 : 0, 0, nullptr, nullptr,
+                  tw ? g->old_of : nullptr);
+    if (phase_ms) TGB_CUDA(cudaEventRecord(ev[it + 2], ctx->stream));
     std::swap(na, nb);
+  }
+  if (phase_ms) {
+    TGB_CUDA(cudaEventSynchronize(ev.back()));
+    for (uint32_t i = 0; i <= iterations; ++i) {
+      float ms = 0;
+      TGB_CUDA(cudaEventElapsedTime(&ms, ev[i], ev[i + 1]));
+      phase_ms[i] = ms;
+    }
+    for (auto& x : ev) cudaEventDestroy(x);
   }
   unsigned long long hb = ~0ull;
   if (weighted) TGB_CUDA(cudaMemcpyAsync(&hb, bad, 8, cudaMemcpyDeviceToHost, ctx->stream));
@@ -904,6 +1044,8 @@ void graph_from_device(tg_ctx* ctx, const uint64_t* doff, uint32_t* tgt, uint64_
   g->ctx = ctx;
   g->n = n;
   g->e = e;
+  g->rb = 0;
+  g->re = n;
   g->tgt = tgt;  // owned from here on
   try {
     TGB_CUDA(cudaMalloc(&g->off, sizeof(uint32_t) * (n + 1)));
@@ -974,9 +1116,127 @@ int tg_graph_create(tg_ctx* ctx, const uint64_t* offsets, const uint64_t* target
   });
 }
 
+int tg_pagerank_relabel_info(tg_ctx* ctx, const tg_graph* g, int* relabelled, double* build_ms) {
+  return guard([&] {
+    DeviceGuard dg(ctx->device);
+    const tg_graph* tw = g->n ? relabel_twin(ctx, g) : nullptr;
+    if (relabelled) *relabelled = tw ? 1 : 0;
+    if (build_ms) *build_ms = tw ? g->twin_ms : 0.0;
+  });
+}
+
+// A row-block graph: rows [row_begin, row_end) of the CSR only (SURVEY §8e,
+// the shard of one rank of a partitioned PageRank). Offsets are the whole
+// graph's (n+1, host or device u64); targets the whole array (host or
+// device), of which only this block's edges are read and uploaded.
+int tg_graph_create_rows(tg_ctx* ctx, const uint64_t* offsets, const uint64_t* targets,
+                         uint64_t n, uint64_t e, uint64_t row_begin, uint64_t row_end,
+                         tg_graph** out) {
+  return guard([&] {
+    if (!ctx || !out) domain_error("tg_graph_create_rows: null argument");
+    if (n >= 0xffffffffull || e >= 0xffffffffull)
+      domain_error("tg_graph_create_rows: n and e must be < 2^32 for the u32 device layout");
+    if (row_begin > row_end || row_end > n)
+      domain_error("tg_graph_create_rows: bad row range [" + std::to_string(row_begin) + ", " +
+                   std::to_string(row_end) + ") of " + std::to_string(n) + " rows");
+    DeviceGuard dg(ctx->device);
+    const uint64_t m = row_end - row_begin;
+    // this block's offsets (m + 1 values) and its edge range
+    std::vector<uint64_t> ho(m + 1);
+    if (is_device_ptr(offsets)) {
+      TGB_CUDA(cudaMemcpy(ho.data(), offsets + row_begin, 8 * (m + 1), cudaMemcpyDeviceToHost));
+    } else {
+      std::memcpy(ho.data(), offsets + row_begin, 8 * (m + 1));
+    }
+    const uint64_t e0 = ho[0], e1 = ho[m];
+    for (uint64_t i = 0; i <= m; ++i)
+      if (ho[i] > e || (i && ho[i] < ho[i - 1]))
+        format_error("csr: offsets invalid at index " + std::to_string(row_begin + i) +
+                     " (need offsets[0]==0, monotone, offsets[num_nodes]==num_edges)");
+    if ((row_begin == 0 && e0 != 0) || (row_end == n && e1 != e))
+      format_error("csr: offsets invalid at index " + std::to_string(row_begin == 0 && e0 ? 0 : n) +
+                   " (need offsets[0]==0, monotone, offsets[num_nodes]==num_edges)");
+    auto* g = new tg_graph;
+    g->ctx = ctx;
+    g->n = n;
+    g->e = e1 - e0;
+    g->rb = row_begin;
+    g->re = row_end;
+    try {
+      std::vector<uint32_t> o32(m + 1);
+      for (uint64_t i = 0; i <= m; ++i) o32[i] = static_cast<uint32_t>(ho[i] - e0);
+      TGB_CUDA(cudaMalloc(&g->off_alloc, 4 * (m + 1)));
+      TGB_CUDA(cudaMemcpy(g->off_alloc, o32.data(), 4 * (m + 1), cudaMemcpyHostToDevice));
+      g->off = g->off_alloc - row_begin;  // off[r] for r in [row_begin, row_end]
+      TGB_CUDA(cudaMalloc(&g->tgt, 4 * std::max<uint64_t>(g->e, 1)));
+      auto* bad = ctx->scratch_t<unsigned long long>(kSmall, 2);
+      TGB_CUDA(cudaMemsetAsync(bad + 1, 0xff, 8, ctx->stream));
+      const bool tdev = is_device_ptr(targets);
+      const uint64_t chunk = tdev ? std::max<uint64_t>(g->e, 1) : (32ull << 20);
+      for (uint64_t base = 0; base < g->e; base += chunk) {
+        const uint64_t cnt = std::min(chunk, g->e - base);
+        const uint64_t* src = targets + e0 + base;
+        if (!tdev) {
+          auto* st = ctx->scratch_t<uint64_t>(kStageIn1, cnt);
+          TGB_CUDA(cudaMemcpyAsync(st, src, cnt * 8, cudaMemcpyHostToDevice, ctx->stream));
+          src = st;
+        }
+        narrow_targets_kernel<<<grid_for(cnt, 256), 256, 0, ctx->stream>>>(src, g->tgt + base, cnt,
+                                                                           e0 + base, n, bad + 1);
+        TGB_LAUNCHED();
+      }
+      unsigned long long hb;
+      TGB_CUDA(cudaMemcpyAsync(&hb, bad + 1, 8, cudaMemcpyDeviceToHost, ctx->stream));
+      ctx->sync();
+      if (hb != ~0ull) format_error("csr: target out of range at edge " + std::to_string(hb));
+      if (m) schedule(ctx, g, row_begin, row_end);
+      TGB_CUDA(cudaMalloc(&g->indeg, 4 * std::max<uint64_t>(n, 1)));
+      compute_indeg(ctx, g, g->indeg);  // partial: this block's edges only
+      ctx->sync();
+    } catch (...) {
+      tg_graph_destroy(g);
+      throw;
+    }
+    *out = g;
+  });
+}
+
+int tg_in_degrees_u32_async(tg_ctx* ctx, const tg_graph* g, uint32_t* out_dev) {
+  return guard([&] {
+    if (!g->n) return;
+    DeviceGuard dg(ctx->device);
+    TGB_CUDA(cudaMemcpyAsync(out_dev, g->indeg, 4 * g->n, cudaMemcpyDeviceToDevice, ctx->stream));
+  });
+}
+
+int tg_pagerank_init_async(tg_ctx* ctx, uint64_t n, const uint64_t* tid_dev, uint64_t ntid,
+                           const uint32_t* indeg_dev, double* norm0_dev) {
+  return guard([&] {
+    if (tid_dev && ntid == 0) domain_error("weighted reverse pagerank needs a non-empty train id set");
+    if (!n) return;
+    DeviceGuard dg(ctx->device);
+    auto* bad = ctx->scratch_t<unsigned long long>(kSmall, 1);
+    if (tid_dev) TGB_CUDA(cudaMemsetAsync(bad, 0xff, 8, ctx->stream));
+    pagerank_init(ctx, n, tid_dev, ntid, indeg_dev, norm0_dev, bad);
+    if (!tid_dev) return;
+    unsigned long long hb = ~0ull;
+    TGB_CUDA(cudaMemcpyAsync(&hb, bad, 8, cudaMemcpyDeviceToHost, ctx->stream));
+    ctx->sync();
+    if (hb != ~0ull) {
+      uint64_t id = 0;
+      TGB_CUDA(cudaMemcpy(&id, tid_dev + hb, sizeof(id), cudaMemcpyDeviceToHost));
+      domain_error("train id " + std::to_string(id) + " out of range");  // scoring.cpp:98
+    }
+  });
+}
+
 int tg_measure_gather_floor_us(tg_ctx* ctx, const tg_graph* g, int reps, double* us) {
   return guard([&] {
     DeviceGuard dg(ctx->device);
+    // K3's labelling (the twin when enabled); reps < 0: g's own labelling
+    if (reps >= 0)
+      if (const tg_graph* tw = g->n ? relabel_twin(ctx, g) : nullptr) g = tw;
+    reps = std::abs(reps);
     double* x = ctx->scratch_t<double>(kScratchA, std::max<uint64_t>(g->n, 1) + 1);
     TGB_CUDA(cudaMemsetAsync(x, 0, 8 * (g->n + 1), ctx->stream));
     cudaEvent_t a, b;
@@ -1001,7 +1261,10 @@ int tg_measure_gather_floor_us(tg_ctx* ctx, const tg_graph* g, int reps, double*
 
 int tg_graph_destroy(tg_graph* g) {
   if (!g) return TG_OK;
-  cudaFree(g->off);
+  tg_graph_destroy(g->twin);
+  cudaFree(g->old_of);
+  cudaFree(g->new_of);
+  cudaFree(g->off_alloc ? g->off_alloc : g->off);
   cudaFree(g->tgt);
   for (auto& sc : g->scheds) cudaFree(sc.order);
   cudaFree(g->indeg);
@@ -1011,12 +1274,25 @@ int tg_graph_destroy(tg_graph* g) {
 
 uint64_t tg_graph_num_nodes(const tg_graph* g) { return g ? g->n : 0; }
 uint64_t tg_graph_num_edges(const tg_graph* g) { return g ? g->e : 0; }
-const uint32_t* tg_graph_offsets32(const tg_graph* g) { return g ? g->off : nullptr; }
-const uint32_t* tg_graph_targets32(const tg_graph* g) { return g ? g->tgt : nullptr; }
+// whole graphs only (a row block's arrays are not indexable by node id)
+const uint32_t* tg_graph_offsets32(const tg_graph* g) {
+  return g && whole_graph(g) ? g->off : nullptr;
+}
+const uint32_t* tg_graph_targets32(const tg_graph* g) {
+  return g && whole_graph(g) ? g->tgt : nullptr;
+}
+int tg_graph_row_range(const tg_graph* g, uint64_t* row_begin, uint64_t* row_end) {
+  return guard([&] {
+    if (!g) domain_error("tg_graph_row_range: null graph");
+    if (row_begin) *row_begin = g->rb;
+    if (row_end) *row_end = g->re;
+  });
+}
 
 int tg_degree_score(tg_ctx* ctx, const tg_graph* g, double* out) {
   return guard([&] {
     if (!g->n) return;
+    if (!whole_graph(g)) domain_error("degree_score: needs a whole graph, not a row block");
     DeviceGuard dg(ctx->device);
     DevOut<double> o(ctx, out, g->n, kStageOut0);
     degree_score_kernel<<<grid_for(g->n, 256), 256, 0, ctx->stream>>>(g->off, g->n, o.dev());
@@ -1046,6 +1322,12 @@ int tg_reverse_pagerank(tg_ctx* ctx, const tg_graph* g, uint32_t iterations, dou
 int tg_weighted_reverse_pagerank(tg_ctx* ctx, const tg_graph* g, uint32_t iterations,
                                  double damp, const uint64_t* tid, uint64_t ntid, double* out) {
   return guard([&] { run_pagerank(ctx, g, iterations, damp, tid, ntid, true, out); });
+}
+
+int tg_weighted_reverse_pagerank_timed(tg_ctx* ctx, const tg_graph* g, uint32_t iterations,
+                                       double damp, const uint64_t* tid, uint64_t ntid,
+                                       double* out, double* phase_ms) {
+  return guard([&] { run_pagerank(ctx, g, iterations, damp, tid, ntid, true, out, phase_ms); });
 }
 
 int tg_pagerank_prepare_async(tg_ctx* ctx, const tg_graph* g, const uint64_t* tid_dev,

@@ -291,7 +291,10 @@ __global__ void perm_kernel(const uint32_t* __restrict__ v0, const uint32_t* __r
 // K3 schedule: keys = ~len (u32 in a u64 key) of rows [rb, rb+m), vals = the
 // row's offset in the range. Ascending keys = descending lengths; the sort is
 // stable, so equal lengths keep ascending ids.
+// (`val` non-null: key = ~val[rb+i] instead -- ids by a u32 value, descending,
+// ties by id: the K3 relabelling by in-degree.)
 __global__ void __launch_bounds__(256) rowlen_key_kernel(const uint32_t* __restrict__ off,
+                                                         const uint32_t* __restrict__ val,
                                                          uint64_t rb, uint64_t m,
                                                          uint64_t* __restrict__ keys,
                                                          uint32_t* __restrict__ vals,
@@ -301,7 +304,7 @@ __global__ void __launch_bounds__(256) rowlen_key_kernel(const uint32_t* __restr
   __syncthreads();
   for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < m;
        i += (uint64_t)gridDim.x * blockDim.x) {
-    const uint32_t k = ~(off[rb + i + 1] - off[rb + i]);
+    const uint32_t k = val ? ~val[rb + i] : ~(off[rb + i + 1] - off[rb + i]);
     keys[i] = k;
     vals[i] = static_cast<uint32_t>(i);
 #pragma unroll
@@ -326,8 +329,20 @@ __global__ void order_out_kernel(const uint32_t* __restrict__ v0, const uint32_t
     order[i] = static_cast<uint32_t>(rb + v[i]);
 }
 
+static void sort_desc_u32(tg_ctx* ctx, const uint32_t* off, const uint32_t* val, uint64_t rb,
+                          uint64_t re, uint32_t* order_dev);
+
 void sort_rows_by_length(tg_ctx* ctx, const uint32_t* off, uint64_t rb, uint64_t re,
                          uint32_t* order_dev) {
+  sort_desc_u32(ctx, off, nullptr, rb, re, order_dev);
+}
+
+void sort_ids_by_value_desc(tg_ctx* ctx, const uint32_t* val, uint64_t n, uint32_t* order_dev) {
+  sort_desc_u32(ctx, nullptr, val, 0, n, order_dev);
+}
+
+static void sort_desc_u32(tg_ctx* ctx, const uint32_t* off, const uint32_t* val, uint64_t rb,
+                          uint64_t re, uint32_t* order_dev) {
   const uint64_t m = re - rb;
   if (m == 0) return;
   const uint32_t nblk = static_cast<uint32_t>((m + kRsTile - 1) / kRsTile);
@@ -348,8 +363,8 @@ void sort_rows_by_length(tg_ctx* ctx, const uint32_t* off, uint64_t rb, uint64_t
   uint32_t* hist = reinterpret_cast<uint32_t*>(p); p = align(p + 8 * 256 * 4);
   uint32_t* totals = reinterpret_cast<uint32_t*>(p);
   TGB_CUDA(cudaMemsetAsync(hist, 0, 8 * 256 * 4, ctx->stream));
-  rowlen_key_kernel<<<grid_for(m, 256, ctx->num_sms * 8), 256, 0, ctx->stream>>>(off, rb, m, k0,
-                                                                                v0, hist);
+  rowlen_key_kernel<<<grid_for(m, 256, ctx->num_sms * 8), 256, 0, ctx->stream>>>(off, val, rb, m,
+                                                                                k0, v0, hist);
   TGB_LAUNCHED();
   plan_kernel<<<1, 256, 0, ctx->stream>>>(hist, m, plan);
   TGB_LAUNCHED();

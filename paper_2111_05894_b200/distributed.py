@@ -11,7 +11,9 @@ worker count, parallel.hpp:5-7).
 
 Two exchanges are provided:
   * `reverse_pagerank_partitioned` / `weighted_reverse_pagerank_multi`: one
-    process per GPU, an all-gather (NCCL) after every step — the baseline;
+    process per GPU, each holding only its edge-balanced row block; K1
+    sharded (partial in-degrees + one all-reduce); an all-gather (NCCL) of the
+    blocks after every step — the baseline;
   * `weighted_reverse_pagerank_peers`: the fused B200 path — each step's
     epilogue stores its rows straight into every rank's `norm` vector (P2P
     stores over NVLink/NVSwitch), and a device-side arrival barrier
@@ -32,70 +34,144 @@ from typing import Optional, Tuple
 import numpy as np
 
 
+def edge_blocks(offsets, world: int) -> list:
+    """Contiguous row blocks with near-equal EDGE counts: block r starts at the
+    first row whose offset reaches ceil(r * E / world) (the same split as
+    tg_row_blocks). Equal-row blocks put 3.4x the mean edge count on rank 0 of
+    an R-MAT graph; these stay within a row's length of E/world."""
+    off = np.asarray(offsets, np.uint64)
+    n = max(len(off) - 1, 0)
+    e = int(off[-1]) if n else 0
+    b = [0]
+    for r in range(1, world):
+        if e == 0:
+            b.append(n * r // world)
+            continue
+        want = (e * r + world - 1) // world
+        b.append(min(max(int(np.searchsorted(off, np.uint64(want), side="left")), b[-1]), n))
+    b.append(n)
+    return [(b[r], b[r + 1]) for r in range(world)]
+
+
 def row_blocks(n: int, world: int) -> Tuple[int, list]:
-    """Equal row blocks, block r = [r*chunk, min(n, (r+1)*chunk)). Equal sizes
-    let the exchange be one in-place all_gather_into_tensor (padding < world
-    rows)."""
+    """Equal row blocks (the fused IPC exchange's split): block r =
+    [r*chunk, min(n, (r+1)*chunk))."""
     chunk = max(1, math.ceil(n / max(world, 1)))
     return chunk, [(min(n, r * chunk), min(n, (r + 1) * chunk)) for r in range(world)]
 
 
 class DeviceStepper:
-    """K1-K3 of one rank on its GPU, through the C-ABI."""
+    """One rank's shard on its GPU, through the C-ABI: a ROW-BLOCK graph
+    (tg_graph_create_rows: only this rank's rows and edges are uploaded), its
+    partial in-degrees (the K1 shard), the K2 init from the summed in-degrees
+    and the K3 steps over its rows."""
 
-    def __init__(self, g, ctx):
+    def __init__(self, g, ctx, block):
+        import ctypes as C
         import torch
         from . import tiergraph as tg
-        self.torch = torch
-        self.tg = tg
+        from ._lib import LIB
+        self.torch, self.tg, self.LIB = torch, tg, LIB
         self.ctx = ctx
-        self.g = g
-        self.gh = g.device(ctx)
         self.n = g.num_nodes()
+        self.rb, self.re = block
         self.dev = torch.device("cuda", ctx.device)
-        self.deg = torch.empty(max(self.n, 1), dtype=torch.int32, device=self.dev)
+        h = C.c_void_p()
+        tg._check(LIB.tg_graph_create_rows(ctx.h, tg._ptr(g.offsets),
+                                           tg._nonempty(g.targets, np.uint64), self.n,
+                                           g.num_edges(), self.rb, self.re, C.byref(h)))
+        self.gh = h
 
     def alloc(self, count: int):
         return self.torch.empty(count, dtype=self.torch.float64, device=self.dev)
 
-    def prepare(self, tid_dev, ntid: int, norm0) -> None:
-        from ._lib import LIB
-        self.tg._check(LIB.tg_pagerank_prepare_async(
-            self.ctx.h, self.gh, tid_dev.data_ptr() if tid_dev is not None else None, ntid,
-            self.deg.data_ptr(), norm0.data_ptr()))
+    def partial_indeg(self):
+        d = self.torch.empty(max(self.n, 1), dtype=self.torch.int32, device=self.dev)
+        self.tg._check(self.LIB.tg_in_degrees_u32_async(self.ctx.h, self.gh, d.data_ptr()))
+        self.sync()
+        return d
+
+    def init(self, tid_dev, ntid: int, indeg, norm0) -> None:
+        self.indeg = indeg
+        self.tg._check(self.LIB.tg_pagerank_init_async(
+            self.ctx.h, self.n, tid_dev.data_ptr() if tid_dev is not None else None, ntid,
+            indeg.data_ptr(), norm0.data_ptr()))
 
     def step(self, damp: float, nin, nout, sout, rb: int, re: int, last: bool) -> None:
-        from ._lib import LIB
-        self.tg._check(LIB.tg_pagerank_step_async(
-            self.ctx.h, self.gh, self.deg.data_ptr(), float(damp), nin.data_ptr(),
+        self.tg._check(self.LIB.tg_pagerank_step_async(
+            self.ctx.h, self.gh, self.indeg.data_ptr(), float(damp), nin.data_ptr(),
             nout.data_ptr(), sout.data_ptr(), int(rb), int(re), int(last)))
 
     def sync(self) -> None:
         self.ctx.sync()
 
+    def close(self) -> None:
+        if self.gh:
+            self.sync()
+            self.LIB.tg_graph_destroy(self.gh)
+            self.gh = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def _exchange(out, stage, blocks, rank, group):
+    """Every rank's block of `out` to every rank: one all-gather of blocks
+    padded to the longest (NCCL over NVLink/NVSwitch on GPUs), then the blocks
+    back in row order (one device copy each)."""
+    import torch.distributed as dist
+    chunk = len(stage) // len(blocks)
+    rb, re = blocks[rank]
+    mine = stage[rank * chunk:(rank + 1) * chunk]
+    mine[:re - rb].copy_(out[rb:re])
+    if out.is_cuda and dist.get_backend(group) != "nccl":
+        # gloo plumbing (tests, shared-GPU bench mode): stage through the host
+        h = stage.cpu()
+        dist.all_gather_into_tensor(h, h[rank * chunk:(rank + 1) * chunk].clone(), group=group)
+        stage.copy_(h)
+    else:
+        dist.all_gather_into_tensor(stage, mine.clone() if not stage.is_cuda else mine,
+                                    group=group)
+    for q, (b0, b1) in enumerate(blocks):
+        if q != rank and b1 > b0:
+            out[b0:b1].copy_(stage[q * chunk:q * chunk + (b1 - b0)])
+
 
 def reverse_pagerank_partitioned(stepper, n: int, iterations: int, damp: float, tid=None,
-                                 ntid: int = 0, group=None):
-    """Runs the recurrence with rows split over the ranks of `group` and
+                                 ntid: int = 0, group=None, blocks=None):
+    """Runs the recurrence with rows split over the ranks of `group`
+    (edge-balanced `blocks`, one per rank; the stepper holds this rank's) and
     returns the full score vector (length n) on every rank.
 
-    `tid` (a device tensor of train ids, or None for the unweighted
-    recurrence) must be the same on every rank.
+    K1 is sharded: every rank counts the in-degrees of its own edges and the
+    counts are summed with one all-reduce. `tid` (a device tensor of train
+    ids, or None for the unweighted recurrence) must be the same on every rank.
     """
+    import torch
     import torch.distributed as dist
     if iterations < 1:
         from .tiergraph import DomainError
         raise DomainError("pagerank: iterations must be >= 1")  # scoring.cpp:43-44
     world = dist.get_world_size(group) if dist.is_initialized() else 1
     rank = dist.get_rank(group) if dist.is_initialized() else 0
-    chunk, blocks = row_blocks(n, world)
     rb, re = blocks[rank]
-    padded = chunk * world
-    a = stepper.alloc(padded)
-    b = stepper.alloc(padded)
-    scores = stepper.alloc(padded)
-    # norm0 for every row (cheap, identical on every rank: no exchange needed)
-    stepper.prepare(tid, ntid, a)
+    indeg = stepper.partial_indeg()
+    if world > 1:
+        if indeg.is_cuda and dist.get_backend(group) != "nccl":
+            h = indeg.cpu()
+            dist.all_reduce(h, group=group)
+            indeg.copy_(h)
+        else:
+            dist.all_reduce(indeg, group=group)  # K1 all-reduce (sum)
+    a = stepper.alloc(max(n, 1))
+    b = stepper.alloc(max(n, 1))
+    scores = stepper.alloc(max(n, 1))
+    chunk = max(1, max(b1 - b0 for b0, b1 in blocks))
+    stage = stepper.alloc(chunk * world)
+    stepper.init(tid, ntid, indeg, a)  # norm0 for every row (identical on every rank)
     x, y = a, b
     for it in range(iterations):
         last = it + 1 == iterations
@@ -103,22 +179,17 @@ def reverse_pagerank_partitioned(stepper, n: int, iterations: int, damp: float, 
         out = scores if last else y
         if world > 1:
             stepper.sync()  # the step must land before the collective reads it
-            if out.is_cuda and dist.get_backend(group) != "nccl":
-                # gloo plumbing (tests, shared-GPU bench mode): stage through the host
-                h = out.cpu()
-                dist.all_gather_into_tensor(h, h[rank * chunk:(rank + 1) * chunk].clone(),
-                                            group=group)
-                out.copy_(h)
-            else:
-                dist.all_gather_into_tensor(out, out[rank * chunk:(rank + 1) * chunk], group=group)
+            _exchange(out, stage, blocks, rank, group)
         x, y = y, x
     stepper.sync()
     return scores[:n]
 
 
 def weighted_reverse_pagerank_multi(g, cfg, tid, ctx=None, group=None):
-    """scoring.hpp:45-46 on all ranks of `group` (one GPU per rank)."""
+    """scoring.hpp:45-46 on all ranks of `group` (one GPU per rank): each rank
+    uploads only its edge-balanced row block."""
     import torch
+    import torch.distributed as dist
     from . import tiergraph as tg
     ctx = ctx or tg.default_context()
     ids = tid.ids if isinstance(tid, tg.TrainIdSet) else tid
@@ -127,20 +198,40 @@ def weighted_reverse_pagerank_multi(g, cfg, tid, ctx=None, group=None):
                              "use reverse_pagerank when no nodes are labeled")  # scoring.cpp:89-91
     if not (0.0 < cfg.damp < 1.0):
         raise tg.DomainError(f"pagerank: damp must lie in (0,1), got {cfg.damp}")
-    st = DeviceStepper(g, ctx)
-    tid_d = torch.as_tensor(np.asarray(ids, np.uint64).astype(np.int64), device=st.dev)
-    return reverse_pagerank_partitioned(st, g.num_nodes(), cfg.iterations, cfg.damp, tid_d,
-                                        len(ids), group)
+    world = dist.get_world_size(group) if dist.is_initialized() else 1
+    rank = dist.get_rank(group) if dist.is_initialized() else 0
+    blocks = edge_blocks(g.offsets, world)
+    st = DeviceStepper(g, ctx, blocks[rank])
+    try:
+        tid_d = torch.as_tensor(np.asarray(ids, np.uint64).astype(np.int64), device=st.dev)
+        return reverse_pagerank_partitioned(st, g.num_nodes(), cfg.iterations, cfg.damp, tid_d,
+                                            len(ids), group, blocks)
+    finally:
+        st.close()
 
 
-def weighted_reverse_pagerank_peers(g, cfg, tid, ctxs, timeout_check=True):
+def _push_blocks(LIB, tg, ctx_h, src_base: int, dst_bases, rb: int, re: int):
+    """This rank's rows [rb, re) of a vector to every peer's copy of it: one
+    contiguous copy per peer (copy engine over NVLink/NVSwitch)."""
+    if re <= rb:
+        return
+    for d in dst_bases:
+        tg._check(LIB.tg_memcpy_async(ctx_h, d + 8 * rb, src_base + 8 * rb, 8 * (re - rb)))
+
+
+def weighted_reverse_pagerank_peers(g, cfg, tid, ctxs, timeout_check=True, exchange="copy"):
     """Partitioned PageRank with the FUSED exchange, one process driving
     several ranks (one context each; ranks may share a GPU): every step writes
     its rows straight into all ranks' `norm` vectors (P2P stores over NVLink
     between GPUs) and a device-side barrier replaces the all-gather
     (tg_pagerank_step_peers_async / tg_peer_barrier_async). Returns the full
     score vector of every rank (all identical, bit-exact to one GPU).
-    `tid=None` runs the unweighted recurrence."""
+    `tid=None` runs the unweighted recurrence.
+
+    exchange="copy" (default): the step writes its rows locally and the block
+    is pushed to every peer as one contiguous copy before the barrier;
+    "stores": the step's epilogue stores each row into every peer's vector
+    (one 8 B remote store per row per peer)."""
     import ctypes as C
     import torch
     from . import tiergraph as tg
@@ -154,7 +245,7 @@ def weighted_reverse_pagerank_peers(g, cfg, tid, ctxs, timeout_check=True):
         for b in range(G):
             if ctxs[a].device != ctxs[b].device:
                 tg._check(LIB.tg_enable_peer_access(ctxs[a].device, ctxs[b].device))
-    chunk, blocks = row_blocks(n, G)
+    blocks = edge_blocks(g.offsets, G)
     gh = [g.device(c) for c in ctxs]
     deg = [torch.empty(max(n, 1), dtype=torch.int32, device=d) for d in devs]
     bufs = [[torch.empty(max(n, 1), dtype=torch.float64, device=d) for _ in range(3)] for d in devs]
@@ -173,13 +264,21 @@ def weighted_reverse_pagerank_peers(g, cfg, tid, ctxs, timeout_check=True):
         nxt = 1 - cur
         for r, c in enumerate(ctxs):
             peers = [q for q in range(G) if q != r]
-            pn = (C.c_void_p * 16)(*[bufs[q][nxt].data_ptr() for q in peers])
-            ps = (C.c_void_p * 16)(*[bufs[q][2].data_ptr() for q in peers])
+            k = 2 if last else nxt
             rb, re = blocks[r]
-            tg._check(LIB.tg_pagerank_step_peers_async(
-                c.h, gh[r], deg[r].data_ptr(), float(cfg.damp), bufs[r][cur].data_ptr(),
-                bufs[r][nxt].data_ptr(), bufs[r][2].data_ptr(), rb, re, last, pn, ps,
-                len(peers)))
+            if exchange == "stores":
+                pn = (C.c_void_p * 16)(*[bufs[q][nxt].data_ptr() for q in peers])
+                ps = (C.c_void_p * 16)(*[bufs[q][2].data_ptr() for q in peers])
+                tg._check(LIB.tg_pagerank_step_peers_async(
+                    c.h, gh[r], deg[r].data_ptr(), float(cfg.damp), bufs[r][cur].data_ptr(),
+                    bufs[r][nxt].data_ptr(), bufs[r][2].data_ptr(), rb, re, last, pn, ps,
+                    len(peers)))
+            else:
+                tg._check(LIB.tg_pagerank_step_async(
+                    c.h, gh[r], deg[r].data_ptr(), float(cfg.damp), bufs[r][cur].data_ptr(),
+                    bufs[r][nxt].data_ptr(), bufs[r][2].data_ptr(), rb, re, last))
+                _push_blocks(LIB, tg, c.h, bufs[r][k].data_ptr(),
+                             [bufs[q][k].data_ptr() for q in peers], rb, re)
         for r, c in enumerate(ctxs):
             pf = (C.c_void_p * 16)(*[flags[q].data_ptr() for q in range(G) if q != r])
             tg._check(LIB.tg_peer_barrier_async(c.h, flags[r].data_ptr(), pf, G - 1,
@@ -224,7 +323,7 @@ class PeerExchangePagerank:
     before arriving there.
     """
 
-    def __init__(self, g, ctx, group=None):
+    def __init__(self, g, ctx, group=None, exchange="copy"):
         import ctypes as C
         import torch
         import torch.distributed as dist
@@ -238,8 +337,8 @@ class PeerExchangePagerank:
         self.rank = dist.get_rank(group) if dist.is_initialized() else 0
         if self.world >= TG_MAX_PEERS + 1:
             raise tg.DomainError(f"at most {TG_MAX_PEERS} peers")
-        _, blocks = row_blocks(n, self.world)
-        self.rb, self.re = blocks[self.rank]
+        self.exchange = exchange
+        self.rb, self.re = edge_blocks(g.offsets, self.world)[self.rank]
         self.vec = ((max(n, 1) * 8 + 255) // 256) * 256
         nbytes = 3 * self.vec + 256
         base = C.c_void_p()
@@ -296,12 +395,21 @@ class PeerExchangePagerank:
         for it in range(iterations):
             last = int(it + 1 == iterations)
             nxt = 1 - cur
-            pn = (C.c_void_p * 16)(*[self._vec(self.bases[q], nxt) for q in self.peers])
-            ps = (C.c_void_p * 16)(*[self._vec(self.bases[q], 2) for q in self.peers])
-            tg._check(LIB.tg_pagerank_step_peers_async(
-                self.ctx.h, self.gh, self.deg.data_ptr(), float(damp), self._vec(self.base, cur),
-                self._vec(self.base, nxt), self._vec(self.base, 2), self.rb, self.re, last,
-                pn, ps, len(self.peers)))
+            if self.exchange == "stores":
+                pn = (C.c_void_p * 16)(*[self._vec(self.bases[q], nxt) for q in self.peers])
+                ps = (C.c_void_p * 16)(*[self._vec(self.bases[q], 2) for q in self.peers])
+                tg._check(LIB.tg_pagerank_step_peers_async(
+                    self.ctx.h, self.gh, self.deg.data_ptr(), float(damp),
+                    self._vec(self.base, cur), self._vec(self.base, nxt),
+                    self._vec(self.base, 2), self.rb, self.re, last, pn, ps, len(self.peers)))
+            else:
+                tg._check(LIB.tg_pagerank_step_async(
+                    self.ctx.h, self.gh, self.deg.data_ptr(), float(damp),
+                    self._vec(self.base, cur), self._vec(self.base, nxt),
+                    self._vec(self.base, 2), self.rb, self.re, last))
+                k = 2 if last else nxt
+                _push_blocks(LIB, tg, self.ctx.h, self._vec(self.base, k),
+                             [self._vec(self.bases[q], k) for q in self.peers], self.rb, self.re)
             if G > 1:
                 self.arrivals += G - 1
                 tg._check(LIB.tg_peer_barrier_async(

@@ -486,6 +486,71 @@ def weighted_reverse_pagerank(g: CsrGraph, cfg: PagerankConfig = PagerankConfig(
     return o
 
 
+def row_blocks(offsets, parts: int) -> np.ndarray:
+    """Edge-balanced contiguous row blocks (tg_row_blocks): parts+1 bounds."""
+    off = _u64(offsets)
+    b = np.zeros(parts + 1, np.uint64)
+    _check(LIB.tg_row_blocks(_ptr(off), max(_len(off) - 1, 0), parts, b.ctypes.data))
+    return b
+
+
+class MultiDeviceGraph:
+    """A CsrGraph partitioned over several devices of this process
+    (tg_mgraph): one edge-balanced row block per context, K1
+    sharded and summed once, K3 steps exchanging the blocks by contiguous peer
+    copies. PageRank is bit-identical to one device for any device count --
+    what the C++ drop-in runs when TIERGRAPH_DEVICES lists several devices."""
+
+    def __init__(self, g: CsrGraph, ctxs):
+        self.ctxs = list(ctxs)
+        self.n, self.e = g.num_nodes(), g.num_edges()
+        arr = (C.c_void_p * len(self.ctxs))(*[c.h.value for c in self.ctxs])
+        h = C.c_void_p()
+        if _len(g.offsets) == 0:
+            raise FormatError("csr: offsets array is empty")
+        _check(LIB.tg_mgraph_create(arr, len(self.ctxs), _ptr(g.offsets),
+                                    _nonempty(g.targets, np.uint64), self.n, self.e, C.byref(h)))
+        self.h = h
+
+    def info(self):
+        G = len(self.ctxs)
+        b = np.zeros(G + 1, np.uint64)
+        e = np.zeros(G, np.uint64)
+        ms = C.c_double()
+        _check(LIB.tg_mgraph_info(self.h, b.ctypes.data, e.ctypes.data, C.byref(ms)))
+        return {"bounds": b, "edges": e, "indeg_ms": ms.value}
+
+    def in_degrees(self):
+        o = np.empty(self.n, np.uint64)
+        if self.n:
+            _check(LIB.tg_mgraph_in_degrees(self.h, o.ctypes.data))
+        return o
+
+    def weighted_reverse_pagerank(self, cfg: PagerankConfig = PagerankConfig(),
+                                  tid: TrainIdSet = None, out=None):
+        ids = _ids(tid if tid is not None else np.zeros(0, np.uint64))
+        o = _out(out, self.n, np.float64, "float64")
+        _check(LIB.tg_mgraph_pagerank(self.h, cfg.iterations, cfg.damp,
+                                      _nonempty(ids, np.uint64), _len(ids), 1, _ptr(o)))
+        return o
+
+    def reverse_pagerank(self, cfg: PagerankConfig = PagerankConfig(), out=None):
+        o = _out(out, self.n, np.float64, "float64")
+        _check(LIB.tg_mgraph_pagerank(self.h, cfg.iterations, cfg.damp, None, 0, 0, _ptr(o)))
+        return o
+
+    def close(self):
+        if getattr(self, "h", None):
+            LIB.tg_mgraph_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
 def score_ordering(scores, *, ctx: Context = None, out=None):
     """scoring.hpp:49 (scoring.cpp:104-115)"""
     c = _ctx(ctx)

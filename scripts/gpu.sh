@@ -8,6 +8,8 @@
 #   bench:<cfg>[:<steps>]   python bench.py --config <cfg> (ours)  -> bench_<cfg>.json
 #   ref:<cfg>[:<steps>]     python bench.py --impl reference       -> ref_<cfg>.json
 #   probe[:<gb>]   scripts/micro/cold_probe (cold-tier translation / CE probe)
+#   hpprobe[:<gb>] scripts/micro/host_pages_probe (cold tier on 4 KB / THP / 2 MB / 1 GB host pages)
+#   testk:<expr>   pytest -m gpu -k <expr>
 #   launches:<cfg> ncu launch list (gpu__time_duration) of a short bench run
 #   ncu_k8:<cfg>   ncu (application replay) of K8 on the cached C3/C4 inputs
 #   ncu_k3:<cfg>   ncu --set full of K3 (pr_step) at <cfg>
@@ -35,6 +37,10 @@ for st in "$@"; do
     probe)
       nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o /tmp/cold_probe scripts/micro/cold_probe.cu &&
       timeout 900 /tmp/cold_probe ${a:-45} 3400 > $O/cold_probe.log 2>&1; echo "rc=$?" >> $O/cold_probe.log ;;
+    hpprobe)
+      nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o /tmp/host_pages_probe scripts/micro/host_pages_probe.cu &&
+      timeout 900 /tmp/host_pages_probe ${a:-45} > $O/host_pages_probe.log 2>&1; echo "rc=$?" >> $O/host_pages_probe.log ;;
+    testk) timeout 2400 python -m pytest tests -x -q -m gpu -k "$a" > $O/pytest_k.log 2>&1; echo "rc=$?" >> $O/pytest_k.log ;;
     launches) timeout 1800 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
         --log-file $O/launches_$a.csv python bench.py --config $a --steps 10 --warmup 3 --no-cpu-baseline \
         > $O/launches_$a.log 2>&1 ;;

@@ -23,17 +23,24 @@ from paper_2111_05894_b200 import distributed as D
 
 
 class CpuStepper:
-    def __init__(self, off, tgt):
+    """One rank's shard: rows [rb, re) only (like tg_graph_create_rows)."""
+
+    def __init__(self, off, tgt, block):
         self.off = off.astype(np.int64)
         self.tgt = tgt.astype(np.int64)
         self.n = len(off) - 1
-        self.deg = np.bincount(self.tgt, minlength=self.n).astype(np.int64)
+        self.rb, self.re = block
 
     def alloc(self, count):
         return torch.zeros(count, dtype=torch.float64)
 
-    def prepare(self, tid, ntid, norm0):
+    def partial_indeg(self):
+        e0, e1 = self.off[self.rb], self.off[self.re]
+        return torch.as_tensor(np.bincount(self.tgt[e0:e1], minlength=self.n).astype(np.int32))
+
+    def init(self, tid, ntid, indeg, norm0):
         n = self.n
+        self.deg = indeg.numpy().astype(np.int64)
         s = [1.0 / n] * n  # scoring.cpp:96
         if tid is not None:
             w = n / ntid  # scoring.cpp:94-95
@@ -43,6 +50,7 @@ class CpuStepper:
             norm0[j] = s[j] / max(int(self.deg[j]), 1)  # :59-61
 
     def step(self, damp, nin, nout, sout, rb, re, last):
+        assert self.rb <= rb and re <= self.re
         base = (1.0 - damp) / self.n  # :53
         x = nin.tolist()
         for r in range(rb, re):
@@ -72,10 +80,11 @@ def _worker(rank, world, port, off, tgt, tid, iters, q):
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
-        st = CpuStepper(off, tgt)
+        blocks = D.edge_blocks(off, world)
+        st = CpuStepper(off, tgt, blocks[rank])
         t = None if tid is None else torch.as_tensor(tid.astype(np.int64))
         out = D.reverse_pagerank_partitioned(st, len(off) - 1, iters, 0.85, t,
-                                             0 if tid is None else len(tid))
+                                             0 if tid is None else len(tid), blocks=blocks)
         q.put((rank, out.numpy().tobytes()))
     finally:
         dist.destroy_process_group()
@@ -103,6 +112,32 @@ def test_row_blocks_cover_and_pad():
             assert chunk * world >= n and (n == 0 or chunk * world - n < world)
             rows = [r for b in blocks for r in range(*b)]
             assert rows == list(range(n))
+
+
+def test_edge_blocks_cover_balance_and_match_the_library():
+    """Edge-balanced blocks cover every row once, keep every block within one
+    row's length of E/world, and equal the C-ABI's tg_row_blocks."""
+    from paper_2111_05894_b200 import synth, tiergraph as tg
+    port = oracle.port()
+    cases = [port.from_edge_list(n, *(np.random.default_rng(n).integers(0, max(n, 1), (2, 6 * n))
+                                      .astype(np.uint64))) for n in (1, 7, 100, 1001)]
+    cases.append((np.zeros(6, np.uint64), np.zeros(0, np.uint64)))
+    cases.append(synth.rmat_graph(200_000, 3_000_000, seed=2, device="cpu"))
+    for off, tgt in cases:
+        n, e = len(off) - 1, len(tgt)
+        rowlen = np.diff(off.astype(np.int64))
+        for world in (1, 2, 3, 8):
+            blocks = D.edge_blocks(off, world)
+            assert [r for b in blocks for r in range(*b)] == list(range(n))
+            b = np.array([x[0] for x in blocks] + [n])
+            assert np.array_equal(b.astype(np.uint64), tg.row_blocks(off, world))
+            per = np.diff(off[b].astype(np.int64))
+            if e:
+                assert per.max() <= e / world + (rowlen.max() if n else 0) + 1
+        if n > 100_000:  # R-MAT: near-equal edges per block
+            for world in (2, 4, 8):
+                b = tg.row_blocks(off, world).astype(np.int64)
+                assert np.diff(off[b].astype(np.int64)).max() <= 1.1 * e / world
 
 
 @pytest.mark.parametrize("world", [2, 3])

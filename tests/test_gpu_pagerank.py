@@ -250,3 +250,46 @@ def test_in_degrees_large_graphs(tg, ctx, n, draws):
     g2 = tg.CsrGraph(off2, tgt2)
     want2 = np.bincount(tgt2.astype(np.int64), minlength=n).astype(np.uint64)
     assert np.array_equal(tg.in_degrees(g2, ctx=ctx), want2)
+
+
+@pytest.mark.parametrize("mode", ["1", "0"])
+def test_relabelled_twin_bit_exact(tg, ctx, monkeypatch, mode):
+    """K3 on the twin renumbered by in-degree (TIERGRAPH_PR_RELABEL=1, the
+    default at C3/C4 sizes) and without it (=0): raw-byte equal to the
+    reference on random, hub-row, tie-prone and R-MAT graphs, weighted and
+    plain, and the timed entry point returns the same bytes."""
+    import ctypes as C
+    from paper_2111_05894_b200._lib import LIB
+    from paper_2111_05894_b200 import synth
+    monkeypatch.setenv("TIERGRAPH_PR_RELABEL", mode)
+    chk, port = checker(), oracle.port()
+    cases = [random_graph(port, 300 + 97 * i, 1.5 + i, 40 + i) for i in range(4)]
+    cases.append(_hub_graph(60000, [(0, 40000), (31, 2049), (1000, 20000), (59999, 3000)], 3))
+    n = 3 * 2 ** 15
+    src = [np.zeros(60000, np.uint64), np.ones(n - 60001, np.uint64)]
+    dst = [np.arange(1, 60001, dtype=np.uint64), np.arange(60001, n, dtype=np.uint64)]
+    cases.append(port.from_edge_list(n, np.concatenate(src), np.concatenate(dst)))
+    cases.append(synth.rmat_graph(300_000, 4_000_000, seed=5))
+    for off, tgt in cases:
+        nn = len(off) - 1
+        g = G(tg, off, tgt)
+        info = C.c_int()
+        assert LIB.tg_pagerank_relabel_info(ctx.h, g.device(ctx), C.byref(info), None) == 0
+        assert info.value == int(mode)
+        tid = port.draw_random_train_ids(nn, max(1, nn // 10), 9)
+        for it in (1, 5):
+            a = tg.weighted_reverse_pagerank(g, tg.PagerankConfig(it, 0.85), tg.TrainIdSet(tid))
+            assert a.tobytes() == chk.weighted_reverse_pagerank(off, tgt, tid, it, 0.85).tobytes()
+        b = tg.reverse_pagerank(g, tg.PagerankConfig(3, 0.85))
+        assert b.tobytes() == chk.reverse_pagerank(off, tgt, 3, 0.85).tobytes()
+        out = np.empty(nn, np.float64)
+        ph = (C.c_double * 6)()
+        t = np.ascontiguousarray(tid, np.uint64)
+        assert LIB.tg_weighted_reverse_pagerank_timed(ctx.h, g.device(ctx), 5, 0.85, t.ctypes.data,
+                                                      len(t), out.ctypes.data, ph) == 0
+        assert out.tobytes() == chk.weighted_reverse_pagerank(off, tgt, tid, 5, 0.85).tobytes()
+        assert all(x > 0 for x in ph)
+    # out-of-range train ids are still a DomainError on the twin
+    g = G(tg, *cases[0])
+    with pytest.raises(tg.DomainError, match="out of range"):
+        tg.weighted_reverse_pagerank(g, tg.PagerankConfig(), tg.TrainIdSet(np.array([0, 10 ** 6], np.uint64)))
