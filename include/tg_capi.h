@@ -97,6 +97,10 @@ int tg_ctx_device(tg_ctx* ctx);
 int tg_default_device(void);
 /* Number of devices listed in TIERGRAPH_DEVICES (>=1), or the visible count. */
 int tg_device_count(void);
+/* The devices TIERGRAPH_DEVICES lists ("0,1,2"; entries may repeat: virtual
+ * devices on one GPU), else {0}. Writes min(count, cap) ids; returns count.
+ * The C++ drop-in partitions PageRank over them when there are several. */
+int tg_device_list(int* out, int cap);
 /* Launches of this library's kernels since process start (all contexts). */
 uint64_t tg_kernel_launches(void);
 

@@ -65,6 +65,7 @@ SIGNATURES = {
     "tg_ctx_device": (I32, [vp]),
     "tg_default_device": (I32, []),
     "tg_device_count": (I32, []),
+    "tg_device_list": (I32, [C.POINTER(I32), I32]),
     "tg_kernel_launches": (U64, []),
     "tg_graph_create": (I32, [vp, vp, vp, U64, U64, C.POINTER(vp)]),
     "tg_graph_destroy": (I32, [vp]),

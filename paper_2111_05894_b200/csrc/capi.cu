@@ -147,6 +147,24 @@ int tg_default_device(void) {
   return 0;
 }
 
+int tg_device_list(int* out, int cap) {
+  std::vector<int> v;
+  if (const char* s = std::getenv("TIERGRAPH_DEVICES")) {
+    const char* p = s;
+    while (*p) {
+      char* end = nullptr;
+      const long d = std::strtol(p, &end, 10);
+      if (end == p) break;
+      if (d >= 0) v.push_back(static_cast<int>(d));
+      p = end;
+      while (*p == ',' || *p == ' ') ++p;
+    }
+  }
+  if (v.empty()) v.push_back(0);
+  for (int i = 0; i < cap && i < static_cast<int>(v.size()); ++i) out[i] = v[i];
+  return static_cast<int>(v.size());
+}
+
 int tg_device_count(void) {
   if (const char* s = std::getenv("TIERGRAPH_DEVICES")) {
     int n = 1;

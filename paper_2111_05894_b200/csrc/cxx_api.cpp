@@ -32,7 +32,6 @@ namespace tiergraph {
 
 using b200::check;
 using b200::Ctx;
-using b200::DevGraph;
 using b200::nonnull;
 
 namespace {
@@ -106,30 +105,48 @@ TrainIdSet draw_random_train_ids(NodeId num_nodes, NodeId count, std::uint64_t s
 ScoreVector degree_score(const CsrGraph& g) {
   ScoreVector out(g.num_nodes());
   if (out.empty()) return out;
-  Ctx ctx;
-  DevGraph dg(ctx, g);
-  check(tg_degree_score(ctx, dg.get(), out.data()));
+  b200::GraphLease dg(g);
+  check(tg_degree_score(dg.ctx(), dg.graph(), out.data()));
   return out;
 }
 
-// scoring.cpp:78-84 (K1 in-degrees, K2 init, K3 SpMV x iterations)
-ScoreVector reverse_pagerank(const CsrGraph& g, const PagerankConfig& cfg) {
-  Ctx ctx;
+// scoring.cpp:78-102 on the device copy cached for g (K1 in-degrees with the
+// upload, K2 init, K3 SpMV x iterations). With several TIERGRAPH_DEVICES the
+// rows are partitioned over them (tg_mgraph), bit-identical to one device.
+static ScoreVector run_pagerank(const CsrGraph& g, const PagerankConfig& cfg,
+                                const TrainIdSet* tid) {
   ScoreVector out(g.num_nodes());
-  DevGraph dg(ctx, g);
-  check(tg_reverse_pagerank(ctx, dg.get(), cfg.iterations, cfg.damp, out.data()));
+  if (out.empty() || (tid && tid->ids.empty())) {
+    // the argument checks of scoring.cpp:42-47 / :89-91 (the library runs
+    // them before touching a context or graph), then {} for an empty graph
+    check(tid ? tg_weighted_reverse_pagerank(nullptr, nullptr, cfg.iterations, cfg.damp,
+                                             nonnull(tid->ids), tid->ids.size(), nullptr)
+              : tg_reverse_pagerank(nullptr, nullptr, cfg.iterations, cfg.damp, nullptr));
+    return out;
+  }
+  b200::GraphLease dg(g);
+  if (dg.devices() > 1) {
+    check(tg_mgraph_pagerank(dg.partitioned(), cfg.iterations, cfg.damp,
+                             tid ? nonnull(tid->ids) : nullptr, tid ? tid->ids.size() : 0,
+                             tid ? 1 : 0, out.data()));
+  } else if (tid) {
+    check(tg_weighted_reverse_pagerank(dg.ctx(), dg.graph(), cfg.iterations, cfg.damp,
+                                       nonnull(tid->ids), tid->ids.size(), out.data()));
+  } else {
+    check(tg_reverse_pagerank(dg.ctx(), dg.graph(), cfg.iterations, cfg.damp, out.data()));
+  }
   return out;
+}
+
+// scoring.cpp:78-84
+ScoreVector reverse_pagerank(const CsrGraph& g, const PagerankConfig& cfg) {
+  return run_pagerank(g, cfg, nullptr);
 }
 
 // scoring.cpp:86-102
 ScoreVector weighted_reverse_pagerank(const CsrGraph& g, const PagerankConfig& cfg,
                                       const TrainIdSet& tid) {
-  Ctx ctx;
-  ScoreVector out(g.num_nodes());
-  DevGraph dg(ctx, g);
-  check(tg_weighted_reverse_pagerank(ctx, dg.get(), cfg.iterations, cfg.damp, nonnull(tid.ids),
-                                     tid.ids.size(), out.data()));
-  return out;
+  return run_pagerank(g, cfg, &tid);
 }
 
 // scoring.cpp:104-115 (K4 key transform + K5 radix sort)

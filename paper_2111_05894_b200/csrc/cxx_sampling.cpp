@@ -23,22 +23,9 @@ namespace {
 
 constexpr std::uint64_t kSampleTag = 0x534Dull;  // sampling.cpp:15 (stream domain)
 
-// The GPU sampler over a graph's device copy, for the duration of one call.
-class DevSampler {
- public:
-  DevSampler(tg_ctx* ctx, const CsrGraph& gt) : g_(ctx, gt) {
-    if (gt.num_nodes() == 0) throw DomainError("build_minibatch: graph has no nodes");
-    b200::check(tg_sampler_create(ctx, g_.get(), &s_));
-  }
-  ~DevSampler() { tg_sampler_destroy(s_); }
-  DevSampler(const DevSampler&) = delete;
-  DevSampler& operator=(const DevSampler&) = delete;
-  tg_sampler* get() const { return s_; }
-
- private:
-  b200::DevGraph g_;
-  tg_sampler* s_ = nullptr;
-};
+// The GPU sampler state lives in the device-graph cache (cxx_common.hpp
+// GraphLease): consecutive build_minibatch calls on the same graph reuse the
+// upload, the stamps and the member bitmap.
 
 }  // namespace
 
@@ -87,25 +74,32 @@ std::vector<NodeId> build_minibatch(const CsrGraph& gt, std::span<const NodeId> 
   if (seeds.empty()) throw DomainError("build_minibatch: seeds must be non-empty");
   for (const NodeId s : seeds)
     if (s >= gt.num_nodes()) throw DomainError("seed " + std::to_string(s) + " out of range");
-  b200::Ctx ctx;
-  DevSampler smp(ctx, gt);
+  b200::GraphLease dg(gt);
+  tg_sampler* smp = dg.sampler();
   const uint64_t n = gt.num_nodes();
-  std::vector<NodeId> members(n);
-  uint64_t count = 0;
   const auto& f = fanouts.fanouts;
+  // layered bounds: frontier_{l+1} <= min(n, frontier_l * k_l); members <=
+  // min(n, sum of frontiers); raw draws <= |seeds| + sum frontier_l * k_l
+  uint64_t fr = std::min<uint64_t>(seeds.size(), n), mem = fr, raw_cap = seeds.size();
+  for (const std::uint32_t k : f) {
+    raw_cap += fr * k;
+    fr = std::min<uint64_t>(n, fr * k);
+    mem += fr;
+  }
+  mem = std::min<uint64_t>(mem, n);
+  std::vector<NodeId> members(mem);
+  uint64_t count = 0;
   if (!raw_draws) {
-    b200::check(tg_sample_minibatch(smp.get(), seeds.data(), seeds.size(), f.data(),
+    b200::check(tg_sample_minibatch(smp, seeds.data(), seeds.size(), f.data(),
                                     static_cast<uint32_t>(f.size()), rng.rng_seed, rng.epoch,
-                                    rng.batch_index, members.data(), n, &count));
+                                    rng.batch_index, members.data(), mem, &count));
   } else {
-    // every draw: seeds plus at most fanout draws per frontier node per layer
-    uint64_t cap = seeds.size();
-    for (const std::uint32_t k : f) cap += static_cast<uint64_t>(k) * n;
+    const uint64_t cap = raw_cap;
     std::vector<NodeId> raw(cap);
     uint64_t raw_n = 0;
-    b200::check(tg_sample_minibatch_raw(smp.get(), seeds.data(), seeds.size(), f.data(),
+    b200::check(tg_sample_minibatch_raw(smp, seeds.data(), seeds.size(), f.data(),
                                         static_cast<uint32_t>(f.size()), rng.rng_seed, rng.epoch,
-                                        rng.batch_index, members.data(), n, &count, raw.data(),
+                                        rng.batch_index, members.data(), mem, &count, raw.data(),
                                         cap, &raw_n));
     raw_draws->insert(raw_draws->end(), raw.begin(), raw.begin() + static_cast<long>(raw_n));
   }
@@ -123,12 +117,33 @@ AccessCounter run_training_trace(const CsrGraph& g, const TrainIdSet& tid,
   const NodeId n = g.num_nodes();
   for (const NodeId id : tid.ids)
     if (id >= n) throw DomainError("train id " + std::to_string(id) + " out of range");
-  const CsrGraph gt = transpose(g);
-  b200::Ctx ctx;
-  DevSampler smp(ctx, gt);
+  // the sampler runs on transpose(g), built on the device (tg_transpose)
+  // and cached with g's entry
+  b200::GraphLease dg(g);
+  b200::CachedGraph* e = dg.entry();
+  if (!e->sampler_t) {
+    tg_ctx* ctx = dg.ctx();
+    const uint64_t m = g.targets.size();
+    void *toff = nullptr, *ttgt = nullptr;
+    b200::check(tg_device_alloc(ctx, 8 * (n + 1), &toff));
+    const int rc0 = tg_device_alloc(ctx, 8 * std::max<uint64_t>(m, 1), &ttgt);
+    int rc = rc0;
+    static const uint64_t kNone = 0;
+    if (rc == TG_OK)
+      rc = tg_transpose(ctx, g.offsets.data(), m ? g.targets.data() : &kNone, n, m,
+                        static_cast<uint64_t*>(toff), static_cast<uint64_t*>(ttgt));
+    if (rc == TG_OK)
+      rc = tg_graph_create(ctx, static_cast<uint64_t*>(toff), static_cast<uint64_t*>(ttgt), n, m,
+                           &e->gt);
+    if (rc == TG_OK) rc = tg_sampler_create(ctx, e->gt, &e->sampler_t);
+    tg_ctx_sync(ctx);
+    tg_device_free(ctx, toff);
+    if (ttgt) tg_device_free(ctx, ttgt);
+    b200::check(rc);
+  }
   std::vector<std::uint64_t> counts(n);
   const auto& f = fanouts.fanouts;
-  b200::check(tg_sampler_trace(smp.get(), tid.ids.data(), tid.ids.size(), f.data(),
+  b200::check(tg_sampler_trace(e->sampler_t, tid.ids.data(), tid.ids.size(), f.data(),
                                static_cast<uint32_t>(f.size()), cfg.batch_size, cfg.epochs,
                                cfg.rng_seed, cfg.dedup_per_batch ? 1 : 0, counts.data()));
   return make_access_counter(std::move(counts));

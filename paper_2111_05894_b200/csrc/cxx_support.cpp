@@ -16,9 +16,8 @@ namespace tiergraph {
 std::vector<EdgeIdx> in_degrees(const CsrGraph& g) {
   std::vector<EdgeIdx> out(g.num_nodes());
   if (out.empty()) return out;
-  b200::Ctx ctx;
-  b200::DevGraph dg(ctx, g);
-  b200::check(tg_in_degrees(ctx, dg.get(), out.data()));
+  b200::GraphLease dg(g);
+  b200::check(tg_in_degrees(dg.ctx(), dg.graph(), out.data()));
   return out;
 }
 
@@ -30,8 +29,9 @@ void validate_features(const FeatureMatrix& f) {
                       " bytes, expected " + std::to_string(want));
 }
 
-// csr_graph.cpp:67-80 — canonical transpose, host (the restatement in
-// csrc/host_producers.cpp: rows in ascending source order).
+// csr_graph.cpp:67-80 — canonical transpose on the device (tg_transpose: a
+// stable radix sort of the edges by target in CSR order, so every transposed
+// row lists its sources ascending, bit-identical to the reference).
 CsrGraph transpose(const CsrGraph& g) {
   const uint64_t n = g.num_nodes();
   CsrGraph t;
@@ -40,8 +40,10 @@ CsrGraph transpose(const CsrGraph& g) {
   if (n == 0) return t;
   static const uint64_t kNone = 0;
   uint64_t scratch = 0;
-  b200::check(tg_transpose_host(g.offsets.data(), g.targets.empty() ? &kNone : g.targets.data(),
-                                n, t.offsets.data(), t.targets.empty() ? &scratch : t.targets.data()));
+  b200::Ctx ctx;
+  b200::check(tg_transpose(ctx, g.offsets.data(), g.targets.empty() ? &kNone : g.targets.data(), n,
+                           g.num_edges(), t.offsets.data(),
+                           t.targets.empty() ? &scratch : t.targets.data()));
   return t;
 }
 

@@ -925,6 +925,8 @@ const tg_graph* relabel_twin(tg_ctx* ctx, const tg_graph* gc) {
   t->ctx = ctx;
   t->n = n;
   t->e = e;
+  t->rb = 0;
+  t->re = n;
   uint64_t* lens = nullptr;
   try {
     TGB_CUDA(cudaMalloc(&g->old_of, 4 * n));

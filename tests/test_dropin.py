@@ -126,3 +126,55 @@ def test_cxx_tiered_store_gather(tmp_path, devices):
     to gather(), for every requesting device of a D-device layout."""
     rc, out = _run([_build_store_check(tmp_path), str(devices)], 300)
     assert rc == 0 and "store_check ok" in out, out[-3000:]
+
+
+def _build_api_check(tmp_path):
+    pkg = os.path.join(ROOT, "paper_2111_05894_b200")
+    exe = tmp_path / "api_check"
+    subprocess.run(["g++", "-std=c++20", "-O1", f"-I{os.path.join(ROOT, 'include')}",
+                    os.path.join(ROOT, "tests", "dropin", "api_check.cpp"), "-o", str(exe),
+                    f"-L{pkg}", "-ltiergraph_b200_cxx", "-ltiergraph_b200", f"-Wl,-rpath,{pkg}"],
+                   check=True)
+    return str(exe)
+
+
+def test_api_check_compiles_against_dropin_headers(tmp_path):
+    _build_api_check(tmp_path)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("devices", ["0", "0,0", "0,0,0,0"])
+def test_cxx_api_cache_and_devices(tmp_path, devices):
+    """The C++ drop-in as a caller uses it: weighted_reverse_pagerank called
+    repeatedly on one CsrGraph (the device copy is cached after the first
+    call), with TIERGRAPH_DEVICES listing 1, 2 or 4 (virtual) devices (the
+    rows partitioned over them): scores raw-byte equal to the reference build,
+    repeated calls faster than the first, build_minibatch lists equal to the
+    reference's, a changed graph recomputed."""
+    import numpy as np
+    import oracle
+    from paper_2111_05894_b200 import synth
+    chk = oracle.ref() or oracle.port()
+    off, tgt = synth.rmat_graph(200_000, 3_000_000, seed=4)
+    n = len(off) - 1
+    tid = chk.draw_random_train_ids(n, n // 10, 3)
+    path = tmp_path / "g.bin"
+    with open(path, "wb") as f:
+        np.array([n, len(tgt)], np.uint64).tofile(f)
+        off.astype(np.uint64).tofile(f)
+        tgt.astype(np.uint64).tofile(f)
+        np.array([len(tid)], np.uint64).tofile(f)
+        tid.astype(np.uint64).tofile(f)
+    env = dict(os.environ, TIERGRAPH_DEVICES=devices)
+    r = subprocess.run([_build_api_check(tmp_path), str(path), str(tmp_path / "o"), "4"],
+                       capture_output=True, text=True, timeout=600, env=env)
+    assert r.returncode == 0 and "api_check ok" in r.stdout, r.stdout[-3000:] + r.stderr[-2000:]
+    got = np.fromfile(tmp_path / "o.scores", np.float64)
+    assert got.tobytes() == chk.weighted_reverse_pagerank(off, tgt, tid).tobytes()
+    plain = np.fromfile(tmp_path / "o.plain", np.float64)
+    assert plain.tobytes() == chk.reverse_pagerank(off, tgt, 3, 0.5).tobytes()
+    t_off, t_tgt = chk.transpose(off, tgt)
+    want_mb = chk.build_minibatch(t_off, t_tgt, tid[:64], [10, 5], 7, 0, 0)
+    assert np.array_equal(np.fromfile(tmp_path / "o.mb0", np.uint64), want_mb)
+    ms = [float(l.split()[2]) for l in r.stdout.splitlines() if l.startswith("call ")]
+    assert len(ms) == 4 and min(ms[1:]) < ms[0]  # cached device graph after the first call

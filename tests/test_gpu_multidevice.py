@@ -100,7 +100,7 @@ def test_row_block_graph_contract(tg, ctx):
     x = torch.zeros(n, dtype=torch.float64, device=dev)
     out = np.empty(n, np.float64)
     h = parts[1]
-    assert LIB.tg_weighted_reverse_pagerank(ctx.h, h, 5, 0.85, None, 0, out.ctypes.data) != 0
+    assert LIB.tg_reverse_pagerank(ctx.h, h, 5, 0.85, out.ctypes.data) == 2
     assert "rows" in LIB.tg_last_error().decode()
     assert LIB.tg_pagerank_step_async(ctx.h, h, tot.data_ptr(), 0.85, x.data_ptr(), x.data_ptr(),
                                       x.data_ptr(), 0, 100, 0) == 2  # rows outside the block
