@@ -204,21 +204,36 @@ def build_inputs(cfg, device, rank=0, world=1):
     return off, tgt, tid
 
 
-def pin_features(cfg, ctx=None):
+def pin_features(cfg, ctx=None, dist=None, rank=0, tag=""):
+    """The host feature fixture in pinned memory. Under torchrun (dist given)
+    ONE copy per node: rank 0 fills a POSIX shared segment that every rank
+    maps and registers, instead of one 57 GB copy per rank.
+    Returns (rows array, R, segment or None)."""
     from paper_2111_05894_b200 import synth, tiergraph as tg
     n, dim = cfg["nodes"], cfg["dim"]
     R = dim * cfg["elem"]
-    if cfg.get("row_cache_gb"):
-        P = cache_rows(cfg)
-        buf = tg.host_alloc(P * R)
-        synth.test_features_f16_gpu(P, dim, buf)
-        return buf.reshape(P, R), R
-    buf = tg.host_alloc(n * R)
-    if n * R > (8 << 30):
-        synth.test_features_pinned_gpu(n, dim, buf)
+    rows = cache_rows(cfg) if cfg.get("row_cache_gb") else n
+    seg = None
+    if dist is not None:
+        name = f"/tg_feat_{tag}"
+        if rank == 0:
+            seg = tg.SharedHostSegment(name, rows * R, create=True)
+        dist.barrier()
+        if rank != 0:
+            seg = tg.SharedHostSegment(name, rows * R, create=False)
+        buf = seg.array
     else:
-        synth.test_features(n, dim, out=buf)
-    return buf, R
+        buf = tg.host_alloc(rows * R)
+    if dist is None or rank == 0:
+        if cfg.get("row_cache_gb"):
+            synth.test_features_f16_gpu(rows, dim, buf)
+        elif n * R > (8 << 30):
+            synth.test_features_pinned_gpu(n, dim, buf)
+        else:
+            synth.test_features(n, dim, out=buf)
+    if dist is not None:
+        dist.barrier()  # filled
+    return buf.reshape(rows, R), R, seg
 
 
 def time_events(torch, fn, reps, warm=1):
@@ -433,7 +448,9 @@ def run_ours(args):
         f"(avg {np.mean([len(l) for l in lists]):.0f} ids) in {time.time()-t0:.1f}s")
 
     # ---- tiered store: hot rows in HBM (sharded across ranks), cold rows pinned
-    feat, R = pin_features(cfg, ctx)
+    cold_seg = None
+    tag = f"{os.environ.get('MASTER_PORT', '0')}_{os.getppid()}"
+    feat, R, feat_seg = pin_features(cfg, ctx, dist if world > 1 else None, rank, tag)
     hot = hot_fraction(cfg, world)
     budget = 0
     if "hot_per_gpu" in cfg:  # plan_layout's per-device HBM budget (tiering.cpp:87-96)
@@ -447,6 +464,24 @@ def run_ours(args):
                                       gather_mode=args.gather_mode)
         store.place_rows(feat, (np.arange(n, dtype=np.uint64) % np.uint64(len(feat)))
                          .astype(np.uint32))
+    elif world > 1:
+        # one cold tier per node: rank 0 writes it into a shared segment, the
+        # other ranks map the same memory
+        store = tg.TieredFeatureStore(None, perm, lay, rank, ctx=ctx,
+                                      cold_mode=cfg.get("cold_mode", "reordered"), place=False,
+                                      gather_mode=args.gather_mode)
+        cname = f"/tg_cold_{tag}"
+        if rank == 0:
+            cold_seg = tg.SharedHostSegment(cname, store.cold_tier_bytes, create=True)
+        dist.barrier()
+        if rank != 0:
+            cold_seg = tg.SharedHostSegment(cname, store.cold_tier_bytes, create=False)
+        store.attach_cold(cold_seg, fill=rank == 0)
+        if rank == 0:
+            store.place(feat, perm)
+        dist.barrier()
+        if rank != 0:
+            store.place(feat, perm)
     else:
         store = tg.TieredFeatureStore(feat, perm, lay, rank, ctx=ctx,
                                       cold_mode=cfg.get("cold_mode", "reordered"),
@@ -636,7 +671,9 @@ def run_ours(args):
                       "cold_mode": cfg.get("cold_mode", "reordered"),
                       "timing": "per-step CUDA events on the launching stream, L2 flushed "
                                 "(256 MB memset) before every step, max over ranks",
-                      "parallelism": f"{world} GPU(s), hot tier sharded, cold tier per rank"
+                      "parallelism": f"{world} GPU(s), hot tier sharded" + (
+                          ", features and cold tier: one POSIX shared segment per node, mapped "
+                          "by every rank" if world > 1 else "")
                                      + (" (TEST MODE: all ranks share cuda:0, gloo plumbing; "
                                         "not a scaling number)" if share else "")},
             "minibatches_per_s": round(mbps, 1),
@@ -742,6 +779,11 @@ def run_ours(args):
                 result["parity"]["transpose_identical"] = transpose_ok
     if dist:
         dist.barrier()
+        store.close()
+        dist.barrier()  # every rank is done with the shared segments
+        for seg in (cold_seg, feat_seg):
+            if seg is not None:
+                seg.close()
         dist.destroy_process_group()
     return result
 

@@ -323,6 +323,20 @@ int tg_store_set_peer(tg_store* s, uint32_t d, const void* peer_local_base);
 /* Share one cold tier between stores/processes: use `host` (mapped pinned or
  * registered memory holding the cold rows in the store's cold format). */
 int tg_store_share_cold(tg_store* s, const tg_store* owner);
+/* Host bytes of this store's cold tier in its cold format (stride, split). */
+uint64_t tg_store_cold_tier_bytes(const tg_store* s);
+/* Use caller memory (mapped: registered or a tg_host_shared_map segment) as
+ * the cold tier, before placement. fill != 0: this store's placement writes
+ * the cold rows there; fill == 0: another store (typically another process
+ * of the node) has written them and this one only reads. */
+int tg_store_attach_cold(tg_store* s, void* host, uint64_t bytes, int fill);
+/* One host segment per node shared by every process: POSIX shared memory
+ * `name` ("/tg_cold_<job>") of `bytes`, created (create != 0, fails if it
+ * exists) or opened, mapped and registered with the device (mapped |
+ * portable). Unmap in every process, unlink once. */
+int tg_host_shared_map(const char* name, uint64_t bytes, int create, void** out);
+int tg_host_shared_unmap(void* p, uint64_t bytes);
+int tg_host_shared_unlink(const char* name);
 
 /* K8: copy rows ids[0..n) (host|device) into dst (n x row_bytes, host|device)
  * and accumulate the reference accounting into report (host). Synchronous. */

@@ -105,6 +105,11 @@ SIGNATURES = {
     "tg_store_cold_host_bytes": (U64, [vp]),
     "tg_store_set_peer": (I32, [vp, U32, vp]),
     "tg_store_share_cold": (I32, [vp, vp]),
+    "tg_store_cold_tier_bytes": (U64, [vp]),
+    "tg_store_attach_cold": (I32, [vp, vp, U64, I32]),
+    "tg_host_shared_map": (I32, [C.c_char_p, U64, I32, C.POINTER(vp)]),
+    "tg_host_shared_unmap": (I32, [vp, U64]),
+    "tg_host_shared_unlink": (I32, [C.c_char_p]),
     "tg_gather_rows": (I32, [vp, vp, U64, vp, PR]),
     "tg_gather_rows_async": (I32, [vp, vp, U64, vp, vp, vp]),
     "tg_enable_peer_access": (I32, [I32, I32]),

@@ -155,16 +155,32 @@ __global__ void train_mult_kernel(const uint64_t* __restrict__ tid, uint64_t nti
 }
 
 // ------------------------------------------------------- K3 relabel twin
-__global__ void twin_lens_kernel(const uint32_t* __restrict__ off, const uint32_t* __restrict__ old_of,
-                                 const uint32_t* __restrict__ indeg, uint64_t n,
-                                 uint64_t* __restrict__ lens, uint32_t* __restrict__ new_of,
-                                 uint32_t* __restrict__ indeg_tw) {
+__global__ void twin_labels_kernel(const uint32_t* __restrict__ old_of,
+                                   const uint32_t* __restrict__ indeg, uint64_t n,
+                                   uint32_t* __restrict__ new_of, uint32_t* __restrict__ indeg_lab) {
   for (uint64_t v = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; v < n;
        v += (uint64_t)gridDim.x * blockDim.x) {
     const uint32_t u = old_of[v];
-    lens[v] = off[u + 1] - off[u];
     new_of[u] = static_cast<uint32_t>(v);
-    indeg_tw[v] = indeg[u];
+    indeg_lab[v] = indeg[u];
+  }
+}
+
+// storage row k of the twin = original row sigma[k] (K3's schedule order)
+__global__ void twin_rows_meta_kernel(const uint32_t* __restrict__ off,
+                                      const uint32_t* __restrict__ sigma,
+                                      const uint32_t* __restrict__ new_of,
+                                      const uint32_t* __restrict__ indeg, uint64_t n,
+                                      uint64_t* __restrict__ lens, uint32_t* __restrict__ row_label,
+                                      uint32_t* __restrict__ row_orig,
+                                      uint32_t* __restrict__ deg_rows) {
+  for (uint64_t k = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; k < n;
+       k += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t u = sigma[k];
+    lens[k] = off[u + 1] - off[u];
+    row_label[k] = new_of[u];
+    row_orig[k] = u;
+    deg_rows[k] = indeg[u];
   }
 }
 
@@ -175,19 +191,43 @@ __global__ void narrow_u64_kernel(const uint64_t* __restrict__ in, uint32_t* __r
     out[i] = static_cast<uint32_t>(in[i]);
 }
 
-// one warp per twin row: copy old row old_of[v] with targets renamed
+// Twin targets: storage row k = original row sigma[k], every target w
+// renamed new_of[w], same order. Rows of <= 8 edges (most of an R-MAT
+// graph) one per thread; longer rows one per warp.
 __global__ void twin_rows_kernel(const uint32_t* __restrict__ off, const uint32_t* __restrict__ tgt,
-                                 const uint32_t* __restrict__ old_of,
-                                 const uint32_t* __restrict__ new_of, uint64_t n,
+                                 const uint32_t* __restrict__ sigma,
+                                 const uint32_t* __restrict__ new_of, uint64_t k_short, uint64_t n,
                                  const uint32_t* __restrict__ off_tw, uint32_t* __restrict__ tgt_tw) {
+  const uint64_t tid = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+  const uint64_t nthreads = (uint64_t)gridDim.x * blockDim.x;
   const int lane = threadIdx.x & 31;
-  const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
-  for (uint64_t v = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5; v < n; v += nw) {
-    const uint32_t u = old_of[v];
+  // long rows [0, k_short): a warp each
+  for (uint64_t k = tid >> 5; k < k_short; k += nthreads >> 5) {
+    const uint32_t u = sigma[k];
     const uint32_t b = off[u], len = off[u + 1] - b;
-    uint32_t* dst = tgt_tw + off_tw[v];
+    uint32_t* dst = tgt_tw + off_tw[k];
     for (uint32_t i = lane; i < len; i += 32) dst[i] = new_of[__ldcs(tgt + b + i)];
   }
+  // short rows [k_short, n): a thread each
+  for (uint64_t k = k_short + tid; k < n; k += nthreads) {
+    const uint32_t u = sigma[k];
+    const uint32_t b = off[u], len = off[u + 1] - b;
+    uint32_t* dst = tgt_tw + off_tw[k];
+    for (uint32_t i = 0; i < len; ++i) dst[i] = new_of[__ldcs(tgt + b + i)];
+  }
+}
+
+// first storage row whose length is <= lim (rows sorted by length, descending)
+__global__ void first_short_kernel(const uint32_t* __restrict__ off_tw, uint64_t n, uint32_t lim,
+                                   uint64_t* out) {
+  if (threadIdx.x || blockIdx.x) return;
+  uint64_t lo = 0, hi = n;
+  while (lo < hi) {
+    const uint64_t mid = (lo + hi) / 2;
+    if (off_tw[mid + 1] - off_tw[mid] > lim) lo = mid + 1;
+    else hi = mid;
+  }
+  *out = lo;
 }
 
 // normalized0[j] = score0[j] / max(indeg[j],1), score0 = 1/N (* weight per
@@ -219,7 +259,11 @@ struct PrStepArgs {
   uint64_t row_begin, row_end;
   double base, damp;
   int last;
-  const uint32_t* score_index;  // last step: score of row r goes to score_out[score_index[r]]
+  // relabelled twin (see tg_graph): row r is stored at position r in length
+  // order; its vectors are indexed by label[r]; its score goes to
+  // score_out[score_index[r]] (the original id). Both null otherwise.
+  const uint32_t* label;
+  const uint32_t* score_index;
   // fused exchange: the same row also goes to every peer's norm / score
   // vector (NVLink P2P stores), replacing the all-gather of a partitioned run
   uint32_t n_peers;
@@ -253,10 +297,11 @@ __device__ __forceinline__ void finish_row(const PrStepArgs& a, uint64_t r, doub
     a.score_out[a.score_index ? a.score_index[r] : r] = nx;
     for (uint32_t p = 0; p < a.n_peers; ++p) a.peer_score[p][r] = nx;
   } else {
-    const uint32_t d = a.deg[r];
+    const uint32_t d = a.deg[r];  // in storage order
     const double v = __ddiv_rn(nx, static_cast<double>(d > 1u ? d : 1u));  // scoring.cpp:61
-    a.norm_out[r] = v;
-    for (uint32_t p = 0; p < a.n_peers; ++p) a.peer_norm[p][r] = v;
+    const uint64_t o = a.label ? a.label[r] : r;
+    a.norm_out[o] = v;
+    for (uint32_t p = 0; p < a.n_peers; ++p) a.peer_norm[p][o] = v;
   }
 }
 
@@ -402,7 +447,8 @@ __global__ void __maxnreg__(80) pr_hub_kernel(const PrStepArgs a, uint32_t row0)
   constexpr int kHubTile = kHubThreads * kHubT;
   extern __shared__ __align__(16) double xs[];  // [kHubTile]
   __shared__ HubShared<W> sh;
-  const uint32_t r = a.order[row0 + blockIdx.x];  // class A
+  const uint32_t r = a.order ? a.order[row0 + blockIdx.x]
+                             : static_cast<uint32_t>(a.row_begin + row0 + blockIdx.x);  // class A
   const uint32_t beg = a.off[r], len = a.off[r + 1] - beg;
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   double acc = 0.0;  // scoring.cpp:67 — identical in every thread
@@ -600,7 +646,7 @@ constexpr int kBStride = kBWin + 1;
 __device__ __forceinline__ void group_row(const PrStepArgs& a, int64_t i, double* buf) {
   const int lane = threadIdx.x & 31, sl = lane & (kBLanes - 1);
   const bool has = i < static_cast<int64_t>(a.nB);
-  const uint32_t r = has ? a.order[i] : 0u;
+  const uint32_t r = has ? (a.order ? a.order[i] : static_cast<uint32_t>(a.row_begin + i)) : 0u;
   const uint32_t beg = has ? a.off[r] : 0u;
   const uint32_t len = has ? a.off[r + 1] - beg : 0u;
   constexpr int K = kBWin / kBLanes;  // 8 per lane per window
@@ -697,12 +743,62 @@ __device__ __forceinline__ void thread_row(const PrStepArgs& a, uint32_t r) {
   finish_row(a, r, acc);
 }
 
+// Class C on the relabelled twin, whose rows are STORED in length order: a
+// warp's 32 rows are consecutive in storage, so their concatenated targets
+// are one contiguous range. The warp streams it in chunks of kCWin edges
+// (coalesced 4 B target loads, the next chunk's targets in flight), gathers
+// the normalized values into shared memory, and every lane then adds its own
+// row's part of the chunk in storage order (scoring.cpp:66-68) -- the same
+// left-to-right chain per row as thread_row, with coalesced target traffic.
+constexpr int kCWin = 256;  // edges per chunk (8 per lane)
+__device__ __forceinline__ void warp_rows_staged(const PrStepArgs& a, uint64_t k0, double* buf) {
+  const int lane = threadIdx.x & 31;
+  const uint64_t kend = min(k0 + 32, a.row_end);
+  const uint32_t nrows = static_cast<uint32_t>(kend > k0 ? kend - k0 : 0);
+  if (nrows == 0) return;
+  const uint32_t e0 = a.off[k0], e1 = a.off[k0 + nrows];
+  const bool has = static_cast<uint32_t>(lane) < nrows;
+  const uint32_t rb = has ? a.off[k0 + lane] - e0 : 0u, re = has ? a.off[k0 + lane + 1] - e0 : 0u;
+  const uint32_t total = e1 - e0;
+  const uint32_t* t = a.tgt + e0;
+  constexpr int K = kCWin / 32;
+  uint32_t tn[K];
+#pragma unroll
+  for (int q = 0; q < K; ++q) {
+    const uint32_t j = q * 32 + lane;
+    tn[q] = j < total ? __ldcs(t + j) : 0xffffffffu;
+  }
+  double acc = 0.0;  // scoring.cpp:67
+  for (uint32_t base = 0; base < total; base += kCWin) {
+    double v[K];
+#pragma unroll
+    for (int q = 0; q < K; ++q) v[q] = tn[q] != 0xffffffffu ? __ldg(a.norm_in + tn[q]) : 0.0;
+#pragma unroll
+    for (int q = 0; q < K; ++q) {  // next chunk's targets in flight
+      const uint32_t j = base + kCWin + q * 32 + lane;
+      tn[q] = j < total ? __ldcs(t + j) : 0xffffffffu;
+    }
+#pragma unroll
+    for (int q = 0; q < K; ++q) buf[q * 32 + lane] = v[q];
+    __syncwarp();
+    const uint32_t lo = max(rb, base), hi = min(re, base + kCWin);
+    for (uint32_t j = lo; j < hi; ++j) acc = __dadd_rn(acc, buf[j - base]);  // in order
+    __syncwarp();
+  }
+  if (has) finish_row(a, k0 + lane, acc);
+}
+
 __global__ void __launch_bounds__(kPrWarps * 32) pr_step_kernel(const PrStepArgs a) {
   __shared__ __align__(16) double smem[kPrWarps * 32 / kBLanes * kBStride];  // 16.6 KB: class B windows
   if (blockIdx.x < a.b_ctas) {
     const int g = threadIdx.x / kBLanes;  // row group within the CTA
     const int64_t i = a.nA + (int64_t)blockIdx.x * (kPrWarps * 32 / kBLanes) + g;
     group_row(a, i, smem + g * kBStride);
+  } else if (!a.order) {
+    // storage-sorted twin: 32 consecutive rows per warp, staged chunks
+    const int w = threadIdx.x >> 5;
+    const uint64_t k0 = a.row_begin + a.nB + ((uint64_t)(blockIdx.x - a.b_ctas) * kPrWarps + w) * 32;
+    warp_rows_staged(a, k0, smem + w * kCWin);
   } else {
     const uint64_t i = a.nB + (uint64_t)(blockIdx.x - a.b_ctas) * blockDim.x + threadIdx.x;
     if (i < a.m) thread_row(a, a.order[i]);
@@ -845,7 +941,7 @@ void pagerank_step(tg_ctx* ctx, const tg_graph* g, const uint32_t* deg, double d
   PrStepArgs a;
   a.off = g->off;
   a.tgt = g->tgt;
-  a.deg = deg;
+  a.deg = g->deg_rows ? g->deg_rows : deg;  // the twin's in-degrees in storage order
   a.norm_in = nin;
   a.norm_out = nout;
   a.score_out = sout;
@@ -860,7 +956,8 @@ void pagerank_step(tg_ctx* ctx, const tg_graph* g, const uint32_t* deg, double d
   a.base = (1.0 - damp) / static_cast<double>(g->n);  // scoring.cpp:53
   a.damp = damp;
   a.last = last;
-  a.score_index = score_index;
+  a.label = g->row_label;
+  a.score_index = g->row_orig ? g->row_orig : score_index;
   a.n_peers = n_peers;
   for (uint32_t p = 0; p < TG_MAX_DEVICES; ++p) {
     a.peer_norm[p] = p < n_peers ? peer_norm[p] : nullptr;
@@ -909,18 +1006,15 @@ bool relabel_wanted(const tg_ctx* ctx, const tg_graph* g) {
   return g->n > 1 && 8.0 * static_cast<double>(g->n) > 0.5 * static_cast<double>(l2);
 }
 
-// Builds g->twin (see tg_graph). One-time per graph: a radix sort of N keys,
-// a scan, and one pass over the targets (12E + 24N bytes).
+// Builds g->twin (see tg_graph). One-time per graph: a radix sort of N
+// keys, two passes over N, a scan and one pass over the targets.
 const tg_graph* relabel_twin(tg_ctx* ctx, const tg_graph* gc) {
   auto* g = const_cast<tg_graph*>(gc);
   if (g->twin || g->twin_tried) return g->twin;
   g->twin_tried = true;
   if (!relabel_wanted(ctx, g)) return nullptr;
   const uint64_t n = g->n, e = g->e;
-  cudaEvent_t ev0, ev1;
-  TGB_CUDA(cudaEventCreate(&ev0));
-  TGB_CUDA(cudaEventCreate(&ev1));
-  TGB_CUDA(cudaEventRecord(ev0, ctx->stream));
+  const tg_graph::Sched sg = schedule(ctx, g, 0, n);  // sigma: K3's row order
   auto* t = new tg_graph;
   t->ctx = ctx;
   t->n = n;
@@ -928,42 +1022,58 @@ const tg_graph* relabel_twin(tg_ctx* ctx, const tg_graph* gc) {
   t->rb = 0;
   t->re = n;
   uint64_t* lens = nullptr;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   try {
     TGB_CUDA(cudaMalloc(&g->old_of, 4 * n));
     TGB_CUDA(cudaMalloc(&g->new_of, 4 * n));
     TGB_CUDA(cudaMalloc(&t->off, 4 * (n + 1)));
     TGB_CUDA(cudaMalloc(&t->tgt, 4 * std::max<uint64_t>(e, 1)));
     TGB_CUDA(cudaMalloc(&t->indeg, 4 * n));
-    TGB_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&lens), 8 * (n + 1), ctx->stream));
+    TGB_CUDA(cudaMalloc(&t->row_label, 4 * n));
+    TGB_CUDA(cudaMalloc(&t->row_orig, 4 * n));
+    TGB_CUDA(cudaMalloc(&t->deg_rows, 4 * n));
+    TGB_CUDA(cudaMalloc(&lens, 8 * (n + 1) + 16));
+    TGB_CUDA(cudaEventCreate(&ev0));
+    TGB_CUDA(cudaEventCreate(&ev1));
+    TGB_CUDA(cudaEventRecord(ev0, ctx->stream));
     sort_ids_by_value_desc(ctx, g->indeg, n, g->old_of);
-    twin_lens_kernel<<<grid_for(n, 256), 256, 0, ctx->stream>>>(g->off, g->old_of, g->indeg, n,
-                                                                lens, g->new_of, t->indeg);
+    twin_labels_kernel<<<grid_for(n, 256), 256, 0, ctx->stream>>>(g->old_of, g->indeg, n,
+                                                                  g->new_of, t->indeg);
+    TGB_LAUNCHED();
+    twin_rows_meta_kernel<<<grid_for(n, 256), 256, 0, ctx->stream>>>(
+        g->off, sg.order, g->new_of, g->indeg, n, lens, t->row_label, t->row_orig, t->deg_rows);
     TGB_LAUNCHED();
     TGB_CUDA(cudaMemsetAsync(lens + n, 0, 8, ctx->stream));
     exclusive_scan_u64(ctx, lens, n + 1);
     narrow_u64_kernel<<<grid_for(n + 1, 256), 256, 0, ctx->stream>>>(lens, t->off, n + 1);
     TGB_LAUNCHED();
-    TGB_CUDA(cudaFreeAsync(lens, ctx->stream));
-    lens = nullptr;
     if (e) {
-      twin_rows_kernel<<<grid_for(n * 32, 256, ctx->num_sms * 16), 256, 0, ctx->stream>>>(
-          g->off, g->tgt, g->old_of, g->new_of, n, t->off, t->tgt);
+      uint64_t* k_short = lens;  // reuse: lens is consumed
+      first_short_kernel<<<1, 32, 0, ctx->stream>>>(t->off, n, 8, k_short);
+      TGB_LAUNCHED();
+      uint64_t ks = 0;
+      TGB_CUDA(cudaMemcpyAsync(&ks, k_short, 8, cudaMemcpyDeviceToHost, ctx->stream));
+      ctx->sync();
+      twin_rows_kernel<<<ctx->num_sms * 16, 256, 0, ctx->stream>>>(
+          g->off, g->tgt, sg.order, g->new_of, ks, n, t->off, t->tgt);
       TGB_LAUNCHED();
     }
-    schedule(ctx, t, 0, n);
     TGB_CUDA(cudaEventRecord(ev1, ctx->stream));
     TGB_CUDA(cudaEventSynchronize(ev1));
     TGB_CUDA(cudaEventElapsedTime(&g->twin_ms, ev0, ev1));
+    // storage order IS the schedule: identity order, the same class bounds
+    t->scheds.push_back(tg_graph::Sched{0, n, nullptr, sg.nA, sg.nB, sg.nLong});
   } catch (...) {
-    if (lens) cudaFree(lens);
+    cudaFree(lens);
     tg_graph_destroy(t);
     cudaFree(g->old_of);
     cudaFree(g->new_of);
     g->old_of = g->new_of = nullptr;
-    cudaEventDestroy(ev0);
-    cudaEventDestroy(ev1);
+    if (ev0) cudaEventDestroy(ev0);
+    if (ev1) cudaEventDestroy(ev1);
     throw;
   }
+  cudaFree(lens);
   cudaEventDestroy(ev0);
   cudaEventDestroy(ev1);
   g->twin = t;
@@ -1013,8 +1123,7 @@ void run_pagerank(tg_ctx* ctx, const tg_graph* g, uint32_t iterations, double da
   if (phase_ms) TGB_CUDA(cudaEventRecord(ev[1], ctx->stream));
   for (uint32_t it = 0; it < iterations; ++it) {
     const bool last = it + 1 == iterations;
-    pagerank_step(ctx, run, deg, damp, na, nb, o.dev(), 0, n, last ? 1 : 0, 0, nullptr, nullptr,
-                  tw ? g->old_of : nullptr);
+    pagerank_step(ctx, run, deg, damp, na, nb, o.dev(), 0, n, last ? 1 : 0);
     if (phase_ms) TGB_CUDA(cudaEventRecord(ev[it + 2], ctx->stream));
     std::swap(na, nb);
   }
@@ -1266,9 +1375,13 @@ int tg_graph_destroy(tg_graph* g) {
   tg_graph_destroy(g->twin);
   cudaFree(g->old_of);
   cudaFree(g->new_of);
+  cudaFree(g->row_label);
+  cudaFree(g->row_orig);
+  cudaFree(g->deg_rows);
   cudaFree(g->off_alloc ? g->off_alloc : g->off);
   cudaFree(g->tgt);
-  for (auto& sc : g->scheds) cudaFree(sc.order);
+  for (auto& sc : g->scheds)
+    if (sc.order) cudaFree(sc.order);
   cudaFree(g->indeg);
   delete g;
   return TG_OK;

@@ -36,11 +36,22 @@ struct tg_graph {
   // so every row sum is the reference's chain over the same values (bit-exact)
   // while the gathered norm values of the most-referenced nodes share sectors
   // and stay L2-resident.
+  //
+  // The twin also STORES its rows in K3's schedule order (length descending,
+  // ties by id), so its schedule is the identity and a warp's class-C rows
+  // are contiguous in memory (coalesced target streaming). Its vectors are
+  // indexed by label: row k writes norm[row_label[k]]; its in-degrees are
+  // kept by label (indeg, for the init) and by storage row (deg_rows); the
+  // last step writes the score of row k to out[row_orig[k]].
   tg_graph* twin = nullptr;
-  uint32_t* old_of = nullptr;  // twin id -> this graph's id
-  uint32_t* new_of = nullptr;  // this graph's id -> twin id
+  uint32_t* old_of = nullptr;  // label -> this graph's id
+  uint32_t* new_of = nullptr;  // this graph's id -> label
   bool twin_tried = false;
-  float twin_ms = 0.0f;        // one-time build time (device)
+  float twin_ms = 0.0f;        // one-time build time (device, allocations excluded)
+  // (twin only)
+  uint32_t* row_label = nullptr;
+  uint32_t* row_orig = nullptr;
+  uint32_t* deg_rows = nullptr;
 };
 
 namespace tgb {

@@ -24,6 +24,8 @@ struct tg_store {
   uint8_t* cold_tail = nullptr;                   // device, (N-mb) x (R - cold_head)
   bool own_cold_tail = false;
   bool own_cold = false;
+  bool cold_attached = false;                     // cold_host is caller memory (tg_store_attach_cold)
+  bool cold_fill = true;                          // ... and this store writes the cold rows
   void* registered = nullptr;                     // caller matrix registered for INDIRECT
   uint32_t* cold_src = nullptr;                   // INDIRECT: cold slot -> original row
   bool own_cold_src = false;

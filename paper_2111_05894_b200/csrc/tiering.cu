@@ -21,6 +21,13 @@
 // up to 8 independent 16 B loads before storing them, so each warp keeps
 // ~4 KB in flight — the queue depth the PCIe zero-copy path needs.
 #include <cuda_runtime.h>
+#include <errno.h>
+#include <fcntl.h>
+#include <sys/mman.h>
+#include <sys/stat.h>
+#include <unistd.h>
+
+#include <cstring>
 
 #include <algorithm>
 #include <cstdlib>
@@ -1222,7 +1229,7 @@ const uint8_t* ensure_cold_tier(tg_store* s) {
       s->own_cold_tail = true;
     }
   }
-  if (!s->own_cold) {
+  if (!s->own_cold && !s->cold_attached) {
     TGB_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&s->cold_host),
                            std::max<uint64_t>(cold * s->cold_stride, 16),
                            cudaHostAllocMapped | cudaHostAllocPortable));
@@ -1296,7 +1303,7 @@ void place_impl(tg_store* s, const void* src_rows, uint64_t src_nrows, const uin
     c.src_idx32 = order;
     c.src_row_base = mb;
     const uint64_t H = s->cold_head ? s->cold_head : R;
-    launch_move(ctx, c, cold, H);
+    if (!s->cold_attached || s->cold_fill) launch_move(ctx, c, cold, H);  // else filled by its owner
     if (s->cold_head) {  // the remainders into HBM
       MoveArgs t = c;
       t.src = src + H;
@@ -1543,6 +1550,84 @@ int tg_host_alloc(uint64_t bytes, void** out) {
 }
 int tg_host_free(void* p) {
   return guard([&] { TGB_CUDA(cudaFreeHost(p)); });
+}
+
+// One host segment per NODE shared by every process (PAPER.md:659-663:
+// shared memory + cudaHostRegister in each process): POSIX shared memory
+// (/dev/shm), mapped and registered (mapped | portable) in the caller.
+int tg_host_shared_map(const char* name, uint64_t bytes, int create, void** out) {
+  return guard([&] {
+    if (!name || !out || !bytes) domain_error("tg_host_shared_map: bad argument");
+    const int fd = shm_open(name, create ? (O_CREAT | O_EXCL | O_RDWR) : O_RDWR, 0600);
+    if (fd < 0)
+      throw Error(TG_ERR_IO, std::string("shm_open ") + name + ": " + std::strerror(errno));
+    if (create && ftruncate(fd, static_cast<off_t>(bytes)) != 0) {
+      const int e = errno;
+      close(fd);
+      shm_unlink(name);
+      throw Error(TG_ERR_IO, std::string("ftruncate ") + name + ": " + std::strerror(e));
+    }
+    struct stat st{};
+    if (fstat(fd, &st) != 0 || static_cast<uint64_t>(st.st_size) < bytes) {
+      close(fd);
+      throw Error(TG_ERR_IO, std::string("shared segment ") + name + " is smaller than requested");
+    }
+    void* p = mmap(nullptr, bytes, PROT_READ | PROT_WRITE, MAP_SHARED, fd, 0);
+    close(fd);
+    if (p == MAP_FAILED) throw Error(TG_ERR_IO, std::string("mmap ") + name + ": " + std::strerror(errno));
+    const cudaError_t e = cudaHostRegister(p, bytes, cudaHostRegisterMapped | cudaHostRegisterPortable);
+    if (e != cudaSuccess) {
+      munmap(p, bytes);
+      TGB_CUDA(e);
+    }
+    *out = p;
+  });
+}
+
+int tg_host_shared_unmap(void* p, uint64_t bytes) {
+  return guard([&] {
+    TGB_CUDA(cudaHostUnregister(p));
+    if (munmap(p, bytes) != 0) throw Error(TG_ERR_IO, std::string("munmap: ") + std::strerror(errno));
+  });
+}
+
+int tg_host_shared_unlink(const char* name) {
+  return guard([&] {
+    if (shm_unlink(name) != 0 && errno != ENOENT)
+      throw Error(TG_ERR_IO, std::string("shm_unlink ") + name + ": " + std::strerror(errno));
+  });
+}
+
+// The cold tier in caller memory (e.g. a tg_host_shared_map segment shared
+// by all processes of a node): `bytes` >= tg_store_cold_tier_bytes(s). With
+// fill != 0 this store's placement writes the cold rows there (one process
+// per node does); with fill == 0 it only reads them (the others, after the
+// filler's placement finished).
+int tg_store_attach_cold(tg_store* s, void* host, uint64_t bytes, int fill) {
+  return guard([&] {
+    if (s->flags & TG_COLD_INDIRECT)
+      domain_error("tg_store_attach_cold: the store reads its cold rows in place (INDIRECT)");
+    if (s->placed) domain_error("tg_store_attach_cold: call before placement");
+    const uint64_t need = tg_store_cold_tier_bytes(s);
+    if (bytes < need)
+      domain_error("tg_store_attach_cold: " + std::to_string(bytes) + " bytes, " +
+                   std::to_string(need) + " needed");
+    if (!mapped_device_ptr(host))
+      domain_error("tg_store_attach_cold: memory is not mapped for the device (register it)");
+    if (s->own_cold && s->cold_host) cudaFreeHost(s->cold_host);
+    s->cold_host = static_cast<uint8_t*>(host);
+    s->own_cold = false;
+    s->cold_attached = true;
+    s->cold_fill = fill != 0;
+  });
+}
+
+uint64_t tg_store_cold_tier_bytes(const tg_store* s) {
+  const uint64_t cold = s->L.num_rows - s->L.multi_boundary;
+  uint64_t stride = (s->flags & TG_COLD_PAD128) ? (s->R + 127) / 128 * 128 : s->R;
+  if ((s->flags & TG_COLD_SPLIT_TAIL) && s->R > 128 && s->R % 128 && s->R % 16 == 0)
+    stride = s->R / 128 * 128;
+  return std::max<uint64_t>(cold * stride, 16);
 }
 
 }  // extern "C"

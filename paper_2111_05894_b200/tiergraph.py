@@ -768,6 +768,21 @@ class TieredFeatureStore:
         self._keep = [data]  # TG_COLD_INDIRECT maps the caller's matrix: keep it alive
         _check(LIB.tg_store_place(self.h, _ptr(data), _nonempty(p, np.uint64)))
 
+    @property
+    def cold_tier_bytes(self) -> int:
+        """Host bytes of the cold tier in this store's format."""
+        return int(LIB.tg_store_cold_tier_bytes(self.h))
+
+    def attach_cold(self, host, fill: bool):
+        """Use `host` (a SharedHostSegment or a mapped/registered array) as the
+        cold tier; call with place=False at construction, before place().
+        fill=True: this store writes the cold rows (one process per node);
+        fill=False: another process has written them."""
+        ptr, nbytes = (host.ptr, host.nbytes) if isinstance(host, SharedHostSegment) else \
+            (_ptr(host), _nbytes(host))
+        self._cold_ref = host
+        _check(LIB.tg_store_attach_cold(self.h, C.c_void_p(ptr), nbytes, int(fill)))
+
     def place_file(self, path, perm):
         """K7 straight from a FEAT v1 file (io.hpp:35): rows to this device's
         HBM slots and the pinned cold tier, no N x R host copy."""
@@ -878,6 +893,33 @@ class TieredFeatureStore:
 
 
 # ------------------------------------------------------------ utilities
+class SharedHostSegment:
+    """One pinned host segment per NODE shared by all its processes
+    (tg_host_shared_map: POSIX shared memory, mapped and registered in each
+    process -- PAPER.md:659-663). `array` is a uint8 numpy view. The creator
+    unlinks the name on close (the memory lives until every process unmaps)."""
+
+    def __init__(self, name: str, nbytes: int, create: bool):
+        p = C.c_void_p()
+        _check(LIB.tg_host_shared_map(name.encode(), int(nbytes), int(create), C.byref(p)))
+        self.name, self.nbytes, self.ptr, self.creator = name, int(nbytes), p.value, create
+        self.array = np.frombuffer((C.c_uint8 * self.nbytes).from_address(self.ptr), np.uint8)
+
+    def close(self):
+        if self.ptr:
+            self.array = None
+            LIB.tg_host_shared_unmap(C.c_void_p(self.ptr), self.nbytes)
+            if self.creator:
+                LIB.tg_host_shared_unlink(self.name.encode())
+            self.ptr = 0
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
 def host_alloc(nbytes: int) -> np.ndarray:
     """Pinned, mapped host buffer (cudaHostAlloc Mapped|Portable) as uint8 numpy."""
     p = C.c_void_p()

@@ -66,7 +66,7 @@ def k8(args):
     torch.cuda.set_stream(stream)
     ctx = tg.Context(0, stream=stream)
     t0 = time.time()
-    feat, R = bench.pin_features(cfg, ctx)
+    feat, R, _ = bench.pin_features(cfg, ctx)
     lay = tg.plan_layout(n, bench.hot_fraction(cfg, 1), 0.0, 1, cfg["dim"], cfg["elem"],
                          (int(np.ceil(cfg["hot_per_gpu"] * n)) + 1) * R if "hot_per_gpu" in cfg
                          else 0)

@@ -204,3 +204,89 @@ def test_fused_exchange_across_processes_is_bit_exact(world):
     for k, iters in enumerate((5, 1, 2)):
         want = chk.weighted_reverse_pagerank(off, tgt, tid, iters, 0.85).tobytes()
         assert all(v[k] == want for v in res.values()), f"world={world} iters={iters}"
+
+
+def _gather_worker(rank, world, port, n, dim, q):
+    """One process per rank on cuda:0: the hot tier sharded over the ranks
+    (interleaved rows, peer reads through CUDA-IPC mappings) and ONE cold tier
+    for the node in POSIX shared memory (rank 0 fills it, the others map it)."""
+    import ctypes as C
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2111_05894_b200 import synth, tiergraph as tg
+        from paper_2111_05894_b200._lib import LIB
+        chk = oracle.ref() or oracle.port()
+        ctx = tg.Context(0)
+        feat = synth.test_features(n, dim)
+        perm = tg.NodePermutation(np.random.default_rng(3).permutation(n).astype(np.uint64))
+        lay = tg.plan_layout(n, 0.3, 0.05, world, dim, 4)
+        store = tg.TieredFeatureStore(None, None, lay, rank, ctx=ctx, place=False)
+        name = f"/tg_test_cold_{port}"
+        seg = tg.SharedHostSegment(name, store.cold_tier_bytes, create=(rank == 0))  \
+            if rank == 0 else None
+        dist.barrier()
+        if rank != 0:
+            seg = tg.SharedHostSegment(name, store.cold_tier_bytes, create=False)
+        store.attach_cold(seg, fill=(rank == 0))
+        if rank == 0:
+            store.place(feat, perm)
+        dist.barrier()  # the cold rows are in the segment
+        if rank != 0:
+            store.place(feat, perm)
+        h = (C.c_uint8 * 64)()
+        assert LIB.tg_ipc_get_handle(C.c_void_p(store.local_base), h) == 0
+        allh = [None] * world
+        dist.all_gather_object(allh, bytes(h))
+        opened = []
+        for d in range(world):
+            if d == rank:
+                continue
+            p = C.c_void_p()
+            assert LIB.tg_ipc_open_handle(ctx.h, (C.c_uint8 * 64).from_buffer_copy(allh[d]),
+                                          C.byref(p)) == 0
+            store.set_peer(d, p.value)
+            opened.append(p.value)
+        dist.barrier()
+        inv = np.empty(n, np.uint64)
+        inv[perm.new_id_of.astype(np.int64)] = np.arange(n, dtype=np.uint64)
+        ok = True
+        rng = np.random.default_rng(10 + rank)
+        for _ in range(4):
+            ids = np.unique(rng.integers(0, n, 3000)).astype(np.uint64)
+            rep = tg.TrafficReport()
+            got = store.gather_rows(ids, report=rep)
+            ok &= bool(np.array_equal(got.view(np.float32), synth.expected_rows(inv[ids], dim)))
+            ok &= bool(np.array_equal(rep.as_array(), chk.gather(lay.as_tuple(), ids, rank)))
+            ok &= rep.peer_accesses > 0 and rep.host_accesses > 0
+        dist.barrier()
+        for p in opened:
+            LIB.tg_ipc_close_handle(C.c_void_p(p))
+        store.close()
+        dist.barrier()
+        seg.close()
+        q.put((rank, ok))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("world", [2, 3])
+def test_ipc_gather_with_node_shared_cold_tier(world):
+    """K8 across processes: rows byte-exact and TrafficReports equal to the
+    reference gather() for every rank, with peer rows read over CUDA-IPC and
+    one shared cold tier for the node."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    p0 = _free_port()
+    procs = [ctx.Process(target=_gather_worker, args=(r, world, p0, 40_000, 64, q))
+             for r in range(world)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=600) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert all(res.values()), res
+    assert not os.path.exists(f"/dev/shm/tg_test_cold_{p0}")
