@@ -10,9 +10,11 @@
 // scores, and equal scores (including +-0) share a key. A stable sort over
 // ids presented in ascending order reproduces the id tie-break exactly.
 //
-// Sort: 8-bit digits, reduce-then-scan per pass (block digit counts -> one
-// scan -> stable block-local ranking via warp __match_any_sync -> scatter).
-// One upfront pass builds all eight digit histograms; passes whose digit is
+// Sort: 8-bit LSD digits, ONE kernel per pass (onesweep: stable block-local
+// ranking via warp __match_any_sync, the earlier tiles' digit counts by
+// decoupled look-back, a digit-ordered shared-memory tile written out in
+// coalesced runs). One upfront pass builds all eight digit histograms (the
+// digits' global bases); passes whose digit is
 // constant over the whole input are skipped on the device (no host sync), with
 // the ping-pong buffer choice planned on the device as well.
 #include <cuda_runtime.h>
@@ -85,80 +87,22 @@ __global__ void __launch_bounds__(256) plan_kernel(const uint32_t* __restrict__ 
   plan->final_src = src;
 }
 
-__global__ void __launch_bounds__(kRsWarps * 32) digit_count_kernel(
-    const uint64_t* __restrict__ k0, const uint64_t* __restrict__ k1, uint64_t n, int pass,
-    const RadixPlan* __restrict__ plan, uint32_t* __restrict__ counts, uint32_t nblk) {
-  if (plan->skip[pass]) return;
-  const uint64_t* keys = plan->src[pass] ? k1 : k0;
-  __shared__ uint32_t h[256];
-  h[threadIdx.x] = 0;
-  __syncthreads();
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  const uint64_t base = (uint64_t)blockIdx.x * kRsTile + w * (32 * kRsIpt);
-  const int shift = 8 * pass;
-#pragma unroll
-  for (int k = 0; k < kRsIpt; ++k) {
-    const uint64_t i = base + k * 32 + lane;
-    if (i < n) atomicAdd(&h[(keys[i] >> shift) & 0xff], 1u);
-  }
-  __syncthreads();
-  counts[(uint64_t)blockIdx.x * 256 + threadIdx.x] = h[threadIdx.x];  // block-major
-}
-
-// Per-digit exclusive scan over the blocks: CTA d scans column d of the
-// block-major count matrix [nblk][256] in place and leaves the digit's total
-// in totals[d]. (The digit bases are an exclusive scan of the 256 totals,
-// done by every scatter CTA in its prologue.)
-__global__ void __launch_bounds__(1024) count_scan_kernel(uint32_t* __restrict__ counts,
-                                                          uint32_t nblk, int pass,
-                                                          const RadixPlan* __restrict__ plan,
-                                                          uint32_t* __restrict__ totals) {
-  if (plan->skip[pass]) return;
-  __shared__ uint32_t warp_tot[32];
-  __shared__ uint32_t carry;
-  const int d = blockIdx.x, lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  if (threadIdx.x == 0) carry = 0;
-  __syncthreads();
-  for (uint32_t b0 = 0; b0 < nblk; b0 += blockDim.x) {
-    const uint32_t b = b0 + threadIdx.x;
-    const uint32_t c = b < nblk ? counts[(uint64_t)b * 256 + d] : 0u;
-    uint32_t incl = c;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
-      if (lane >= o) incl += y;
-    }
-    if (lane == 31) warp_tot[w] = incl;
-    __syncthreads();
-    if (w == 0) {
-      const uint32_t t = lane < (int)(blockDim.x / 32) ? warp_tot[lane] : 0u;
-      uint32_t ti = t;
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const uint32_t y = __shfl_up_sync(0xffffffffu, ti, o);
-        if (lane >= o) ti += y;
-      }
-      warp_tot[lane] = ti - t;
-    }
-    __syncthreads();
-    const uint32_t base = carry;
-    if (b < nblk) counts[(uint64_t)b * 256 + d] = base + warp_tot[w] + incl - c;
-    __syncthreads();
-    if (threadIdx.x == blockDim.x - 1) carry = base + warp_tot[w] + incl;
-    __syncthreads();
-  }
-  if (threadIdx.x == 0) totals[d] = carry;
-}
-
-// Stable block-local ranking (warp rounds in index order + per-warp digit
-// counters). The tile is then reordered by digit in shared memory and written
-// out in that order, so consecutive threads store consecutive positions of a
-// digit's run (coalesced) instead of 32 unrelated runs per store.
+// One onesweep pass (a single kernel per digit: no separate count and scan
+// kernels). Each CTA takes the next tile id from a counter (tiles are
+// claimed in launch order, so every tile waits only on tiles already
+// running), ranks its 4,096 keys stably (warp rounds in index order +
+// per-warp digit counters, __match_any_sync), publishes its per-digit counts
+// and finds the counts of all earlier tiles by DECOUPLED LOOK-BACK over their
+// published status words (flag: 1 = this tile's count, 2 = inclusive prefix
+// of tiles 0..t). The digit's global base comes from the all-pass histogram
+// of the key-prep kernel. The tile is then reordered by digit in shared
+// memory and written out in that order (coalesced runs).
 constexpr int kRsScatterSmem = kRsTile * (8 + 4);  // staged keys + values
+constexpr uint64_t kStAgg = 1ull << 62, kStInc = 2ull << 62, kStMask = (1ull << 62) - 1;
 __global__ void __launch_bounds__(kRsWarps * 32, 3) scatter_kernel(
     uint64_t* __restrict__ k0, uint32_t* __restrict__ v0, uint64_t* __restrict__ k1,
     uint32_t* __restrict__ v1, uint64_t n, int pass, const RadixPlan* __restrict__ plan,
-    const uint32_t* __restrict__ offs, uint32_t nblk, const uint32_t* __restrict__ totals) {
+    const uint32_t* __restrict__ hist, uint64_t* __restrict__ status, uint32_t* __restrict__ tile_ctr) {
   if (plan->skip[pass]) return;
   const bool from1 = plan->src[pass] != 0;
   const uint64_t* kin = from1 ? k1 : k0;
@@ -171,27 +115,14 @@ __global__ void __launch_bounds__(kRsWarps * 32, 3) scatter_kernel(
   __shared__ uint32_t wcnt[kRsWarps][256];
   __shared__ uint32_t doff[256];
   __shared__ uint32_t tstart[256];
+  __shared__ uint32_t tile_s;
+  if (threadIdx.x == 0) tile_s = atomicAdd(tile_ctr + pass, 1u);
   for (int i = threadIdx.x; i < kRsWarps * 256; i += blockDim.x) (&wcnt[0][0])[i] = 0;
-  {  // digit base (exclusive scan of the 256 totals) + this block's column prefix
-    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-    const uint32_t t = totals[threadIdx.x];
-    uint32_t incl = t;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
-      if (lane >= o) incl += y;
-    }
-    __shared__ uint32_t wt[kRsWarps];
-    if (lane == 31) wt[w] = incl;
-    __syncthreads();
-    uint32_t before = 0;
-    for (int k = 0; k < w; ++k) before += wt[k];
-    doff[threadIdx.x] = before + incl - t + offs[(uint64_t)blockIdx.x * 256 + threadIdx.x];
-  }
   __syncthreads();
+  const uint32_t tile = tile_s;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const uint32_t lt = (1u << lane) - 1u;
-  const uint64_t base = (uint64_t)blockIdx.x * kRsTile + w * (32 * kRsIpt);
+  const uint64_t base = (uint64_t)tile * kRsTile + w * (32 * kRsIpt);
   const int shift = 8 * pass;
   uint64_t key[kRsIpt];
   uint32_t val[kRsIpt];
@@ -224,19 +155,46 @@ __global__ void __launch_bounds__(kRsWarps * 32, 3) scatter_kernel(
       wcnt[ww][d] = run;
       run += c;
     }
-    // the digit's start within the tile: exclusive scan of the tile totals
-    uint32_t incl = run;
+    // publish this tile's count, then look back for the earlier tiles'
+    volatile uint64_t* st = status;
+    st[(uint64_t)tile * 256 + d] = (tile ? kStAgg : kStInc) | run;
+    uint64_t excl = 0;
+    for (int64_t j = (int64_t)tile - 1; j >= 0;) {
+      const uint64_t v = st[(uint64_t)j * 256 + d];
+      if (!(v & (kStAgg | kStInc))) continue;  // not published yet: spin
+      excl += v & kStMask;
+      if (v & kStInc) break;
+      --j;
+    }
+    if (tile) st[(uint64_t)tile * 256 + d] = kStInc | (excl + run);
+    // the digit's global base: exclusive scan of this pass's histogram
+    const uint32_t t = hist[pass * 256 + d];
+    uint32_t incl = t;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
       const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
       if (lane >= o) incl += y;
     }
-    __shared__ uint32_t st[kRsWarps];
-    if (lane == 31) st[w] = incl;
+    // tile-local digit start: exclusive scan of `run`
+    uint32_t incl2 = run;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, incl2, o);
+      if (lane >= o) incl2 += y;
+    }
+    __shared__ uint32_t wt[kRsWarps], st2[kRsWarps];
+    if (lane == 31) {
+      wt[w] = incl;
+      st2[w] = incl2;
+    }
     __syncthreads();
-    uint32_t before = 0;
-    for (int k = 0; k < w; ++k) before += st[k];
-    tstart[d] = before + incl - run;
+    uint32_t before = 0, before2 = 0;
+    for (int k = 0; k < w; ++k) {
+      before += wt[k];
+      before2 += st2[k];
+    }
+    doff[d] = before + incl - t + static_cast<uint32_t>(excl);
+    tstart[d] = before2 + incl2 - run;
   }
   __syncthreads();
 #pragma unroll
@@ -250,7 +208,7 @@ __global__ void __launch_bounds__(kRsWarps * 32, 3) scatter_kernel(
     }
   }
   __syncthreads();
-  const uint64_t t0 = (uint64_t)blockIdx.x * kRsTile;
+  const uint64_t t0 = (uint64_t)tile * kRsTile;
   const uint32_t tn = static_cast<uint32_t>(n - t0 < (uint64_t)kRsTile ? n - t0 : kRsTile);
   for (uint32_t j = threadIdx.x; j < tn; j += blockDim.x) {
     const uint64_t kk = skey[j];
@@ -261,18 +219,29 @@ __global__ void __launch_bounds__(kRsWarps * 32, 3) scatter_kernel(
   }
 }
 
-// Launches scatter_kernel with its staged tile (dynamic shared memory).
-void launch_scatter(tg_ctx* ctx, uint64_t* k0, uint32_t* v0, uint64_t* k1, uint32_t* v1,
-                    uint64_t n, int pass, const RadixPlan* plan, const uint32_t* counts,
-                    uint32_t nblk, const uint32_t* totals) {
+// The passes of one LSD sort (keys k0/v0 in, result where plan->final_src
+// says): one onesweep kernel per digit that is not constant.
+void radix_passes(tg_ctx* ctx, uint64_t* k0, uint32_t* v0, uint64_t* k1, uint32_t* v1, uint64_t n,
+                  int passes, const RadixPlan* plan, const uint32_t* hist) {
   static bool attr[TG_MAX_DEVICES] = {};
   if (!attr[ctx->device % TG_MAX_DEVICES]) {
     TGB_CUDA(cudaFuncSetAttribute(scatter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   kRsScatterSmem));
     attr[ctx->device % TG_MAX_DEVICES] = true;
   }
-  scatter_kernel<<<nblk, kRsWarps * 32, kRsScatterSmem, ctx->stream>>>(k0, v0, k1, v1, n, pass,
-                                                                       plan, counts, nblk, totals);
+  const uint32_t nblk = static_cast<uint32_t>((n + kRsTile - 1) / kRsTile);
+  uint64_t* status = nullptr;
+  const size_t sbytes = 8ull * 256 * nblk;
+  TGB_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&status), sbytes + 64, ctx->stream));
+  auto* ctr = reinterpret_cast<uint32_t*>(reinterpret_cast<char*>(status) + sbytes);
+  TGB_CUDA(cudaMemsetAsync(ctr, 0, 64, ctx->stream));
+  for (int p = 0; p < passes; ++p) {
+    TGB_CUDA(cudaMemsetAsync(status, 0, sbytes, ctx->stream));
+    scatter_kernel<<<nblk, kRsWarps * 32, kRsScatterSmem, ctx->stream>>>(k0, v0, k1, v1, n, p, plan,
+                                                                         hist, status, ctr);
+    TGB_LAUNCHED();
+  }
+  TGB_CUDA(cudaFreeAsync(status, ctx->stream));
 }
 
 // K6: order[r] = id, new_id_of[id] = r (reorder.cpp:27)
@@ -345,11 +314,9 @@ static void sort_desc_u32(tg_ctx* ctx, const uint32_t* off, const uint32_t* val,
                           uint64_t re, uint32_t* order_dev) {
   const uint64_t m = re - rb;
   if (m == 0) return;
-  const uint32_t nblk = static_cast<uint32_t>((m + kRsTile - 1) / kRsTile);
   // private temporaries (stream-ordered allocations): callers may hold the
   // context's scratch slots across this call
-  const size_t bytes = 2 * 8 * m + 2 * 4 * m + 4ull * 256 * nblk + 64 + sizeof(RadixPlan) +
-                       8 * 256 * 4 + 256 * 4 + 256;
+  const size_t bytes = 2 * 8 * m + 2 * 4 * m + 64 + sizeof(RadixPlan) + 8 * 256 * 4 + 256;
   char* base = nullptr;
   TGB_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&base), bytes, ctx->stream));
   auto align = [](char* p) { return reinterpret_cast<char*>((reinterpret_cast<uintptr_t>(p) + 15) & ~uintptr_t(15)); };
@@ -358,24 +325,15 @@ static void sort_desc_u32(tg_ctx* ctx, const uint32_t* off, const uint32_t* val,
   uint64_t* k1 = reinterpret_cast<uint64_t*>(p); p = align(p + 8 * m);
   uint32_t* v0 = reinterpret_cast<uint32_t*>(p); p = align(p + 4 * m);
   uint32_t* v1 = reinterpret_cast<uint32_t*>(p); p = align(p + 4 * m);
-  uint32_t* counts = reinterpret_cast<uint32_t*>(p); p = align(p + 4ull * 256 * nblk);
   auto* plan = reinterpret_cast<RadixPlan*>(p); p = align(p + sizeof(RadixPlan));
-  uint32_t* hist = reinterpret_cast<uint32_t*>(p); p = align(p + 8 * 256 * 4);
-  uint32_t* totals = reinterpret_cast<uint32_t*>(p);
+  uint32_t* hist = reinterpret_cast<uint32_t*>(p);
   TGB_CUDA(cudaMemsetAsync(hist, 0, 8 * 256 * 4, ctx->stream));
   rowlen_key_kernel<<<grid_for(m, 256, ctx->num_sms * 8), 256, 0, ctx->stream>>>(off, val, rb, m,
                                                                                 k0, v0, hist);
   TGB_LAUNCHED();
   plan_kernel<<<1, 256, 0, ctx->stream>>>(hist, m, plan);
   TGB_LAUNCHED();
-  for (int pass = 0; pass < 4; ++pass) {  // digits 4..7 are constant: planned as skipped
-    digit_count_kernel<<<nblk, kRsWarps * 32, 0, ctx->stream>>>(k0, k1, m, pass, plan, counts, nblk);
-    TGB_LAUNCHED();
-    count_scan_kernel<<<256, 1024, 0, ctx->stream>>>(counts, nblk, pass, plan, totals);
-    TGB_LAUNCHED();
-    launch_scatter(ctx, k0, v0, k1, v1, m, pass, plan, counts, nblk, totals);
-    TGB_LAUNCHED();
-  }
+  radix_passes(ctx, k0, v0, k1, v1, m, 4, plan, hist);  // digits 4..7 are constant
   order_out_kernel<<<grid_for(m, 256), 256, 0, ctx->stream>>>(v0, v1, plan, rb, m, order_dev);
   TGB_LAUNCHED();
   TGB_CUDA(cudaFreeAsync(base, ctx->stream));
@@ -389,15 +347,12 @@ void sort_scores(tg_ctx* ctx, const double* scores_dev, uint64_t n, uint64_t* or
   uint64_t* k1 = ctx->scratch_t<uint64_t>(kScratchB, n);
   uint32_t* v0 = ctx->scratch_t<uint32_t>(kScratchC, n);
   uint32_t* v1 = ctx->scratch_t<uint32_t>(kScratchD, n);
-  const uint32_t nblk = static_cast<uint32_t>((n + kRsTile - 1) / kRsTile);
   // small slot layout: [bad u64][plan][hist 8x256 u32]
   char* small = static_cast<char*>(
       ctx->scratch(kSmall, 64 + sizeof(RadixPlan) + 8 * 256 * 4 + 256 * 4));
   auto* bad = reinterpret_cast<unsigned long long*>(small);
   auto* plan = reinterpret_cast<RadixPlan*>(small + 64);
   auto* hist = reinterpret_cast<uint32_t*>(small + 64 + sizeof(RadixPlan));
-  auto* totals = hist + 8 * 256;
-  uint32_t* counts = ctx->scratch_t<uint32_t>(kScratchE, (uint64_t)256 * nblk);
   TGB_CUDA(cudaMemsetAsync(bad, 0xff, 8, ctx->stream));
   TGB_CUDA(cudaMemsetAsync(hist, 0, 8 * 256 * 4, ctx->stream));
   key_prep_kernel<<<grid_for(n, 256, ctx->num_sms * 8), 256, 0, ctx->stream>>>(scores_dev, n, k0,
@@ -405,14 +360,7 @@ void sort_scores(tg_ctx* ctx, const double* scores_dev, uint64_t n, uint64_t* or
   TGB_LAUNCHED();
   plan_kernel<<<1, 256, 0, ctx->stream>>>(hist, n, plan);
   TGB_LAUNCHED();
-  for (int p = 0; p < 8; ++p) {
-    digit_count_kernel<<<nblk, kRsWarps * 32, 0, ctx->stream>>>(k0, k1, n, p, plan, counts, nblk);
-    TGB_LAUNCHED();
-    count_scan_kernel<<<256, 1024, 0, ctx->stream>>>(counts, nblk, p, plan, totals);
-    TGB_LAUNCHED();
-    launch_scatter(ctx, k0, v0, k1, v1, n, p, plan, counts, nblk, totals);
-    TGB_LAUNCHED();
-  }
+  radix_passes(ctx, k0, v0, k1, v1, n, 8, plan, hist);
   perm_kernel<<<grid_for(n, 256), 256, 0, ctx->stream>>>(v0, v1, plan, n, order_dev, perm_dev);
   TGB_LAUNCHED();
   unsigned long long hb = 0;
@@ -490,9 +438,7 @@ void transpose_device(tg_ctx* ctx, const uint64_t* off, const uint64_t* tgt, uin
     TGB_CUDA(cudaMemsetAsync(t_off, 0, 8 * (n + 1), ctx->stream));
     return;
   }
-  const uint32_t nblk = static_cast<uint32_t>((e + kRsTile - 1) / kRsTile);
-  const size_t bytes = 2 * 8 * e + 2 * 4 * e + 4ull * 256 * nblk + 64 + sizeof(RadixPlan) +
-                       8 * 256 * 4 + 256 * 4 + 256;
+  const size_t bytes = 2 * 8 * e + 2 * 4 * e + 64 + sizeof(RadixPlan) + 8 * 256 * 4 + 256;
   char* base = nullptr;
   TGB_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&base), bytes, ctx->stream));
   auto align = [](char* p) { return reinterpret_cast<char*>((reinterpret_cast<uintptr_t>(p) + 15) & ~uintptr_t(15)); };
@@ -501,11 +447,9 @@ void transpose_device(tg_ctx* ctx, const uint64_t* off, const uint64_t* tgt, uin
   uint64_t* k1 = reinterpret_cast<uint64_t*>(p); p = align(p + 8 * e);
   uint32_t* v0 = reinterpret_cast<uint32_t*>(p); p = align(p + 4 * e);
   uint32_t* v1 = reinterpret_cast<uint32_t*>(p); p = align(p + 4 * e);
-  uint32_t* counts = reinterpret_cast<uint32_t*>(p); p = align(p + 4ull * 256 * nblk);
   auto* bad = reinterpret_cast<unsigned long long*>(p); p = align(p + 64);
   auto* plan = reinterpret_cast<RadixPlan*>(p); p = align(p + sizeof(RadixPlan));
-  uint32_t* hist = reinterpret_cast<uint32_t*>(p); p = align(p + 8 * 256 * 4);
-  uint32_t* totals = reinterpret_cast<uint32_t*>(p);
+  uint32_t* hist = reinterpret_cast<uint32_t*>(p);
   TGB_CUDA(cudaMemsetAsync(hist, 0, 8 * 256 * 4, ctx->stream));
   TGB_CUDA(cudaMemsetAsync(bad, 0xff, 8, ctx->stream));
   key_range_check_kernel<<<grid_for(e, 256, ctx->num_sms * 8), 256, 0, ctx->stream>>>(tgt, e, n,
@@ -523,14 +467,7 @@ void transpose_device(tg_ctx* ctx, const uint64_t* off, const uint64_t* tgt, uin
   TGB_LAUNCHED();
   plan_kernel<<<1, 256, 0, ctx->stream>>>(hist, e, plan);
   TGB_LAUNCHED();
-  for (int pass = 0; pass < 4; ++pass) {  // digits 4..7 are constant: planned as skipped
-    digit_count_kernel<<<nblk, kRsWarps * 32, 0, ctx->stream>>>(k0, k1, e, pass, plan, counts, nblk);
-    TGB_LAUNCHED();
-    count_scan_kernel<<<256, 1024, 0, ctx->stream>>>(counts, nblk, pass, plan, totals);
-    TGB_LAUNCHED();
-    launch_scatter(ctx, k0, v0, k1, v1, e, pass, plan, counts, nblk, totals);
-    TGB_LAUNCHED();
-  }
+  radix_passes(ctx, k0, v0, k1, v1, e, 4, plan, hist);  // digits 4..7 are constant
   transpose_out_kernel<<<grid_for(e + 1, 256, ctx->num_sms * 16), 256, 0, ctx->stream>>>(
       k0, k1, v0, v1, plan, n, e, t_off, t_tgt);
   TGB_LAUNCHED();
