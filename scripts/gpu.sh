@@ -13,6 +13,7 @@
 #   launches:<cfg> ncu launch list (gpu__time_duration) of a short bench run
 #   ncu_k8:<cfg>   ncu (application replay) of K8 on the cached C3/C4 inputs
 #   ncu_k3:<cfg>   ncu --set full of K3 (pr_step) at <cfg>
+#   prlaunch:<cfg> per-launch time / DRAM / L2 of every K3 kernel (pr_*) at <cfg>
 #   sanitize       compute-sanitizer memcheck/racecheck/synccheck on small cases
 #   shared2        2-process runs on one GPU (IPC gather, PageRank exchange)
 T=${1:?tag}; shift
@@ -52,6 +53,9 @@ for st in "$@"; do
         --metrics dram__bytes_read.sum,dram__bytes_write.sum,lts__t_sectors_aperture_sysmem.sum,lts__t_sectors_aperture_device.sum,lts__t_sectors_srcunit_tex_aperture_sysmem.sum \
         -k regex:gather -s 2 -c 1 -o $O/k8_$a python scripts/profile_target.py k8 --config $a --launches 3 \
         > $O/ncu_k8_$a.log 2>&1 ;;
+    prlaunch) timeout 1800 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum,lts__t_sectors_op_read.sum,lts__t_sector_hit_rate.pct \
+        --clock-control none --csv -k regex:"pr_|gather_floor" --log-file $O/prlaunch_$a.csv \
+        python scripts/profile_target.py k3 --config $a --launches 1 > $O/prlaunch_$a.log 2>&1 ;;
     ncu_k3) timeout 2400 ncu --set full --clock-control none --import-source on -k regex:pr_step -s 2 -c 1 \
         -o $O/k3_$a python scripts/profile_target.py k3 --config $a --launches 1 > $O/ncu_k3_$a.log 2>&1 ;;
     sanitize) bash scripts/sanitize.sh $O ;;
