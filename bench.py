@@ -343,6 +343,96 @@ def bench_pagerank_multi(torch, tg, ctx, g, tid, single, dist, reps=3):
     return res
 
 
+def bench_structure(torch, tg, producers, ctx, gt, new_tid, cfg, lay, lists, nbat, rank, world,
+                    dist, tag):
+    """Graph-structure tiering: the
+    sampler's transposed graph placed by the features' TierLayout (hot rows
+    in HBM, sharded over the ranks and read over CUDA-IPC peer pointers;
+    cold rows in ONE pinned host copy per node). Checked bit-exact against
+    the whole-graph sampler's lists; reports the sampler rate and the
+    neighbour-id bytes each tier served over this rank's share of the epoch
+    against the untiered case (every id read over PCIe from host memory, as
+    in the paper's CPU-resident graph)."""
+    import ctypes as C
+    from paper_2111_05894_b200._lib import LIB
+    seg = None
+    t0 = time.time()
+    if world > 1:
+        nb = producers.TieredGraph.cold_bytes(gt.offsets, lay)
+        name = f"/tg_sgcold_{tag}"
+        if rank == 0:
+            seg = tg.SharedHostSegment(name, nb, create=True)
+        dist.barrier()
+        if rank != 0:
+            seg = tg.SharedHostSegment(name, nb, create=False)
+    sg = producers.TieredGraph(gt.offsets, gt.targets, lay, rank, ctx=ctx, cold=seg,
+                               fill=(rank == 0))
+    opened = []
+    if world > 1:
+        dist.barrier()  # rank 0 wrote the shared cold rows
+        h = (C.c_uint8 * 64)()
+        assert LIB.tg_ipc_get_handle(C.c_void_p(sg.local_base), h) == 0, LIB.tg_last_error()
+        allh = [None] * world
+        dist.all_gather_object(allh, bytes(h))
+        for d in range(world):
+            if d == rank:
+                continue
+            hb = (C.c_uint8 * 64).from_buffer_copy(allh[d])
+            p = C.c_void_p()
+            assert LIB.tg_ipc_open_handle(ctx.h, hb, C.byref(p)) == 0, LIB.tg_last_error()
+            sg.set_peer(d, p.value)
+            opened.append(p.value)
+    build_s = time.time() - t0
+    s = producers.GpuSampler(sg, ctx=ctx)
+    order = producers.epoch_order(new_tid, 7, 0)
+    B = cfg["batch"]
+    per = max(1, nbat // world)  # a contiguous block of the epoch's batches per rank
+    mine = list(range(rank * per, min(nbat, (rank + 1) * per)))
+    chunk = min(len(mine), 32)
+    s.batches(order, cfg["fanouts"], B, 7, 0, mine[0], chunk, device=True)  # warm
+    s.structure_reads(reset=True)
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    t_s = time.perf_counter()
+    ok = True
+    for b0 in range(mine[0], mine[-1] + 1, chunk):  # members left in HBM, as the sampler leg
+        s.batches(order, cfg["fanouts"], B, 7, 0, b0, min(chunk, mine[-1] + 1 - b0), device=True)
+    torch.cuda.synchronize()
+    el = time.perf_counter() - t_s
+    reads = s.structure_reads(reset=True)
+    for b in mine[:4]:  # spot check against the whole-graph sampler's lists
+        ok &= bool(np.array_equal(s.batches(order, cfg["fanouts"], B, 7, 0, b, 1)[0], lists[b]))
+    info = sg.info()
+    vals = [float(reads[0]), float(reads[1]), float(reads[2]), el, float(ok)]
+    if dist:
+        vals = allreduce(dist, vals[:3], torch.device("cuda", ctx.device)) + \
+            allreduce(dist, [el], torch.device("cuda", ctx.device), dist.ReduceOp.MAX) + \
+            allreduce(dist, [float(ok)], torch.device("cuda", ctx.device), dist.ReduceOp.MIN)
+    s.close()
+    if dist:
+        dist.barrier()
+    for p in opened:
+        LIB.tg_ipc_close_handle(C.c_void_p(p))
+    sg.close()
+    if dist:
+        dist.barrier()
+    if seg is not None:
+        seg.close()
+    r0, r1, r2, el, ok = vals
+    tot = r0 + r1 + r2
+    return {"minibatches_per_s": round(len(mine) * world / el, 1), "minibatches": len(mine) * world,
+            "bit_exact_vs_whole_graph": bool(ok),
+            "neighbour_id_bytes": {"local_hbm": int(4 * r0), "peer_hbm": int(4 * r1),
+                                   "host_pcie": int(4 * r2), "untiered_host_pcie": int(4 * tot)},
+            "pcie_reduction": round(1 - r2 / max(tot, 1), 4),
+            "placement": dict(info, build_s=round(build_s, 2)),
+            "how": "tg_sampler_create_tiered over tg_sgraph (csrc/structure.cu): row v of the "
+                   "transposed reordered graph where resolve(v) puts feature row v; "
+                   "tg_sample_batches over a contiguous block of the epoch's minibatches per "
+                   "rank, 32 per call, members left in HBM, host-timed, max over ranks"}
+
+
 def allreduce(dist, vals, device, op=None):
     """All-reduce a few host numbers (fp64) over the ranks; on the gloo
     plumbing of the shared-GPU test mode the tensor stays on the host."""
@@ -516,6 +606,10 @@ def run_ours(args):
     if world > 1:
         exchange_peers(torch, tg, store, rank, world)
         dist.barrier()
+
+    # ---- graph-structure tiering: the sampler over the tiered transposed graph
+    structure = bench_structure(torch, tg, producers, ctx, gt, new_tid, cfg, lay, lists, nbat,
+                                rank, world, dist, tag)
 
     # ---- device-resident per-step inputs
     nsteps = args.steps + args.warmup
@@ -783,7 +877,8 @@ def run_ours(args):
                                 "per call, 4 concurrent sampler lanes), member lists left in HBM; "
                                 "host-timed, median of 3 passes over the epoch",
                          "with_host_copy_minibatches_per_s": round(nbat / sample_s, 1),
-                         "matches_host_restatement": bool(sampler_ok)},
+                         "matches_host_restatement": bool(sampler_ok),
+                         "tiered_structure": structure},
             "epoch": {"minibatches": len(lists), "host_bytes_tiered": int(host_epoch),
                       "bytes_untiered": int(total_epoch),
                       "reduction": round(1 - host_epoch / max(total_epoch, 1), 4),

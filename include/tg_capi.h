@@ -483,6 +483,40 @@ int tg_sample_batches(tg_sampler* s, const uint64_t* order, uint64_t n_order, ui
 int tg_sampler_trace(tg_sampler* s, const uint64_t* tid, uint64_t ntid, const uint32_t* fanouts,
                      uint32_t nf, uint64_t batch_size, uint64_t epochs, uint64_t rng_seed,
                      int dedup_per_batch, uint64_t* counts);
+/* ------------------------------------ graph-structure tiering (§8f row 2)
+ * the sampler's graph distributed like the features. The
+ * reference only estimates it (tools/tiergraph_cli.cpp:389-406,
+ * --structure-of). Row v of the TRANSPOSED, score-reordered graph (new ids)
+ * is placed where resolve(v) (tiering.cpp:48-65) puts feature row v: rows
+ * [0, lb) in every device's HBM, device (v-lb) % D's slice for [lb, mb), and
+ * [mb, N) in pinned mapped host memory (UVA). Offsets (u64, host|device,
+ * validated like tg_graph_create: FormatError "csr: ...") are kept as u32 on
+ * every device. cold_host: optional caller memory mapped for the device
+ * (tg_host_register / a shared segment), >= tg_sgraph_cold_bytes; with
+ * cold_fill = 0 another tiered graph (process) writes it. Without cold_host
+ * the graph allocates its own pinned cold tier. */
+typedef struct tg_sgraph tg_sgraph;
+uint64_t tg_sgraph_cold_bytes(const uint64_t* offsets, uint64_t n, const tg_layout* layout);
+int tg_sgraph_create(tg_ctx* ctx, const tg_layout* layout, uint32_t device_index,
+                     const uint64_t* offsets, const uint64_t* targets, uint64_t n, uint64_t e,
+                     void* cold_host, uint64_t cold_bytes, int cold_fill, tg_sgraph** out);
+int tg_sgraph_destroy(tg_sgraph* s);
+/* This device's interleaved slice (for CUDA IPC) and a peer's slice base
+ * (same process: its tg_sgraph_local_base; other process: the IPC mapping). */
+void* tg_sgraph_local_base(const tg_sgraph* s);
+int tg_sgraph_set_peer(tg_sgraph* s, uint32_t d, const void* peer_slice_base);
+void* tg_sgraph_cold_host(const tg_sgraph* s);
+/* out[4]: bytes of replicated rows (HBM), this device's slice (HBM), the cold
+ * rows (host), and offsets + slice starts (HBM). */
+int tg_sgraph_info(const tg_sgraph* s, uint64_t* out);
+/* A sampler over a tiered graph: the same bit-identical build_minibatch
+ * lists as tg_sampler_create on the whole graph. tg_sampler_structure_reads
+ * returns the neighbour ids read since the last reset per tier {local HBM,
+ * peer HBM, host}: min(deg, fanout) per frontier node, counted where the
+ * node's row lives for this device. */
+int tg_sampler_create_tiered(tg_ctx* ctx, const tg_sgraph* sg, tg_sampler** out);
+int tg_sampler_structure_reads(tg_sampler* s, uint64_t* out, int reset);
+
 /* sampling.cpp:106-109: the epoch's shuffled train-id order (Fisher-Yates,
  * key {0x5348, epoch}); batch b is order[b*batch_size ..). Host arrays. */
 int tg_epoch_order(const uint64_t* tid, uint64_t ntid, uint64_t rng_seed, uint64_t epoch,

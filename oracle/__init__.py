@@ -124,6 +124,8 @@ class PortOracle:
                                           C.POINTER(vp), C.POINTER(U64)]),
             "tgo_sample_index_subset": (U64, [C.POINTER(U64), U64, U64, u64p]),
             "tgo_shuffle": (None, [C.POINTER(U64), u64p, U64]),
+            "tgo_build_minibatch_tier_reads": (I32, [u64p, u64p, U64, u64p, U64, u32p, U32, U64, U64,
+                                                      U64, u64p, U32, u64p]),
             "tgo_free": (None, [vp]),
         }
         for name, (res, args) in sig.items():
@@ -322,6 +324,23 @@ class PortOracle:
         out = out[: m.value].copy()
         self.L.tgo_free(p)
         return out
+
+    def structure_tier_reads(self, gt_off, gt_tgt, seeds, fanouts, layout, device,
+                             rng_seed=0, epoch=0, batch=0):
+        """Neighbour ids build_minibatch reads per tier {local, peer, host}
+        when gt's rows are placed by `layout` (lb, mb, D) for `device`
+        (graph-structure tiering)."""
+        go, gt, s = _u64(gt_off), _u64(gt_tgt), _u64(seeds)
+        f = np.ascontiguousarray(np.asarray(fanouts, np.uint32))
+        lay = layout6(layout)
+        lay3 = np.array([lay[1], lay[2], lay[3]], np.uint64)
+        reads = np.zeros(3, np.uint64)
+        rc = self.L.tgo_build_minibatch_tier_reads(
+            go, gt if len(gt) else np.zeros(1, np.uint64), len(go) - 1,
+            s if len(s) else np.zeros(1, np.uint64), len(s), f if len(f) else np.zeros(1, np.uint32),
+            len(f), rng_seed, epoch, batch, lay3, int(device), reads)
+        _raise(rc, "build_minibatch")
+        return reads
 
     def epoch_minibatches(self, gt_off, gt_tgt, tid, fanouts, batch_size, rng_seed, epoch,
                           max_batches=0):

@@ -461,9 +461,50 @@ static u64 sort_unique(u64* a, u64 n) {
 /* sampling.cpp:56-90 build_minibatch over the transposed graph (gt) with
  * sampling.cpp:39-54 sample_in_neighbors. Returns a malloc'ed sorted unique id
  * list and its length; 2 on a bad argument (:59-62, sampling.cpp:18-25). */
+/* Graph-structure tiering: the neighbour ids a sampler
+ * reads per tier when row v of gt lives where resolve(v) puts it
+ * (tiering.cpp:48-65; lay = {lb, mb, D}): min(deg(v), fanout) ids per
+ * frontier node, counted local (v < lb, or interleaved on `dev`), peer or
+ * host (v >= mb). Not in the reference (it only sizes pseudo-rows,
+ * tiergraph_cli.cpp:389-406); the GPU sampler's counters are checked
+ * against it. */
+static void count_tier_reads(u64 v, u64 c, const u64* lay, uint32_t dev, u64* reads) {
+  if (!reads) return;
+  int t = 2;
+  if (v < lay[0]) t = 0;
+  else if (v < lay[1]) t = ((v - lay[0]) % lay[2]) == dev ? 0 : 1;
+  reads[t] += c;
+}
+
+static int build_minibatch_impl(const u64* gt_off, const u64* gt_tgt, u64 n, const u64* seeds,
+                                u64 nseeds, const uint32_t* fanouts, uint32_t nf, u64 rng_seed,
+                                u64 epoch, u64 batch, u64** out, u64* out_n, const u64* lay,
+                                uint32_t dev, u64* reads);
+
 int tgo_build_minibatch(const u64* gt_off, const u64* gt_tgt, u64 n, const u64* seeds,
                         u64 nseeds, const uint32_t* fanouts, uint32_t nf, u64 rng_seed,
                         u64 epoch, u64 batch, u64** out, u64* out_n) {
+  return build_minibatch_impl(gt_off, gt_tgt, n, seeds, nseeds, fanouts, nf, rng_seed, epoch,
+                              batch, out, out_n, NULL, 0, NULL);
+}
+
+int tgo_build_minibatch_tier_reads(const u64* gt_off, const u64* gt_tgt, u64 n, const u64* seeds,
+                                   u64 nseeds, const uint32_t* fanouts, uint32_t nf,
+                                   u64 rng_seed, u64 epoch, u64 batch, const u64* lay,
+                                   uint32_t dev, u64* reads) {
+  u64* m = NULL;
+  u64 nm = 0;
+  reads[0] = reads[1] = reads[2] = 0;
+  const int rc = build_minibatch_impl(gt_off, gt_tgt, n, seeds, nseeds, fanouts, nf, rng_seed,
+                                      epoch, batch, &m, &nm, lay, dev, reads);
+  free(m);
+  return rc;
+}
+
+static int build_minibatch_impl(const u64* gt_off, const u64* gt_tgt, u64 n, const u64* seeds,
+                                u64 nseeds, const uint32_t* fanouts, uint32_t nf, u64 rng_seed,
+                                u64 epoch, u64 batch, u64** out, u64* out_n, const u64* lay,
+                                uint32_t dev, u64* reads) {
   if (nf == 0 || nf > 5) return 2;
   for (uint32_t i = 0; i < nf; ++i)
     if (fanouts[i] < 1) return 2;
@@ -486,6 +527,7 @@ int tgo_build_minibatch(const u64* gt_off, const u64* gt_tgt, u64 n, const u64* 
     for (u64 i = 0; i < nfr; ++i) {
       const u64 v = frontier[i];
       const u64 b = gt_off[v], deg = gt_off[v + 1] - b;
+      count_tier_reads(v, deg < fanouts[layer] ? deg : fanouts[layer], lay, dev, reads);
       if (deg <= fanouts[layer]) {
         for (u64 k = 0; k < deg; ++k) next[nn++] = gt_tgt[b + k];
       } else {

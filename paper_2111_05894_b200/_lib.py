@@ -153,6 +153,15 @@ SIGNATURES = {
     "tg_mgraph_pagerank": (I32, [vp, U32, D, vp, U64, I32, vp]),
     "tg_pagerank_relabel_info": (I32, [vp, vp, C.POINTER(I32), C.POINTER(D)]),
     "tg_sampler_create": (I32, [vp, vp, C.POINTER(vp)]),
+    "tg_sgraph_cold_bytes": (U64, [vp, U64, PL]),
+    "tg_sgraph_create": (I32, [vp, PL, U32, vp, vp, U64, U64, vp, U64, I32, C.POINTER(vp)]),
+    "tg_sgraph_destroy": (I32, [vp]),
+    "tg_sgraph_local_base": (vp, [vp]),
+    "tg_sgraph_set_peer": (I32, [vp, U32, vp]),
+    "tg_sgraph_cold_host": (vp, [vp]),
+    "tg_sgraph_info": (I32, [vp, vp]),
+    "tg_sampler_create_tiered": (I32, [vp, vp, C.POINTER(vp)]),
+    "tg_sampler_structure_reads": (I32, [vp, vp, I32]),
     "tg_sampler_destroy": (I32, [vp]),
     "tg_sample_minibatch": (I32, [vp, vp, U64, vp, U32, U64, U64, U64, vp, U64, C.POINTER(U64)]),
     "tg_epoch_order": (I32, [vp, U64, U64, U64, vp]),

@@ -28,6 +28,7 @@
 #include <vector>
 
 #include "internal.cuh"
+#include "structure_internal.cuh"
 
 namespace tgb {
 
@@ -57,8 +58,7 @@ struct DevRng {  // rng.hpp:32-59
 };
 
 struct SampleArgs {
-  const uint32_t* off;  // transposed graph (row v = in-neighbours of v)
-  const uint32_t* tgt;
+  SGraphView g;  // transposed graph (row v = in-neighbours of v), tiered or not
   const uint32_t* frontier;
   const uint32_t* f_dev;  // frontier size, written by the previous launch (no host round trip)
   uint32_t fanout;
@@ -171,20 +171,29 @@ __device__ __forceinline__ void admit_batch(const SampleArgs& a, const uint32_t 
 constexpr uint32_t kRegK = 16;
 __global__ void __launch_bounds__(256) sample_layer_kernel(const SampleArgs a) {
   const uint32_t f = *a.f_dev;  // written by the previous launch: no host round trip
+  uint32_t rd0 = 0, rd1 = 0, rd2 = 0;  // neighbour ids read per tier (local, peer, host)
   for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < f; i += gridDim.x * blockDim.x) {
     const uint32_t v = a.frontier[i];
-    const uint32_t b = a.off[v], deg = a.off[v + 1] - b;
+    const uint32_t b = a.g.off[v], deg = a.g.off[v + 1] - b;
+    int tier;
+    const uint32_t* nb = a.g.row(v, b, &tier);  // row v's neighbour ids, in its tier
+    {
+      const uint32_t c = deg < a.fanout ? deg : a.fanout;  // ids this node reads
+      rd0 += tier == 0 ? c : 0u;
+      rd1 += tier == 1 ? c : 0u;
+      rd2 += tier == 2 ? c : 0u;
+    }
     if (deg <= a.fanout) {  // all in-neighbours
       uint32_t p = 0;
       for (; p + kRegK <= deg; p += kRegK) {
         uint32_t u[kRegK];
 #pragma unroll
-        for (uint32_t q = 0; q < kRegK; ++q) u[q] = a.tgt[b + p + q];
+        for (uint32_t q = 0; q < kRegK; ++q) u[q] = nb[p + q];
         admit_batch<kRegK>(a, u, kRegK);
       }
       uint32_t u[kRegK];
 #pragma unroll
-      for (uint32_t q = 0; q < kRegK; ++q) u[q] = p + q < deg ? a.tgt[b + p + q] : 0u;
+      for (uint32_t q = 0; q < kRegK; ++q) u[q] = p + q < deg ? nb[p + q] : 0u;
       admit_batch<kRegK>(a, u, deg - p);
       continue;
     }
@@ -204,7 +213,7 @@ __global__ void __launch_bounds__(256) sample_layer_kernel(const SampleArgs a) {
       }
       uint32_t u[kRegK];
 #pragma unroll
-      for (uint32_t q = 0; q < kRegK; ++q) u[q] = q < a.fanout ? a.tgt[b + pk[q]] : 0u;
+      for (uint32_t q = 0; q < kRegK; ++q) u[q] = q < a.fanout ? nb[pk[q]] : 0u;
       admit_batch<kRegK>(a, u, a.fanout);  // draw order, as the reference emits them
       continue;
     }
@@ -216,8 +225,16 @@ __global__ void __launch_bounds__(256) sample_layer_kernel(const SampleArgs a) {
       for (uint32_t q = 0; q < cnt; ++q) seen |= picks[q] == t;
       const uint32_t p = seen ? static_cast<uint32_t>(j) : t;
       picks[cnt++] = p;
-      admit(a, a.tgt[b + p]);
+      admit(a, nb[p]);
     }
+  }
+  if (a.g.reads) {  // every lane is here (blocks are whole warps)
+    const uint32_t r[3] = {__reduce_add_sync(0xffffffffu, rd0), __reduce_add_sync(0xffffffffu, rd1),
+                           __reduce_add_sync(0xffffffffu, rd2)};
+    if ((threadIdx.x & 31) == 0)
+#pragma unroll
+      for (int t = 0; t < 3; ++t)
+        if (r[t]) atomicAdd(a.g.reads + t, (unsigned long long)r[t]);
   }
 }
 
@@ -346,8 +363,9 @@ using namespace tgb;
 
 struct tg_sampler {
   tg_ctx* ctx = nullptr;
-  const uint32_t* off = nullptr;
-  const uint32_t* tgt = nullptr;
+  SGraphView g;  // the graph the sampler reads (a plain device graph, or a tiered one)
+  const tg_sgraph* sg = nullptr;          // the tiered graph, when there is one
+  unsigned long long* reads = nullptr;    // device: ids read per tier (shared by the lanes)
   uint64_t n = 0;
   uint32_t* layer_mark = nullptr;   // n
   uint32_t* member_bits = nullptr;  // ceil(n / 32)
@@ -421,8 +439,10 @@ int tg_sampler_create(tg_ctx* ctx, const tg_graph* gt, tg_sampler** out) {
     s->ctx = ctx;
     s->stream = ctx->stream;
     s->n = tg_graph_num_nodes(gt);
-    s->off = tg_graph_offsets32(gt);
-    s->tgt = tg_graph_targets32(gt);
+    // an untiered graph: every row "replicated" in this device's HBM
+    s->g.off = tg_graph_offsets32(gt);
+    s->g.rep = tg_graph_targets32(gt);
+    s->g.lb = s->g.mb = s->g.n = static_cast<uint32_t>(s->n);
     try {
       sampler_alloc(s);
     } catch (...) {
@@ -430,6 +450,42 @@ int tg_sampler_create(tg_ctx* ctx, const tg_graph* gt, tg_sampler** out) {
       throw;
     }
     *out = s;
+  });
+}
+
+int tg_sampler_create_tiered(tg_ctx* ctx, const tg_sgraph* sg, tg_sampler** out) {
+  return guard([&] {
+    if (!ctx || !sg || !out) domain_error("tg_sampler_create_tiered: null argument");
+    if (sg->ctx->device != ctx->device)
+      domain_error("tg_sampler_create_tiered: the tiered graph lives on another device");
+    DeviceGuard dg(ctx->device);
+    auto* s = new tg_sampler;
+    s->ctx = ctx;
+    s->stream = ctx->stream;
+    s->n = sg->n;
+    s->sg = sg;
+    try {
+      TGB_CUDA(cudaMalloc(&s->reads, 3 * sizeof(unsigned long long)));
+      TGB_CUDA(cudaMemsetAsync(s->reads, 0, 3 * sizeof(unsigned long long), s->stream));
+      s->g = sg->view();
+      s->g.reads = s->reads;
+      sampler_alloc(s);
+    } catch (...) {
+      tg_sampler_destroy(s);
+      throw;
+    }
+    *out = s;
+  });
+}
+
+int tg_sampler_structure_reads(tg_sampler* s, uint64_t* out, int reset) {
+  return guard([&] {
+    if (!s || !out) domain_error("tg_sampler_structure_reads: null argument");
+    if (!s->reads) domain_error("tg_sampler_structure_reads: the sampler's graph is not tiered");
+    DeviceGuard dg(s->ctx->device);
+    TGB_CUDA(cudaMemcpyAsync(out, s->reads, 3 * 8, cudaMemcpyDeviceToHost, s->stream));
+    if (reset) TGB_CUDA(cudaMemsetAsync(s->reads, 0, 3 * 8, s->stream));
+    TGB_CUDA(cudaStreamSynchronize(s->stream));
   });
 }
 
@@ -447,6 +503,7 @@ int tg_sampler_destroy(tg_sampler* s) {
   cudaFree(s->picks);
   cudaFree(s->small);
   cudaFree(s->blk);
+  if (!s->is_lane) cudaFree(s->reads);
   delete s;
   return TG_OK;
 }
@@ -493,6 +550,10 @@ uint64_t expand(tg_sampler* s, const uint64_t* sd, uint64_t ns, const uint32_t* 
   if (ns == 0) domain_error("build_minibatch: seeds must be non-empty");
   tg_ctx* ctx = s->ctx;
   const uint64_t n = s->n;
+  if (s->sg) {  // peers may have been attached since the sampler was made
+    s->g = s->sg->view();
+    s->g.reads = s->reads;
+  }
   uint64_t cap0 = s->buf_cap;
   ensure(&s->buf[0], &cap0, n + 1);
   uint64_t cap1 = s->buf_cap;
@@ -530,7 +591,7 @@ uint64_t expand(tg_sampler* s, const uint64_t* sd, uint64_t ns, const uint32_t* 
     }
     ensure(&s->picks, &s->picks_cap, std::max<uint64_t>(f * k, 1));
     lstamp = next_stamp(s);
-    SampleArgs a{s->off, s->tgt, s->buf[cur], cnt + layer, k, key, s->picks, s->layer_mark, lstamp,
+    SampleArgs a{s->g, s->buf[cur], cnt + layer, k, key, s->picks, s->layer_mark, lstamp,
                  s->member_bits, s->buf[cur ^ 1], cnt + layer + 1, o.counts, o.count_raw, o.raw,
                  raw_n, o.raw_cap};
     sample_layer_kernel<<<grid_for(f, 256, ctx->num_sms * 16), 256, 0, s->stream>>>(a);
@@ -680,8 +741,9 @@ int tg_sample_batches(tg_sampler* s, const uint64_t* order, uint64_t n_order, ui
       auto* l = new tg_sampler;
       l->ctx = ctx;
       l->n = s->n;
-      l->off = s->off;
-      l->tgt = s->tgt;
+      l->g = s->g;
+      l->sg = s->sg;
+      l->reads = s->reads;
       l->is_lane = true;
       s->lanes.push_back(l);
       TGB_CUDA(cudaStreamCreateWithFlags(&l->stream, cudaStreamNonBlocking));

@@ -86,18 +86,91 @@ def epoch_order(tid, seed: int, epoch: int) -> np.ndarray:
     return out[:len(ids)]
 
 
+class TieredGraph:
+    """Graph-structure tiering: the
+    TRANSPOSED, score-reordered graph placed by `layout` for device
+    `device_index` (csrc/structure.cu): rows [0, lb) and this device's
+    interleaved slice of [lb, mb) in HBM, rows [mb, N) in pinned host memory
+    (own, or `cold` = a mapped caller buffer / SharedHostSegment written by
+    this graph when fill=True). Peers: set_peer(d, other.local_base) in one
+    process, or the CUDA-IPC mapping of another process's local_base."""
+
+    def __init__(self, offsets, targets, layout, device_index: int = 0, ctx=None, cold=None,
+                 fill: bool = True):
+        from . import tiergraph as tg
+        self.tg = tg
+        self.ctx = ctx or tg.default_context()
+        off, tgt = tg._u64(offsets), tg._u64(targets)
+        self.n = len(off) - 1
+        self.e = len(tgt)
+        self.layout = layout
+        lay = layout._c() if hasattr(layout, "_c") else layout
+        cptr, cbytes = None, 0
+        if cold is not None:
+            arr = cold.array if hasattr(cold, "array") else cold
+            cptr, cbytes = tg._ptr(arr), int(arr.nbytes)
+        h = C.c_void_p()
+        tg._check(LIB.tg_sgraph_create(self.ctx.h, C.byref(lay), int(device_index), tg._ptr(off),
+                                       tg._nonempty(tgt, np.uint64), self.n, self.e, cptr, cbytes,
+                                       int(bool(fill)), C.byref(h)))
+        self.h = h
+        self.device_index = int(device_index)
+
+    @staticmethod
+    def cold_bytes(offsets, layout) -> int:
+        from . import tiergraph as tg
+        off = tg._u64(offsets)
+        lay = layout._c() if hasattr(layout, "_c") else layout
+        return int(LIB.tg_sgraph_cold_bytes(tg._ptr(off), len(off) - 1, C.byref(lay)))
+
+    @property
+    def local_base(self) -> int:
+        return LIB.tg_sgraph_local_base(self.h) or 0
+
+    @property
+    def cold_host(self) -> int:
+        return LIB.tg_sgraph_cold_host(self.h) or 0
+
+    def set_peer(self, d: int, base: int) -> None:
+        self.tg._check(LIB.tg_sgraph_set_peer(self.h, int(d), C.c_void_p(base)))
+
+    def info(self) -> dict:
+        out = np.zeros(4, np.uint64)
+        self.tg._check(LIB.tg_sgraph_info(self.h, out.ctypes.data))
+        return {"replicated_bytes": int(out[0]), "slice_bytes": int(out[1]),
+                "host_bytes": int(out[2]), "offsets_bytes": int(out[3])}
+
+    def close(self):
+        if getattr(self, "h", None):
+            LIB.tg_sgraph_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
 class GpuSampler:
     """build_minibatch (sampling.cpp:56-90) on the GPU, bit-identical member
     lists (csrc/sampling.cu). `gt` is the TRANSPOSED graph (producers.transpose)."""
 
-    def __init__(self, gt: CsrGraph, ctx=None):
+    def __init__(self, gt, ctx=None):
+        """gt: a CsrGraph (the whole transposed graph on this device) or a
+        TieredGraph (its rows placed by a TierLayout)."""
         from . import tiergraph as tg
         self.tg = tg
-        self.ctx = ctx or tg.default_context()
         self.gt = gt
-        self.n = gt.num_nodes()
         h = C.c_void_p()
-        tg._check(LIB.tg_sampler_create(self.ctx.h, gt.device(self.ctx), C.byref(h)))
+        if isinstance(gt, TieredGraph):
+            self.ctx = ctx or gt.ctx
+            self.n = gt.n
+            tg._check(LIB.tg_sampler_create_tiered(self.ctx.h, gt.h, C.byref(h)))
+        else:
+            self.ctx = ctx or tg.default_context()
+            self.n = gt.num_nodes()
+            tg._check(LIB.tg_sampler_create(self.ctx.h, gt.device(self.ctx), C.byref(h)))
         self.h = h
         self._pinned = None  # reusable pinned output (members of one minibatch)
 
@@ -205,6 +278,13 @@ class GpuSampler:
                                        int(batch_size), int(epochs), int(seed),
                                        int(bool(dedup_per_batch)), tg._ptr(dst)))
         return dst if out is not None else dst[:self.n]
+
+    def structure_reads(self, reset: bool = False) -> np.ndarray:
+        """Neighbour ids read per tier {local HBM, peer HBM, host} since the
+        last reset (a sampler over a TieredGraph only)."""
+        out = np.zeros(3, np.uint64)
+        self.tg._check(LIB.tg_sampler_structure_reads(self.h, out.ctypes.data, int(reset)))
+        return out
 
     def close(self):
         if getattr(self, "h", None):
