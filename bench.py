@@ -770,6 +770,22 @@ def run_ours(args):
             cts.append((a, b))
         torch.cuda.synchronize()
         cold_floor = statistics.mean(a.elapsed_time(b) for a, b in cts) * 1e3
+    # the platform's own ceiling for that cold part: the same number of random
+    # rows of the same cold tier by a plain copy kernel (host-memory path:
+    # translation of the mapped region + PCIe), and the mixed roofline with
+    # it in place of the link peak
+    platform = None
+    if cold_rows and not cfg.get("cold_mode") == "indirect":
+        plat_us = store.measure_cold_rows_us(cold_rows, 10)
+        t_plat = max(t_hbm, t_nvl, plat_us * 1e-6)
+        platform = {"cold_rows_copy_us": round(plat_us, 2), "t_star_us": round(t_plat * 1e6, 2),
+                    "frac": round(t_plat / t_launch, 4),
+                    "what": "t* with the host term = a plain one-warp-per-row copy of the same "
+                            "number of random rows of the same pinned cold tier (L2 flushed; "
+                            "tg_store_measure_cold_rows_us): what this box's host-memory path "
+                            "delivers for random rows (scripts/micro/cold_probe.cu: the cost "
+                            "follows distinct 4 KB pages, independent of host page size and "
+                            "copy engine, i.e. off-GPU translation)"}
     traffic = None
     tf = os.path.join(ROOT, "profiles", f"ncu_traffic_{args.config}.json")
     if os.path.exists(tf):
@@ -823,6 +839,7 @@ def run_ours(args):
                                                f"zero-copy row read {pcie_zc:.1f})",
                                    "nvlink_gbs": nvl_peak, "t_star_us": round(t_star * 1e6, 2),
                                    "t_launch_us": round(t_launch * 1e6, 2)},
+                         "platform": platform,
                          "cold_floor": None if cold_floor is None else {
                              "us": round(cold_floor, 2), "rows": cold_rows,
                              "frac": round(cold_floor / (t_launch * 1e6), 4),

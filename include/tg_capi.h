@@ -408,6 +408,10 @@ int tg_measure_host_read_gbps(tg_ctx* ctx, uint64_t bytes, uint64_t row_bytes, i
  * ids only, L2 flushed before each launch: the cold part of a gather timed
  * alone, on the same region, mapping and load path. */
 int tg_store_measure_cold_us(tg_store* s, uint64_t rows, int reps, double* us);
+/* The platform ceiling of the same: `rows` random rows of the store's cold
+ * tier (same region, stride, host bytes per row) by a plain one-warp-per-row
+ * copy kernel, L2 flushed; mean us per launch. */
+int tg_store_measure_cold_rows_us(tg_store* s, uint64_t rows, int reps, double* us);
 int tg_measure_host_rows_us(tg_ctx* ctx, const void* host, uint64_t region_rows, uint64_t stride,
                             uint64_t row_bytes, uint64_t rows, int reps, double* us);
 int tg_measure_hbm_copy_gbps(tg_ctx* ctx, uint64_t bytes, int reps, double* gbps);

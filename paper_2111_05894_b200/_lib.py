@@ -118,6 +118,7 @@ SIGNATURES = {
     "tg_ipc_close_handle": (I32, [vp]),
     "tg_measure_host_rows_us": (I32, [vp, vp, U64, U64, U64, U64, C.c_int, C.POINTER(C.c_double)]),
     "tg_store_measure_cold_us": (I32, [vp, U64, C.c_int, C.POINTER(C.c_double)]),
+    "tg_store_measure_cold_rows_us": (I32, [vp, U64, C.c_int, C.POINTER(C.c_double)]),
     "tg_mapped_device_ptr": (vp, [vp]),
     "tg_store_place_rows": (I32, [vp, vp, U64, vp]),
     "tg_time_gather_rows": (I32, [vp, vp, vp, U64, vp, C.c_int, vp, C.POINTER(C.c_double)]),

@@ -221,11 +221,14 @@ int tg_ctx_destroy(tg_ctx* c) {
   if (c->aux) {
     cudaStreamSynchronize(c->aux);
     cudaStreamSynchronize(c->aux2);
+    cudaStreamSynchronize(c->aux3);
     cudaStreamDestroy(c->aux);
     cudaStreamDestroy(c->aux2);
+    cudaStreamDestroy(c->aux3);
     cudaEventDestroy(c->ev_fork);
     cudaEventDestroy(c->ev_join);
     cudaEventDestroy(c->ev_join2);
+    cudaEventDestroy(c->ev_join3);
   }
   if (c->own_stream) cudaStreamDestroy(c->stream);
   delete c;

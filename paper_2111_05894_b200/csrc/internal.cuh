@@ -69,8 +69,8 @@ struct tg_ctx {
   size_t slot_size[tgb::kNumSlots] = {};
   void* pinned_small = nullptr;  // 4 KB mapped host scratch for small results
   // Fork-join side stream (concurrent kernels inside one stream-ordered call).
-  cudaStream_t aux = nullptr, aux2 = nullptr;
-  cudaEvent_t ev_fork = nullptr, ev_join = nullptr, ev_join2 = nullptr;
+  cudaStream_t aux = nullptr, aux2 = nullptr, aux3 = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr, ev_join2 = nullptr, ev_join3 = nullptr;
 
   // Work enqueued on `aux` between fork() and join() runs concurrently with
   // `stream` and is ordered after everything before fork() and before
@@ -83,19 +83,24 @@ struct tg_ctx {
       tgb::cuda_check(cudaDeviceGetStreamPriorityRange(&lo, &hi), "priority range");
       tgb::cuda_check(cudaStreamCreateWithPriority(&aux, cudaStreamNonBlocking, hi), "aux stream");
       tgb::cuda_check(cudaStreamCreateWithPriority(&aux2, cudaStreamNonBlocking, hi), "aux stream");
+      tgb::cuda_check(cudaStreamCreateWithPriority(&aux3, cudaStreamNonBlocking, lo), "aux stream");
       tgb::cuda_check(cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming), "event");
       tgb::cuda_check(cudaEventCreateWithFlags(&ev_join, cudaEventDisableTiming), "event");
       tgb::cuda_check(cudaEventCreateWithFlags(&ev_join2, cudaEventDisableTiming), "event");
+      tgb::cuda_check(cudaEventCreateWithFlags(&ev_join3, cudaEventDisableTiming), "event");
     }
     tgb::cuda_check(cudaEventRecord(ev_fork, stream), "fork record");
     tgb::cuda_check(cudaStreamWaitEvent(aux, ev_fork, 0), "fork wait");
     tgb::cuda_check(cudaStreamWaitEvent(aux2, ev_fork, 0), "fork wait");
+    tgb::cuda_check(cudaStreamWaitEvent(aux3, ev_fork, 0), "fork wait");
   }
   void join() {
     tgb::cuda_check(cudaEventRecord(ev_join, aux), "join record");
     tgb::cuda_check(cudaStreamWaitEvent(stream, ev_join, 0), "join wait");
     tgb::cuda_check(cudaEventRecord(ev_join2, aux2), "join record");
     tgb::cuda_check(cudaStreamWaitEvent(stream, ev_join2, 0), "join wait");
+    tgb::cuda_check(cudaEventRecord(ev_join3, aux3), "join record");
+    tgb::cuda_check(cudaStreamWaitEvent(stream, ev_join3, 0), "join wait");
   }
 
   // Grow-only scratch buffer bound to a slot. Stream-ordered reuse is safe

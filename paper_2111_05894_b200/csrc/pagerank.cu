@@ -788,6 +788,110 @@ __device__ __forceinline__ void warp_rows_staged(const PrStepArgs& a, uint64_t k
   if (has) finish_row(a, k0 + lane, acc);
 }
 
+// Class C on the relabelled twin, streamed (TIERGRAPH_PR_CSTREAM, default
+// on): one warp takes kCsRows consecutive rows (one contiguous edge range,
+// rows stored in length order) and streams it in kCsChunk-edge chunks with
+// the memory pipeline never drained: cp.async copies the targets three
+// chunks ahead (16 B, coalesced) and gathers the normalized values one chunk
+// ahead straight into shared memory (8 B cp.async, no registers held), while
+// the lanes add the current chunk. Row j of the warp belongs to lane j % 32,
+// which adds its part of every chunk the row spans in storage order
+// (scoring.cpp:66-68: the same left-to-right chain as thread_row), carrying
+// the accumulator across chunk boundaries.
+constexpr int kCsWarps = 4, kCsRows = 256, kCsChunk = 256;
+constexpr int kCsTRing = 3, kCsVRing = 2;
+struct CsWarpSmem {
+  uint32_t off[kCsRows + 4];
+  uint32_t t[kCsTRing][kCsChunk];
+  double v[kCsVRing][kCsChunk];
+};
+constexpr int kCsSmem = kCsWarps * static_cast<int>(sizeof(CsWarpSmem));
+
+__device__ __forceinline__ void cp_async16(void* sdst, const void* gsrc, uint32_t src_bytes) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(smem_u32(sdst)), "l"(gsrc),
+               "r"(src_bytes)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async8(void* sdst, const void* gsrc, uint32_t src_bytes) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(smem_u32(sdst)), "l"(gsrc),
+               "r"(src_bytes)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
+__global__ void __launch_bounds__(kCsWarps * 32) pr_cstream_kernel(const PrStepArgs a,
+                                                                   uint64_t c_begin) {
+  extern __shared__ __align__(16) uint8_t cs_smem[];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  CsWarpSmem& S = reinterpret_cast<CsWarpSmem*>(cs_smem)[w];
+  const uint64_t k0 = c_begin + ((uint64_t)blockIdx.x * kCsWarps + w) * kCsRows;
+  if (k0 >= a.row_end) return;
+  const uint32_t nrows = static_cast<uint32_t>((a.row_end - k0 < (uint64_t)kCsRows ? a.row_end - k0 : (uint64_t)kCsRows));
+  for (uint32_t j = lane; j <= nrows; j += 32) S.off[j] = a.off[k0 + j];
+  __syncwarp();
+  const uint32_t e0 = S.off[0], e1 = S.off[nrows];
+  const uint32_t A = e0 & ~3u;  // chunks on a 16 B grid of the target array
+  const uint32_t nch = (e1 - A + kCsChunk - 1) / kCsChunk;
+  auto load_t = [&](uint32_t c) {  // targets of chunk c: 64 x 16 B, 2 per lane
+    if (c < nch) {
+#pragma unroll
+      for (int q = 0; q < 2; ++q) {
+        const uint32_t i = q * 32 + lane;
+        const uint32_t pos = A + c * kCsChunk + 4 * i;
+        const uint32_t nb = pos < e1 ? min(16u, 4 * (e1 - pos)) : 0u;
+        cp_async16(&S.t[c % kCsTRing][4 * i], a.tgt + (nb ? pos : A), nb);
+      }
+    }
+    cp_async_commit();
+  };
+  auto gather = [&](uint32_t c) {  // normalized values of chunk c: 8 per lane
+    if (c < nch) {
+      const uint32_t* tt = S.t[c % kCsTRing];
+#pragma unroll
+      for (int q = 0; q < kCsChunk / 32; ++q) {
+        const uint32_t p = q * 32 + lane;
+        const uint32_t pos = A + c * kCsChunk + p;
+        const bool ok = pos >= e0 && pos < e1;
+        cp_async8(&S.v[c % kCsVRing][p], a.norm_in + (ok ? tt[p] : 0u), ok ? 8u : 0u);
+      }
+    }
+    cp_async_commit();
+  };
+  load_t(0);
+  load_t(1);
+  cp_async_wait<1>();  // T0
+  __syncwarp();
+  gather(0);
+  load_t(2);
+  uint32_t j = lane;
+  double acc = 0.0;  // scoring.cpp:67
+  for (uint32_t c = 0; c < nch; ++c) {
+    cp_async_wait<1>();  // everything but T(c+2): V(c) and T(c+1) have landed
+    __syncwarp();
+    gather(c + 1);
+    load_t(c + 3);  // into T(c)'s slot: T(c) was last read by gather(c)
+    const double* vv = S.v[c % kCsVRing];
+    const uint32_t cb = A + c * kCsChunk, ce = cb + kCsChunk;
+    while (j < nrows) {
+      const uint32_t rs = S.off[j], re = S.off[j + 1];
+      if (rs >= ce) break;  // starts after this chunk
+      const uint32_t lo = max(rs, cb), hi = min(re, ce);
+      for (uint32_t k = lo; k < hi; ++k) acc = __dadd_rn(acc, vv[k - cb]);  // in order
+      if (re > ce) break;  // continues in the next chunk
+      finish_row(a, k0 + j, acc);
+      acc = 0.0;
+      j += 32;
+    }
+    __syncwarp();  // V(c)'s slot is refilled by gather(c + 2)
+  }
+  cp_async_wait<0>();
+  for (; j < nrows; j += 32) finish_row(a, k0 + j, 0.0);  // empty rows at the very end
+}
+
 __global__ void __launch_bounds__(kPrWarps * 32) pr_step_kernel(const PrStepArgs a) {
   __shared__ __align__(16) double smem[kPrWarps * 32 / kBLanes * kBStride];  // 16.6 KB: class B windows
   if (blockIdx.x < a.b_ctas) {
@@ -963,7 +1067,25 @@ void pagerank_step(tg_ctx* ctx, const tg_graph* g, const uint32_t* deg, double d
     a.peer_norm[p] = p < n_peers ? peer_norm[p] : nullptr;
     a.peer_score[p] = p < n_peers ? peer_score[p] : nullptr;
   }
-  const uint64_t c_ctas = (a.m - sc.nB + kPrWarps * 32 - 1) / (kPrWarps * 32);
+  uint64_t c_ctas = (a.m - sc.nB + kPrWarps * 32 - 1) / (kPrWarps * 32);
+  // class C streamed on its own stream (relabelled twin: rows in storage order)
+  const char* csv = std::getenv("TIERGRAPH_PR_CSTREAM");
+  const bool cstream = !(csv && csv[0] == '0');
+  const bool cs = cstream && !sc.order && a.m > sc.nB;
+  if (cs) c_ctas = 0;
+  if (sc.nA || cs) ctx->fork();
+  if (cs) {
+    static bool cattr[TG_MAX_DEVICES] = {};
+    if (!cattr[ctx->device % TG_MAX_DEVICES]) {
+      TGB_CUDA(cudaFuncSetAttribute(pr_cstream_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    kCsSmem));
+      cattr[ctx->device % TG_MAX_DEVICES] = true;
+    }
+    const uint64_t warps = (a.m - sc.nB + kCsRows - 1) / kCsRows;
+    pr_cstream_kernel<<<static_cast<unsigned>((warps + kCsWarps - 1) / kCsWarps), kCsWarps * 32,
+                        kCsSmem, ctx->aux3>>>(a, rb + sc.nB);
+    TGB_LAUNCHED();
+  }
   if (sc.nA) {
     // class A on the side streams, concurrently with classes B and C: the
     // longest rows (> kHubLong) with 512-thread CTAs, the rest with 256
@@ -975,7 +1097,6 @@ void pagerank_step(tg_ctx* ctx, const tg_graph* g, const uint32_t* deg, double d
                                     cudaFuncAttributeMaxDynamicSharedMemorySize, 8 * 32 * 8 * 8));
       attr[ctx->device % TG_MAX_DEVICES] = true;
     }
-    ctx->fork();
     const uint32_t nl = sc.nLong;
     if (nl) {
       pr_hub_kernel<16, 8><<<nl, 16 * 32, 16 * 32 * 8 * 8, ctx->aux>>>(a, 0);
@@ -992,7 +1113,7 @@ void pagerank_step(tg_ctx* ctx, const tg_graph* g, const uint32_t* deg, double d
     pr_step_kernel<<<grid, kPrWarps * 32, 0, ctx->stream>>>(a);
     TGB_LAUNCHED();
   }
-  if (sc.nA) ctx->join();
+  if (sc.nA || cs) ctx->join();
 }
 
 // TIERGRAPH_PR_RELABEL: "0" never, "1" always, default: when the norm vector
@@ -1086,6 +1207,58 @@ void check_config(uint32_t iterations, double damp) {  // scoring.cpp:42-47
     domain_error("pagerank: damp must lie in (0,1), got " + std::to_string(damp));
 }
 
+// L2 residency of the hot norm values (C3/C4, where the vector exceeds L2):
+// on the relabelled twin the most-gathered nodes have the lowest labels, so
+// the first bytes of norm_in are the hottest. They are marked persisting for
+// every K3 launch of the run (an access-policy window on the three K3
+// streams) so the streamed targets (4 B per edge, read once) cannot evict
+// them; the lines are released when the run ends.
+// TIERGRAPH_PR_PERSIST_MB: window size in MB (0 = off); default: as large as
+// the device allows (cudaDevAttrMaxAccessPolicyWindowSize, persisting limit)
+// whenever the relabelled twin runs.
+struct L2Persist {
+  tg_ctx* ctx = nullptr;
+  size_t bytes = 0;
+  L2Persist(tg_ctx* c, bool twin, uint64_t n) : ctx(c) {
+    long want = -1;
+    if (const char* e = std::getenv("TIERGRAPH_PR_PERSIST_MB")) want = std::atol(e);
+    if (want == 0 || (want < 0 && !twin)) return;
+    int maxwin = 0, maxpers = 0;
+    cudaDeviceGetAttribute(&maxwin, cudaDevAttrMaxAccessPolicyWindowSize, ctx->device);
+    cudaDeviceGetAttribute(&maxpers, cudaDevAttrMaxPersistingL2CacheSize, ctx->device);
+    size_t b = std::min<size_t>(static_cast<size_t>(maxwin), static_cast<size_t>(maxpers));
+    if (want > 0) b = std::min<size_t>(b, static_cast<size_t>(want) << 20);
+    b = std::min<size_t>(b, 8 * n);
+    if (b == 0) return;
+    TGB_CUDA(cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, b));
+    if (!ctx->aux) {  // the side streams of K3's class A
+      ctx->fork();
+      ctx->join();
+    }
+    bytes = b;
+  }
+  void window(const void* base) {
+    if (!bytes) return;
+    cudaStreamAttrValue v{};
+    v.accessPolicyWindow.base_ptr = const_cast<void*>(base);
+    v.accessPolicyWindow.num_bytes = bytes;
+    v.accessPolicyWindow.hitRatio = 1.0f;
+    v.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+    v.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+    for (cudaStream_t s : {ctx->stream, ctx->aux, ctx->aux2, ctx->aux3})
+      TGB_CUDA(cudaStreamSetAttribute(s, cudaStreamAttributeAccessPolicyWindow, &v));
+  }
+  ~L2Persist() {
+    if (!bytes) return;
+    cudaStreamAttrValue v{};
+    v.accessPolicyWindow.num_bytes = 0;
+    for (cudaStream_t s : {ctx->stream, ctx->aux, ctx->aux2, ctx->aux3})
+      cudaStreamSetAttribute(s, cudaStreamAttributeAccessPolicyWindow, &v);
+    cudaCtxResetPersistingL2Cache();  // the run's end synchronised the stream (DevOut::finish)
+    cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, 0);
+  }
+};
+
 void run_pagerank(tg_ctx* ctx, const tg_graph* g, uint32_t iterations, double damp,
                   const uint64_t* tid, uint64_t ntid, bool weighted, double* out,
                   double* phase_ms = nullptr) {
@@ -1121,8 +1294,10 @@ void run_pagerank(tg_ctx* ctx, const tg_graph* g, uint32_t iterations, double da
   }
   pagerank_prepare(ctx, run, tid_dev, ntid, deg, na, bad, tw ? g->new_of : nullptr);
   if (phase_ms) TGB_CUDA(cudaEventRecord(ev[1], ctx->stream));
+  L2Persist persist(ctx, tw != nullptr, n);
   for (uint32_t it = 0; it < iterations; ++it) {
     const bool last = it + 1 == iterations;
+    persist.window(na);
     pagerank_step(ctx, run, deg, damp, na, nb, o.dev(), 0, n, last ? 1 : 0);
     if (phase_ms) TGB_CUDA(cudaEventRecord(ev[it + 2], ctx->stream));
     std::swap(na, nb);

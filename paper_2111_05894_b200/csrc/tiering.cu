@@ -1191,6 +1191,25 @@ int tg_store_measure_cold_us(tg_store* s, uint64_t rows, int reps, double* us) {
     *us = tot / std::max(reps, 1) * 1e3;
   });
 }
+// The platform's ceiling for the cold part of a launch: `rows` random rows of
+// the store's own cold tier (same region, stride and host bytes per row)
+// read by a plain one-warp-per-row copy kernel, L2 flushed before each
+// launch. Against K8's cold-only time this separates the kernel from the
+// host-memory path (translation of the mapped region, PCIe).
+int tg_store_measure_cold_rows_us(tg_store* s, uint64_t rows, int reps, double* us) {
+  return guard([&] {
+    if (!s || !us) domain_error("tg_store_measure_cold_rows_us: null argument");
+    if (!s->placed) domain_error("tiered store: tg_store_place has not run");
+    const uint64_t mb = s->L.multi_boundary, N = s->L.num_rows;
+    if (mb >= N) domain_error("tiered store: no cold rows");
+    if (s->flags & TG_COLD_INDIRECT) domain_error("tiered store: the cold tier is read in place");
+    DeviceGuard dg(s->ctx->device);
+    const tg_store* o = s->cold_owner ? s->cold_owner : s;
+    const uint64_t hc = s->cold_head ? s->cold_head : s->R;
+    *us = measure_rows_us(s->ctx, o->cold_dev, N - mb, s->cold_stride, hc, rows, reps);
+  });
+}
+
 uint64_t tg_store_local_rows(const tg_store* s) { return s ? s->local_rows : 0; }
 uint64_t tg_store_cold_host_bytes(const tg_store* s) {
   return s ? (s->cold_head ? s->cold_head : s->R) : 0;

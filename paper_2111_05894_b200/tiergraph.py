@@ -828,6 +828,13 @@ class TieredFeatureStore:
         _check(LIB.tg_store_measure_cold_us(self.h, int(rows), int(reps), C.byref(v)))
         return float(v.value)
 
+    def measure_cold_rows_us(self, rows: int, reps: int = 5) -> float:
+        """The platform ceiling of the same: a plain one-warp-per-row copy of
+        `rows` random rows of the cold tier (tg_store_measure_cold_rows_us)."""
+        v = C.c_double()
+        _check(LIB.tg_store_measure_cold_rows_us(self.h, int(rows), int(reps), C.byref(v)))
+        return float(v.value)
+
     def set_peer(self, device_index: int, peer_local_base: int):
         _check(LIB.tg_store_set_peer(self.h, int(device_index), C.c_void_p(peer_local_base)))
 

@@ -14,6 +14,8 @@
 #   ncu_k8:<cfg>   ncu (application replay) of K8 on the cached C3/C4 inputs
 #   ncu_k3:<cfg>   ncu --set full of K3 (pr_step) at <cfg>
 #   prlaunch:<cfg> per-launch time / DRAM / L2 of every K3 kernel (pr_*) at <cfg>
+#   k3probe:<cfg>  scripts/k3_probe.py <cfg> over the settings in $K3_SETTINGS (';'-separated)
+#   pytestf:<file> pytest -m gpu of one test file
 #   sanitize       compute-sanitizer memcheck/racecheck/synccheck on small cases
 #   shared2        2-process runs on one GPU (IPC gather, PageRank exchange)
 T=${1:?tag}; shift
@@ -59,6 +61,8 @@ for st in "$@"; do
     ncu_k3) timeout 2400 ncu --set full --clock-control none --import-source on -k regex:pr_step -s 2 -c 1 \
         -o $O/k3_$a python scripts/profile_target.py k3 --config $a --launches 1 > $O/ncu_k3_$a.log 2>&1 ;;
     sanitize) bash scripts/sanitize.sh $O ;;
+    k3probe) timeout 1500 python scripts/k3_probe.py $a > $O/k3probe_$a.log 2>&1 ;;
+    pytestf) timeout 2400 python -m pytest tests/$a -x -q -m gpu > $O/pytest_$a.log 2>&1; echo "rc=$?" >> $O/pytest_$a.log ;;
     shared2)
       TG_BENCH_SHARE_GPU=1 timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 \
         --master-addr 127.0.0.1 --master-port 29511 bench.py --gpus 2 --config ${a:-c1} --steps 20 --warmup 3 \

@@ -252,8 +252,8 @@ def test_in_degrees_large_graphs(tg, ctx, n, draws):
     assert np.array_equal(tg.in_degrees(g2, ctx=ctx), want2)
 
 
-@pytest.mark.parametrize("mode", ["1", "0"])
-def test_relabelled_twin_bit_exact(tg, ctx, monkeypatch, mode):
+@pytest.mark.parametrize("mode,cstream", [("1", "1"), ("1", "0"), ("0", "1")])
+def test_relabelled_twin_bit_exact(tg, ctx, monkeypatch, mode, cstream):
     """K3 on the twin renumbered by in-degree (TIERGRAPH_PR_RELABEL=1, the
     default at C3/C4 sizes) and without it (=0): raw-byte equal to the
     reference on random, hub-row, tie-prone and R-MAT graphs, weighted and
@@ -262,6 +262,7 @@ def test_relabelled_twin_bit_exact(tg, ctx, monkeypatch, mode):
     from paper_2111_05894_b200._lib import LIB
     from paper_2111_05894_b200 import synth
     monkeypatch.setenv("TIERGRAPH_PR_RELABEL", mode)
+    monkeypatch.setenv("TIERGRAPH_PR_CSTREAM", cstream)  # streamed class C (twin only)
     chk, port = checker(), oracle.port()
     cases = [random_graph(port, 300 + 97 * i, 1.5 + i, 40 + i) for i in range(4)]
     cases.append(_hub_graph(60000, [(0, 40000), (31, 2049), (1000, 20000), (59999, 3000)], 3))
