@@ -1,0 +1,306 @@
+// K1, binned: in_degrees (proj/src/csr_graph.cpp:89-93 — deg[t]++ for every
+// stored target t) as a partition followed by shared-memory histograms.
+//
+// Why not one atomic per edge: an L2 atomic costs a slice cycle whatever the
+// counter array's size, and on this part the L2 retires ~95 G RED/s (K1 ran
+// at 97 G/s at C3, 444 MB of counters, and 93 G/s at C2, 9.8 MB of counters:
+// the same rate), 15.8 ms for papers100M's 1.53 G targets. Shared-memory
+// atomics retire an order of magnitude faster, but 111 M counters do not fit
+// one SM. So:
+//   1. count   per-chunk counts of the BUCKET b = t >> 15 (32,768 ids per
+//              bucket; <= 8,192 buckets), one CTA per chunk of the target
+//              array, shared-memory histogram;
+//   2. scan    bucket-major exclusive scan of the (bucket, chunk) counts: the
+//              chunk's write cursor inside each bucket's segment of a
+//              temporary copy of the targets;
+//   3. scatter every CTA re-reads its chunk tile by tile, orders each tile
+//              by bucket in shared memory and writes it out in bucket runs
+//              (coalesced; the <= 8,192 open run ends stay in L2, so DRAM
+//              sees full sectors);
+//   4. count   one CTA per (bucket, <= 1 M element piece), persistent: a
+//              32,768-bin shared-memory histogram of the piece, flushed with
+//              plain coalesced stores when the bucket is one piece, with
+//              atomics when a hub bucket is split over several.
+// Traffic: 4 B x E read (1), 8 B x E (3), 4 B x E (4), 4 B x N written —
+// 16 B per edge against the 4 B per edge of the one-pass form, in exchange
+// for shared-memory instead of L2 atomics. The counts are exact integers
+// whatever the order (no summation-order question).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdlib>
+#include <cstring>
+
+#include "internal.cuh"
+
+namespace tgb {
+
+constexpr int kK1Shift = 15;
+constexpr uint32_t kK1Bins = 1u << kK1Shift;    // ids per bucket (128 KB of counters)
+constexpr uint32_t kK1MaxBuckets = 8192;        // n <= 2^28
+constexpr int kK1Threads = 512, kK1Ipt = 16;
+constexpr uint32_t kK1Tile = kK1Threads * kK1Ipt;  // 8,192 targets per scatter tile
+constexpr uint32_t kK1Piece = 1u << 20;         // elements per histogram work item
+constexpr int kK1HistThreads = 1024;
+
+// (1) per-chunk bucket counts, bucket-major: cnt[b * G + c]
+__global__ void __launch_bounds__(kK1Threads) k1_count_kernel(const uint32_t* __restrict__ tgt,
+                                                              uint64_t e, uint64_t chunk,
+                                                              uint32_t nb, uint32_t G,
+                                                              uint64_t* __restrict__ cnt) {
+  extern __shared__ uint32_t h[];  // nb
+  for (uint32_t i = threadIdx.x; i < nb; i += blockDim.x) h[i] = 0;
+  __syncthreads();
+  const uint64_t c0 = blockIdx.x * chunk, c1 = min(e, c0 + chunk);  // c0 % 4 == 0
+  const uint64_t v1 = c0 + ((c1 - c0) & ~3ull);
+  for (uint64_t i = c0 + 4 * (uint64_t)threadIdx.x; i < v1; i += 4 * (uint64_t)blockDim.x) {
+    const uint4 v = __ldcs(reinterpret_cast<const uint4*>(tgt + i));
+    atomicAdd(&h[v.x >> kK1Shift], 1u);
+    atomicAdd(&h[v.y >> kK1Shift], 1u);
+    atomicAdd(&h[v.z >> kK1Shift], 1u);
+    atomicAdd(&h[v.w >> kK1Shift], 1u);
+  }
+  for (uint64_t i = v1 + threadIdx.x; i < c1; i += blockDim.x) atomicAdd(&h[tgt[i] >> kK1Shift], 1u);
+  __syncthreads();
+  for (uint32_t b = threadIdx.x; b < nb; b += blockDim.x) cnt[(uint64_t)b * G + blockIdx.x] = h[b];
+}
+
+// Block-wide exclusive scan of the nb counters in `c` into `s` (512 threads).
+__device__ __forceinline__ void k1_block_scan(const uint32_t* c, uint32_t* s, uint32_t nb,
+                                              uint32_t* wsum) {
+  const uint32_t per = (nb + kK1Threads - 1) / kK1Threads;
+  const uint32_t b0 = min(nb, threadIdx.x * per), b1 = min(nb, b0 + per);
+  uint32_t run = 0;
+  for (uint32_t b = b0; b < b1; ++b) run += c[b];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  uint32_t incl = run;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += y;
+  }
+  if (lane == 31) wsum[w] = incl;
+  __syncthreads();
+  uint32_t before = 0;
+  for (int k = 0; k < w; ++k) before += wsum[k];
+  uint32_t x = before + incl - run;
+  for (uint32_t b = b0; b < b1; ++b) {
+    s[b] = x;
+    x += c[b];
+  }
+}
+
+// (3) scatter: chunk blockIdx.x, tile by tile, bucket-ordered in shared memory
+__global__ void __launch_bounds__(kK1Threads) k1_scatter_kernel(const uint32_t* __restrict__ tgt,
+                                                                uint64_t e, uint64_t chunk,
+                                                                uint32_t nb, uint32_t G,
+                                                                const uint64_t* __restrict__ cnt,
+                                                                uint32_t* __restrict__ out) {
+  extern __shared__ __align__(16) uint32_t sm[];
+  uint32_t* st = sm;                 // kK1Tile staged targets
+  uint32_t* tcnt = st + kK1Tile;     // nb: this tile's count per bucket
+  uint32_t* tst = tcnt + nb;         // nb: this tile's bucket starts in st
+  uint32_t* cur = tst + nb;          // nb: this chunk's write cursor per bucket
+  __shared__ uint32_t wsum[kK1Threads / 32];
+  for (uint32_t b = threadIdx.x; b < nb; b += blockDim.x)
+    cur[b] = static_cast<uint32_t>(cnt[(uint64_t)b * G + blockIdx.x]);
+  const uint64_t c0 = blockIdx.x * chunk, c1 = min(e, c0 + chunk);
+  for (uint64_t t0 = c0; t0 < c1; t0 += kK1Tile) {
+    const uint32_t tn = static_cast<uint32_t>((c1 - t0 < kK1Tile ? c1 - t0 : (uint64_t)kK1Tile));
+    for (uint32_t b = threadIdx.x; b < nb; b += blockDim.x) tcnt[b] = 0;
+    __syncthreads();
+    uint32_t v[kK1Ipt], r[kK1Ipt];
+    if (tn == kK1Tile) {
+#pragma unroll
+      for (int k = 0; k < kK1Ipt / 4; ++k) {
+        const uint4 q = __ldcs(reinterpret_cast<const uint4*>(tgt + t0) + k * kK1Threads + threadIdx.x);
+        v[4 * k] = q.x;
+        v[4 * k + 1] = q.y;
+        v[4 * k + 2] = q.z;
+        v[4 * k + 3] = q.w;
+      }
+    } else {
+#pragma unroll
+      for (int k = 0; k < kK1Ipt; ++k) {
+        const uint32_t j = (k >> 2) * (4 * kK1Threads) + 4 * threadIdx.x + (k & 3);
+        v[k] = j < tn ? tgt[t0 + j] : 0xffffffffu;
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < kK1Ipt; ++k)  // ids < 2^28: 0xffffffff only marks a partial tile's end
+      if (v[k] != 0xffffffffu) r[k] = atomicAdd(&tcnt[v[k] >> kK1Shift], 1u);
+    __syncthreads();
+    k1_block_scan(tcnt, tst, nb, wsum);
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < kK1Ipt; ++k)
+      if (v[k] != 0xffffffffu) st[tst[v[k] >> kK1Shift] + r[k]] = v[k];
+    __syncthreads();
+    for (uint32_t j = threadIdx.x; j < tn; j += blockDim.x) {
+      const uint32_t t = st[j], b = t >> kK1Shift;
+      out[cur[b] + (j - tst[b])] = t;
+    }
+    __syncthreads();
+    for (uint32_t b = threadIdx.x; b < nb; b += blockDim.x) cur[b] += tcnt[b];
+  }
+}
+
+struct K1Item {
+  uint32_t bucket, begin, end, split;
+};
+
+// Work items: bucket b's segment [cnt[b*G], cnt[(b+1)*G]) cut into pieces of
+// at most kK1Piece elements. One CTA of 1024 threads.
+__global__ void __launch_bounds__(1024) k1_items_kernel(const uint64_t* __restrict__ cnt,
+                                                        uint32_t nb, uint32_t G,
+                                                        K1Item* __restrict__ items,
+                                                        uint32_t* __restrict__ nitems) {
+  __shared__ uint32_t wsum[32];
+  __shared__ uint32_t base_s;
+  if (threadIdx.x == 0) base_s = 0;
+  __syncthreads();
+  for (uint32_t b0 = 0; b0 < nb; b0 += blockDim.x) {
+    const uint32_t b = b0 + threadIdx.x;
+    uint64_t beg = 0, end = 0;
+    uint32_t np = 0;
+    if (b < nb) {
+      beg = cnt[(uint64_t)b * G];
+      end = cnt[(uint64_t)(b + 1) * G];
+      np = end > beg ? static_cast<uint32_t>((end - beg + kK1Piece - 1) / kK1Piece) : 1u;
+    }
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    uint32_t incl = np;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += y;
+    }
+    if (lane == 31) wsum[w] = incl;
+    __syncthreads();
+    uint32_t before = base_s;
+    for (int k = 0; k < w; ++k) before += wsum[k];
+    const uint32_t first = before + incl - np;
+    for (uint32_t p = 0; p < np; ++p) {
+      const uint64_t pb = beg + (uint64_t)p * kK1Piece;
+      items[first + p] = K1Item{b, static_cast<uint32_t>(pb),
+                                static_cast<uint32_t>(end < pb + kK1Piece ? end : pb + kK1Piece),
+                                np > 1 ? 1u : 0u};
+    }
+    __syncthreads();
+    if (threadIdx.x == blockDim.x - 1) base_s = first + np;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) *nitems = base_s;
+}
+
+// (4) persistent: claim a piece, histogram it into 32,768 shared counters, flush.
+__global__ void __launch_bounds__(kK1HistThreads) k1_hist_kernel(const uint32_t* __restrict__ part,
+                                                                 const K1Item* __restrict__ items,
+                                                                 const uint32_t* __restrict__ nitems,
+                                                                 uint32_t* __restrict__ ctr,
+                                                                 uint64_t n,
+                                                                 uint32_t* __restrict__ deg) {
+  extern __shared__ __align__(16) uint32_t hb[];  // kK1Bins
+  __shared__ uint32_t item_s;
+  const uint32_t ni = *nitems;
+  for (;;) {
+    if (threadIdx.x == 0) item_s = atomicAdd(ctr, 1u);
+    for (uint32_t i = threadIdx.x; i < kK1Bins; i += blockDim.x) hb[i] = 0;
+    __syncthreads();
+    const uint32_t it = item_s;
+    if (it >= ni) break;
+    const K1Item m = items[it];
+    // head to a 16 B boundary, uint4 body, tail
+    const uint32_t hb_end = min(m.end, (m.begin + 3u) & ~3u);
+    for (uint32_t i = m.begin + threadIdx.x; i < hb_end; i += blockDim.x)
+      atomicAdd(&hb[part[i] & (kK1Bins - 1)], 1u);
+    const uint32_t vb = hb_end, ve = vb + ((m.end - vb) & ~3u);
+    for (uint32_t i = vb + 4 * threadIdx.x; i < ve; i += 4 * blockDim.x) {
+      const uint4 v = __ldcs(reinterpret_cast<const uint4*>(part + i));
+      atomicAdd(&hb[v.x & (kK1Bins - 1)], 1u);
+      atomicAdd(&hb[v.y & (kK1Bins - 1)], 1u);
+      atomicAdd(&hb[v.z & (kK1Bins - 1)], 1u);
+      atomicAdd(&hb[v.w & (kK1Bins - 1)], 1u);
+    }
+    for (uint32_t i = ve + threadIdx.x; i < m.end; i += blockDim.x)
+      atomicAdd(&hb[part[i] & (kK1Bins - 1)], 1u);
+    __syncthreads();
+    const uint64_t id0 = (uint64_t)m.bucket << kK1Shift;
+    const uint32_t nbin = static_cast<uint32_t>((n - id0 < kK1Bins ? n - id0 : (uint64_t)kK1Bins));
+    if (m.split) {
+      for (uint32_t i = threadIdx.x; i < nbin; i += blockDim.x)
+        if (hb[i]) atomicAdd(&deg[id0 + i], hb[i]);
+    } else {
+      for (uint32_t i = threadIdx.x; i < nbin; i += blockDim.x) deg[id0 + i] = hb[i];
+    }
+    __syncthreads();
+  }
+}
+
+// deg must be zeroed by the caller (split buckets accumulate into it).
+// Returns false when the binned form does not apply (tiny graphs, n > 2^28,
+// or no room for the 4 B x E temporary) so the caller runs the one-pass form.
+bool compute_indeg_binned(tg_ctx* ctx, const uint32_t* tgt, uint64_t e, uint64_t n,
+                          uint32_t* deg) {
+  if (const char* k = std::getenv("TIERGRAPH_K1")) {
+    if (std::strcmp(k, "atomic") == 0) return false;
+  } else if (e < (1u << 20) || n <= 12288) {
+    return false;  // launch-bound sizes: the one-pass kernel is cheaper
+  }
+  const uint64_t nb64 = (n + kK1Bins - 1) >> kK1Shift;
+  if (nb64 > kK1MaxBuckets || e == 0 || e >= 0xffffffffull ||
+      (reinterpret_cast<uintptr_t>(tgt) & 15))
+    return false;
+  const uint32_t nb = static_cast<uint32_t>(nb64);
+  static bool attr[TG_MAX_DEVICES] = {};
+  const size_t scat_smem = 4 * (kK1Tile + 3 * (size_t)nb);
+  if (!attr[ctx->device % TG_MAX_DEVICES]) {
+    TGB_CUDA(cudaFuncSetAttribute(k1_scatter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  4 * (kK1Tile + 3 * kK1MaxBuckets)));
+    TGB_CUDA(cudaFuncSetAttribute(k1_hist_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  4 * kK1Bins));
+    TGB_CUDA(cudaFuncSetAttribute(k1_count_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  4 * kK1MaxBuckets));
+    attr[ctx->device % TG_MAX_DEVICES] = true;
+  }
+  int occ = 0;
+  TGB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k1_scatter_kernel, kK1Threads,
+                                                         scat_smem));
+  occ = std::max(occ, 1);
+  // one wave of chunks; each chunk a whole number of tiles
+  uint64_t chunk = (e + (uint64_t)ctx->num_sms * occ - 1) / ((uint64_t)ctx->num_sms * occ);
+  chunk = (chunk + kK1Tile - 1) / kK1Tile * kK1Tile;
+  const uint32_t G = static_cast<uint32_t>((e + chunk - 1) / chunk);
+  const uint64_t ncnt = (uint64_t)nb * G + 1;
+  const uint64_t max_items = nb + e / kK1Piece + 1;
+  const size_t bytes = 4 * e + 16 + 8 * ncnt + 16 + sizeof(K1Item) * max_items + 64;
+  char* base = nullptr;
+  if (cudaMallocAsync(reinterpret_cast<void**>(&base), bytes, ctx->stream) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  auto align = [](char* p) {
+    return reinterpret_cast<char*>((reinterpret_cast<uintptr_t>(p) + 15) & ~uintptr_t(15));
+  };
+  char* p = base;
+  auto* part = reinterpret_cast<uint32_t*>(p);  p = align(p + 4 * e);
+  auto* cnt = reinterpret_cast<uint64_t*>(p);   p = align(p + 8 * ncnt);
+  auto* items = reinterpret_cast<K1Item*>(p);   p = align(p + sizeof(K1Item) * max_items);
+  auto* small = reinterpret_cast<uint32_t*>(p);  // [nitems, claim counter]
+  TGB_CUDA(cudaMemsetAsync(small, 0, 8, ctx->stream));
+  TGB_CUDA(cudaMemsetAsync(cnt + ncnt - 1, 0, 8, ctx->stream));
+  k1_count_kernel<<<G, kK1Threads, 4 * nb, ctx->stream>>>(tgt, e, chunk, nb, G, cnt);
+  TGB_LAUNCHED();
+  exclusive_scan_u64(ctx, cnt, ncnt);
+  k1_scatter_kernel<<<G, kK1Threads, scat_smem, ctx->stream>>>(tgt, e, chunk, nb, G, cnt, part);
+  TGB_LAUNCHED();
+  k1_items_kernel<<<1, 1024, 0, ctx->stream>>>(cnt, nb, G, items, small);
+  TGB_LAUNCHED();
+  k1_hist_kernel<<<ctx->num_sms, kK1HistThreads, 4 * kK1Bins, ctx->stream>>>(part, items, small,
+                                                                             small + 1, n, deg);
+  TGB_LAUNCHED();
+  TGB_CUDA(cudaFreeAsync(base, ctx->stream));
+  return true;
+}
+
+}  // namespace tgb

@@ -963,6 +963,7 @@ unsigned long long read_flag(tg_ctx* ctx, unsigned long long* dflag) {
 void compute_indeg(tg_ctx* ctx, const tg_graph* g, uint32_t* deg) {
   TGB_CUDA(cudaMemsetAsync(deg, 0, sizeof(uint32_t) * std::max<uint64_t>(g->n, 1), ctx->stream));
   if (g->e == 0) return;
+  if (compute_indeg_binned(ctx, g->tgt, g->e, g->n, deg)) return;  // indegree.cu
   const unsigned grid = grid_for(g->e / 4 + 1, 512, ctx->num_sms * 4);
   indeg_kernel<<<grid, 512, 0, ctx->stream>>>(g->tgt, g->e, static_cast<uint32_t>(g->n), deg);
   TGB_LAUNCHED();
@@ -1148,7 +1149,7 @@ const tg_graph* relabel_twin(tg_ctx* ctx, const tg_graph* gc) {
     TGB_CUDA(cudaMalloc(&g->old_of, 4 * n));
     TGB_CUDA(cudaMalloc(&g->new_of, 4 * n));
     TGB_CUDA(cudaMalloc(&t->off, 4 * (n + 1)));
-    TGB_CUDA(cudaMalloc(&t->tgt, 4 * std::max<uint64_t>(e, 1)));
+    TGB_CUDA(cudaMalloc(&t->tgt, 4 * std::max<uint64_t>(e, 1) + 16));  // +16: K3 reads 16 B target groups
     TGB_CUDA(cudaMalloc(&t->indeg, 4 * n));
     TGB_CUDA(cudaMalloc(&t->row_label, 4 * n));
     TGB_CUDA(cudaMalloc(&t->row_orig, 4 * n));
@@ -1157,7 +1158,14 @@ const tg_graph* relabel_twin(tg_ctx* ctx, const tg_graph* gc) {
     TGB_CUDA(cudaEventCreate(&ev0));
     TGB_CUDA(cudaEventCreate(&ev1));
     TGB_CUDA(cudaEventRecord(ev0, ctx->stream));
-    sort_ids_by_value_desc(ctx, g->indeg, n, g->old_of);
+    // TIERGRAPH_PR_LABEL=rows (experiment): label = storage row, so every
+    // row's norm write is sequential; the hub norms are then packed by
+    // out-degree rather than by in-degree. Default: labels by in-degree.
+    const char* lab = std::getenv("TIERGRAPH_PR_LABEL");
+    if (lab && std::string(lab) == "rows")
+      TGB_CUDA(cudaMemcpyAsync(g->old_of, sg.order, 4 * n, cudaMemcpyDeviceToDevice, ctx->stream));
+    else
+      sort_ids_by_value_desc(ctx, g->indeg, n, g->old_of);
     twin_labels_kernel<<<grid_for(n, 256), 256, 0, ctx->stream>>>(g->old_of, g->indeg, n,
                                                                   g->new_of, t->indeg);
     TGB_LAUNCHED();
@@ -1369,7 +1377,7 @@ int tg_graph_create(tg_ctx* ctx, const uint64_t* offsets, const uint64_t* target
       domain_error("tg_graph_create: n and e must be < 2^32 for the u32 device layout");
     DeviceGuard dg(ctx->device);
     uint32_t* tgt = nullptr;
-    TGB_CUDA(cudaMalloc(&tgt, sizeof(uint32_t) * std::max<uint64_t>(e, 1)));
+    TGB_CUDA(cudaMalloc(&tgt, sizeof(uint32_t) * std::max<uint64_t>(e, 1) + 16));  // +16: K3 reads 16 B target groups
     try {
       auto* bad = ctx->scratch_t<unsigned long long>(kSmall, 2);
       TGB_CUDA(cudaMemsetAsync(bad + 1, 0xff, sizeof(unsigned long long), ctx->stream));
@@ -1454,7 +1462,7 @@ int tg_graph_create_rows(tg_ctx* ctx, const uint64_t* offsets, const uint64_t* t
       TGB_CUDA(cudaMalloc(&g->off_alloc, 4 * (m + 1)));
       TGB_CUDA(cudaMemcpy(g->off_alloc, o32.data(), 4 * (m + 1), cudaMemcpyHostToDevice));
       g->off = g->off_alloc - row_begin;  // off[r] for r in [row_begin, row_end]
-      TGB_CUDA(cudaMalloc(&g->tgt, 4 * std::max<uint64_t>(g->e, 1)));
+      TGB_CUDA(cudaMalloc(&g->tgt, 4 * std::max<uint64_t>(g->e, 1) + 16));  // +16: K3 reads 16 B target groups
       auto* bad = ctx->scratch_t<unsigned long long>(kSmall, 2);
       TGB_CUDA(cudaMemsetAsync(bad + 1, 0xff, 8, ctx->stream));
       const bool tdev = is_device_ptr(targets);

@@ -57,6 +57,8 @@ struct tg_graph {
 namespace tgb {
 inline bool whole_graph(const tg_graph* g) { return g->rb == 0 && g->re == g->n; }
 void compute_indeg(tg_ctx* ctx, const tg_graph* g, uint32_t* deg);
+// K1 as partition + shared-memory histograms (indegree.cu); false = not applicable
+bool compute_indeg_binned(tg_ctx* ctx, const uint32_t* tgt, uint64_t e, uint64_t n, uint32_t* deg);
 const tg_graph::Sched& schedule(tg_ctx* ctx, const tg_graph* g, uint64_t rb, uint64_t re);
 void check_config(uint32_t iterations, double damp);
 // deg + norm0 (full length) from in-degrees `deg` (already final).

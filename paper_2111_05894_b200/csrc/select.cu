@@ -158,13 +158,26 @@ __global__ void __launch_bounds__(kRsWarps * 32, 3) scatter_kernel(
     // publish this tile's count, then look back for the earlier tiles'
     volatile uint64_t* st = status;
     st[(uint64_t)tile * 256 + d] = (tile ? kStAgg : kStInc) | run;
+    // Look back four tiles per round trip: the four status words are loaded
+    // together (independent L2 loads), then consumed in order up to the first
+    // inclusive prefix; an unpublished one is re-read from there (spin).
     uint64_t excl = 0;
     for (int64_t j = (int64_t)tile - 1; j >= 0;) {
-      const uint64_t v = st[(uint64_t)j * 256 + d];
-      if (!(v & (kStAgg | kStInc))) continue;  // not published yet: spin
-      excl += v & kStMask;
-      if (v & kStInc) break;
-      --j;
+      uint64_t v[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) v[q] = j - q >= 0 ? st[(uint64_t)(j - q) * 256 + d] : (2ull << 62);  // kStInc, 0
+      int q = 0;
+      bool done = false;
+      for (; q < 4; ++q) {
+        if (!(v[q] & (kStAgg | kStInc))) break;  // not published yet
+        excl += v[q] & kStMask;
+        if (v[q] & kStInc) {
+          done = true;
+          break;
+        }
+      }
+      if (done) break;
+      j -= q;
     }
     if (tile) st[(uint64_t)tile * 256 + d] = kStInc | (excl + run);
     // the digit's global base: exclusive scan of this pass's histogram
@@ -339,6 +352,96 @@ static void sort_desc_u32(tg_ctx* ctx, const uint32_t* off, const uint32_t* val,
   TGB_CUDA(cudaFreeAsync(base, ctx->stream));
 }
 
+// K6 without the random 8 B scatter. new_id_of[order[r]] = r over N ids is a
+// scatter of 8 B values into an 8N-byte array: at C3 (888 MB, far beyond L2)
+// every store lands in a different sector that L2 must fill from DRAM first,
+// 4.9 ms for 8.3 GB of DRAM traffic. Instead, (1) the ranks are partitioned by
+// id bucket (id >> 20, 1 Mi ids = 8 MB of new_id_of per bucket) with
+// coalesced staged writes -- bucket b's region of the pair array is exactly
+// [b << 20, ...) because every id occurs once, so no counting pass -- and (2)
+// the pairs are replayed in bucket order by the whole grid at once, so the
+// live window of new_id_of is a few MB and every sector is completed in L2
+// before it is written back.
+constexpr int kPmShift = 20;
+constexpr int kPmIpt = 16;
+constexpr int kPmTile = 256 * kPmIpt;
+constexpr uint32_t kPmMaxBuckets = 1024;
+
+__global__ void __launch_bounds__(256) perm_part_kernel(const uint32_t* __restrict__ v0,
+                                                        const uint32_t* __restrict__ v1,
+                                                        const RadixPlan* __restrict__ plan,
+                                                        uint64_t n, uint32_t nb,
+                                                        uint64_t* __restrict__ order,
+                                                        uint2* __restrict__ pairs,
+                                                        uint32_t* __restrict__ bcur) {
+  const uint32_t* v = plan->final_src ? v1 : v0;
+  __shared__ uint2 st[kPmTile];
+  __shared__ uint32_t tcnt[kPmMaxBuckets], tst[kPmMaxBuckets], tbase[kPmMaxBuckets];
+  __shared__ uint32_t wsum[8];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  for (uint64_t t0 = (uint64_t)blockIdx.x * kPmTile; t0 < n; t0 += (uint64_t)gridDim.x * kPmTile) {
+    for (uint32_t b = threadIdx.x; b < nb; b += blockDim.x) tcnt[b] = 0;
+    __syncthreads();
+    uint32_t id[kPmIpt], rk[kPmIpt];
+#pragma unroll
+    for (int k = 0; k < kPmIpt; ++k) {
+      const uint64_t i = t0 + k * 256 + threadIdx.x;
+      id[k] = i < n ? v[i] : 0xffffffffu;
+      if (i < n) {
+        if (order) order[i] = id[k];
+        rk[k] = atomicAdd(&tcnt[id[k] >> kPmShift], 1u);
+      }
+    }
+    __syncthreads();
+    {  // exclusive scan of tcnt (nb <= 1024: 4 per thread) + global reservations
+      const uint32_t per = (nb + 255) / 256;
+      const uint32_t b0 = min(nb, threadIdx.x * per), b1 = min(nb, b0 + per);
+      uint32_t run = 0;
+      for (uint32_t b = b0; b < b1; ++b) run += tcnt[b];
+      uint32_t incl = run;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += y;
+      }
+      if (lane == 31) wsum[w] = incl;
+      __syncthreads();
+      uint32_t x = incl - run;
+      for (int k = 0; k < w; ++k) x += wsum[k];
+      for (uint32_t b = b0; b < b1; ++b) {
+        tst[b] = x;
+        x += tcnt[b];
+        if (tcnt[b]) tbase[b] = atomicAdd(&bcur[b], tcnt[b]);
+      }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < kPmIpt; ++k) {
+      const uint64_t i = t0 + k * 256 + threadIdx.x;
+      if (i < n) st[tst[id[k] >> kPmShift] + rk[k]] = make_uint2(id[k], static_cast<uint32_t>(i));
+    }
+    __syncthreads();
+    const uint32_t tn = static_cast<uint32_t>(n - t0 < (uint64_t)kPmTile ? n - t0 : kPmTile);
+    for (uint32_t j = threadIdx.x; j < tn; j += blockDim.x) {
+      const uint2 p = st[j];
+      const uint32_t b = p.x >> kPmShift;
+      pairs[((uint64_t)b << kPmShift) + tbase[b] + (j - tst[b])] = p;
+    }
+    __syncthreads();
+  }
+}
+
+// (2) replay in bucket order: consecutive threads take consecutive pairs
+__global__ void __launch_bounds__(256) perm_replay_kernel(const uint2* __restrict__ pairs,
+                                                          uint64_t n,
+                                                          uint64_t* __restrict__ new_id_of) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    const uint2 p = __ldcs(pairs + i);
+    new_id_of[p.x] = p.y;
+  }
+}
+
 // Sorts scores -> (order, new_id_of). Either output may be null. Device pointers.
 void sort_scores(tg_ctx* ctx, const double* scores_dev, uint64_t n, uint64_t* order_dev,
                  uint64_t* perm_dev) {
@@ -361,8 +464,22 @@ void sort_scores(tg_ctx* ctx, const double* scores_dev, uint64_t n, uint64_t* or
   plan_kernel<<<1, 256, 0, ctx->stream>>>(hist, n, plan);
   TGB_LAUNCHED();
   radix_passes(ctx, k0, v0, k1, v1, n, 8, plan, hist);
-  perm_kernel<<<grid_for(n, 256), 256, 0, ctx->stream>>>(v0, v1, plan, n, order_dev, perm_dev);
-  TGB_LAUNCHED();
+  const uint64_t nb = (n + (1ull << kPmShift) - 1) >> kPmShift;
+  if (perm_dev && nb <= kPmMaxBuckets) {
+    uint32_t* bcur = ctx->scratch_t<uint32_t>(kScratchE, kPmMaxBuckets);
+    TGB_CUDA(cudaMemsetAsync(bcur, 0, 4 * nb, ctx->stream));
+    // both key buffers are free after the sort; pairs (8N bytes) go in k0
+    uint2* pairs = reinterpret_cast<uint2*>(k0);
+    perm_part_kernel<<<grid_for(n, kPmTile, ctx->num_sms * 8), 256, 0, ctx->stream>>>(
+        v0, v1, plan, n, static_cast<uint32_t>(nb), order_dev, pairs, bcur);
+    TGB_LAUNCHED();
+    perm_replay_kernel<<<grid_for(n, 256, ctx->num_sms * 8), 256, 0, ctx->stream>>>(pairs, n,
+                                                                                    perm_dev);
+    TGB_LAUNCHED();
+  } else {
+    perm_kernel<<<grid_for(n, 256), 256, 0, ctx->stream>>>(v0, v1, plan, n, order_dev, perm_dev);
+    TGB_LAUNCHED();
+  }
   unsigned long long hb = 0;
   TGB_CUDA(cudaMemcpyAsync(&hb, bad, 8, cudaMemcpyDeviceToHost, ctx->stream));
   ctx->sync();

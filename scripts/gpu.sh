@@ -13,10 +13,14 @@
 #   launches:<cfg> ncu launch list (gpu__time_duration) of a short bench run
 #   ncu_k8:<cfg>   ncu (application replay) of K8 on the cached C3/C4 inputs
 #   ncu_k3:<cfg>   ncu --set full of K3 (pr_step) at <cfg>
+#   ncu_k3all:<cfg> ncu --set full of every K3 kernel of one step (class A hub x2, B, C stream) at <cfg>
 #   prlaunch:<cfg> per-launch time / DRAM / L2 of every K3 kernel (pr_*) at <cfg>
 #   k3probe:<cfg>  scripts/k3_probe.py <cfg> over the settings in $K3_SETTINGS (';'-separated)
 #   pytestf:<file> pytest -m gpu of one test file
 #   sanitize       compute-sanitizer memcheck/racecheck/synccheck on small cases
+#   k1probe:<cfg>  scripts/k1_probe.py: K1 atomic vs binned at <cfg>
+#   k1launch:<cfg> the same under an ncu launch list (per-kernel time and DRAM bytes)
+#   selprobe       selection (K4-K6) at C2/C3 sizes: ours, ncu per-kernel list, and cub's LSD sort as a yardstick
 #   shared2        2-process runs on one GPU (IPC gather, PageRank exchange)
 T=${1:?tag}; shift
 O=gpurun_out/$T; mkdir -p $O
@@ -58,11 +62,25 @@ for st in "$@"; do
     prlaunch) timeout 1800 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum,lts__t_sectors_op_read.sum,lts__t_sector_hit_rate.pct \
         --clock-control none --csv -k regex:"pr_|gather_floor" --log-file $O/prlaunch_$a.csv \
         python scripts/profile_target.py k3 --config $a --launches 1 > $O/prlaunch_$a.log 2>&1 ;;
+    ncu_k3all) timeout 2400 ncu --set full --clock-control none --import-source on -k regex:"pr_(hub|step|cstream)" -s 4 -c 4 \
+        -o $O/k3all_$a python scripts/profile_target.py k3 --config $a --launches 1 > $O/ncu_k3all_$a.log 2>&1 ;;
     ncu_k3) timeout 2400 ncu --set full --clock-control none --import-source on -k regex:pr_step -s 2 -c 1 \
         -o $O/k3_$a python scripts/profile_target.py k3 --config $a --launches 1 > $O/ncu_k3_$a.log 2>&1 ;;
     sanitize) bash scripts/sanitize.sh $O ;;
     k3probe) timeout 1500 python scripts/k3_probe.py $a > $O/k3probe_$a.log 2>&1 ;;
     pytestf) timeout 2400 python -m pytest tests/$a -x -q -m gpu > $O/pytest_$a.log 2>&1; echo "rc=$?" >> $O/pytest_$a.log ;;
+    k1probe) timeout 1200 python scripts/k1_probe.py $a >> $O/k1probe_$a.log 2>&1 ;;
+    k1launch) timeout 1200 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum \
+        --clock-control none --csv -k regex:"k1_|indeg|exclusive|tile_|sums_" --log-file $O/k1_launches_$a.csv \
+        python scripts/k1_probe.py $a > $O/k1launch_$a.log 2>&1 ;;
+    selprobe)
+      nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o /tmp/sort_probe scripts/micro/sort_probe.cu
+      for nn in 2450000 111000000; do
+        timeout 300 /tmp/sort_probe $nn >> $O/selprobe.log 2>&1
+        timeout 300 python scripts/select_probe.py $nn >> $O/selprobe.log 2>&1
+        timeout 600 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv \
+          --log-file $O/sel_launches_$nn.csv python scripts/select_probe.py $nn 1 >> $O/selprobe_ncu.log 2>&1
+      done ;;
     shared2)
       TG_BENCH_SHARE_GPU=1 timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 \
         --master-addr 127.0.0.1 --master-port 29511 bench.py --gpus 2 --config ${a:-c1} --steps 20 --warmup 3 \

@@ -1,5 +1,9 @@
-"""Experiment: K1 (in-degree) timing on a config graph, host-timed per call.
-Not part of the bench."""
+"""Experiment: K1 (in-degree) timing on a config graph, host-timed per call,
+one-pass atomic form vs binned form (TIERGRAPH_K1), results compared.
+Not part of the bench.
+
+  python scripts/k1_probe.py c3
+"""
 import os
 import sys
 import time
@@ -17,13 +21,26 @@ def main():
     off, tgt, tid = bench.build_inputs(cfg, 0)
     g = tg.CsrGraph(off, tgt)
     g.device(ctx)
-    out = torch.empty(len(off) - 1, dtype=torch.int64, device="cuda")
-    for _ in range(6):
-        torch.cuda.synchronize()
-        t0 = time.perf_counter()
-        tg.in_degrees(g, ctx=ctx, out=out)
-        torch.cuda.synchronize()
-        print(f"in_degrees {(time.perf_counter() - t0) * 1e6:.0f} us", flush=True)
+    e = len(tgt)
+    outs = {}
+    for mode in ("atomic", "binned"):
+        if mode == "atomic":
+            os.environ["TIERGRAPH_K1"] = "atomic"
+        else:
+            os.environ.pop("TIERGRAPH_K1", None)
+        out = torch.empty(len(off) - 1, dtype=torch.int64, device="cuda")
+        ts = []
+        for _ in range(6):
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            tg.in_degrees(g, ctx=ctx, out=out)
+            torch.cuda.synchronize()
+            ts.append(time.perf_counter() - t0)
+        outs[mode] = out
+        best = min(ts[1:])
+        print(f"K1 {mode:7s}: {best * 1e6:9.0f} us (median {sorted(ts[1:])[2] * 1e6:.0f}), "
+              f"{4 * e / best / 1e12:.3f} TB/s of targets read", flush=True)
+    print("equal:", bool(torch.equal(outs["atomic"], outs["binned"])), flush=True)
 
 
 if __name__ == "__main__":

@@ -24,8 +24,21 @@ def main():
     ctx = tg.Context(0)
     off, tgt, tid = bench.build_inputs(cfg, 0)
     n, e = len(off) - 1, len(tgt)
+    import numpy as np
+    lens = np.diff(np.asarray(off, dtype=np.int64))
+    for lo, hi in ((4096, None), (512, 4096), (0, 512)):
+        m = (lens > lo) & ((lens <= hi) if hi else True)
+        print(f"class len in ({lo}, {hi or 'inf'}]: {int(m.sum())} rows, {int(lens[m].sum())} edges",
+              flush=True)
+    indeg = np.bincount(np.asarray(tgt, dtype=np.int64), minlength=n)
+    cum = np.cumsum(np.sort(indeg)[::-1])
+    for k in (1 << 20, 1 << 22, 1 << 24, 1 << 25):
+        print(f"top {k} in-degree nodes ({8 * k >> 20} MB of norm): {cum[min(k, n) - 1] / e:.3f} "
+              f"of the gathers", flush=True)
+    del indeg, cum, lens
     g = tg.CsrGraph(off, tgt)
     gh = g.device(ctx)
+    fresh = os.environ.get("K3_FRESH_GRAPH") == "1"  # rebuild the device graph (and twin) per setting
     dev = torch.device("cuda", 0)
     tid_d = torch.as_tensor(tid.ids.astype("int64"), device=dev)
     ref = None
@@ -37,20 +50,28 @@ def main():
                 os.environ[k] = v
             else:
                 os.environ.pop(k, None)
+        if fresh:
+            g.release()
+            torch.cuda.synchronize()
+            gh = g.device(ctx)
         out = torch.empty(n, dtype=torch.float64, device=dev)
         ph = (C.c_double * (iters + 1))()
         steps = []
+        clk = bench.ClockSampler(0)
+        clk.__enter__()
         for _ in range(3):
             assert LIB.tg_weighted_reverse_pagerank_timed(ctx.h, gh, iters, 0.85, tid_d.data_ptr(),
                                                           len(tid.ids), out.data_ptr(), ph) == 0, \
                 LIB.tg_last_error()
             steps.extend(ph[1:])
+        clk.__exit__()
+        mhz = sorted(c for _, c, _ in clk.samples)[len(clk.samples) // 2] if clk.samples else None
         if ref is None:
             ref = out.clone()
         same = bool(torch.equal(out, ref))
         ms = statistics.mean(steps)
         print(f"{st or '(default)':50s} step {ms:8.3f} ms  {e / ms / 1e6:7.1f} GTEPS/iter  "
-              f"bit-identical {same}", flush=True)
+              f"bit-identical {same}  sm {mhz} MHz", flush=True)
 
 
 if __name__ == "__main__":

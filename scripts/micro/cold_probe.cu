@@ -7,7 +7,8 @@
 //     page, rows per 2 MB page): tells 4 KB (host IOMMU / 4 KB PTE) from
 //     2 MB translation;
 //   * the ENGINE: SM zero-copy loads vs the copy engines
-//     (cudaMemcpyBatchAsync, one 512 B descriptor per row), which share the
+//     (one cudaMemcpyAsync per row; r02b used a batched-copy call that this
+//     pool has since closed), which share the
 //     GPU page tables and the host IOMMU but not the SM-side TLBs;
 //   * the REGION size (1 GB control vs the C3-sized region).
 // Every launch reads FRESH random units (no translation reuse across
@@ -115,12 +116,8 @@ static Res run(Pattern p, bool ce, const uint8_t* host_dev, const uint8_t* host_
     CK(cudaMemsetAsync(flush, l & 0xff, 256u << 20, st));
     CK(cudaEventRecord(a, st));
     if (ce) {
-      cudaMemcpyAttributes at{};
-      at.srcAccessOrder = cudaMemcpySrcAccessOrderStream;
-      at.srcLocHint.type = cudaMemLocationTypeHost;
-      at.dstLocHint.type = cudaMemLocationTypeDevice;
-      size_t idx = 0, fail = 0;
-      CK(cudaMemcpyBatchAsync(dsts.data(), srcs.data(), sizes.data(), units, &at, &idx, 1, &fail, st));
+      for (uint64_t i = 0; i < units; ++i)
+        CK(cudaMemcpyAsync(dsts[i], srcs[i], sizes[i], cudaMemcpyHostToDevice, st));
     } else {
       zc_gather<<<148 * 8, 256, 0, st>>>(reinterpret_cast<const uint4*>(host_dev), off_d, units, ub,
                                          reinterpret_cast<uint4*>(dst));

@@ -40,7 +40,7 @@ def hub_graph(n, hubs, seed):
                                np.concatenate(dst).astype(np.uint64))
 
 
-def case_k8(ctx):
+def case_k8(ctx, gather_mode="bulk+spread+dynamic"):
     n, dim = 4000, 100  # 400 B rows: split cold rows (384 + 16)
     rng = np.random.default_rng(1)
     feat = rng.integers(0, 256, (n, dim * 4), dtype=np.uint8)
@@ -48,7 +48,8 @@ def case_k8(ctx):
     want = PORT.reorder_features(feat, perm.new_id_of)
     lay = tg.plan_layout(n, 0.4, 0.05, 2, dim, 4)
     ctxs = [ctx, tg.Context(ctx.device)]
-    stores = [tg.TieredFeatureStore(feat, perm, lay, d, ctx=ctxs[d]) for d in range(2)]
+    stores = [tg.TieredFeatureStore(feat, perm, lay, d, ctx=ctxs[d], gather_mode=gather_mode)
+              for d in range(2)]
     for d, s in enumerate(stores):
         for q, o in enumerate(stores):
             if q != d:
@@ -131,7 +132,31 @@ def case_transpose(ctx):
     assert np.array_equal(t.offsets, wo) and np.array_equal(t.targets, wt), "transpose"
 
 
-CASES = {"k8": case_k8, "sampler": case_sampler, "k3": case_k3, "peers": case_peers,
+def case_k8ldg(ctx):
+    """K8's LDG path (16 B loads/stores, no TMA): initcheck does not track the
+    bytes a cp.async.bulk smem->global copy writes, so the bulk path's output
+    reads as uninitialized there; this case covers the same gathers with
+    tracked stores."""
+    case_k8(ctx, "ldg")
+
+
+def case_k1(ctx):
+    """Binned K1 (partition + shared-memory histograms; indegree.cu), forced on
+    a small graph whose bucket 0 is split over two histogram pieces."""
+    os.environ["TIERGRAPH_K1"] = "binned"
+    try:
+        n = 100_000
+        rng = np.random.default_rng(4)
+        tgt = np.concatenate([np.full(1_100_000, 5), rng.integers(0, n, 300_000)]).astype(np.uint64)
+        off = np.zeros(n + 1, np.uint64)
+        off[1:] = len(tgt)
+        got = tg.in_degrees(tg.CsrGraph(off, tgt), ctx=ctx)
+        assert np.array_equal(got, np.bincount(tgt.astype(np.int64), minlength=n)), "k1"
+    finally:
+        os.environ.pop("TIERGRAPH_K1", None)
+
+
+CASES = {"k8": case_k8, "k8ldg": case_k8ldg, "k1": case_k1, "sampler": case_sampler, "k3": case_k3, "peers": case_peers,
          "mgraph": case_mgraph, "select": case_select, "transpose": case_transpose}
 
 
