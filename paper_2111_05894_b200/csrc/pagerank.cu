@@ -35,7 +35,15 @@ namespace tgb {
 //   A  len > kLenA          one CTA per row, exact parallel evaluation of the chain
 //   B  kLenB < len <= kLenA one warp per row: lanes stage 256-edge windows, lane 0 chains
 //   C  len <= kLenB         one thread per row (a warp's rows have near-equal lengths)
+// The class-A bound is adaptive: max(kLenA, min(E >> 14, kLenAMax)). A class-B
+// row's serial chain costs ~8 cycles per edge, so rows up to E / 2^14 edges
+// finish well inside a step that streams E edges (C3: rows up to 65,536 edges,
+// chain <= 0.3 ms of an 11 ms step); only rows longer than that need class
+// A's exact parallel evaluation, whose per-edge instruction count (~9 per
+// lane) made the 20.8k C3 rows of 4-65k edges cost 4.2 ms on their own
+// (profiles/r02h, r02i: C3 step 13.9 -> 11.0 ms; C2 keeps 4096).
 constexpr uint32_t kLenA = 4096;
+constexpr uint32_t kLenAMax = 65536;
 constexpr uint32_t kLenB = 512;
 // class-A CTAs: 256 threads x 8 addends (2,048 per tile); 512 x 8 for the
 // rows longer than kHubLong and a quarter of the longest row (half the tiles
@@ -163,6 +171,27 @@ __global__ void twin_labels_kernel(const uint32_t* __restrict__ old_of,
     const uint32_t u = old_of[v];
     new_of[u] = static_cast<uint32_t>(v);
     indeg_lab[v] = indeg[u];
+  }
+}
+
+// Hybrid twin order key (descending sort, ties by id): class A rows (more
+// than kLenA edges) by length above everything else; every other row by its
+// length bucket (0: empty, 1 + ceil(log2 len)) and then its in-degree.
+__global__ void hybrid_key_kernel(const uint32_t* __restrict__ off,
+                                  const uint32_t* __restrict__ indeg, uint64_t n,
+                                  uint32_t* __restrict__ key) {
+  for (uint64_t v = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; v < n;
+       v += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t len = off[v + 1] - off[v];
+    constexpr uint32_t kLow = (1u << 26) - 1;
+    uint32_t k;
+    if (len > kLenA) {
+      k = (63u << 26) | min(len, kLow);
+    } else {
+      const uint32_t b = len ? 1u + (32u - __clz(len - 1u)) : 0u;  // <= 13
+      k = (b << 26) | min(indeg[v], kLow);
+    }
+    key[v] = k;
   }
 }
 
@@ -788,8 +817,9 @@ __device__ __forceinline__ void warp_rows_staged(const PrStepArgs& a, uint64_t k
   if (has) finish_row(a, k0 + lane, acc);
 }
 
-// Class C on the relabelled twin, streamed (TIERGRAPH_PR_CSTREAM, default
-// on): one warp takes kCsRows consecutive rows (one contiguous edge range,
+// Class C on the relabelled twin, streamed (TIERGRAPH_PR_CSTREAM=1; default
+// off: at C3 a step takes 24.2 ms with it against 14.2 ms with the warp-staged
+// class C of pr_step_kernel, profiles/r02g): one warp takes kCsRows consecutive rows (one contiguous edge range,
 // rows stored in length order) and streams it in kCsChunk-edge chunks with
 // the memory pipeline never drained: cp.async copies the targets three
 // chunks ahead (16 B, coalesced) and gathers the normalized values one chunk
@@ -892,7 +922,10 @@ __global__ void __launch_bounds__(kCsWarps * 32) pr_cstream_kernel(const PrStepA
   for (; j < nrows; j += 32) finish_row(a, k0 + j, 0.0);  // empty rows at the very end
 }
 
-__global__ void __launch_bounds__(kPrWarps * 32) pr_step_kernel(const PrStepArgs a) {
+// MinB: CTAs per SM the register allocation must allow (1: no cap, 68
+// registers, 3 CTAs fit; 4: <= 64 registers). TIERGRAPH_PR_MINB picks one.
+template <int MinB>
+__global__ void __launch_bounds__(kPrWarps * 32, MinB) pr_step_kernel(const PrStepArgs a) {
   __shared__ __align__(16) double smem[kPrWarps * 32 / kBLanes * kBStride];  // 16.6 KB: class B windows
   if (blockIdx.x < a.b_ctas) {
     const int g = threadIdx.x / kBLanes;  // row group within the CTA
@@ -1018,7 +1051,9 @@ const tg_graph::Sched& schedule(tg_ctx* ctx, const tg_graph* g, uint64_t rb, uin
   // TIERGRAPH_PR_LENA / _LENB override the class boundaries (experiments)
   const char* ea = std::getenv("TIERGRAPH_PR_LENA");
   const char* eb = std::getenv("TIERGRAPH_PR_LENB");
-  const uint32_t la = ea ? static_cast<uint32_t>(std::atoi(ea)) : kLenA;
+  const uint32_t la = ea ? static_cast<uint32_t>(std::atoi(ea))
+                         : static_cast<uint32_t>(std::max<uint64_t>(
+                               kLenA, std::min<uint64_t>(g->e >> 14, kLenAMax)));
   const uint32_t lbn = eb ? static_cast<uint32_t>(std::atoi(eb)) : kLenB;
   class_bounds_kernel<<<1, 32, 0, ctx->stream>>>(g->off, sc.order, re - rb, la, std::min(lbn, la),
                                                  bounds);
@@ -1071,7 +1106,7 @@ void pagerank_step(tg_ctx* ctx, const tg_graph* g, const uint32_t* deg, double d
   uint64_t c_ctas = (a.m - sc.nB + kPrWarps * 32 - 1) / (kPrWarps * 32);
   // class C streamed on its own stream (relabelled twin: rows in storage order)
   const char* csv = std::getenv("TIERGRAPH_PR_CSTREAM");
-  const bool cstream = !(csv && csv[0] == '0');
+  const bool cstream = csv && csv[0] == '1';
   const bool cs = cstream && !sc.order && a.m > sc.nB;
   if (cs) c_ctas = 0;
   if (sc.nA || cs) ctx->fork();
@@ -1111,7 +1146,11 @@ void pagerank_step(tg_ctx* ctx, const tg_graph* g, const uint32_t* deg, double d
   const unsigned grid = static_cast<unsigned>(a.b_ctas + c_ctas);
   if (grid) {
     // classes B (first CTAs: long chains start early) and C in one grid
-    pr_step_kernel<<<grid, kPrWarps * 32, 0, ctx->stream>>>(a);
+    const char* mb = std::getenv("TIERGRAPH_PR_MINB");
+    if (mb && mb[0] == '4')
+      pr_step_kernel<4><<<grid, kPrWarps * 32, 0, ctx->stream>>>(a);
+    else
+      pr_step_kernel<1><<<grid, kPrWarps * 32, 0, ctx->stream>>>(a);
     TGB_LAUNCHED();
   }
   if (sc.nA || cs) ctx->join();
@@ -1158,19 +1197,35 @@ const tg_graph* relabel_twin(tg_ctx* ctx, const tg_graph* gc) {
     TGB_CUDA(cudaEventCreate(&ev0));
     TGB_CUDA(cudaEventCreate(&ev1));
     TGB_CUDA(cudaEventRecord(ev0, ctx->stream));
-    // TIERGRAPH_PR_LABEL=rows (experiment): label = storage row, so every
-    // row's norm write is sequential; the hub norms are then packed by
-    // out-degree rather than by in-degree. Default: labels by in-degree.
+    // Labels (TIERGRAPH_PR_LABEL):
+    //   indeg  label = in-degree rank; rows stored in K3's length order, so
+    //          a row's norm write goes to a scattered label;
+    //   rows   label = storage row (length order): sequential norm writes,
+    //          hub norms packed by out-degree;
+    //   hybrid (default) rows stored by (class A: length; else length
+    //          bucket 2^k, then in-degree), label = storage row: sequential
+    //          writes AND, inside every length bucket, the most-gathered
+    //          norms first. Class boundaries (4096, 512) are bucket edges, so
+    //          the class A/B/C row sets are those of the length order.
     const char* lab = std::getenv("TIERGRAPH_PR_LABEL");
-    if (lab && std::string(lab) == "rows")
+    const std::string mode = lab && lab[0] ? lab : "hybrid";
+    uint32_t* sigma = sg.order;
+    if (mode == "rows") {
       TGB_CUDA(cudaMemcpyAsync(g->old_of, sg.order, 4 * n, cudaMemcpyDeviceToDevice, ctx->stream));
-    else
+    } else if (mode == "indeg") {
       sort_ids_by_value_desc(ctx, g->indeg, n, g->old_of);
+    } else {
+      uint32_t* key = reinterpret_cast<uint32_t*>(lens);  // lens is filled later
+      hybrid_key_kernel<<<grid_for(n, 256), 256, 0, ctx->stream>>>(g->off, g->indeg, n, key);
+      TGB_LAUNCHED();
+      sort_ids_by_value_desc(ctx, key, n, g->old_of);
+      sigma = g->old_of;
+    }
     twin_labels_kernel<<<grid_for(n, 256), 256, 0, ctx->stream>>>(g->old_of, g->indeg, n,
                                                                   g->new_of, t->indeg);
     TGB_LAUNCHED();
     twin_rows_meta_kernel<<<grid_for(n, 256), 256, 0, ctx->stream>>>(
-        g->off, sg.order, g->new_of, g->indeg, n, lens, t->row_label, t->row_orig, t->deg_rows);
+        g->off, sigma, g->new_of, g->indeg, n, lens, t->row_label, t->row_orig, t->deg_rows);
     TGB_LAUNCHED();
     TGB_CUDA(cudaMemsetAsync(lens + n, 0, 8, ctx->stream));
     exclusive_scan_u64(ctx, lens, n + 1);
@@ -1184,7 +1239,7 @@ const tg_graph* relabel_twin(tg_ctx* ctx, const tg_graph* gc) {
       TGB_CUDA(cudaMemcpyAsync(&ks, k_short, 8, cudaMemcpyDeviceToHost, ctx->stream));
       ctx->sync();
       twin_rows_kernel<<<ctx->num_sms * 16, 256, 0, ctx->stream>>>(
-          g->off, g->tgt, sg.order, g->new_of, ks, n, t->off, t->tgt);
+          g->off, g->tgt, sigma, g->new_of, ks, n, t->off, t->tgt);
       TGB_LAUNCHED();
     }
     TGB_CUDA(cudaEventRecord(ev1, ctx->stream));
@@ -1221,9 +1276,10 @@ void check_config(uint32_t iterations, double damp) {  // scoring.cpp:42-47
 // every K3 launch of the run (an access-policy window on the three K3
 // streams) so the streamed targets (4 B per edge, read once) cannot evict
 // them; the lines are released when the run ends.
-// TIERGRAPH_PR_PERSIST_MB: window size in MB (0 = off); default: as large as
-// the device allows (cudaDevAttrMaxAccessPolicyWindowSize, persisting limit)
-// whenever the relabelled twin runs.
+// TIERGRAPH_PR_PERSIST_MB: window size in MB (0 = off); default: 48 MB
+// (within the device's window and persisting limits) whenever the relabelled
+// twin runs.
+constexpr long kPersistDefaultMB = 48;
 struct L2Persist {
   tg_ctx* ctx = nullptr;
   size_t bytes = 0;
@@ -1235,7 +1291,11 @@ struct L2Persist {
     cudaDeviceGetAttribute(&maxwin, cudaDevAttrMaxAccessPolicyWindowSize, ctx->device);
     cudaDeviceGetAttribute(&maxpers, cudaDevAttrMaxPersistingL2CacheSize, ctx->device);
     size_t b = std::min<size_t>(static_cast<size_t>(maxwin), static_cast<size_t>(maxpers));
-    if (want > 0) b = std::min<size_t>(b, static_cast<size_t>(want) << 20);
+    // default 48 MB: the hottest 6M norm values (~88 % of the C3 gathers);
+    // 48 MB measured better than the device maximum (10.80 vs 10.99 ms per
+    // C3 step, profiles/r02i), which leaves too little L2 for the rest
+    if (want < 0) want = kPersistDefaultMB;
+    b = std::min<size_t>(b, static_cast<size_t>(want) << 20);
     b = std::min<size_t>(b, 8 * n);
     if (b == 0) return;
     TGB_CUDA(cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, b));

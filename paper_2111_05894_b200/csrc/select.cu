@@ -354,14 +354,16 @@ static void sort_desc_u32(tg_ctx* ctx, const uint32_t* off, const uint32_t* val,
 
 // K6 without the random 8 B scatter. new_id_of[order[r]] = r over N ids is a
 // scatter of 8 B values into an 8N-byte array: at C3 (888 MB, far beyond L2)
-// every store lands in a different sector that L2 must fill from DRAM first,
-// 4.9 ms for 8.3 GB of DRAM traffic. Instead, (1) the ranks are partitioned by
-// id bucket (id >> 20, 1 Mi ids = 8 MB of new_id_of per bucket) with
-// coalesced staged writes -- bucket b's region of the pair array is exactly
-// [b << 20, ...) because every id occurs once, so no counting pass -- and (2)
-// the pairs are replayed in bucket order by the whole grid at once, so the
-// live window of new_id_of is a few MB and every sector is completed in L2
-// before it is written back.
+// every store lands in a different sector, and a partial-sector store makes L2
+// fill the sector from DRAM first: 4.9 ms for 8.3 GB of DRAM traffic. Replaying
+// bucket-partitioned pairs with the whole grid (an 8 MB live window that L2
+// holds) still cost 2.1 ms: the fills happen per partial store, not per
+// eviction. So every store must write whole sectors: (1) the (id, rank) pairs
+// are partitioned by id >> 20 with coalesced staged writes -- bucket b's region
+// of the pair array is exactly [b << 20, ...) because every id occurs once, so
+// no counting pass -- (2) again by id >> 12 inside each bucket, (3) one CTA
+// per 4,096 ids assembles their new_id_of in shared memory and stores it in
+// whole sectors. 52 B per id, all of it streamed.
 constexpr int kPmShift = 20;
 constexpr int kPmIpt = 16;
 constexpr int kPmTile = 256 * kPmIpt;
@@ -431,14 +433,87 @@ __global__ void __launch_bounds__(256) perm_part_kernel(const uint32_t* __restri
   }
 }
 
-// (2) replay in bucket order: consecutive threads take consecutive pairs
-__global__ void __launch_bounds__(256) perm_replay_kernel(const uint2* __restrict__ pairs,
-                                                          uint64_t n,
-                                                          uint64_t* __restrict__ new_id_of) {
-  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
-       i += (uint64_t)gridDim.x * blockDim.x) {
-    const uint2 p = __ldcs(pairs + i);
-    new_id_of[p.x] = p.y;
+// (2) each bucket's pairs again, by sub-bucket id >> 12 (4,096 ids, 32 KB of
+// new_id_of): a tile of pairs spans at most two buckets, so at most 512
+// sub-buckets, staged in shared memory and written out in runs; sub-bucket
+// sb's region is again exactly [sb << 12, ...).
+constexpr int kPmSubShift = 12;
+constexpr int kPmSubThreads = 512, kPmSubIpt = 16;
+constexpr int kPmSubTile = kPmSubThreads * kPmSubIpt;  // 8,192 pairs
+constexpr uint32_t kPmSubLocal = 2u << (kPmShift - kPmSubShift);  // 512: one per thread
+__global__ void __launch_bounds__(kPmSubThreads) perm_sub_kernel(const uint2* __restrict__ in,
+                                                                 uint64_t n,
+                                                                 uint2* __restrict__ out,
+                                                                 uint32_t* __restrict__ scur) {
+  extern __shared__ __align__(16) uint2 sst[];  // kPmSubTile
+  __shared__ uint32_t tcnt[kPmSubLocal], tst[kPmSubLocal], tbase[kPmSubLocal];
+  __shared__ uint32_t wsum[kPmSubThreads / 32];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  for (uint64_t t0 = (uint64_t)blockIdx.x * kPmSubTile; t0 < n;
+       t0 += (uint64_t)gridDim.x * kPmSubTile) {
+    const uint32_t tn = static_cast<uint32_t>(n - t0 < (uint64_t)kPmSubTile ? n - t0 : kPmSubTile);
+    // the tile's first bucket: pairs [t0, ...) belong to buckets t0 >> 20 and, at most, the next
+    const uint32_t sb0 = static_cast<uint32_t>(t0 >> kPmShift) << (kPmShift - kPmSubShift);
+    tcnt[threadIdx.x] = 0;
+    __syncthreads();
+    uint2 p[kPmSubIpt];
+    uint32_t rk[kPmSubIpt];
+#pragma unroll
+    for (int k = 0; k < kPmSubIpt; ++k) {
+      const uint32_t j = k * kPmSubThreads + threadIdx.x;
+      if (j < tn) {
+        p[k] = __ldcs(in + t0 + j);
+        rk[k] = atomicAdd(&tcnt[(p[k].x >> kPmSubShift) - sb0], 1u);
+      }
+    }
+    __syncthreads();
+    {  // exclusive scan of the 512 counters (one per thread) + global reservations
+      const uint32_t c = tcnt[threadIdx.x];
+      uint32_t incl = c;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += y;
+      }
+      if (lane == 31) wsum[w] = incl;
+      __syncthreads();
+      uint32_t x = incl - c;
+      for (int k = 0; k < w; ++k) x += wsum[k];
+      tst[threadIdx.x] = x;
+      if (c) tbase[threadIdx.x] = atomicAdd(&scur[sb0 + threadIdx.x], c);
+    }
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < kPmSubIpt; ++k) {
+      const uint32_t j = k * kPmSubThreads + threadIdx.x;
+      if (j < tn) sst[tst[(p[k].x >> kPmSubShift) - sb0] + rk[k]] = p[k];
+    }
+    __syncthreads();
+    for (uint32_t j = threadIdx.x; j < tn; j += blockDim.x) {
+      const uint2 q = sst[j];
+      const uint32_t lb = (q.x >> kPmSubShift) - sb0;
+      out[((uint64_t)(sb0 + lb) << kPmSubShift) + tbase[lb] + (j - tst[lb])] = q;
+    }
+    __syncthreads();
+  }
+}
+
+// (3) one CTA per sub-bucket: new_id_of of its 4,096 ids assembled in shared
+// memory, then stored as whole sectors
+__global__ void __launch_bounds__(256) perm_fill_kernel(const uint2* __restrict__ in, uint64_t n,
+                                                        uint64_t* __restrict__ new_id_of) {
+  __shared__ uint32_t r[1u << kPmSubShift];
+  const uint64_t nsb = (n + (1u << kPmSubShift) - 1) >> kPmSubShift;
+  for (uint64_t sb = blockIdx.x; sb < nsb; sb += gridDim.x) {
+    const uint64_t i0 = sb << kPmSubShift;
+    const uint32_t cnt = static_cast<uint32_t>(n - i0 < (1u << kPmSubShift) ? n - i0 : (1u << kPmSubShift));
+    for (uint32_t j = threadIdx.x; j < cnt; j += blockDim.x) {
+      const uint2 q = __ldcs(in + i0 + j);
+      r[q.x & ((1u << kPmSubShift) - 1)] = q.y;
+    }
+    __syncthreads();
+    for (uint32_t j = threadIdx.x; j < cnt; j += blockDim.x) new_id_of[i0 + j] = r[j];
+    __syncthreads();
   }
 }
 
@@ -470,11 +545,29 @@ void sort_scores(tg_ctx* ctx, const double* scores_dev, uint64_t n, uint64_t* or
     TGB_CUDA(cudaMemsetAsync(bcur, 0, 4 * nb, ctx->stream));
     // both key buffers are free after the sort; pairs (8N bytes) go in k0
     uint2* pairs = reinterpret_cast<uint2*>(k0);
-    perm_part_kernel<<<grid_for(n, kPmTile, ctx->num_sms * 8), 256, 0, ctx->stream>>>(
+    int pocc = 1;
+    TGB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&pocc, perm_part_kernel, 256, 0));
+    perm_part_kernel<<<grid_for(n, kPmTile, ctx->num_sms * std::max(pocc, 1)), 256, 0, ctx->stream>>>(
         v0, v1, plan, n, static_cast<uint32_t>(nb), order_dev, pairs, bcur);
     TGB_LAUNCHED();
-    perm_replay_kernel<<<grid_for(n, 256, ctx->num_sms * 8), 256, 0, ctx->stream>>>(pairs, n,
-                                                                                    perm_dev);
+    const uint64_t nsb = (n + (1u << kPmSubShift) - 1) >> kPmSubShift;
+    uint32_t* scur = ctx->scratch_t<uint32_t>(kScratchF, nsb);
+    TGB_CUDA(cudaMemsetAsync(scur, 0, 4 * nsb, ctx->stream));
+    uint2* pairs2 = reinterpret_cast<uint2*>(k1);
+    static bool sattr[TG_MAX_DEVICES] = {};
+    if (!sattr[ctx->device % TG_MAX_DEVICES]) {
+      TGB_CUDA(cudaFuncSetAttribute(perm_sub_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    8 * kPmSubTile));
+      sattr[ctx->device % TG_MAX_DEVICES] = true;
+    }
+    int occ = 1;
+    TGB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, perm_sub_kernel, kPmSubThreads,
+                                                           8 * kPmSubTile));
+    perm_sub_kernel<<<grid_for(n, kPmSubTile, ctx->num_sms * std::max(occ, 1)), kPmSubThreads,
+                      8 * kPmSubTile, ctx->stream>>>(pairs, n, pairs2, scur);
+    TGB_LAUNCHED();
+    perm_fill_kernel<<<grid_for(nsb, 1, ctx->num_sms * 8), 256, 0, ctx->stream>>>(pairs2, n,
+                                                                                  perm_dev);
     TGB_LAUNCHED();
   } else {
     perm_kernel<<<grid_for(n, 256), 256, 0, ctx->stream>>>(v0, v1, plan, n, order_dev, perm_dev);

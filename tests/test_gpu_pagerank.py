@@ -260,17 +260,21 @@ def test_in_degrees_large_graphs(tg, ctx, monkeypatch, n, draws, k1):
     assert np.array_equal(tg.in_degrees(g2, ctx=ctx), want2)
 
 
-@pytest.mark.parametrize("mode,cstream", [("1", "1"), ("1", "0"), ("0", "1")])
-def test_relabelled_twin_bit_exact(tg, ctx, monkeypatch, mode, cstream):
-    """K3 on the twin renumbered by in-degree (TIERGRAPH_PR_RELABEL=1, the
-    default at C3/C4 sizes) and without it (=0): raw-byte equal to the
-    reference on random, hub-row, tie-prone and R-MAT graphs, weighted and
-    plain, and the timed entry point returns the same bytes."""
+@pytest.mark.parametrize("mode,cstream,label", [("1", "1", ""), ("1", "0", ""), ("0", "1", ""),
+                                                ("1", "0", "indeg"), ("1", "0", "rows"),
+                                                ("1", "1", "indeg")])
+def test_relabelled_twin_bit_exact(tg, ctx, monkeypatch, mode, cstream, label):
+    """K3 on the relabelled twin (TIERGRAPH_PR_RELABEL=1, the default at C3/C4
+    sizes; labels by TIERGRAPH_PR_LABEL: hybrid (default), indeg, rows) and
+    without it (=0): raw-byte equal to the reference on random, hub-row,
+    tie-prone and R-MAT graphs, weighted and plain, and the timed entry point
+    returns the same bytes."""
     import ctypes as C
     from paper_2111_05894_b200._lib import LIB
     from paper_2111_05894_b200 import synth
     monkeypatch.setenv("TIERGRAPH_PR_RELABEL", mode)
     monkeypatch.setenv("TIERGRAPH_PR_CSTREAM", cstream)  # streamed class C (twin only)
+    monkeypatch.setenv("TIERGRAPH_PR_LABEL", label)
     chk, port = checker(), oracle.port()
     cases = [random_graph(port, 300 + 97 * i, 1.5 + i, 40 + i) for i in range(4)]
     cases.append(_hub_graph(60000, [(0, 40000), (31, 2049), (1000, 20000), (59999, 3000)], 3))
