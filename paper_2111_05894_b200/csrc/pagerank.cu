@@ -45,6 +45,7 @@ namespace tgb {
 constexpr uint32_t kLenA = 4096;
 constexpr uint32_t kLenAMax = 65536;
 constexpr uint32_t kLenB = 512;
+constexpr uint32_t kLenBTwin = 256;
 // class-A CTAs: 256 threads x 8 addends (2,048 per tile); 512 x 8 for the
 // rows longer than kHubLong and a quarter of the longest row (half the tiles
 // on the critical path; 1024 x 4 was measured no faster for the 77k-edge C2
@@ -922,8 +923,9 @@ __global__ void __launch_bounds__(kCsWarps * 32) pr_cstream_kernel(const PrStepA
   for (; j < nrows; j += 32) finish_row(a, k0 + j, 0.0);  // empty rows at the very end
 }
 
-// MinB: CTAs per SM the register allocation must allow (1: no cap, 68
-// registers, 3 CTAs fit; 4: <= 64 registers). TIERGRAPH_PR_MINB picks one.
+// MinB: CTAs per SM the register allocation must allow (1: no cap, 71
+// registers, 3 CTAs fit; 4: <= 64 registers). TIERGRAPH_PR_MINB=1|4 overrides
+// the default (4 on the relabelled twin, else 1).
 template <int MinB>
 __global__ void __launch_bounds__(kPrWarps * 32, MinB) pr_step_kernel(const PrStepArgs a) {
   __shared__ __align__(16) double smem[kPrWarps * 32 / kBLanes * kBStride];  // 16.6 KB: class B windows
@@ -1040,6 +1042,8 @@ void pagerank_prepare(tg_ctx* ctx, const tg_graph* g, const uint64_t* tid_dev, u
   pagerank_init(ctx, g->n, tid_dev, ntid, deg, norm0, bad, relabel);
 }
 
+bool relabel_wanted(const tg_ctx* ctx, const tg_graph* g);
+
 const tg_graph::Sched& schedule(tg_ctx* ctx, const tg_graph* g, uint64_t rb, uint64_t re) {
   auto& v = const_cast<tg_graph*>(g)->scheds;
   for (const auto& sc : v)
@@ -1054,7 +1058,11 @@ const tg_graph::Sched& schedule(tg_ctx* ctx, const tg_graph* g, uint64_t rb, uin
   const uint32_t la = ea ? static_cast<uint32_t>(std::atoi(ea))
                          : static_cast<uint32_t>(std::max<uint64_t>(
                                kLenA, std::min<uint64_t>(g->e >> 14, kLenAMax)));
-  const uint32_t lbn = eb ? static_cast<uint32_t>(std::atoi(eb)) : kLenB;
+  // class B/C bound: 512, or 256 when K3 will run on the relabelled twin
+  // (warp-staged class C over storage-consecutive rows; C3 10.1 -> 9.9 ms,
+  // profiles/r02k)
+  const uint32_t lbn = eb ? static_cast<uint32_t>(std::atoi(eb))
+                          : (whole_graph(g) && relabel_wanted(ctx, g) ? kLenBTwin : kLenB);
   class_bounds_kernel<<<1, 32, 0, ctx->stream>>>(g->off, sc.order, re - rb, la, std::min(lbn, la),
                                                  bounds);
   TGB_LAUNCHED();
@@ -1146,8 +1154,12 @@ void pagerank_step(tg_ctx* ctx, const tg_graph* g, const uint32_t* deg, double d
   const unsigned grid = static_cast<unsigned>(a.b_ctas + c_ctas);
   if (grid) {
     // classes B (first CTAs: long chains start early) and C in one grid
+    // 4 CTAs per SM (<= 64 registers) on the relabelled twin, where the
+    // classes B/C are latency-bound on L2-missing gathers (C3 step 10.8 ->
+    // 10.2 ms, profiles/r02j); 3 (71 registers) otherwise
     const char* mb = std::getenv("TIERGRAPH_PR_MINB");
-    if (mb && mb[0] == '4')
+    const bool four = mb ? mb[0] == '4' : !a.order;
+    if (four)
       pr_step_kernel<4><<<grid, kPrWarps * 32, 0, ctx->stream>>>(a);
     else
       pr_step_kernel<1><<<grid, kPrWarps * 32, 0, ctx->stream>>>(a);
