@@ -523,6 +523,12 @@ def run_ours(args):
     # ---- reordered graph -> the reference's minibatch schedule (host producer)
     t0 = time.time()
     rg = tg.reorder_graph(g, perm, ctx=ctx)
+    # the PageRank device graph (and its relabelled twin) and the sort / staging
+    # scratch are done with: free them before the largest allocations (C4:
+    # the transpose stages 2 x 15 GB of u64 CSR and sorts 1.7G edges)
+    g.release()
+    ctx.trim()
+    torch.cuda.empty_cache()
     gt = tg.transpose(rg, ctx=ctx)  # on the device (csr_graph.cpp:67-80)
     transpose_ok = None
     if world == 1 and not args.no_cpu_baseline and cfg.get("cpu_gather", True):

@@ -91,6 +91,11 @@ int tg_ctx_destroy(tg_ctx* ctx);
  * partitioned PageRank exchange (copy engines over NVLink). */
 int tg_memcpy_async(tg_ctx* ctx, void* dst, const void* src, uint64_t bytes);
 int tg_ctx_sync(tg_ctx* ctx);
+/* Synchronises the context, frees its grow-only scratch (staging buffers and
+ * sort temporaries) and returns the device pool's cached free memory to the
+ * driver: for a caller about to make one very large allocation (no
+ * reference counterpart; the reference holds no device memory). */
+int tg_ctx_trim(tg_ctx* ctx);
 void* tg_ctx_stream(tg_ctx* ctx);
 int tg_ctx_device(tg_ctx* ctx);
 /* First entry of TIERGRAPH_DEVICES ("0,1,..."), else 0. */

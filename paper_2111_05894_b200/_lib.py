@@ -60,6 +60,7 @@ SIGNATURES = {
     "tg_ctx_create_on_stream": (I32, [I32, vp, C.POINTER(vp)]),
     "tg_ctx_destroy": (I32, [vp]),
     "tg_ctx_sync": (I32, [vp]),
+    "tg_ctx_trim": (I32, [vp]),
     "tg_memcpy_async": (I32, [vp, vp, vp, U64]),
     "tg_ctx_stream": (vp, [vp]),
     "tg_ctx_device": (I32, [vp]),

@@ -251,6 +251,19 @@ int tg_ctx_destroy(tg_ctx* c) {
   return TG_OK;
 }
 
+int tg_ctx_trim(tg_ctx* c) {
+  return guard([&] {
+    DeviceGuard dg(c->device);
+    c->sync();
+    for (int i = 0; i < kNumSlots; ++i) {
+      if (c->slot_ptr[i]) TGB_CUDA(cudaFree(c->slot_ptr[i]));
+      c->slot_ptr[i] = nullptr;
+      c->slot_size[i] = 0;
+    }
+    trim_default_pool();
+  });
+}
+
 int tg_memcpy_async(tg_ctx* c, void* dst, const void* src, uint64_t bytes) {
   return guard([&] {
     if (!bytes) return;

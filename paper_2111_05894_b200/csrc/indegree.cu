@@ -21,6 +21,11 @@
 //              32,768-bin shared-memory histogram of the piece, flushed with
 //              plain coalesced stores when the bucket is one piece, with
 //              atomics when a hub bucket is split over several.
+// With thousands of buckets (C3: 3,388) a tile's runs are ~2 targets long,
+// partial sectors that L2 fills from DRAM first (C3: 9.9 GB read + 10.8 GB
+// written by the scatter for 6.1 GB of targets); a two-level partition
+// (<= 128 x <= 32 buckets, per-tile cursor reservations) removed the fills
+// but its two passes took 7.7 ms each (profiles/r02n), so one level stays.
 // Traffic: 4 B x E read (1), 8 B x E (3), 4 B x E (4), 4 B x N written —
 // 16 B per edge against the 4 B per edge of the one-pass form, in exchange
 // for shared-memory instead of L2 atomics. The counts are exact integers
@@ -253,6 +258,7 @@ bool compute_indeg_binned(tg_ctx* ctx, const uint32_t* tgt, uint64_t e, uint64_t
     return false;
   const uint32_t nb = static_cast<uint32_t>(nb64);
   static bool attr[TG_MAX_DEVICES] = {};
+
   const size_t scat_smem = 4 * (kK1Tile + 3 * (size_t)nb);
   if (!attr[ctx->device % TG_MAX_DEVICES]) {
     TGB_CUDA(cudaFuncSetAttribute(k1_scatter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -275,7 +281,7 @@ bool compute_indeg_binned(tg_ctx* ctx, const uint32_t* tgt, uint64_t e, uint64_t
   const uint64_t max_items = nb + e / kK1Piece + 1;
   const size_t bytes = 4 * e + 16 + 8 * ncnt + 16 + sizeof(K1Item) * max_items + 64;
   char* base = nullptr;
-  if (cudaMallocAsync(reinterpret_cast<void**>(&base), bytes, ctx->stream) != cudaSuccess) {
+  if (tgb::dev_malloc_async(reinterpret_cast<void**>(&base), bytes, ctx->stream) != cudaSuccess) {
     cudaGetLastError();
     return false;
   }

@@ -30,6 +30,41 @@ inline void cuda_check(cudaError_t e, const char* what) {
 }
 #define TGB_CUDA(x) ::tgb::cuda_check((x), #x)
 
+// Device allocations that survive the memory pool's cache: the library
+// keeps freed stream-ordered temporaries mapped in the device's default pool
+// (capi.cu, TIERGRAPH_POOL_KEEP_MB), which plain cudaMalloc and the next large
+// cudaMallocAsync cannot use. On an out-of-memory error the pool is trimmed
+// to zero (after a device synchronise, so pending frees have landed) and the
+// allocation is retried once.
+inline void trim_default_pool() {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceSynchronize();
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) cudaMemPoolTrimTo(pool, 0);
+  cudaGetLastError();
+}
+template <typename T>
+inline cudaError_t dev_malloc(T** p, size_t bytes) {
+  cudaError_t e = cudaMalloc(p, bytes);
+  if (e == cudaErrorMemoryAllocation) {
+    cudaGetLastError();
+    trim_default_pool();
+    e = cudaMalloc(p, bytes);
+  }
+  return e;
+}
+template <typename T>
+inline cudaError_t dev_malloc_async(T** p, size_t bytes, cudaStream_t s) {
+  cudaError_t e = cudaMallocAsync(p, bytes, s);
+  if (e == cudaErrorMemoryAllocation) {
+    cudaGetLastError();
+    trim_default_pool();
+    e = cudaMallocAsync(p, bytes, s);
+  }
+  return e;
+}
+
 extern std::atomic<uint64_t> g_launches;
 inline void count_launch(int n = 1) { g_launches.fetch_add(n, std::memory_order_relaxed); }
 // Check the launch itself (configuration errors); execution errors surface at
@@ -115,7 +150,7 @@ struct tg_ctx {
         slot_size[slot] = 0;
       }
       size_t sz = bytes + bytes / 8;
-      tgb::cuda_check(cudaMalloc(&slot_ptr[slot], sz), "scratch alloc");
+      tgb::cuda_check(tgb::dev_malloc(&slot_ptr[slot], sz), "scratch alloc");
       slot_size[slot] = sz;
     }
     return slot_ptr[slot];

@@ -189,8 +189,8 @@ int tg_graph_load_csrg(tg_ctx* ctx, const char* path, tg_graph** out) {
     // offsets: whole array to the device (u64), narrowed + validated there
     uint64_t* off64 = nullptr;
     uint32_t* tgt32 = nullptr;
-    TGB_CUDA(cudaMallocAsync(&off64, 8 * (n + 1), ctx->stream));
-    TGB_CUDA(cudaMalloc(&tgt32, 4 * std::max<uint64_t>(e, 1) + 16));  // +16: K3 reads 16 B target groups
+    TGB_CUDA(tgb::dev_malloc_async(&off64, 8 * (n + 1), ctx->stream));
+    TGB_CUDA(tgb::dev_malloc(&tgt32, 4 * std::max<uint64_t>(e, 1) + 16));  // +16: K3 reads 16 B target groups
     auto* bad = ctx->scratch_t<unsigned long long>(kSmall, 1);
     TGB_CUDA(cudaMemsetAsync(bad, 0xff, 8, ctx->stream));
     {

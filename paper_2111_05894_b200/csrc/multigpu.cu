@@ -158,7 +158,7 @@ int tg_mgraph_create(tg_ctx* const* ctxs, uint32_t ndev, const uint64_t* offsets
         const int rc = tg_graph_create_rows(ctxs[r], offsets, targets, n, e, m->bounds[r],
                                             m->bounds[r + 1], &m->g[r]);
         if (rc != TG_OK) throw Error(rc, tg_last_error());
-        TGB_CUDA(cudaMalloc(&m->indeg[r], 4 * std::max<uint64_t>(n, 1)));
+        TGB_CUDA(tgb::dev_malloc(&m->indeg[r], 4 * std::max<uint64_t>(n, 1)));
         TGB_CUDA(cudaEventCreateWithFlags(&m->ev[r], cudaEventDisableTiming));
       }
       // K1 all-reduce: partial counts -> device 0 (sum) -> every device

@@ -781,6 +781,10 @@ __device__ __forceinline__ void thread_row(const PrStepArgs& a, uint32_t r) {
 // row's part of the chunk in storage order (scoring.cpp:66-68) -- the same
 // left-to-right chain per row as thread_row, with coalesced target traffic.
 constexpr int kCWin = 256;  // edges per chunk (8 per lane)
+// Pipe: the next chunk's gathers are issued before the lanes chain the
+// current chunk (from shared memory), so they overlap the chain instead of
+// starting after it.
+template <bool Pipe>
 __device__ __forceinline__ void warp_rows_staged(const PrStepArgs& a, uint64_t k0, double* buf) {
   const int lane = threadIdx.x & 31;
   const uint64_t kend = min(k0 + 32, a.row_end);
@@ -799,18 +803,38 @@ __device__ __forceinline__ void warp_rows_staged(const PrStepArgs& a, uint64_t k
     tn[q] = j < total ? __ldcs(t + j) : 0xffffffffu;
   }
   double acc = 0.0;  // scoring.cpp:67
-  for (uint32_t base = 0; base < total; base += kCWin) {
-    double v[K];
+  double v[K];
+  if (Pipe) {
 #pragma unroll
     for (int q = 0; q < K; ++q) v[q] = tn[q] != 0xffffffffu ? __ldg(a.norm_in + tn[q]) : 0.0;
 #pragma unroll
-    for (int q = 0; q < K; ++q) {  // next chunk's targets in flight
-      const uint32_t j = base + kCWin + q * 32 + lane;
+    for (int q = 0; q < K; ++q) {
+      const uint32_t j = kCWin + q * 32 + lane;
       tn[q] = j < total ? __ldcs(t + j) : 0xffffffffu;
+    }
+  }
+  for (uint32_t base = 0; base < total; base += kCWin) {
+    if (!Pipe) {
+#pragma unroll
+      for (int q = 0; q < K; ++q) v[q] = tn[q] != 0xffffffffu ? __ldg(a.norm_in + tn[q]) : 0.0;
+#pragma unroll
+      for (int q = 0; q < K; ++q) {  // next chunk's targets in flight
+        const uint32_t j = base + kCWin + q * 32 + lane;
+        tn[q] = j < total ? __ldcs(t + j) : 0xffffffffu;
+      }
     }
 #pragma unroll
     for (int q = 0; q < K; ++q) buf[q * 32 + lane] = v[q];
     __syncwarp();
+    if (Pipe) {  // the next chunk's gathers, then the chunk after's targets
+#pragma unroll
+      for (int q = 0; q < K; ++q) v[q] = tn[q] != 0xffffffffu ? __ldg(a.norm_in + tn[q]) : 0.0;
+#pragma unroll
+      for (int q = 0; q < K; ++q) {
+        const uint32_t j = base + 2 * kCWin + q * 32 + lane;
+        tn[q] = j < total ? __ldcs(t + j) : 0xffffffffu;
+      }
+    }
     const uint32_t lo = max(rb, base), hi = min(re, base + kCWin);
     for (uint32_t j = lo; j < hi; ++j) acc = __dadd_rn(acc, buf[j - base]);  // in order
     __syncwarp();
@@ -926,7 +950,7 @@ __global__ void __launch_bounds__(kCsWarps * 32) pr_cstream_kernel(const PrStepA
 // MinB: CTAs per SM the register allocation must allow (1: no cap, 71
 // registers, 3 CTAs fit; 4: <= 64 registers). TIERGRAPH_PR_MINB=1|4 overrides
 // the default (4 on the relabelled twin, else 1).
-template <int MinB>
+template <int MinB, bool Pipe>
 __global__ void __launch_bounds__(kPrWarps * 32, MinB) pr_step_kernel(const PrStepArgs a) {
   __shared__ __align__(16) double smem[kPrWarps * 32 / kBLanes * kBStride];  // 16.6 KB: class B windows
   if (blockIdx.x < a.b_ctas) {
@@ -937,7 +961,7 @@ __global__ void __launch_bounds__(kPrWarps * 32, MinB) pr_step_kernel(const PrSt
     // storage-sorted twin: 32 consecutive rows per warp, staged chunks
     const int w = threadIdx.x >> 5;
     const uint64_t k0 = a.row_begin + a.nB + ((uint64_t)(blockIdx.x - a.b_ctas) * kPrWarps + w) * 32;
-    warp_rows_staged(a, k0, smem + w * kCWin);
+    warp_rows_staged<Pipe>(a, k0, smem + w * kCWin);
   } else {
     const uint64_t i = a.nB + (uint64_t)(blockIdx.x - a.b_ctas) * blockDim.x + threadIdx.x;
     if (i < a.m) thread_row(a, a.order[i]);
@@ -1049,7 +1073,7 @@ const tg_graph::Sched& schedule(tg_ctx* ctx, const tg_graph* g, uint64_t rb, uin
   for (const auto& sc : v)
     if (sc.rb == rb && sc.re == re) return sc;
   tg_graph::Sched sc{rb, re, nullptr, 0, 0, 0};
-  TGB_CUDA(cudaMalloc(&sc.order, sizeof(uint32_t) * std::max<uint64_t>(re - rb, 1) + 16));
+  TGB_CUDA(tgb::dev_malloc(&sc.order, sizeof(uint32_t) * std::max<uint64_t>(re - rb, 1) + 16));
   sort_rows_by_length(ctx, g->off, rb, re, sc.order);
   uint32_t* bounds = sc.order + std::max<uint64_t>(re - rb, 1);
   // TIERGRAPH_PR_LENA / _LENB override the class boundaries (experiments)
@@ -1159,10 +1183,16 @@ void pagerank_step(tg_ctx* ctx, const tg_graph* g, const uint32_t* deg, double d
     // 10.2 ms, profiles/r02j); 3 (71 registers) otherwise
     const char* mb = std::getenv("TIERGRAPH_PR_MINB");
     const bool four = mb ? mb[0] == '4' : !a.order;
-    if (four)
-      pr_step_kernel<4><<<grid, kPrWarps * 32, 0, ctx->stream>>>(a);
+    const char* cp = std::getenv("TIERGRAPH_PR_CPIPE");  // pipelined class C (twin)
+    const bool pipe = cp && cp[0] == '1';
+    if (four && pipe)
+      pr_step_kernel<4, true><<<grid, kPrWarps * 32, 0, ctx->stream>>>(a);
+    else if (four)
+      pr_step_kernel<4, false><<<grid, kPrWarps * 32, 0, ctx->stream>>>(a);
+    else if (pipe)
+      pr_step_kernel<1, true><<<grid, kPrWarps * 32, 0, ctx->stream>>>(a);
     else
-      pr_step_kernel<1><<<grid, kPrWarps * 32, 0, ctx->stream>>>(a);
+      pr_step_kernel<1, false><<<grid, kPrWarps * 32, 0, ctx->stream>>>(a);
     TGB_LAUNCHED();
   }
   if (sc.nA || cs) ctx->join();
@@ -1197,15 +1227,15 @@ const tg_graph* relabel_twin(tg_ctx* ctx, const tg_graph* gc) {
   uint64_t* lens = nullptr;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   try {
-    TGB_CUDA(cudaMalloc(&g->old_of, 4 * n));
-    TGB_CUDA(cudaMalloc(&g->new_of, 4 * n));
-    TGB_CUDA(cudaMalloc(&t->off, 4 * (n + 1)));
-    TGB_CUDA(cudaMalloc(&t->tgt, 4 * std::max<uint64_t>(e, 1) + 16));  // +16: K3 reads 16 B target groups
-    TGB_CUDA(cudaMalloc(&t->indeg, 4 * n));
-    TGB_CUDA(cudaMalloc(&t->row_label, 4 * n));
-    TGB_CUDA(cudaMalloc(&t->row_orig, 4 * n));
-    TGB_CUDA(cudaMalloc(&t->deg_rows, 4 * n));
-    TGB_CUDA(cudaMalloc(&lens, 8 * (n + 1) + 16));
+    TGB_CUDA(tgb::dev_malloc(&g->old_of, 4 * n));
+    TGB_CUDA(tgb::dev_malloc(&g->new_of, 4 * n));
+    TGB_CUDA(tgb::dev_malloc(&t->off, 4 * (n + 1)));
+    TGB_CUDA(tgb::dev_malloc(&t->tgt, 4 * std::max<uint64_t>(e, 1) + 16));  // +16: K3 reads 16 B target groups
+    TGB_CUDA(tgb::dev_malloc(&t->indeg, 4 * n));
+    TGB_CUDA(tgb::dev_malloc(&t->row_label, 4 * n));
+    TGB_CUDA(tgb::dev_malloc(&t->row_orig, 4 * n));
+    TGB_CUDA(tgb::dev_malloc(&t->deg_rows, 4 * n));
+    TGB_CUDA(tgb::dev_malloc(&lens, 8 * (n + 1) + 16));
     TGB_CUDA(cudaEventCreate(&ev0));
     TGB_CUDA(cudaEventCreate(&ev1));
     TGB_CUDA(cudaEventRecord(ev0, ctx->stream));
@@ -1414,7 +1444,7 @@ void graph_from_device(tg_ctx* ctx, const uint64_t* doff, uint32_t* tgt, uint64_
   g->re = n;
   g->tgt = tgt;  // owned from here on
   try {
-    TGB_CUDA(cudaMalloc(&g->off, sizeof(uint32_t) * (n + 1)));
+    TGB_CUDA(tgb::dev_malloc(&g->off, sizeof(uint32_t) * (n + 1)));
     auto* bad = ctx->scratch_t<unsigned long long>(kSmall, 2);
     TGB_CUDA(cudaMemsetAsync(bad, 0xff, sizeof(unsigned long long), ctx->stream));
     narrow_offsets_kernel<<<grid_for(n + 1, 256), 256, 0, ctx->stream>>>(doff, g->off, n, e, bad);
@@ -1426,7 +1456,7 @@ void graph_from_device(tg_ctx* ctx, const uint64_t* doff, uint32_t* tgt, uint64_
       format_error("csr: offsets invalid at index " + std::to_string(hb) +
                    " (need offsets[0]==0, monotone, offsets[num_nodes]==num_edges)");
     if (n) schedule(ctx, g, 0, n);  // K3 schedule of the whole graph
-    TGB_CUDA(cudaMalloc(&g->indeg, sizeof(uint32_t) * std::max<uint64_t>(n, 1)));
+    TGB_CUDA(tgb::dev_malloc(&g->indeg, sizeof(uint32_t) * std::max<uint64_t>(n, 1)));
     compute_indeg(ctx, g, g->indeg);
     ctx->sync();
   } catch (...) {
@@ -1449,7 +1479,7 @@ int tg_graph_create(tg_ctx* ctx, const uint64_t* offsets, const uint64_t* target
       domain_error("tg_graph_create: n and e must be < 2^32 for the u32 device layout");
     DeviceGuard dg(ctx->device);
     uint32_t* tgt = nullptr;
-    TGB_CUDA(cudaMalloc(&tgt, sizeof(uint32_t) * std::max<uint64_t>(e, 1) + 16));  // +16: K3 reads 16 B target groups
+    TGB_CUDA(tgb::dev_malloc(&tgt, sizeof(uint32_t) * std::max<uint64_t>(e, 1) + 16));  // +16: K3 reads 16 B target groups
     try {
       auto* bad = ctx->scratch_t<unsigned long long>(kSmall, 2);
       TGB_CUDA(cudaMemsetAsync(bad + 1, 0xff, sizeof(unsigned long long), ctx->stream));
@@ -1531,10 +1561,10 @@ int tg_graph_create_rows(tg_ctx* ctx, const uint64_t* offsets, const uint64_t* t
     try {
       std::vector<uint32_t> o32(m + 1);
       for (uint64_t i = 0; i <= m; ++i) o32[i] = static_cast<uint32_t>(ho[i] - e0);
-      TGB_CUDA(cudaMalloc(&g->off_alloc, 4 * (m + 1)));
+      TGB_CUDA(tgb::dev_malloc(&g->off_alloc, 4 * (m + 1)));
       TGB_CUDA(cudaMemcpy(g->off_alloc, o32.data(), 4 * (m + 1), cudaMemcpyHostToDevice));
       g->off = g->off_alloc - row_begin;  // off[r] for r in [row_begin, row_end]
-      TGB_CUDA(cudaMalloc(&g->tgt, 4 * std::max<uint64_t>(g->e, 1) + 16));  // +16: K3 reads 16 B target groups
+      TGB_CUDA(tgb::dev_malloc(&g->tgt, 4 * std::max<uint64_t>(g->e, 1) + 16));  // +16: K3 reads 16 B target groups
       auto* bad = ctx->scratch_t<unsigned long long>(kSmall, 2);
       TGB_CUDA(cudaMemsetAsync(bad + 1, 0xff, 8, ctx->stream));
       const bool tdev = is_device_ptr(targets);
@@ -1556,7 +1586,7 @@ int tg_graph_create_rows(tg_ctx* ctx, const uint64_t* offsets, const uint64_t* t
       ctx->sync();
       if (hb != ~0ull) format_error("csr: target out of range at edge " + std::to_string(hb));
       if (m) schedule(ctx, g, row_begin, row_end);
-      TGB_CUDA(cudaMalloc(&g->indeg, 4 * std::max<uint64_t>(n, 1)));
+      TGB_CUDA(tgb::dev_malloc(&g->indeg, 4 * std::max<uint64_t>(n, 1)));
       compute_indeg(ctx, g, g->indeg);  // partial: this block's edges only
       ctx->sync();
     } catch (...) {

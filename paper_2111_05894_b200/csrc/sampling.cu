@@ -394,7 +394,7 @@ void ensure(uint32_t** p, uint64_t* cap, uint64_t want) {
   cudaFree(*p);
   *p = nullptr;
   want = std::max<uint64_t>(want, 1024);
-  TGB_CUDA(cudaMalloc(p, sizeof(uint32_t) * want));
+  TGB_CUDA(tgb::dev_malloc(p, sizeof(uint32_t) * want));
   *cap = want;
 }
 
@@ -416,14 +416,14 @@ uint32_t sampler_lanes() {
 
 // Per-state device buffers (layer stamps, member bits, counters).
 void sampler_alloc(tg_sampler* s) {
-  TGB_CUDA(cudaMalloc(&s->layer_mark, 4 * std::max<uint64_t>(s->n, 1)));
+  TGB_CUDA(tgb::dev_malloc(&s->layer_mark, 4 * std::max<uint64_t>(s->n, 1)));
   s->nwords = std::max<uint64_t>((s->n + 31) / 32, 1);
-  TGB_CUDA(cudaMalloc(&s->member_bits, 4 * s->nwords));
+  TGB_CUDA(tgb::dev_malloc(&s->member_bits, 4 * s->nwords));
   TGB_CUDA(cudaMemsetAsync(s->layer_mark, 0, 4 * std::max<uint64_t>(s->n, 1), s->stream));
   TGB_CUDA(cudaMemsetAsync(s->member_bits, 0, 4 * s->nwords, s->stream));
-  TGB_CUDA(cudaMalloc(&s->small, 256));
+  TGB_CUDA(tgb::dev_malloc(&s->small, 256));
   const uint64_t nblk = (s->nwords + kCompactBlock - 1) / kCompactBlock;
-  TGB_CUDA(cudaMalloc(&s->blk, 4 * std::max<uint64_t>(nblk, 1)));
+  TGB_CUDA(tgb::dev_malloc(&s->blk, 4 * std::max<uint64_t>(nblk, 1)));
 }
 
 }  // namespace
@@ -465,7 +465,7 @@ int tg_sampler_create_tiered(tg_ctx* ctx, const tg_sgraph* sg, tg_sampler** out)
     s->n = sg->n;
     s->sg = sg;
     try {
-      TGB_CUDA(cudaMalloc(&s->reads, 3 * sizeof(unsigned long long)));
+      TGB_CUDA(tgb::dev_malloc(&s->reads, 3 * sizeof(unsigned long long)));
       TGB_CUDA(cudaMemsetAsync(s->reads, 0, 3 * sizeof(unsigned long long), s->stream));
       s->g = sg->view();
       s->g.reads = s->reads;

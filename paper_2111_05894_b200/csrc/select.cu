@@ -41,8 +41,24 @@ __device__ __forceinline__ uint64_t score_key(double s) {
   return ~b;
 }
 
-// K4: validate (scoring.cpp:105-107), build keys/ids, and all 8 digit histograms.
+// K4a: the smallest key (kmin). Sorting key - kmin orders and ties exactly
+// like key, and digits above the top bit of (kmax - kmin) become constant
+// zero, so the planner skips their passes: scores spanning fewer than 2^4
+// binades need 7 passes instead of 8.
+__global__ void __launch_bounds__(256) key_min_kernel(const double* __restrict__ s, uint64_t n,
+                                                      unsigned long long* kmin) {
+  unsigned long long m = ~0ull;
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+       i += (uint64_t)gridDim.x * blockDim.x)
+    m = min(m, (unsigned long long)score_key(__ldcs(s + i)));
+#pragma unroll
+  for (int o = 16; o; o >>= 1) m = min(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if ((threadIdx.x & 31) == 0) atomicMin(kmin, m);
+}
+
+// K4: validate (scoring.cpp:105-107), build keys (- kmin)/ids, and all 8 digit histograms.
 __global__ void __launch_bounds__(256) key_prep_kernel(const double* __restrict__ s, uint64_t n,
+                                                       const unsigned long long* __restrict__ kmin,
                                                        uint64_t* __restrict__ keys,
                                                        uint32_t* __restrict__ vals,
                                                        uint32_t* __restrict__ hist,
@@ -54,7 +70,7 @@ __global__ void __launch_bounds__(256) key_prep_kernel(const double* __restrict_
        i += (uint64_t)gridDim.x * blockDim.x) {
     const double v = s[i];
     if (!(isfinite(v) && v >= 0.0)) atomicMin(bad, (unsigned long long)i);
-    const uint64_t k = score_key(v);
+    const uint64_t k = score_key(v) - *kmin;
     keys[i] = k;
     vals[i] = static_cast<uint32_t>(i);
 #pragma unroll
@@ -245,7 +261,7 @@ void radix_passes(tg_ctx* ctx, uint64_t* k0, uint32_t* v0, uint64_t* k1, uint32_
   const uint32_t nblk = static_cast<uint32_t>((n + kRsTile - 1) / kRsTile);
   uint64_t* status = nullptr;
   const size_t sbytes = 8ull * 256 * nblk;
-  TGB_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&status), sbytes + 64, ctx->stream));
+  TGB_CUDA(tgb::dev_malloc_async(reinterpret_cast<void**>(&status), sbytes + 64, ctx->stream));
   auto* ctr = reinterpret_cast<uint32_t*>(reinterpret_cast<char*>(status) + sbytes);
   TGB_CUDA(cudaMemsetAsync(ctr, 0, 64, ctx->stream));
   for (int p = 0; p < passes; ++p) {
@@ -331,7 +347,7 @@ static void sort_desc_u32(tg_ctx* ctx, const uint32_t* off, const uint32_t* val,
   // context's scratch slots across this call
   const size_t bytes = 2 * 8 * m + 2 * 4 * m + 64 + sizeof(RadixPlan) + 8 * 256 * 4 + 256;
   char* base = nullptr;
-  TGB_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&base), bytes, ctx->stream));
+  TGB_CUDA(tgb::dev_malloc_async(reinterpret_cast<void**>(&base), bytes, ctx->stream));
   auto align = [](char* p) { return reinterpret_cast<char*>((reinterpret_cast<uintptr_t>(p) + 15) & ~uintptr_t(15)); };
   char* p = base;
   uint64_t* k0 = reinterpret_cast<uint64_t*>(p); p = align(p + 8 * m);
@@ -533,7 +549,11 @@ void sort_scores(tg_ctx* ctx, const double* scores_dev, uint64_t n, uint64_t* or
   auto* hist = reinterpret_cast<uint32_t*>(small + 64 + sizeof(RadixPlan));
   TGB_CUDA(cudaMemsetAsync(bad, 0xff, 8, ctx->stream));
   TGB_CUDA(cudaMemsetAsync(hist, 0, 8 * 256 * 4, ctx->stream));
-  key_prep_kernel<<<grid_for(n, 256, ctx->num_sms * 8), 256, 0, ctx->stream>>>(scores_dev, n, k0,
+  auto* kmin = reinterpret_cast<unsigned long long*>(small) + 1;
+  TGB_CUDA(cudaMemsetAsync(kmin, 0xff, 8, ctx->stream));
+  key_min_kernel<<<grid_for(n, 256, ctx->num_sms * 8), 256, 0, ctx->stream>>>(scores_dev, n, kmin);
+  TGB_LAUNCHED();
+  key_prep_kernel<<<grid_for(n, 256, ctx->num_sms * 8), 256, 0, ctx->stream>>>(scores_dev, n, kmin, k0,
                                                                                v0, hist, bad);
   TGB_LAUNCHED();
   plan_kernel<<<1, 256, 0, ctx->stream>>>(hist, n, plan);
@@ -650,7 +670,7 @@ void transpose_device(tg_ctx* ctx, const uint64_t* off, const uint64_t* tgt, uin
   }
   const size_t bytes = 2 * 8 * e + 2 * 4 * e + 64 + sizeof(RadixPlan) + 8 * 256 * 4 + 256;
   char* base = nullptr;
-  TGB_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&base), bytes, ctx->stream));
+  TGB_CUDA(tgb::dev_malloc_async(reinterpret_cast<void**>(&base), bytes, ctx->stream));
   auto align = [](char* p) { return reinterpret_cast<char*>((reinterpret_cast<uintptr_t>(p) + 15) & ~uintptr_t(15)); };
   char* p = base;
   uint64_t* k0 = reinterpret_cast<uint64_t*>(p); p = align(p + 8 * e);

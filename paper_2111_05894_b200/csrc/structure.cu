@@ -163,12 +163,12 @@ int tg_sgraph_create(tg_ctx* ctx, const tg_layout* layout, uint32_t device_index
       auto* bad = ctx->scratch_t<unsigned long long>(kSmall, 2);
       TGB_CUDA(cudaMemsetAsync(bad, 0xff, 2 * sizeof(unsigned long long), ctx->stream));
       // offsets -> u32 on this device (every device holds them)
-      TGB_CUDA(cudaMalloc(&s->off, 4 * (n + 1)));
+      TGB_CUDA(tgb::dev_malloc(&s->off, 4 * (n + 1)));
       const uint64_t* doff = dev_in(ctx, offsets, n + 1, kStageIn0);
       sg_narrow_offsets<<<grid_for(n + 1, 256), 256, 0, ctx->stream>>>(doff, s->off, n, e, bad);
       TGB_LAUNCHED();
       // the transient u32 copy of every neighbour id (range-checked)
-      TGB_CUDA(cudaMalloc(&tmp, 4 * std::max<uint64_t>(e, 1)));
+      TGB_CUDA(tgb::dev_malloc(&tmp, 4 * std::max<uint64_t>(e, 1)));
       const bool tdev = is_device_ptr(targets);
       const uint64_t chunk = tdev ? std::max<uint64_t>(e, 1) : (32ull << 20);
       for (uint64_t base = 0; base < e; base += chunk) {
@@ -194,15 +194,15 @@ int tg_sgraph_create(tg_ctx* ctx, const tg_layout* layout, uint32_t device_index
       TGB_CUDA(cudaMemcpy(&off_lb, s->off + lb, 4, cudaMemcpyDeviceToHost));
       TGB_CUDA(cudaMemcpy(&off_mb, s->off + mb, 4, cudaMemcpyDeviceToHost));
       // [0, lb): replicated
-      TGB_CUDA(cudaMalloc(&s->rep, 4 * std::max<uint64_t>(off_lb, 1)));
+      TGB_CUDA(tgb::dev_malloc(&s->rep, 4 * std::max<uint64_t>(off_lb, 1)));
       if (off_lb)
         TGB_CUDA(cudaMemcpyAsync(s->rep, tmp, 4ull * off_lb, cudaMemcpyDeviceToDevice, ctx->stream));
       // [lb, mb): slice starts from one scan over (device, slot)-ordered lengths
       const uint64_t inter = mb - lb, S = (inter + D - 1) / D;
-      TGB_CUDA(cudaMalloc(&s->ilv_start, 4 * std::max<uint64_t>(inter, 1)));
+      TGB_CUDA(tgb::dev_malloc(&s->ilv_start, 4 * std::max<uint64_t>(inter, 1)));
       if (inter) {
         const uint64_t m = static_cast<uint64_t>(D) * S + 1;
-        TGB_CUDA(cudaMalloc(&lens, 8 * m));
+        TGB_CUDA(tgb::dev_malloc(&lens, 8 * m));
         sg_class_lengths<<<grid_for(m, 256), 256, 0, ctx->stream>>>(s->off, lb, mb, D, S, lens);
         TGB_LAUNCHED();
         exclusive_scan_u64(ctx, lens, m);
@@ -215,7 +215,7 @@ int tg_sgraph_create(tg_ctx* ctx, const tg_layout* layout, uint32_t device_index
         ctx->sync();
         s->slice_len = se[1] - se[0];
       }
-      TGB_CUDA(cudaMalloc(&s->slice, 4 * std::max<uint64_t>(s->slice_len, 1)));
+      TGB_CUDA(tgb::dev_malloc(&s->slice, 4 * std::max<uint64_t>(s->slice_len, 1)));
       if (s->slice_len) {
         sg_fill_slice<<<grid_for((S + 7) / 8, 1, ctx->num_sms * 8), 256, 0, ctx->stream>>>(
             s->off, tmp, lb, mb, D, device_index, s->ilv_start, s->slice);

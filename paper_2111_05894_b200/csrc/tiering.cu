@@ -1121,8 +1121,8 @@ int tg_store_create(tg_ctx* ctx, const tg_layout* layout, uint32_t device_index,
     const uint64_t mine = inter > device_index ? (inter - device_index + D - 1) / D : 0;
     s->local_rows = lb + mine;
     try {
-      TGB_CUDA(cudaMalloc(&s->local, std::max<uint64_t>(s->local_rows * s->R, 16)));
-      TGB_CUDA(cudaMalloc(&s->counters, 64));
+      TGB_CUDA(tgb::dev_malloc(&s->local, std::max<uint64_t>(s->local_rows * s->R, 16)));
+      TGB_CUDA(tgb::dev_malloc(&s->counters, 64));
       // [0..2] counters, [3] first bad index (~0 = none), [4] CTA ticket
       TGB_CUDA(cudaMemsetAsync(s->counters, 0, 64, ctx->stream));
       TGB_CUDA(cudaMemsetAsync(s->counters + 3, 0xff, 8, ctx->stream));
@@ -1244,7 +1244,7 @@ const uint8_t* ensure_cold_tier(tg_store* s) {
     s->cold_head = s->R / 128 * 128;
     s->cold_stride = s->cold_head;
     if (!s->own_cold_tail) {
-      TGB_CUDA(cudaMalloc(&s->cold_tail, std::max<uint64_t>(cold * (s->R - s->cold_head), 16)));
+      TGB_CUDA(tgb::dev_malloc(&s->cold_tail, std::max<uint64_t>(cold * (s->R - s->cold_head), 16)));
       s->own_cold_tail = true;
     }
   }
@@ -1298,7 +1298,7 @@ void place_impl(tg_store* s, const void* src_rows, uint64_t src_nrows, const uin
     // the caller's rows are read in place through the row map
     const uint64_t cold = N - mb;
     if (!s->cold_src) {
-      TGB_CUDA(cudaMalloc(&s->cold_src, sizeof(uint32_t) * std::max<uint64_t>(cold, 1)));
+      TGB_CUDA(tgb::dev_malloc(&s->cold_src, sizeof(uint32_t) * std::max<uint64_t>(cold, 1)));
       s->own_cold_src = true;
     }
     if (cold)
@@ -1539,7 +1539,7 @@ int tg_ipc_close_handle(void* p) {
 int tg_device_alloc(tg_ctx* ctx, uint64_t bytes, void** out) {
   return guard([&] {
     DeviceGuard dg(ctx->device);
-    TGB_CUDA(cudaMalloc(out, std::max<uint64_t>(bytes, 16)));
+    TGB_CUDA(tgb::dev_malloc(out, std::max<uint64_t>(bytes, 16)));
     TGB_CUDA(cudaMemsetAsync(*out, 0, std::max<uint64_t>(bytes, 16), ctx->stream));
     ctx->sync();
   });

@@ -144,6 +144,10 @@ class Context:
     def sync(self):
         _check(LIB.tg_ctx_sync(self.h))
 
+    def trim(self):
+        """Free the context's scratch and the device pool's cached memory."""
+        _check(LIB.tg_ctx_trim(self.h))
+
     @property
     def stream_ptr(self) -> int:
         return int(LIB.tg_ctx_stream(self.h) or 0)

@@ -232,13 +232,14 @@ def test_fused_peer_exchange_virtual_ranks(tg, ctx, ranks):
 
 
 @pytest.mark.parametrize("k1", ["", "atomic"])
-@pytest.mark.parametrize("n,draws", [(200_000, 5_000_000), (1_500_000, 6_000_000)])
+@pytest.mark.parametrize("n,draws", [(200_000, 5_000_000), (1_500_000, 6_000_000),
+                                     (6_000_000, 8_000_000)])
 def test_in_degrees_large_graphs(tg, ctx, monkeypatch, n, draws, k1):
     """K1 on graphs with >= 4M edges (R-MAT hubs, privatised low ids, one id
     holding 1.5M edges) equals csr_graph.cpp:89-93 exactly, in both forms:
     binned (partition + shared-memory histograms, the default at these sizes;
-    the 1.5M-edge bucket is split over two histogram pieces) and one-pass
-    atomic (TIERGRAPH_K1=atomic)."""
+    the 1.5M-edge bucket is split over two histogram pieces; 184 buckets at
+    6M nodes) and one-pass atomic (TIERGRAPH_K1=atomic)."""
     from paper_2111_05894_b200 import synth
     if k1:
         monkeypatch.setenv("TIERGRAPH_K1", k1)
