@@ -286,6 +286,7 @@ struct PrStepArgs {
   const uint32_t* order;   // the range's rows by length, descending
   uint32_t nA, nB, m;      // class boundaries in `order`, range size
   uint32_t b_ctas;         // CTAs of class B (then class C)
+  uint64_t c_end;          // end (absolute row) of the class-C rows (twin: first empty row)
   uint64_t row_begin, row_end;
   double base, damp;
   int last;
@@ -781,13 +782,9 @@ __device__ __forceinline__ void thread_row(const PrStepArgs& a, uint32_t r) {
 // row's part of the chunk in storage order (scoring.cpp:66-68) -- the same
 // left-to-right chain per row as thread_row, with coalesced target traffic.
 constexpr int kCWin = 256;  // edges per chunk (8 per lane)
-// Pipe: the next chunk's gathers are issued before the lanes chain the
-// current chunk (from shared memory), so they overlap the chain instead of
-// starting after it.
-template <bool Pipe>
 __device__ __forceinline__ void warp_rows_staged(const PrStepArgs& a, uint64_t k0, double* buf) {
   const int lane = threadIdx.x & 31;
-  const uint64_t kend = min(k0 + 32, a.row_end);
+  const uint64_t kend = min(k0 + 32, a.c_end);
   const uint32_t nrows = static_cast<uint32_t>(kend > k0 ? kend - k0 : 0);
   if (nrows == 0) return;
   const uint32_t e0 = a.off[k0], e1 = a.off[k0 + nrows];
@@ -803,38 +800,18 @@ __device__ __forceinline__ void warp_rows_staged(const PrStepArgs& a, uint64_t k
     tn[q] = j < total ? __ldcs(t + j) : 0xffffffffu;
   }
   double acc = 0.0;  // scoring.cpp:67
-  double v[K];
-  if (Pipe) {
+  for (uint32_t base = 0; base < total; base += kCWin) {
+    double v[K];
 #pragma unroll
     for (int q = 0; q < K; ++q) v[q] = tn[q] != 0xffffffffu ? __ldg(a.norm_in + tn[q]) : 0.0;
 #pragma unroll
-    for (int q = 0; q < K; ++q) {
-      const uint32_t j = kCWin + q * 32 + lane;
+    for (int q = 0; q < K; ++q) {  // next chunk's targets in flight
+      const uint32_t j = base + kCWin + q * 32 + lane;
       tn[q] = j < total ? __ldcs(t + j) : 0xffffffffu;
-    }
-  }
-  for (uint32_t base = 0; base < total; base += kCWin) {
-    if (!Pipe) {
-#pragma unroll
-      for (int q = 0; q < K; ++q) v[q] = tn[q] != 0xffffffffu ? __ldg(a.norm_in + tn[q]) : 0.0;
-#pragma unroll
-      for (int q = 0; q < K; ++q) {  // next chunk's targets in flight
-        const uint32_t j = base + kCWin + q * 32 + lane;
-        tn[q] = j < total ? __ldcs(t + j) : 0xffffffffu;
-      }
     }
 #pragma unroll
     for (int q = 0; q < K; ++q) buf[q * 32 + lane] = v[q];
     __syncwarp();
-    if (Pipe) {  // the next chunk's gathers, then the chunk after's targets
-#pragma unroll
-      for (int q = 0; q < K; ++q) v[q] = tn[q] != 0xffffffffu ? __ldg(a.norm_in + tn[q]) : 0.0;
-#pragma unroll
-      for (int q = 0; q < K; ++q) {
-        const uint32_t j = base + 2 * kCWin + q * 32 + lane;
-        tn[q] = j < total ? __ldcs(t + j) : 0xffffffffu;
-      }
-    }
     const uint32_t lo = max(rb, base), hi = min(re, base + kCWin);
     for (uint32_t j = lo; j < hi; ++j) acc = __dadd_rn(acc, buf[j - base]);  // in order
     __syncwarp();
@@ -884,8 +861,8 @@ __global__ void __launch_bounds__(kCsWarps * 32) pr_cstream_kernel(const PrStepA
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   CsWarpSmem& S = reinterpret_cast<CsWarpSmem*>(cs_smem)[w];
   const uint64_t k0 = c_begin + ((uint64_t)blockIdx.x * kCsWarps + w) * kCsRows;
-  if (k0 >= a.row_end) return;
-  const uint32_t nrows = static_cast<uint32_t>((a.row_end - k0 < (uint64_t)kCsRows ? a.row_end - k0 : (uint64_t)kCsRows));
+  if (k0 >= a.c_end) return;
+  const uint32_t nrows = static_cast<uint32_t>((a.c_end - k0 < (uint64_t)kCsRows ? a.c_end - k0 : (uint64_t)kCsRows));
   for (uint32_t j = lane; j <= nrows; j += 32) S.off[j] = a.off[k0 + j];
   __syncwarp();
   const uint32_t e0 = S.off[0], e1 = S.off[nrows];
@@ -947,10 +924,21 @@ __global__ void __launch_bounds__(kCsWarps * 32) pr_cstream_kernel(const PrStepA
   for (; j < nrows; j += 32) finish_row(a, k0 + j, 0.0);  // empty rows at the very end
 }
 
+// Rows without edges on the relabelled twin (61 % of the C3 rows): their
+// row sum is 0.0, so every step writes the same norm = base / max(deg, 1)
+// (scoring.cpp:59-70 with an empty chain) and the last step the same score =
+// base. A streaming epilogue instead of a warp per 32 rows; the caller skips
+// it once both Jacobi buffers hold the value (steps 3 .. n-1).
+__global__ void __launch_bounds__(256) pr_empty_kernel(const PrStepArgs a, uint64_t k_begin) {
+  for (uint64_t k = k_begin + blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; k < a.row_end;
+       k += (uint64_t)gridDim.x * blockDim.x)
+    finish_row(a, k, 0.0);
+}
+
 // MinB: CTAs per SM the register allocation must allow (1: no cap, 71
 // registers, 3 CTAs fit; 4: <= 64 registers). TIERGRAPH_PR_MINB=1|4 overrides
 // the default (4 on the relabelled twin, else 1).
-template <int MinB, bool Pipe>
+template <int MinB>
 __global__ void __launch_bounds__(kPrWarps * 32, MinB) pr_step_kernel(const PrStepArgs a) {
   __shared__ __align__(16) double smem[kPrWarps * 32 / kBLanes * kBStride];  // 16.6 KB: class B windows
   if (blockIdx.x < a.b_ctas) {
@@ -961,7 +949,7 @@ __global__ void __launch_bounds__(kPrWarps * 32, MinB) pr_step_kernel(const PrSt
     // storage-sorted twin: 32 consecutive rows per warp, staged chunks
     const int w = threadIdx.x >> 5;
     const uint64_t k0 = a.row_begin + a.nB + ((uint64_t)(blockIdx.x - a.b_ctas) * kPrWarps + w) * 32;
-    warp_rows_staged<Pipe>(a, k0, smem + w * kCWin);
+    warp_rows_staged(a, k0, smem + w * kCWin);
   } else {
     const uint64_t i = a.nB + (uint64_t)(blockIdx.x - a.b_ctas) * blockDim.x + threadIdx.x;
     if (i < a.m) thread_row(a, a.order[i]);
@@ -1103,7 +1091,7 @@ const tg_graph::Sched& schedule(tg_ctx* ctx, const tg_graph* g, uint64_t rb, uin
 void pagerank_step(tg_ctx* ctx, const tg_graph* g, const uint32_t* deg, double damp,
                    const double* nin, double* nout, double* sout, uint64_t rb, uint64_t re,
                    int last, uint32_t n_peers, double* const* peer_norm,
-                   double* const* peer_score, const uint32_t* score_index) {
+                   double* const* peer_score, const uint32_t* score_index, int skip_empty) {
   if (re <= rb) return;
   if (rb < g->rb || re > g->re)
     domain_error("pagerank step: rows [" + std::to_string(rb) + ", " + std::to_string(re) +
@@ -1135,11 +1123,14 @@ void pagerank_step(tg_ctx* ctx, const tg_graph* g, const uint32_t* deg, double d
     a.peer_norm[p] = p < n_peers ? peer_norm[p] : nullptr;
     a.peer_score[p] = p < n_peers ? peer_score[p] : nullptr;
   }
-  uint64_t c_ctas = (a.m - sc.nB + kPrWarps * 32 - 1) / (kPrWarps * 32);
+  // twin: class C ends at the first empty row; the empty rows get their own epilogue
+  const uint64_t mC = (!sc.order && sc.nE < a.m) ? sc.nE : a.m;
+  a.c_end = rb + mC;
+  uint64_t c_ctas = (mC - sc.nB + kPrWarps * 32 - 1) / (kPrWarps * 32);
   // class C streamed on its own stream (relabelled twin: rows in storage order)
   const char* csv = std::getenv("TIERGRAPH_PR_CSTREAM");
   const bool cstream = csv && csv[0] == '1';
-  const bool cs = cstream && !sc.order && a.m > sc.nB;
+  const bool cs = cstream && !sc.order && mC > sc.nB;
   if (cs) c_ctas = 0;
   if (sc.nA || cs) ctx->fork();
   if (cs) {
@@ -1149,7 +1140,7 @@ void pagerank_step(tg_ctx* ctx, const tg_graph* g, const uint32_t* deg, double d
                                     kCsSmem));
       cattr[ctx->device % TG_MAX_DEVICES] = true;
     }
-    const uint64_t warps = (a.m - sc.nB + kCsRows - 1) / kCsRows;
+    const uint64_t warps = (mC - sc.nB + kCsRows - 1) / kCsRows;
     pr_cstream_kernel<<<static_cast<unsigned>((warps + kCsWarps - 1) / kCsWarps), kCsWarps * 32,
                         kCsSmem, ctx->aux3>>>(a, rb + sc.nB);
     TGB_LAUNCHED();
@@ -1183,19 +1174,18 @@ void pagerank_step(tg_ctx* ctx, const tg_graph* g, const uint32_t* deg, double d
     // 10.2 ms, profiles/r02j); 3 (71 registers) otherwise
     const char* mb = std::getenv("TIERGRAPH_PR_MINB");
     const bool four = mb ? mb[0] == '4' : !a.order;
-    const char* cp = std::getenv("TIERGRAPH_PR_CPIPE");  // pipelined class C (twin)
-    const bool pipe = cp && cp[0] == '1';
-    if (four && pipe)
-      pr_step_kernel<4, true><<<grid, kPrWarps * 32, 0, ctx->stream>>>(a);
-    else if (four)
-      pr_step_kernel<4, false><<<grid, kPrWarps * 32, 0, ctx->stream>>>(a);
-    else if (pipe)
-      pr_step_kernel<1, true><<<grid, kPrWarps * 32, 0, ctx->stream>>>(a);
+    if (four)
+      pr_step_kernel<4><<<grid, kPrWarps * 32, 0, ctx->stream>>>(a);
     else
-      pr_step_kernel<1, false><<<grid, kPrWarps * 32, 0, ctx->stream>>>(a);
+      pr_step_kernel<1><<<grid, kPrWarps * 32, 0, ctx->stream>>>(a);
     TGB_LAUNCHED();
   }
   if (sc.nA || cs) ctx->join();
+  if (mC < a.m && !(skip_empty && !last)) {
+    pr_empty_kernel<<<grid_for(a.m - mC, 256, ctx->num_sms * 8), 256, 0, ctx->stream>>>(a,
+                                                                                      rb + mC);
+    TGB_LAUNCHED();
+  }
 }
 
 // TIERGRAPH_PR_RELABEL: "0" never, "1" always, default: when the norm vector
@@ -1288,7 +1278,16 @@ const tg_graph* relabel_twin(tg_ctx* ctx, const tg_graph* gc) {
     TGB_CUDA(cudaEventSynchronize(ev1));
     TGB_CUDA(cudaEventElapsedTime(&g->twin_ms, ev0, ev1));
     // storage order IS the schedule: identity order, the same class bounds
-    t->scheds.push_back(tg_graph::Sched{0, n, nullptr, sg.nA, sg.nB, sg.nLong});
+    tg_graph::Sched tsc{0, n, nullptr, sg.nA, sg.nB, sg.nLong};
+    tsc.nE = n;
+    if (e) {  // first storage row without edges (empty rows are stored last)
+      uint64_t* k_e = lens;
+      first_short_kernel<<<1, 32, 0, ctx->stream>>>(t->off, n, 0, k_e);
+      TGB_LAUNCHED();
+      TGB_CUDA(cudaMemcpyAsync(&tsc.nE, k_e, 8, cudaMemcpyDeviceToHost, ctx->stream));
+      ctx->sync();
+    }
+    t->scheds.push_back(tsc);
   } catch (...) {
     cudaFree(lens);
     tg_graph_destroy(t);
@@ -1408,7 +1407,9 @@ void run_pagerank(tg_ctx* ctx, const tg_graph* g, uint32_t iterations, double da
   for (uint32_t it = 0; it < iterations; ++it) {
     const bool last = it + 1 == iterations;
     persist.window(na);
-    pagerank_step(ctx, run, deg, damp, na, nb, o.dev(), 0, n, last ? 1 : 0);
+    // steps 3.. (it >= 2) find both buffers already holding the empty rows' norm
+    pagerank_step(ctx, run, deg, damp, na, nb, o.dev(), 0, n, last ? 1 : 0, 0, nullptr, nullptr,
+                  nullptr, tw && it >= 2 ? 1 : 0);
     if (phase_ms) TGB_CUDA(cudaEventRecord(ev[it + 2], ctx->stream));
     std::swap(na, nb);
   }

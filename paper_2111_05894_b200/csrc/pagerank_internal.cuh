@@ -27,6 +27,10 @@ struct tg_graph {
     uint32_t* order;
     uint32_t nA, nB;  // order[0,nA): len > kLenA; [nA,nB): kLenB < len <= kLenA
     uint32_t nLong;   // order[0,nLong): len > kHubLong (512-thread class-A CTAs)
+    // relabelled twin only (storage order = schedule): rows [nE, re-rb) have
+    // no edges; their step is a streaming epilogue, skipped once both norm
+    // buffers hold its constant value. Otherwise nE = re - rb.
+    uint64_t nE = ~0ull;
   };
   std::vector<Sched> scheds;
   // K3 relabelling ("K3 relabel"): a twin of this graph with node
@@ -68,5 +72,6 @@ void pagerank_init(tg_ctx* ctx, uint64_t n, const uint64_t* tid_dev, uint64_t nt
 void pagerank_step(tg_ctx* ctx, const tg_graph* g, const uint32_t* deg, double damp,
                    const double* nin, double* nout, double* sout, uint64_t rb, uint64_t re,
                    int last, uint32_t n_peers = 0, double* const* peer_norm = nullptr,
-                   double* const* peer_score = nullptr, const uint32_t* score_index = nullptr);
+                   double* const* peer_score = nullptr, const uint32_t* score_index = nullptr,
+                   int skip_empty = 0);
 }  // namespace tgb

@@ -70,8 +70,9 @@ def main():
             ref = out.clone()
         same = bool(torch.equal(out, ref))
         ms = statistics.mean(steps)
+        per_step = [round(statistics.mean(steps[i::iters]), 3) for i in range(iters)]
         print(f"{st or '(default)':50s} step {ms:8.3f} ms  {e / ms / 1e6:7.1f} GTEPS/iter  "
-              f"bit-identical {same}  sm {mhz} MHz", flush=True)
+              f"bit-identical {same}  sm {mhz} MHz  per step {per_step}", flush=True)
 
 
 if __name__ == "__main__":
