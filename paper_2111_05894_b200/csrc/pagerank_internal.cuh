@@ -73,5 +73,5 @@ void pagerank_step(tg_ctx* ctx, const tg_graph* g, const uint32_t* deg, double d
                    const double* nin, double* nout, double* sout, uint64_t rb, uint64_t re,
                    int last, uint32_t n_peers = 0, double* const* peer_norm = nullptr,
                    double* const* peer_score = nullptr, const uint32_t* score_index = nullptr,
-                   int skip_empty = 0);
+                   int skip_empty = 0, int score_to_norm = 0);
 }  // namespace tgb
