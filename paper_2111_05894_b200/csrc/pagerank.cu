@@ -46,6 +46,8 @@ constexpr uint32_t kLenA = 4096;
 constexpr uint32_t kLenAMax = 65536;
 constexpr uint32_t kLenB = 512;
 constexpr uint32_t kLenBTwin = 256;
+// K3's L2 persisting window over the first labels of the twin (see L2Persist)
+constexpr long kPersistDefaultMB = 48;
 // class-A CTAs: 256 threads x 8 addends (2,048 per tile); 512 x 8 for the
 // rows longer than kHubLong and a quarter of the longest row (half the tiles
 // on the critical path; 1024 x 4 was measured no faster for the 77k-edge C2
@@ -1294,6 +1296,10 @@ const tg_graph* relabel_twin(tg_ctx* ctx, const tg_graph* gc) {
     TGB_CUDA(cudaEventRecord(ev1, ctx->stream));
     TGB_CUDA(cudaEventSynchronize(ev1));
     TGB_CUDA(cudaEventElapsedTime(&g->twin_ms, ev0, ev1));
+    if (mode != "indeg") {  // label = storage row: K3 indexes by the row itself
+      TGB_CUDA(cudaFree(t->row_label));
+      t->row_label = nullptr;
+    }
     // storage order IS the schedule: identity order, the same class bounds
     tg_graph::Sched tsc{0, n, nullptr, sg.nA, sg.nB, sg.nLong};
     tsc.nE = n;
@@ -1337,7 +1343,6 @@ void check_config(uint32_t iterations, double damp) {  // scoring.cpp:42-47
 // TIERGRAPH_PR_PERSIST_MB: window size in MB (0 = off); default: 48 MB
 // (within the device's window and persisting limits) whenever the relabelled
 // twin runs.
-constexpr long kPersistDefaultMB = 48;
 struct L2Persist {
   tg_ctx* ctx = nullptr;
   size_t bytes = 0;

@@ -86,7 +86,7 @@ __global__ void __launch_bounds__(256) key_prep_kernel(const double* __restrict_
 // One 256-thread CTA: thread d checks digit value d of every pass (a pass
 // whose histogram holds all n keys in one bucket is skipped).
 __global__ void __launch_bounds__(256) plan_kernel(const uint32_t* __restrict__ hist, uint64_t n,
-                                                   RadixPlan* plan) {
+                                                   RadixPlan* plan, int keep = -1) {
   __shared__ int trivial[8];
   for (int p = 0; p < 8; ++p) {
     const int t = __syncthreads_or(hist[p * 256 + threadIdx.x] == n);
@@ -96,9 +96,9 @@ __global__ void __launch_bounds__(256) plan_kernel(const uint32_t* __restrict__ 
   if (threadIdx.x != 0) return;
   int src = 0;
   for (int p = 0; p < 8; ++p) {
-    plan->skip[p] = trivial[p] ? 1 : 0;
+    plan->skip[p] = (trivial[p] && p != keep) ? 1 : 0;  // `keep` narrows the keys: always runs
     plan->src[p] = src;
-    if (!trivial[p]) src ^= 1;
+    if (!plan->skip[p]) src ^= 1;
   }
   plan->final_src = src;
 }
@@ -113,21 +113,27 @@ __global__ void __launch_bounds__(256) plan_kernel(const uint32_t* __restrict__ 
 // of tiles 0..t). The digit's global base comes from the all-pass histogram
 // of the key-prep kernel. The tile is then reordered by digit in shared
 // memory and written out in that order (coalesced runs).
-constexpr int kRsScatterSmem = kRsTile * (8 + 4);  // staged keys + values
+// Keys are u64 (scores) or u32 (row lengths, in-degrees, edge targets); a
+// u64 sort narrows to u32 at the pass that sorts bits 32..39 (after it only
+// bits 32..63 still order anything): that pass writes k >> 32, the later
+// passes move 4 B keys instead of 8 B.
+template <typename KIn>
+constexpr int rs_scatter_smem() { return kRsTile * static_cast<int>(sizeof(KIn) + 4); }
 constexpr uint64_t kStAgg = 1ull << 62, kStInc = 2ull << 62, kStMask = (1ull << 62) - 1;
+template <typename KIn, typename KOut>
 __global__ void __launch_bounds__(kRsWarps * 32, 3) scatter_kernel(
-    uint64_t* __restrict__ k0, uint32_t* __restrict__ v0, uint64_t* __restrict__ k1,
-    uint32_t* __restrict__ v1, uint64_t n, int pass, const RadixPlan* __restrict__ plan,
+    void* __restrict__ k0v, uint32_t* __restrict__ v0, void* __restrict__ k1v,
+    uint32_t* __restrict__ v1, uint64_t n, int pass, int shift, const RadixPlan* __restrict__ plan,
     const uint32_t* __restrict__ hist, uint64_t* __restrict__ status, uint32_t* __restrict__ tile_ctr) {
   if (plan->skip[pass]) return;
   const bool from1 = plan->src[pass] != 0;
-  const uint64_t* kin = from1 ? k1 : k0;
+  const KIn* kin = reinterpret_cast<const KIn*>(from1 ? k1v : k0v);
   const uint32_t* vin = from1 ? v1 : v0;
-  uint64_t* kout = from1 ? k0 : k1;
+  KOut* kout = reinterpret_cast<KOut*>(from1 ? k0v : k1v);
   uint32_t* vout = from1 ? v0 : v1;
   extern __shared__ __align__(16) uint8_t rs_smem[];
-  uint64_t* skey = reinterpret_cast<uint64_t*>(rs_smem);
-  uint32_t* sval = reinterpret_cast<uint32_t*>(rs_smem + kRsTile * 8);
+  KIn* skey = reinterpret_cast<KIn*>(rs_smem);
+  uint32_t* sval = reinterpret_cast<uint32_t*>(rs_smem + kRsTile * sizeof(KIn));
   __shared__ uint32_t wcnt[kRsWarps][256];
   __shared__ uint32_t doff[256];
   __shared__ uint32_t tstart[256];
@@ -139,8 +145,7 @@ __global__ void __launch_bounds__(kRsWarps * 32, 3) scatter_kernel(
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const uint32_t lt = (1u << lane) - 1u;
   const uint64_t base = (uint64_t)tile * kRsTile + w * (32 * kRsIpt);
-  const int shift = 8 * pass;
-  uint64_t key[kRsIpt];
+  KIn key[kRsIpt];
   uint32_t val[kRsIpt];
   uint32_t rank[kRsIpt];
 #pragma unroll
@@ -240,24 +245,39 @@ __global__ void __launch_bounds__(kRsWarps * 32, 3) scatter_kernel(
   const uint64_t t0 = (uint64_t)tile * kRsTile;
   const uint32_t tn = static_cast<uint32_t>(n - t0 < (uint64_t)kRsTile ? n - t0 : kRsTile);
   for (uint32_t j = threadIdx.x; j < tn; j += blockDim.x) {
-    const uint64_t kk = skey[j];
+    const KIn kk = skey[j];
     const uint32_t d = static_cast<uint32_t>((kk >> shift) & 0xff);
     const uint32_t pos = doff[d] + (j - tstart[d]);
-    kout[pos] = kk;
+    if constexpr (sizeof(KOut) < sizeof(KIn))
+      kout[pos] = static_cast<KOut>(static_cast<uint64_t>(kk) >> 32);
+    else
+      kout[pos] = kk;
     vout[pos] = sval[j];
   }
 }
 
 // The passes of one LSD sort (keys k0/v0 in, result where plan->final_src
-// says): one onesweep kernel per digit that is not constant.
-void radix_passes(tg_ctx* ctx, uint64_t* k0, uint32_t* v0, uint64_t* k1, uint32_t* v1, uint64_t n,
-                  int passes, const RadixPlan* plan, const uint32_t* hist) {
+// says): one onesweep kernel per digit that is not constant. key_bytes 8:
+// u64 keys, narrowed to u32 at pass `narrow_at` (>= 4; the plan must keep
+// that pass, plan_kernel's `keep`), or never (-1); key_bytes 4: u32 keys.
+template <typename KIn, typename KOut>
+static void launch_pass(tg_ctx* ctx, void* k0, uint32_t* v0, void* k1, uint32_t* v1, uint64_t n,
+                        int pass, int shift, const RadixPlan* plan, const uint32_t* hist,
+                        uint64_t* status, uint32_t* ctr, uint32_t nblk) {
   static bool attr[TG_MAX_DEVICES] = {};
   if (!attr[ctx->device % TG_MAX_DEVICES]) {
-    TGB_CUDA(cudaFuncSetAttribute(scatter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  kRsScatterSmem));
+    TGB_CUDA(cudaFuncSetAttribute(scatter_kernel<KIn, KOut>,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize, rs_scatter_smem<KIn>()));
     attr[ctx->device % TG_MAX_DEVICES] = true;
   }
+  scatter_kernel<KIn, KOut><<<nblk, kRsWarps * 32, rs_scatter_smem<KIn>(), ctx->stream>>>(
+      k0, v0, k1, v1, n, pass, shift, plan, hist, status, ctr);
+  TGB_LAUNCHED();
+}
+
+void radix_passes(tg_ctx* ctx, void* k0, uint32_t* v0, void* k1, uint32_t* v1, uint64_t n,
+                  int passes, const RadixPlan* plan, const uint32_t* hist, int key_bytes,
+                  int narrow_at) {
   const uint32_t nblk = static_cast<uint32_t>((n + kRsTile - 1) / kRsTile);
   uint64_t* status = nullptr;
   const size_t sbytes = 8ull * 256 * nblk;
@@ -266,9 +286,15 @@ void radix_passes(tg_ctx* ctx, uint64_t* k0, uint32_t* v0, uint64_t* k1, uint32_
   TGB_CUDA(cudaMemsetAsync(ctr, 0, 64, ctx->stream));
   for (int p = 0; p < passes; ++p) {
     TGB_CUDA(cudaMemsetAsync(status, 0, sbytes, ctx->stream));
-    scatter_kernel<<<nblk, kRsWarps * 32, kRsScatterSmem, ctx->stream>>>(k0, v0, k1, v1, n, p, plan,
-                                                                         hist, status, ctr);
-    TGB_LAUNCHED();
+    if (key_bytes == 4)
+      launch_pass<uint32_t, uint32_t>(ctx, k0, v0, k1, v1, n, p, 8 * p, plan, hist, status, ctr, nblk);
+    else if (narrow_at < 0 || p < narrow_at)
+      launch_pass<uint64_t, uint64_t>(ctx, k0, v0, k1, v1, n, p, 8 * p, plan, hist, status, ctr, nblk);
+    else if (p == narrow_at)
+      launch_pass<uint64_t, uint32_t>(ctx, k0, v0, k1, v1, n, p, 8 * p, plan, hist, status, ctr, nblk);
+    else
+      launch_pass<uint32_t, uint32_t>(ctx, k0, v0, k1, v1, n, p, 8 * p - 32, plan, hist, status, ctr,
+                                      nblk);
   }
   TGB_CUDA(cudaFreeAsync(status, ctx->stream));
 }
@@ -294,7 +320,7 @@ __global__ void perm_kernel(const uint32_t* __restrict__ v0, const uint32_t* __r
 __global__ void __launch_bounds__(256) rowlen_key_kernel(const uint32_t* __restrict__ off,
                                                          const uint32_t* __restrict__ val,
                                                          uint64_t rb, uint64_t m,
-                                                         uint64_t* __restrict__ keys,
+                                                         uint32_t* __restrict__ keys,
                                                          uint32_t* __restrict__ vals,
                                                          uint32_t* __restrict__ hist) {
   __shared__ uint32_t h[4][256];
@@ -345,13 +371,13 @@ static void sort_desc_u32(tg_ctx* ctx, const uint32_t* off, const uint32_t* val,
   if (m == 0) return;
   // private temporaries (stream-ordered allocations): callers may hold the
   // context's scratch slots across this call
-  const size_t bytes = 2 * 8 * m + 2 * 4 * m + 64 + sizeof(RadixPlan) + 8 * 256 * 4 + 256;
+  const size_t bytes = 4 * 4 * m + 4 * 16 + sizeof(RadixPlan) + 8 * 256 * 4 + 256;
   char* base = nullptr;
   TGB_CUDA(tgb::dev_malloc_async(reinterpret_cast<void**>(&base), bytes, ctx->stream));
   auto align = [](char* p) { return reinterpret_cast<char*>((reinterpret_cast<uintptr_t>(p) + 15) & ~uintptr_t(15)); };
   char* p = base;
-  uint64_t* k0 = reinterpret_cast<uint64_t*>(p); p = align(p + 8 * m);
-  uint64_t* k1 = reinterpret_cast<uint64_t*>(p); p = align(p + 8 * m);
+  uint32_t* k0 = reinterpret_cast<uint32_t*>(p); p = align(p + 4 * m);  // u32 keys
+  uint32_t* k1 = reinterpret_cast<uint32_t*>(p); p = align(p + 4 * m);
   uint32_t* v0 = reinterpret_cast<uint32_t*>(p); p = align(p + 4 * m);
   uint32_t* v1 = reinterpret_cast<uint32_t*>(p); p = align(p + 4 * m);
   auto* plan = reinterpret_cast<RadixPlan*>(p); p = align(p + sizeof(RadixPlan));
@@ -362,7 +388,7 @@ static void sort_desc_u32(tg_ctx* ctx, const uint32_t* off, const uint32_t* val,
   TGB_LAUNCHED();
   plan_kernel<<<1, 256, 0, ctx->stream>>>(hist, m, plan);
   TGB_LAUNCHED();
-  radix_passes(ctx, k0, v0, k1, v1, m, 4, plan, hist);  // digits 4..7 are constant
+  radix_passes(ctx, k0, v0, k1, v1, m, 4, plan, hist, 4, -1);  // digits 4..7 are constant
   order_out_kernel<<<grid_for(m, 256), 256, 0, ctx->stream>>>(v0, v1, plan, rb, m, order_dev);
   TGB_LAUNCHED();
   TGB_CUDA(cudaFreeAsync(base, ctx->stream));
@@ -556,9 +582,9 @@ void sort_scores(tg_ctx* ctx, const double* scores_dev, uint64_t n, uint64_t* or
   key_prep_kernel<<<grid_for(n, 256, ctx->num_sms * 8), 256, 0, ctx->stream>>>(scores_dev, n, kmin, k0,
                                                                                v0, hist, bad);
   TGB_LAUNCHED();
-  plan_kernel<<<1, 256, 0, ctx->stream>>>(hist, n, plan);
+  plan_kernel<<<1, 256, 0, ctx->stream>>>(hist, n, plan, 4);  // pass 4 narrows to u32 keys
   TGB_LAUNCHED();
-  radix_passes(ctx, k0, v0, k1, v1, n, 8, plan, hist);
+  radix_passes(ctx, k0, v0, k1, v1, n, 8, plan, hist, 8, 4);
   const uint64_t nb = (n + (1ull << kPmShift) - 1) >> kPmShift;
   if (perm_dev && nb <= kPmMaxBuckets) {
     uint32_t* bcur = ctx->scratch_t<uint32_t>(kScratchE, kPmMaxBuckets);
@@ -608,7 +634,7 @@ void sort_scores(tg_ctx* ctx, const double* scores_dev, uint64_t n, uint64_t* or
 // as the value; the transposed offsets are the key boundaries.
 __global__ void __launch_bounds__(256) edge_keys_kernel(const uint64_t* __restrict__ off,
                                                         const uint64_t* __restrict__ tgt,
-                                                        uint64_t n, uint64_t* __restrict__ keys,
+                                                        uint64_t n, uint32_t* __restrict__ keys,
                                                         uint32_t* __restrict__ vals,
                                                         uint32_t* __restrict__ hist) {
   __shared__ uint32_t h[4][256];
@@ -620,7 +646,7 @@ __global__ void __launch_bounds__(256) edge_keys_kernel(const uint64_t* __restri
   const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
   for (uint64_t u = warp; u < n; u += nw) {
     for (uint64_t i = off[u] + lane; i < off[u + 1]; i += 32) {
-      const uint64_t k = tgt[i];
+      const uint32_t k = static_cast<uint32_t>(tgt[i]);  // < n < 2^32 (range-checked first)
       keys[i] = k;
       vals[i] = static_cast<uint32_t>(u);
 #pragma unroll
@@ -645,11 +671,11 @@ __global__ void key_range_check_kernel(const uint64_t* __restrict__ tgt, uint64_
 }
 
 // t_off[v] = first sorted position with key >= v; t_tgt[i] = source (u64)
-__global__ void transpose_out_kernel(const uint64_t* __restrict__ k0, const uint64_t* __restrict__ k1,
+__global__ void transpose_out_kernel(const uint32_t* __restrict__ k0, const uint32_t* __restrict__ k1,
                                      const uint32_t* __restrict__ v0, const uint32_t* __restrict__ v1,
                                      const RadixPlan* __restrict__ plan, uint64_t n, uint64_t e,
                                      uint64_t* __restrict__ t_off, uint64_t* __restrict__ t_tgt) {
-  const uint64_t* k = plan->final_src ? k1 : k0;
+  const uint32_t* k = plan->final_src ? k1 : k0;
   const uint32_t* v = plan->final_src ? v1 : v0;
   for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i <= e;
        i += (uint64_t)gridDim.x * blockDim.x) {
@@ -668,13 +694,13 @@ void transpose_device(tg_ctx* ctx, const uint64_t* off, const uint64_t* tgt, uin
     TGB_CUDA(cudaMemsetAsync(t_off, 0, 8 * (n + 1), ctx->stream));
     return;
   }
-  const size_t bytes = 2 * 8 * e + 2 * 4 * e + 64 + sizeof(RadixPlan) + 8 * 256 * 4 + 256;
+  const size_t bytes = 4 * 4 * e + 64 + 64 + sizeof(RadixPlan) + 8 * 256 * 4 + 256;
   char* base = nullptr;
   TGB_CUDA(tgb::dev_malloc_async(reinterpret_cast<void**>(&base), bytes, ctx->stream));
   auto align = [](char* p) { return reinterpret_cast<char*>((reinterpret_cast<uintptr_t>(p) + 15) & ~uintptr_t(15)); };
   char* p = base;
-  uint64_t* k0 = reinterpret_cast<uint64_t*>(p); p = align(p + 8 * e);
-  uint64_t* k1 = reinterpret_cast<uint64_t*>(p); p = align(p + 8 * e);
+  uint32_t* k0 = reinterpret_cast<uint32_t*>(p); p = align(p + 4 * e);  // u32 keys (targets)
+  uint32_t* k1 = reinterpret_cast<uint32_t*>(p); p = align(p + 4 * e);
   uint32_t* v0 = reinterpret_cast<uint32_t*>(p); p = align(p + 4 * e);
   uint32_t* v1 = reinterpret_cast<uint32_t*>(p); p = align(p + 4 * e);
   auto* bad = reinterpret_cast<unsigned long long*>(p); p = align(p + 64);
@@ -697,7 +723,7 @@ void transpose_device(tg_ctx* ctx, const uint64_t* off, const uint64_t* tgt, uin
   TGB_LAUNCHED();
   plan_kernel<<<1, 256, 0, ctx->stream>>>(hist, e, plan);
   TGB_LAUNCHED();
-  radix_passes(ctx, k0, v0, k1, v1, e, 4, plan, hist);  // digits 4..7 are constant
+  radix_passes(ctx, k0, v0, k1, v1, e, 4, plan, hist, 4, -1);  // digits 4..7 are constant
   transpose_out_kernel<<<grid_for(e + 1, 256, ctx->num_sms * 16), 256, 0, ctx->stream>>>(
       k0, k1, v0, v1, plan, n, e, t_off, t_tgt);
   TGB_LAUNCHED();
