@@ -872,11 +872,12 @@ def run_ours(args):
                                                      "arrival barrier"}[name]}
                              for name, v in pr_multi.items()},
                          "relabel": dict(relabel, what=(
-                             "K3 runs on a twin of the device graph with node ids renumbered by "
-                             "in-degree (descending, ties by id), rows kept in storage order: "
-                             "bit-identical sums, hot norm values packed into L2-resident "
-                             "sectors; built once per device graph like the row schedule "
-                             "(build_ms, not in `ms`)")),
+                             "K3 runs on a twin of the device graph whose rows are stored in "
+                             "(class A by length, then length bucket, then in-degree) order and "
+                             "whose nodes are labelled by storage row (sequential norm stores; "
+                             "the most-gathered norms of each bucket share sectors); each row "
+                             "keeps its own edge order, so sums are bit-identical; built once "
+                             "per device graph like the row schedule (build_ms, not in `ms`)")),
                          "e2e": pr_e2e,
                          "spmv_step_us": round(step_ms * 1e3, 2),
                          "prepare_us": round(prep_ms * 1e3, 2),
