@@ -34,6 +34,7 @@ struct tg_store {
   uint64_t* counters = nullptr;                   // device: 3 x u64 + err
   uint64_t* result_host = nullptr;                // mapped pinned: the counters read back
   uint64_t* result_dev = nullptr;                 // its device address
+  uint64_t fin_seq = 0;                           // sequence number of the last synchronous gather
 };
 
 namespace tgb {

@@ -266,6 +266,7 @@ struct GatherTable {
   // mapped pinned host memory and re-arms them (no memset / D2H copy calls)
   uint64_t* fin_host;
   unsigned* fin_done;
+  uint64_t fin_seq;  // written to fin_host[4] last: the host's "this call is done" flag
   // TG_GATHER_DYNAMIC: after the first (statically spread) round, warps claim
   // batches from this counter, so a warp waiting on a cold (PCIe) batch does
   // not hold HBM batches behind it; the last CTA re-arms it
@@ -307,6 +308,8 @@ __device__ __forceinline__ void gather_finalize(const GatherTable& t, uint64_t* 
       c[2] = 0;
       e[0] = ~0ull;
       *reinterpret_cast<volatile unsigned*>(t.fin_done) = 0u;
+      __threadfence_system();
+      h[4] = t.fin_seq;  // every CTA's rows and the counters above are out
       __threadfence_system();
     }
   }
@@ -870,6 +873,7 @@ void launch_gather(tg_store* s, const uint64_t* ids_dev, uint64_t n, void* dst_d
   if (finalize) {
     t.fin_host = s->result_dev;
     t.fin_done = reinterpret_cast<unsigned*>(s->counters + 4);
+    t.fin_seq = s->fin_seq;
   }
   if (s->flags & TG_GATHER_DYNAMIC) {  // store-owned, zero between launches
     t.claim = reinterpret_cast<unsigned long long*>(s->counters + 5);
@@ -1127,6 +1131,7 @@ int tg_store_create(tg_ctx* ctx, const tg_layout* layout, uint32_t device_index,
       TGB_CUDA(cudaMemsetAsync(s->counters, 0, 64, ctx->stream));
       TGB_CUDA(cudaMemsetAsync(s->counters + 3, 0xff, 8, ctx->stream));
       TGB_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&s->result_host), 64, cudaHostAllocMapped));
+      std::memset(s->result_host, 0, 64);  // [4] = 0: no call posted yet (sequence numbers start at 1)
       void* rd = nullptr;
       TGB_CUDA(cudaHostGetDevicePointer(&rd, s->result_host, 0));
       s->result_dev = static_cast<uint64_t*>(rd);
@@ -1412,9 +1417,27 @@ int tg_gather_rows(tg_store* s, const uint64_t* ids, uint64_t n, void* dst, tg_r
     DevOut<uint8_t> o(ctx, static_cast<uint8_t*>(dst), n * s->R, kStageOut0);
     uint64_t* c = s->counters;  // armed: zero counters, err = ~0 (re-armed by the kernel)
     auto* err = reinterpret_cast<unsigned long long*>(c + 3);
-    launch_gather(s, d, n, o.dev(), c, err, /*finalize=*/true);
-    o.finish();  // stream sync: the last CTA's host stores are visible
     volatile uint64_t* hv = s->result_host;
+    const uint64_t seq = ++s->fin_seq;
+    launch_gather(s, d, n, o.dev(), c, err, /*finalize=*/true);
+    if (o.host) {
+      o.finish();  // the rows come back to host memory: copy + stream sync
+    } else {
+      // Rows stay in HBM: return as soon as the kernel's last CTA has posted
+      // the counters and the call's sequence number to mapped host memory
+      // (every CTA's rows are out by then), instead of waiting for the
+      // stream's completion. A kernel that never posts (a fault) falls back
+      // to the stream sync after 2 s, which reports the error.
+      const auto t0 = std::chrono::steady_clock::now();
+      for (uint32_t k = 1; hv[4] != seq; ++k) {
+        if ((k & 4095) == 0 &&
+            std::chrono::steady_clock::now() - t0 > std::chrono::seconds(2)) {
+          ctx->sync();
+          if (hv[4] != seq) throw Error(TG_ERR_INTERNAL, "gather: the kernel did not post its result");
+          break;
+        }
+      }
+    }
     uint64_t h[4] = {hv[0], hv[1], hv[2], hv[3]};
     if (h[3] != ~0ull) {  // reference semantics: prefix accounted, then DomainError
       const uint64_t first = h[3];

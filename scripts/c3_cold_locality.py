@@ -77,7 +77,7 @@ def main():
         print(f"{name:7s} share of second-half cold reads within the first "
               + ", ".join(f"{x:g} GB: {f:.3f}" for x, f in zip(gbs, fr)), flush=True)
 
-    feat, _ = bench.pin_features(cfg)
+    feat, _, _ = bench.pin_features(cfg)
     dev = torch.device("cuda", 0)
     timed = lists[half:half + 60]
     ids_d = [torch.as_tensor(x.astype(np.int64), device=dev) for x in timed]

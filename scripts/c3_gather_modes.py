@@ -33,7 +33,7 @@ def main():
     order = producers.epoch_order(new_tid, 7, 0)
     lists = [sampler.minibatch(order[b * 1024:(b + 1) * 1024], cfg["fanouts"], 7, 0, b)
              for b in range(40)]
-    feat, R = bench.pin_features(cfg)
+    feat, R, _ = bench.pin_features(cfg)
     dev = torch.device("cuda", 0)
     ids_d = [torch.as_tensor(x.astype(np.int64), device=dev) for x in lists]
     maxu = max(len(x) for x in lists)

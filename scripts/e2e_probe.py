@@ -32,7 +32,7 @@ def main():
     sampler = producers.GpuSampler(tg.CsrGraph(gt.offsets, gt.targets), ctx=ctx)
     order = producers.epoch_order(new_tid, 7, 0)
     lists = sampler.batches(order, cfg["fanouts"], cfg["batch"], 7, 0, 0, 60)
-    feat, R = bench.pin_features(cfg)
+    feat, R, _ = bench.pin_features(cfg)
     lay = tg.plan_layout(n, 0.2, 0.0, 1, cfg["dim"], cfg["elem"])
     st = tg.TieredFeatureStore(feat, perm, lay, ctx=ctx)
     dev = torch.device("cuda", 0)

@@ -34,7 +34,7 @@ def main():
     new_tid = np.sort(perm.new_id_of[tid.ids])
     lists = producers.epoch_minibatches(gt, new_tid, cfg["fanouts"], cfg["batch"], 7, 0,
                                         max_batches=steps)
-    feat, R = bench.pin_features(cfg)
+    feat, R, _ = bench.pin_features(cfg)
     dev = torch.device("cuda", 0)
     ids_d = [torch.as_tensor(x.astype(np.int64), device=dev) for x in lists]
     maxu = max(len(x) for x in lists)
