@@ -54,7 +54,10 @@ constexpr long kPersistDefaultMB = 48;
 // row: 158 vs 151 us)
 constexpr uint32_t kHubLong = 16384;
 constexpr int kPrWin = 256;         // edges staged per warp per window (class B)
-constexpr int kPrWarps = 8;         // warps per CTA (classes B, C)
+#ifndef TG_PR_WARPS
+#define TG_PR_WARPS 8
+#endif
+constexpr int kPrWarps = TG_PR_WARPS;  // warps per CTA (classes B, C)
 
 // ------------------------------------------------------------ graph upload
 __global__ void narrow_offsets_kernel(const uint64_t* __restrict__ in, uint32_t* __restrict__ out,
@@ -674,7 +677,10 @@ __global__ void __maxnreg__(80) pr_hub_kernel(const PrStepArgs a, uint32_t row0)
 // row), gather the normalized values into shared memory with the next
 // window's gathers and the window after's targets in flight, and the group's
 // first lane adds each window in storage order — 4 chains per warp.
-constexpr int kBLanes = 8;
+#ifndef TG_PR_BLANES  // lanes per class-B row (compile-time experiment knob)
+#define TG_PR_BLANES 8
+#endif
+constexpr int kBLanes = TG_PR_BLANES;
 constexpr int kBWin = kBLanes * 8;  // 64 edges per window
 // a group's window buffer stride: one double of padding puts the four chain
 // lanes of a warp (one per group) on different banks (ncu: 4-way conflicts)
@@ -786,7 +792,10 @@ __device__ __forceinline__ void thread_row(const PrStepArgs& a, uint32_t r) {
 // the normalized values into shared memory, and every lane then adds its own
 // row's part of the chunk in storage order (scoring.cpp:66-68) -- the same
 // left-to-right chain per row as thread_row, with coalesced target traffic.
-constexpr int kCWin = 256;  // edges per chunk (8 per lane)
+#ifndef TG_PR_CWIN  // class-C chunk on the twin (compile-time experiment knob)
+#define TG_PR_CWIN 256
+#endif
+constexpr int kCWin = TG_PR_CWIN;  // edges per chunk (8 per lane at 256)
 __device__ __forceinline__ void warp_rows_staged(const PrStepArgs& a, uint64_t k0, double* buf) {
   const int lane = threadIdx.x & 31;
   const uint64_t kend = min(k0 + 32, a.c_end);
@@ -957,7 +966,9 @@ __global__ void __launch_bounds__(256) pr_empty_kernel(const PrStepArgs a, uint6
 // the default (4 on the relabelled twin, else 1).
 template <int MinB>
 __global__ void __launch_bounds__(kPrWarps * 32, MinB) pr_step_kernel(const PrStepArgs a) {
-  __shared__ __align__(16) double smem[kPrWarps * 32 / kBLanes * kBStride];  // 16.6 KB: class B windows
+  // class B windows (16.6 KB) or, on the twin, class C chunks (16 KB)
+  constexpr int kSmemB = kPrWarps * 32 / kBLanes * kBStride, kSmemC = kPrWarps * kCWin;
+  __shared__ __align__(16) double smem[kSmemB > kSmemC ? kSmemB : kSmemC];
   if (blockIdx.x < a.b_ctas) {
     const int g = threadIdx.x / kBLanes;  // row group within the CTA
     const int64_t i = a.nA + (int64_t)blockIdx.x * (kPrWarps * 32 / kBLanes) + g;
