@@ -144,21 +144,26 @@ __global__ void __launch_bounds__(kRsWarps * 32, 3) scatter_kernel(
   const uint32_t tile = tile_s;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const uint32_t lt = (1u << lane) - 1u;
-  const uint64_t base = (uint64_t)tile * kRsTile + w * (32 * kRsIpt);
+  // tile-local 32-bit offsets; a full tile (all but the last) needs no bound checks
+  const uint64_t t0 = (uint64_t)tile * kRsTile;
+  const uint32_t tn = static_cast<uint32_t>(n - t0 < (uint64_t)kRsTile ? n - t0 : kRsTile);
+  const bool full = tn == kRsTile;
+  const uint32_t o0 = w * (32 * kRsIpt) + lane;  // + k * 32
+  const KIn* kin_t = kin + t0 + o0;
+  const uint32_t* vin_t = vin + t0 + o0;
   KIn key[kRsIpt];
   uint32_t val[kRsIpt];
   uint32_t rank[kRsIpt];
 #pragma unroll
   for (int k = 0; k < kRsIpt; ++k) {
-    const uint64_t i = base + k * 32 + lane;
-    const bool ok = i < n;
-    key[k] = ok ? kin[i] : 0;
-    val[k] = ok ? vin[i] : 0;
+    const bool ok = full || o0 + k * 32 < tn;
+    key[k] = ok ? kin_t[k * 32] : 0;
+    val[k] = ok ? vin_t[k * 32] : 0;
   }
 #pragma unroll
   for (int k = 0; k < kRsIpt; ++k) {
-    const uint64_t i = base + k * 32 + lane;
-    const uint32_t d = i < n ? static_cast<uint32_t>((key[k] >> shift) & 0xff) : 256u;
+    const bool ok = full || o0 + k * 32 < tn;
+    const uint32_t d = ok ? static_cast<uint32_t>((key[k] >> shift) & 0xff) : 256u;
     // lanes with the same 9-bit digit (256 = past the end), from 9 ballots:
     // 4 % faster per pass at C3 size than __match_any_sync (profiles/r02ab)
     uint32_t peers = 0xffffffffu;
@@ -240,8 +245,7 @@ __global__ void __launch_bounds__(kRsWarps * 32, 3) scatter_kernel(
   __syncthreads();
 #pragma unroll
   for (int k = 0; k < kRsIpt; ++k) {
-    const uint64_t i = base + k * 32 + lane;
-    if (i < n) {
+    if (full || o0 + k * 32 < tn) {
       const uint32_t d = static_cast<uint32_t>((key[k] >> shift) & 0xff);
       const uint32_t lp = tstart[d] + wcnt[w][d] + rank[k];
       skey[lp] = key[k];
@@ -249,8 +253,6 @@ __global__ void __launch_bounds__(kRsWarps * 32, 3) scatter_kernel(
     }
   }
   __syncthreads();
-  const uint64_t t0 = (uint64_t)tile * kRsTile;
-  const uint32_t tn = static_cast<uint32_t>(n - t0 < (uint64_t)kRsTile ? n - t0 : kRsTile);
   for (uint32_t j = threadIdx.x; j < tn; j += blockDim.x) {
     const KIn kk = skey[j];
     const uint32_t d = static_cast<uint32_t>((kk >> shift) & 0xff);
