@@ -3,7 +3,7 @@ tg_permutation_from_scores) on device-resident log-normal scores of n nodes,
 host-timed around a synchronous call (the call syncs once for its error word),
 plus a check that the result is a sort by (score desc, id asc).
 
-  python scripts/select_probe.py [n=111000000] [reps=5]
+  python scripts/select_probe.py [n=111000000 | scores.npy] [reps=5]
 """
 import os
 import sys
@@ -16,14 +16,20 @@ def main():
     import torch
     from paper_2111_05894_b200 import tiergraph as tg
     from paper_2111_05894_b200._lib import LIB
-    n = int(sys.argv[1]) if len(sys.argv) > 1 else 111_000_000
+    src = sys.argv[1] if len(sys.argv) > 1 else "111000000"
     reps = int(sys.argv[2]) if len(sys.argv) > 2 else 5
     dev = torch.device("cuda", 0)
     torch.cuda.set_device(0)
     ctx = tg.Context(0)
-    g = torch.Generator(device=dev).manual_seed(5)
-    s = 1e-8 * torch.exp(2.5 * torch.randn(n, dtype=torch.float64, device=dev, generator=g))
-    s[: n // 10] = s[n // 10: 2 * (n // 10)]  # exact duplicates: the id tie-break matters
+    if src.endswith(".npy"):  # real scores (e.g. a config's PageRank output)
+        import numpy as np
+        s = torch.as_tensor(np.load(src), device=dev)
+        n = s.numel()
+    else:
+        n = int(src)
+        g = torch.Generator(device=dev).manual_seed(5)
+        s = 1e-8 * torch.exp(2.5 * torch.randn(n, dtype=torch.float64, device=dev, generator=g))
+        s[: n // 10] = s[n // 10: 2 * (n // 10)]  # exact duplicates: the id tie-break matters
     perm = torch.empty(n, dtype=torch.int64, device=dev)
     order = torch.empty(n, dtype=torch.int64, device=dev)
     ts = []
