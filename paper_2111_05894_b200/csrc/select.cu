@@ -41,19 +41,122 @@ __device__ __forceinline__ uint64_t score_key(double s) {
   return ~b;
 }
 
-// K4a: the smallest key (kmin). Sorting key - kmin orders and ties exactly
-// like key, and digits above the top bit of (kmax - kmin) become constant
-// zero, so the planner skips their passes: scores spanning fewer than 2^4
-// binades need 7 passes instead of 8.
-__global__ void __launch_bounds__(256) key_min_kernel(const double* __restrict__ s, uint64_t n,
-                                                      unsigned long long* kmin) {
-  unsigned long long m = ~0ull;
+// K4a: the smallest key (kmin) and the largest. Sorting key - kmin orders
+// and ties exactly like key, and digits above the top bit of (kmax - kmin)
+// become constant zero, so the planner skips their passes. The largest key
+// is the lowest score.
+__global__ void __launch_bounds__(256) key_range_kernel(const double* __restrict__ s, uint64_t n,
+                                                        unsigned long long* kmin,
+                                                        unsigned long long* kmax) {
+  unsigned long long lo = ~0ull, hi = 0ull;
   for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
-       i += (uint64_t)gridDim.x * blockDim.x)
-    m = min(m, (unsigned long long)score_key(__ldcs(s + i)));
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    const unsigned long long k = score_key(__ldcs(s + i));
+    lo = min(lo, k);
+    hi = max(hi, k);
+  }
 #pragma unroll
-  for (int o = 16; o; o >>= 1) m = min(m, __shfl_xor_sync(0xffffffffu, m, o));
-  if ((threadIdx.x & 31) == 0) atomicMin(kmin, m);
+  for (int o = 16; o; o >>= 1) {
+    lo = min(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+    hi = max(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+  }
+  if ((threadIdx.x & 31) == 0) {
+    atomicMin(kmin, lo);
+    atomicMax(kmax, hi);
+  }
+}
+
+// The lowest score ties (key == kmax) go last in id order: reverse PageRank
+// gives every node without out-edges exactly the teleport score (1-d)/N, the
+// minimum (scoring.cpp:65-70 with an empty sum) -- 61 % of the C3 nodes. They
+// are compacted out of the sort (K4b/K4c) and written behind its result.
+constexpr int kKpIpt = 16;
+constexpr int kKpTile = 256 * kKpIpt;
+__global__ void __launch_bounds__(256) key_tile_count_kernel(const double* __restrict__ s,
+                                                             uint64_t n,
+                                                             const unsigned long long* kmax,
+                                                             uint64_t* __restrict__ cnt) {
+  __shared__ uint32_t c;
+  const uint64_t nt = (n + kKpTile - 1) / kKpTile;
+  const unsigned long long km = *kmax;
+  for (uint64_t t = blockIdx.x; t < nt; t += gridDim.x) {
+    if (threadIdx.x == 0) c = 0;
+    __syncthreads();
+    uint32_t mine = 0;
+#pragma unroll
+    for (int k = 0; k < kKpIpt; ++k) {
+      const uint64_t i = t * kKpTile + k * 256 + threadIdx.x;
+      if (i < n && score_key(__ldcs(s + i)) != km) ++mine;
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) mine += __shfl_xor_sync(0xffffffffu, mine, o);
+    if ((threadIdx.x & 31) == 0 && mine) atomicAdd(&c, mine);
+    __syncthreads();
+    if (threadIdx.x == 0) cnt[t] = c;
+    __syncthreads();
+  }
+}
+
+// K4c: validate, compact the keys below kmax (key - kmin, id) in id order to
+// [0, m) with all 8 digit histograms; the ids of the kmax ties in id order to
+// [m, n) of both value buffers (the sort's result lands in either).
+__global__ void __launch_bounds__(256) key_prep_compact_kernel(
+    const double* __restrict__ s, uint64_t n, const unsigned long long* __restrict__ kmin,
+    const unsigned long long* __restrict__ kmax, const uint64_t* __restrict__ off,
+    uint64_t* __restrict__ keys, uint32_t* __restrict__ vals, uint32_t* __restrict__ vals_alt,
+    uint32_t* __restrict__ hist, unsigned long long* bad) {
+  __shared__ uint32_t h[8][256];
+  __shared__ uint32_t wc[8];
+  for (int i = threadIdx.x; i < 8 * 256; i += blockDim.x) (&h[0][0])[i] = 0;
+  const uint64_t nt = (n + kKpTile - 1) / kKpTile;
+  const uint64_t m = off[nt];
+  const unsigned long long km = *kmax, k0 = *kmin;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  for (uint64_t t = blockIdx.x; t < nt; t += gridDim.x) {
+    const uint64_t base = off[t];
+    uint32_t run = 0;  // low keys of this tile in the rounds so far (same in every thread)
+    for (int k = 0; k < kKpIpt; ++k) {  // index order: round k, then thread
+      const uint64_t i = t * kKpTile + k * 256 + threadIdx.x;
+      bool ok = i < n, low = false;
+      unsigned long long key = 0;
+      if (ok) {
+        const double v = s[i];
+        if (!(isfinite(v) && v >= 0.0)) atomicMin(bad, (unsigned long long)i);
+        key = score_key(v);
+        low = key != km;
+      }
+      const uint32_t bal = __ballot_sync(0xffffffffu, low);
+      if (lane == 0) wc[w] = __popc(bal);
+      __syncthreads();
+      uint32_t before = run, total = 0;
+      for (int q = 0; q < 8; ++q) {
+        if (q < w) before += wc[q];
+        total += wc[q];
+      }
+      run += total;
+      before += __popc(bal & ((1u << lane) - 1u));  // low keys of this tile before i
+      if (ok) {
+        if (low) {
+          const uint64_t p = base + before;
+          const uint64_t kk = key - k0;
+          keys[p] = kk;
+          vals[p] = static_cast<uint32_t>(i);
+#pragma unroll
+          for (int q = 0; q < 8; ++q) atomicAdd(&h[q][(kk >> (8 * q)) & 0xff], 1u);
+        } else {
+          const uint64_t p = m + (i - base - before);
+          vals[p] = static_cast<uint32_t>(i);
+          vals_alt[p] = static_cast<uint32_t>(i);
+        }
+      }
+      __syncthreads();  // wc is rewritten by the next round
+    }
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < 8 * 256; i += blockDim.x) {
+    const uint32_t c = (&h[0][0])[i];
+    if (c) atomicAdd(hist + i, c);
+  }
 }
 
 // K4: validate (scoring.cpp:105-107), build keys (- kmin)/ids, and all 8 digit histograms.
@@ -583,15 +686,36 @@ void sort_scores(tg_ctx* ctx, const double* scores_dev, uint64_t n, uint64_t* or
   TGB_CUDA(cudaMemsetAsync(bad, 0xff, 8, ctx->stream));
   TGB_CUDA(cudaMemsetAsync(hist, 0, 8 * 256 * 4, ctx->stream));
   auto* kmin = reinterpret_cast<unsigned long long*>(small) + 1;
+  auto* kmax = reinterpret_cast<unsigned long long*>(small) + 2;
   TGB_CUDA(cudaMemsetAsync(kmin, 0xff, 8, ctx->stream));
-  key_min_kernel<<<grid_for(n, 256, ctx->num_sms * 8), 256, 0, ctx->stream>>>(scores_dev, n, kmin);
+  TGB_CUDA(cudaMemsetAsync(kmax, 0, 8, ctx->stream));
+  key_range_kernel<<<grid_for(n, 256, ctx->num_sms * 8), 256, 0, ctx->stream>>>(scores_dev, n, kmin,
+                                                                                kmax);
   TGB_LAUNCHED();
-  key_prep_kernel<<<grid_for(n, 256, ctx->num_sms * 8), 256, 0, ctx->stream>>>(scores_dev, n, kmin, k0,
-                                                                               v0, hist, bad);
+  // the lowest-score ties: how many keys stay in the sort (m)
+  const uint64_t nt = (n + kKpTile - 1) / kKpTile;
+  uint64_t* toff = ctx->scratch_t<uint64_t>(kScratchF, nt + 1);
+  TGB_CUDA(cudaMemsetAsync(toff + nt, 0, 8, ctx->stream));
+  key_tile_count_kernel<<<grid_for(nt, 1, ctx->num_sms * 8), 256, 0, ctx->stream>>>(scores_dev, n,
+                                                                                    kmax, toff);
   TGB_LAUNCHED();
-  plan_kernel<<<1, 256, 0, ctx->stream>>>(hist, n, plan, 4);  // pass 4 narrows to u32 keys
+  exclusive_scan_u64(ctx, toff, nt + 1);
+  uint64_t m = n;
+  TGB_CUDA(cudaMemcpyAsync(&m, toff + nt, 8, cudaMemcpyDeviceToHost, ctx->stream));
+  ctx->sync();
+  const bool compact = (n - m) * 8 >= n;  // worth it when >= 1/8 of the keys tie at the bottom
+  if (compact) {
+    key_prep_compact_kernel<<<grid_for(nt, 1, ctx->num_sms * 4), 256, 0, ctx->stream>>>(
+        scores_dev, n, kmin, kmax, toff, k0, v0, v1, hist, bad);
+  } else {
+    m = n;
+    key_prep_kernel<<<grid_for(n, 256, ctx->num_sms * 8), 256, 0, ctx->stream>>>(scores_dev, n, kmin,
+                                                                                 k0, v0, hist, bad);
+  }
   TGB_LAUNCHED();
-  radix_passes(ctx, k0, v0, k1, v1, n, 8, plan, hist, 8, 4);
+  plan_kernel<<<1, 256, 0, ctx->stream>>>(hist, m, plan, 4);  // pass 4 narrows to u32 keys
+  TGB_LAUNCHED();
+  if (m) radix_passes(ctx, k0, v0, k1, v1, m, 8, plan, hist, 8, 4);
   const uint64_t nb = (n + (1ull << kPmShift) - 1) >> kPmShift;
   if (perm_dev && nb <= kPmMaxBuckets) {
     uint32_t* bcur = ctx->scratch_t<uint32_t>(kScratchE, kPmMaxBuckets);

@@ -44,6 +44,24 @@ def test_random_scores_with_ties(tg, ctx, n):
     assert np.array_equal(p, oracle.port().permutation_from_scores(s))
 
 
+@pytest.mark.parametrize("n", [2, 4096, 100_003, 1_300_000])
+def test_lowest_score_ties_compacted(tg, ctx, n):
+    """>= 1/8 of the scores equal the minimum (reverse PageRank: every node
+    without out-edges scores exactly the teleport term): those ids leave the
+    radix sort and go last in id order; -0.0 and +0.0 minima tie."""
+    rng = np.random.default_rng(n + 7)
+    base = 0.15 / max(n, 1)
+    s = base + rng.random(n) * 10.0 ** rng.integers(-12, -3, n)
+    s[rng.random(n) < 0.6] = base
+    s[0] = base
+    z = np.where(rng.random(n) < 0.3, np.where(rng.random(n) < 0.5, -0.0, 0.0), s)
+    port = oracle.port()
+    for case in (s, z):
+        assert np.array_equal(tg.score_ordering(case), port.score_ordering(case))
+        assert np.array_equal(tg.permutation_from_scores(case).new_id_of,
+                              port.permutation_from_scores(case))
+
+
 def test_permutation_validation_and_invert(tg, ctx):
     for bad, msg in (([0, 0, 1], "assigned twice"), ([0, 1, 5], "out of range")):
         with pytest.raises(tg.DomainError, match=msg):
