@@ -40,12 +40,18 @@
 
 namespace tgb {
 
-constexpr int kK1Shift = 15;
+#ifndef TG_K1_SHIFT  // ids per bucket = 2^shift (compile-time experiment knob)
+#define TG_K1_SHIFT 15
+#endif
+#ifndef TG_K1_PIECE_LOG2  // elements per histogram work item = 2^this
+#define TG_K1_PIECE_LOG2 18
+#endif
+constexpr int kK1Shift = TG_K1_SHIFT;
 constexpr uint32_t kK1Bins = 1u << kK1Shift;    // ids per bucket (128 KB of counters)
 constexpr uint32_t kK1MaxBuckets = 8192;        // n <= 2^28
 constexpr int kK1Threads = 512, kK1Ipt = 16;
 constexpr uint32_t kK1Tile = kK1Threads * kK1Ipt;  // 8,192 targets per scatter tile
-constexpr uint32_t kK1Piece = 1u << 20;         // elements per histogram work item
+constexpr uint32_t kK1Piece = 1u << TG_K1_PIECE_LOG2;  // elements per histogram work item
 constexpr int kK1HistThreads = 1024;
 
 // (1) per-chunk bucket counts, bucket-major: cnt[b * G + c]
@@ -302,8 +308,9 @@ bool compute_indeg_binned(tg_ctx* ctx, const uint32_t* tgt, uint64_t e, uint64_t
   TGB_LAUNCHED();
   k1_items_kernel<<<1, 1024, 0, ctx->stream>>>(cnt, nb, G, items, small);
   TGB_LAUNCHED();
-  k1_hist_kernel<<<ctx->num_sms, kK1HistThreads, 4 * kK1Bins, ctx->stream>>>(part, items, small,
-                                                                             small + 1, n, deg);
+  // persistent: as many 1024-thread CTAs per SM as shared memory allows (2 at most)
+  k1_hist_kernel<<<ctx->num_sms * (kK1Bins <= 16384 ? 2 : 1), kK1HistThreads, 4 * kK1Bins,
+                   ctx->stream>>>(part, items, small, small + 1, n, deg);
   TGB_LAUNCHED();
   TGB_CUDA(cudaFreeAsync(base, ctx->stream));
   return true;
