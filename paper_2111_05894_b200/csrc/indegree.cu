@@ -49,6 +49,10 @@ namespace tgb {
 constexpr int kK1Shift = TG_K1_SHIFT;
 constexpr uint32_t kK1Bins = 1u << kK1Shift;    // ids per bucket (128 KB of counters)
 constexpr uint32_t kK1MaxBuckets = 8192;        // n <= 2^28
+#ifndef TG_K1_AGG_MAX  // warp-aggregated tile ranks up to this many buckets (off: C2
+#define TG_K1_AGG_MAX 0    // 475 vs 403 us -- __match_any_sync + spills cost more than
+#endif                     // the same-bucket atomics save; profiles/r02k1d)
+constexpr uint32_t kK1AggMaxBuckets = TG_K1_AGG_MAX;
 constexpr int kK1Threads = 512, kK1Ipt = 16;
 constexpr uint32_t kK1Tile = kK1Threads * kK1Ipt;  // 8,192 targets per scatter tile
 constexpr uint32_t kK1Piece = 1u << TG_K1_PIECE_LOG2;  // elements per histogram work item
@@ -64,14 +68,29 @@ __global__ void __launch_bounds__(kK1Threads) k1_count_kernel(const uint32_t* __
   __syncthreads();
   const uint64_t c0 = blockIdx.x * chunk, c1 = min(e, c0 + chunk);  // c0 % 4 == 0
   const uint64_t v1 = c0 + ((c1 - c0) & ~3ull);
-  for (uint64_t i = c0 + 4 * (uint64_t)threadIdx.x; i < v1; i += 4 * (uint64_t)blockDim.x) {
+  // four 16 B loads in flight per thread, then their 16 shared-memory atomics
+  const uint64_t step = 4 * (uint64_t)blockDim.x;
+  uint64_t i = c0 + 4 * (uint64_t)threadIdx.x;
+  for (; i + 3 * step < v1; i += 4 * step) {
+    uint4 v[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) v[q] = __ldcs(reinterpret_cast<const uint4*>(tgt + i + q * step));
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      atomicAdd(&h[v[q].x >> kK1Shift], 1u);
+      atomicAdd(&h[v[q].y >> kK1Shift], 1u);
+      atomicAdd(&h[v[q].z >> kK1Shift], 1u);
+      atomicAdd(&h[v[q].w >> kK1Shift], 1u);
+    }
+  }
+  for (; i < v1; i += step) {
     const uint4 v = __ldcs(reinterpret_cast<const uint4*>(tgt + i));
     atomicAdd(&h[v.x >> kK1Shift], 1u);
     atomicAdd(&h[v.y >> kK1Shift], 1u);
     atomicAdd(&h[v.z >> kK1Shift], 1u);
     atomicAdd(&h[v.w >> kK1Shift], 1u);
   }
-  for (uint64_t i = v1 + threadIdx.x; i < c1; i += blockDim.x) atomicAdd(&h[tgt[i] >> kK1Shift], 1u);
+  for (uint64_t j = v1 + threadIdx.x; j < c1; j += blockDim.x) atomicAdd(&h[tgt[j] >> kK1Shift], 1u);
   __syncthreads();
   for (uint32_t b = threadIdx.x; b < nb; b += blockDim.x) cnt[(uint64_t)b * G + blockIdx.x] = h[b];
 }
@@ -101,8 +120,12 @@ __device__ __forceinline__ void k1_block_scan(const uint32_t* c, uint32_t* s, ui
   }
 }
 
-// (3) scatter: chunk blockIdx.x, tile by tile, bucket-ordered in shared memory
-__global__ void __launch_bounds__(kK1Threads) k1_scatter_kernel(const uint32_t* __restrict__ tgt,
+// (3) scatter: chunk blockIdx.x, tile by tile, bucket-ordered in shared memory.
+// Agg (few buckets): lanes of a warp with the same bucket take their tile
+// ranks with one shared-memory atomic (leader + popc) instead of one each --
+// R-MAT puts ~19 % of C2's targets in bucket 0.
+template <bool Agg>
+__global__ void __launch_bounds__(kK1Threads, 2) k1_scatter_kernel(const uint32_t* __restrict__ tgt,
                                                                 uint64_t e, uint64_t chunk,
                                                                 uint32_t nb, uint32_t G,
                                                                 const uint64_t* __restrict__ cnt,
@@ -137,9 +160,24 @@ __global__ void __launch_bounds__(kK1Threads) k1_scatter_kernel(const uint32_t* 
         v[k] = j < tn ? tgt[t0 + j] : 0xffffffffu;
       }
     }
+    if (Agg) {
+      const uint32_t lane = threadIdx.x & 31, lt = (1u << lane) - 1u;
 #pragma unroll
-    for (int k = 0; k < kK1Ipt; ++k)  // ids < 2^28: 0xffffffff only marks a partial tile's end
-      if (v[k] != 0xffffffffu) r[k] = atomicAdd(&tcnt[v[k] >> kK1Shift], 1u);
+      for (int k = 0; k < kK1Ipt; ++k) {
+        const uint32_t b = v[k] != 0xffffffffu ? v[k] >> kK1Shift : 0xffffffffu;
+        const uint32_t peers = __match_any_sync(0xffffffffu, b);
+        const int leader = __ffs(peers) - 1;
+        uint32_t base = 0;
+        if (lane == static_cast<uint32_t>(leader) && b != 0xffffffffu)
+          base = atomicAdd(&tcnt[b], static_cast<uint32_t>(__popc(peers)));
+        base = __shfl_sync(0xffffffffu, base, leader);
+        r[k] = base + __popc(peers & lt);
+      }
+    } else {
+#pragma unroll
+      for (int k = 0; k < kK1Ipt; ++k)  // ids < 2^28: 0xffffffff only marks a partial tile's end
+        if (v[k] != 0xffffffffu) r[k] = atomicAdd(&tcnt[v[k] >> kK1Shift], 1u);
+    }
     __syncthreads();
     k1_block_scan(tcnt, tst, nb, wsum);
     __syncthreads();
@@ -226,7 +264,21 @@ __global__ void __launch_bounds__(kK1HistThreads) k1_hist_kernel(const uint32_t*
     for (uint32_t i = m.begin + threadIdx.x; i < hb_end; i += blockDim.x)
       atomicAdd(&hb[part[i] & (kK1Bins - 1)], 1u);
     const uint32_t vb = hb_end, ve = vb + ((m.end - vb) & ~3u);
-    for (uint32_t i = vb + 4 * threadIdx.x; i < ve; i += 4 * blockDim.x) {
+    const uint32_t step = 4 * blockDim.x;
+    uint32_t i = vb + 4 * threadIdx.x;
+    for (; i + 3 * step < ve; i += 4 * step) {  // four 16 B loads in flight per thread
+      uint4 v[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) v[q] = __ldcs(reinterpret_cast<const uint4*>(part + i + q * step));
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        atomicAdd(&hb[v[q].x & (kK1Bins - 1)], 1u);
+        atomicAdd(&hb[v[q].y & (kK1Bins - 1)], 1u);
+        atomicAdd(&hb[v[q].z & (kK1Bins - 1)], 1u);
+        atomicAdd(&hb[v[q].w & (kK1Bins - 1)], 1u);
+      }
+    }
+    for (; i < ve; i += step) {
       const uint4 v = __ldcs(reinterpret_cast<const uint4*>(part + i));
       atomicAdd(&hb[v.x & (kK1Bins - 1)], 1u);
       atomicAdd(&hb[v.y & (kK1Bins - 1)], 1u);
@@ -267,7 +319,11 @@ bool compute_indeg_binned(tg_ctx* ctx, const uint32_t* tgt, uint64_t e, uint64_t
 
   const size_t scat_smem = 4 * (kK1Tile + 3 * (size_t)nb);
   if (!attr[ctx->device % TG_MAX_DEVICES]) {
-    TGB_CUDA(cudaFuncSetAttribute(k1_scatter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    TGB_CUDA(cudaFuncSetAttribute(k1_scatter_kernel<false>,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  4 * (kK1Tile + 3 * kK1MaxBuckets)));
+    TGB_CUDA(cudaFuncSetAttribute(k1_scatter_kernel<true>,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   4 * (kK1Tile + 3 * kK1MaxBuckets)));
     TGB_CUDA(cudaFuncSetAttribute(k1_hist_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   4 * kK1Bins));
@@ -276,8 +332,13 @@ bool compute_indeg_binned(tg_ctx* ctx, const uint32_t* tgt, uint64_t e, uint64_t
     attr[ctx->device % TG_MAX_DEVICES] = true;
   }
   int occ = 0;
-  TGB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k1_scatter_kernel, kK1Threads,
-                                                         scat_smem));
+  const bool agg = nb <= kK1AggMaxBuckets;
+  if (agg)
+    TGB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k1_scatter_kernel<true>,
+                                                           kK1Threads, scat_smem));
+  else
+    TGB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k1_scatter_kernel<false>,
+                                                           kK1Threads, scat_smem));
   occ = std::max(occ, 1);
   // one wave of chunks; each chunk a whole number of tiles
   uint64_t chunk = (e + (uint64_t)ctx->num_sms * occ - 1) / ((uint64_t)ctx->num_sms * occ);
@@ -304,7 +365,12 @@ bool compute_indeg_binned(tg_ctx* ctx, const uint32_t* tgt, uint64_t e, uint64_t
   k1_count_kernel<<<G, kK1Threads, 4 * nb, ctx->stream>>>(tgt, e, chunk, nb, G, cnt);
   TGB_LAUNCHED();
   exclusive_scan_u64(ctx, cnt, ncnt);
-  k1_scatter_kernel<<<G, kK1Threads, scat_smem, ctx->stream>>>(tgt, e, chunk, nb, G, cnt, part);
+  if (agg)
+    k1_scatter_kernel<true><<<G, kK1Threads, scat_smem, ctx->stream>>>(tgt, e, chunk, nb, G, cnt,
+                                                                       part);
+  else
+    k1_scatter_kernel<false><<<G, kK1Threads, scat_smem, ctx->stream>>>(tgt, e, chunk, nb, G, cnt,
+                                                                        part);
   TGB_LAUNCHED();
   k1_items_kernel<<<1, 1024, 0, ctx->stream>>>(cnt, nb, G, items, small);
   TGB_LAUNCHED();
