@@ -344,7 +344,10 @@ int tg_host_shared_unmap(void* p, uint64_t bytes);
 int tg_host_shared_unlink(const char* name);
 
 /* K8: copy rows ids[0..n) (host|device) into dst (n x row_bytes, host|device)
- * and accumulate the reference accounting into report (host). Synchronous. */
+ * and accumulate the reference accounting into report (host). Synchronous:
+ * returns once every row is in dst and the report is final (device dst: when
+ * the kernel's last CTA has posted the counters to mapped host memory, before
+ * the stream drains; host dst: after the copy back). */
 int tg_gather_rows(tg_store* s, const uint64_t* ids, uint64_t n, void* dst, tg_report* report);
 /* Same, stream-ordered: ids_dev/dst_dev device pointers, counters_dev = 3 x
  * u64 device accumulator {local, peer, host} accesses, err_dev = 1 x u64
