@@ -579,7 +579,7 @@ __global__ void __launch_bounds__(256) perm_part_kernel(const uint32_t* __restri
     for (uint32_t j = threadIdx.x; j < tn; j += blockDim.x) {
       const uint2 p = st[j];
       const uint32_t b = p.x >> kPmShift;
-      pairs[((uint64_t)b << kPmShift) + tbase[b] + (j - tst[b])] = p;
+      pairs[tbase[b] + (j - tst[b])] = p;  // bcur starts at the bucket's region
     }
     __syncthreads();
   }
@@ -604,8 +604,11 @@ __global__ void __launch_bounds__(kPmSubThreads) perm_sub_kernel(const uint2* __
   for (uint64_t t0 = (uint64_t)blockIdx.x * kPmSubTile; t0 < n;
        t0 += (uint64_t)gridDim.x * kPmSubTile) {
     const uint32_t tn = static_cast<uint32_t>(n - t0 < (uint64_t)kPmSubTile ? n - t0 : kPmSubTile);
-    // the tile's first bucket: pairs [t0, ...) belong to buckets t0 >> 20 and, at most, the next
-    const uint32_t sb0 = static_cast<uint32_t>(t0 >> kPmShift) << (kPmShift - kPmSubShift);
+    // the window of sub-buckets: from the first one of the tile's first bucket
+    // (a tile of full 1 Mi-id bucket regions spans at most two buckets; pairs
+    // beyond the window -- small regions after tail compaction -- take one
+    // slot each)
+    const uint32_t sb0 = (__ldg(&in[t0].x) >> kPmShift) << (kPmShift - kPmSubShift);
     tcnt[threadIdx.x] = 0;
     __syncthreads();
     uint2 p[kPmSubIpt];
@@ -613,9 +616,16 @@ __global__ void __launch_bounds__(kPmSubThreads) perm_sub_kernel(const uint2* __
 #pragma unroll
     for (int k = 0; k < kPmSubIpt; ++k) {
       const uint32_t j = k * kPmSubThreads + threadIdx.x;
+      p[k] = make_uint2(0xffffffffu, 0u);
       if (j < tn) {
-        p[k] = __ldcs(in + t0 + j);
-        rk[k] = atomicAdd(&tcnt[(p[k].x >> kPmSubShift) - sb0], 1u);
+        const uint2 q = __ldcs(in + t0 + j);
+        const uint32_t lb = (q.x >> kPmSubShift) - sb0;
+        if (lb < kPmSubLocal) {
+          p[k] = q;
+          rk[k] = atomicAdd(&tcnt[lb], 1u);
+        } else {
+          out[atomicAdd(&scur[q.x >> kPmSubShift], 1u)] = q;
+        }
       }
     }
     __syncthreads();
@@ -636,33 +646,69 @@ __global__ void __launch_bounds__(kPmSubThreads) perm_sub_kernel(const uint2* __
     }
     __syncthreads();
 #pragma unroll
-    for (int k = 0; k < kPmSubIpt; ++k) {
-      const uint32_t j = k * kPmSubThreads + threadIdx.x;
-      if (j < tn) sst[tst[(p[k].x >> kPmSubShift) - sb0] + rk[k]] = p[k];
-    }
+    for (int k = 0; k < kPmSubIpt; ++k)
+      if (p[k].x != 0xffffffffu) sst[tst[(p[k].x >> kPmSubShift) - sb0] + rk[k]] = p[k];
     __syncthreads();
-    for (uint32_t j = threadIdx.x; j < tn; j += blockDim.x) {
+    const uint32_t ns = tst[kPmSubLocal - 1] + tcnt[kPmSubLocal - 1];  // in-window pairs
+    for (uint32_t j = threadIdx.x; j < ns; j += blockDim.x) {
       const uint2 q = sst[j];
       const uint32_t lb = (q.x >> kPmSubShift) - sb0;
-      out[((uint64_t)(sb0 + lb) << kPmSubShift) + tbase[lb] + (j - tst[lb])] = q;
+      out[tbase[lb] + (j - tst[lb])] = q;  // scur starts at the sub-bucket's region
     }
     __syncthreads();
   }
 }
 
+// Region starts of the ranked (non-tail) pairs: bucket b of width 2^shift
+// starts at x - T(x), x = min(b << shift, n), T(x) = tail ids below x (the
+// tail is sorted); starts[count] = m.
+__global__ void perm_bounds_kernel(const uint32_t* __restrict__ tail, uint64_t nt, uint64_t count,
+                                   int shift, uint64_t n, uint32_t* __restrict__ starts,
+                                   uint32_t* __restrict__ cursor) {
+  for (uint64_t b = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; b <= count;
+       b += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t x = (b << shift) < n ? (b << shift) : n;
+    uint64_t lo = 0, hi = nt;  // lower_bound(tail, x)
+    while (lo < hi) {
+      const uint64_t mid = (lo + hi) / 2;
+      if (tail[mid] < x) lo = mid + 1;
+      else hi = mid;
+    }
+    starts[b] = static_cast<uint32_t>(x - lo);
+    if (cursor && b < count) cursor[b] = static_cast<uint32_t>(x - lo);
+  }
+}
+
+// order[r] for the compacted tail: the ids in their (ascending) order
+__global__ void order_tail_kernel(const uint32_t* __restrict__ tail, uint64_t nt, uint64_t m,
+                                  uint64_t* __restrict__ order) {
+  for (uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; t < nt;
+       t += (uint64_t)gridDim.x * blockDim.x)
+    order[m + t] = tail[t];
+}
+
 // (3) one CTA per sub-bucket: new_id_of of its 4,096 ids assembled in shared
 // memory, then stored as whole sectors
 __global__ void __launch_bounds__(256) perm_fill_kernel(const uint2* __restrict__ in, uint64_t n,
+                                                        uint64_t m,
+                                                        const uint32_t* __restrict__ tail,
+                                                        const uint32_t* __restrict__ sbstart,
                                                         uint64_t* __restrict__ new_id_of) {
   __shared__ uint32_t r[1u << kPmSubShift];
   const uint64_t nsb = (n + (1u << kPmSubShift) - 1) >> kPmSubShift;
   for (uint64_t sb = blockIdx.x; sb < nsb; sb += gridDim.x) {
     const uint64_t i0 = sb << kPmSubShift;
-    const uint32_t cnt = static_cast<uint32_t>(n - i0 < (1u << kPmSubShift) ? n - i0 : (1u << kPmSubShift));
-    for (uint32_t j = threadIdx.x; j < cnt; j += blockDim.x) {
-      const uint2 q = __ldcs(in + i0 + j);
+    const uint64_t i1 = n - i0 < (1u << kPmSubShift) ? n : i0 + (1u << kPmSubShift);
+    const uint32_t cnt = static_cast<uint32_t>(i1 - i0);
+    const uint32_t h0 = sbstart[sb], h1 = sbstart[sb + 1];  // this sub-bucket's ranked pairs
+    for (uint32_t j = h0 + threadIdx.x; j < h1; j += blockDim.x) {
+      const uint2 q = __ldcs(in + j);
       r[q.x & ((1u << kPmSubShift) - 1)] = q.y;
     }
+    // its ids among the compacted lowest-score ties (tail[t] has rank m + t):
+    // tail ids < x number x - sbstart(x)
+    for (uint64_t t = (i0 - h0) + threadIdx.x; t < i1 - h1; t += blockDim.x)
+      r[tail[t] & ((1u << kPmSubShift) - 1)] = static_cast<uint32_t>(m + t);
     __syncthreads();
     for (uint32_t j = threadIdx.x; j < cnt; j += blockDim.x) new_id_of[i0 + j] = r[j];
     __syncthreads();
@@ -718,18 +764,36 @@ void sort_scores(tg_ctx* ctx, const double* scores_dev, uint64_t n, uint64_t* or
   if (m) radix_passes(ctx, k0, v0, k1, v1, m, 8, plan, hist, 8, 4);
   const uint64_t nb = (n + (1ull << kPmShift) - 1) >> kPmShift;
   if (perm_dev && nb <= kPmMaxBuckets) {
-    uint32_t* bcur = ctx->scratch_t<uint32_t>(kScratchE, kPmMaxBuckets);
-    TGB_CUDA(cudaMemsetAsync(bcur, 0, 4 * nb, ctx->stream));
-    // both key buffers are free after the sort; pairs (8N bytes) go in k0
+    // ranks [0, m) come from the sort; the compacted lowest-score ties (sorted
+    // ids, ranks m..n-1) sit in v0[m, n) (and v1[m, n)): they skip the
+    // partition and are merged in by perm_fill
+    const uint32_t* tail = v0 + m;
+    const uint64_t nt = n - m;
+    const uint64_t nsb = (n + (1u << kPmSubShift) - 1) >> kPmSubShift;
+    uint32_t* bstart = ctx->scratch_t<uint32_t>(kScratchE, 2 * (kPmMaxBuckets + 1) + 2 * (nsb + 1));
+    uint32_t* bcur = bstart + kPmMaxBuckets + 1;
+    uint32_t* sbstart = bcur + kPmMaxBuckets + 1;
+    uint32_t* scur = sbstart + nsb + 1;
+    perm_bounds_kernel<<<grid_for(nb + 1, 256), 256, 0, ctx->stream>>>(tail, nt, nb, kPmShift, n,
+                                                                        bstart, bcur);
+    TGB_LAUNCHED();
+    perm_bounds_kernel<<<grid_for(nsb + 1, 256), 256, 0, ctx->stream>>>(tail, nt, nsb, kPmSubShift,
+                                                                         n, sbstart, scur);
+    TGB_LAUNCHED();
+    // both key buffers are free after the sort; pairs (8m bytes) go in k0
     uint2* pairs = reinterpret_cast<uint2*>(k0);
     int pocc = 1;
     TGB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&pocc, perm_part_kernel, 256, 0));
-    perm_part_kernel<<<grid_for(n, kPmTile, ctx->num_sms * std::max(pocc, 1)), 256, 0, ctx->stream>>>(
-        v0, v1, plan, n, static_cast<uint32_t>(nb), order_dev, pairs, bcur);
+    if (m)
+      perm_part_kernel<<<grid_for(m, kPmTile, ctx->num_sms * std::max(pocc, 1)), 256, 0,
+                         ctx->stream>>>(v0, v1, plan, m, static_cast<uint32_t>(nb), order_dev,
+                                        pairs, bcur);
     TGB_LAUNCHED();
-    const uint64_t nsb = (n + (1u << kPmSubShift) - 1) >> kPmSubShift;
-    uint32_t* scur = ctx->scratch_t<uint32_t>(kScratchF, nsb);
-    TGB_CUDA(cudaMemsetAsync(scur, 0, 4 * nsb, ctx->stream));
+    if (order_dev && nt) {
+      order_tail_kernel<<<grid_for(nt, 256, ctx->num_sms * 8), 256, 0, ctx->stream>>>(tail, nt, m,
+                                                                                      order_dev);
+      TGB_LAUNCHED();
+    }
     uint2* pairs2 = reinterpret_cast<uint2*>(k1);
     static bool sattr[TG_MAX_DEVICES] = {};
     if (!sattr[ctx->device % TG_MAX_DEVICES]) {
@@ -740,11 +804,12 @@ void sort_scores(tg_ctx* ctx, const double* scores_dev, uint64_t n, uint64_t* or
     int occ = 1;
     TGB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, perm_sub_kernel, kPmSubThreads,
                                                            8 * kPmSubTile));
-    perm_sub_kernel<<<grid_for(n, kPmSubTile, ctx->num_sms * std::max(occ, 1)), kPmSubThreads,
-                      8 * kPmSubTile, ctx->stream>>>(pairs, n, pairs2, scur);
+    if (m)
+      perm_sub_kernel<<<grid_for(m, kPmSubTile, ctx->num_sms * std::max(occ, 1)), kPmSubThreads,
+                        8 * kPmSubTile, ctx->stream>>>(pairs, m, pairs2, scur);
     TGB_LAUNCHED();
-    perm_fill_kernel<<<grid_for(nsb, 1, ctx->num_sms * 8), 256, 0, ctx->stream>>>(pairs2, n,
-                                                                                  perm_dev);
+    perm_fill_kernel<<<grid_for(nsb, 1, ctx->num_sms * 8), 256, 0, ctx->stream>>>(
+        pairs2, n, m, tail, sbstart, perm_dev);
     TGB_LAUNCHED();
   } else {
     perm_kernel<<<grid_for(n, 256), 256, 0, ctx->stream>>>(v0, v1, plan, n, order_dev, perm_dev);
