@@ -7,9 +7,9 @@
 // the same rate), 15.8 ms for papers100M's 1.53 G targets. Shared-memory
 // atomics retire an order of magnitude faster, but 111 M counters do not fit
 // one SM. So:
-//   1. count   per-chunk counts of the BUCKET b = t >> 15 (32,768 ids per
-//              bucket; <= 8,192 buckets), one CTA per chunk of the target
-//              array, shared-memory histogram;
+//   1. count   per-chunk counts of the BUCKET b = t >> bs (2^bs ids per
+//              bucket, bs in [15, 18], <= ~2,048 buckets), one CTA per chunk
+//              of the target array, shared-memory histogram;
 //   2. scan    bucket-major exclusive scan of the (bucket, chunk) counts: the
 //              chunk's write cursor inside each bucket's segment of a
 //              temporary copy of the targets;
@@ -17,8 +17,9 @@
 //              by bucket in shared memory and writes it out in bucket runs
 //              (coalesced; the <= 8,192 open run ends stay in L2, so DRAM
 //              sees full sectors);
-//   4. count   one CTA per (bucket, <= 1 M element piece), persistent: a
-//              32,768-bin shared-memory histogram of the piece, flushed with
+//   4. count   2^(bs-15) CTAs per (bucket, <= 256k-target piece), persistent:
+//              each a 32,768-bin shared-memory histogram of its id range of
+//              the piece (the CTAs of one piece read it from L2), flushed with
 //              plain coalesced stores when the bucket is one piece, with
 //              atomics when a hub bucket is split over several.
 // With thousands of buckets (C3: 3,388) a tile's runs are ~2 targets long,
@@ -61,7 +62,7 @@ constexpr int kK1HistThreads = 1024;
 // (1) per-chunk bucket counts, bucket-major: cnt[b * G + c]
 __global__ void __launch_bounds__(kK1Threads) k1_count_kernel(const uint32_t* __restrict__ tgt,
                                                               uint64_t e, uint64_t chunk,
-                                                              uint32_t nb, uint32_t G,
+                                                              uint32_t nb, uint32_t G, int bs,
                                                               uint64_t* __restrict__ cnt) {
   extern __shared__ uint32_t h[];  // nb
   for (uint32_t i = threadIdx.x; i < nb; i += blockDim.x) h[i] = 0;
@@ -77,20 +78,20 @@ __global__ void __launch_bounds__(kK1Threads) k1_count_kernel(const uint32_t* __
     for (int q = 0; q < 4; ++q) v[q] = __ldcs(reinterpret_cast<const uint4*>(tgt + i + q * step));
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
-      atomicAdd(&h[v[q].x >> kK1Shift], 1u);
-      atomicAdd(&h[v[q].y >> kK1Shift], 1u);
-      atomicAdd(&h[v[q].z >> kK1Shift], 1u);
-      atomicAdd(&h[v[q].w >> kK1Shift], 1u);
+      atomicAdd(&h[v[q].x >> bs], 1u);
+      atomicAdd(&h[v[q].y >> bs], 1u);
+      atomicAdd(&h[v[q].z >> bs], 1u);
+      atomicAdd(&h[v[q].w >> bs], 1u);
     }
   }
   for (; i < v1; i += step) {
     const uint4 v = __ldcs(reinterpret_cast<const uint4*>(tgt + i));
-    atomicAdd(&h[v.x >> kK1Shift], 1u);
-    atomicAdd(&h[v.y >> kK1Shift], 1u);
-    atomicAdd(&h[v.z >> kK1Shift], 1u);
-    atomicAdd(&h[v.w >> kK1Shift], 1u);
+    atomicAdd(&h[v.x >> bs], 1u);
+    atomicAdd(&h[v.y >> bs], 1u);
+    atomicAdd(&h[v.z >> bs], 1u);
+    atomicAdd(&h[v.w >> bs], 1u);
   }
-  for (uint64_t j = v1 + threadIdx.x; j < c1; j += blockDim.x) atomicAdd(&h[tgt[j] >> kK1Shift], 1u);
+  for (uint64_t j = v1 + threadIdx.x; j < c1; j += blockDim.x) atomicAdd(&h[tgt[j] >> bs], 1u);
   __syncthreads();
   for (uint32_t b = threadIdx.x; b < nb; b += blockDim.x) cnt[(uint64_t)b * G + blockIdx.x] = h[b];
 }
@@ -127,7 +128,7 @@ __device__ __forceinline__ void k1_block_scan(const uint32_t* c, uint32_t* s, ui
 template <bool Agg>
 __global__ void __launch_bounds__(kK1Threads, 2) k1_scatter_kernel(const uint32_t* __restrict__ tgt,
                                                                 uint64_t e, uint64_t chunk,
-                                                                uint32_t nb, uint32_t G,
+                                                                uint32_t nb, uint32_t G, int bs,
                                                                 const uint64_t* __restrict__ cnt,
                                                                 uint32_t* __restrict__ out) {
   extern __shared__ __align__(16) uint32_t sm[];
@@ -164,7 +165,7 @@ __global__ void __launch_bounds__(kK1Threads, 2) k1_scatter_kernel(const uint32_
       const uint32_t lane = threadIdx.x & 31, lt = (1u << lane) - 1u;
 #pragma unroll
       for (int k = 0; k < kK1Ipt; ++k) {
-        const uint32_t b = v[k] != 0xffffffffu ? v[k] >> kK1Shift : 0xffffffffu;
+        const uint32_t b = v[k] != 0xffffffffu ? v[k] >> bs : 0xffffffffu;
         const uint32_t peers = __match_any_sync(0xffffffffu, b);
         const int leader = __ffs(peers) - 1;
         uint32_t base = 0;
@@ -176,17 +177,17 @@ __global__ void __launch_bounds__(kK1Threads, 2) k1_scatter_kernel(const uint32_
     } else {
 #pragma unroll
       for (int k = 0; k < kK1Ipt; ++k)  // ids < 2^28: 0xffffffff only marks a partial tile's end
-        if (v[k] != 0xffffffffu) r[k] = atomicAdd(&tcnt[v[k] >> kK1Shift], 1u);
+        if (v[k] != 0xffffffffu) r[k] = atomicAdd(&tcnt[v[k] >> bs], 1u);
     }
     __syncthreads();
     k1_block_scan(tcnt, tst, nb, wsum);
     __syncthreads();
 #pragma unroll
     for (int k = 0; k < kK1Ipt; ++k)
-      if (v[k] != 0xffffffffu) st[tst[v[k] >> kK1Shift] + r[k]] = v[k];
+      if (v[k] != 0xffffffffu) st[tst[v[k] >> bs] + r[k]] = v[k];
     __syncthreads();
     for (uint32_t j = threadIdx.x; j < tn; j += blockDim.x) {
-      const uint32_t t = st[j], b = t >> kK1Shift;
+      const uint32_t t = st[j], b = t >> bs;
       out[cur[b] + (j - tst[b])] = t;
     }
     __syncthreads();
@@ -243,26 +244,32 @@ __global__ void __launch_bounds__(1024) k1_items_kernel(const uint64_t* __restri
 }
 
 // (4) persistent: claim a piece, histogram it into 32,768 shared counters, flush.
+// A bucket of 2^bs ids (bs >= 15) is counted by 2^(bs-15) CTAs per piece,
+// each over its own 32,768-id range: every CTA reads the whole piece (the
+// others' reads of it hit L2) and skips the targets outside its range.
 __global__ void __launch_bounds__(kK1HistThreads) k1_hist_kernel(const uint32_t* __restrict__ part,
                                                                  const K1Item* __restrict__ items,
                                                                  const uint32_t* __restrict__ nitems,
                                                                  uint32_t* __restrict__ ctr,
-                                                                 uint64_t n,
+                                                                 uint64_t n, int bs,
                                                                  uint32_t* __restrict__ deg) {
   extern __shared__ __align__(16) uint32_t hb[];  // kK1Bins
   __shared__ uint32_t item_s;
-  const uint32_t ni = *nitems;
+  const int qs = bs - kK1Shift;  // log2 of the CTAs per piece
+  const uint32_t qm = (1u << qs) - 1;
+  const uint32_t ni = *nitems << qs;
   for (;;) {
     if (threadIdx.x == 0) item_s = atomicAdd(ctr, 1u);
     for (uint32_t i = threadIdx.x; i < kK1Bins; i += blockDim.x) hb[i] = 0;
     __syncthreads();
     const uint32_t it = item_s;
     if (it >= ni) break;
-    const K1Item m = items[it];
+    const K1Item m = items[it >> qs];
+    const uint32_t qr = it & qm;  // this CTA's 32,768-id range of the bucket
     // head to a 16 B boundary, uint4 body, tail
     const uint32_t hb_end = min(m.end, (m.begin + 3u) & ~3u);
     for (uint32_t i = m.begin + threadIdx.x; i < hb_end; i += blockDim.x)
-      atomicAdd(&hb[part[i] & (kK1Bins - 1)], 1u);
+      { const uint32_t t = part[i]; if (((t >> kK1Shift) & qm) == qr) atomicAdd(&hb[t & (kK1Bins - 1)], 1u); }
     const uint32_t vb = hb_end, ve = vb + ((m.end - vb) & ~3u);
     const uint32_t step = 4 * blockDim.x;
     uint32_t i = vb + 4 * threadIdx.x;
@@ -272,24 +279,25 @@ __global__ void __launch_bounds__(kK1HistThreads) k1_hist_kernel(const uint32_t*
       for (int q = 0; q < 4; ++q) v[q] = __ldcs(reinterpret_cast<const uint4*>(part + i + q * step));
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
-        atomicAdd(&hb[v[q].x & (kK1Bins - 1)], 1u);
-        atomicAdd(&hb[v[q].y & (kK1Bins - 1)], 1u);
-        atomicAdd(&hb[v[q].z & (kK1Bins - 1)], 1u);
-        atomicAdd(&hb[v[q].w & (kK1Bins - 1)], 1u);
+        if (((v[q].x >> kK1Shift) & qm) == qr) atomicAdd(&hb[v[q].x & (kK1Bins - 1)], 1u);
+        if (((v[q].y >> kK1Shift) & qm) == qr) atomicAdd(&hb[v[q].y & (kK1Bins - 1)], 1u);
+        if (((v[q].z >> kK1Shift) & qm) == qr) atomicAdd(&hb[v[q].z & (kK1Bins - 1)], 1u);
+        if (((v[q].w >> kK1Shift) & qm) == qr) atomicAdd(&hb[v[q].w & (kK1Bins - 1)], 1u);
       }
     }
     for (; i < ve; i += step) {
       const uint4 v = __ldcs(reinterpret_cast<const uint4*>(part + i));
-      atomicAdd(&hb[v.x & (kK1Bins - 1)], 1u);
-      atomicAdd(&hb[v.y & (kK1Bins - 1)], 1u);
-      atomicAdd(&hb[v.z & (kK1Bins - 1)], 1u);
-      atomicAdd(&hb[v.w & (kK1Bins - 1)], 1u);
+      if (((v.x >> kK1Shift) & qm) == qr) atomicAdd(&hb[v.x & (kK1Bins - 1)], 1u);
+      if (((v.y >> kK1Shift) & qm) == qr) atomicAdd(&hb[v.y & (kK1Bins - 1)], 1u);
+      if (((v.z >> kK1Shift) & qm) == qr) atomicAdd(&hb[v.z & (kK1Bins - 1)], 1u);
+      if (((v.w >> kK1Shift) & qm) == qr) atomicAdd(&hb[v.w & (kK1Bins - 1)], 1u);
     }
     for (uint32_t i = ve + threadIdx.x; i < m.end; i += blockDim.x)
-      atomicAdd(&hb[part[i] & (kK1Bins - 1)], 1u);
+      { const uint32_t t = part[i]; if (((t >> kK1Shift) & qm) == qr) atomicAdd(&hb[t & (kK1Bins - 1)], 1u); }
     __syncthreads();
-    const uint64_t id0 = (uint64_t)m.bucket << kK1Shift;
-    const uint32_t nbin = static_cast<uint32_t>((n - id0 < kK1Bins ? n - id0 : (uint64_t)kK1Bins));
+    const uint64_t id0 = ((uint64_t)m.bucket << bs) + ((uint64_t)qr << kK1Shift);
+    const uint32_t nbin =
+        id0 >= n ? 0u : static_cast<uint32_t>((n - id0 < kK1Bins ? n - id0 : (uint64_t)kK1Bins));
     if (m.split) {
       for (uint32_t i = threadIdx.x; i < nbin; i += blockDim.x)
         if (hb[i]) atomicAdd(&deg[id0 + i], hb[i]);
@@ -310,7 +318,15 @@ bool compute_indeg_binned(tg_ctx* ctx, const uint32_t* tgt, uint64_t e, uint64_t
   } else if (e < (1u << 20) || n <= 12288) {
     return false;  // launch-bound sizes: the one-pass kernel is cheaper
   }
-  const uint64_t nb64 = (n + kK1Bins - 1) >> kK1Shift;
+  // bucket width 2^bs: at most ~2,048 buckets (longer scatter runs, fewer
+  // partial sectors), at least the 32,768 ids of one shared-memory histogram
+  // and at most 8 of them (C3: 2^16, 1,694 buckets: 11.8 ms against 14.4 at
+  // 2^15, 12.6 at 2^17, 14.7 at 2^18; profiles/r02k1f). TIERGRAPH_K1_BS
+  // overrides (experiments).
+  int bs = kK1Shift;
+  while (bs < kK1Shift + 3 && ((n + (1ull << bs) - 1) >> bs) > 2048) ++bs;
+  if (const char* b = std::getenv("TIERGRAPH_K1_BS")) bs = std::max(kK1Shift, std::min(kK1Shift + 3, std::atoi(b)));
+  const uint64_t nb64 = (n + (1ull << bs) - 1) >> bs;
   if (nb64 > kK1MaxBuckets || e == 0 || e >= 0xffffffffull ||
       (reinterpret_cast<uintptr_t>(tgt) & 15))
     return false;
@@ -362,21 +378,21 @@ bool compute_indeg_binned(tg_ctx* ctx, const uint32_t* tgt, uint64_t e, uint64_t
   auto* small = reinterpret_cast<uint32_t*>(p);  // [nitems, claim counter]
   TGB_CUDA(cudaMemsetAsync(small, 0, 8, ctx->stream));
   TGB_CUDA(cudaMemsetAsync(cnt + ncnt - 1, 0, 8, ctx->stream));
-  k1_count_kernel<<<G, kK1Threads, 4 * nb, ctx->stream>>>(tgt, e, chunk, nb, G, cnt);
+  k1_count_kernel<<<G, kK1Threads, 4 * nb, ctx->stream>>>(tgt, e, chunk, nb, G, bs, cnt);
   TGB_LAUNCHED();
   exclusive_scan_u64(ctx, cnt, ncnt);
   if (agg)
-    k1_scatter_kernel<true><<<G, kK1Threads, scat_smem, ctx->stream>>>(tgt, e, chunk, nb, G, cnt,
-                                                                       part);
+    k1_scatter_kernel<true><<<G, kK1Threads, scat_smem, ctx->stream>>>(tgt, e, chunk, nb, G, bs,
+                                                                       cnt, part);
   else
-    k1_scatter_kernel<false><<<G, kK1Threads, scat_smem, ctx->stream>>>(tgt, e, chunk, nb, G, cnt,
-                                                                        part);
+    k1_scatter_kernel<false><<<G, kK1Threads, scat_smem, ctx->stream>>>(tgt, e, chunk, nb, G, bs,
+                                                                        cnt, part);
   TGB_LAUNCHED();
   k1_items_kernel<<<1, 1024, 0, ctx->stream>>>(cnt, nb, G, items, small);
   TGB_LAUNCHED();
   // persistent: as many 1024-thread CTAs per SM as shared memory allows (2 at most)
   k1_hist_kernel<<<ctx->num_sms * (kK1Bins <= 16384 ? 2 : 1), kK1HistThreads, 4 * kK1Bins,
-                   ctx->stream>>>(part, items, small, small + 1, n, deg);
+                   ctx->stream>>>(part, items, small, small + 1, n, bs, deg);
   TGB_LAUNCHED();
   TGB_CUDA(cudaFreeAsync(base, ctx->stream));
   return true;

@@ -231,20 +231,24 @@ def test_fused_peer_exchange_virtual_ranks(tg, ctx, ranks):
     assert all(o.cpu().numpy().tobytes() == want_un.tobytes() for o in un)
 
 
-@pytest.mark.parametrize("k1", ["", "atomic"])
+@pytest.mark.parametrize("k1", ["", "atomic", "bs17"])
 @pytest.mark.parametrize("n,draws", [(200_000, 5_000_000), (1_500_000, 6_000_000),
                                      (6_000_000, 8_000_000)])
 def test_in_degrees_large_graphs(tg, ctx, monkeypatch, n, draws, k1):
     """K1 on graphs with >= 4M edges (R-MAT hubs, privatised low ids, one id
     holding 1.5M edges) equals csr_graph.cpp:89-93 exactly, in both forms:
     binned (partition + shared-memory histograms, the default at these sizes;
-    the 1.5M-edge bucket is split over two histogram pieces; 184 buckets at
-    6M nodes) and one-pass atomic (TIERGRAPH_K1=atomic)."""
+    the 1.5M-edge bucket is split over histogram pieces; 184 buckets at 6M
+    nodes; TIERGRAPH_K1_BS=17: 2^17-id buckets, each piece counted by four
+    CTAs over their own ranges, the C3 shape) and one-pass atomic
+    (TIERGRAPH_K1=atomic)."""
     from paper_2111_05894_b200 import synth
-    if k1:
+    monkeypatch.delenv("TIERGRAPH_K1", raising=False)
+    monkeypatch.delenv("TIERGRAPH_K1_BS", raising=False)
+    if k1 == "bs17":  # 2^17-id buckets, four histogram CTAs per piece (the C3 shape)
+        monkeypatch.setenv("TIERGRAPH_K1_BS", "17")
+    elif k1:
         monkeypatch.setenv("TIERGRAPH_K1", k1)
-    else:
-        monkeypatch.delenv("TIERGRAPH_K1", raising=False)
     off, tgt = synth.rmat_graph(n, draws, seed=11)
     assert len(tgt) >= 1 << 22
     want = np.bincount(tgt.astype(np.int64), minlength=n).astype(np.uint64)
