@@ -54,7 +54,10 @@ constexpr uint32_t kK1MaxBuckets = 8192;        // n <= 2^28
 #define TG_K1_AGG_MAX 0    // 475 vs 403 us -- __match_any_sync + spills cost more than
 #endif                     // the same-bucket atomics save; profiles/r02k1d)
 constexpr uint32_t kK1AggMaxBuckets = TG_K1_AGG_MAX;
-constexpr int kK1Threads = 512, kK1Ipt = 16;
+#ifndef TG_K1_THREADS  // threads of the count / scatter CTAs (tile = 16 per thread)
+#define TG_K1_THREADS 512
+#endif
+constexpr int kK1Threads = TG_K1_THREADS, kK1Ipt = 16;
 constexpr uint32_t kK1Tile = kK1Threads * kK1Ipt;  // 8,192 targets per scatter tile
 constexpr uint32_t kK1Piece = 1u << TG_K1_PIECE_LOG2;  // elements per histogram work item
 constexpr int kK1HistThreads = 1024;
@@ -126,7 +129,7 @@ __device__ __forceinline__ void k1_block_scan(const uint32_t* c, uint32_t* s, ui
 // ranks with one shared-memory atomic (leader + popc) instead of one each --
 // R-MAT puts ~19 % of C2's targets in bucket 0.
 template <bool Agg>
-__global__ void __launch_bounds__(kK1Threads, 2) k1_scatter_kernel(const uint32_t* __restrict__ tgt,
+__global__ void __launch_bounds__(kK1Threads, 1024 / kK1Threads) k1_scatter_kernel(const uint32_t* __restrict__ tgt,
                                                                 uint64_t e, uint64_t chunk,
                                                                 uint32_t nb, uint32_t G, int bs,
                                                                 const uint64_t* __restrict__ cnt,
