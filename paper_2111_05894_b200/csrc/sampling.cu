@@ -726,7 +726,12 @@ int tg_sample_batches(tg_sampler* s, const uint64_t* order, uint64_t n_order, ui
                    std::to_string(nb_all) + " batches of the order");
     tg_ctx* ctx = s->ctx;
     DeviceGuard dg(ctx->device);
-    const uint64_t* od = dev_in(ctx, order, n_order, kStageIn1);
+    // only the called batches' seeds cross to the device (a host order of a
+    // whole epoch -- 11M ids at C3 -- is not re-sent for every 32 batches);
+    // od is indexed by order position either way
+    const uint64_t beg0 = first_batch * batch_size;
+    const uint64_t m = std::min(n_order, (first_batch + nbatches) * batch_size) - beg0;
+    const uint64_t* od = dev_in(ctx, order + beg0, m, kStageIn1) - beg0;
     DevOut<uint64_t> offs(ctx, out_offsets, nbatches + 1, kStageOut0);
     TGB_CUDA(cudaMemsetAsync(offs.dev(), 0, 8, ctx->stream));
     uint64_t* md = out_members;
@@ -754,8 +759,6 @@ int tg_sample_batches(tg_sampler* s, const uint64_t* order, uint64_t n_order, ui
     auto lane = [&](uint64_t k) { return k % L == 0 ? s : s->lanes[k % L - 1]; };
     // every seed of the called batches range-checked once (sampling.cpp:61-62);
     // the first offending position is read back with the output total
-    const uint64_t beg0 = first_batch * batch_size;
-    const uint64_t m = std::min(n_order, (first_batch + nbatches) * batch_size) - beg0;
     auto* obad = reinterpret_cast<unsigned long long*>(s->small + kSmallOrderBad);
     TGB_CUDA(cudaMemsetAsync(obad, 0xff, 8, ctx->stream));
     if (m) {
