@@ -50,10 +50,6 @@ namespace tgb {
 constexpr int kK1Shift = TG_K1_SHIFT;
 constexpr uint32_t kK1Bins = 1u << kK1Shift;    // ids per bucket (128 KB of counters)
 constexpr uint32_t kK1MaxBuckets = 8192;        // n <= 2^28
-#ifndef TG_K1_AGG_MAX  // warp-aggregated tile ranks up to this many buckets (off: C2
-#define TG_K1_AGG_MAX 0    // 475 vs 403 us -- __match_any_sync + spills cost more than
-#endif                     // the same-bucket atomics save; profiles/r02k1d)
-constexpr uint32_t kK1AggMaxBuckets = TG_K1_AGG_MAX;
 #ifndef TG_K1_THREADS  // threads of the count / scatter CTAs (tile = 16 per thread)
 #define TG_K1_THREADS 512
 #endif
@@ -125,10 +121,8 @@ __device__ __forceinline__ void k1_block_scan(const uint32_t* c, uint32_t* s, ui
 }
 
 // (3) scatter: chunk blockIdx.x, tile by tile, bucket-ordered in shared memory.
-// Agg (few buckets): lanes of a warp with the same bucket take their tile
-// ranks with one shared-memory atomic (leader + popc) instead of one each --
-// R-MAT puts ~19 % of C2's targets in bucket 0.
-template <bool Agg>
+// (Warp-aggregated tile ranks -- one shared atomic per bucket per warp -- were
+// slower at C2: 475 vs 403 us, __match_any_sync plus spills; profiles/r02k1d.)
 __global__ void __launch_bounds__(kK1Threads, 1024 / kK1Threads) k1_scatter_kernel(const uint32_t* __restrict__ tgt,
                                                                 uint64_t e, uint64_t chunk,
                                                                 uint32_t nb, uint32_t G, int bs,
@@ -164,24 +158,9 @@ __global__ void __launch_bounds__(kK1Threads, 1024 / kK1Threads) k1_scatter_kern
         v[k] = j < tn ? tgt[t0 + j] : 0xffffffffu;
       }
     }
-    if (Agg) {
-      const uint32_t lane = threadIdx.x & 31, lt = (1u << lane) - 1u;
 #pragma unroll
-      for (int k = 0; k < kK1Ipt; ++k) {
-        const uint32_t b = v[k] != 0xffffffffu ? v[k] >> bs : 0xffffffffu;
-        const uint32_t peers = __match_any_sync(0xffffffffu, b);
-        const int leader = __ffs(peers) - 1;
-        uint32_t base = 0;
-        if (lane == static_cast<uint32_t>(leader) && b != 0xffffffffu)
-          base = atomicAdd(&tcnt[b], static_cast<uint32_t>(__popc(peers)));
-        base = __shfl_sync(0xffffffffu, base, leader);
-        r[k] = base + __popc(peers & lt);
-      }
-    } else {
-#pragma unroll
-      for (int k = 0; k < kK1Ipt; ++k)  // ids < 2^28: 0xffffffff only marks a partial tile's end
-        if (v[k] != 0xffffffffu) r[k] = atomicAdd(&tcnt[v[k] >> bs], 1u);
-    }
+    for (int k = 0; k < kK1Ipt; ++k)  // ids < 2^28: 0xffffffff only marks a partial tile's end
+      if (v[k] != 0xffffffffu) r[k] = atomicAdd(&tcnt[v[k] >> bs], 1u);
     __syncthreads();
     k1_block_scan(tcnt, tst, nb, wsum);
     __syncthreads();
@@ -338,11 +317,7 @@ bool compute_indeg_binned(tg_ctx* ctx, const uint32_t* tgt, uint64_t e, uint64_t
 
   const size_t scat_smem = 4 * (kK1Tile + 3 * (size_t)nb);
   if (!attr[ctx->device % TG_MAX_DEVICES]) {
-    TGB_CUDA(cudaFuncSetAttribute(k1_scatter_kernel<false>,
-                                  cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  4 * (kK1Tile + 3 * kK1MaxBuckets)));
-    TGB_CUDA(cudaFuncSetAttribute(k1_scatter_kernel<true>,
-                                  cudaFuncAttributeMaxDynamicSharedMemorySize,
+    TGB_CUDA(cudaFuncSetAttribute(k1_scatter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   4 * (kK1Tile + 3 * kK1MaxBuckets)));
     TGB_CUDA(cudaFuncSetAttribute(k1_hist_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   4 * kK1Bins));
@@ -351,13 +326,8 @@ bool compute_indeg_binned(tg_ctx* ctx, const uint32_t* tgt, uint64_t e, uint64_t
     attr[ctx->device % TG_MAX_DEVICES] = true;
   }
   int occ = 0;
-  const bool agg = nb <= kK1AggMaxBuckets;
-  if (agg)
-    TGB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k1_scatter_kernel<true>,
-                                                           kK1Threads, scat_smem));
-  else
-    TGB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k1_scatter_kernel<false>,
-                                                           kK1Threads, scat_smem));
+  TGB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k1_scatter_kernel, kK1Threads,
+                                                         scat_smem));
   occ = std::max(occ, 1);
   // one wave of chunks; each chunk a whole number of tiles
   uint64_t chunk = (e + (uint64_t)ctx->num_sms * occ - 1) / ((uint64_t)ctx->num_sms * occ);
@@ -384,12 +354,7 @@ bool compute_indeg_binned(tg_ctx* ctx, const uint32_t* tgt, uint64_t e, uint64_t
   k1_count_kernel<<<G, kK1Threads, 4 * nb, ctx->stream>>>(tgt, e, chunk, nb, G, bs, cnt);
   TGB_LAUNCHED();
   exclusive_scan_u64(ctx, cnt, ncnt);
-  if (agg)
-    k1_scatter_kernel<true><<<G, kK1Threads, scat_smem, ctx->stream>>>(tgt, e, chunk, nb, G, bs,
-                                                                       cnt, part);
-  else
-    k1_scatter_kernel<false><<<G, kK1Threads, scat_smem, ctx->stream>>>(tgt, e, chunk, nb, G, bs,
-                                                                        cnt, part);
+  k1_scatter_kernel<<<G, kK1Threads, scat_smem, ctx->stream>>>(tgt, e, chunk, nb, G, bs, cnt, part);
   TGB_LAUNCHED();
   k1_items_kernel<<<1, 1024, 0, ctx->stream>>>(cnt, nb, G, items, small);
   TGB_LAUNCHED();
