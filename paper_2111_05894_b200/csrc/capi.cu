@@ -5,6 +5,7 @@
 #include <mutex>
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdlib>
 #include <string>
 
@@ -133,6 +134,58 @@ __global__ void relabel_rows_kernel(const uint64_t* __restrict__ off, const uint
 struct tg_ctx;
 using namespace tgb;
 
+namespace tgb {
+constexpr size_t kPipeChunk = 64ull << 20;
+
+static void pipe_init(tg_ctx* c) {
+  if (c->pipe_buf[0]) return;
+  for (int i = 0; i < 2; ++i) {
+    TGB_CUDA(cudaHostAlloc(&c->pipe_buf[i], kPipeChunk, cudaHostAllocDefault));
+    TGB_CUDA(cudaEventCreateWithFlags(&c->pipe_ev[i], cudaEventDisableTiming));
+  }
+}
+
+// chunk k: host memcpy into pinned buffer k%2 (all cores), then its DMA on
+// the stream; buffer k%2 is refilled only after chunk k-2's DMA completed
+void copy_h2d(tg_ctx* ctx, void* dst_dev, const void* src_host, size_t bytes, bool sync_end) {
+  pipe_init(ctx);
+  const size_t nch = (bytes + kPipeChunk - 1) / kPipeChunk;
+  for (size_t k = 0; k < nch; ++k) {
+    const size_t off = k * kPipeChunk, len = std::min(kPipeChunk, bytes - off);
+    const int b = static_cast<int>(k & 1);
+    TGB_CUDA(cudaEventSynchronize(ctx->pipe_ev[b]));  // its previous DMA (this call or an earlier one)
+    parallel_memcpy(ctx->pipe_buf[b], static_cast<const char*>(src_host) + off, len);
+    TGB_CUDA(cudaMemcpyAsync(static_cast<char*>(dst_dev) + off, ctx->pipe_buf[b], len,
+                             cudaMemcpyHostToDevice, ctx->stream));
+    TGB_CUDA(cudaEventRecord(ctx->pipe_ev[b], ctx->stream));
+  }
+  if (sync_end) ctx->sync();
+}
+
+// chunk k's DMA into pinned buffer k%2 is issued before chunk k-1 is moved
+// out of buffer (k-1)%2 by the host cores
+void copy_d2h(tg_ctx* ctx, void* dst_host, const void* src_dev, size_t bytes) {
+  pipe_init(ctx);
+  const size_t nch = (bytes + kPipeChunk - 1) / kPipeChunk;
+  auto issue = [&](size_t k) {
+    const size_t off = k * kPipeChunk, len = std::min(kPipeChunk, bytes - off);
+    const int b = static_cast<int>(k & 1);
+    TGB_CUDA(cudaMemcpyAsync(ctx->pipe_buf[b], static_cast<const char*>(src_dev) + off, len,
+                             cudaMemcpyDeviceToHost, ctx->stream));
+    TGB_CUDA(cudaEventRecord(ctx->pipe_ev[b], ctx->stream));
+  };
+  issue(0);
+  for (size_t k = 0; k < nch; ++k) {
+    const size_t off = k * kPipeChunk, len = std::min(kPipeChunk, bytes - off);
+    const int b = static_cast<int>(k & 1);
+    TGB_CUDA(cudaEventSynchronize(ctx->pipe_ev[b]));
+    if (k + 1 < nch) issue(k + 1);  // into the other buffer, drained at step k-1
+    parallel_memcpy(static_cast<char*>(dst_host) + off, ctx->pipe_buf[b], len);
+  }
+  ctx->sync();
+}
+}  // namespace tgb
+
 extern "C" {
 
 const char* tg_last_error(void) { return t_err.c_str(); }
@@ -234,6 +287,10 @@ int tg_ctx_destroy(tg_ctx* c) {
   cudaStreamSynchronize(c->stream);
   for (int i = 0; i < kNumSlots; ++i)
     if (c->slot_ptr[i]) cudaFree(c->slot_ptr[i]);
+  for (int i = 0; i < 2; ++i) {
+    if (c->pipe_buf[i]) cudaFreeHost(c->pipe_buf[i]);
+    if (c->pipe_ev[i]) cudaEventDestroy(c->pipe_ev[i]);
+  }
   if (c->aux) {
     cudaStreamSynchronize(c->aux);
     cudaStreamSynchronize(c->aux2);

@@ -103,6 +103,8 @@ struct tg_ctx {
   void* slot_ptr[tgb::kNumSlots] = {};
   size_t slot_size[tgb::kNumSlots] = {};
   void* pinned_small = nullptr;  // 4 KB mapped host scratch for small results
+  void* pipe_buf[2] = {};        // pinned staging of copy_h2d / copy_d2h (allocated on first use)
+  cudaEvent_t pipe_ev[2] = {};
   // Fork-join side stream (concurrent kernels inside one stream-ordered call).
   cudaStream_t aux = nullptr, aux2 = nullptr, aux3 = nullptr;
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr, ev_join2 = nullptr, ev_join3 = nullptr;
@@ -187,6 +189,24 @@ inline void* mapped_device_ptr(const void* p) {
   return nullptr;
 }
 
+// Large pageable host <-> device copies, pipelined through two pinned staging
+// buffers of the context (DMA of one chunk while the host cores move the
+// other): several times the rate of a cudaMemcpy from pageable memory, which
+// the driver stages through one thread. Synchronous on return. Small copies
+// (< kPipeMin) use cudaMemcpyAsync on the stream as before.
+void parallel_memcpy(void* dst, const void* src, size_t bytes);  // host_memcpy.cpp (OpenMP)
+constexpr size_t kPipeMin = 32ull << 20;
+void copy_h2d(tg_ctx* ctx, void* dst_dev, const void* src_host, size_t bytes, bool sync_end = true);
+void copy_d2h(tg_ctx* ctx, void* dst_host, const void* src_dev, size_t bytes);
+inline bool is_pinned_host(const void* p) {
+  cudaPointerAttributes a;
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeHost;
+}
+
 // Read-only input that may live on the host: returns a device pointer,
 // copying into a scratch slot when needed.
 template <typename T>
@@ -194,7 +214,10 @@ const T* dev_in(tg_ctx* ctx, const T* p, size_t count, int slot) {
   if (count == 0) return ctx->scratch_t<T>(slot, 1);
   if (is_device_ptr(p)) return p;
   T* d = ctx->scratch_t<T>(slot, count);
-  TGB_CUDA(cudaMemcpyAsync(d, p, count * sizeof(T), cudaMemcpyHostToDevice, ctx->stream));
+  if (count * sizeof(T) >= kPipeMin && !is_pinned_host(p))
+    copy_h2d(ctx, d, p, count * sizeof(T));
+  else
+    TGB_CUDA(cudaMemcpyAsync(d, p, count * sizeof(T), cudaMemcpyHostToDevice, ctx->stream));
   return d;
 }
 
@@ -213,8 +236,13 @@ struct DevOut {
   }
   T* dev() { return d; }
   void finish() {
-    if (host && count)
+    if (host && count) {
+      if (count * sizeof(T) >= kPipeMin && !is_pinned_host(user)) {
+        copy_d2h(ctx, user, d, count * sizeof(T));
+        return;
+      }
       TGB_CUDA(cudaMemcpyAsync(user, d, count * sizeof(T), cudaMemcpyDeviceToHost, ctx->stream));
+    }
     ctx->sync();
   }
 };

@@ -1524,14 +1524,19 @@ int tg_graph_create(tg_ctx* ctx, const uint64_t* offsets, const uint64_t* target
       TGB_CUDA(cudaMemsetAsync(bad + 1, 0xff, sizeof(unsigned long long), ctx->stream));
       // targets: straight from device memory, or in 32M-entry chunks from the host
       const bool tdev = is_device_ptr(targets);
+      const bool tpinned = !tdev && is_pinned_host(targets);
       const uint64_t chunk = tdev ? std::max<uint64_t>(e, 1) : (32ull << 20);
       for (uint64_t base = 0; base < e; base += chunk) {
         const uint64_t cnt = std::min(chunk, e - base);
         const uint64_t* src = targets + base;
         if (!tdev) {
-          auto* st = ctx->scratch_t<uint64_t>(kStageIn1, cnt);
-          TGB_CUDA(cudaMemcpyAsync(st, src, cnt * sizeof(uint64_t), cudaMemcpyHostToDevice,
-                                   ctx->stream));
+          // two staging slots: chunk k+1 crosses PCIe while chunk k narrows
+          auto* st = ctx->scratch_t<uint64_t>((base / chunk) & 1 ? kStageIn2 : kStageIn1, cnt);
+          if (cnt * sizeof(uint64_t) >= kPipeMin && !tpinned)
+            copy_h2d(ctx, st, src, cnt * sizeof(uint64_t), /*sync_end=*/false);
+          else
+            TGB_CUDA(cudaMemcpyAsync(st, src, cnt * sizeof(uint64_t), cudaMemcpyHostToDevice,
+                                     ctx->stream));
           src = st;
         }
         narrow_targets_kernel<<<grid_for(cnt, 256), 256, 0, ctx->stream>>>(src, tgt + base, cnt,
@@ -1607,6 +1612,7 @@ int tg_graph_create_rows(tg_ctx* ctx, const uint64_t* offsets, const uint64_t* t
       auto* bad = ctx->scratch_t<unsigned long long>(kSmall, 2);
       TGB_CUDA(cudaMemsetAsync(bad + 1, 0xff, 8, ctx->stream));
       const bool tdev = is_device_ptr(targets);
+      const bool tpinned = !tdev && is_pinned_host(targets);
       const uint64_t chunk = tdev ? std::max<uint64_t>(g->e, 1) : (32ull << 20);
       for (uint64_t base = 0; base < g->e; base += chunk) {
         const uint64_t cnt = std::min(chunk, g->e - base);
