@@ -2,7 +2,7 @@
 # Compile-time A/B experiments: builds a copy of the library with extra nvcc
 # defines under variants/<name>/ (git-ignored, travels to the GPU box).
 #   bash scripts/variant.sh <name> "-DTG_PR_BLANES=4 ..."
-# then: python variants/run.py <name> scripts/k3_probe.py c3 ...
+# then: python scripts/variant_run.py <name> scripts/k3_probe.py c3 ...
 set -e
 R=$(cd "$(dirname "$0")/.." && pwd)
 V=$R/variants/$1
