@@ -303,7 +303,13 @@ def bench_pagerank_e2e(torch, tg, ctx, off, tgt, tid, want_d):
     return {"first_call_s": round(ts[0], 4), "cached_call_s": round(min(ts[1:]), 4),
             "gteps_first_call": round(5 * e / ts[0] / 1e9, 3),
             "gteps_cached": round(5 * e / min(ts[1:]) / 1e9, 3),
+            # the host arrays handed to the API (u64) ...
             "h2d_bytes_first_call": int(8 * (len(off) + len(tgt) + len(tid.ids))),
+            # ... and what crosses PCIe: targets >= 4M narrowed to u32 by the
+            # host cores on their way into the pinned pipeline (tg_graph_create)
+            "pcie_h2d_bytes_first_call": int(8 * (len(off) + len(tid.ids)) + sum(
+                min(32 << 20, e - b) * (4 if min(32 << 20, e - b) * 8 >= (32 << 20) else 8)
+                for b in range(0, e, 32 << 20))),
             "d2h_bytes": int(8 * (len(off) - 1)), "bit_exact": same,
             "how": "tiergraph.weighted_reverse_pagerank(CsrGraph(host u64 arrays), host train "
                    "ids) -> host f64 scores, host perf_counter around each call"}

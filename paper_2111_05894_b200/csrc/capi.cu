@@ -162,6 +162,25 @@ void copy_h2d(tg_ctx* ctx, void* dst_dev, const void* src_host, size_t bytes, bo
   if (sync_end) ctx->sync();
 }
 
+uint64_t copy_h2d_narrow(tg_ctx* ctx, uint32_t* dst_dev, const uint64_t* src_host, size_t count,
+                         uint64_t limit) {
+  pipe_init(ctx);
+  constexpr size_t per = kPipeChunk / sizeof(uint32_t);
+  uint64_t first = ~0ull;
+  for (size_t off = 0, k = 0; off < count; off += per, ++k) {
+    const size_t len = std::min(per, count - off);
+    const int b = static_cast<int>(k & 1);
+    TGB_CUDA(cudaEventSynchronize(ctx->pipe_ev[b]));
+    const uint64_t f = parallel_narrow_u64(static_cast<uint32_t*>(ctx->pipe_buf[b]), src_host + off,
+                                           len, limit);
+    if (first == ~0ull && f != ~0ull) first = off + f;
+    TGB_CUDA(cudaMemcpyAsync(dst_dev + off, ctx->pipe_buf[b], len * sizeof(uint32_t),
+                             cudaMemcpyHostToDevice, ctx->stream));
+    TGB_CUDA(cudaEventRecord(ctx->pipe_ev[b], ctx->stream));
+  }
+  return first;
+}
+
 // chunk k's DMA into pinned buffer k%2 is issued before chunk k-1 is moved
 // out of buffer (k-1)%2 by the host cores
 void copy_d2h(tg_ctx* ctx, void* dst_host, const void* src_dev, size_t bytes) {

@@ -197,6 +197,12 @@ inline void* mapped_device_ptr(const void* p) {
 void parallel_memcpy(void* dst, const void* src, size_t bytes);  // host_memcpy.cpp (OpenMP)
 constexpr size_t kPipeMin = 32ull << 20;
 void copy_h2d(tg_ctx* ctx, void* dst_dev, const void* src_host, size_t bytes, bool sync_end = true);
+// u64 host values -> u32 device array through the same pinned pipeline,
+// narrowed by the host cores; returns the first index whose value is >= limit
+// (~0 when none is). Asynchronous like copy_h2d(sync_end = false).
+uint64_t copy_h2d_narrow(tg_ctx* ctx, uint32_t* dst_dev, const uint64_t* src_host, size_t count,
+                         uint64_t limit);
+uint64_t parallel_narrow_u64(uint32_t* dst, const uint64_t* src, size_t count, uint64_t limit);
 void copy_d2h(tg_ctx* ctx, void* dst_host, const void* src_dev, size_t bytes);
 inline bool is_pinned_host(const void* p) {
   cudaPointerAttributes a;

@@ -1526,17 +1526,23 @@ int tg_graph_create(tg_ctx* ctx, const uint64_t* offsets, const uint64_t* target
       const bool tdev = is_device_ptr(targets);
       const bool tpinned = !tdev && is_pinned_host(targets);
       const uint64_t chunk = tdev ? std::max<uint64_t>(e, 1) : (32ull << 20);
+      uint64_t host_bad = ~0ull;  // first out-of-range target seen by host-side narrowing
       for (uint64_t base = 0; base < e; base += chunk) {
         const uint64_t cnt = std::min(chunk, e - base);
         const uint64_t* src = targets + base;
+        if (!tdev && !tpinned && cnt * sizeof(uint64_t) >= kPipeMin) {
+          // large pageable targets: narrowed to u32 by the host cores on their
+          // way into the pinned pipeline (half the PCIe bytes, no u64 staging)
+          const uint64_t f = copy_h2d_narrow(ctx, tgt + base, src, cnt, n);
+          if (host_bad == ~0ull && f != ~0ull) host_bad = base + f;
+          continue;
+        }
         if (!tdev) {
-          // two staging slots: chunk k+1 crosses PCIe while chunk k narrows
+          // pinned or small: DMA the u64 values, narrow on the device; two
+          // staging slots, so chunk k+1 crosses PCIe while chunk k narrows
           auto* st = ctx->scratch_t<uint64_t>((base / chunk) & 1 ? kStageIn2 : kStageIn1, cnt);
-          if (cnt * sizeof(uint64_t) >= kPipeMin && !tpinned)
-            copy_h2d(ctx, st, src, cnt * sizeof(uint64_t), /*sync_end=*/false);
-          else
-            TGB_CUDA(cudaMemcpyAsync(st, src, cnt * sizeof(uint64_t), cudaMemcpyHostToDevice,
-                                     ctx->stream));
+          TGB_CUDA(cudaMemcpyAsync(st, src, cnt * sizeof(uint64_t), cudaMemcpyHostToDevice,
+                                   ctx->stream));
           src = st;
         }
         narrow_targets_kernel<<<grid_for(cnt, 256), 256, 0, ctx->stream>>>(src, tgt + base, cnt,
@@ -1546,6 +1552,7 @@ int tg_graph_create(tg_ctx* ctx, const uint64_t* offsets, const uint64_t* target
       unsigned long long hb;
       TGB_CUDA(cudaMemcpyAsync(&hb, bad + 1, sizeof(hb), cudaMemcpyDeviceToHost, ctx->stream));
       ctx->sync();
+      hb = std::min<unsigned long long>(hb, host_bad);
       if (hb != ~0ull) format_error("csr: target out of range at edge " + std::to_string(hb));
     } catch (...) {
       cudaFree(tgt);

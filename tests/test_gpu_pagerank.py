@@ -52,6 +52,26 @@ def test_errors(tg, ctx):
         tg.weighted_reverse_pagerank(g, tg.PagerankConfig(), tg.TrainIdSet(np.array([0, 7], np.uint64)))
     with pytest.raises(tg.FormatError):
         tg.reverse_pagerank(G(tg, np.array([0, 1, 1], np.uint64), np.array([5], np.uint64)))
+    # large pageable targets are narrowed by the host cores on the way into
+    # the pinned pipeline (copy_h2d_narrow): the first offending edge is still
+    # the one reported, whichever chunk or pipeline buffer it falls in
+    # (32M-edge chunks: 80M edges = three host-narrowed chunks; 2 x 2^25 + 1000
+    # = two host-narrowed chunks and a small tail narrowed on the device)
+    n = 1000
+    for e, bads in ((80_000_000, ((50_000_001, 79_999_999), (3, 70_000_000), (33_554_431,),
+                                  (79_999_999,))),
+                    (2 * 2 ** 25 + 1000, ((2 ** 26 + 10,), (100, 2 ** 26 + 999)))):
+        off = np.linspace(0, e, n + 1).astype(np.uint64)
+        tgt = (np.arange(e, dtype=np.uint64) * np.uint64(7919)) % np.uint64(n)
+        for bad in bads:
+            t = tgt.copy()
+            for i in bad:
+                t[i] = n + i % 5
+            with pytest.raises(tg.FormatError, match=rf"target out of range at edge {bad[0]}(?!\d)"):
+                tg.reverse_pagerank(G(tg, off, t), tg.PagerankConfig(iterations=1))
+    # the same graph without bad targets uploads and runs (host-narrowed path)
+    s = tg.reverse_pagerank(G(tg, off, tgt), tg.PagerankConfig(iterations=1))
+    assert len(s) == n and np.all(np.isfinite(s))
     # empty graph: config still validated, result empty
     e = G(tg, np.zeros(1, np.uint64), np.zeros(0, np.uint64))
     assert tg.reverse_pagerank(e).size == 0
