@@ -1530,7 +1530,11 @@ int tg_graph_create(tg_ctx* ctx, const uint64_t* offsets, const uint64_t* target
       for (uint64_t base = 0; base < e; base += chunk) {
         const uint64_t cnt = std::min(chunk, e - base);
         const uint64_t* src = targets + base;
-        if (!tdev && !tpinned && cnt * sizeof(uint64_t) >= kPipeMin) {
+        static const bool host_narrow = [] {  // TIERGRAPH_UPLOAD_NARROW=0: u64 over PCIe (A/B)
+          const char* v = std::getenv("TIERGRAPH_UPLOAD_NARROW");
+          return !(v && v[0] == '0');
+        }();
+        if (!tdev && !tpinned && cnt * sizeof(uint64_t) >= kPipeMin && host_narrow) {
           // large pageable targets: narrowed to u32 by the host cores on their
           // way into the pinned pipeline (half the PCIe bytes, no u64 staging)
           const uint64_t f = copy_h2d_narrow(ctx, tgt + base, src, cnt, n);
@@ -1541,8 +1545,11 @@ int tg_graph_create(tg_ctx* ctx, const uint64_t* offsets, const uint64_t* target
           // pinned or small: DMA the u64 values, narrow on the device; two
           // staging slots, so chunk k+1 crosses PCIe while chunk k narrows
           auto* st = ctx->scratch_t<uint64_t>((base / chunk) & 1 ? kStageIn2 : kStageIn1, cnt);
-          TGB_CUDA(cudaMemcpyAsync(st, src, cnt * sizeof(uint64_t), cudaMemcpyHostToDevice,
-                                   ctx->stream));
+          if (cnt * sizeof(uint64_t) >= kPipeMin && !tpinned)
+            copy_h2d(ctx, st, src, cnt * sizeof(uint64_t), /*sync_end=*/false);
+          else
+            TGB_CUDA(cudaMemcpyAsync(st, src, cnt * sizeof(uint64_t), cudaMemcpyHostToDevice,
+                                     ctx->stream));
           src = st;
         }
         narrow_targets_kernel<<<grid_for(cnt, 256), 256, 0, ctx->stream>>>(src, tgt + base, cnt,
