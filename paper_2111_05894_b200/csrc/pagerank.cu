@@ -1527,13 +1527,13 @@ int tg_graph_create(tg_ctx* ctx, const uint64_t* offsets, const uint64_t* target
       const bool tpinned = !tdev && is_pinned_host(targets);
       const uint64_t chunk = tdev ? std::max<uint64_t>(e, 1) : (32ull << 20);
       uint64_t host_bad = ~0ull;  // first out-of-range target seen by host-side narrowing
+      static const bool host_narrow = [] {  // TIERGRAPH_UPLOAD_NARROW=0: u64 over PCIe (A/B)
+        const char* v = std::getenv("TIERGRAPH_UPLOAD_NARROW");
+        return !(v && v[0] == '0');
+      }();
       for (uint64_t base = 0; base < e; base += chunk) {
         const uint64_t cnt = std::min(chunk, e - base);
         const uint64_t* src = targets + base;
-        static const bool host_narrow = [] {  // TIERGRAPH_UPLOAD_NARROW=0: u64 over PCIe (A/B)
-          const char* v = std::getenv("TIERGRAPH_UPLOAD_NARROW");
-          return !(v && v[0] == '0');
-        }();
         if (!tdev && !tpinned && cnt * sizeof(uint64_t) >= kPipeMin && host_narrow) {
           // large pageable targets: narrowed to u32 by the host cores on their
           // way into the pinned pipeline (half the PCIe bytes, no u64 staging)
@@ -1542,8 +1542,9 @@ int tg_graph_create(tg_ctx* ctx, const uint64_t* offsets, const uint64_t* target
           continue;
         }
         if (!tdev) {
-          // pinned or small: DMA the u64 values, narrow on the device; two
-          // staging slots, so chunk k+1 crosses PCIe while chunk k narrows
+          // pinned, small (or TIERGRAPH_UPLOAD_NARROW=0): DMA the u64 values,
+          // narrow on the device; two staging slots, so chunk k+1 crosses
+          // PCIe while chunk k narrows
           auto* st = ctx->scratch_t<uint64_t>((base / chunk) & 1 ? kStageIn2 : kStageIn1, cnt);
           if (cnt * sizeof(uint64_t) >= kPipeMin && !tpinned)
             copy_h2d(ctx, st, src, cnt * sizeof(uint64_t), /*sync_end=*/false);
